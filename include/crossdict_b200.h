@@ -1,0 +1,148 @@
+/*
+ * crossdict_b200.h -- C ABI of the B200 batched-OMP / zero-tree-OMP engine.
+ *
+ * This is the drop-in boundary for the reference package `crossdict`
+ * (/root/reference/pkg/src/crossdict).  The reference has exactly one
+ * compiled seam on this path, the numba kernel
+ *
+ *     omp_batch_kernel(mat_t, ys, k_max, eps, allowed, restricted,
+ *                      out_sel, out_coef, out_count, out_rnorm, out_scans,
+ *                      out_flag)                           (_kernels.py:50-168)
+ *
+ * bound into crossdict.pursuit by `from ._kernels import omp_batch_kernel`
+ * (pursuit.py:32) and called only from pursuit._run_kernel (pursuit.py:234-250).
+ * cdb_omp_batch() below takes the same arguments, in the same dtypes and
+ * layouts, plus a dictionary handle (the device-resident form of `mat_t`) and
+ * a CUDA stream.  The batched zero-tree driver (crossscale.py:235-283) is one
+ * more entry point so that its grouping/routing runs on the device.
+ *
+ * Conventions (mirroring the reference seam, pursuit.py:240-245):
+ *   - plain pointers and sizes; arrays are C-contiguous; int64/fp64/uint8 as
+ *     in the reference; every pointer may be HOST or DEVICE memory (detected
+ *     per pointer; host buffers are staged through the stream);
+ *   - the caller allocates every output; the library overwrites them
+ *     entirely (it does not rely on the caller's -1 / 0 pre-initialisation);
+ *   - no exceptions cross the ABI; every function returns a cdb_status;
+ *     validation that the reference performs in Python (ConfigError,
+ *     DimensionError, DomainError) stays in the host layer, the ABI only
+ *     re-checks sizes and returns CDB_ERR_ARG;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *     stream-ordered and return after the outputs are complete (host
+ *     outputs) or enqueued (device outputs).
+ */
+#ifndef CROSSDICT_B200_H
+#define CROSSDICT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CDB_OK = 0,
+    CDB_ERR_ARG = 1,      /* size / pointer argument invalid                   */
+    CDB_ERR_CUDA = 2,     /* a CUDA runtime call failed (see cdb_last_error)   */
+    CDB_ERR_NOMEM = 3,    /* device or pinned allocation failed                */
+    CDB_ERR_NODEV = 4     /* no sm_100 device available                        */
+} cdb_status;
+
+/* Opaque device-resident dictionary (atoms as rows, T x N). */
+typedef struct cdb_dictionary cdb_dictionary;
+
+/* Message for the last non-OK status on this thread. */
+const char *cdb_last_error(void);
+
+/* Library / device facts: writes the SM count and compute capability. */
+cdb_status cdb_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/*
+ * Stage a dictionary on the current device.
+ * Replaces: tensor.py:124-129 (Dictionary.atoms_t, the T x N C-contiguous
+ * kernel operand) and pursuit.py:96-123 (DenseColumns.mat_t).
+ * atoms_t: T x N fp64 row-major (one atom per row), host or device.
+ * Builds the fp64 copy, the bf16 tensor-core operand, squared norms and,
+ * when T*T*8 bytes <= gram_budget_bytes, the fp64 Gram matrix.
+ */
+cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
+                                 int64_t gram_budget_bytes, void *stream,
+                                 cdb_dictionary **out);
+cdb_status cdb_dictionary_destroy(cdb_dictionary *dict);
+/* Bytes of device memory held by the handle. */
+int64_t cdb_dictionary_bytes(const cdb_dictionary *dict);
+
+/* Engine selection for cdb_omp_batch / cdb_zero_tree_batch. */
+typedef enum {
+    CDB_ENGINE_AUTO = 0,     /* pick per problem shape (default)               */
+    CDB_ENGINE_EXACT = 1,    /* warp-per-signal fp64 restatement of the kernel  */
+    CDB_ENGINE_GRAM = 2,     /* signal-stationary fp64 Gram/Cholesky OMP        */
+    CDB_ENGINE_TENSOR = 3    /* tcgen05 bf16 correlation + certified fp64 LS    */
+} cdb_engine;
+
+/*
+ * Batched OMP.  Replaces omp_batch_kernel (_kernels.py:50-168) as called by
+ * pursuit._run_kernel (pursuit.py:234-250).
+ *   ys       : P x N signals as rows (pursuit.py:433 `ys_rows`); fp64, or fp32
+ *              when ys_is_f32 != 0 (a compact exact input, e.g. fp32 data)
+ *   eps      : P absolute residual tolerances (pursuit.py:434-437)
+ *   allowed  : P x S ascending 0-based candidate ids, read only when
+ *              restricted != 0 (pursuit.py:421-422), else may be NULL
+ *   out_sel  : P x k_max int64, pick order, -1 padded
+ *   out_coef : P x k_max fp64, aligned with out_sel
+ *   out_count, out_scans : P int64;  out_rnorm : P fp64;  out_flag : P uint8
+ */
+cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f32,
+                         int64_t p, int64_t k_max, const double *eps,
+                         const int64_t *allowed, int64_t s_allowed, int restricted,
+                         int64_t *out_sel, double *out_coef, int64_t *out_count,
+                         double *out_rnorm, int64_t *out_scans, uint8_t *out_flag,
+                         int engine, void *stream);
+
+/*
+ * Block-restricted batched OMP: allowed = blocks * q + [0, q)
+ * (pursuit.py:417-423, the `allowed_blocks` / `block_q` form).
+ * blocks: P x nb int64, each row ascending, 0-based block ids.
+ * k_max is the caller's already clipped budget min(K, nb*q, N).
+ */
+cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int ys_is_f32,
+                                 int64_t p, int64_t k_max, const double *eps,
+                                 const int64_t *blocks, int64_t nb, int64_t q,
+                                 int64_t *out_sel, double *out_coef, int64_t *out_count,
+                                 double *out_rnorm, int64_t *out_scans, uint8_t *out_flag,
+                                 int engine, void *stream);
+
+/*
+ * Batched zero-tree OMP.  Replaces crossscale.zero_tree_many_arrays
+ * (crossscale.py:235-283) and, with phi_mode != 0, the Phi-composed
+ * two-step solve of zero_tree_omp (crossscale.py:169-232) on precomputed
+ * effective dictionaries.
+ *   low, high      : step-1 / step-2 dictionaries (T_high = q * T_low)
+ *   fine_shape, factors, rank : the ScaleSpec (scaling.py:20-61); used for
+ *                    the block-mean downsample W y when phi_mode == 0
+ *   ys             : P x N rows (N = fine size, or M when phi_mode != 0)
+ *   k1             : step-1 budget (k_low, or min(k_low, M, T_low) for Phi)
+ *   k_high         : step-2 budget; per signal min(k_high, nb*q, N)
+ *   rel_tol        : REL_RESIDUAL_TOL (pursuit.py:37), read at call time by
+ *                    the host layer; step-1 tolerances use ||W y|| (identity)
+ *   low_*  outputs : width k1;   high_* outputs : width k_high
+ * Returns wall-clock-free results; per-step device times (ms) are written to
+ * step_ms[2] when non-NULL (the reference's `timings` dict, crossscale.py:283).
+ */
+cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *high,
+                               const int64_t *fine_shape, const int64_t *factors, int rank,
+                               const void *ys, int ys_is_f32, int64_t p,
+                               int64_t k1, int64_t k_high, double rel_tol, int phi_mode,
+                               int64_t *low_sel, double *low_coef, int64_t *low_count,
+                               double *low_rnorm, int64_t *low_scans, uint8_t *low_flag,
+                               int64_t *high_sel, double *high_coef, int64_t *high_count,
+                               double *high_rnorm, int64_t *high_scans, uint8_t *high_flag,
+                               int engine, float *step_ms, void *stream);
+
+/* Number of kernels this library has launched since load (instrumentation). */
+int64_t cdb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CROSSDICT_B200_H */

@@ -1,0 +1,88 @@
+"""ctypes binding of the C ABI in include/crossdict_b200.h.
+
+There is no fallback: if ``_lib/libcrossdict_b200.so`` is missing the import of
+any compute entry point raises immediately (build it with
+``python -c "import __graft_entry__ as g; g.build()"`` or ``make -C
+paper_1511_05174_b200/csrc``).  The library itself returns CDB_ERR_NODEV on a
+machine without an sm_100 GPU; the host layer turns that into a RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                        "libcrossdict_b200.so")
+
+ENGINES = {"auto": 0, "exact": 1, "gram": 2, "tensor": 3}
+
+#: every symbol include/crossdict_b200.h declares (checked by tests/test_abi.py)
+SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",
+           "cdb_dictionary_destroy", "cdb_dictionary_bytes", "cdb_omp_batch",
+           "cdb_omp_batch_blocked", "cdb_zero_tree_batch", "cdb_launch_count")
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """A non-OK cdb_status from the native library."""
+
+
+def load():
+    """Load the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(
+            f"native library not built: {LIB_PATH} is missing "
+            "(run `make -C paper_1511_05174_b200/csrc`); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    lib.cdb_last_error.restype = ctypes.c_char_p
+    lib.cdb_launch_count.restype = I64
+    lib.cdb_device_info.argtypes = [P, P, P]
+    lib.cdb_dictionary_create.argtypes = [P, I64, I64, I64, P, P]
+    lib.cdb_dictionary_destroy.argtypes = [P]
+    lib.cdb_dictionary_bytes.argtypes = [P]
+    lib.cdb_dictionary_bytes.restype = I64
+    lib.cdb_omp_batch.argtypes = [P, P, I32, I64, I64, P, P, I64, I32, P, P, P, P, P, P, I32, P]
+    lib.cdb_omp_batch_blocked.argtypes = [P, P, I32, I64, I64, P, P, I64, I64, P, P, P, P, P, P,
+                                          I32, P]
+    lib.cdb_zero_tree_batch.argtypes = [P, P, P, P, I32, P, I32, I64, I64, I64, D, I32,
+                                        P, P, P, P, P, P, P, P, P, P, P, P, I32, P, P]
+    for name in ("cdb_device_info", "cdb_dictionary_create", "cdb_dictionary_destroy",
+                 "cdb_omp_batch", "cdb_omp_batch_blocked", "cdb_zero_tree_batch"):
+        getattr(lib, name).restype = I32
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status != 0:
+        msg = load().cdb_last_error()
+        raise NativeError(f"cdb status {status}: {msg.decode() if msg else ''}")
+
+
+def ptr(a) -> ctypes.c_void_p | None:
+    """Address of a numpy array, a torch tensor or an int; None for None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return ctypes.c_void_p(a)
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())  # torch.Tensor (device or pinned host)
+
+
+def launch_count() -> int:
+    return int(load().cdb_launch_count())
+
+
+def device_info():
+    sms, major, minor = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    check(load().cdb_device_info(ctypes.byref(sms), ctypes.byref(major), ctypes.byref(minor)))
+    return sms.value, major.value, minor.value

@@ -1,0 +1,467 @@
+// C ABI (include/crossdict_b200.h): dictionary staging, engine selection and
+// the batched OMP / zero-tree drivers.  Host code only; kernels live in the
+// *_engine.cu / helpers.cu translation units.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/crossdict_b200.h"
+#include "engines.h"
+
+struct cdb_dictionary {
+  int64_t t = 0, n = 0, n_pad = 0;
+  double *d64 = nullptr;   // T x N fp64 atoms (rows)
+  double *gram = nullptr;  // T x T fp64 (optional)
+  void *d16 = nullptr;     // T x n_pad bf16 (tensor-core operand)
+  int64_t bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+cdb_status fail(cdb_status st, const std::string &msg) {
+  g_last_error = msg;
+  return st;
+}
+
+#define CDB_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(CDB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// Stream-ordered device scratch that frees itself.
+struct DevBuf {
+  void *ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  ~DevBuf() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+  cudaError_t alloc(size_t bytes, cudaStream_t s) {
+    stream = s;
+    if (bytes == 0) bytes = 16;
+    return cudaMallocAsync(&ptr, bytes, s);
+  }
+  template <typename T>
+  T *as() const {
+    return (T *)ptr;
+  }
+};
+
+// An input array usable on the device (copied when it lives on the host).
+struct InArr {
+  const void *dev = nullptr;
+  DevBuf buf;
+  cudaError_t bind(const void *p, size_t bytes, cudaStream_t s) {
+    if (!p || is_device_ptr(p)) {
+      dev = p;
+      return cudaSuccess;
+    }
+    cudaError_t e = buf.alloc(bytes, s);
+    if (e != cudaSuccess) return e;
+    dev = buf.ptr;
+    return cudaMemcpyAsync(buf.ptr, p, bytes, cudaMemcpyHostToDevice, s);
+  }
+};
+
+// An output array written on the device and copied back when host-resident.
+struct OutArr {
+  void *host = nullptr;
+  void *dev = nullptr;
+  size_t bytes = 0;
+  DevBuf buf;
+  cudaError_t bind(void *p, size_t nbytes, cudaStream_t s) {
+    bytes = nbytes;
+    if (p && is_device_ptr(p)) {
+      dev = p;
+      return cudaSuccess;
+    }
+    host = p;
+    cudaError_t e = buf.alloc(nbytes, s);
+    dev = buf.ptr;
+    return e;
+  }
+  cudaError_t finish(cudaStream_t s) {
+    if (!host || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s);
+  }
+};
+
+struct Outs {
+  OutArr sel, coef, count, rnorm, scans, flag;
+  cudaError_t bind(int64_t p, int64_t kw, int64_t *s, double *c, int64_t *cnt, double *rn,
+                   int64_t *sc, uint8_t *fl, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = sel.bind(s, sizeof(int64_t) * p * kw, st)) != cudaSuccess) return e;
+    if ((e = coef.bind(c, sizeof(double) * p * kw, st)) != cudaSuccess) return e;
+    if ((e = count.bind(cnt, sizeof(int64_t) * p, st)) != cudaSuccess) return e;
+    if ((e = rnorm.bind(rn, sizeof(double) * p, st)) != cudaSuccess) return e;
+    if ((e = scans.bind(sc, sizeof(int64_t) * p, st)) != cudaSuccess) return e;
+    return flag.bind(fl, sizeof(uint8_t) * p, st);
+  }
+  cudaError_t finish(cudaStream_t st) {
+    cudaError_t e;
+    for (OutArr *o : {&sel, &coef, &count, &rnorm, &scans, &flag})
+      if ((e = o->finish(st)) != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+  bool any_host() const {
+    return sel.host || coef.host || count.host || rnorm.host || scans.host || flag.host;
+  }
+};
+
+struct DevInfo {
+  int sms = 0, smem_optin = 0, major = 0, minor = 0;
+};
+
+cdb_status device_info(DevInfo &di) {
+  int dev = 0;
+  CDB_CUDA(cudaGetDevice(&dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (di.major != 10) return fail(CDB_ERR_NODEV, "device is not sm_100 (B200)");
+  return CDB_OK;
+}
+
+constexpr int64_t kGramSmemLimit = 100 * 1024;       // per-warp smem for H in smem
+constexpr int64_t kScratchBudget = int64_t(4) << 30;  // per-call global scratch cap
+
+// Run the exact engine over `count` signals (all, or the ids in sig_ids).
+cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t count,
+                     const int64_t *sig_ids, int64_t k_max, int64_t kw, const double *eps,
+                     const cdb::Cands &cands, int64_t max_cands, Outs &o, const DevInfo &di,
+                     cudaStream_t st) {
+  if (count <= 0) return CDB_OK;
+  cdb::ExactArgs a{};
+  a.mat_t = d->d64;
+  a.t = d->t;
+  a.n = d->n;
+  a.ys_stride = d->n;
+  a.sig_ids = sig_ids;
+  a.p_count = count;
+  a.k_max = k_max;
+  a.k_width = kw;
+  a.eps = eps;
+  a.cands = cands;
+  a.out_sel = o.sel.dev ? (int64_t *)o.sel.dev : nullptr;
+  a.out_coef = (double *)o.coef.dev;
+  a.out_count = (int64_t *)o.count.dev;
+  a.out_rnorm = (double *)o.rnorm.dev;
+  a.out_scans = (int64_t *)o.scans.dev;
+  a.out_flag = (uint8_t *)o.flag.dev;
+  a.work_stride = cdb::exact_work_stride(d->n, kw, max_cands);
+  int64_t warps = count < (int64_t)di.sms * 8 ? count : (int64_t)di.sms * 8;
+  const int64_t cap = kScratchBudget / (8 * a.work_stride);
+  if (warps > cap) warps = cap < 4 ? 4 : cap;
+  warps = (warps + 3) & ~int64_t(3);
+  DevBuf work;
+  CDB_CUDA(work.alloc(sizeof(double) * a.work_stride * warps, st));
+  a.work = work.as<double>();
+  CDB_CUDA(cdb::launch_exact(a, ys, f32, (int)warps, st));
+  return CDB_OK;
+}
+
+// The OMP driver shared by every entry point.
+cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p, int64_t k_max,
+                   int64_t kw, const double *eps, const cdb::Cands &cands, int64_t max_cands,
+                   Outs &o, int engine, const DevInfo &di, cudaStream_t st) {
+  if (p <= 0) return CDB_OK;
+  const int64_t smem_h = cdb::gram_total_smem(max_cands, kw, d->n, true);
+  bool use_gram = false;
+  if (engine == CDB_ENGINE_GRAM || engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_TENSOR)
+    use_gram = d->gram != nullptr && max_cands > 0;
+  if (engine == CDB_ENGINE_GRAM && !d->gram)
+    return fail(CDB_ERR_ARG, "Gram engine requested but the dictionary has no Gram matrix");
+  if (!use_gram)
+    return run_exact(d, ys, f32, p, nullptr, k_max, kw, eps, cands, max_cands, o, di, st);
+
+  DevBuf status;
+  CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
+  CDB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(uint32_t) * p, st));
+  cdb::GramArgs g{};
+  g.d64 = d->d64;
+  g.gram = d->gram;
+  g.t = d->t;
+  g.n = d->n;
+  g.ys_stride = d->n;
+  g.k_max = k_max;
+  g.k_width = kw;
+  g.eps = eps;
+  g.cands = cands;
+  g.max_cands = max_cands;
+  g.out_sel = (int64_t *)o.sel.dev;
+  g.out_coef = (double *)o.coef.dev;
+  g.out_count = (int64_t *)o.count.dev;
+  g.out_rnorm = (double *)o.rnorm.dev;
+  g.out_scans = (int64_t *)o.scans.dev;
+  g.out_flag = (uint8_t *)o.flag.dev;
+  g.status = status.as<uint32_t>();
+  const bool h_smem = smem_h <= kGramSmemLimit;
+  int64_t chunk = p;
+  DevBuf hwork;
+  if (!h_smem) {
+    const int64_t per_sig = 8 * max_cands * kw;
+    chunk = kScratchBudget / per_sig;
+    if (chunk < 1) chunk = 1;
+    if (chunk > p) chunk = p;
+    CDB_CUDA(hwork.alloc((size_t)per_sig * chunk, st));
+    g.hwork = hwork.as<double>();
+  }
+  for (int64_t off = 0; off < p; off += chunk) {
+    g.p_offset = off;
+    g.p = (p - off) < chunk ? (p - off) : chunk;
+    CDB_CUDA(cdb::launch_gram(g, ys, f32, di.smem_optin, di.sms, st));
+  }
+  // signals the Gram engine handed over -> exact engine
+  DevBuf ids, cnt;
+  CDB_CUDA(ids.alloc(sizeof(int64_t) * p, st));
+  CDB_CUDA(cnt.alloc(sizeof(int), st));
+  CDB_CUDA(cudaMemsetAsync(cnt.ptr, 0, sizeof(int), st));
+  CDB_CUDA(cdb::launch_collect_delegates(status.as<uint32_t>(), p, ids.as<int64_t>(),
+                                         cnt.as<int>(), st));
+  int h_cnt = 0;
+  CDB_CUDA(cudaMemcpyAsync(&h_cnt, cnt.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  if (h_cnt > 0) {
+    cdb_status s2 =
+        run_exact(d, ys, f32, h_cnt, ids.as<int64_t>(), k_max, kw, eps, cands, max_cands, o, di, st);
+    if (s2 != CDB_OK) return s2;
+  }
+  return CDB_OK;
+}
+
+}  // namespace
+
+namespace cdb {
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace cdb
+
+extern "C" {
+
+const char *cdb_last_error(void) { return g_last_error.c_str(); }
+
+int64_t cdb_launch_count(void) { return g_launches.load(); }
+
+cdb_status cdb_device_info(int *sm_count, int *cc_major, int *cc_minor) {
+  DevInfo di;
+  int dev = 0;
+  CDB_CUDA(cudaGetDevice(&dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, dev));
+  CDB_CUDA(cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (sm_count) *sm_count = di.sms;
+  if (cc_major) *cc_major = di.major;
+  if (cc_minor) *cc_minor = di.minor;
+  return CDB_OK;
+}
+
+cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
+                                 int64_t gram_budget_bytes, void *stream, cdb_dictionary **out) {
+  if (!atoms_t || t < 1 || n < 1 || !out) return fail(CDB_ERR_ARG, "bad dictionary arguments");
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto *d = new cdb_dictionary();
+  d->t = t;
+  d->n = n;
+  d->n_pad = (n + 63) / 64 * 64;
+  auto cleanup = [&](cdb_status s, const std::string &m) {
+    cdb_dictionary_destroy(d);
+    return fail(s, m);
+  };
+  const size_t b64 = sizeof(double) * t * n;
+  if (cudaMalloc(&d->d64, b64) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "d64 alloc");
+  if (cudaMemcpyAsync(d->d64, atoms_t, b64, cudaMemcpyDefault, st) != cudaSuccess)
+    return cleanup(CDB_ERR_CUDA, "d64 copy");
+  d->bytes += b64;
+  const size_t b16 = 2 * t * d->n_pad;
+  if (cudaMalloc(&d->d16, b16) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "d16 alloc");
+  d->bytes += b16;
+  if (cdb::launch_to_bf16(d->d64, t, n, d->n_pad, d->d16, st) != cudaSuccess)
+    return cleanup(CDB_ERR_CUDA, "bf16 conversion");
+  const double gb = 8.0 * (double)t * (double)t;
+  if (gb <= (double)gram_budget_bytes) {
+    if (cudaMalloc(&d->gram, (size_t)gb) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "gram alloc");
+    d->bytes += (int64_t)gb;
+    if (cdb::launch_gram_matrix(d->d64, t, n, d->gram, st) != cudaSuccess)
+      return cleanup(CDB_ERR_CUDA, "gram kernel");
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cleanup(CDB_ERR_CUDA, "dictionary sync");
+  *out = d;
+  return CDB_OK;
+}
+
+cdb_status cdb_dictionary_destroy(cdb_dictionary *d) {
+  if (!d) return CDB_OK;
+  if (d->d64) cudaFree(d->d64);
+  if (d->gram) cudaFree(d->gram);
+  if (d->d16) cudaFree(d->d16);
+  delete d;
+  return CDB_OK;
+}
+
+int64_t cdb_dictionary_bytes(const cdb_dictionary *d) { return d ? d->bytes : 0; }
+
+static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_is_f32, int64_t p,
+                             int64_t k_max, const double *eps, const int64_t *ids, int64_t stride,
+                             int mode, int64_t q, int64_t *out_sel, double *out_coef,
+                             int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                             uint8_t *out_flag, int engine, void *stream) {
+  if (!dict || p < 0 || k_max < 0 || (p > 0 && (!ys || !eps)))
+    return fail(CDB_ERR_ARG, "bad omp arguments");
+  if (p == 0) return CDB_OK;
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool f32 = ys_is_f32 != 0;
+  const int64_t n = dict->n;
+  InArr y_in, e_in, id_in;
+  CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
+  CDB_CUDA(e_in.bind(eps, sizeof(double) * p, st));
+  if (mode != 0) CDB_CUDA(id_in.bind(ids, sizeof(int64_t) * p * stride, st));
+  Outs o;
+  CDB_CUDA(o.bind(p, k_max, out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, st));
+  cdb::Cands c{};
+  c.mode = mode;
+  c.t = dict->t;
+  c.ids = (const int64_t *)id_in.dev;
+  c.stride = stride;
+  c.q = q;
+  c.nb = nullptr;
+  c.nb_fixed = stride;
+  c.clip = 0;
+  const int64_t max_c = mode == 0 ? dict->t : (mode == 1 ? stride : stride * q);
+  cdb_status s = run_omp(dict, y_in.dev, f32, p, k_max, k_max, (const double *)e_in.dev, c, max_c,
+                         o, engine, di, st);
+  if (s != CDB_OK) return s;
+  CDB_CUDA(o.finish(st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  return CDB_OK;
+}
+
+cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f32, int64_t p,
+                         int64_t k_max, const double *eps, const int64_t *allowed,
+                         int64_t s_allowed, int restricted, int64_t *out_sel, double *out_coef,
+                         int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                         uint8_t *out_flag, int engine, void *stream) {
+  if (restricted && (!allowed || s_allowed < 1) && p > 0)
+    return fail(CDB_ERR_ARG, "restricted call without allowed ids");
+  return omp_common(dict, ys, ys_is_f32, p, k_max, eps, allowed, s_allowed, restricted ? 1 : 0, 1,
+                    out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, engine, stream);
+}
+
+cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int ys_is_f32,
+                                 int64_t p, int64_t k_max, const double *eps,
+                                 const int64_t *blocks, int64_t nb, int64_t q, int64_t *out_sel,
+                                 double *out_coef, int64_t *out_count, double *out_rnorm,
+                                 int64_t *out_scans, uint8_t *out_flag, int engine, void *stream) {
+  if (p > 0 && (!blocks || nb < 1 || q < 1)) return fail(CDB_ERR_ARG, "bad block arguments");
+  return omp_common(dict, ys, ys_is_f32, p, k_max, eps, blocks, nb, 2, q, out_sel, out_coef,
+                    out_count, out_rnorm, out_scans, out_flag, engine, stream);
+}
+
+cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *high,
+                               const int64_t *fine_shape, const int64_t *factors, int rank,
+                               const void *ys, int ys_is_f32, int64_t p, int64_t k1,
+                               int64_t k_high, double rel_tol, int phi_mode, int64_t *low_sel,
+                               double *low_coef, int64_t *low_count, double *low_rnorm,
+                               int64_t *low_scans, uint8_t *low_flag, int64_t *high_sel,
+                               double *high_coef, int64_t *high_count, double *high_rnorm,
+                               int64_t *high_scans, uint8_t *high_flag, int engine,
+                               float *step_ms, void *stream) {
+  if (!low || !high || p < 0 || k1 < 1 || k_high < 1 || high->t % low->t)
+    return fail(CDB_ERR_ARG, "bad zero-tree arguments");
+  if (!phi_mode && (!fine_shape || !factors || rank < 1 || rank > 4))
+    return fail(CDB_ERR_ARG, "bad scale spec");
+  if (phi_mode && low->n != high->n) return fail(CDB_ERR_ARG, "Phi mode needs equal M");
+  if (p == 0) return CDB_OK;
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool f32 = ys_is_f32 != 0;
+  const int64_t n = high->n, q = high->t / low->t;
+  InArr y_in;
+  CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
+  Outs lo, hi;
+  CDB_CUDA(lo.bind(p, k1, low_sel, low_coef, low_count, low_rnorm, low_scans, low_flag, st));
+  CDB_CUDA(hi.bind(p, k_high, high_sel, high_coef, high_count, high_rnorm, high_scans, high_flag, st));
+  cudaEvent_t ev[3];
+  for (auto &e : ev) CDB_CUDA(cudaEventCreate(&e));
+  CDB_CUDA(cudaEventRecord(ev[0], st));
+
+  // ---- step 1: W y (identity) or y (Phi), tolerance relative to it
+  DevBuf ylow, eps1, eps2, blocks;
+  const void *y1 = y_in.dev;
+  bool y1_f32 = f32;
+  if (!phi_mode) {
+    int64_t n_low = 1;
+    for (int d = 0; d < rank; d++) n_low *= fine_shape[d] / factors[d];
+    if (n_low != low->n) return fail(CDB_ERR_ARG, "coarse size != low dictionary dim");
+    CDB_CUDA(ylow.alloc(sizeof(double) * p * n_low, st));
+    CDB_CUDA(cdb::launch_downsample(y_in.dev, f32, p, n, fine_shape, factors, rank,
+                                    ylow.as<double>(), n_low, st));
+    y1 = ylow.ptr;
+    y1_f32 = false;
+  }
+  CDB_CUDA(eps1.alloc(sizeof(double) * p, st));
+  CDB_CUDA(cdb::launch_row_tol(y1, y1_f32, p, low->n, rel_tol, eps1.as<double>(), st));
+  cdb::Cands c1{};
+  c1.mode = 0;
+  c1.t = low->t;
+  cdb_status s = run_omp(low, y1, y1_f32, p, k1, k1, eps1.as<double>(), c1, low->t, lo, engine, di, st);
+  if (s != CDB_OK) return s;
+  CDB_CUDA(cudaEventRecord(ev[1], st));
+
+  // ---- step 2: restricted to the children of the sorted coarse support
+  CDB_CUDA(blocks.alloc(sizeof(int64_t) * p * k1, st));
+  CDB_CUDA(cdb::launch_sort_blocks((const int64_t *)lo.sel.dev, (const int64_t *)lo.count.dev, p,
+                                   k1, blocks.as<int64_t>(), st));
+  CDB_CUDA(eps2.alloc(sizeof(double) * p, st));
+  CDB_CUDA(cdb::launch_row_tol(y_in.dev, f32, p, n, rel_tol, eps2.as<double>(), st));
+  cdb::Cands c2{};
+  c2.mode = 2;
+  c2.t = high->t;
+  c2.ids = blocks.as<int64_t>();
+  c2.stride = k1;
+  c2.q = q;
+  c2.nb = (const int64_t *)lo.count.dev;
+  c2.clip = 1;
+  s = run_omp(high, y_in.dev, f32, p, k_high, k_high, eps2.as<double>(), c2, k1 * q, hi, engine, di,
+              st);
+  if (s != CDB_OK) return s;
+  CDB_CUDA(cudaEventRecord(ev[2], st));
+  CDB_CUDA(lo.finish(st));
+  CDB_CUDA(hi.finish(st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  if (step_ms) {
+    CDB_CUDA(cudaEventElapsedTime(&step_ms[0], ev[0], ev[1]));
+    CDB_CUDA(cudaEventElapsedTime(&step_ms[1], ev[1], ev[2]));
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  return CDB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Shared device helpers for the crossdict B200 engine (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CDB_FULL_MASK 0xffffffffu
+
+namespace cdb {
+
+// Per-signal status bits written by the engines (internal; the ABI exports
+// only the reference's out_flag = "dense min-norm fallback engaged").
+enum : uint32_t {
+  ST_DONE = 1u,        // finished (budget, tolerance or orthogonal break)
+  ST_DELEGATE = 2u,    // hand the signal to the exact engine (rank trouble /
+                       // uncertifiable selection); its results are replaced
+};
+
+// Reference constants (crossdict): _kernels.py:24 RANK_TOL.
+constexpr double RANK_TOL = 1e-10;
+// Gram/Cholesky engines hand a signal to the exact engine when the new
+// atom's distance to the span of the support falls below this (relative, in
+// squared units): 1e-8 ||a||^2, i.e. d < 1e-4 ||a||, far above RANK_TOL so
+// the exact MGS test of the reference decides every borderline case.
+constexpr double GRAM_DELEGATE_D2 = 1e-8;
+
+template <typename T>
+__device__ __forceinline__ double ld_f64(const T *p) { return (double)(*p); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CDB_FULL_MASK, v, o);
+  return v;
+}
+
+// Arg-max over (value, index) with "strictly larger wins, ties -> lower
+// index" -- the reduction form of the reference's ascending scan with a
+// strict '>' (_kernels.py:94-103).  Index -1 means "none".
+__device__ __forceinline__ void warp_argmax(double &v, int64_t &idx) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(CDB_FULL_MASK, v, o);
+    int64_t oi = __shfl_xor_sync(CDB_FULL_MASK, idx, o);
+    bool take = (oi >= 0) && (idx < 0 || ov > v || (ov == v && oi < idx));
+    if (take) {
+      v = ov;
+      idx = oi;
+    }
+  }
+}
+
+// The reference _dot4 (_kernels.py:27-42) computed by the 4 lanes of each
+// lane-quad: lane m owns the i = m (mod 4) accumulator chain; the quad
+// combines ((s0+s1)+s2)+s3 and adds the tail last.  Explicit _rn intrinsics
+// keep every product and sum separately rounded (numba fastmath=False), so
+// the value is bit-identical to the reference's.  All 32 lanes must call it
+// together; every lane of a quad gets the quad's full sum.
+__device__ __forceinline__ double dot4_quad(const double *a, const double *b, int64_t n,
+                                            int lane) {
+  const int m = lane & 3;
+  const int64_t m4 = (n / 4) * 4;
+  double s = 0.0;
+  for (int64_t i = m; i < m4; i += 4) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+  const int base = lane & ~3;
+  const double s0 = __shfl_sync(CDB_FULL_MASK, s, base + 0);
+  const double s1 = __shfl_sync(CDB_FULL_MASK, s, base + 1);
+  const double s2 = __shfl_sync(CDB_FULL_MASK, s, base + 2);
+  const double s3 = __shfl_sync(CDB_FULL_MASK, s, base + 3);
+  double tot = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3);
+  for (int64_t i = m4; i < n; i++) tot = __dadd_rn(tot, __dmul_rn(a[i], b[i]));
+  return tot;
+}
+
+}  // namespace cdb

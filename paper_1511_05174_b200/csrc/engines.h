@@ -1,0 +1,77 @@
+// Internal engine interfaces (host side) of the crossdict B200 library.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "candidates.cuh"
+
+namespace cdb {
+
+void note_launch(int n = 1);
+
+// ---------------------------------------------------------------- exact
+struct ExactArgs {
+  const double *mat_t;   // T x N fp64
+  int64_t t, n;
+  int64_t ys_stride;     // elements between signal rows
+  const int64_t *sig_ids;  // optional: process only these signals
+  int64_t p_count;       // number of signals to process (len(sig_ids) or P)
+  int64_t k_max;         // budget (clipped per signal when cands.clip)
+  int64_t k_width;       // output row width
+  const double *eps;
+  Cands cands;
+  int64_t *out_sel;
+  double *out_coef;
+  int64_t *out_count;
+  double *out_rnorm;
+  int64_t *out_scans;
+  uint8_t *out_flag;
+  double *work;          // warps * work_stride doubles
+  int64_t work_stride;
+};
+int64_t exact_work_stride(int64_t n, int64_t k_width, int64_t max_cands);
+cudaError_t launch_exact(const ExactArgs &args, const void *ys, bool ys_f32, int warps,
+                         cudaStream_t stream);
+
+// ---------------------------------------------------------------- gram
+struct GramArgs {
+  const double *d64;     // T x N fp64 atoms (rows)
+  const double *gram;    // T x T fp64 Gram matrix
+  int64_t t, n;
+  int64_t ys_stride;
+  int64_t p;             // signals in this launch
+  int64_t p_offset;      // first signal of this launch
+  int64_t k_max, k_width;
+  const double *eps;
+  Cands cands;
+  int64_t max_cands;     // upper bound of cands.count(p) over the batch
+  int64_t *out_sel;
+  double *out_coef;
+  int64_t *out_count;
+  double *out_rnorm;
+  int64_t *out_scans;
+  uint8_t *out_flag;
+  uint32_t *status;      // per-signal status bits (ST_DELEGATE ...)
+  double *hwork;         // optional global H storage when it does not fit smem
+};
+// Shared-memory bytes per warp of the Gram engine (H in smem or global).
+int64_t gram_total_smem(int64_t max_cands, int64_t k_width, int64_t n, bool h_in_smem);
+cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
+                        int num_sms, cudaStream_t stream);
+
+// ---------------------------------------------------------------- helpers
+cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
+                              const int64_t *fine_shape, const int64_t *factors, int rank,
+                              double *y_low, int64_t n_low, cudaStream_t stream);
+cudaError_t launch_row_tol(const void *ys, bool ys_f32, int64_t p, int64_t n, double rel,
+                           double *eps, cudaStream_t stream);
+cudaError_t launch_sort_blocks(const int64_t *low_sel, const int64_t *low_count, int64_t p,
+                               int64_t k1, int64_t *blocks, cudaStream_t stream);
+cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *gram,
+                               cudaStream_t stream);
+cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad,
+                           void *d16, cudaStream_t stream);
+cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids,
+                                     int *count, cudaStream_t stream);
+
+}  // namespace cdb

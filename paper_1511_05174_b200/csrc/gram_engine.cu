@@ -1,0 +1,283 @@
+// Gram engine: signal-stationary exact fp64 OMP driven by the dictionary's
+// Gram matrix -- one warp per signal, all iterations in one launch.
+//
+// Same algorithm as the reference kernel (crossdict/_kernels.py:50-168):
+// greedy pick of max |<d_j, r>| over the allowed, not-taken candidates with
+// the lowest index winning ties, exact least squares on the support,
+// residual-norm stop test -- but the least squares is an incremental
+// Cholesky of the support Gram G_SS kept as its explicit inverse factor
+// L^{-1}, and the residual is never materialised.  With q_i the orthonormal
+// basis the reference builds by MGS (_kernels.py:111-137), z_i = q_i^T y
+// (its `qty`) and h_i[j] = d_j^T q_i:
+//
+//     c_j   = alpha0_j - sum_i z_i h_i[j]            (correlation, fp64)
+//     w     = L^{-1} G[S, new],  d^2 = G_nn - |w|^2  (MGS projection defect)
+//     z_k   = (alpha0_new - w.z) / d
+//     h_k   = (G[C, new] - sum_i w_i h_i) / d
+//     |r|^2 = |y|^2 - |z|^2                          (stop test, exact band check)
+//
+// so per iteration a signal touches one Gram row and S*k fp64 values of H
+// held in shared memory, instead of re-reading S atoms of length N.  All
+// arithmetic is fp64; correlations agree with the reference's to ~1e-13
+// relative of |r|, far inside the 1e-6 near-tie band of the parity
+// contract.  Signals whose new atom is within 1e-4 |a| of the span of the
+// support (the reference's rank test is d <= 1e-10 |a|, _kernels.py:126)
+// are delegated to the exact engine, which reproduces the reference bit for
+// bit, including the dense minimum-norm mode.
+#include "candidates.cuh"
+#include "common.cuh"
+#include "engines.h"
+
+namespace cdb {
+namespace {
+
+struct GramSmem {
+  double *y;       // n
+  double *alpha0;  // S
+  double *c;       // S
+  double *linv;    // kw * kw (row-major, lower triangle)
+  double *z;       // kw
+  double *w;       // kw
+  double *x;       // kw
+  int64_t *sup;    // kw
+  uint32_t *taken; // (S + 31) / 32
+  double *h;       // kw * S (row i = h_i over candidates) -- smem or global
+};
+
+__host__ __device__ inline int64_t align8(int64_t v) { return (v + 7) & ~int64_t(7); }
+
+__host__ __device__ inline int64_t gram_smem_bytes_no_h(int64_t s, int64_t kw, int64_t n) {
+  return 8 * (n + 2 * s + kw * kw + 3 * kw) + 8 * kw + 4 * align8((s + 31) / 32);
+}
+
+template <typename YT>
+__global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__restrict__ ys,
+                                                       int h_in_smem, int64_t smem_per_warp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t local = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (local >= a.p) return;
+  const int64_t p = a.p_offset + local;
+
+  const int64_t n = a.n, kw = a.k_width, smax = a.max_cands, T = a.t;
+  const Cands &cs = a.cands;
+  unsigned char *base = smem_raw + wib * smem_per_warp;
+  GramSmem s;
+  s.y = (double *)base;
+  s.alpha0 = s.y + n;
+  s.c = s.alpha0 + smax;
+  s.linv = s.c + smax;
+  s.z = s.linv + kw * kw;
+  s.w = s.z + kw;
+  s.x = s.w + kw;
+  s.sup = (int64_t *)(s.x + kw);
+  s.taken = (uint32_t *)(s.sup + kw);
+  s.h = h_in_smem ? (double *)(base + align8(gram_smem_bytes_no_h(smax, kw, n)))
+                  : a.hwork + local * kw * smax;
+
+  const int64_t S = cs.count(p);
+  const int64_t k_max = cs.budget(p, a.k_max, n);
+  int64_t *out_sel = a.out_sel + p * kw;
+  double *out_coef = a.out_coef + p * kw;
+
+  for (int64_t i = lane; i < n; i += 32) s.y[i] = (double)ys[p * a.ys_stride + i];
+  for (int64_t w = lane; w < (S + 31) / 32; w += 32) s.taken[w] = 0u;
+  __syncwarp();
+  const double ynorm = sqrt(dot4_quad(s.y, s.y, n, lane));
+  const double tol = a.eps[p];
+
+  int64_t kdone = 0, scans = 0;
+  double rnorm = ynorm;
+  bool delegate = false, exact_stop = false;
+
+  if (!(ynorm <= tol) && k_max > 0) {
+    // alpha0_j = <d_j, y> for every candidate (lane per candidate).
+    for (int64_t j = lane; j < S; j += 32) {
+      const double *dj = a.d64 + cs.id(p, j) * n;
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; i++) acc = fma(dj[i], s.y[i], acc);
+      s.alpha0[j] = acc;
+      s.c[j] = acc;
+    }
+    double yy = 0.0;
+    for (int64_t i = lane; i < n; i += 32) yy = fma(s.y[i], s.y[i], yy);
+    yy = warp_sum(yy);
+    double rn2 = yy;
+    const double tol2 = tol * tol;
+    const double band = 1e-12 * yy;
+    __syncwarp();
+
+    for (int64_t k = 0; k < k_max; k++) {
+      scans += S - k;
+      // ---- selection: max |c_j| over non-taken, ties -> lowest index
+      double best = -1.0;
+      int64_t bestj = -1;
+      for (int64_t j = lane; j < S; j += 32) {
+        if ((s.taken[j >> 5] >> (j & 31)) & 1u) continue;
+        const double v = fabs(s.c[j]);
+        if (v > best) {
+          best = v;
+          bestj = j;
+        }
+      }
+      warp_argmax(best, bestj);
+      if (bestj < 0 || best <= 0.0) break;
+      const int64_t nid = cs.id(p, bestj);
+      if (lane == 0) {
+        s.taken[bestj >> 5] |= 1u << (bestj & 31);
+        s.sup[k] = nid;
+      }
+      const double *grow = a.gram + nid * T;
+      // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l+32)
+      __syncwarp();
+      for (int64_t l = lane; l < k; l += 32) {
+        double acc = 0.0;
+        for (int64_t i = 0; i <= l; i++) acc = fma(s.linv[l * kw + i], grow[s.sup[i]], acc);
+        s.w[l] = acc;
+      }
+      __syncwarp();
+      double ww = 0.0, wz = 0.0;
+      for (int64_t l = lane; l < k; l += 32) {
+        ww = fma(s.w[l], s.w[l], ww);
+        wz = fma(s.w[l], s.z[l], wz);
+      }
+      ww = warp_sum(ww);
+      wz = warp_sum(wz);
+      const double gnn = grow[nid];
+      const double d2 = gnn - ww;
+      if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
+        delegate = true;
+        kdone = k + 1;
+        break;
+      }
+      const double d = sqrt(d2);
+      const double inv_d = 1.0 / d;
+      const double zk = (s.alpha0[bestj] - wz) * inv_d;
+      // ---- new row of L^{-1}: [-(w^T L^{-1}) / d, 1/d]
+      for (int64_t i = lane; i <= k; i += 32) {
+        double v;
+        if (i == k) {
+          v = inv_d;
+        } else {
+          double acc = 0.0;
+          for (int64_t l = i; l < k; l++) acc = fma(s.w[l], s.linv[l * kw + i], acc);
+          v = -acc * inv_d;
+        }
+        s.linv[k * kw + i] = v;
+      }
+      if (lane == 0) s.z[k] = zk;
+      // ---- h_k over candidates, correlation update
+      double *hk = s.h + k * smax;
+      for (int64_t j = lane; j < S; j += 32) {
+        double acc = grow[cs.id(p, j)];
+        for (int64_t i = 0; i < k; i++) acc = fma(-s.w[i], s.h[i * smax + j], acc);
+        const double h = acc * inv_d;
+        hk[j] = h;
+        s.c[j] = fma(-zk, h, s.c[j]);
+      }
+      rn2 -= zk * zk;
+      kdone = k + 1;
+      __syncwarp();
+      // ---- stop test (_kernels.py:156), exact residual inside the band
+      const double gap = rn2 - tol2;
+      if (gap > band) continue;
+      if (gap < -band) {
+        exact_stop = true;
+        break;
+      }
+      // band: materialise r = y - D_S x exactly and test its norm
+      for (int64_t i = lane; i < kdone; i += 32) {
+        double acc = 0.0;
+        for (int64_t l = i; l < kdone; l++) acc = fma(s.linv[l * kw + i], s.z[l], acc);
+        s.x[i] = acc;
+      }
+      __syncwarp();
+      double rr = 0.0;
+      for (int64_t i = lane; i < n; i += 32) {
+        double ri = s.y[i];
+        for (int64_t l = 0; l < kdone; l++) ri = fma(-s.x[l], a.d64[s.sup[l] * n + i], ri);
+        rr = fma(ri, ri, rr);
+      }
+      rr = warp_sum(rr);
+      if (sqrt(rr) <= tol) {
+        exact_stop = true;
+        break;
+      }
+    }
+    (void)exact_stop;
+  }
+
+  if (delegate) {
+    if (lane == 0) a.status[p] |= ST_DELEGATE;
+    return;  // the exact engine rewrites every output of this signal
+  }
+  // ---- coefficients x = L^{-T} z (pick order), exact final residual norm
+  __syncwarp();
+  for (int64_t i = lane; i < kdone; i += 32) {
+    double acc = 0.0;
+    for (int64_t l = i; l < kdone; l++) acc = fma(s.linv[l * kw + i], s.z[l], acc);
+    s.x[i] = acc;
+  }
+  __syncwarp();
+  if (kdone > 0) {
+    double rr = 0.0;
+    for (int64_t i = lane; i < n; i += 32) {
+      double ri = s.y[i];
+      for (int64_t l = 0; l < kdone; l++) ri = fma(-s.x[l], a.d64[s.sup[l] * n + i], ri);
+      rr = fma(ri, ri, rr);
+    }
+    rnorm = sqrt(warp_sum(rr));
+  }
+  for (int64_t j = lane; j < kw; j += 32) {
+    out_sel[j] = j < kdone ? s.sup[j] : -1;
+    out_coef[j] = j < kdone ? s.x[j] : 0.0;
+  }
+  if (lane == 0) {
+    a.out_count[p] = kdone;
+    a.out_rnorm[p] = rnorm;
+    a.out_scans[p] = scans;
+    a.out_flag[p] = 0;
+  }
+}
+
+}  // namespace
+
+int64_t gram_total_smem(int64_t s, int64_t kw, int64_t n, bool h_in_smem) {
+  int64_t b = align8(gram_smem_bytes_no_h(s, kw, n));
+  if (h_in_smem) b += 8 * s * kw;
+  return (b + 15) & ~int64_t(15);
+}
+
+cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
+                        int num_sms, cudaStream_t stream) {
+  (void)num_sms;
+  if (args.p <= 0) return cudaSuccess;
+  const int64_t s = args.max_cands, kw = args.k_width, n = args.n;
+  const bool h_in_smem = args.hwork == nullptr;
+  const int64_t per_warp = gram_total_smem(s, kw, n, h_in_smem);
+  if (per_warp > max_smem_per_block) return cudaErrorInvalidValue;
+  int wpb = (int)(max_smem_per_block / per_warp);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) wpb = 1;
+  const int64_t smem = per_warp * wpb;
+  const int64_t blocks = (args.p + wpb - 1) / wpb;
+  cudaError_t e;
+  if (ys_f32) {
+    e = cudaFuncSetAttribute(gram_omp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    gram_omp_kernel<float><<<(unsigned)blocks, wpb * 32, smem, stream>>>(
+        args, (const float *)ys, h_in_smem ? 1 : 0, per_warp);
+  } else {
+    e = cudaFuncSetAttribute(gram_omp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    gram_omp_kernel<double><<<(unsigned)blocks, wpb * 32, smem, stream>>>(
+        args, (const double *)ys, h_in_smem ? 1 : 0, per_warp);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cdb

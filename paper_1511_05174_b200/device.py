@@ -1,0 +1,152 @@
+"""Device-resident dictionaries and the raw batched calls (C ABI wrappers).
+
+A dictionary enters the path as ``atoms_t`` (T x N fp64, the reference's
+kernel operand, crossdict/tensor.py:124-129).  ``device_dictionary`` stages it
+once per array (identity for read-only arrays such as ``Dictionary.atoms_t``,
+content digest for writable ones) and keeps the handle cached, so repeated
+calls -- K-SVD coding stages, pipelines over many images -- pay the upload,
+bf16 conversion and Gram build once.
+
+Every array argument of the ``*_raw`` calls may be a host numpy array or a
+CUDA tensor (anything with ``data_ptr()``); the library stages host memory.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import weakref
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native as N
+
+#: build the fp64 Gram matrix when T*T*8 bytes fit this budget
+GRAM_BUDGET_BYTES = 4 << 30
+#: number of staged dictionaries kept alive
+CACHE_ENTRIES = 8
+
+
+class DeviceDictionary:
+    """Opaque ``cdb_dictionary`` handle (fp64 atoms, bf16 operand, fp64 Gram)."""
+
+    def __init__(self, atoms_t: np.ndarray, gram_budget: int = GRAM_BUDGET_BYTES):
+        atoms_t = np.ascontiguousarray(atoms_t, dtype=np.float64)
+        self.t, self.n = atoms_t.shape
+        self._handle = ctypes.c_void_p()
+        self._lib = N.load()
+        N.check(self._lib.cdb_dictionary_create(N.ptr(atoms_t), self.t, self.n, int(gram_budget),
+                                                None, ctypes.byref(self._handle)))
+
+    @property
+    def handle(self):
+        return self._handle
+
+    @property
+    def nbytes(self) -> int:
+        return int(self._lib.cdb_dictionary_bytes(self._handle))
+
+    def close(self):
+        if self._handle:
+            self._lib.cdb_dictionary_destroy(self._handle)
+            self._handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_cache: "OrderedDict[tuple, tuple]" = OrderedDict()
+
+
+def device_dictionary(atoms_t: np.ndarray) -> DeviceDictionary:
+    """Cached device staging of a T x N atom-row matrix."""
+    atoms_t = np.asarray(atoms_t)
+    if not atoms_t.flags.writeable:
+        key = ("ro", id(atoms_t), atoms_t.shape)
+        hit = _cache.get(key)
+        if hit is not None and hit[0]() is atoms_t:
+            _cache.move_to_end(key)
+            return hit[1]
+        ref = weakref.ref(atoms_t)
+    else:
+        data = np.ascontiguousarray(atoms_t, dtype=np.float64)
+        key = ("rw", atoms_t.shape, hashlib.blake2b(data.tobytes(), digest_size=16).hexdigest())
+        hit = _cache.get(key)
+        if hit is not None:
+            _cache.move_to_end(key)
+            return hit[1]
+        ref = (lambda: None)
+    dd = DeviceDictionary(atoms_t)
+    _cache[key] = (ref, dd)
+    while len(_cache) > CACHE_ENTRIES:
+        _cache.popitem(last=False)[1][1].close()
+    return dd
+
+
+def clear_cache():
+    while _cache:
+        _cache.popitem(last=False)[1][1].close()
+
+
+def _out(p, k):
+    return dict(sel=np.empty((p, k), np.int64), alpha=np.empty((p, k)),
+                counts=np.empty(p, np.int64), rnorm=np.empty(p), scans=np.empty(p, np.int64),
+                flag=np.empty(p, np.uint8))
+
+
+def _out_ptrs(o):
+    return [N.ptr(o[k]) for k in ("sel", "alpha", "counts", "rnorm", "scans", "flag")]
+
+
+def _ys_arg(ys):
+    """(pointer, is_f32) for fp64/fp32 signal rows (numpy or CUDA tensor)."""
+    if isinstance(ys, np.ndarray):
+        if ys.dtype == np.float32:
+            return N.ptr(np.ascontiguousarray(ys)), 1
+        return N.ptr(np.ascontiguousarray(ys, dtype=np.float64)), 0
+    import torch  # device tensor
+    return N.ptr(ys), 1 if ys.dtype == torch.float32 else 0
+
+
+def omp_batch_raw(dd: DeviceDictionary, ys, p: int, k_max: int, eps, allowed=None,
+                  engine: str = "auto", out=None, stream=None):
+    """cdb_omp_batch: signals as rows; returns the BatchSolve arrays (dict)."""
+    o = out if out is not None else _out(p, k_max)
+    yptr, f32 = _ys_arg(ys)
+    s = 0 if allowed is None else int(allowed.shape[1])
+    N.check(N.load().cdb_omp_batch(dd.handle, yptr, f32, p, k_max, N.ptr(eps), N.ptr(allowed), s,
+                                   0 if allowed is None else 1, *_out_ptrs(o),
+                                   N.ENGINES[engine], stream))
+    return o
+
+
+def omp_batch_blocked_raw(dd: DeviceDictionary, ys, p: int, k_max: int, eps, blocks, q: int,
+                          engine: str = "auto", out=None, stream=None):
+    """cdb_omp_batch_blocked: allowed = blocks * q + [0, q)."""
+    o = out if out is not None else _out(p, k_max)
+    yptr, f32 = _ys_arg(ys)
+    N.check(N.load().cdb_omp_batch_blocked(dd.handle, yptr, f32, p, k_max, N.ptr(eps),
+                                           N.ptr(blocks), int(blocks.shape[1]), int(q),
+                                           *_out_ptrs(o), N.ENGINES[engine], stream))
+    return o
+
+
+def zero_tree_raw(low: DeviceDictionary, high: DeviceDictionary, fine_shape, factors, ys,
+                  p: int, k1: int, k_high: int, rel_tol: float, phi_mode: bool,
+                  engine: str = "auto", out_low=None, out_high=None, stream=None):
+    """cdb_zero_tree_batch; returns (low dict, high dict, [step1_ms, step2_ms])."""
+    lo = out_low if out_low is not None else _out(p, k1)
+    hi = out_high if out_high is not None else _out(p, k_high)
+    fs = np.asarray(fine_shape if fine_shape is not None else [1], dtype=np.int64)
+    fa = np.asarray(factors if factors is not None else [1], dtype=np.int64)
+    ms = np.zeros(2, np.float32)
+    yptr, f32 = _ys_arg(ys)
+    N.check(N.load().cdb_zero_tree_batch(low.handle, high.handle, N.ptr(fs), N.ptr(fa), int(fs.size),
+                                         yptr, f32, p, k1, k_high, float(rel_tol), int(phi_mode),
+                                         *_out_ptrs(lo), *_out_ptrs(hi), N.ENGINES[engine],
+                                         N.ptr(ms), stream))
+    return lo, hi, ms

@@ -1,0 +1,84 @@
+"""Drop-in installation into the reference package ``crossdict``.
+
+``install()`` rebinds the reference's pursuit entry points -- wherever the
+reference imported them by name -- to this package's B200 implementations:
+
+* ``crossdict.pursuit.{omp, omp_many, omp_many_arrays}``      (pursuit.py:253-461)
+* ``crossdict.crossscale.{zero_tree_omp, zero_tree_omp_many,
+  zero_tree_many_arrays}``                                    (crossscale.py:169-312)
+* the re-exports in ``crossdict/__init__.py:12-33`` and the by-name imports
+  of the callers ``crossdict.pipelines`` (pipelines.py:214-297) and
+  ``crossdict.learn`` (learn.py:245-260).
+
+After installation results are the reference's own types (``PursuitResult``,
+``BatchSolve``, ``SparseCode``, ``ZeroTreeResult``), errors are its own
+exception classes, and ``crossdict.pursuit.REL_RESIDUAL_TOL`` is the global
+read at call time -- callers cannot tell the difference except for speed.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import crossscale as _cs
+from . import errors as _errors
+from . import pursuit as _pursuit
+
+_saved: dict = {}
+_ERRORS = ("CrossdictError", "DimensionError", "DomainError", "DegenerateAtomError",
+           "ConfigError")
+_FUNCS = {
+    "omp": _pursuit.omp,
+    "omp_many": _pursuit.omp_many,
+    "omp_many_arrays": _pursuit.omp_many_arrays,
+    "zero_tree_omp": _cs.zero_tree_omp,
+    "zero_tree_omp_many": _cs.zero_tree_omp_many,
+    "zero_tree_many_arrays": _cs.zero_tree_many_arrays,
+}
+_MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
+            "crossdict.learn")
+
+
+def install(package: str = "crossdict") -> list:
+    """Rebind the reference's entry points; returns the patched 'module.name' list."""
+    if _saved:
+        return sorted(k for k in _saved if not k.startswith("#"))
+    ref_pursuit = importlib.import_module(f"{package}.pursuit")
+    ref_cs = importlib.import_module(f"{package}.crossscale")
+    ref_tensor = importlib.import_module(f"{package}.tensor")
+    ref_errors = importlib.import_module(f"{package}.errors")
+    patched = []
+    for modname in _MODULES:
+        modname = modname.replace("crossdict", package, 1)
+        try:
+            mod = importlib.import_module(modname)
+        except ImportError:
+            continue
+        for name, fn in _FUNCS.items():
+            if hasattr(mod, name):
+                _saved[f"{modname}.{name}"] = (mod, name, getattr(mod, name))
+                setattr(mod, name, fn)
+                patched.append(f"{modname}.{name}")
+    _saved["#types"] = dict(_pursuit._types)
+    _pursuit._types.update(SparseCode=ref_tensor.SparseCode, PursuitResult=ref_pursuit.PursuitResult,
+                           BatchSolve=ref_pursuit.BatchSolve, ZeroTreeResult=ref_cs.ZeroTreeResult,
+                           pursuit_module=ref_pursuit)
+    _saved["#errors"] = {n: getattr(_errors, n) for n in _ERRORS}
+    for n in _ERRORS:
+        setattr(_errors, n, getattr(ref_errors, n))
+    return patched
+
+
+def uninstall() -> None:
+    """Restore everything install() changed."""
+    for key, val in list(_saved.items()):
+        if key == "#types":
+            _pursuit._types.clear()
+            _pursuit._types.update(val)
+        elif key == "#errors":
+            for n, cls in val.items():
+                setattr(_errors, n, cls)
+        else:
+            mod, name, orig = val
+            setattr(mod, name, orig)
+    _saved.clear()
