@@ -141,6 +141,10 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
 /* Number of kernels this library has launched since load (instrumentation). */
 int64_t cdb_launch_count(void);
 
+/* Engine used by the last OMP pass on this thread, and how many of its
+ * signals were handed to the exact engine (instrumentation). */
+void cdb_last_run_info(int *engine, int *delegated);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,8 @@ ENGINES = {"auto": 0, "exact": 1, "gram": 2, "tensor": 3}
 #: every symbol include/crossdict_b200.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",
            "cdb_dictionary_destroy", "cdb_dictionary_bytes", "cdb_omp_batch",
-           "cdb_omp_batch_blocked", "cdb_zero_tree_batch", "cdb_launch_count")
+           "cdb_omp_batch_blocked", "cdb_zero_tree_batch", "cdb_launch_count",
+           "cdb_last_run_info")
 
 _lib = None
 
@@ -45,6 +46,8 @@ def load():
     lib.cdb_last_error.restype = ctypes.c_char_p
     lib.cdb_launch_count.restype = I64
     lib.cdb_device_info.argtypes = [P, P, P]
+    lib.cdb_last_run_info.argtypes = [P, P]
+    lib.cdb_last_run_info.restype = None
     lib.cdb_dictionary_create.argtypes = [P, I64, I64, I64, P, P]
     lib.cdb_dictionary_destroy.argtypes = [P]
     lib.cdb_dictionary_bytes.argtypes = [P]
@@ -76,6 +79,14 @@ def ptr(a) -> ctypes.c_void_p | None:
     if isinstance(a, np.ndarray):
         return ctypes.c_void_p(a.ctypes.data)
     return ctypes.c_void_p(a.data_ptr())  # torch.Tensor (device or pinned host)
+
+
+def last_run_info():
+    """(engine name, delegated signal count) of the last OMP pass on this thread."""
+    e, d = ctypes.c_int(), ctypes.c_int()
+    load().cdb_last_run_info(ctypes.byref(e), ctypes.byref(d))
+    names = {v: k for k, v in ENGINES.items()}
+    return names.get(e.value, str(e.value)), d.value
 
 
 def launch_count() -> int:

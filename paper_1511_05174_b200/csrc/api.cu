@@ -15,12 +15,15 @@ struct cdb_dictionary {
   double *d64 = nullptr;   // T x N fp64 atoms (rows)
   double *gram = nullptr;  // T x T fp64 (optional)
   void *d16 = nullptr;     // T x n_pad bf16 (tensor-core operand)
+  double dmax = 0.0;       // largest atom norm
   int64_t bytes = 0;
 };
 
 namespace {
 
 thread_local std::string g_last_error;
+thread_local int g_last_engine = 0;     // engine the last run_omp used
+thread_local int g_last_delegated = 0;  // signals handed to the exact engine
 std::atomic<int64_t> g_launches{0};
 
 cdb_status fail(cdb_status st, const std::string &msg) {
@@ -181,19 +184,97 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
   return CDB_OK;
 }
 
-// The OMP driver shared by every entry point.
+// Signals an engine handed over (status ST_DELEGATE) -> exact engine.
+cdb_status finish_delegates(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
+                            int64_t k_max, int64_t kw, const double *eps, const cdb::Cands &cands,
+                            int64_t max_cands, Outs &o, const uint32_t *status, const DevInfo &di,
+                            cudaStream_t st) {
+  DevBuf ids, cnt;
+  CDB_CUDA(ids.alloc(sizeof(int64_t) * p, st));
+  CDB_CUDA(cnt.alloc(sizeof(int), st));
+  CDB_CUDA(cudaMemsetAsync(cnt.ptr, 0, sizeof(int), st));
+  CDB_CUDA(cdb::launch_collect_delegates(status, p, ids.as<int64_t>(), cnt.as<int>(), st));
+  int h_cnt = 0;
+  CDB_CUDA(cudaMemcpyAsync(&h_cnt, cnt.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  g_last_delegated = h_cnt;
+  if (h_cnt > 0)
+    return run_exact(d, ys, f32, h_cnt, ids.as<int64_t>(), k_max, kw, eps, cands, max_cands, o,
+                     di, st);
+  return CDB_OK;
+}
+
+cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t p, int64_t k_max,
+                      int64_t kw, const double *eps, const cdb::Cands &cands, Outs &o,
+                      const DevInfo &di, cudaStream_t st) {
+  DevBuf status;
+  CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
+  CDB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(uint32_t) * p, st));
+  const int64_t per = cdb::tensor_state_bytes(1, d->n, kw) + 1024;
+  int64_t chunk = kScratchBudget / per;
+  if (chunk < 128) chunk = 128;
+  if (chunk > p) chunk = p;
+  DevBuf work;
+  CDB_CUDA(work.alloc((size_t)cdb::tensor_state_bytes(chunk, d->n, kw) + 65536, st));
+  const size_t ysz = f32 ? 4 : 8;
+  for (int64_t off = 0; off < p; off += chunk) {
+    cdb::TensorArgs a{};
+    a.p = (p - off) < chunk ? (p - off) : chunk;
+    a.ys = (const uint8_t *)ys + off * d->n * ysz;
+    a.ys_f32 = f32;
+    a.n = d->n;
+    a.n_pad = d->n_pad;
+    a.t = d->t;
+    a.k_max = k_max;
+    a.k_width = kw;
+    a.eps = eps + off;
+    a.d64 = d->d64;
+    a.d16 = d->d16;
+    a.gram = d->gram;
+    a.dmax = d->dmax;
+    a.out_sel = (int64_t *)o.sel.dev + off * kw;
+    a.out_coef = (double *)o.coef.dev + off * kw;
+    a.out_count = (int64_t *)o.count.dev + off;
+    a.out_rnorm = (double *)o.rnorm.dev + off;
+    a.out_scans = (int64_t *)o.scans.dev + off;
+    a.out_flag = (uint8_t *)o.flag.dev + off;
+    a.status = status.as<uint32_t>() + off;
+    a.work = work.ptr;
+    a.num_sms = di.sms;
+    CDB_CUDA(cdb::run_tensor_chunk(a, st));
+  }
+  return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, d->t, o, status.as<uint32_t>(),
+                          di, st);
+}
+
+// The OMP driver shared by every entry point: picks the engine.
+//   exact  : any problem (reference restatement)
+//   gram   : Gram matrix available; H (max_cands x k) kept in smem when it fits
+//   tensor : full-dictionary scans (mode 0) with a Gram matrix
+// auto = gram when H fits in shared memory (small candidate sets: zero-tree
+// steps, small dictionaries), tensor for large full-dictionary scans.
 cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p, int64_t k_max,
                    int64_t kw, const double *eps, const cdb::Cands &cands, int64_t max_cands,
                    Outs &o, int engine, const DevInfo &di, cudaStream_t st) {
   if (p <= 0) return CDB_OK;
-  const int64_t smem_h = cdb::gram_total_smem(max_cands, kw, d->n, true);
-  bool use_gram = false;
-  if (engine == CDB_ENGINE_GRAM || engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_TENSOR)
-    use_gram = d->gram != nullptr && max_cands > 0;
-  if (engine == CDB_ENGINE_GRAM && !d->gram)
-    return fail(CDB_ERR_ARG, "Gram engine requested but the dictionary has no Gram matrix");
-  if (!use_gram)
+  const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit;
+  if (engine == CDB_ENGINE_AUTO) {
+    if (!d->gram || max_cands <= 0)
+      engine = CDB_ENGINE_EXACT;
+    else if (h_smem)
+      engine = CDB_ENGINE_GRAM;
+    else if (cands.mode == 0)
+      engine = CDB_ENGINE_TENSOR;
+    else
+      engine = CDB_ENGINE_GRAM;
+  }
+  if ((engine == CDB_ENGINE_GRAM || engine == CDB_ENGINE_TENSOR) && !d->gram)
+    return fail(CDB_ERR_ARG, "engine needs the dictionary's Gram matrix (raise the budget)");
+  if (engine == CDB_ENGINE_TENSOR && cands.mode != 0) engine = CDB_ENGINE_GRAM;
+  g_last_engine = engine;
+  if (engine == CDB_ENGINE_EXACT)
     return run_exact(d, ys, f32, p, nullptr, k_max, kw, eps, cands, max_cands, o, di, st);
+  if (engine == CDB_ENGINE_TENSOR) return run_tensor(d, ys, f32, p, k_max, kw, eps, cands, o, di, st);
 
   DevBuf status;
   CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
@@ -216,7 +297,6 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   g.out_scans = (int64_t *)o.scans.dev;
   g.out_flag = (uint8_t *)o.flag.dev;
   g.status = status.as<uint32_t>();
-  const bool h_smem = smem_h <= kGramSmemLimit;
   int64_t chunk = p;
   DevBuf hwork;
   if (!h_smem) {
@@ -232,22 +312,8 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
     g.p = (p - off) < chunk ? (p - off) : chunk;
     CDB_CUDA(cdb::launch_gram(g, ys, f32, di.smem_optin, di.sms, st));
   }
-  // signals the Gram engine handed over -> exact engine
-  DevBuf ids, cnt;
-  CDB_CUDA(ids.alloc(sizeof(int64_t) * p, st));
-  CDB_CUDA(cnt.alloc(sizeof(int), st));
-  CDB_CUDA(cudaMemsetAsync(cnt.ptr, 0, sizeof(int), st));
-  CDB_CUDA(cdb::launch_collect_delegates(status.as<uint32_t>(), p, ids.as<int64_t>(),
-                                         cnt.as<int>(), st));
-  int h_cnt = 0;
-  CDB_CUDA(cudaMemcpyAsync(&h_cnt, cnt.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CDB_CUDA(cudaStreamSynchronize(st));
-  if (h_cnt > 0) {
-    cdb_status s2 =
-        run_exact(d, ys, f32, h_cnt, ids.as<int64_t>(), k_max, kw, eps, cands, max_cands, o, di, st);
-    if (s2 != CDB_OK) return s2;
-  }
-  return CDB_OK;
+  return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, max_cands, o,
+                          status.as<uint32_t>(), di, st);
 }
 
 }  // namespace
@@ -261,6 +327,11 @@ extern "C" {
 const char *cdb_last_error(void) { return g_last_error.c_str(); }
 
 int64_t cdb_launch_count(void) { return g_launches.load(); }
+
+void cdb_last_run_info(int *engine, int *delegated) {
+  if (engine) *engine = g_last_engine;
+  if (delegated) *delegated = g_last_delegated;
+}
 
 cdb_status cdb_device_info(int *sm_count, int *cc_major, int *cc_minor) {
   DevInfo di;
@@ -300,6 +371,15 @@ cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
   d->bytes += b16;
   if (cdb::launch_to_bf16(d->d64, t, n, d->n_pad, d->d16, st) != cudaSuccess)
     return cleanup(CDB_ERR_CUDA, "bf16 conversion");
+  {
+    double *dm = nullptr;
+    if (cudaMallocAsync((void **)&dm, sizeof(double), st) != cudaSuccess)
+      return cleanup(CDB_ERR_NOMEM, "dmax alloc");
+    if (cdb::launch_row_norm_max(d->d64, t, n, dm, st) != cudaSuccess ||
+        cudaMemcpyAsync(&d->dmax, dm, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return cleanup(CDB_ERR_CUDA, "dmax kernel");
+    cudaFreeAsync(dm, st);
+  }
   const double gb = 8.0 * (double)t * (double)t;
   if (gb <= (double)gram_budget_bytes) {
     if (cudaMalloc(&d->gram, (size_t)gb) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "gram alloc");

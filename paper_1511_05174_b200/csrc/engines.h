@@ -59,7 +59,32 @@ int64_t gram_total_smem(int64_t max_cands, int64_t k_width, int64_t n, bool h_in
 cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
                         int num_sms, cudaStream_t stream);
 
+// ---------------------------------------------------------------- tensor
+struct TensorArgs {
+  const void *ys;
+  bool ys_f32;
+  int64_t p, n, n_pad, t, k_max, k_width;
+  const double *eps;
+  const double *d64;
+  const void *d16;
+  const double *gram;
+  double dmax;           // max atom norm (error bound)
+  int64_t *out_sel;
+  double *out_coef;
+  int64_t *out_count;
+  double *out_rnorm;
+  int64_t *out_scans;
+  uint8_t *out_flag;
+  uint32_t *status;
+  void *work;            // tensor_state_bytes(p, n, k_width) bytes
+  int num_sms;
+};
+int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw);
+cudaError_t run_tensor_chunk(const TensorArgs &args, cudaStream_t stream);
+
 // ---------------------------------------------------------------- helpers
+cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double *out,
+                                cudaStream_t stream);
 cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
                               const int64_t *fine_shape, const int64_t *factors, int rank,
                               double *y_low, int64_t n_low, cudaStream_t stream);

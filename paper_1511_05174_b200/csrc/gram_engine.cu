@@ -34,10 +34,13 @@ namespace {
 struct GramSmem {
   double *y;       // n
   double *alpha0;  // S
-  double *c;       // S
-  double *linv;    // kw * kw (row-major, lower triangle)
+  double *c;       // S    current correlations
+  double *gc;      // S    G[new, C] (this iteration's Gram row slice)
+  double *lr;      // kw*kw  L^{-1} row-major  (lr[l*kw+i])
+  double *lc;      // kw*kw  L^{-1} col-major  (lc[i*kw+l])
   double *z;       // kw
   double *w;       // kw
+  double *g;       // kw   G[new, support]
   double *x;       // kw
   int64_t *sup;    // kw
   uint32_t *taken; // (S + 31) / 32
@@ -47,7 +50,36 @@ struct GramSmem {
 __host__ __device__ inline int64_t align8(int64_t v) { return (v + 7) & ~int64_t(7); }
 
 __host__ __device__ inline int64_t gram_smem_bytes_no_h(int64_t s, int64_t kw, int64_t n) {
-  return 8 * (n + 2 * s + kw * kw + 3 * kw) + 8 * kw + 4 * align8((s + 31) / 32);
+  return 8 * (n + 3 * s + 2 * kw * kw + 4 * kw) + 8 * kw + 4 * align8((s + 31) / 32);
+}
+
+// alpha0_j = <d_{C_j}, y> for every candidate: the warp streams 8 atom rows
+// at a time with coalesced loads (lane i reads element i of each row) and
+// reduces the 8 partial sums across the warp.
+__device__ __forceinline__ void alpha0_rows(const double *__restrict__ d64, const Cands &cs,
+                                            int64_t p, int64_t S, int64_t n, const double *y,
+                                            double *alpha0, double *c, int lane) {
+  for (int64_t j0 = 0; j0 < S; j0 += 8) {
+    const double *rows[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) rows[r] = d64 + (j0 + r < S ? cs.id(p, j0 + r) : 0) * n;
+    double acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) acc[r] = 0.0;
+    for (int64_t i = lane; i < n; i += 32) {
+      const double yi = y[i];
+#pragma unroll
+      for (int r = 0; r < 8; r++) acc[r] = fma(__ldg(rows[r] + i), yi, acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const double v = warp_sum(acc[r]);
+      if (lane == r && j0 + r < S) {
+        alpha0[j0 + r] = v;
+        c[j0 + r] = v;
+      }
+    }
+  }
 }
 
 template <typename YT>
@@ -67,10 +99,13 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   s.y = (double *)base;
   s.alpha0 = s.y + n;
   s.c = s.alpha0 + smax;
-  s.linv = s.c + smax;
-  s.z = s.linv + kw * kw;
+  s.gc = s.c + smax;
+  s.lr = s.gc + smax;
+  s.lc = s.lr + kw * kw;
+  s.z = s.lc + kw * kw;
   s.w = s.z + kw;
-  s.x = s.w + kw;
+  s.g = s.w + kw;
+  s.x = s.g + kw;
   s.sup = (int64_t *)(s.x + kw);
   s.taken = (uint32_t *)(s.sup + kw);
   s.h = h_in_smem ? (double *)(base + align8(gram_smem_bytes_no_h(smax, kw, n)))
@@ -89,17 +124,10 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
 
   int64_t kdone = 0, scans = 0;
   double rnorm = ynorm;
-  bool delegate = false, exact_stop = false;
+  bool delegate = false;
 
   if (!(ynorm <= tol) && k_max > 0) {
-    // alpha0_j = <d_j, y> for every candidate (lane per candidate).
-    for (int64_t j = lane; j < S; j += 32) {
-      const double *dj = a.d64 + cs.id(p, j) * n;
-      double acc = 0.0;
-      for (int64_t i = 0; i < n; i++) acc = fma(dj[i], s.y[i], acc);
-      s.alpha0[j] = acc;
-      s.c[j] = acc;
-    }
+    alpha0_rows(a.d64, cs, p, S, n, s.y, s.alpha0, s.c, lane);
     double yy = 0.0;
     for (int64_t i = lane; i < n; i += 32) yy = fma(s.y[i], s.y[i], yy);
     yy = warp_sum(yy);
@@ -128,12 +156,17 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
         s.taken[bestj >> 5] |= 1u << (bestj & 31);
         s.sup[k] = nid;
       }
+      // ---- gathers from Gram row `nid` (independent loads, all lanes)
       const double *grow = a.gram + nid * T;
-      // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l+32)
+      for (int64_t l = lane; l < k; l += 32) s.g[l] = __ldg(grow + s.sup[l]);
+#pragma unroll 4
+      for (int64_t j = lane; j < S; j += 32) s.gc[j] = __ldg(grow + cs.id(p, j));
+      const double gnn = __ldg(grow + nid);
       __syncwarp();
+      // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l+32)
       for (int64_t l = lane; l < k; l += 32) {
         double acc = 0.0;
-        for (int64_t i = 0; i <= l; i++) acc = fma(s.linv[l * kw + i], grow[s.sup[i]], acc);
+        for (int64_t i = 0; i <= l; i++) acc = fma(s.lc[i * kw + l], s.g[i], acc);
         s.w[l] = acc;
       }
       __syncwarp();
@@ -144,11 +177,9 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
       }
       ww = warp_sum(ww);
       wz = warp_sum(wz);
-      const double gnn = grow[nid];
       const double d2 = gnn - ww;
       if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
         delegate = true;
-        kdone = k + 1;
         break;
       }
       const double d = sqrt(d2);
@@ -161,16 +192,17 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
           v = inv_d;
         } else {
           double acc = 0.0;
-          for (int64_t l = i; l < k; l++) acc = fma(s.w[l], s.linv[l * kw + i], acc);
+          for (int64_t l = i; l < k; l++) acc = fma(s.w[l], s.lr[l * kw + i], acc);
           v = -acc * inv_d;
         }
-        s.linv[k * kw + i] = v;
+        s.lr[k * kw + i] = v;
+        s.lc[i * kw + k] = v;
       }
       if (lane == 0) s.z[k] = zk;
       // ---- h_k over candidates, correlation update
       double *hk = s.h + k * smax;
       for (int64_t j = lane; j < S; j += 32) {
-        double acc = grow[cs.id(p, j)];
+        double acc = s.gc[j];
         for (int64_t i = 0; i < k; i++) acc = fma(-s.w[i], s.h[i * smax + j], acc);
         const double h = acc * inv_d;
         hk[j] = h;
@@ -182,14 +214,10 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
       // ---- stop test (_kernels.py:156), exact residual inside the band
       const double gap = rn2 - tol2;
       if (gap > band) continue;
-      if (gap < -band) {
-        exact_stop = true;
-        break;
-      }
-      // band: materialise r = y - D_S x exactly and test its norm
+      if (gap < -band) break;
       for (int64_t i = lane; i < kdone; i += 32) {
         double acc = 0.0;
-        for (int64_t l = i; l < kdone; l++) acc = fma(s.linv[l * kw + i], s.z[l], acc);
+        for (int64_t l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
         s.x[i] = acc;
       }
       __syncwarp();
@@ -200,12 +228,8 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
         rr = fma(ri, ri, rr);
       }
       rr = warp_sum(rr);
-      if (sqrt(rr) <= tol) {
-        exact_stop = true;
-        break;
-      }
+      if (sqrt(rr) <= tol) break;
     }
-    (void)exact_stop;
   }
 
   if (delegate) {
@@ -216,7 +240,7 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   __syncwarp();
   for (int64_t i = lane; i < kdone; i += 32) {
     double acc = 0.0;
-    for (int64_t l = i; l < kdone; l++) acc = fma(s.linv[l * kw + i], s.z[l], acc);
+    for (int64_t l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
     s.x[i] = acc;
   }
   __syncwarp();
@@ -224,7 +248,7 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
     double rr = 0.0;
     for (int64_t i = lane; i < n; i += 32) {
       double ri = s.y[i];
-      for (int64_t l = 0; l < kdone; l++) ri = fma(-s.x[l], a.d64[s.sup[l] * n + i], ri);
+      for (int64_t l = 0; l < kdone; l++) ri = fma(-s.x[l], __ldg(a.d64 + s.sup[l] * n + i), ri);
       rr = fma(ri, ri, rr);
     }
     rnorm = sqrt(warp_sum(rr));

@@ -135,6 +135,17 @@ __global__ void collect_delegates_kernel(const uint32_t *__restrict__ status, in
   if (status[s] & ST_DELEGATE) ids[atomicAdd(count, 1)] = s;
 }
 
+__global__ void row_norm_max_kernel(const double *__restrict__ d, int64_t t, int64_t n,
+                                    unsigned long long *__restrict__ out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= t) return;
+  double acc = 0.0;
+  for (int64_t i = lane; i < n; i += 32) acc = fma(d[w * n + i], d[w * n + i], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(sqrt(acc)));
+}
+
 inline unsigned blocks_for(int64_t work, int threads) {
   return (unsigned)((work + threads - 1) / threads);
 }
@@ -202,6 +213,16 @@ cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t 
                                      cudaStream_t stream) {
   if (p <= 0) return cudaSuccess;
   collect_delegates_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(status, p, ids, count);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double *out,
+                                cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), stream);
+  if (e != cudaSuccess) return e;
+  row_norm_max_kernel<<<blocks_for(t * 32, 256), 256, 0, stream>>>(d64, t, n,
+                                                                     (unsigned long long *)out);
   note_launch();
   return cudaGetLastError();
 }

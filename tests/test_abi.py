@@ -1,0 +1,40 @@
+"""The C-ABI library loads without a GPU and exports every declared symbol."""
+
+import ctypes
+import os
+import re
+
+from paper_1511_05174_b200 import _native as N
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "crossdict_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cdb_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_python_symbol_list():
+    assert declared_functions() == sorted(N.SYMBOLS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    lib = N.load()
+    for name in declared_functions():
+        assert isinstance(getattr(lib, name), ctypes._CFuncPtr), name
+
+
+def test_library_is_sm100a_only():
+    # every kernel image in the .so is sm_100a SASS (no PTX JIT fallback)
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-lelf", N.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        return  # cuobjdump unavailable
+    archs = set(re.findall(r"sm_(\d+a?)", out.stdout))
+    assert archs == {"100a"}, archs
+
+
+def test_launch_counter_callable_without_gpu():
+    assert N.launch_count() >= 0
