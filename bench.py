@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: signals/s of zero-tree OMP (headline) and full OMP on B200.
+
+Workload: BASELINE.json configs[1] ("video": N=256 fine / 32 coarse, T_high=2048,
+T_low=256, Q=8, K=16, 100,000 signals, sigma=0.01, fp32 inputs, stop at K or
+|r| <= 1e-3 |y|) -- the largest config whose metric fits one GPU comfortably.
+Synthetic, seeded (paper_1511_05174_b200.workloads); each rank codes its
+own 100,000-signal shard of the deterministic stream (weak scaling, no
+data-path collective: signals are independent).
+
+A step = one pass of the hot path over the whole batch.  `value` times the
+step through the C ABI with the inputs resident in HBM (CUDA events on the
+launching stream, L2 flushed between steps); `e2e` times the same C-ABI call
+with pinned HOST buffers (H2D of the inputs and D2H of every output inside
+the timed region).  `--impl reference` times the reference algorithm on the
+host cores (oracle/, the C restatement of crossdict's kernel, all threads)
+on a bounded sample of the same workload.
+
+Run:  python bench.py [--gpus N --steps K --warmup W]   (torchrun for N > 1)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1511_05174_b200 import workloads as W  # noqa: E402
+
+METRIC = "signals/sec for zero-tree OMP and full OMP at 1/2/4/8 B200; % of roofline"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return dict(PEAKS_FALLBACK), "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        smax = None
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                smax = float(s[1])
+            except ValueError:
+                continue
+            for i, nm in enumerate(names):
+                if s[2 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def flops_ls(n, counts):
+    """MGS/Cholesky least-squares flops of the reference cost model,
+    4N k(k-1) + 11 N k per signal, summed over signals."""
+    k = counts.astype(np.float64)
+    return float(np.sum(4.0 * n * k * (k - 1.0) + 11.0 * n * k))
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_oracle_zero_tree(ci, ys_rows, threads):
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    if w.measurements:
+        return O.zero_tree_phi_many(d.e_low_t, d.e_high_t, w.k, w.k, ys_rows, rel_tol=W.REL_TOL,
+                                    nthreads=threads)
+    return O.zero_tree_many_arrays(d.low_t, d.high_t, w.fine_shape, w.factors, w.k, w.k, ys_rows,
+                                   rel_tol=W.REL_TOL, nthreads=threads)
+
+
+def cpu_rate(ci, threads, budget_s=12.0, max_signals=65536):
+    """Oracle zero-tree sig/s on a bounded sample (calibrated to ~budget_s)."""
+    probe = W.signals(ci, 0, 256)
+    t0 = time.perf_counter()
+    run_oracle_zero_tree(ci, probe, threads)
+    rate = 256 / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(max_signals, max(256, rate * budget_s)))
+    ys = W.signals(ci, 0, n)
+    t0 = time.perf_counter()
+    run_oracle_zero_tree(ci, ys, threads)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+# ------------------------------------------------------------------ reference arm
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    ci = args.config
+    threads = cpu_threads()
+    w = W.CONFIGS[ci]
+    # bounded per-step sample so that warmup + steps finish within minutes
+    probe = W.signals(ci, 0, 256)
+    t0 = time.perf_counter()
+    run_oracle_zero_tree(ci, probe, threads)
+    rate = 256 / max(time.perf_counter() - t0, 1e-6)
+    sample = int(min(w.signals, max(256, rate * 4.0)))
+    ys = W.signals(ci, 0, sample)
+    for _ in range(args.warmup):
+        run_oracle_zero_tree(ci, ys[: min(sample, 512)], threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run_oracle_zero_tree(ci, ys, threads)
+        times.append(time.perf_counter() - t0)
+    value = sample * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "signals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, fp32-exact inputs)",
+        "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP",
+                   "signals_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "signals/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} signals of configs[{ci}] per step "
+                                   f"(oracle/omp_oracle.c, {threads} threads)"},
+        "e2e": {"value": value, "unit": "signals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1511_05174_b200 import _native as N
+    from paper_1511_05174_b200 import device as D
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ci = args.config
+    w = W.CONFIGS[ci]
+    P = args.signals or w.signals
+    phi = bool(w.measurements)
+    d = W.dictionaries(ci)
+    low_t = d.e_low_t if phi else d.low_t
+    high_t = d.e_high_t if phi else d.high_t
+    k1 = min(w.k, w.n_signal, w.t_low) if phi else w.k
+    fs = None if phi else w.fine_shape
+    fa = None if phi else w.factors
+
+    ys_host = W.signals(ci, rank * P, (rank + 1) * P).astype(np.float32)
+    yd = torch.from_numpy(ys_host).cuda()
+    eps_full = torch.from_numpy(
+        W.REL_TOL * np.linalg.norm(ys_host.astype(np.float64), axis=1)).cuda()
+    lo = D.device_dictionary(low_t)
+    hi = D.device_dictionary(high_t)
+
+    def outs(k, dev="cuda", pin=False):
+        mk = (lambda shape, dt: torch.empty(shape, dtype=dt, device=dev, pin_memory=pin))
+        return dict(sel=mk((P, k), torch.int64), alpha=mk((P, k), torch.float64),
+                    counts=mk((P,), torch.int64), rnorm=mk((P,), torch.float64),
+                    scans=mk((P,), torch.int64), flag=mk((P,), torch.uint8))
+
+    olo, ohi, ofull = outs(k1), outs(w.k), outs(w.k)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def zt_step():
+        D.zero_tree_raw(lo, hi, fs, fa, yd, P, k1, w.k, W.REL_TOL, phi, "auto", olo, ohi)
+
+    def full_step():
+        D.omp_batch_raw(hi, yd, P, w.k, eps_full, None, "auto", ofull)
+
+    def timed(step, k_steps):
+        total = 0.0
+        for _ in range(k_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            total += a.elapsed_time(b)
+        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        zt_step()
+        full_step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = N.launch_count()
+    N.profile_enable(True)
+    zt_ms = timed(zt_step, args.steps)
+    prof_zt = N.profile_read()
+    N.profile_enable(True)
+    full_ms = timed(full_step, args.steps)
+    prof_full = N.profile_read()
+    N.profile_enable(False)
+    launches = N.launch_count() - launches0
+    clk = clocks.stop()
+    engine_full = N.last_run_info()
+
+    # ---- e2e through the C ABI with pinned host buffers
+    yh = torch.from_numpy(ys_host).pin_memory()
+    hlo, hhi = outs(k1, "cpu", True), outs(w.k, "cpu", True)
+    # numpy views so the library sees host pointers
+    def npv(o):
+        return {k: v.numpy() for k, v in o.items()}
+    hlo_n, hhi_n, yh_n = npv(hlo), npv(hhi), yh.numpy()
+    D.zero_tree_raw(lo, hi, fs, fa, yh_n, P, k1, w.k, W.REL_TOL, phi, "auto", hlo_n, hhi_n)
+    e2e_total = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        D.zero_tree_raw(lo, hi, fs, fa, yh_n, P, k1, w.k, W.REL_TOL, phi, "auto", hlo_n, hhi_n)
+        e2e_total += time.perf_counter() - t0
+    t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_total = float(t.item())
+    h2d = P * w.n_signal * 4
+    d2h = sum(v.numel() * v.element_size() for o in (hlo, hhi) for v in o.values())
+
+    # ---- roofline of the dominant kernel (zero-tree step), algorithmic flops
+    peaks, peaks_kind = load_peaks()
+    low_scans = olo["scans"].double().sum().item()
+    high_scans = ohi["scans"].double().sum().item()
+    n_low = w.n_signal if phi else w.n_low
+    flops = {
+        "gram_step1": 2.0 * n_low * low_scans + flops_ls(n_low, olo["counts"].cpu().numpy()),
+        "gram_step2": 2.0 * w.n_signal * high_scans + flops_ls(w.n_signal,
+                                                             ohi["counts"].cpu().numpy()),
+    }
+    dom = max(prof_zt.items(), key=lambda kv: kv[1][0]) if prof_zt else ("none", (1.0, 1))
+    dom_name, (dom_ms_total, dom_launches) = dom
+    dom_ms = dom_ms_total / max(dom_launches, 1)
+    p_emu = peaks["bf16_tflops"] / 6.0
+    dom_flops = flops.get(dom_name, 0.0)
+    achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
+    roofline = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": p_emu,
+                "unit": "TFLOP/s", "frac": achieved / p_emu if p_emu else None, "traffic": None,
+                "basis": "SURVEY §8.0 algorithmic flops 2*N*scans + 4Nk(k-1) + 11Nk per signal "
+                         f"(actual scan counts) / mean launch time; peak = {peaks_kind} bf16 "
+                         f"{peaks['bf16_tflops']} TF/s / 6 (3xTF32-emulated fp32, SURVEY §8(d))",
+                "launch_ms": dom_ms}
+    # full-OMP correlation kernel against the measured bf16 tensor peak
+    corr = prof_full.get("corr_topk")
+    full_roof = None
+    if corr:
+        c_ms = corr[0] / max(corr[1], 1)
+        c_flops = 2.0 * w.n_signal * w.t_high * P  # one launch scores every atom of every signal
+        full_roof = {"bound": "tensor", "kernel": "corr_topk",
+                     "achieved": c_flops / (c_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
+                     "unit": "TFLOP/s",
+                     "frac": c_flops / (c_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                     "traffic": None, "launch_ms": c_ms}
+
+    zt_value = world * P * args.steps / (zt_ms * 1e-3)
+    full_value = world * P * args.steps / (full_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        rate, n, dt = cpu_rate(ci, threads)
+        cpu = {"value": rate, "unit": "signals/s", "cores": threads, "kind": "port",
+               "sample": f"{n} signals of configs[{ci}] zero-tree OMP in {dt:.1f} s "
+                         f"(oracle/omp_oracle.c restating crossdict's kernel, {threads} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": zt_value, "unit": "signals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": zt_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE generator, fp32 inputs, fp64 dictionaries)",
+            "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP: N={w.n_high}, "
+                                   f"N_low={w.n_low}, T_high={w.t_high}, T_low={w.t_low}, "
+                                   f"Q={w.q}, K={w.k}, {P} signals per GPU, stop K or "
+                                   f"|r|<=1e-3|y|",
+                       "signals_per_gpu": P, "l2": "flushed between steps (256 MiB write)"},
+            "full_omp": {"value": full_value, "unit": "signals/s",
+                         "ms_per_step": full_ms / args.steps, "engine": engine_full[0],
+                         "roofline": full_roof},
+            "roofline": roofline,
+            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_zt.items()},
+            "kernels_full_ms_per_step": {k: v[0] / args.steps for k, v in prof_full.items()},
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * P * args.steps / e2e_total, "unit": "signals/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--signals", type=int, default=0, help="signals per GPU (default: config's)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

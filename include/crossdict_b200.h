@@ -138,12 +138,29 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
                                double *high_rnorm, int64_t *high_scans, uint8_t *high_flag,
                                int engine, float *step_ms, void *stream);
 
+/* Device-time profiler: when enabled, every kernel launch is bracketed by
+ * CUDA events on its own stream.  cdb_profile_enable(1) also clears the
+ * records.  cdb_profile_read aggregates per kernel name: up to max_entries
+ * names (name_len bytes each), total milliseconds and launch counts; it
+ * returns the number of distinct kernels recorded. */
+void cdb_profile_enable(int on);
+int cdb_profile_read(int max_entries, char *names, int name_len, double *ms, int64_t *launches);
+
+/* Test hook: one tcgen05 correlation pass (the tensor engine's scan) on
+ * caller residual rows.  rows: P x N fp32 DEVICE; outputs DEVICE: the 8
+ * largest |<d_j, bf16(r)>| per row (cand_idx/cand_val, P x 8) and the largest
+ * value not kept (cand_drop, P).  grid_cap > 0 limits the persistent grid. */
+cdb_status cdb_debug_corr_topk(const cdb_dictionary *dict, const float *rows, int64_t p,
+                               int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
+                               void *stream);
+
 /* Number of kernels this library has launched since load (instrumentation). */
 int64_t cdb_launch_count(void);
 
-/* Engine used by the last OMP pass on this thread, and how many of its
- * signals were handed to the exact engine (instrumentation). */
-void cdb_last_run_info(int *engine, int *delegated);
+/* Engine used by the last OMP pass on this thread, how many of its signals
+ * were handed to the exact engine, and how many picks needed an inline exact
+ * rescan (tensor engine) -- instrumentation. */
+void cdb_last_run_info(int *engine, int *delegated, int *rescans);
 
 #ifdef __cplusplus
 }

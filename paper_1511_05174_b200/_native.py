@@ -23,7 +23,8 @@ ENGINES = {"auto": 0, "exact": 1, "gram": 2, "tensor": 3}
 SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",
            "cdb_dictionary_destroy", "cdb_dictionary_bytes", "cdb_omp_batch",
            "cdb_omp_batch_blocked", "cdb_zero_tree_batch", "cdb_launch_count",
-           "cdb_last_run_info")
+           "cdb_last_run_info", "cdb_profile_enable", "cdb_profile_read",
+           "cdb_debug_corr_topk")
 
 _lib = None
 
@@ -46,8 +47,14 @@ def load():
     lib.cdb_last_error.restype = ctypes.c_char_p
     lib.cdb_launch_count.restype = I64
     lib.cdb_device_info.argtypes = [P, P, P]
-    lib.cdb_last_run_info.argtypes = [P, P]
+    lib.cdb_last_run_info.argtypes = [P, P, P]
     lib.cdb_last_run_info.restype = None
+    lib.cdb_debug_corr_topk.argtypes = [P, P, I64, P, P, P, I32, P]
+    lib.cdb_debug_corr_topk.restype = I32
+    lib.cdb_profile_enable.argtypes = [I32]
+    lib.cdb_profile_enable.restype = None
+    lib.cdb_profile_read.argtypes = [I32, P, I32, P, P]
+    lib.cdb_profile_read.restype = I32
     lib.cdb_dictionary_create.argtypes = [P, I64, I64, I64, P, P]
     lib.cdb_dictionary_destroy.argtypes = [P]
     lib.cdb_dictionary_bytes.argtypes = [P]
@@ -82,11 +89,32 @@ def ptr(a) -> ctypes.c_void_p | None:
 
 
 def last_run_info():
-    """(engine name, delegated signal count) of the last OMP pass on this thread."""
-    e, d = ctypes.c_int(), ctypes.c_int()
-    load().cdb_last_run_info(ctypes.byref(e), ctypes.byref(d))
+    """(engine, delegated signals, inline exact rescans) of the last OMP pass."""
+    e, d, r = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    load().cdb_last_run_info(ctypes.byref(e), ctypes.byref(d), ctypes.byref(r))
     names = {v: k for k, v in ENGINES.items()}
-    return names.get(e.value, str(e.value)), d.value
+    return names.get(e.value, str(e.value)), d.value, r.value
+
+
+def profile_enable(on: bool = True) -> None:
+    load().cdb_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel name: (total ms, launches)} recorded since profile_enable()."""
+    lib = load()
+    n = lib.cdb_profile_read(0, None, 0, None, None)
+    if n <= 0:
+        return {}
+    names = ctypes.create_string_buffer(n * 64)
+    ms = np.zeros(n)
+    cnt = np.zeros(n, np.int64)
+    lib.cdb_profile_read(n, names, 64, ptr(ms), ptr(cnt))
+    out = {}
+    for i in range(n):
+        nm = names.raw[i * 64:(i + 1) * 64].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(cnt[i]))
+    return out
 
 
 def launch_count() -> int:

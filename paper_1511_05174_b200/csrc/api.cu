@@ -15,6 +15,7 @@ struct cdb_dictionary {
   double *d64 = nullptr;   // T x N fp64 atoms (rows)
   double *gram = nullptr;  // T x T fp64 (optional)
   void *d16 = nullptr;     // T x n_pad bf16 (tensor-core operand)
+  float *d32 = nullptr;    // T x N fp32 (residual materialisation of the scan operand)
   double dmax = 0.0;       // largest atom norm
   int64_t bytes = 0;
 };
@@ -24,6 +25,7 @@ namespace {
 thread_local std::string g_last_error;
 thread_local int g_last_engine = 0;     // engine the last run_omp used
 thread_local int g_last_delegated = 0;  // signals handed to the exact engine
+thread_local int g_last_rescans = 0;    // inline exact rescans (tensor engine)
 std::atomic<int64_t> g_launches{0};
 
 cdb_status fail(cdb_status st, const std::string &msg) {
@@ -214,8 +216,10 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
   int64_t chunk = kScratchBudget / per;
   if (chunk < 128) chunk = 128;
   if (chunk > p) chunk = p;
-  DevBuf work;
+  DevBuf work, rescans;
   CDB_CUDA(work.alloc((size_t)cdb::tensor_state_bytes(chunk, d->n, kw) + 65536, st));
+  CDB_CUDA(rescans.alloc(sizeof(int), st));
+  CDB_CUDA(cudaMemsetAsync(rescans.ptr, 0, sizeof(int), st));
   const size_t ysz = f32 ? 4 : 8;
   for (int64_t off = 0; off < p; off += chunk) {
     cdb::TensorArgs a{};
@@ -230,7 +234,9 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
     a.eps = eps + off;
     a.d64 = d->d64;
     a.d16 = d->d16;
+    a.d32 = d->d32;
     a.gram = d->gram;
+    a.rescans = rescans.as<int>();
     a.dmax = d->dmax;
     a.out_sel = (int64_t *)o.sel.dev + off * kw;
     a.out_coef = (double *)o.coef.dev + off * kw;
@@ -243,6 +249,7 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
     a.num_sms = di.sms;
     CDB_CUDA(cdb::run_tensor_chunk(a, st));
   }
+  CDB_CUDA(cudaMemcpyAsync(&g_last_rescans, rescans.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
   return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, d->t, o, status.as<uint32_t>(),
                           di, st);
 }
@@ -255,7 +262,8 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
 // steps, small dictionaries), tensor for large full-dictionary scans.
 cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p, int64_t k_max,
                    int64_t kw, const double *eps, const cdb::Cands &cands, int64_t max_cands,
-                   Outs &o, int engine, const DevInfo &di, cudaStream_t st) {
+                   Outs &o, int engine, const DevInfo &di, cudaStream_t st,
+                   const char *tag = nullptr) {
   if (p <= 0) return CDB_OK;
   const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit;
   if (engine == CDB_ENGINE_AUTO) {
@@ -272,6 +280,8 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
     return fail(CDB_ERR_ARG, "engine needs the dictionary's Gram matrix (raise the budget)");
   if (engine == CDB_ENGINE_TENSOR && cands.mode != 0) engine = CDB_ENGINE_GRAM;
   g_last_engine = engine;
+  g_last_rescans = 0;
+  g_last_delegated = 0;
   if (engine == CDB_ENGINE_EXACT)
     return run_exact(d, ys, f32, p, nullptr, k_max, kw, eps, cands, max_cands, o, di, st);
   if (engine == CDB_ENGINE_TENSOR) return run_tensor(d, ys, f32, p, k_max, kw, eps, cands, o, di, st);
@@ -297,6 +307,7 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   g.out_scans = (int64_t *)o.scans.dev;
   g.out_flag = (uint8_t *)o.flag.dev;
   g.status = status.as<uint32_t>();
+  g.tag = tag;
   int64_t chunk = p;
   DevBuf hwork;
   if (!h_smem) {
@@ -318,19 +329,101 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
 
 }  // namespace
 
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::atomic<bool> g_prof_on{false};
+std::vector<ProfRec> g_prof_open;   // begun, not ended
+std::vector<ProfRec> g_prof_done;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
 namespace cdb {
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void prof_begin(const char *name, cudaStream_t stream) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  ProfRec r{name, prof_event(), prof_event()};
+  cudaEventRecord(r.a, stream);
+  g_prof_open.push_back(r);
+}
+
+void prof_end(const char *name, cudaStream_t stream) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  for (size_t i = g_prof_open.size(); i-- > 0;) {
+    if (g_prof_open[i].name == name) {
+      cudaEventRecord(g_prof_open[i].b, stream);
+      g_prof_done.push_back(g_prof_open[i]);
+      g_prof_open.erase(g_prof_open.begin() + (long)i);
+      return;
+    }
+  }
+}
 }  // namespace cdb
 
 extern "C" {
 
 const char *cdb_last_error(void) { return g_last_error.c_str(); }
 
+void cdb_profile_enable(int on) {
+  g_prof_on.store(on != 0);
+  for (auto &r : g_prof_done) {
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_done.clear();
+}
+
+int cdb_profile_read(int max_entries, char *names, int name_len, double *ms, int64_t *launches) {
+  // aggregate by name (synchronises on the recorded events)
+  std::vector<std::string> keys;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto &r : g_prof_done) {
+    float t = 0.0f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&t, r.a, r.b);
+    size_t k = 0;
+    while (k < keys.size() && keys[k] != r.name) k++;
+    if (k == keys.size()) {
+      keys.push_back(r.name);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[k] += t;
+    cnt[k] += 1;
+  }
+  const int n = (int)keys.size() < max_entries ? (int)keys.size() : max_entries;
+  for (int i = 0; i < n; i++) {
+    if (names) {
+      std::strncpy(names + (size_t)i * name_len, keys[i].c_str(), (size_t)name_len - 1);
+      names[(size_t)i * name_len + name_len - 1] = 0;
+    }
+    if (ms) ms[i] = tot[i];
+    if (launches) launches[i] = cnt[i];
+  }
+  return (int)keys.size();
+}
+
 int64_t cdb_launch_count(void) { return g_launches.load(); }
 
-void cdb_last_run_info(int *engine, int *delegated) {
+void cdb_last_run_info(int *engine, int *delegated, int *rescans) {
   if (engine) *engine = g_last_engine;
   if (delegated) *delegated = g_last_delegated;
+  if (rescans) *rescans = g_last_rescans;
 }
 
 cdb_status cdb_device_info(int *sm_count, int *cc_major, int *cc_minor) {
@@ -371,6 +464,10 @@ cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
   d->bytes += b16;
   if (cdb::launch_to_bf16(d->d64, t, n, d->n_pad, d->d16, st) != cudaSuccess)
     return cleanup(CDB_ERR_CUDA, "bf16 conversion");
+  if (cudaMalloc(&d->d32, 4 * t * n) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "d32 alloc");
+  d->bytes += 4 * t * n;
+  if (cdb::launch_to_f32(d->d64, t * n, d->d32, st) != cudaSuccess)
+    return cleanup(CDB_ERR_CUDA, "f32 conversion");
   {
     double *dm = nullptr;
     if (cudaMallocAsync((void **)&dm, sizeof(double), st) != cudaSuccess)
@@ -397,11 +494,23 @@ cdb_status cdb_dictionary_destroy(cdb_dictionary *d) {
   if (d->d64) cudaFree(d->d64);
   if (d->gram) cudaFree(d->gram);
   if (d->d16) cudaFree(d->d16);
+  if (d->d32) cudaFree(d->d32);
   delete d;
   return CDB_OK;
 }
 
 int64_t cdb_dictionary_bytes(const cdb_dictionary *d) { return d ? d->bytes : 0; }
+
+cdb_status cdb_debug_corr_topk(const cdb_dictionary *d, const float *rows, int64_t p,
+                               int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
+                               void *stream) {
+  if (!d || !rows || p < 1) return fail(CDB_ERR_ARG, "bad debug_corr_topk arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  CDB_CUDA(cdb::debug_corr_topk(d->d16, d->t, d->n, rows, p, cand_idx, cand_val, cand_drop,
+                                grid_cap, st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  return CDB_OK;
+}
 
 static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_is_f32, int64_t p,
                              int64_t k_max, const double *eps, const int64_t *ids, int64_t stride,
@@ -511,7 +620,8 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   cdb::Cands c1{};
   c1.mode = 0;
   c1.t = low->t;
-  cdb_status s = run_omp(low, y1, y1_f32, p, k1, k1, eps1.as<double>(), c1, low->t, lo, engine, di, st);
+  cdb_status s = run_omp(low, y1, y1_f32, p, k1, k1, eps1.as<double>(), c1, low->t, lo, engine, di,
+                         st, "gram_step1");
   if (s != CDB_OK) return s;
   CDB_CUDA(cudaEventRecord(ev[1], st));
 
@@ -530,7 +640,7 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   c2.nb = (const int64_t *)lo.count.dev;
   c2.clip = 1;
   s = run_omp(high, y_in.dev, f32, p, k_high, k_high, eps2.as<double>(), c2, k1 * q, hi, engine, di,
-              st);
+              st, "gram_step2");
   if (s != CDB_OK) return s;
   CDB_CUDA(cudaEventRecord(ev[2], st));
   CDB_CUDA(lo.finish(st));

@@ -9,6 +9,17 @@ namespace cdb {
 
 void note_launch(int n = 1);
 
+// Device-time profiler (cdb_profile_*): CUDA events recorded on the launching
+// stream around each kernel launch, summed per kernel name.
+void prof_begin(const char *name, cudaStream_t stream);
+void prof_end(const char *name, cudaStream_t stream);
+struct ProfScope {
+  const char *name;
+  cudaStream_t stream;
+  ProfScope(const char *n, cudaStream_t s) : name(n), stream(s) { prof_begin(n, s); }
+  ~ProfScope() { prof_end(name, stream); }
+};
+
 // ---------------------------------------------------------------- exact
 struct ExactArgs {
   const double *mat_t;   // T x N fp64
@@ -53,6 +64,7 @@ struct GramArgs {
   uint8_t *out_flag;
   uint32_t *status;      // per-signal status bits (ST_DELEGATE ...)
   double *hwork;         // optional global H storage when it does not fit smem
+  const char *tag;       // profiler name
 };
 // Shared-memory bytes per warp of the Gram engine (H in smem or global).
 int64_t gram_total_smem(int64_t max_cands, int64_t k_width, int64_t n, bool h_in_smem);
@@ -67,8 +79,10 @@ struct TensorArgs {
   const double *eps;
   const double *d64;
   const void *d16;
+  const float *d32;      // T x N fp32 atoms (residual materialisation)
   const double *gram;
   double dmax;           // max atom norm (error bound)
+  int *rescans;          // device counter of inline exact rescans
   int64_t *out_sel;
   double *out_coef;
   int64_t *out_count;
@@ -78,9 +92,13 @@ struct TensorArgs {
   uint32_t *status;
   void *work;            // tensor_state_bytes(p, n, k_width) bytes
   int num_sms;
+  const char *tag;       // profiler name prefix
 };
 int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw);
 cudaError_t run_tensor_chunk(const TensorArgs &args, cudaStream_t stream);
+cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *rows, int64_t p,
+                            int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
+                            cudaStream_t stream);
 
 // ---------------------------------------------------------------- helpers
 cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double *out,
@@ -96,6 +114,7 @@ cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *
                                cudaStream_t stream);
 cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad,
                            void *d16, cudaStream_t stream);
+cudaError_t launch_to_f32(const double *d64, int64_t count, float *d32, cudaStream_t stream);
 cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids,
                                      int *count, cudaStream_t stream);
 

@@ -241,6 +241,7 @@ int64_t exact_work_stride(int64_t n, int64_t k_width, int64_t max_cands) {
 
 cudaError_t launch_exact(const ExactArgs &args, const void *ys, bool ys_f32, int warps,
                          cudaStream_t stream) {
+  ProfScope _ps("exact_omp", stream);
   if (args.p_count <= 0) return cudaSuccess;
   const int wpb = 4;
   const int blocks = (warps + wpb - 1) / wpb;

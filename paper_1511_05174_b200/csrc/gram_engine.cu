@@ -275,6 +275,7 @@ int64_t gram_total_smem(int64_t s, int64_t kw, int64_t n, bool h_in_smem) {
 
 cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
                         int num_sms, cudaStream_t stream) {
+  ProfScope _ps(args.tag ? args.tag : "gram_omp", stream);
   (void)num_sms;
   if (args.p <= 0) return cudaSuccess;
   const int64_t s = args.max_cands, kw = args.k_width, n = args.n;

@@ -128,6 +128,11 @@ __global__ void to_bf16_kernel(const double *__restrict__ d, int64_t t, int64_t 
   out[gid] = __float2bfloat16_rn(col < n ? (float)d[row * n + col] : 0.0f);
 }
 
+__global__ void to_f32_kernel(const double *__restrict__ d, int64_t count, float *__restrict__ out) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid < count) out[gid] = (float)d[gid];
+}
+
 __global__ void collect_delegates_kernel(const uint32_t *__restrict__ status, int64_t p,
                                          int64_t *__restrict__ ids, int *__restrict__ count) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -155,6 +160,7 @@ inline unsigned blocks_for(int64_t work, int threads) {
 cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
                               const int64_t *fine_shape, const int64_t *factors, int rank,
                               double *y_low, int64_t n_low, cudaStream_t stream) {
+  ProfScope _ps("downsample", stream);
   if (p <= 0) return cudaSuccess;
   if (rank < 1 || rank > 4) return cudaErrorInvalidValue;
   Shape4 sh{};
@@ -175,6 +181,7 @@ cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
 
 cudaError_t launch_row_tol(const void *ys, bool ys_f32, int64_t p, int64_t n, double rel,
                            double *eps, cudaStream_t stream) {
+  ProfScope _ps("row_tol", stream);
   if (p <= 0) return cudaSuccess;
   const unsigned g = blocks_for(p * 32, 256);
   if (ys_f32)
@@ -187,6 +194,7 @@ cudaError_t launch_row_tol(const void *ys, bool ys_f32, int64_t p, int64_t n, do
 
 cudaError_t launch_sort_blocks(const int64_t *low_sel, const int64_t *low_count, int64_t p,
                                int64_t k1, int64_t *blocks, cudaStream_t stream) {
+  ProfScope _ps("sort_blocks", stream);
   if (p <= 0) return cudaSuccess;
   sort_blocks_kernel<<<blocks_for(p, 128), 128, 0, stream>>>(low_sel, low_count, p, k1, blocks);
   note_launch();
@@ -195,6 +203,7 @@ cudaError_t launch_sort_blocks(const int64_t *low_sel, const int64_t *low_count,
 
 cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *gram,
                                cudaStream_t stream) {
+  ProfScope _ps("gram_matrix", stream);
   dim3 grid((unsigned)((t + 63) / 64), (unsigned)((t + 63) / 64));
   gram_matrix_kernel<<<grid, 256, 0, stream>>>(d64, t, n, gram);
   note_launch();
@@ -203,14 +212,23 @@ cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *
 
 cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad, void *d16,
                            cudaStream_t stream) {
+  ProfScope _ps("to_bf16", stream);
   to_bf16_kernel<<<blocks_for(t * n_pad, 256), 256, 0, stream>>>(d64, t, n, n_pad,
                                                                   (__nv_bfloat16 *)d16);
   note_launch();
   return cudaGetLastError();
 }
 
+cudaError_t launch_to_f32(const double *d64, int64_t count, float *d32, cudaStream_t stream) {
+  ProfScope _ps("to_f32", stream);
+  to_f32_kernel<<<blocks_for(count, 256), 256, 0, stream>>>(d64, count, d32);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids, int *count,
                                      cudaStream_t stream) {
+  ProfScope _ps("collect_delegates", stream);
   if (p <= 0) return cudaSuccess;
   collect_delegates_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(status, p, ids, count);
   note_launch();
@@ -219,6 +237,7 @@ cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t 
 
 cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double *out,
                                 cudaStream_t stream) {
+  ProfScope _ps("row_norm_max", stream);
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), stream);
   if (e != cudaSuccess) return e;
   row_norm_max_kernel<<<blocks_for(t * 32, 256), 256, 0, stream>>>(d64, t, n,

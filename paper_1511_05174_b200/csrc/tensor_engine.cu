@@ -25,6 +25,10 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "engines.h"
 #include "sm100.cuh"
@@ -32,28 +36,29 @@
 namespace cdb {
 namespace {
 
-constexpr int BM = 128;          // signals per tile (MMA M)
-constexpr int BN = 256;          // atoms per tile (MMA N)
+constexpr int BMH = 128;         // rows per M half (one MMA, M = 128)
+constexpr int BM = 2 * BMH;      // signals per CTA tile (two halves share each B stage)
+constexpr int BN = 128;          // atoms per tile (MMA N)
 constexpr int BK = 64;           // bf16 elements per 128-byte swizzled row chunk
-constexpr int STAGES = 4;
 constexpr int NCAND = 8;         // approximate candidates kept per signal
-constexpr int EPI_WARPS = 8;     // 2 per TMEM lane quarter (column halves)
+constexpr int EPI_WARPS = 8;     // 4 TMEM lane quarters x 2 M halves: one row per thread
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr uint32_t A_BYTES = BM * BK * 2;
-constexpr uint32_t B_BYTES = BN * BK * 2;
-constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr uint32_t TMEM_COLS = 2 * BN;
+constexpr uint32_t AH_BYTES = BMH * BK * 2;   // one M half, one K chunk (16 KB)
+constexpr uint32_t B_BYTES = BN * BK * 2;     // one atom tile, one K chunk (16 KB)
+constexpr uint32_t TMEM_COLS = 4 * BN;        // 2 buffers x 2 halves
+constexpr int RES_KCHUNKS = 4;                // A resident when n_pad <= 256
+constexpr int RES_BSTAGES = 4;
+constexpr int STR_STAGES = 4;
 
-struct __align__(16) EpiList {
-  float val[NCAND];
-  int idx[NCAND];
-  float dropped;
+struct CorrSmemRes {                                   // A resident in smem
+  uint8_t a[RES_KCHUNKS][2][AH_BYTES];
+  uint8_t b[RES_BSTAGES][B_BYTES];
+  uint64_t full[RES_BSTAGES], empty[RES_BSTAGES], tfull[2], tempty[2], afull, aempty;
+  uint32_t tmem_base;
 };
-
-struct CorrSmem {
-  uint8_t stage[STAGES][STAGE_BYTES];  // 1024-aligned (base is)
-  EpiList part[BM];                    // half-1 partial lists for the merge
-  uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+struct CorrSmemStr {                                   // A streamed with B
+  uint8_t st[STR_STAGES][2 * AH_BYTES + B_BYTES];
+  uint64_t full[STR_STAGES], empty[STR_STAGES], tfull[2], tempty[2], afull, aempty;
   uint32_t tmem_base;
 };
 
@@ -78,6 +83,7 @@ __device__ __forceinline__ void list_insert(float (&val)[NCAND], int (&idx)[NCAN
   }
 }
 
+template <bool A_RES>
 __global__ void __launch_bounds__(THREADS, 1)
     corr_topk_kernel(const __grid_constant__ CUtensorMap tm_a,
                      const __grid_constant__ CUtensorMap tm_b, int64_t p, int64_t t,
@@ -85,16 +91,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                      int *__restrict__ cand_idx, float *__restrict__ cand_val,
                      float *__restrict__ cand_drop) {
   if (active && *active == 0) return;  // every signal already finished
+  using Smem = typename std::conditional<A_RES, CorrSmemRes, CorrSmemStr>::type;
+  constexpr int NST = A_RES ? RES_BSTAGES : STR_STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  CorrSmem &sm = *reinterpret_cast<CorrSmem *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Smem &sm = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                       ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t_tiles = (int)((t + BN - 1) / BN);
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tm_a);
     sm100::tma_prefetch(&tm_b);
-    for (int s = 0; s < STAGES; s++) {
+    for (int s = 0; s < NST; s++) {
       sm100::mbar_init(&sm.full[s], 1);
       sm100::mbar_init(&sm.empty[s], 1);
     }
@@ -102,6 +110,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       sm100::mbar_init(&sm.tfull[a], 1);
       sm100::mbar_init(&sm.tempty[a], EPI_WARPS * 32);
     }
+    sm100::mbar_init(&sm.afull, 1);
+    sm100::mbar_init(&sm.aempty, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 1) sm100::tmem_alloc(&sm.tmem_base, TMEM_COLS);
@@ -113,15 +123,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t s = 0, ph = 0;
+      uint32_t s = 0, ph = 0, aph = 0;
       for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+        const int row0 = (int)(mt * BM);
+        if constexpr (A_RES) {
+          sm100::mbar_wait(&sm.aempty, aph ^ 1);
+          sm100::mbar_expect_tx(&sm.afull, (uint32_t)n_kchunks * 2 * AH_BYTES);
+          for (int kc = 0; kc < n_kchunks; kc++)
+            for (int h = 0; h < 2; h++)
+              sm100::tma_load_2d(sm.a[kc][h], &tm_a, &sm.afull, kc * BK, row0 + h * BMH);
+          aph ^= 1;
+        }
         for (int tt = 0; tt < t_tiles; tt++) {
           for (int kc = 0; kc < n_kchunks; kc++) {
             sm100::mbar_wait(&sm.empty[s], ph ^ 1);
-            sm100::mbar_expect_tx(&sm.full[s], STAGE_BYTES);
-            sm100::tma_load_2d(sm.stage[s], &tm_a, &sm.full[s], kc * BK, (int)(mt * BM));
-            sm100::tma_load_2d(sm.stage[s] + A_BYTES, &tm_b, &sm.full[s], kc * BK, tt * BN);
-            if (++s == STAGES) {
+            if constexpr (A_RES) {
+              sm100::mbar_expect_tx(&sm.full[s], B_BYTES);
+              sm100::tma_load_2d(sm.b[s], &tm_b, &sm.full[s], kc * BK, tt * BN);
+            } else {
+              sm100::mbar_expect_tx(&sm.full[s], 2 * AH_BYTES + B_BYTES);
+              sm100::tma_load_2d(sm.st[s], &tm_a, &sm.full[s], kc * BK, row0);
+              sm100::tma_load_2d(sm.st[s] + AH_BYTES, &tm_a, &sm.full[s], kc * BK, row0 + BMH);
+              sm100::tma_load_2d(sm.st[s] + 2 * AH_BYTES, &tm_b, &sm.full[s], kc * BK, tt * BN);
+            }
+            if (++s == NST) {
               s = 0;
               ph ^= 1;
             }
@@ -132,26 +157,41 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
-      constexpr uint32_t idesc = sm100::idesc_bf16_f32(BM, BN);
-      uint32_t s = 0, ph = 0, acc = 0, acc_ph = 0;
+      constexpr uint32_t idesc = sm100::idesc_bf16_f32(BMH, BN);
+      uint32_t s = 0, ph = 0, acc = 0, acc_ph = 0, aph = 0;
       for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+        if constexpr (A_RES) {
+          sm100::mbar_wait(&sm.afull, aph);
+          aph ^= 1;
+          sm100::tc_fence_after();
+        }
         for (int tt = 0; tt < t_tiles; tt++) {
           sm100::mbar_wait(&sm.tempty[acc], acc_ph ^ 1);
           sm100::tc_fence_after();
-          const uint32_t d_tmem = tmem + acc * BN;
           for (int kc = 0; kc < n_kchunks; kc++) {
             sm100::mbar_wait(&sm.full[s], ph);
             sm100::tc_fence_after();
-            const uint32_t a_addr = sm100::smem_u32(sm.stage[s]);
-            const uint32_t b_addr = a_addr + A_BYTES;
+            uint32_t a0, a1, b;
+            if constexpr (A_RES) {
+              a0 = sm100::smem_u32(sm.a[kc][0]);
+              a1 = sm100::smem_u32(sm.a[kc][1]);
+              b = sm100::smem_u32(sm.b[s]);
+            } else {
+              a0 = sm100::smem_u32(sm.st[s]);
+              a1 = a0 + AH_BYTES;
+              b = a0 + 2 * AH_BYTES;
+            }
 #pragma unroll
             for (int k = 0; k < BK / 16; k++) {
-              sm100::mma_bf16(d_tmem, sm100::desc_kmajor_sw128(a_addr + k * 32),
-                              sm100::desc_kmajor_sw128(b_addr + k * 32), idesc,
-                              (kc | k) != 0 ? 1u : 0u);
+              const uint64_t bd = sm100::desc_kmajor_sw128(b + k * 32);
+              const uint32_t accum = (kc | k) != 0 ? 1u : 0u;
+              sm100::mma_bf16(tmem + (acc * 2 + 0) * BN, sm100::desc_kmajor_sw128(a0 + k * 32), bd,
+                              idesc, accum);
+              sm100::mma_bf16(tmem + (acc * 2 + 1) * BN, sm100::desc_kmajor_sw128(a1 + k * 32), bd,
+                              idesc, accum);
             }
             sm100::mma_commit(&sm.empty[s]);
-            if (++s == STAGES) {
+            if (++s == NST) {
               s = 0;
               ph ^= 1;
             }
@@ -162,14 +202,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             acc_ph ^= 1;
           }
         }
+        if constexpr (A_RES) sm100::mma_commit(&sm.aempty);
       }
     }
   } else {
     // ------------------------------------------------ epilogue: top-k |c| per row
-    const int ew = warp - 2;            // 0..7
-    const int quarter = warp & 3;       // TMEM lane quarter this warp may access
-    const int half = ew >> 2;           // column half of each 256-atom tile
-    const int row = quarter * 32 + lane;
+    const int ew = warp - 2;       // 0..7
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = ew >> 2;      // M half
+    const int row = half * BMH + quarter * 32 + lane;
     uint32_t acc = 0, acc_ph = 0;
     for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
       float val[NCAND];
@@ -183,17 +224,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int tt = 0; tt < t_tiles; tt++) {
         sm100::mbar_wait(&sm.tfull[acc], acc_ph);
         sm100::tc_fence_after();
-        const int col0 = tt * BN + half * (BN / 2);
+        const uint32_t tbase = tmem + (acc * 2 + half) * BN + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
+        for (int c = 0; c < BN; c += 32) {
           float v[32];
-          sm100::tmem_ld32(tmem + acc * BN + half * (BN / 2) + c + ((uint32_t)(quarter * 32) << 16),
-                           v);
+          sm100::tmem_ld32(tbase + c, v);
+          // branchless chunk top-2 on packed keys: |v| with its low 8 mantissa
+          // bits replaced by the tile-local column (truncation <= 2^-15 rel.)
+          uint32_t c1 = 0u, c2 = 0u, rest = 0u;
+          const int jbase = tt * BN + c;
 #pragma unroll
           for (int i = 0; i < 32; i++) {
-            const int j = col0 + c + i;
-            if (j < t) list_insert(val, idx, dropped, fabsf(v[i]), j);
+            uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFF00u) | (uint32_t)(c + i);
+            key = (jbase + i < t) ? key : 0u;
+            const uint32_t m = min(c1, key);
+            c1 = max(c1, key);
+            rest = max(rest, min(c2, m));
+            c2 = max(c2, m);
           }
+          dropped = fmaxf(dropped, __uint_as_float(rest & 0xFFFFFF00u));
+          if (c1) list_insert(val, idx, dropped, __uint_as_float(c1 & 0xFFFFFF00u),
+                              tt * BN + (int)(c1 & 0xFFu));
+          if (c2) list_insert(val, idx, dropped, __uint_as_float(c2 & 0xFFFFFF00u),
+                              tt * BN + (int)(c2 & 0xFFu));
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.tempty[acc]);
@@ -202,34 +255,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           acc_ph ^= 1;
         }
       }
-      // merge the two column halves of each row, write the row's list
-      if (half == 1) {
+      const int64_t grow = mt * BM + row;
+      if (grow < p) {
 #pragma unroll
         for (int i = 0; i < NCAND; i++) {
-          sm.part[row].val[i] = val[i];
-          sm.part[row].idx[i] = idx[i];
+          cand_idx[grow * NCAND + i] = idx[i];
+          cand_val[grow * NCAND + i] = val[i];
         }
-        sm.part[row].dropped = dropped;
+        cand_drop[grow] = dropped;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
-      if (half == 0) {
-#pragma unroll
-        for (int i = 0; i < NCAND; i++) {
-          const int oi = sm.part[row].idx[i];
-          if (oi >= 0) list_insert(val, idx, dropped, sm.part[row].val[i], oi);
-        }
-        dropped = fmaxf(dropped, sm.part[row].dropped);
-        const int64_t grow = mt * BM + row;
-        if (grow < p) {
-#pragma unroll
-          for (int i = 0; i < NCAND; i++) {
-            cand_idx[grow * NCAND + i] = idx[i];
-            cand_val[grow * NCAND + i] = val[i];
-          }
-          cand_drop[grow] = dropped;
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
     }
   }
   sm100::tc_fence_before();
@@ -240,19 +274,35 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+__global__ void to_bf16_rows(const float *__restrict__ rows, int64_t p, int64_t n, int64_t n_pad,
+                             __nv_bfloat16 *__restrict__ out) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= p * n_pad) return;
+  const int64_t r = gid / n_pad, c = gid % n_pad;
+  out[gid] = __float2bfloat16_rn(c < n ? rows[r * n + c] : 0.0f);
+}
+
 // ---------------------------------------------------------------- LS side
 struct TensorState {
-  double *r64;          // P x n    residual (fp64, exact)
-  __nv_bfloat16 *r16;   // Ppad x n_pad   GEMM operand
+  __nv_bfloat16 *r16;   // Ppad x n_pad   GEMM operand  bf16(r~), r~ = y - D32_S x
   double *linv;         // P x kw x kw    L^{-1} row-major
-  double *z;            // P x kw
-  double *rnorm;        // P   ||r||
+  double *z;            // P x kw         q_i^T y
+  double *rn2;          // P   |y|^2 - |z|^2   (= |r|^2 up to rounding)
+  double *yy;           // P   |y|^2
+  double *rt;           // P   |r~|  (operand of the bf16 scan)
+  double *dr;           // P   bound on |r~ - r|
   double *tol;          // P
   uint32_t *status;     // P   ST_DONE | ST_DELEGATE
   const int *cand_idx;
   const float *cand_val;
   const float *cand_drop;
   int *active;          // per iteration: signals still running after it
+  int *rescans;         // count of exact rescans (uncertifiable picks)
+  int *npending;        // per iteration: queued rescans
+  int64_t *pending;     // queued signal ids
+  int64_t *rs_j;        // rescan result: atom
+  double *rs_c;         // rescan result: exact correlation
+  int64_t debug_sig;    // CDB_LS_DEBUG: printf trace of one signal
 };
 
 template <typename YT>
@@ -266,17 +316,31 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
   const int64_t sig = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (sig >= p) return;
-  double *r = st.r64 + sig * n;
-  double ss = 0.0;
+  const YT *y = ys + sig * n;
+  double yy = 0.0;
   for (int64_t i = lane; i < n; i += 32) {
-    const double v = (double)ys[sig * n + i];
-    r[i] = v;
+    const double v = (double)y[i];
     st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)v);
-    ss = fma(v, v, ss);
+    yy = fma(v, v, yy);
   }
-  __syncwarp();
-  const double ynorm = sqrt(dot4_quad(r, r, n, lane));  // reference order (_kernels.py:71)
-  (void)ss;
+  yy = warp_sum(yy);
+  // |y| in the reference's _dot4 order (_kernels.py:27-47,71): lanes 0-3
+  // run the four accumulator chains, the tail is added last
+  const int64_t m4 = (n / 4) * 4;
+  double part = 0.0;
+  if (lane < 4)
+    for (int64_t i = lane; i < m4; i += 4) {
+      const double v = (double)y[i];
+      part = __dadd_rn(part, __dmul_rn(v, v));
+    }
+  const double s0 = __shfl_sync(CDB_FULL_MASK, part, 0), s1 = __shfl_sync(CDB_FULL_MASK, part, 1);
+  const double s2 = __shfl_sync(CDB_FULL_MASK, part, 2), s3 = __shfl_sync(CDB_FULL_MASK, part, 3);
+  double tot = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3);
+  for (int64_t i = m4; i < n; i++) {
+    const double v = (double)y[i];
+    tot = __dadd_rn(tot, __dmul_rn(v, v));
+  }
+  const double ynorm = sqrt(tot);
   for (int64_t j = lane; j < kw; j += 32) {
     out_sel[sig * kw + j] = -1;
     out_coef[sig * kw + j] = 0.0;
@@ -284,7 +348,10 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
   if (lane == 0) {
     const double tol = eps[sig];
     st.tol[sig] = tol;
-    st.rnorm[sig] = ynorm;
+    st.yy[sig] = yy;
+    st.rn2[sig] = yy;
+    st.rt[sig] = sqrt(yy);
+    st.dr[sig] = 0.0;
     st.status[sig] = ynorm <= tol ? ST_DONE : 0u;
     out_count[sig] = 0;
     out_rnorm[sig] = ynorm;
@@ -293,82 +360,34 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
   }
 }
 
-// One OMP iteration of one signal per warp (see file comment, step 2).
-template <typename YT>
-__global__ void __launch_bounds__(256) ls_step_kernel(
-    const YT *__restrict__ ys, const double *__restrict__ d64, const double *__restrict__ gram,
-    int64_t p, int64_t t, int64_t n, int64_t n_pad, int64_t k_max, int64_t kw, int iter,
-    double c_err, double dmax, TensorState st, int64_t *out_sel, double *out_coef,
-    int64_t *out_count, double *out_rnorm, int64_t *out_scans) {
-  extern __shared__ double lsm[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t sig = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (sig >= p) return;
-  if (st.status[sig] & (ST_DONE | ST_DELEGATE)) return;
-  double *lin = lsm + wib * (kw * kw + 4 * kw);  // L^{-1} rows 0..k-1 (row-major)
-  double *wv = lin + kw * kw;                      // w
-  double *xv = wv + kw;                            // x
-  double *gv = xv + kw;                            // G[new, S]
-  double *zv = gv + kw;                            // z
-  const int64_t k = iter;                          // atoms selected so far
-  int64_t *sel = out_sel + sig * kw;
-  const double *r = st.r64 + sig * n;
+// exact c_j = <d_j, y> - sum_s G[j, s] x_s  (fp64; the whole warp)
+__device__ __forceinline__ double exact_corr(const double *__restrict__ d64,
+                                             const double *__restrict__ gram, int64_t t, int64_t n,
+                                             int64_t j, const double *y, const int64_t *sel,
+                                             const double *x, int64_t k, int lane) {
+  const double *dj = d64 + j * n;
+  double acc = 0.0;
+  for (int64_t i = lane; i < n; i += 32) acc = fma(__ldg(dj + i), y[i], acc);
+  const double *gj = gram + j * t;
+  for (int64_t s = lane; s < k; s += 32) acc = fma(-__ldg(gj + sel[s]), x[s], acc);
+  return warp_sum(acc);
+}
 
-  // ---- candidates: drop taken atoms, rigorous error bound of the bf16 scan
-  int cidx = -1;
-  float cval = -1.0f;
-  if (lane < NCAND) {
-    cidx = st.cand_idx[sig * NCAND + lane];
-    cval = st.cand_val[sig * NCAND + lane];
-    for (int64_t i = 0; i < k && cidx >= 0; i++)
-      if (sel[i] == cidx) cidx = -1;
-    if (cidx < 0) cval = -1.0f;
-  }
-  const double E = c_err * st.rnorm[sig] * dmax;
-  double best_apx = (double)cval;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) best_apx = fmax(best_apx, __shfl_xor_sync(CDB_FULL_MASK, best_apx, o));
-  // every candidate whose approximate value is within 2E of the best is re-scored
-  const bool rescore = cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
-  const unsigned rmask = __ballot_sync(CDB_FULL_MASK, rescore);
-  double unscored = rescore || cidx < 0 ? -1.0 : (double)cval;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) unscored = fmax(unscored, __shfl_xor_sync(CDB_FULL_MASK, unscored, o));
-  unscored = fmax(unscored, (double)st.cand_drop[sig]);
+constexpr uint32_t ST_RESCAN = 4u;  // pick needs the exact full rescan
 
-  // exact fp64 correlations of the re-scored candidates (warp dot each)
-  double best = -1.0;
-  int64_t bestj = -1;
-  for (unsigned m = rmask; m; m &= m - 1) {
-    const int c = __ffs(m) - 1;
-    const int64_t j = __shfl_sync(CDB_FULL_MASK, cidx, c);
-    const double *dj = d64 + j * n;
-    double acc = 0.0;
-    for (int64_t i = lane; i < n; i += 32) acc = fma(__ldg(dj + i), r[i], acc);
-    const double v = fabs(warp_sum(acc));
-    if (v > best || (v == best && j < bestj)) {
-      best = v;
-      bestj = j;
-    }
-  }
-  const int64_t scans_it = t - k;  // scans += c - k (_kernels.py:91)
-  if (bestj < 0 || !(unscored + E < best)) {
-    // uncertifiable (or no candidate): the exact engine redoes this signal
-    if (lane == 0) st.status[sig] |= ST_DELEGATE;
-    return;
-  }
-  if (lane == 0) out_scans[sig] += scans_it;
-  if (best <= 0.0) {  // residual orthogonal to every atom (_kernels.py:104)
-    if (lane == 0) st.status[sig] |= ST_DONE;
-    return;
-  }
-  // ---- Cholesky append through the Gram row of the new atom
+// Append atom `bestj` (exact correlation cbest) to the signal's support:
+// Cholesky update through the Gram row, coefficients, stop test, and the
+// bf16 operand of the next scan.  Whole warp; smem per warp as in ls_step.
+__device__ void ls_update(const double *__restrict__ d64, const float *__restrict__ d32,
+                          const double *__restrict__ gram, int64_t sig, int64_t t, int64_t n,
+                          int64_t n_pad, int64_t k_max, int64_t kw, int iter, double dmax,
+                          TensorState &st, int64_t *sel, double *out_coef, int64_t *out_count,
+                          int64_t bestj, double cbest, double *lin, double *wv, double *xv,
+                          double *gv, double *zv, const double *y, int lane) {
+  const int64_t k = iter;
   const double *grow = gram + bestj * t;
   for (int64_t i = lane; i < k * kw; i += 32) lin[i] = st.linv[sig * kw * kw + i];
-  for (int64_t i = lane; i < k; i += 32) {
-    gv[i] = __ldg(grow + sel[i]);
-    zv[i] = st.z[sig * kw + i];
-  }
+  for (int64_t i = lane; i < k; i += 32) gv[i] = __ldg(grow + sel[i]);
   const double gnn = __ldg(grow + bestj);
   __syncwarp();
   for (int64_t l = lane; l < k; l += 32) {
@@ -381,19 +400,13 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
   for (int64_t l = lane; l < k; l += 32) ww = fma(wv[l], wv[l], ww);
   ww = warp_sum(ww);
   const double d2 = gnn - ww;
-  if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {
+  if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
     if (lane == 0) st.status[sig] |= ST_DELEGATE;
     return;
   }
   const double inv_d = 1.0 / sqrt(d2);
-  // c_new = <d_new, r> = q_k^T r * d and q_k^T y = q_k^T r  =>  z_k = c_new / d
-  double cnew = 0.0;
-  {
-    const double *dj = d64 + bestj * n;
-    for (int64_t i = lane; i < n; i += 32) cnew = fma(__ldg(dj + i), r[i], cnew);
-    cnew = warp_sum(cnew);
-  }
-  const double zk = cnew * inv_d;
+  // <d_new, r> = d q_k^T r and q_k^T y = q_k^T r  =>  z_k = c_new / d
+  const double zk = cbest * inv_d;
   for (int64_t i = lane; i <= k; i += 32) {
     double v;
     if (i == k) {
@@ -412,7 +425,6 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
     sel[k] = bestj;
   }
   __syncwarp();
-  // ---- coefficients x = L^{-T} z (pick order)
   const int64_t kd = k + 1;
   for (int64_t i = lane; i < kd; i += 32) {
     double acc = 0.0;
@@ -421,27 +433,254 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
     out_coef[sig * kw + i] = acc;
   }
   __syncwarp();
-  // ---- residual r = y - D_S x in fp64, its norm, its bf16 copy
-  double *rw = st.r64 + sig * n;
+  // ---- stop test on |r|^2 = |y|^2 - |z|^2, exact residual inside the band
+  const double rn2 = st.rn2[sig] - zk * zk;
+  const double tol = st.tol[sig];
+  const double gap = rn2 - tol * tol;
+  bool stop;
+  if (fabs(gap) > 1e-12 * st.yy[sig]) {
+    stop = gap < 0.0;
+  } else {
+    double rr = 0.0;
+    for (int64_t i = lane; i < n; i += 32) {
+      double ri = y[i];
+      for (int64_t l = 0; l < kd; l++) ri = fma(-xv[l], __ldg(d64 + sel[l] * n + i), ri);
+      rr = fma(ri, ri, rr);
+    }
+    stop = sqrt(warp_sum(rr)) <= tol;
+  }
+  if (lane == 0) {
+    st.rn2[sig] = rn2;
+    out_count[sig] = kd;
+  }
+  if (stop || kd >= k_max) {
+    if (lane == 0) st.status[sig] |= ST_DONE;
+    return;
+  }
+  // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16.
+  // 8 elements per lane per pass: each support atom row is read coalesced.
+  double rr = 0.0, sx = 0.0;
+  for (int64_t i0 = 0; i0 < n; i0 += 256) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int64_t i = i0 + u * 32 + lane;
+      acc[u] = i < n ? y[i] : 0.0;
+    }
+    for (int64_t l = 0; l < kd; l++) {
+      const float *row = d32 + sel[l] * n;
+      const double xl = xv[l];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int64_t i = i0 + u * 32 + lane;
+        if (i < n) acc[u] = fma(-xl, (double)__ldg(row + i), acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int64_t i = i0 + u * 32 + lane;
+      if (i < n) {
+        st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)acc[u]);
+        rr = fma(acc[u], acc[u], rr);
+      }
+    }
+  }
+  for (int64_t l = lane; l < kd; l += 32) sx += fabs(xv[l]);
+  rr = warp_sum(rr);
+  sx = warp_sum(sx);
+  if (lane == 0) {
+    st.rt[sig] = sqrt(rr);
+    st.dr[sig] = 0x1p-24 * sx * dmax * 1.0000001;  // |(D64 - D32) x| bound
+    atomicAdd(st.active + iter, 1);
+  }
+}
+
+// One OMP iteration of one signal per warp (see file comment, step 2).
+// resume == 0: certify the scan's candidates; resume == 1: take the pick
+// the exact rescan produced for the signals listed in st.pending.
+template <typename YT>
+__global__ void __launch_bounds__(256) ls_step_kernel(
+    const YT *__restrict__ ys, const double *__restrict__ d64, const float *__restrict__ d32,
+    const double *__restrict__ gram, int64_t p, int64_t t, int64_t n, int64_t n_pad,
+    int64_t k_max, int64_t kw, int iter, double c_err, double dmax, TensorState st,
+    int64_t *out_sel, double *out_coef, int64_t *out_count, int64_t *out_scans, int resume) {
+  extern __shared__ double lsm[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per_warp = kw * kw + 4 * kw + n;
+  double *lin = lsm + wib * per_warp;  // L^{-1} rows (row-major)
+  double *wv = lin + kw * kw;          // w
+  double *xv = wv + kw;                // x (current coefficients)
+  double *gv = xv + kw;                // G[new, S]
+  double *zv = gv + kw;                // z
+  double *y = zv + kw;                 // the signal (fp64)
+  const int64_t k = iter;              // atoms selected so far
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t count = resume ? (int64_t)st.npending[iter] : p;
+
+  for (int64_t e = wid; e < count; e += nw) {
+    const int64_t sig = resume ? st.pending[e] : e;
+    if (!resume && (st.status[sig] & (ST_DONE | ST_DELEGATE))) continue;
+    int64_t *sel = out_sel + sig * kw;
+    for (int64_t i = lane; i < n; i += 32) y[i] = (double)ys[sig * n + i];
+    for (int64_t i = lane; i < k; i += 32) {
+      xv[i] = out_coef[sig * kw + i];
+      zv[i] = st.z[sig * kw + i];
+    }
+    __syncwarp();
+    double best = -1.0, cbest = 0.0;
+    int64_t bestj = -1;
+    if (resume) {
+      bestj = st.rs_j[sig];
+      cbest = st.rs_c[sig];
+      best = fabs(cbest);
+      if (lane == 0) st.status[sig] &= ~ST_RESCAN;
+    } else {
+      // ---- candidates: drop taken atoms; rigorous bound E of the bf16 scan
+      int cidx = -1;
+      float cval = -1.0f;
+      if (lane < NCAND) {
+        cidx = st.cand_idx[sig * NCAND + lane];
+        cval = st.cand_val[sig * NCAND + lane];
+        for (int64_t i = 0; i < k && cidx >= 0; i++)
+          if (sel[i] == cidx) cidx = -1;
+        if (cidx < 0) cval = -1.0f;
+      }
+      const double E = (c_err * st.rt[sig] + st.dr[sig]) * dmax;
+      double best_apx = (double)cval;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        best_apx = fmax(best_apx, __shfl_xor_sync(CDB_FULL_MASK, best_apx, o));
+      const bool rescore = cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
+      const unsigned rmask = __ballot_sync(CDB_FULL_MASK, rescore);
+      double unscored = rescore || cidx < 0 ? -1.0 : (double)cval;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        unscored = fmax(unscored, __shfl_xor_sync(CDB_FULL_MASK, unscored, o));
+      unscored = fmax(unscored, (double)st.cand_drop[sig]);
+      for (unsigned m = rmask; m; m &= m - 1) {
+        const int c = __ffs(m) - 1;
+        const int64_t j = __shfl_sync(CDB_FULL_MASK, cidx, c);
+        const double cj = exact_corr(d64, gram, t, n, j, y, sel, xv, k, lane);
+        const double v = fabs(cj);
+        if (v > best || (v == best && j < bestj)) {
+          best = v;
+          bestj = j;
+          cbest = cj;
+        }
+      }
+      if (sig == st.debug_sig && lane == 0)
+        printf("[ls dbg] sig %lld k %lld E %.6g rt %.6g dr %.6g best_apx %.6g unscored %.6g "
+               "best %.6g bestj %lld cbest %.6g rmask %x drop %.6g\n",
+               (long long)sig, (long long)k, E, st.rt[sig], st.dr[sig], best_apx, unscored, best,
+               (long long)bestj, cbest, rmask, (double)st.cand_drop[sig]);
+      if (bestj < 0 || !(unscored + E < best)) {
+        // uncertifiable: queue for the CTA-wide exact rescan, resume later
+        if (lane == 0) {
+          st.status[sig] |= ST_RESCAN;
+          st.pending[atomicAdd(st.npending + iter, 1)] = sig;
+          atomicAdd(st.rescans, 1);
+        }
+        __syncwarp();
+        continue;
+      }
+    }
+    if (lane == 0) out_scans[sig] += t - k;  // scans += c - k (_kernels.py:91)
+    if (bestj < 0 || best <= 0.0) {          // orthogonal break (_kernels.py:104)
+      if (lane == 0) st.status[sig] |= ST_DONE;
+      __syncwarp();
+      continue;
+    }
+    ls_update(d64, d32, gram, sig, t, n, n_pad, k_max, kw, iter, dmax, st, sel, out_coef,
+              out_count, bestj, cbest, lin, wv, xv, gv, zv, y, lane);
+    __syncwarp();
+  }
+}
+
+// Exact fp64 argmax over every non-taken atom for the queued signals: one
+// CTA per signal, 8 warps split the atoms, coalesced row reads.
+template <typename YT>
+__global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
+                                                     const double *__restrict__ d64,
+                                                     const double *__restrict__ gram, int64_t t,
+                                                     int64_t n, int64_t kw, int iter,
+                                                     TensorState st, const int64_t *out_sel,
+                                                     const double *out_coef) {
+  __shared__ double sv[8];
+  __shared__ int64_t sj[8];
+  __shared__ double sc[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t count = st.npending[iter];
+  for (int64_t e = blockIdx.x; e < count; e += gridDim.x) {
+    const int64_t sig = st.pending[e];
+    const int64_t k = iter;
+    const int64_t *sel = out_sel + sig * kw;
+    const double *x = out_coef + sig * kw;
+    const YT *y = ys + sig * n;
+    double best = -1.0, cbest = 0.0;
+    int64_t bestj = -1;
+    for (int64_t j = warp; j < t; j += 8) {
+      bool live = true;
+      for (int64_t i = 0; i < k; i++)
+        if (sel[i] == j) live = false;
+      if (!live) continue;
+      const double *dj = d64 + j * n;
+      double acc = 0.0;
+      for (int64_t i = lane; i < n; i += 32) acc = fma(__ldg(dj + i), (double)y[i], acc);
+      const double *gj = gram + j * t;
+      for (int64_t s = lane; s < k; s += 32) acc = fma(-__ldg(gj + sel[s]), x[s], acc);
+      const double cj = warp_sum(acc);
+      const double v = fabs(cj);
+      if (v > best || (v == best && j < bestj)) {
+        best = v;
+        bestj = j;
+        cbest = cj;
+      }
+    }
+    if (lane == 0) {
+      sv[warp] = best;
+      sj[warp] = bestj;
+      sc[warp] = cbest;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; w++)
+        if (sj[w] >= 0 && (bestj < 0 || sv[w] > best || (sv[w] == best && sj[w] < bestj))) {
+          best = sv[w];
+          bestj = sj[w];
+          cbest = sc[w];
+        }
+      st.rs_j[sig] = bestj;
+      st.rs_c[sig] = cbest;
+    }
+    __syncthreads();
+  }
+}
+
+// Final exact residual norms |y - D64_S x| (the reported rnorm).
+template <typename YT>
+__global__ void __launch_bounds__(256) ls_final_kernel(const YT *__restrict__ ys,
+                                                       const double *__restrict__ d64, int64_t p,
+                                                       int64_t n, int64_t kw, TensorState st,
+                                                       const int64_t *out_sel,
+                                                       const double *out_coef,
+                                                       const int64_t *out_count,
+                                                       double *out_rnorm) {
+  const int64_t sig = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sig >= p || (st.status[sig] & ST_DELEGATE)) return;
+  const int64_t kd = out_count[sig];
+  if (kd == 0) return;
+  const int64_t *sel = out_sel + sig * kw;
+  const double *x = out_coef + sig * kw;
   double rr = 0.0;
   for (int64_t i = lane; i < n; i += 32) {
     double ri = (double)ys[sig * n + i];
-    for (int64_t l = 0; l < kd; l++) ri = fma(-xv[l], __ldg(d64 + sel[l] * n + i), ri);
-    rw[i] = ri;
-    st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)ri);
+    for (int64_t l = 0; l < kd; l++) ri = fma(-x[l], __ldg(d64 + sel[l] * n + i), ri);
     rr = fma(ri, ri, rr);
   }
-  const double rnorm = sqrt(warp_sum(rr));
-  if (lane == 0) {
-    st.rnorm[sig] = rnorm;
-    out_rnorm[sig] = rnorm;
-    out_count[sig] = kd;
-    const bool done = rnorm <= st.tol[sig] || kd >= k_max;
-    if (done)
-      st.status[sig] |= ST_DONE;
-    else
-      atomicAdd(st.active + iter, 1);
-  }
+  rr = warp_sum(rr);
+  if (lane == 0) out_rnorm[sig] = sqrt(rr);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -475,8 +714,8 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols_pad, 
 int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw) {
   const int64_t n_pad = (n + BK - 1) / BK * BK;
   const int64_t p_pad = (p + BM - 1) / BM * BM;
-  return p * n * 8 + p_pad * n_pad * 2 + p * kw * kw * 8 + p * kw * 8 + p * 8 * 2 + p * 4 +
-         p * NCAND * 8 + p * 4;
+  return p_pad * n_pad * 2 + p * kw * kw * 8 + p * kw * 8 + p * 8 * 5 + p * NCAND * 8 + p * 4 +
+         p * 8 * 3 + 4 * 4096 + 16 * 256;
 }
 
 cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
@@ -491,11 +730,13 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     return r;
   };
   TensorState st{};
-  st.r64 = (double *)take(p * n * 8);
   st.r16 = (__nv_bfloat16 *)take(p_pad * n_pad * 2);
   st.linv = (double *)take(p * kw * kw * 8);
   st.z = (double *)take(p * kw * 8);
-  st.rnorm = (double *)take(p * 8);
+  st.rn2 = (double *)take(p * 8);
+  st.yy = (double *)take(p * 8);
+  st.rt = (double *)take(p * 8);
+  st.dr = (double *)take(p * 8);
   st.tol = (double *)take(p * 8);
   st.status = a.status;
   int *cidx = (int *)take(p * NCAND * 4);
@@ -505,15 +746,24 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   st.cand_val = cval;
   st.cand_drop = cdrop;
   st.active = (int *)take((a.k_max + 1) * 4);
+  st.npending = (int *)take((a.k_max + 1) * 4);
+  st.pending = (int64_t *)take(p * 8);
+  st.rs_j = (int64_t *)take(p * 8);
+  st.rs_c = (double *)take(p * 8);
+  st.rescans = a.rescans;
+  st.debug_sig = getenv("CDB_LS_DEBUG") ? atoll(getenv("CDB_LS_DEBUG")) : -1;
   cudaError_t e;
   if ((e = cudaMemsetAsync(st.r16, 0, p_pad * n_pad * 2, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(st.active, 0, (a.k_max + 1) * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(st.npending, 0, (a.k_max + 1) * 4, stream)) != cudaSuccess) return e;
 
   CUtensorMap tm_a, tm_b;
-  if (!make_map(&tm_a, st.r16, p_pad, n_pad, BM) || !make_map(&tm_b, a.d16, t, n_pad, BN))
+  if (!make_map(&tm_a, st.r16, p_pad, n_pad, BMH) || !make_map(&tm_b, a.d16, t, n_pad, BN))
     return cudaErrorInvalidValue;
 
   const unsigned wblocks = (unsigned)((p * 32 + 255) / 256);
+  {
+  ProfScope _ps("ls_init", stream);
   if (a.ys_f32)
     ls_init_kernel<float><<<wblocks, 256, 0, stream>>>((const float *)a.ys, p, n, n_pad, kw, a.eps,
                                                        st, a.out_sel, a.out_coef, a.out_count,
@@ -523,52 +773,118 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
                                                         a.eps, st, a.out_sel, a.out_coef,
                                                         a.out_count, a.out_rnorm, a.out_scans,
                                                         a.out_flag);
+  }
   note_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-  const size_t corr_smem = sizeof(CorrSmem) + 1024;
-  if ((e = cudaFuncSetAttribute(corr_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)corr_smem)) != cudaSuccess)
+  const bool a_res = n_pad / BK <= RES_KCHUNKS;
+  const size_t corr_smem = (a_res ? sizeof(CorrSmemRes) : sizeof(CorrSmemStr)) + 1024;
+  if ((e = cudaFuncSetAttribute(a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)corr_smem)) !=
+      cudaSuccess)
     return e;
   const int64_t m_tiles = p_pad / BM;
-  const unsigned corr_grid = (unsigned)(m_tiles < a.num_sms ? m_tiles : a.num_sms);
-  const int64_t ls_per_warp = (int64_t)sizeof(double) * (kw * kw + 4 * kw);
+  unsigned corr_grid = (unsigned)(m_tiles < a.num_sms ? m_tiles : a.num_sms);
+  if (const char *cap = getenv("CDB_CORR_GRID_CAP")) {
+    const int c = atoi(cap);
+    if (c > 0 && (unsigned)c < corr_grid) corr_grid = (unsigned)c;
+  }
+  const int64_t ls_per_warp = (int64_t)sizeof(double) * (kw * kw + 4 * kw + n);
   int ls_wpb = (int)((160 * 1024) / ls_per_warp);
   if (ls_wpb > 8) ls_wpb = 8;
   if (ls_wpb < 1) ls_wpb = 1;
   const size_t ls_smem = (size_t)ls_per_warp * ls_wpb;
-  if (a.ys_f32) {
-    if ((e = cudaFuncSetAttribute(ls_step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ls_smem)) != cudaSuccess)
-      return e;
-  } else {
-    if ((e = cudaFuncSetAttribute(ls_step_kernel<double>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls_smem)) !=
-        cudaSuccess)
-      return e;
-  }
-  // rigorous bound of |c_bf16 - c| / (|r| |d|): bf16 rounding of both
-  // operands (2u + u^2, u = 2^-8) plus fp32 accumulation over n_pad terms
-  const double c_err = 2.0 * 0x1p-8 + 0x1p-16 + (double)(n_pad + 16) * 0x1p-23;
+  if (a.ys_f32)
+    e = cudaFuncSetAttribute(ls_step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ls_smem);
+  else
+    e = cudaFuncSetAttribute(ls_step_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ls_smem);
+  if (e != cudaSuccess) return e;
+  // rigorous bound of |c~ - <d, r~>| / (|r~| |d|): bf16 rounding of both
+  // operands (2u + u^2, u = 2^-8), fp32 accumulation over n_pad terms, and
+  // the 2^-15 truncation of the packed epilogue keys
+  const double c_err = 2.0 * 0x1p-8 + 0x1p-16 + (double)(n_pad + 16) * 0x1p-23 + 0x1p-15;
   const unsigned ls_grid = (unsigned)((p + ls_wpb - 1) / ls_wpb);
   for (int it = 0; it < a.k_max; it++) {
-    corr_topk_kernel<<<corr_grid, THREADS, corr_smem, stream>>>(
-        tm_a, tm_b, p, t, (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, cidx,
-        cval, cdrop);
+    {
+    ProfScope _ps("corr_topk", stream);
+    auto kern = a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>;
+    kern<<<corr_grid, THREADS, corr_smem, stream>>>(tm_a, tm_b, p, t, (int)(n_pad / BK), m_tiles,
+                                                    it ? st.active + it - 1 : nullptr, cidx, cval,
+                                                    cdrop);
+    }
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (a.ys_f32)
-      ls_step_kernel<float><<<ls_grid, ls_wpb * 32, ls_smem, stream>>>(
-          (const float *)a.ys, a.d64, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err, a.dmax, st,
-          a.out_sel, a.out_coef, a.out_count, a.out_rnorm, a.out_scans);
-    else
-      ls_step_kernel<double><<<ls_grid, ls_wpb * 32, ls_smem, stream>>>(
-          (const double *)a.ys, a.d64, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err, a.dmax, st,
-          a.out_sel, a.out_coef, a.out_count, a.out_rnorm, a.out_scans);
-    note_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    for (int resume = 0; resume < 2; resume++) {
+      if (resume) {
+        ProfScope _ps("rescan", stream);
+        if (a.ys_f32)
+          rescan_kernel<float><<<(unsigned)a.num_sms, 256, 0, stream>>>(
+              (const float *)a.ys, a.d64, a.gram, t, n, kw, it, st, a.out_sel, a.out_coef);
+        else
+          rescan_kernel<double><<<(unsigned)a.num_sms, 256, 0, stream>>>(
+              (const double *)a.ys, a.d64, a.gram, t, n, kw, it, st, a.out_sel, a.out_coef);
+        note_launch();
+      }
+      ProfScope _ps(resume ? "ls_resume" : "ls_step", stream);
+      const unsigned grid = resume ? (unsigned)a.num_sms : ls_grid;
+      if (a.ys_f32)
+        ls_step_kernel<float><<<grid, ls_wpb * 32, ls_smem, stream>>>(
+            (const float *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
+            a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
+      else
+        ls_step_kernel<double><<<grid, ls_wpb * 32, ls_smem, stream>>>(
+            (const double *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
+            a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
+      note_launch();
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
   }
-  return cudaSuccess;
+  ProfScope _ps("ls_final", stream);
+  if (a.ys_f32)
+    ls_final_kernel<float><<<wblocks, 256, 0, stream>>>((const float *)a.ys, a.d64, p, n, kw, st,
+                                                        a.out_sel, a.out_coef, a.out_count,
+                                                        a.out_rnorm);
+  else
+    ls_final_kernel<double><<<wblocks, 256, 0, stream>>>((const double *)a.ys, a.d64, p, n, kw, st,
+                                                         a.out_sel, a.out_coef, a.out_count,
+                                                         a.out_rnorm);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// One correlation pass on caller-provided residual rows (debug / unit tests):
+// r16 = bf16(rows) (P x n fp32 device), candidate lists out.
+cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *rows, int64_t p,
+                            int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
+                            cudaStream_t stream) {
+  const int64_t n_pad = (n + BK - 1) / BK * BK;
+  const int64_t p_pad = (p + BM - 1) / BM * BM;
+  __nv_bfloat16 *r16 = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&r16, p_pad * n_pad * 2, stream);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(r16, 0, p_pad * n_pad * 2, stream);
+  to_bf16_rows<<<(unsigned)((p * n_pad + 255) / 256), 256, 0, stream>>>(rows, p, n, n_pad, r16);
+  CUtensorMap tm_a, tm_b;
+  if (!make_map(&tm_a, r16, p_pad, n_pad, BMH) || !make_map(&tm_b, d16, t, n_pad, BN))
+    return cudaErrorInvalidValue;
+  const bool a_res = n_pad / BK <= RES_KCHUNKS;
+  const size_t corr_smem = (a_res ? sizeof(CorrSmemRes) : sizeof(CorrSmemStr)) + 1024;
+  auto kern = a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>;
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)corr_smem)) != cudaSuccess)
+    return e;
+  const int64_t m_tiles = p_pad / BM;
+  int64_t grid = m_tiles < 148 ? m_tiles : 148;
+  if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
+  kern<<<(unsigned)grid, THREADS, corr_smem, stream>>>(tm_a, tm_b, p, t, (int)(n_pad / BK),
+                                                       m_tiles, nullptr, cand_idx, cand_val,
+                                                       cand_drop);
+  note_launch();
+  e = cudaGetLastError();
+  cudaFreeAsync(r16, stream);
+  return e;
 }
 
 }  // namespace cdb
