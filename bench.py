@@ -329,7 +329,8 @@ def bench_ours(args):
     full_roof = None
     if corr:
         c_ms = corr[0] / max(corr[1], 1)
-        c_flops = 2.0 * w.n_signal * w.t_high * P  # one launch scores every atom of every signal
+        # one launch scores every atom of every signal of its chunk
+        c_flops = 2.0 * w.n_signal * w.t_high * P * args.steps * w.k / max(corr[1], 1)
         full_roof = {"bound": "tensor", "kernel": "corr_topk",
                      "achieved": c_flops / (c_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
                      "unit": "TFLOP/s",

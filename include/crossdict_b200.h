@@ -76,7 +76,8 @@ typedef enum {
     CDB_ENGINE_AUTO = 0,     /* pick per problem shape (default)               */
     CDB_ENGINE_EXACT = 1,    /* warp-per-signal fp64 restatement of the kernel  */
     CDB_ENGINE_GRAM = 2,     /* signal-stationary fp64 Gram/Cholesky OMP        */
-    CDB_ENGINE_TENSOR = 3    /* tcgen05 bf16 correlation + certified fp64 LS    */
+    CDB_ENGINE_TENSOR = 3,   /* tcgen05 bf16 correlation + certified fp64 LS    */
+    CDB_ENGINE_RESIDENT = 4  /* dictionary resident in smem, fp64, warp/signal  */
 } cdb_engine;
 
 /*

@@ -17,7 +17,7 @@ import numpy as np
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                         "libcrossdict_b200.so")
 
-ENGINES = {"auto": 0, "exact": 1, "gram": 2, "tensor": 3}
+ENGINES = {"auto": 0, "exact": 1, "gram": 2, "tensor": 3, "resident": 4}
 
 #: every symbol include/crossdict_b200.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",

@@ -140,6 +140,17 @@ struct DevInfo {
 cdb_status device_info(DevInfo &di) {
   int dev = 0;
   CDB_CUDA(cudaGetDevice(&dev));
+  static int pool_configured = -1;
+  if (pool_configured != dev) {
+    // keep freed stream-ordered scratch cached in the pool: the engines
+    // allocate hundreds of MB of state per call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_configured = dev;
+  }
   CDB_CUDA(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
   CDB_CUDA(cudaDeviceGetAttribute(&di.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   CDB_CUDA(cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, dev));
@@ -212,7 +223,7 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
   DevBuf status;
   CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
   CDB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(uint32_t) * p, st));
-  const int64_t per = cdb::tensor_state_bytes(1, d->n, kw) + 1024;
+  const int64_t per = cdb::tensor_state_bytes(1 << 16, d->n, kw) / (1 << 16) + 1;
   int64_t chunk = kScratchBudget / per;
   if (chunk < 128) chunk = 128;
   if (chunk > p) chunk = p;
@@ -263,11 +274,15 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
 cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p, int64_t k_max,
                    int64_t kw, const double *eps, const cdb::Cands &cands, int64_t max_cands,
                    Outs &o, int engine, const DevInfo &di, cudaStream_t st,
-                   const char *tag = nullptr) {
+                   const char *tag = nullptr, const double *alpha0 = nullptr) {
   if (p <= 0) return CDB_OK;
   const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit;
+  const bool resident = cdb::resident_fits(d->n, d->t, kw, max_cands, di.smem_optin);
+  if (engine == CDB_ENGINE_RESIDENT && !resident) engine = CDB_ENGINE_AUTO;  // a preference
   if (engine == CDB_ENGINE_AUTO) {
-    if (!d->gram || max_cands <= 0)
+    if (resident && max_cands > 0)
+      engine = CDB_ENGINE_RESIDENT;
+    else if (!d->gram || max_cands <= 0)
       engine = CDB_ENGINE_EXACT;
     else if (h_smem)
       engine = CDB_ENGINE_GRAM;
@@ -279,12 +294,41 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   if ((engine == CDB_ENGINE_GRAM || engine == CDB_ENGINE_TENSOR) && !d->gram)
     return fail(CDB_ERR_ARG, "engine needs the dictionary's Gram matrix (raise the budget)");
   if (engine == CDB_ENGINE_TENSOR && cands.mode != 0) engine = CDB_ENGINE_GRAM;
+  if (engine == CDB_ENGINE_GRAM && (max_cands > 512 || kw > 64))  // beyond the Gram kernel's tiles
+    engine = cands.mode == 0 ? CDB_ENGINE_TENSOR : CDB_ENGINE_EXACT;
   g_last_engine = engine;
   g_last_rescans = 0;
   g_last_delegated = 0;
   if (engine == CDB_ENGINE_EXACT)
     return run_exact(d, ys, f32, p, nullptr, k_max, kw, eps, cands, max_cands, o, di, st);
   if (engine == CDB_ENGINE_TENSOR) return run_tensor(d, ys, f32, p, k_max, kw, eps, cands, o, di, st);
+  if (engine == CDB_ENGINE_RESIDENT) {
+    if (!resident) return fail(CDB_ERR_ARG, "dictionary too large for the resident engine");
+    DevBuf status;
+    CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
+    CDB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(uint32_t) * p, st));
+    cdb::ResidentArgs r{};
+    r.d64 = d->d64;
+    r.t = d->t;
+    r.n = d->n;
+    r.p = p;
+    r.k_max = k_max;
+    r.k_width = kw;
+    r.eps = eps;
+    r.cands = cands;
+    r.max_cands = max_cands;
+    r.out_sel = (int64_t *)o.sel.dev;
+    r.out_coef = (double *)o.coef.dev;
+    r.out_count = (int64_t *)o.count.dev;
+    r.out_rnorm = (double *)o.rnorm.dev;
+    r.out_scans = (int64_t *)o.scans.dev;
+    r.out_flag = (uint8_t *)o.flag.dev;
+    r.status = status.as<uint32_t>();
+    r.tag = tag ? (std::string(tag) == "gram_step1" ? "resident_step1" : "resident_step2") : nullptr;
+    CDB_CUDA(cdb::launch_resident(r, ys, f32, di.smem_optin, di.sms, st));
+    return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, max_cands, o,
+                            status.as<uint32_t>(), di, st);
+  }
 
   DevBuf status;
   CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
@@ -308,6 +352,7 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   g.out_flag = (uint8_t *)o.flag.dev;
   g.status = status.as<uint32_t>();
   g.tag = tag;
+  g.alpha0_in = alpha0;
   int64_t chunk = p;
   DevBuf hwork;
   if (!h_smem) {
@@ -639,8 +684,22 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   c2.q = q;
   c2.nb = (const int64_t *)lo.count.dev;
   c2.clip = 1;
+  // the Gram engine gets its alpha0 = <d_C, y> from the parent-routed kernel
+  DevBuf alpha0, rwork;
+  const bool high_resident =
+      cdb::resident_fits(high->n, high->t, k_high, k1 * q, di.smem_optin) &&
+      (engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_RESIDENT);
+  const bool use_route = high->gram && !high_resident && engine != CDB_ENGINE_EXACT &&
+                         high->t / q == low->t && 8 * q * n <= 192 * 1024;
+  if (use_route) {
+    CDB_CUDA(alpha0.alloc(sizeof(double) * p * k1 * q, st));
+    CDB_CUDA(rwork.alloc((size_t)cdb::route_work_bytes(low->t, p, k1), st));
+    CDB_CUDA(cdb::launch_route_alpha0(high->d64, low->t, n, q, y_in.dev, f32, blocks.as<int64_t>(),
+                                      (const int64_t *)lo.count.dev, p, k1, k1 * q,
+                                      alpha0.as<double>(), rwork.ptr, st));
+  }
   s = run_omp(high, y_in.dev, f32, p, k_high, k_high, eps2.as<double>(), c2, k1 * q, hi, engine, di,
-              st, "gram_step2");
+              st, "gram_step2", use_route ? alpha0.as<double>() : nullptr);
   if (s != CDB_OK) return s;
   CDB_CUDA(cudaEventRecord(ev[2], st));
   CDB_CUDA(lo.finish(st));

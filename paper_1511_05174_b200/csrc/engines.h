@@ -65,11 +65,36 @@ struct GramArgs {
   uint32_t *status;      // per-signal status bits (ST_DELEGATE ...)
   double *hwork;         // optional global H storage when it does not fit smem
   const char *tag;       // profiler name
+  const double *alpha0_in;  // optional precomputed <d_{C_j}, y> (P x max_cands)
 };
 // Shared-memory bytes per warp of the Gram engine (H in smem or global).
 int64_t gram_total_smem(int64_t max_cands, int64_t k_width, int64_t n, bool h_in_smem);
 cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
                         int num_sms, cudaStream_t stream);
+
+// ---------------------------------------------------------------- resident
+struct ResidentArgs {
+  const double *d64;     // T x N fp64 atoms (rows)
+  int64_t t, n;
+  int64_t p;
+  int64_t k_max, k_width;
+  const double *eps;
+  Cands cands;
+  int64_t max_cands;
+  int64_t *out_sel;
+  double *out_coef;
+  int64_t *out_count;
+  double *out_rnorm;
+  int64_t *out_scans;
+  uint8_t *out_flag;
+  uint32_t *status;
+  int64_t per_warp;      // filled by the launcher
+  int64_t t_pad;         // filled by the launcher
+  const char *tag;
+};
+bool resident_fits(int64_t n, int64_t t, int64_t kw, int64_t max_cands, int smem_optin);
+cudaError_t launch_resident(const ResidentArgs &args, const void *ys, bool ys_f32, int smem_optin,
+                            int num_sms, cudaStream_t stream);
 
 // ---------------------------------------------------------------- tensor
 struct TensorArgs {
@@ -114,6 +139,11 @@ cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *
                                cudaStream_t stream);
 cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad,
                            void *d16, cudaStream_t stream);
+cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q,
+                               const void *ys, bool ys_f32, const int64_t *blocks,
+                               const int64_t *nb, int64_t p, int64_t k1, int64_t smax,
+                               double *alpha0, void *work, cudaStream_t stream);
+int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1);
 cudaError_t launch_to_f32(const double *d64, int64_t count, float *d32, cudaStream_t stream);
 cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids,
                                      int *count, cudaStream_t stream);

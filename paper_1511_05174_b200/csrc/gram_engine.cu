@@ -82,7 +82,9 @@ __device__ __forceinline__ void alpha0_rows(const double *__restrict__ d64, cons
   }
 }
 
-template <typename YT>
+// KWT >= k_width and U * 32 >= max_cands are compile-time bounds so every
+// k-loop and candidate loop unrolls (predicated) with independent chains.
+template <typename YT, int KWT, int U>
 __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__restrict__ ys,
                                                        int h_in_smem, int64_t smem_per_warp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -92,8 +94,9 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   if (local >= a.p) return;
   const int64_t p = a.p_offset + local;
 
-  const int64_t n = a.n, kw = a.k_width, smax = a.max_cands, T = a.t;
-  const Cands &cs = a.cands;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
+  const int64_t T = a.t;
+  const Cands cs = a.cands;
   unsigned char *base = smem_raw + wib * smem_per_warp;
   GramSmem s;
   s.y = (double *)base;
@@ -111,67 +114,109 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   s.h = h_in_smem ? (double *)(base + align8(gram_smem_bytes_no_h(smax, kw, n)))
                   : a.hwork + local * kw * smax;
 
-  const int64_t S = cs.count(p);
-  const int64_t k_max = cs.budget(p, a.k_max, n);
+  const int S = (int)cs.count(p);
+  const int k_max = (int)cs.budget(p, a.k_max, n);
   int64_t *out_sel = a.out_sel + p * kw;
   double *out_coef = a.out_coef + p * kw;
 
-  for (int64_t i = lane; i < n; i += 32) s.y[i] = (double)ys[p * a.ys_stride + i];
-  for (int64_t w = lane; w < (S + 31) / 32; w += 32) s.taken[w] = 0u;
+  // this lane's candidates j = lane + 32u and their atom ids
+  int cid[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int j = lane + 32 * u;
+    cid[u] = j < S ? (int)cs.id(p, j) : 0;
+  }
+  for (int i = lane; i < n; i += 32) s.y[i] = (double)ys[p * a.ys_stride + i];
+  if (lane < (S + 31) / 32) s.taken[lane] = 0u;
+  for (int w = lane + 32; w < (S + 31) / 32; w += 32) s.taken[w] = 0u;
   __syncwarp();
   const double ynorm = sqrt(dot4_quad(s.y, s.y, n, lane));
   const double tol = a.eps[p];
 
-  int64_t kdone = 0, scans = 0;
+  int kdone = 0;
+  int64_t scans = 0;
   double rnorm = ynorm;
   bool delegate = false;
 
   if (!(ynorm <= tol) && k_max > 0) {
-    alpha0_rows(a.d64, cs, p, S, n, s.y, s.alpha0, s.c, lane);
+    if (a.alpha0_in) {
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int j = lane + 32 * u;
+        if (j < S) {
+          const double v = a.alpha0_in[p * smax + j];
+          s.alpha0[j] = v;
+          s.c[j] = v;
+        }
+      }
+    } else {
+      alpha0_rows(a.d64, cs, p, S, n, s.y, s.alpha0, s.c, lane);
+    }
     double yy = 0.0;
-    for (int64_t i = lane; i < n; i += 32) yy = fma(s.y[i], s.y[i], yy);
+    for (int i = lane; i < n; i += 32) yy = fma(s.y[i], s.y[i], yy);
     yy = warp_sum(yy);
     double rn2 = yy;
     const double tol2 = tol * tol;
     const double band = 1e-12 * yy;
     __syncwarp();
 
-    for (int64_t k = 0; k < k_max; k++) {
+    for (int k = 0; k < k_max; k++) {
       scans += S - k;
       // ---- selection: max |c_j| over non-taken, ties -> lowest index
       double best = -1.0;
-      int64_t bestj = -1;
-      for (int64_t j = lane; j < S; j += 32) {
-        if ((s.taken[j >> 5] >> (j & 31)) & 1u) continue;
-        const double v = fabs(s.c[j]);
-        if (v > best) {
-          best = v;
-          bestj = j;
+      int bestj = -1;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int j = lane + 32 * u;
+        if (j < S && !((s.taken[j >> 5] >> (j & 31)) & 1u)) {
+          const double v = fabs(s.c[j]);
+          if (v > best) {
+            best = v;
+            bestj = j;
+          }
         }
       }
-      warp_argmax(best, bestj);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(CDB_FULL_MASK, best, o);
+        const int oj = __shfl_xor_sync(CDB_FULL_MASK, bestj, o);
+        if (oj >= 0 && (bestj < 0 || ov > best || (ov == best && oj < bestj))) {
+          best = ov;
+          bestj = oj;
+        }
+      }
       if (bestj < 0 || best <= 0.0) break;
       const int64_t nid = cs.id(p, bestj);
       if (lane == 0) {
         s.taken[bestj >> 5] |= 1u << (bestj & 31);
         s.sup[k] = nid;
       }
-      // ---- gathers from Gram row `nid` (independent loads, all lanes)
+      // ---- gathers from Gram row `nid` (independent loads)
       const double *grow = a.gram + nid * T;
-      for (int64_t l = lane; l < k; l += 32) s.g[l] = __ldg(grow + s.sup[l]);
-#pragma unroll 4
-      for (int64_t j = lane; j < S; j += 32) s.gc[j] = __ldg(grow + cs.id(p, j));
+      double gcv[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) gcv[u] = lane + 32 * u < S ? __ldg(grow + cid[u]) : 0.0;
+      const double gl = lane < k ? __ldg(grow + s.sup[lane]) : 0.0;
+      const double gl2 = lane + 32 < k ? __ldg(grow + s.sup[lane + 32]) : 0.0;
       const double gnn = __ldg(grow + nid);
+      if (lane < k) s.g[lane] = gl;
+      if (lane + 32 < k) s.g[lane + 32] = gl2;
       __syncwarp();
       // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l+32)
-      for (int64_t l = lane; l < k; l += 32) {
-        double acc = 0.0;
-        for (int64_t i = 0; i <= l; i++) acc = fma(s.lc[i * kw + l], s.g[i], acc);
-        s.w[l] = acc;
+#pragma unroll
+      for (int half = 0; half < (KWT + 31) / 32; half++) {
+        const int l = lane + 32 * half;
+        if (l < k) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < KWT; i++)
+            if (i <= l) acc = fma(s.lc[i * kw + l], s.g[i], acc);
+          s.w[l] = acc;
+        }
       }
       __syncwarp();
       double ww = 0.0, wz = 0.0;
-      for (int64_t l = lane; l < k; l += 32) {
+      for (int l = lane; l < k; l += 32) {
         ww = fma(s.w[l], s.w[l], ww);
         wz = fma(s.w[l], s.z[l], wz);
       }
@@ -182,31 +227,51 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
         delegate = true;
         break;
       }
-      const double d = sqrt(d2);
-      const double inv_d = 1.0 / d;
+      const double inv_d = 1.0 / sqrt(d2);
       const double zk = (s.alpha0[bestj] - wz) * inv_d;
       // ---- new row of L^{-1}: [-(w^T L^{-1}) / d, 1/d]
-      for (int64_t i = lane; i <= k; i += 32) {
-        double v;
-        if (i == k) {
-          v = inv_d;
-        } else {
-          double acc = 0.0;
-          for (int64_t l = i; l < k; l++) acc = fma(s.w[l], s.lr[l * kw + i], acc);
-          v = -acc * inv_d;
+#pragma unroll
+      for (int half = 0; half < (KWT + 31) / 32; half++) {
+        const int i = lane + 32 * half;
+        if (i <= k) {
+          double v;
+          if (i == k) {
+            v = inv_d;
+          } else {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < KWT; l++)
+              if (l >= i && l < k) acc = fma(s.w[l], s.lr[l * kw + i], acc);
+            v = -acc * inv_d;
+          }
+          s.lr[k * kw + i] = v;
+          s.lc[i * kw + k] = v;
         }
-        s.lr[k * kw + i] = v;
-        s.lc[i * kw + k] = v;
       }
       if (lane == 0) s.z[k] = zk;
-      // ---- h_k over candidates, correlation update
-      double *hk = s.h + k * smax;
-      for (int64_t j = lane; j < S; j += 32) {
-        double acc = s.gc[j];
-        for (int64_t i = 0; i < k; i++) acc = fma(-s.w[i], s.h[i * smax + j], acc);
-        const double h = acc * inv_d;
-        hk[j] = h;
-        s.c[j] = fma(-zk, h, s.c[j]);
+      // ---- h_k over candidates, correlation update (U independent chains)
+      double hacc[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) hacc[u] = gcv[u];
+#pragma unroll
+      for (int i = 0; i < KWT; i++) {
+        if (i < k) {
+          const double wi = s.w[i];
+          const double *hi = s.h + i * smax + lane;
+#pragma unroll
+          for (int u = 0; u < U; u++)
+            if (lane + 32 * u < S) hacc[u] = fma(-wi, hi[32 * u], hacc[u]);
+        }
+      }
+      double *hk = s.h + k * smax + lane;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int j = lane + 32 * u;
+        if (j < S) {
+          const double h = hacc[u] * inv_d;
+          hk[32 * u] = h;
+          s.c[j] = fma(-zk, h, s.c[j]);
+        }
       }
       rn2 -= zk * zk;
       kdone = k + 1;
@@ -215,16 +280,16 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
       const double gap = rn2 - tol2;
       if (gap > band) continue;
       if (gap < -band) break;
-      for (int64_t i = lane; i < kdone; i += 32) {
+      for (int i = lane; i < kdone; i += 32) {
         double acc = 0.0;
-        for (int64_t l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
+        for (int l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
         s.x[i] = acc;
       }
       __syncwarp();
       double rr = 0.0;
-      for (int64_t i = lane; i < n; i += 32) {
+      for (int i = lane; i < n; i += 32) {
         double ri = s.y[i];
-        for (int64_t l = 0; l < kdone; l++) ri = fma(-s.x[l], a.d64[s.sup[l] * n + i], ri);
+        for (int l = 0; l < kdone; l++) ri = fma(-s.x[l], a.d64[s.sup[l] * n + i], ri);
         rr = fma(ri, ri, rr);
       }
       rr = warp_sum(rr);
@@ -238,22 +303,22 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   }
   // ---- coefficients x = L^{-T} z (pick order), exact final residual norm
   __syncwarp();
-  for (int64_t i = lane; i < kdone; i += 32) {
+  for (int i = lane; i < kdone; i += 32) {
     double acc = 0.0;
-    for (int64_t l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
+    for (int l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
     s.x[i] = acc;
   }
   __syncwarp();
   if (kdone > 0) {
     double rr = 0.0;
-    for (int64_t i = lane; i < n; i += 32) {
+    for (int i = lane; i < n; i += 32) {
       double ri = s.y[i];
-      for (int64_t l = 0; l < kdone; l++) ri = fma(-s.x[l], __ldg(a.d64 + s.sup[l] * n + i), ri);
+      for (int l = 0; l < kdone; l++) ri = fma(-s.x[l], __ldg(a.d64 + s.sup[l] * n + i), ri);
       rr = fma(ri, ri, rr);
     }
     rnorm = sqrt(warp_sum(rr));
   }
-  for (int64_t j = lane; j < kw; j += 32) {
+  for (int j = lane; j < kw; j += 32) {
     out_sel[j] = j < kdone ? s.sup[j] : -1;
     out_coef[j] = j < kdone ? s.x[j] : 0.0;
   }
@@ -263,6 +328,43 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
     a.out_scans[p] = scans;
     a.out_flag[p] = 0;
   }
+}
+
+template <typename YT, int KWT, int U>
+cudaError_t launch_gram_tu(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
+                           int wpb, int64_t blocks, cudaStream_t stream) {
+  const int64_t smem = per_warp * wpb;
+  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, KWT, U>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gram_omp_kernel<YT, KWT, U><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
+                                                                            per_warp);
+  return cudaGetLastError();
+}
+
+template <typename YT, int KWT>
+cudaError_t launch_gram_t(const GramArgs &args, const YT *ys, int u, int h_in_smem,
+                          int64_t per_warp, int wpb, int64_t blocks, cudaStream_t stream) {
+  switch (u) {
+    case 1: return launch_gram_tu<YT, KWT, 1>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 2: return launch_gram_tu<YT, KWT, 2>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 4: return launch_gram_tu<YT, KWT, 4>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 8: return launch_gram_tu<YT, KWT, 8>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 16: return launch_gram_tu<YT, KWT, 16>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename YT>
+cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int kwt, int u, int h_in_smem,
+                          int64_t per_warp, int wpb, int64_t blocks, cudaStream_t stream) {
+  switch (kwt) {
+    case 8: return launch_gram_t<YT, 8>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
+    case 16: return launch_gram_t<YT, 16>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
+    case 32: return launch_gram_t<YT, 32>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
+    case 64: return launch_gram_t<YT, 64>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -282,27 +384,21 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   const bool h_in_smem = args.hwork == nullptr;
   const int64_t per_warp = gram_total_smem(s, kw, n, h_in_smem);
   if (per_warp > max_smem_per_block) return cudaErrorInvalidValue;
+  if (kw > 64 || s > 512) return cudaErrorInvalidValue;
   int wpb = (int)(max_smem_per_block / per_warp);
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
-  const int64_t smem = per_warp * wpb;
   const int64_t blocks = (args.p + wpb - 1) / wpb;
-  cudaError_t e;
-  if (ys_f32) {
-    e = cudaFuncSetAttribute(gram_omp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-    gram_omp_kernel<float><<<(unsigned)blocks, wpb * 32, smem, stream>>>(
-        args, (const float *)ys, h_in_smem ? 1 : 0, per_warp);
-  } else {
-    e = cudaFuncSetAttribute(gram_omp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-    gram_omp_kernel<double><<<(unsigned)blocks, wpb * 32, smem, stream>>>(
-        args, (const double *)ys, h_in_smem ? 1 : 0, per_warp);
-  }
+  int kwt = 8;
+  while (kwt < kw) kwt *= 2;
+  int u = 1;
+  while (32 * u < s) u *= 2;
   note_launch();
-  return cudaGetLastError();
+  if (ys_f32)
+    return launch_gram_y<float>(args, (const float *)ys, kwt, u, h_in_smem ? 1 : 0, per_warp, wpb,
+                                blocks, stream);
+  return launch_gram_y<double>(args, (const double *)ys, kwt, u, h_in_smem ? 1 : 0, per_warp, wpb,
+                               blocks, stream);
 }
 
 }  // namespace cdb

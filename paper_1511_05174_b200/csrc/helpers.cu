@@ -151,6 +151,92 @@ __global__ void row_norm_max_kernel(const double *__restrict__ d, int64_t t, int
   if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(sqrt(acc)));
 }
 
+// ---- zero-tree step-2 routing: (signal, slot) pairs grouped by parent block
+__global__ void route_count_kernel(const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb,
+                                   int64_t p, int64_t k1, int *__restrict__ count) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= p) return;
+  for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&count[blocks[s * k1 + b]], 1);
+}
+
+// exclusive scan of count[0..m) into offs[0..m] and cursor copy (one CTA)
+__global__ void route_scan_kernel(const int *__restrict__ count, int64_t m,
+                                  int64_t *__restrict__ offs, int64_t *__restrict__ cursor) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (m + blockDim.x - 1) / blockDim.x;
+  int64_t sum = 0;
+  for (int64_t i = tid * per; i < (tid + 1) * per && i < m; i++) sum += count[i];
+  part[tid] = sum;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; i++) {
+      const int64_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    offs[m] = run;
+  }
+  __syncthreads();
+  int64_t run = part[tid];
+  for (int64_t i = tid * per; i < (tid + 1) * per && i < m; i++) {
+    offs[i] = run;
+    cursor[i] = run;
+    run += count[i];
+  }
+}
+
+__global__ void route_fill_kernel(const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb,
+                                  int64_t p, int64_t k1, unsigned long long *__restrict__ cursor,
+                                  int64_t *__restrict__ pairs) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= p) return;
+  for (int64_t b = 0; b < nb[s]; b++) {
+    const int64_t pos = (int64_t)atomicAdd(&cursor[blocks[s * k1 + b]], 1ull);
+    pairs[pos] = s * k1 + b;
+  }
+}
+
+// alpha0[s][b*Q + c] = <d_{parent*Q + c}, y_s> for every routed pair: one CTA
+// per parent keeps its Q children in shared memory (fp64) and streams the
+// signals routed to it; one warp per pair, coalesced signal reads.
+template <typename YT>
+__global__ void __launch_bounds__(256) alpha0_routed_kernel(
+    const double *__restrict__ d64, int64_t n, int64_t q, const YT *__restrict__ ys,
+    const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t k1,
+    int64_t smax, double *__restrict__ alpha0) {
+  extern __shared__ double child[];  // q x n
+  const int64_t parent = blockIdx.x;
+  const int64_t lo = offs[parent], hi = offs[parent + 1];
+  if (lo == hi) return;
+  for (int64_t e = threadIdx.x; e < q * n; e += blockDim.x) child[e] = d64[parent * q * n + e];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t e = lo + warp; e < hi; e += blockDim.x >> 5) {
+    const int64_t pr = pairs[e];
+    const int64_t s = pr / k1, b = pr % k1;
+    const YT *y = ys + s * n;
+    double *out = alpha0 + s * smax + b * q;
+    for (int64_t c0 = 0; c0 < q; c0 += 8) {
+      double acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) acc[c] = 0.0;
+      for (int64_t i = lane; i < n; i += 32) {
+        const double yi = (double)y[i];
+#pragma unroll
+        for (int c = 0; c < 8; c++)
+          if (c0 + c < q) acc[c] = fma(child[(c0 + c) * n + i], yi, acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const double v = warp_sum(acc[c]);
+        if (lane == c && c0 + c < q) out[c0 + c] = v;
+      }
+    }
+  }
+}
+
 inline unsigned blocks_for(int64_t work, int threads) {
   return (unsigned)((work + threads - 1) / threads);
 }
@@ -244,6 +330,49 @@ cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double 
                                                                      (unsigned long long *)out);
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q,
+                               const void *ys, bool ys_f32, const int64_t *blocks,
+                               const int64_t *nb, int64_t p, int64_t k1, int64_t smax,
+                               double *alpha0, void *work, cudaStream_t stream) {
+  ProfScope _ps("route_alpha0", stream);
+  // work: count int[t_low] | offs int64[t_low+1] | cursor u64[t_low] | pairs int64[p*k1]
+  uint8_t *w = (uint8_t *)work;
+  int *count = (int *)w;
+  w += ((t_low * 4 + 255) / 256) * 256;
+  int64_t *offs = (int64_t *)w;
+  w += (((t_low + 1) * 8 + 255) / 256) * 256;
+  int64_t *cursor = (int64_t *)w;
+  w += ((t_low * 8 + 255) / 256) * 256;
+  int64_t *pairs = (int64_t *)w;
+  cudaError_t e = cudaMemsetAsync(count, 0, t_low * 4, stream);
+  if (e != cudaSuccess) return e;
+  route_count_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1, count);
+  route_scan_kernel<<<1, 1024, 0, stream>>>(count, t_low, offs, cursor);
+  route_fill_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1,
+                                                            (unsigned long long *)cursor, pairs);
+  const size_t smem = sizeof(double) * q * n;
+  if (smem > 48 * 1024) {
+    e = ys_f32 ? cudaFuncSetAttribute(alpha0_routed_kernel<float>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+               : cudaFuncSetAttribute(alpha0_routed_kernel<double>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if (ys_f32)
+    alpha0_routed_kernel<float><<<(unsigned)t_low, 256, smem, stream>>>(
+        d64, n, q, (const float *)ys, offs, pairs, k1, smax, alpha0);
+  else
+    alpha0_routed_kernel<double><<<(unsigned)t_low, 256, smem, stream>>>(
+        d64, n, q, (const double *)ys, offs, pairs, k1, smax, alpha0);
+  note_launch(4);
+  return cudaGetLastError();
+}
+
+int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1) {
+  return ((t_low * 4 + 255) / 256) * 256 + (((t_low + 1) * 8 + 255) / 256) * 256 +
+         ((t_low * 8 + 255) / 256) * 256 + p * k1 * 8 + 256;
 }
 
 }  // namespace cdb

@@ -598,7 +598,9 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
 }
 
 // Exact fp64 argmax over every non-taken atom for the queued signals: one
-// CTA per signal, 8 warps split the atoms, coalesced row reads.
+// CTA per signal; the signal, its coefficients and a taken-atom bit mask sit
+// in shared memory; each warp streams 8 atom rows at a time with coalesced
+// loads (c_j = <d_j, y> - sum_s G[j, s] x_s, as in ls_step).
 template <typename YT>
 __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
                                                      const double *__restrict__ d64,
@@ -606,35 +608,61 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
                                                      int64_t n, int64_t kw, int iter,
                                                      TensorState st, const int64_t *out_sel,
                                                      const double *out_coef) {
+  extern __shared__ double rsm[];
   __shared__ double sv[8];
   __shared__ int64_t sj[8];
   __shared__ double sc[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t count = st.npending[iter];
+  double *y = rsm;                                   // n
+  double *x = y + n;                                 // kw
+  int64_t *sel = (int64_t *)(x + kw);                // kw
+  uint32_t *taken = (uint32_t *)(sel + kw);          // (t + 31) / 32
   for (int64_t e = blockIdx.x; e < count; e += gridDim.x) {
     const int64_t sig = st.pending[e];
     const int64_t k = iter;
-    const int64_t *sel = out_sel + sig * kw;
-    const double *x = out_coef + sig * kw;
-    const YT *y = ys + sig * n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = (double)ys[sig * n + i];
+    for (int64_t i = threadIdx.x; i < (t + 31) / 32; i += blockDim.x) taken[i] = 0u;
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+      x[i] = out_coef[sig * kw + i];
+      sel[i] = out_sel[sig * kw + i];
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {
+      const int64_t j = sel[threadIdx.x];
+      atomicOr(&taken[j >> 5], 1u << (j & 31));
+    }
+    __syncthreads();
     double best = -1.0, cbest = 0.0;
     int64_t bestj = -1;
-    for (int64_t j = warp; j < t; j += 8) {
-      bool live = true;
-      for (int64_t i = 0; i < k; i++)
-        if (sel[i] == j) live = false;
-      if (!live) continue;
-      const double *dj = d64 + j * n;
-      double acc = 0.0;
-      for (int64_t i = lane; i < n; i += 32) acc = fma(__ldg(dj + i), (double)y[i], acc);
-      const double *gj = gram + j * t;
-      for (int64_t s = lane; s < k; s += 32) acc = fma(-__ldg(gj + sel[s]), x[s], acc);
-      const double cj = warp_sum(acc);
-      const double v = fabs(cj);
-      if (v > best || (v == best && j < bestj)) {
-        best = v;
-        bestj = j;
-        cbest = cj;
+    for (int64_t j0 = (int64_t)warp * 8; j0 < t; j0 += 64) {
+      const double *rows[8];
+#pragma unroll
+      for (int r = 0; r < 8; r++) rows[r] = d64 + (j0 + r < t ? j0 + r : 0) * n;
+      double acc[8];
+#pragma unroll
+      for (int r = 0; r < 8; r++) acc[r] = 0.0;
+      for (int64_t i = lane; i < n; i += 32) {
+        const double yi = y[i];
+#pragma unroll
+        for (int r = 0; r < 8; r++) acc[r] = fma(__ldg(rows[r] + i), yi, acc[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int64_t j = j0 + r;
+        if (j < t) {
+          const double *gj = gram + j * t;
+          for (int64_t s = lane; s < k; s += 32) acc[r] = fma(-__ldg(gj + sel[s]), x[s], acc[r]);
+        }
+        const double cj = warp_sum(acc[r]);
+        if (j < t && !((taken[j >> 5] >> (j & 31)) & 1u)) {
+          const double v = fabs(cj);
+          if (v > best || (v == best && j < bestj)) {
+            best = v;
+            bestj = j;
+            cbest = cj;
+          }
+        }
       }
     }
     if (lane == 0) {
@@ -819,11 +847,12 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     for (int resume = 0; resume < 2; resume++) {
       if (resume) {
         ProfScope _ps("rescan", stream);
+        const size_t rs_smem = 8 * (n + 2 * kw) + 4 * ((t + 31) / 32) + 64;
         if (a.ys_f32)
-          rescan_kernel<float><<<(unsigned)a.num_sms, 256, 0, stream>>>(
+          rescan_kernel<float><<<(unsigned)a.num_sms, 256, rs_smem, stream>>>(
               (const float *)a.ys, a.d64, a.gram, t, n, kw, it, st, a.out_sel, a.out_coef);
         else
-          rescan_kernel<double><<<(unsigned)a.num_sms, 256, 0, stream>>>(
+          rescan_kernel<double><<<(unsigned)a.num_sms, 256, rs_smem, stream>>>(
               (const double *)a.ys, a.d64, a.gram, t, n, kw, it, st, a.out_sel, a.out_coef);
         note_launch();
       }

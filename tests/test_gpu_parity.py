@@ -17,7 +17,7 @@ from paper_1511_05174_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
 
-FAST_ENGINES = ["gram", "tensor", "auto"]
+FAST_ENGINES = ["gram", "tensor", "resident", "auto"]
 
 
 def _eps(g, ys_rows):
