@@ -690,7 +690,8 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
       cdb::resident_fits(high->n, high->t, k_high, k1 * q, di.smem_optin) &&
       (engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_RESIDENT);
   const bool use_route = high->gram && !high_resident && engine != CDB_ENGINE_EXACT &&
-                         high->t / q == low->t && 8 * q * n <= 192 * 1024;
+                         high->t / q == low->t && 8 * q * n <= 192 * 1024 &&
+                         (q == 1 || q == 2 || q == 4 || q == 8 || q == 16);
   if (use_route) {
     CDB_CUDA(alpha0.alloc(sizeof(double) * p * k1 * q, st));
     CDB_CUDA(rwork.alloc((size_t)cdb::route_work_bytes(low->t, p, k1), st));

@@ -199,42 +199,97 @@ __global__ void route_fill_kernel(const int64_t *__restrict__ blocks, const int6
 }
 
 // alpha0[s][b*Q + c] = <d_{parent*Q + c}, y_s> for every routed pair: one CTA
-// per parent keeps its Q children in shared memory (fp64) and streams the
-// signals routed to it; one warp per pair, coalesced signal reads.
-template <typename YT>
+// per parent keeps its Q children in shared memory (fp64); each thread codes
+// two routed signals against them (the child values are warp-broadcast
+// shared-memory reads, each used for two FMAs; no cross-lane reductions).
+template <typename YT, int QT>
 __global__ void __launch_bounds__(256) alpha0_routed_kernel(
-    const double *__restrict__ d64, int64_t n, int64_t q, const YT *__restrict__ ys,
+    const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t k1,
     int64_t smax, double *__restrict__ alpha0) {
-  extern __shared__ double child[];  // q x n
+  extern __shared__ double child[];  // QT x n
   const int64_t parent = blockIdx.x;
   const int64_t lo = offs[parent], hi = offs[parent + 1];
   if (lo == hi) return;
-  for (int64_t e = threadIdx.x; e < q * n; e += blockDim.x) child[e] = d64[parent * q * n + e];
+  for (int e = threadIdx.x; e < QT * n; e += blockDim.x) child[e] = d64[parent * QT * n + e];
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t e = lo + warp; e < hi; e += blockDim.x >> 5) {
-    const int64_t pr = pairs[e];
-    const int64_t s = pr / k1, b = pr % k1;
-    const YT *y = ys + s * n;
-    double *out = alpha0 + s * smax + b * q;
-    for (int64_t c0 = 0; c0 < q; c0 += 8) {
-      double acc[8];
+  for (int64_t e0 = lo + 2 * threadIdx.x; e0 < hi; e0 += 2 * blockDim.x) {
+    const bool two = e0 + 1 < hi;
+    const int64_t pr0 = pairs[e0], pr1 = two ? pairs[e0 + 1] : pr0;
+    const YT *y0 = ys + (pr0 / k1) * n;
+    const YT *y1 = ys + (pr1 / k1) * n;
+    double a0[QT], a1[QT];
 #pragma unroll
-      for (int c = 0; c < 8; c++) acc[c] = 0.0;
-      for (int64_t i = lane; i < n; i += 32) {
-        const double yi = (double)y[i];
+    for (int c = 0; c < QT; c++) {
+      a0[c] = 0.0;
+      a1[c] = 0.0;
+    }
+    int i = 0;
+    if constexpr (sizeof(YT) == 4) {
+      if ((n & 3) == 0) {  // 16-byte loads of both rows
+        const float4 *q0 = reinterpret_cast<const float4 *>(y0);
+        const float4 *q1 = reinterpret_cast<const float4 *>(y1);
+#pragma unroll 2
+        for (; i < n; i += 4) {
+          const float4 f0 = q0[i >> 2], f1 = q1[i >> 2];
+          const double u0[4] = {f0.x, f0.y, f0.z, f0.w}, u1[4] = {f1.x, f1.y, f1.z, f1.w};
 #pragma unroll
-        for (int c = 0; c < 8; c++)
-          if (c0 + c < q) acc[c] = fma(child[(c0 + c) * n + i], yi, acc[c]);
-      }
+          for (int t4 = 0; t4 < 4; t4++)
 #pragma unroll
-      for (int c = 0; c < 8; c++) {
-        const double v = warp_sum(acc[c]);
-        if (lane == c && c0 + c < q) out[c0 + c] = v;
+            for (int c = 0; c < QT; c++) {
+              const double dv = child[c * n + i + t4];
+              a0[c] = fma(dv, u0[t4], a0[c]);
+              a1[c] = fma(dv, u1[t4], a1[c]);
+            }
+        }
       }
     }
+#pragma unroll 4
+    for (; i < n; i++) {
+      const double v0 = (double)y0[i], v1 = (double)y1[i];
+#pragma unroll
+      for (int c = 0; c < QT; c++) {
+        const double dv = child[c * n + i];
+        a0[c] = fma(dv, v0, a0[c]);
+        a1[c] = fma(dv, v1, a1[c]);
+      }
+    }
+    double *o0 = alpha0 + (pr0 / k1) * smax + (pr0 % k1) * QT;
+#pragma unroll
+    for (int c = 0; c < QT; c++) o0[c] = a0[c];
+    if (two) {
+      double *o1 = alpha0 + (pr1 / k1) * smax + (pr1 % k1) * QT;
+#pragma unroll
+      for (int c = 0; c < QT; c++) o1[c] = a1[c];
+    }
   }
+}
+
+template <typename YT, int QT>
+cudaError_t launch_alpha0_q(const double *d64, int64_t t_low, int64_t n, const YT *ys,
+                            const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
+                            double *alpha0, cudaStream_t stream) {
+  const size_t smem = sizeof(double) * QT * n;
+  cudaError_t e = cudaFuncSetAttribute(alpha0_routed_kernel<YT, QT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  alpha0_routed_kernel<YT, QT><<<(unsigned)t_low, 256, smem, stream>>>(d64, (int)n, ys, offs,
+                                                                      pairs, k1, smax, alpha0);
+  return cudaGetLastError();
+}
+
+template <typename YT>
+cudaError_t launch_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q, const YT *ys,
+                          const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
+                          double *alpha0, cudaStream_t stream) {
+  switch (q) {
+    case 1: return launch_alpha0_q<YT, 1>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
+    case 2: return launch_alpha0_q<YT, 2>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
+    case 4: return launch_alpha0_q<YT, 4>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
+    case 8: return launch_alpha0_q<YT, 8>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
+    case 16: return launch_alpha0_q<YT, 16>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
+  }
+  return cudaErrorInvalidValue;
 }
 
 inline unsigned blocks_for(int64_t work, int threads) {
@@ -352,20 +407,11 @@ cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int
   route_scan_kernel<<<1, 1024, 0, stream>>>(count, t_low, offs, cursor);
   route_fill_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1,
                                                             (unsigned long long *)cursor, pairs);
-  const size_t smem = sizeof(double) * q * n;
-  if (smem > 48 * 1024) {
-    e = ys_f32 ? cudaFuncSetAttribute(alpha0_routed_kernel<float>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-               : cudaFuncSetAttribute(alpha0_routed_kernel<double>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  if (ys_f32)
-    alpha0_routed_kernel<float><<<(unsigned)t_low, 256, smem, stream>>>(
-        d64, n, q, (const float *)ys, offs, pairs, k1, smax, alpha0);
-  else
-    alpha0_routed_kernel<double><<<(unsigned)t_low, 256, smem, stream>>>(
-        d64, n, q, (const double *)ys, offs, pairs, k1, smax, alpha0);
+  e = ys_f32 ? launch_alpha0<float>(d64, t_low, n, q, (const float *)ys, offs, pairs, k1, smax,
+                                     alpha0, stream)
+             : launch_alpha0<double>(d64, t_low, n, q, (const double *)ys, offs, pairs, k1, smax,
+                                      alpha0, stream);
+  if (e != cudaSuccess) return e;
   note_launch(4);
   return cudaGetLastError();
 }

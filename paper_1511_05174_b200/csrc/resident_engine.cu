@@ -17,10 +17,14 @@
 namespace cdb {
 namespace {
 
+constexpr int RES_R = 2;        // signals per warp
+constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
+
 // FULL: candidate jl of lane l is atom l + 32u (mode 0) -> compile-time
-// shared-memory offsets in the correlation loop.
-template <typename YT, int U, bool FULL>
-__global__ void __launch_bounds__(1024, 1)
+// shared-memory offsets in the correlation loop.  R signals per warp share
+// every dictionary element loaded from shared memory (R FMAs per LDS).
+template <typename YT, int U, bool FULL, int R>
+__global__ void __launch_bounds__(512, 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
   extern __shared__ __align__(16) double rs[];
   const int n = (int)a.n, T = (int)a.t, kw = (int)a.k_width, Tp = (int)a.t_pad;
@@ -29,16 +33,7 @@ __global__ void __launch_bounds__(1024, 1)
   double *Dt = rs;                 // n x Tp  (columns T..Tp-1 are zero)
   double *nrm2 = Dt + n * Tp;      // Tp  (|d_j|^2)
   double *wbase = nrm2 + Tp;
-  const int per_warp = (int)a.per_warp;
-  double *y = wbase + warp * per_warp;
-  double *r = y + n;
-  double *lin = r + n;             // kw x kw
-  double *zv = lin + kw * kw;
-  double *wv = zv + kw;
-  double *xv = wv + kw;
-  double *gv = xv + kw;
-  int *sup = (int *)(gv + kw);     // kw ints (kw doubles reserved)
-  uint32_t *taken = (uint32_t *)(gv + 2 * kw);
+  const int per_sig = (int)a.per_warp;  // doubles of state per signal
 
   for (int e = threadIdx.x; e < n * Tp; e += blockDim.x) {
     const int i = e / Tp, j = e % Tp;
@@ -54,54 +49,102 @@ __global__ void __launch_bounds__(1024, 1)
 
   const Cands cs = a.cands;
   const double *eps = a.eps;
-  for (int64_t p = (int64_t)blockIdx.x * nwarps + warp; p < P; p += (int64_t)gridDim.x * nwarps) {
-    const int S = (int)cs.count(p);
-    const int k_max = (int)cs.budget(p, a.k_max, n);
-    int cid[U];
+  double *sbase = wbase + warp * R * per_sig;
+  for (int64_t p0 = ((int64_t)blockIdx.x * nwarps + warp) * R; p0 < P;
+       p0 += (int64_t)gridDim.x * nwarps * R) {
+    // ---- per-signal setup
+    int S[R], kmax[R], kdone[R];
+    int64_t scans[R];
+    double tol[R], rnorm[R];
+    bool live[R], delegate[R];
+    int cid[R][U];
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int jl = lane + 32 * u;
-      cid[u] = FULL ? jl : (jl < S ? (int)cs.id(p, jl) : Tp - 1);  // zero column pads
+    for (int q = 0; q < R; q++) {
+      const int64_t p = p0 + q;
+      double *y = sbase + q * per_sig;
+      double *r = y + n;
+      uint32_t *taken = (uint32_t *)(r + n + kw * kw + 5 * kw);
+      const bool valid = p < P;
+      S[q] = valid ? (int)cs.count(p) : 0;
+      kmax[q] = valid ? (int)cs.budget(p, a.k_max, n) : 0;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int jl = lane + 32 * u;
+        cid[q][u] = FULL ? jl : (jl < S[q] ? (int)cs.id(p, jl) : Tp - 1);
+      }
+      for (int i = lane; i < n; i += 32) {
+        const double v = valid ? (double)ys[p * n + i] : 0.0;
+        y[i] = v;
+        r[i] = v;
+      }
+      for (int w = lane; w < (S[q] + 31) / 32; w += 32) taken[w] = 0u;
+      __syncwarp();
+      const double ynorm = sqrt(dot4_quad(y, y, n, lane));  // reference order (_kernels.py:71)
+      tol[q] = valid ? eps[p] : 0.0;
+      rnorm[q] = ynorm;
+      kdone[q] = 0;
+      scans[q] = 0;
+      delegate[q] = false;
+      live[q] = valid && !(ynorm <= tol[q]) && kmax[q] > 0;
     }
-    for (int i = lane; i < n; i += 32) {
-      const double v = (double)ys[p * n + i];
-      y[i] = v;
-      r[i] = v;
-    }
-    for (int w = lane; w < (S + 31) / 32; w += 32) taken[w] = 0u;
-    __syncwarp();
-    const double ynorm = sqrt(dot4_quad(y, y, n, lane));  // reference order (_kernels.py:71)
-    const double tol = eps[p];
-    int kdone = 0;
-    int64_t scans = 0;
-    double rnorm = ynorm;
-    bool delegate = false;
-    if (!(ynorm <= tol)) {
-      for (int k = 0; k < k_max; k++) {
-        scans += S - k;
-        // ---- correlations of this lane's candidates with r (fp64)
-        double acc[U];
+    for (int k = 0;; k++) {
+      bool any = false;
 #pragma unroll
-        for (int u = 0; u < U; u++) acc[u] = 0.0;
-        const double *col = FULL ? Dt + lane : Dt;
-#pragma unroll 4
-        for (int i = 0; i < n; i++) {
-          const double ri = r[i];
-          const double *row = col + i * Tp;
+      for (int q = 0; q < R; q++) {
+        if (live[q] && k >= kmax[q]) live[q] = false;
+        any |= live[q];
+      }
+      if (!any) break;
+      // ---- correlations of this lane's candidates with each live residual
+      double acc[R][U];
 #pragma unroll
-          for (int u = 0; u < U; u++) acc[u] = fma(FULL ? row[32 * u] : row[cid[u]], ri, acc[u]);
+      for (int q = 0; q < R; q++)
+#pragma unroll
+        for (int u = 0; u < U; u++) acc[q][u] = 0.0;
+      const double *col = FULL ? Dt + lane : Dt;
+#pragma unroll 2
+      for (int i = 0; i < n; i++) {
+        double ri[R];
+#pragma unroll
+        for (int q = 0; q < R; q++) ri[q] = sbase[q * per_sig + n + i];
+        const double *row = col + i * Tp;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          if (FULL) {
+            const double dv = row[32 * u];
+#pragma unroll
+            for (int q = 0; q < R; q++) acc[q][u] = fma(dv, ri[q], acc[q][u]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < R; q++) acc[q][u] = fma(row[cid[q][u]], ri[q], acc[q][u]);
+          }
         }
+      }
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        if (!live[q]) continue;
+        const int64_t p = p0 + q;
+        double *y = sbase + q * per_sig;
+        double *r = y + n;
+        double *lin = r + n;
+        double *zv = lin + kw * kw;
+        double *wv = zv + kw;
+        double *xv = wv + kw;
+        double *gv = xv + kw;
+        int *sup = (int *)(gv + kw);
+        uint32_t *taken = (uint32_t *)(gv + 2 * kw);
+        scans[q] += S[q] - k;
         double best = -1.0, cbest = 0.0;
         int bestj = -1;
 #pragma unroll
         for (int u = 0; u < U; u++) {
           const int jl = lane + 32 * u;
-          if (jl < S && !((taken[jl >> 5] >> (jl & 31)) & 1u)) {
-            const double v = fabs(acc[u]);
+          if (jl < S[q] && !((taken[jl >> 5] >> (jl & 31)) & 1u)) {
+            const double v = fabs(acc[q][u]);
             if (v > best) {
               best = v;
               bestj = jl;
-              cbest = acc[u];
+              cbest = acc[q][u];
             }
           }
         }
@@ -116,7 +159,10 @@ __global__ void __launch_bounds__(1024, 1)
             cbest = oc;
           }
         }
-        if (bestj < 0 || best <= 0.0) break;  // _kernels.py:104
+        if (bestj < 0 || best <= 0.0) {  // _kernels.py:104
+          live[q] = false;
+          continue;
+        }
         const int nid = FULL ? bestj : (int)cs.id(p, bestj);
         if (lane == 0) {
           taken[bestj >> 5] |= 1u << (bestj & 31);
@@ -124,13 +170,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
         __syncwarp();
         // ---- Cholesky append: g_l = <d_{s_l}, d_new> from the resident atoms
-        if (lane < k) {
-          double g = 0.0;
-          const int sl = sup[lane];
-          for (int i = 0; i < n; i++) g = fma(Dt[i * Tp + sl], Dt[i * Tp + nid], g);
-          gv[lane] = g;
-        }
-        for (int l = lane + 32; l < k; l += 32) {
+        for (int l = lane; l < k; l += 32) {
           double g = 0.0;
           const int sl = sup[l];
           for (int i = 0; i < n; i++) g = fma(Dt[i * Tp + sl], Dt[i * Tp + nid], g);
@@ -149,8 +189,9 @@ __global__ void __launch_bounds__(1024, 1)
         const double gnn = nrm2[nid];
         const double d2 = gnn - ww;
         if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {
-          delegate = true;
-          break;
+          delegate[q] = true;
+          live[q] = false;
+          continue;
         }
         const double inv_d = 1.0 / sqrt(d2);
         const double zk = cbest * inv_d;  // q_k^T y = q_k^T r = <d_new, r> / d
@@ -167,43 +208,51 @@ __global__ void __launch_bounds__(1024, 1)
         }
         if (lane == 0) zv[k] = zk;
         __syncwarp();
-        kdone = k + 1;
-        for (int i = lane; i < kdone; i += 32) {
+        kdone[q] = k + 1;
+        for (int i = lane; i <= k; i += 32) {
           double accx = 0.0;
-          for (int l = i; l < kdone; l++) accx = fma(lin[l * kw + i], zv[l], accx);
+          for (int l = i; l <= k; l++) accx = fma(lin[l * kw + i], zv[l], accx);
           xv[i] = accx;
         }
         __syncwarp();
         // ---- residual r = y - D_S x (fp64) and its norm; stop test
         double rr = 0.0;
         for (int i = lane; i < n; i += 32) {
-          double ri = y[i];
+          double rv = y[i];
           const double *row = Dt + i * Tp;
-          for (int l = 0; l < kdone; l++) ri = fma(-xv[l], row[sup[l]], ri);
-          r[i] = ri;
-          rr = fma(ri, ri, rr);
+          for (int l = 0; l <= k; l++) rv = fma(-xv[l], row[sup[l]], rv);
+          r[i] = rv;
+          rr = fma(rv, rv, rr);
         }
-        rnorm = sqrt(warp_sum(rr));
+        rnorm[q] = sqrt(warp_sum(rr));
         __syncwarp();
-        if (rnorm <= tol) break;
+        if (rnorm[q] <= tol[q]) live[q] = false;
       }
     }
-    if (delegate) {
-      if (lane == 0) a.status[p] |= ST_DELEGATE;
-      __syncwarp();
-      continue;
-    }
-    int64_t *out_sel = a.out_sel + p * kw;
-    double *out_coef = a.out_coef + p * kw;
-    for (int j = lane; j < kw; j += 32) {
-      out_sel[j] = j < kdone ? sup[j] : -1;
-      out_coef[j] = j < kdone ? xv[j] : 0.0;
-    }
-    if (lane == 0) {
-      a.out_count[p] = kdone;
-      a.out_rnorm[p] = rnorm;
-      a.out_scans[p] = scans;
-      a.out_flag[p] = 0;
+    // ---- outputs
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      const int64_t p = p0 + q;
+      if (p >= P) continue;
+      if (delegate[q]) {
+        if (lane == 0) a.status[p] |= ST_DELEGATE;
+        continue;
+      }
+      double *y = sbase + q * per_sig;
+      double *xv = y + 2 * n + kw * kw + 2 * kw;
+      int *sup = (int *)(xv + 2 * kw);
+      int64_t *out_sel = a.out_sel + p * kw;
+      double *out_coef = a.out_coef + p * kw;
+      for (int j = lane; j < kw; j += 32) {
+        out_sel[j] = j < kdone[q] ? sup[j] : -1;
+        out_coef[j] = j < kdone[q] ? xv[j] : 0.0;
+      }
+      if (lane == 0) {
+        a.out_count[p] = kdone[q];
+        a.out_rnorm[p] = rnorm[q];
+        a.out_scans[p] = scans[q];
+        a.out_flag[p] = 0;
+      }
     }
     __syncwarp();
   }
@@ -212,8 +261,8 @@ __global__ void __launch_bounds__(1024, 1)
 template <typename YT, int U>
 cudaError_t launch_u(const ResidentArgs &a, const YT *ys, int threads, size_t smem,
                      int grid, cudaStream_t stream) {
-  auto kern = a.cands.mode == 0 ? resident_omp_kernel<YT, U, true>
-                                : resident_omp_kernel<YT, U, false>;
+  auto kern = a.cands.mode == 0 ? resident_omp_kernel<YT, U, true, RES_R>
+                                : resident_omp_kernel<YT, U, false, RES_R>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, threads, smem, stream>>>(a, ys);
@@ -250,7 +299,7 @@ bool resident_fits(int64_t n, int64_t t, int64_t kw, int64_t max_cands, int smem
   if (max_cands > 512) return false;
   const int64_t tp = resident_tpad(t, max_cands);
   const int64_t base = 8 * (n * tp + tp);
-  const int64_t per = 8 * resident_warp_doubles(n, kw, max_cands);
+  const int64_t per = 8 * resident_warp_doubles(n, kw, max_cands) * RES_R;
   return base + 4 * per <= smem_optin && base <= 144 * 1024;
 }
 
@@ -263,13 +312,13 @@ cudaError_t launch_resident(const ResidentArgs &args, const void *ys, bool ys_f3
   a.t_pad = resident_tpad(a.t, a.max_cands);
   if (a.cands.mode == 0 && a.t_pad < 32 * ((a.max_cands + 31) / 32)) return cudaErrorInvalidValue;
   const int64_t base = 8 * (a.n * a.t_pad + a.t_pad);
-  int warps = (int)((smem_optin - base) / (8 * a.per_warp));
-  if (warps > 32) warps = 32;
+  int warps = (int)((smem_optin - base) / (8 * a.per_warp * RES_R));
+  if (warps > RES_WARPS) warps = RES_WARPS;
   if (warps < 1) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)(base + 8 * a.per_warp * warps);
+  const size_t smem = (size_t)(base + 8 * a.per_warp * RES_R * warps);
   int u = 1;
   while (32 * u < a.max_cands) u *= 2;
-  int64_t grid = (a.p + warps - 1) / warps;
+  int64_t grid = (a.p + warps * RES_R - 1) / (warps * RES_R);
   if (grid > num_sms) grid = num_sms;
   note_launch();
   if (ys_f32) return launch_t<float>(a, (const float *)ys, u, warps * 32, smem, (int)grid, stream);

@@ -233,14 +233,25 @@ __global__ void __launch_bounds__(THREADS, 1)
           // bits replaced by the tile-local column (truncation <= 2^-15 rel.)
           uint32_t c1 = 0u, c2 = 0u, rest = 0u;
           const int jbase = tt * BN + c;
+          if (jbase + 32 <= t) {
 #pragma unroll
-          for (int i = 0; i < 32; i++) {
-            uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFF00u) | (uint32_t)(c + i);
-            key = (jbase + i < t) ? key : 0u;
-            const uint32_t m = min(c1, key);
-            c1 = max(c1, key);
-            rest = max(rest, min(c2, m));
-            c2 = max(c2, m);
+            for (int i = 0; i < 32; i++) {
+              const uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFF00u) | (uint32_t)(c + i);
+              const uint32_t m = min(c1, key);
+              c1 = max(c1, key);
+              rest = max(rest, min(c2, m));
+              c2 = max(c2, m);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFF00u) | (uint32_t)(c + i);
+              key = (jbase + i < t) ? key : 0u;
+              const uint32_t m = min(c1, key);
+              c1 = max(c1, key);
+              rest = max(rest, min(c2, m));
+              c2 = max(c2, m);
+            }
           }
           dropped = fmaxf(dropped, __uint_as_float(rest & 0xFFFFFF00u));
           if (c1) list_insert(val, idx, dropped, __uint_as_float(c1 & 0xFFFFFF00u),
@@ -598,9 +609,9 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
 }
 
 // Exact fp64 argmax over every non-taken atom for the queued signals: one
-// CTA per signal; the signal, its coefficients and a taken-atom bit mask sit
-// in shared memory; each warp streams 8 atom rows at a time with coalesced
-// loads (c_j = <d_j, y> - sum_s G[j, s] x_s, as in ls_step).
+// CTA per signal; the exact residual r = y - D64_S x, the coefficients and a
+// taken-atom bit mask sit in shared memory; each warp streams 8 atom rows at
+// a time with coalesced loads (c_j = <d_j, r>).
 template <typename YT>
 __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
                                                      const double *__restrict__ d64,
@@ -633,6 +644,13 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
       atomicOr(&taken[j >> 5], 1u << (j & 31));
     }
     __syncthreads();
+    // r = y - D64_S x, exact fp64, once per signal (then plain dots)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      double ri = y[i];
+      for (int64_t l = 0; l < k; l++) ri = fma(-x[l], __ldg(d64 + sel[l] * n + i), ri);
+      y[i] = ri;  // y now holds r
+    }
+    __syncthreads();
     double best = -1.0, cbest = 0.0;
     int64_t bestj = -1;
     for (int64_t j0 = (int64_t)warp * 8; j0 < t; j0 += 64) {
@@ -643,17 +661,13 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
 #pragma unroll
       for (int r = 0; r < 8; r++) acc[r] = 0.0;
       for (int64_t i = lane; i < n; i += 32) {
-        const double yi = y[i];
+        const double ri = y[i];
 #pragma unroll
-        for (int r = 0; r < 8; r++) acc[r] = fma(__ldg(rows[r] + i), yi, acc[r]);
+        for (int r = 0; r < 8; r++) acc[r] = fma(__ldg(rows[r] + i), ri, acc[r]);
       }
 #pragma unroll
       for (int r = 0; r < 8; r++) {
         const int64_t j = j0 + r;
-        if (j < t) {
-          const double *gj = gram + j * t;
-          for (int64_t s = lane; s < k; s += 32) acc[r] = fma(-__ldg(gj + sel[s]), x[s], acc[r]);
-        }
         const double cj = warp_sum(acc[r]);
         if (j < t && !((taken[j >> 5] >> (j & 31)) & 1u)) {
           const double v = fabs(cj);
