@@ -371,16 +371,29 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
   }
 }
 
-// exact c_j = <d_j, y> - sum_s G[j, s] x_s  (fp64; the whole warp)
+// exact c_j = <d_j, y> - sum_s G[j, s] x_s  (fp64; the whole warp).  The
+// gathered G[j, S] entries stay in the caller's registers (g0: s = lane,
+// g1: s = lane + 32) so the winner's row is reused by the Cholesky update.
 __device__ __forceinline__ double exact_corr(const double *__restrict__ d64,
-                                             const double *__restrict__ gram, int64_t t, int64_t n,
+                                             const double *__restrict__ gram, int64_t t, int n,
                                              int64_t j, const double *y, const int64_t *sel,
-                                             const double *x, int64_t k, int lane) {
+                                             const double *x, int k, int lane, double &g0,
+                                             double &g1) {
   const double *dj = d64 + j * n;
-  double acc = 0.0;
-  for (int64_t i = lane; i < n; i += 32) acc = fma(__ldg(dj + i), y[i], acc);
   const double *gj = gram + j * t;
-  for (int64_t s = lane; s < k; s += 32) acc = fma(-__ldg(gj + sel[s]), x[s], acc);
+  g0 = lane < k ? __ldg(gj + sel[lane]) : 0.0;
+  g1 = lane + 32 < k ? __ldg(gj + sel[lane + 32]) : 0.0;
+  double acc = 0.0, acc2 = 0.0;
+  int i = lane;
+  for (; i + 32 < n; i += 64) {
+    acc = fma(__ldg(dj + i), y[i], acc);
+    acc2 = fma(__ldg(dj + i + 32), y[i + 32], acc2);
+  }
+  if (i < n) acc = fma(__ldg(dj + i), y[i], acc);
+  acc += acc2;
+  acc = fma(-g0, lane < k ? x[lane] : 0.0, acc);
+  acc = fma(-g1, lane + 32 < k ? x[lane + 32] : 0.0, acc);
+  for (int s = lane + 64; s < k; s += 32) acc = fma(-__ldg(gj + sel[s]), x[s], acc);
   return warp_sum(acc);
 }
 
@@ -392,14 +405,16 @@ constexpr uint32_t ST_RESCAN = 4u;  // pick needs the exact full rescan
 __device__ void ls_update(const double *__restrict__ d64, const float *__restrict__ d32,
                           const double *__restrict__ gram, int64_t sig, int64_t t, int64_t n,
                           int64_t n_pad, int64_t k_max, int64_t kw, int iter, double dmax,
-                          TensorState &st, int64_t *sel, double *out_coef, int64_t *out_count,
+                          TensorState &st, int64_t *sel, int64_t *ssel, double *out_coef,
+                          int64_t *out_count,
                           int64_t bestj, double cbest, double *lin, double *wv, double *xv,
-                          double *gv, double *zv, const double *y, int lane) {
+                          double *gv, double *zv, const double *y, int lane, double g0, double g1) {
   const int64_t k = iter;
   const double *grow = gram + bestj * t;
-  for (int64_t i = lane; i < k * kw; i += 32) lin[i] = st.linv[sig * kw * kw + i];
-  for (int64_t i = lane; i < k; i += 32) gv[i] = __ldg(grow + sel[i]);
   const double gnn = __ldg(grow + bestj);
+  if (lane < k) gv[lane] = g0;
+  if (lane + 32 < k) gv[lane + 32] = g1;
+  for (int64_t i = lane + 64; i < k; i += 32) gv[i] = __ldg(grow + sel[i]);
   __syncwarp();
   for (int64_t l = lane; l < k; l += 32) {
     double acc = 0.0;
@@ -434,6 +449,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
     zv[k] = zk;
     st.z[sig * kw + k] = zk;
     sel[k] = bestj;
+    ssel[k] = bestj;
   }
   __syncwarp();
   const int64_t kd = k + 1;
@@ -455,7 +471,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
     double rr = 0.0;
     for (int64_t i = lane; i < n; i += 32) {
       double ri = y[i];
-      for (int64_t l = 0; l < kd; l++) ri = fma(-xv[l], __ldg(d64 + sel[l] * n + i), ri);
+      for (int64_t l = 0; l < kd; l++) ri = fma(-xv[l], __ldg(d64 + ssel[l] * n + i), ri);
       rr = fma(ri, ri, rr);
     }
     stop = sqrt(warp_sum(rr)) <= tol;
@@ -478,8 +494,23 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
       const int64_t i = i0 + u * 32 + lane;
       acc[u] = i < n ? y[i] : 0.0;
     }
-    for (int64_t l = 0; l < kd; l++) {
-      const float *row = d32 + sel[l] * n;
+    int64_t l = 0;
+    for (; l + 1 < kd; l += 2) {  // two support atoms per step: 16 loads in flight
+      const float *row0 = d32 + ssel[l] * n;
+      const float *row1 = d32 + ssel[l + 1] * n;
+      const double x0 = xv[l], x1 = xv[l + 1];
+      float v0[8], v1[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int64_t i = i0 + u * 32 + lane;
+        v0[u] = i < n ? __ldg(row0 + i) : 0.0f;
+        v1[u] = i < n ? __ldg(row1 + i) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc[u] = fma(-x1, (double)v1[u], fma(-x0, (double)v0[u], acc[u]));
+    }
+    if (l < kd) {
+      const float *row = d32 + ssel[l] * n;
       const double xl = xv[l];
 #pragma unroll
       for (int u = 0; u < 8; u++) {
@@ -510,14 +541,14 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
 // resume == 0: certify the scan's candidates; resume == 1: take the pick
 // the exact rescan produced for the signals listed in st.pending.
 template <typename YT>
-__global__ void __launch_bounds__(256) ls_step_kernel(
+__global__ void __launch_bounds__(256, 3) ls_step_kernel(
     const YT *__restrict__ ys, const double *__restrict__ d64, const float *__restrict__ d32,
     const double *__restrict__ gram, int64_t p, int64_t t, int64_t n, int64_t n_pad,
     int64_t k_max, int64_t kw, int iter, double c_err, double dmax, TensorState st,
     int64_t *out_sel, double *out_coef, int64_t *out_count, int64_t *out_scans, int resume) {
   extern __shared__ double lsm[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t per_warp = kw * kw + 4 * kw + n;
+  const int64_t per_warp = kw * kw + 5 * kw + n;
   double *lin = lsm + wib * per_warp;  // L^{-1} rows (row-major)
   double *wv = lin + kw * kw;          // w
   double *xv = wv + kw;                // x (current coefficients)
@@ -532,32 +563,45 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
   for (int64_t e = wid; e < count; e += nw) {
     const int64_t sig = resume ? st.pending[e] : e;
     if (!resume && (st.status[sig] & (ST_DONE | ST_DELEGATE))) continue;
-    int64_t *sel = out_sel + sig * kw;
+    int64_t *sel = out_sel + sig * kw;  // global (written for the new atom)
+    int64_t *ssel = (int64_t *)(y + n); // smem copy of the support ids
+    // ---- independent loads first: signal, coefficients, z, support, L^{-1}, candidates
+    int cidx = -1;
+    float cval = -1.0f;
+    if (!resume && lane < NCAND) {
+      cidx = st.cand_idx[sig * NCAND + lane];
+      cval = st.cand_val[sig * NCAND + lane];
+    }
+    const float cdrop = resume ? 0.0f : st.cand_drop[sig];
+    const double rt = st.rt[sig], drs = st.dr[sig];
     for (int64_t i = lane; i < n; i += 32) y[i] = (double)ys[sig * n + i];
     for (int64_t i = lane; i < k; i += 32) {
       xv[i] = out_coef[sig * kw + i];
       zv[i] = st.z[sig * kw + i];
+      ssel[i] = sel[i];
     }
+    for (int64_t i = lane; i < k * kw; i += 32) lin[i] = st.linv[sig * kw * kw + i];
     __syncwarp();
-    double best = -1.0, cbest = 0.0;
+    double best = -1.0, cbest = 0.0, bg0 = 0.0, bg1 = 0.0;
     int64_t bestj = -1;
     if (resume) {
       bestj = st.rs_j[sig];
       cbest = st.rs_c[sig];
       best = fabs(cbest);
       if (lane == 0) st.status[sig] &= ~ST_RESCAN;
+      if (bestj >= 0) {
+        const double *grow = gram + bestj * t;
+        bg0 = lane < k ? __ldg(grow + ssel[lane]) : 0.0;
+        bg1 = lane + 32 < k ? __ldg(grow + ssel[lane + 32]) : 0.0;
+      }
     } else {
       // ---- candidates: drop taken atoms; rigorous bound E of the bf16 scan
-      int cidx = -1;
-      float cval = -1.0f;
       if (lane < NCAND) {
-        cidx = st.cand_idx[sig * NCAND + lane];
-        cval = st.cand_val[sig * NCAND + lane];
         for (int64_t i = 0; i < k && cidx >= 0; i++)
-          if (sel[i] == cidx) cidx = -1;
+          if (ssel[i] == cidx) cidx = -1;
         if (cidx < 0) cval = -1.0f;
       }
-      const double E = (c_err * st.rt[sig] + st.dr[sig]) * dmax;
+      const double E = (c_err * rt + drs) * dmax;
       double best_apx = (double)cval;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
@@ -568,23 +612,21 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
         unscored = fmax(unscored, __shfl_xor_sync(CDB_FULL_MASK, unscored, o));
-      unscored = fmax(unscored, (double)st.cand_drop[sig]);
+      unscored = fmax(unscored, (double)cdrop);
       for (unsigned m = rmask; m; m &= m - 1) {
         const int c = __ffs(m) - 1;
         const int64_t j = __shfl_sync(CDB_FULL_MASK, cidx, c);
-        const double cj = exact_corr(d64, gram, t, n, j, y, sel, xv, k, lane);
+        double g0, g1;
+        const double cj = exact_corr(d64, gram, t, (int)n, j, y, ssel, xv, (int)k, lane, g0, g1);
         const double v = fabs(cj);
         if (v > best || (v == best && j < bestj)) {
           best = v;
           bestj = j;
           cbest = cj;
+          bg0 = g0;
+          bg1 = g1;
         }
       }
-      if (sig == st.debug_sig && lane == 0)
-        printf("[ls dbg] sig %lld k %lld E %.6g rt %.6g dr %.6g best_apx %.6g unscored %.6g "
-               "best %.6g bestj %lld cbest %.6g rmask %x drop %.6g\n",
-               (long long)sig, (long long)k, E, st.rt[sig], st.dr[sig], best_apx, unscored, best,
-               (long long)bestj, cbest, rmask, (double)st.cand_drop[sig]);
       if (bestj < 0 || !(unscored + E < best)) {
         // uncertifiable: queue for the CTA-wide exact rescan, resume later
         if (lane == 0) {
@@ -602,8 +644,8 @@ __global__ void __launch_bounds__(256) ls_step_kernel(
       __syncwarp();
       continue;
     }
-    ls_update(d64, d32, gram, sig, t, n, n_pad, k_max, kw, iter, dmax, st, sel, out_coef,
-              out_count, bestj, cbest, lin, wv, xv, gv, zv, y, lane);
+    ls_update(d64, d32, gram, sig, t, n, n_pad, k_max, kw, iter, dmax, st, sel, ssel, out_coef,
+              out_count, bestj, cbest, lin, wv, xv, gv, zv, y, lane, bg0, bg1);
     __syncwarp();
   }
 }
@@ -831,7 +873,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     const int c = atoi(cap);
     if (c > 0 && (unsigned)c < corr_grid) corr_grid = (unsigned)c;
   }
-  const int64_t ls_per_warp = (int64_t)sizeof(double) * (kw * kw + 4 * kw + n);
+  const int64_t ls_per_warp = (int64_t)sizeof(double) * (kw * kw + 5 * kw + n);
   int ls_wpb = (int)((160 * 1024) / ls_per_warp);
   if (ls_wpb > 8) ls_wpb = 8;
   if (ls_wpb < 1) ls_wpb = 1;
