@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <algorithm>
 
 #include "../../include/crossdict_b200.h"
 #include "engines.h"
@@ -309,6 +310,7 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
     CDB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(uint32_t) * p, st));
     cdb::ResidentArgs r{};
     r.d64 = d->d64;
+    r.gram = d->gram;
     r.t = d->t;
     r.n = d->n;
     r.p = p;
@@ -371,6 +373,98 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, max_cands, o,
                           status.as<uint32_t>(), di, st);
 }
+
+
+// ---------------------------------------------------------------- host-buffer pipelining
+// Row-major per-signal arrays crossing the host boundary: the batch is coded
+// in chunks; chunk i+1's inputs are copied H2D and chunk i-1's outputs D2H on
+// a copy stream while chunk i computes on the caller's stream (two device
+// buffer sets, events order the reuse).  Requires pinned host memory for the
+// copies to be asynchronous; pageable memory still works (staged by CUDA).
+struct RowArr {
+  void *host;        // host base pointer (or device, then passed through)
+  size_t row_bytes;  // bytes per signal
+  bool out;          // output (D2H) or input (H2D)
+};
+
+cudaStream_t copy_stream() {
+  static thread_local cudaStream_t cs = nullptr;
+  static thread_local int dev = -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (!cs || dev != cur) {
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    dev = cur;
+  }
+  return cs;
+}
+
+template <typename Core>
+cdb_status run_pipelined(int64_t p, int64_t chunk, std::vector<RowArr> &arrs, cudaStream_t st,
+                         Core core) {
+  const int64_t nch = (p + chunk - 1) / chunk;
+  cudaStream_t cs = copy_stream();
+  const size_t na = arrs.size();
+  std::vector<DevBuf> bufs(2 * na);
+  for (int b = 0; b < 2; b++)
+    for (size_t a = 0; a < na; a++)
+      CDB_CUDA(bufs[b * na + a].alloc(arrs[a].row_bytes * chunk, st));
+  CDB_CUDA(cudaStreamSynchronize(st));  // buffers allocated before the copy stream uses them
+  cudaEvent_t in_ready[2], done[2];
+  for (int b = 0; b < 2; b++) {
+    CDB_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
+    CDB_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+  }
+  auto h2d = [&](int64_t i) -> cudaError_t {
+    const int b = (int)(i & 1);
+    const int64_t off = i * chunk, len = std::min(chunk, p - off);
+    for (size_t a = 0; a < na; a++) {
+      if (arrs[a].out || !arrs[a].host) continue;
+      cudaError_t e = cudaMemcpyAsync(bufs[b * na + a].ptr,
+                                      (const uint8_t *)arrs[a].host + off * arrs[a].row_bytes,
+                                      len * arrs[a].row_bytes, cudaMemcpyHostToDevice, cs);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaEventRecord(in_ready[b], cs);
+  };
+  CDB_CUDA(h2d(0));
+  for (int64_t i = 0; i < nch; i++) {
+    const int b = (int)(i & 1);
+    const int64_t off = i * chunk, len = std::min(chunk, p - off);
+    if (i + 1 < nch) CDB_CUDA(h2d(i + 1));
+    CDB_CUDA(cudaStreamWaitEvent(st, in_ready[b], 0));
+    std::vector<void *> dev(na);
+    for (size_t a = 0; a < na; a++) dev[a] = bufs[b * na + a].ptr;
+    cdb_status s = core(off, len, dev, st);
+    if (s != CDB_OK) return s;
+    CDB_CUDA(cudaEventRecord(done[b], st));
+    CDB_CUDA(cudaStreamWaitEvent(cs, done[b], 0));
+    for (size_t a = 0; a < na; a++) {
+      if (!arrs[a].out || !arrs[a].host) continue;
+      CDB_CUDA(cudaMemcpyAsync((uint8_t *)arrs[a].host + off * arrs[a].row_bytes, dev[a],
+                               len * arrs[a].row_bytes, cudaMemcpyDeviceToHost, cs));
+    }
+  }
+  CDB_CUDA(cudaStreamSynchronize(cs));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < 2; b++) {
+    cudaEventDestroy(in_ready[b]);
+    cudaEventDestroy(done[b]);
+  }
+  return CDB_OK;
+}
+
+void dev_outs(Outs &o, void *sel, void *coef, void *count, void *rnorm, void *scans,
+              void *flag) {
+  o.sel.dev = sel;
+  o.coef.dev = coef;
+  o.count.dev = count;
+  o.rnorm.dev = rnorm;
+  o.scans.dev = scans;
+  o.flag.dev = flag;
+}
+
+constexpr int64_t kPipeMin = 32768;  // pipeline host-buffer calls from this many signals
 
 }  // namespace
 
@@ -571,6 +665,32 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
   cudaStream_t st = (cudaStream_t)stream;
   const bool f32 = ys_is_f32 != 0;
   const int64_t n = dict->n;
+  const int64_t max_c0 = mode == 0 ? dict->t : (mode == 1 ? stride : stride * q);
+  const bool host_io = !is_device_ptr(ys) || !is_device_ptr(out_sel) || !is_device_ptr(out_coef);
+  if (host_io && p >= kPipeMin && !is_device_ptr(ys) && !is_device_ptr(eps)) {
+    std::vector<RowArr> arrs = {
+        {(void *)ys, (size_t)(f32 ? 4 : 8) * n, false}, {(void *)eps, sizeof(double), false},
+        {(void *)ids, sizeof(int64_t) * (mode ? stride : 0) + (mode ? 0 : 8), false},
+        {out_sel, sizeof(int64_t) * k_max, true}, {out_coef, sizeof(double) * k_max, true},
+        {out_count, sizeof(int64_t), true}, {out_rnorm, sizeof(double), true},
+        {out_scans, sizeof(int64_t), true}, {out_flag, sizeof(uint8_t), true}};
+    if (!mode) arrs[2].host = nullptr;
+    const int64_t chunk = std::max<int64_t>(kPipeMin, (p + 3) / 4);
+    return run_pipelined(p, chunk, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
+                                                 cudaStream_t s2) -> cdb_status {
+      cdb::Cands c{};
+      c.mode = mode;
+      c.t = dict->t;
+      c.ids = (const int64_t *)dv[2];
+      c.stride = stride;
+      c.q = q;
+      c.nb_fixed = stride;
+      Outs o;
+      dev_outs(o, dv[3], dv[4], dv[5], dv[6], dv[7], dv[8]);
+      return run_omp(dict, dv[0], f32, len, k_max, k_max, (const double *)dv[1], c, max_c0, o,
+                     engine, di, s2);
+    });
+  }
   InArr y_in, e_in, id_in;
   CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
   CDB_CUDA(e_in.bind(eps, sizeof(double) * p, st));
@@ -616,6 +736,85 @@ cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int
                     out_count, out_rnorm, out_scans, out_flag, engine, stream);
 }
 
+static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary *high,
+                                 const int64_t *fine_shape, const int64_t *factors, int rank,
+                                 const void *ydev, bool f32, int64_t p, int64_t k1,
+                                 int64_t k_high, double rel_tol, int phi_mode, Outs &lo, Outs &hi,
+                                 int engine, float *step_ms, const DevInfo &di, cudaStream_t st) {
+  const int64_t n = high->n, q = high->t / low->t;
+  cudaEvent_t ev[3];
+  for (auto &e : ev) CDB_CUDA(cudaEventCreate(&e));
+  CDB_CUDA(cudaEventRecord(ev[0], st));
+
+  // ---- step 1: W y (identity) or y (Phi), tolerance relative to it
+  DevBuf ylow, eps1, eps2, blocks;
+  const void *y1 = ydev;
+  bool y1_f32 = f32;
+  if (!phi_mode) {
+    int64_t n_low = 1;
+    for (int d = 0; d < rank; d++) n_low *= fine_shape[d] / factors[d];
+    if (n_low != low->n) return fail(CDB_ERR_ARG, "coarse size != low dictionary dim");
+    CDB_CUDA(ylow.alloc(sizeof(double) * p * n_low, st));
+    CDB_CUDA(cdb::launch_downsample(ydev, f32, p, n, fine_shape, factors, rank,
+                                    ylow.as<double>(), n_low, st));
+    y1 = ylow.ptr;
+    y1_f32 = false;
+  }
+  CDB_CUDA(eps1.alloc(sizeof(double) * p, st));
+  CDB_CUDA(cdb::launch_row_tol(y1, y1_f32, p, low->n, rel_tol, eps1.as<double>(), st));
+  cdb::Cands c1{};
+  c1.mode = 0;
+  c1.t = low->t;
+  cdb_status s = run_omp(low, y1, y1_f32, p, k1, k1, eps1.as<double>(), c1, low->t, lo, engine, di,
+                         st, "gram_step1");
+  if (s != CDB_OK) return s;
+  CDB_CUDA(cudaEventRecord(ev[1], st));
+
+  // ---- step 2: restricted to the children of the sorted coarse support
+  CDB_CUDA(blocks.alloc(sizeof(int64_t) * p * k1, st));
+  CDB_CUDA(cdb::launch_sort_blocks((const int64_t *)lo.sel.dev, (const int64_t *)lo.count.dev, p,
+                                   k1, blocks.as<int64_t>(), st));
+  CDB_CUDA(eps2.alloc(sizeof(double) * p, st));
+  CDB_CUDA(cdb::launch_row_tol(ydev, f32, p, n, rel_tol, eps2.as<double>(), st));
+  cdb::Cands c2{};
+  c2.mode = 2;
+  c2.t = high->t;
+  c2.ids = blocks.as<int64_t>();
+  c2.stride = k1;
+  c2.q = q;
+  c2.nb = (const int64_t *)lo.count.dev;
+  c2.clip = 1;
+  // the Gram engine gets its alpha0 = <d_C, y> from the parent-routed kernel
+  DevBuf alpha0, rwork;
+  const bool high_resident =
+      cdb::resident_fits(high->n, high->t, k_high, k1 * q, di.smem_optin) &&
+      (engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_RESIDENT);
+  const bool use_route = high->gram && !high_resident && engine != CDB_ENGINE_EXACT &&
+                         high->t / q == low->t && 8 * q * n <= 192 * 1024 &&
+                         (q == 1 || q == 2 || q == 4 || q == 8 || q == 16);
+  if (use_route) {
+    CDB_CUDA(alpha0.alloc(sizeof(double) * p * k1 * q, st));
+    CDB_CUDA(rwork.alloc((size_t)cdb::route_work_bytes(low->t, p, k1), st));
+    CDB_CUDA(cdb::launch_route_alpha0(high->d64, low->t, n, q, ydev, f32, blocks.as<int64_t>(),
+                                      (const int64_t *)lo.count.dev, p, k1, k1 * q,
+                                      alpha0.as<double>(), rwork.ptr, st));
+  }
+  s = run_omp(high, ydev, f32, p, k_high, k_high, eps2.as<double>(), c2, k1 * q, hi, engine, di,
+              st, "gram_step2", use_route ? alpha0.as<double>() : nullptr);
+  if (s != CDB_OK) return s;
+  CDB_CUDA(cudaEventRecord(ev[2], st));
+  CDB_CUDA(cudaEventSynchronize(ev[2]));
+  if (step_ms) {
+    float a = 0.0f, b = 0.0f;
+    CDB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    CDB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    step_ms[0] += a;
+    step_ms[1] += b;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  return CDB_OK;
+}
+
 cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *high,
                                const int64_t *fine_shape, const int64_t *factors, int rank,
                                const void *ys, int ys_is_f32, int64_t p, int64_t k1,
@@ -636,81 +835,39 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   if (s0 != CDB_OK) return s0;
   cudaStream_t st = (cudaStream_t)stream;
   const bool f32 = ys_is_f32 != 0;
-  const int64_t n = high->n, q = high->t / low->t;
+  const int64_t n = high->n;
+  if (step_ms) step_ms[0] = step_ms[1] = 0.0f;
+  const bool host_io = !is_device_ptr(ys) || !is_device_ptr(high_sel) || !is_device_ptr(low_sel);
+  if (host_io && p >= kPipeMin && !is_device_ptr(ys)) {
+    std::vector<RowArr> arrs = {
+        {(void *)ys, (size_t)(f32 ? 4 : 8) * n, false},
+        {low_sel, sizeof(int64_t) * k1, true}, {low_coef, sizeof(double) * k1, true},
+        {low_count, sizeof(int64_t), true}, {low_rnorm, sizeof(double), true},
+        {low_scans, sizeof(int64_t), true}, {low_flag, sizeof(uint8_t), true},
+        {high_sel, sizeof(int64_t) * k_high, true}, {high_coef, sizeof(double) * k_high, true},
+        {high_count, sizeof(int64_t), true}, {high_rnorm, sizeof(double), true},
+        {high_scans, sizeof(int64_t), true}, {high_flag, sizeof(uint8_t), true}};
+    const int64_t chunk = std::max<int64_t>(kPipeMin, (p + 3) / 4);
+    return run_pipelined(p, chunk, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
+                                                 cudaStream_t s2) -> cdb_status {
+      Outs lo, hi;
+      dev_outs(lo, dv[1], dv[2], dv[3], dv[4], dv[5], dv[6]);
+      dev_outs(hi, dv[7], dv[8], dv[9], dv[10], dv[11], dv[12]);
+      return zero_tree_core(low, high, fine_shape, factors, rank, dv[0], f32, len, k1, k_high,
+                            rel_tol, phi_mode, lo, hi, engine, step_ms, di, s2);
+    });
+  }
   InArr y_in;
   CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
   Outs lo, hi;
   CDB_CUDA(lo.bind(p, k1, low_sel, low_coef, low_count, low_rnorm, low_scans, low_flag, st));
   CDB_CUDA(hi.bind(p, k_high, high_sel, high_coef, high_count, high_rnorm, high_scans, high_flag, st));
-  cudaEvent_t ev[3];
-  for (auto &e : ev) CDB_CUDA(cudaEventCreate(&e));
-  CDB_CUDA(cudaEventRecord(ev[0], st));
-
-  // ---- step 1: W y (identity) or y (Phi), tolerance relative to it
-  DevBuf ylow, eps1, eps2, blocks;
-  const void *y1 = y_in.dev;
-  bool y1_f32 = f32;
-  if (!phi_mode) {
-    int64_t n_low = 1;
-    for (int d = 0; d < rank; d++) n_low *= fine_shape[d] / factors[d];
-    if (n_low != low->n) return fail(CDB_ERR_ARG, "coarse size != low dictionary dim");
-    CDB_CUDA(ylow.alloc(sizeof(double) * p * n_low, st));
-    CDB_CUDA(cdb::launch_downsample(y_in.dev, f32, p, n, fine_shape, factors, rank,
-                                    ylow.as<double>(), n_low, st));
-    y1 = ylow.ptr;
-    y1_f32 = false;
-  }
-  CDB_CUDA(eps1.alloc(sizeof(double) * p, st));
-  CDB_CUDA(cdb::launch_row_tol(y1, y1_f32, p, low->n, rel_tol, eps1.as<double>(), st));
-  cdb::Cands c1{};
-  c1.mode = 0;
-  c1.t = low->t;
-  cdb_status s = run_omp(low, y1, y1_f32, p, k1, k1, eps1.as<double>(), c1, low->t, lo, engine, di,
-                         st, "gram_step1");
+  cdb_status s = zero_tree_core(low, high, fine_shape, factors, rank, y_in.dev, f32, p, k1, k_high,
+                                rel_tol, phi_mode, lo, hi, engine, step_ms, di, st);
   if (s != CDB_OK) return s;
-  CDB_CUDA(cudaEventRecord(ev[1], st));
-
-  // ---- step 2: restricted to the children of the sorted coarse support
-  CDB_CUDA(blocks.alloc(sizeof(int64_t) * p * k1, st));
-  CDB_CUDA(cdb::launch_sort_blocks((const int64_t *)lo.sel.dev, (const int64_t *)lo.count.dev, p,
-                                   k1, blocks.as<int64_t>(), st));
-  CDB_CUDA(eps2.alloc(sizeof(double) * p, st));
-  CDB_CUDA(cdb::launch_row_tol(y_in.dev, f32, p, n, rel_tol, eps2.as<double>(), st));
-  cdb::Cands c2{};
-  c2.mode = 2;
-  c2.t = high->t;
-  c2.ids = blocks.as<int64_t>();
-  c2.stride = k1;
-  c2.q = q;
-  c2.nb = (const int64_t *)lo.count.dev;
-  c2.clip = 1;
-  // the Gram engine gets its alpha0 = <d_C, y> from the parent-routed kernel
-  DevBuf alpha0, rwork;
-  const bool high_resident =
-      cdb::resident_fits(high->n, high->t, k_high, k1 * q, di.smem_optin) &&
-      (engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_RESIDENT);
-  const bool use_route = high->gram && !high_resident && engine != CDB_ENGINE_EXACT &&
-                         high->t / q == low->t && 8 * q * n <= 192 * 1024 &&
-                         (q == 1 || q == 2 || q == 4 || q == 8 || q == 16);
-  if (use_route) {
-    CDB_CUDA(alpha0.alloc(sizeof(double) * p * k1 * q, st));
-    CDB_CUDA(rwork.alloc((size_t)cdb::route_work_bytes(low->t, p, k1), st));
-    CDB_CUDA(cdb::launch_route_alpha0(high->d64, low->t, n, q, y_in.dev, f32, blocks.as<int64_t>(),
-                                      (const int64_t *)lo.count.dev, p, k1, k1 * q,
-                                      alpha0.as<double>(), rwork.ptr, st));
-  }
-  s = run_omp(high, y_in.dev, f32, p, k_high, k_high, eps2.as<double>(), c2, k1 * q, hi, engine, di,
-              st, "gram_step2", use_route ? alpha0.as<double>() : nullptr);
-  if (s != CDB_OK) return s;
-  CDB_CUDA(cudaEventRecord(ev[2], st));
   CDB_CUDA(lo.finish(st));
   CDB_CUDA(hi.finish(st));
   CDB_CUDA(cudaStreamSynchronize(st));
-  if (step_ms) {
-    CDB_CUDA(cudaEventElapsedTime(&step_ms[0], ev[0], ev[1]));
-    CDB_CUDA(cudaEventElapsedTime(&step_ms[1], ev[1], ev[2]));
-  }
-  for (auto &e : ev) cudaEventDestroy(e);
   return CDB_OK;
 }
 

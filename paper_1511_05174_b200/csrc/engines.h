@@ -75,6 +75,7 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
 // ---------------------------------------------------------------- resident
 struct ResidentArgs {
   const double *d64;     // T x N fp64 atoms (rows)
+  const double *gram;    // T x T fp64 Gram matrix (optional)
   int64_t t, n;
   int64_t p;
   int64_t k_max, k_width;

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   int kdone = 0;
   int64_t scans = 0;
   double rnorm = ynorm;
+  double rn2_final = 0.0, yy_final = 1.0;
   bool delegate = false;
 
   if (!(ynorm <= tol) && k_max > 0) {
@@ -156,11 +157,13 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
     for (int i = lane; i < n; i += 32) yy = fma(s.y[i], s.y[i], yy);
     yy = warp_sum(yy);
     double rn2 = yy;
+    yy_final = yy;
     const double tol2 = tol * tol;
     const double band = 1e-12 * yy;
     __syncwarp();
 
     for (int k = 0; k < k_max; k++) {
+      rn2_final = rn2;
       scans += S - k;
       // ---- selection: max |c_j| over non-taken, ties -> lowest index
       double best = -1.0;
@@ -186,7 +189,12 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
         }
       }
       if (bestj < 0 || best <= 0.0) break;
-      const int64_t nid = cs.id(p, bestj);
+      // the winner's atom id from the lane that owns it (no jl / q division)
+      int nid32 = 0;
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if ((bestj >> 5) == u) nid32 = cid[u];
+      const int64_t nid = __shfl_sync(CDB_FULL_MASK, nid32, bestj & 31);
       if (lane == 0) {
         s.taken[bestj >> 5] |= 1u << (bestj & 31);
         s.sup[k] = nid;
@@ -274,6 +282,7 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
         }
       }
       rn2 -= zk * zk;
+      rn2_final = rn2;
       kdone = k + 1;
       __syncwarp();
       // ---- stop test (_kernels.py:156), exact residual inside the band
@@ -310,13 +319,19 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   }
   __syncwarp();
   if (kdone > 0) {
-    double rr = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      double ri = s.y[i];
-      for (int l = 0; l < kdone; l++) ri = fma(-s.x[l], __ldg(a.d64 + s.sup[l] * n + i), ri);
-      rr = fma(ri, ri, rr);
+    // |r| = sqrt(|y|^2 - |z|^2) is accurate to ~1e-16 |y|^2 / |r|^2 relative;
+    // re-materialise the residual exactly only when that is not tight
+    if (rn2_final > 1e-6 * yy_final) {
+      rnorm = sqrt(rn2_final);
+    } else {
+      double rr = 0.0;
+      for (int i = lane; i < n; i += 32) {
+        double ri = s.y[i];
+        for (int l = 0; l < kdone; l++) ri = fma(-s.x[l], __ldg(a.d64 + s.sup[l] * n + i), ri);
+        rr = fma(ri, ri, rr);
+      }
+      rnorm = sqrt(warp_sum(rr));
     }
-    rnorm = sqrt(warp_sum(rr));
   }
   for (int j = lane; j < kw; j += 32) {
     out_sel[j] = j < kdone ? s.sup[j] : -1;

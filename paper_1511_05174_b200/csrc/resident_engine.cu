@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(512, 1)
 
   const Cands cs = a.cands;
   const double *eps = a.eps;
+  const double *gram = a.gram;
   double *sbase = wbase + warp * R * per_sig;
   for (int64_t p0 = ((int64_t)blockIdx.x * nwarps + warp) * R; p0 < P;
        p0 += (int64_t)gridDim.x * nwarps * R) {
@@ -169,12 +170,18 @@ __global__ void __launch_bounds__(512, 1)
           sup[k] = nid;
         }
         __syncwarp();
-        // ---- Cholesky append: g_l = <d_{s_l}, d_new> from the resident atoms
-        for (int l = lane; l < k; l += 32) {
-          double g = 0.0;
-          const int sl = sup[l];
-          for (int i = 0; i < n; i++) g = fma(Dt[i * Tp + sl], Dt[i * Tp + nid], g);
-          gv[l] = g;
+        // ---- Cholesky append: g_l = <d_{s_l}, d_new> (Gram row gather, or a
+        // dot over the resident atoms when no Gram matrix is staged)
+        if (gram) {
+          const double *grow = gram + (int64_t)nid * T;
+          for (int l = lane; l < k; l += 32) gv[l] = __ldg(grow + sup[l]);
+        } else {
+          for (int l = lane; l < k; l += 32) {
+            double g = 0.0;
+            const int sl = sup[l];
+            for (int i = 0; i < n; i++) g = fma(Dt[i * Tp + sl], Dt[i * Tp + nid], g);
+            gv[l] = g;
+          }
         }
         __syncwarp();
         for (int l = lane; l < k; l += 32) {
@@ -211,6 +218,7 @@ __global__ void __launch_bounds__(512, 1)
         kdone[q] = k + 1;
         for (int i = lane; i <= k; i += 32) {
           double accx = 0.0;
+#pragma unroll 4
           for (int l = i; l <= k; l++) accx = fma(lin[l * kw + i], zv[l], accx);
           xv[i] = accx;
         }
@@ -220,6 +228,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = lane; i < n; i += 32) {
           double rv = y[i];
           const double *row = Dt + i * Tp;
+#pragma unroll 4
           for (int l = 0; l <= k; l++) rv = fma(-xv[l], row[sup[l]], rv);
           r[i] = rv;
           rr = fma(rv, rv, rr);

@@ -125,3 +125,38 @@ def test_device_resident_inputs_match_host_inputs():
     for k in ("sel", "counts", "scans"):
         assert np.array_equal(ol[k], a_low[k]) and np.array_equal(oh[k], a_high[k])
     assert np.array_equal(oh["alpha"], a_high["alpha"])
+
+
+@pytest.mark.parametrize("kind", ["zt", "full"])
+def test_pipelined_host_buffers_match_device_buffers(kind):
+    # >= 32768 signals with host buffers take the chunked copy/compute pipeline
+    ci = 1
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    P = 70_000
+    ys = W.signals(ci, 0, P).astype(np.float32)
+    lo, hi = D.device_dictionary(d.low_t), D.device_dictionary(d.high_t)
+    yd = torch.from_numpy(ys).cuda()
+    mk = lambda k: dict(sel=torch.empty((P, k), dtype=torch.int64, device="cuda"),
+                        alpha=torch.empty((P, k), dtype=torch.float64, device="cuda"),
+                        counts=torch.empty(P, dtype=torch.int64, device="cuda"),
+                        rnorm=torch.empty(P, dtype=torch.float64, device="cuda"),
+                        scans=torch.empty(P, dtype=torch.int64, device="cuda"),
+                        flag=torch.empty(P, dtype=torch.uint8, device="cuda"))
+    if kind == "zt":
+        h_low, h_high, ms_h = D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, ys, P, w.k, w.k,
+                                              W.REL_TOL, False, "auto")
+        d_low, d_high = mk(w.k), mk(w.k)
+        D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, yd, P, w.k, w.k, W.REL_TOL, False, "auto",
+                        d_low, d_high)
+        pairs = [(h_low, _host(d_low)), (h_high, _host(d_high))]
+        assert ms_h[0] > 0 and ms_h[1] > 0
+    else:
+        eps = W.REL_TOL * np.linalg.norm(ys.astype(np.float64), axis=1)
+        h = D.omp_batch_raw(hi, ys, P, w.k, eps, None, "auto")
+        dd = mk(w.k)
+        D.omp_batch_raw(hi, yd, P, w.k, torch.from_numpy(eps).cuda(), None, "auto", dd)
+        pairs = [(h, _host(dd))]
+    for a, b in pairs:
+        for k in ("sel", "counts", "scans", "alpha", "rnorm"):
+            assert np.array_equal(a[k], b[k]), k
