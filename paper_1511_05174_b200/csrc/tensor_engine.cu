@@ -408,7 +408,8 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
                           TensorState &st, int64_t *sel, int64_t *ssel, double *out_coef,
                           int64_t *out_count,
                           int64_t bestj, double cbest, double *lin, double *wv, double *xv,
-                          double *gv, double *zv, const double *y, int lane, double g0, double g1) {
+                          double *gv, double *zv, const double *y, int lane, double g0, double g1,
+                          double rn2_prev, double tol, double yy) {
   const int64_t k = iter;
   const double *grow = gram + bestj * t;
   const double gnn = __ldg(grow + bestj);
@@ -461,11 +462,10 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
   }
   __syncwarp();
   // ---- stop test on |r|^2 = |y|^2 - |z|^2, exact residual inside the band
-  const double rn2 = st.rn2[sig] - zk * zk;
-  const double tol = st.tol[sig];
+  const double rn2 = rn2_prev - zk * zk;
   const double gap = rn2 - tol * tol;
   bool stop;
-  if (fabs(gap) > 1e-12 * st.yy[sig]) {
+  if (fabs(gap) > 1e-12 * yy) {
     stop = gap < 0.0;
   } else {
     double rr = 0.0;
@@ -574,6 +574,7 @@ __global__ void __launch_bounds__(256, 3) ls_step_kernel(
     }
     const float cdrop = resume ? 0.0f : st.cand_drop[sig];
     const double rt = st.rt[sig], drs = st.dr[sig];
+    const double rn2_prev = st.rn2[sig], tol_s = st.tol[sig], yy_s = st.yy[sig];
     for (int64_t i = lane; i < n; i += 32) y[i] = (double)ys[sig * n + i];
     for (int64_t i = lane; i < k; i += 32) {
       xv[i] = out_coef[sig * kw + i];
@@ -645,7 +646,298 @@ __global__ void __launch_bounds__(256, 3) ls_step_kernel(
       continue;
     }
     ls_update(d64, d32, gram, sig, t, n, n_pad, k_max, kw, iter, dmax, st, sel, ssel, out_coef,
-              out_count, bestj, cbest, lin, wv, xv, gv, zv, y, lane, bg0, bg1);
+              out_count, bestj, cbest, lin, wv, xv, gv, zv, y, lane, bg0, bg1, rn2_prev, tol_s,
+              yy_s);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- grouped LS step
+// The LS step is bound by each signal's chain of dependent memory round trips,
+// not by bandwidth, so throughput scales with signals in flight.  Here a warp
+// runs NG = 32 / G signals, one per G-lane group (the signal stays in global
+// memory; per-signal shared state is only L^{-1} and five k-vectors).  All
+// warp-level primitives run on every lane (group-local reductions via
+// width-G xor shuffles); per-group work is predicated by `act`, so groups in
+// different states never diverge around a shuffle.  Same arithmetic as
+// ls_step_kernel / ls_update.
+template <int G>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(CDB_FULL_MASK, v, o);
+  return v;
+}
+template <int G>
+__device__ __forceinline__ double gmax(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(CDB_FULL_MASK, v, o));
+  return v;
+}
+
+template <typename YT, int G>
+__global__ void __launch_bounds__(128) ls_group_kernel(
+    const YT *__restrict__ ys, const double *__restrict__ d64, const float *__restrict__ d32,
+    const double *__restrict__ gram, int64_t p, int64_t t, int n, int64_t n_pad, int k_max,
+    int kw, int iter, double c_err, double dmax, TensorState st, int64_t *out_sel,
+    double *out_coef, int64_t *out_count, int64_t *out_scans, int resume) {
+  constexpr int NG = 32 / G;
+  extern __shared__ double lsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gi = lane / G, gl = lane % G;
+  const unsigned gbits = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (gi * G);
+  const int per_group = kw * kw + 5 * kw;
+  double *lin = lsm + (wib * NG + gi) * per_group;
+  double *wv = lin + kw * kw;
+  double *xv = wv + kw;
+  double *gv = xv + kw;
+  double *zv = gv + kw;
+  int64_t *ssel = (int64_t *)(zv + kw);
+  const int k = iter;
+  const int64_t slots = (int64_t)gridDim.x * (blockDim.x >> 5) * NG;
+  const int64_t count = resume ? (int64_t)st.npending[iter] : p;
+
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * NG; base < count;
+       base += slots) {
+    const int64_t e = base + gi;
+    const bool valid = e < count;
+    const int64_t sig = valid ? (resume ? st.pending[e] : e) : 0;
+    bool act = valid && (resume || !(st.status[sig] & (ST_DONE | ST_DELEGATE)));
+    int64_t *sel = out_sel + sig * kw;
+    const YT *y = ys + sig * (int64_t)n;
+    // ---- independent loads
+    int cidx = -1;
+    float cval = -1.0f;
+    if (act && !resume && gl < NCAND) {
+      cidx = st.cand_idx[sig * NCAND + gl];
+      cval = st.cand_val[sig * NCAND + gl];
+    }
+    float cdrop = 0.0f;
+    double rt = 0.0, drs = 0.0, rn2_prev = 0.0, tol = 0.0, yy = 1.0;
+    if (act) {
+      if (!resume) cdrop = st.cand_drop[sig];
+      rt = st.rt[sig];
+      drs = st.dr[sig];
+      rn2_prev = st.rn2[sig];
+      tol = st.tol[sig];
+      yy = st.yy[sig];
+      for (int i = gl; i < k; i += G) {
+        xv[i] = out_coef[sig * kw + i];
+        zv[i] = st.z[sig * kw + i];
+        ssel[i] = sel[i];
+      }
+      for (int i = gl; i < k * kw; i += G) lin[i] = st.linv[sig * kw * kw + i];
+    }
+    __syncwarp();
+    double best = -1.0, cbest = 0.0;
+    int64_t bestj = -1;
+    if (resume) {
+      if (act) {
+        bestj = st.rs_j[sig];
+        cbest = st.rs_c[sig];
+        best = fabs(cbest);
+        if (gl == 0) st.status[sig] &= ~ST_RESCAN;
+      }
+    } else {
+      // ---- candidates: drop taken atoms; rigorous bound E of the bf16 scan
+      if (cidx >= 0) {
+        for (int i = 0; i < k; i++)
+          if (ssel[i] == cidx) cidx = -1;
+        if (cidx < 0) cval = -1.0f;
+      }
+      const double E = (c_err * rt + drs) * dmax;
+      const double best_apx = gmax<G>((double)cval);
+      const bool rescore = act && cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
+      const unsigned rm = (__ballot_sync(CDB_FULL_MASK, rescore) & gbits) >> (gi * G);
+      double unsc = gmax<G>(rescore || cidx < 0 ? -1.0 : (double)cval);
+      unsc = fmax(unsc, (double)cdrop);
+      const int nre = __popc(rm);
+      const int maxre = (int)__reduce_max_sync(CDB_FULL_MASK, (unsigned)nre);
+      unsigned mm = rm;
+      for (int r = 0; r < maxre; r++) {
+        const int src = mm ? __ffs(mm) - 1 : 0;
+        const bool on = mm != 0;
+        if (mm) mm &= mm - 1;
+        const int64_t j = __shfl_sync(CDB_FULL_MASK, (long long)cidx, gi * G + src);
+        double acc = 0.0;
+        if (on) {
+          const double *dj = d64 + j * n;
+          double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int i = gl;
+          for (; i + 3 * G < n; i += 4 * G) {  // 8 loads in flight
+            const double d0 = __ldg(dj + i), d1 = __ldg(dj + i + G), d2 = __ldg(dj + i + 2 * G),
+                         d3 = __ldg(dj + i + 3 * G);
+            const double y0 = (double)y[i], y1 = (double)y[i + G], y2 = (double)y[i + 2 * G],
+                         y3 = (double)y[i + 3 * G];
+            acc = fma(d0, y0, acc);
+            a1 = fma(d1, y1, a1);
+            a2 = fma(d2, y2, a2);
+            a3 = fma(d3, y3, a3);
+          }
+          for (; i < n; i += G) acc = fma(__ldg(dj + i), (double)y[i], acc);
+          acc += (a1 + a2) + a3;
+          const double *gj = gram + j * t;
+#pragma unroll 4
+          for (int s2 = gl; s2 < k; s2 += G) acc = fma(-__ldg(gj + ssel[s2]), xv[s2], acc);
+        }
+        const double cj = gsum<G>(acc);
+        if (on) {
+          const double v = fabs(cj);
+          if (v > best || (v == best && j < bestj)) {
+            best = v;
+            bestj = j;
+            cbest = cj;
+          }
+        }
+      }
+      if (act && !(bestj >= 0 && unsc + E < best)) {
+        // uncertifiable: queue for the CTA-wide exact rescan, resume later
+        if (gl == 0) {
+          st.status[sig] |= ST_RESCAN;
+          st.pending[atomicAdd(st.npending + iter, 1)] = sig;
+          atomicAdd(st.rescans, 1);
+        }
+        act = false;
+      }
+    }
+    if (act && gl == 0) out_scans[sig] += t - k;  // scans += c - k (_kernels.py:91)
+    if (act && (bestj < 0 || best <= 0.0)) {      // orthogonal break (_kernels.py:104)
+      if (gl == 0) st.status[sig] |= ST_DONE;
+      act = false;
+    }
+    // ---- Cholesky append through the Gram row of the new atom
+    const double *grow = gram + (act ? bestj : 0) * t;
+    if (act)
+      for (int l = gl; l < k; l += G) gv[l] = __ldg(grow + ssel[l]);
+    const double gnn = act ? __ldg(grow + bestj) : 1.0;
+    __syncwarp();
+    if (act)
+      for (int l = gl; l < k; l += G) {
+        double acc = 0.0;
+        for (int i = 0; i <= l; i++) acc = fma(lin[l * kw + i], gv[i], acc);
+        wv[l] = acc;
+      }
+    __syncwarp();
+    double ww = 0.0;
+    if (act)
+      for (int l = gl; l < k; l += G) ww = fma(wv[l], wv[l], ww);
+    ww = gsum<G>(ww);
+    const double d2 = gnn - ww;
+    if (act && !(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine
+      if (gl == 0) st.status[sig] |= ST_DELEGATE;
+      act = false;
+    }
+    const double inv_d = act ? 1.0 / sqrt(d2) : 0.0;
+    const double zk = cbest * inv_d;  // q_k^T y = q_k^T r = <d_new, r> / d
+    if (act) {
+      for (int i = gl; i <= k; i += G) {
+        double v;
+        if (i == k) {
+          v = inv_d;
+        } else {
+          double acc = 0.0;
+          for (int l = i; l < k; l++) acc = fma(wv[l], lin[l * kw + i], acc);
+          v = -acc * inv_d;
+        }
+        lin[k * kw + i] = v;
+        st.linv[sig * kw * kw + k * kw + i] = v;
+      }
+      if (gl == 0) {
+        zv[k] = zk;
+        st.z[sig * kw + k] = zk;
+        sel[k] = bestj;
+        ssel[k] = bestj;
+      }
+    }
+    __syncwarp();
+    const int kd = k + 1;
+    if (act)
+      for (int i = gl; i < kd; i += G) {
+        double acc = 0.0;
+        for (int l = i; l < kd; l++) acc = fma(lin[l * kw + i], zv[l], acc);
+        xv[i] = acc;
+        out_coef[sig * kw + i] = acc;
+      }
+    __syncwarp();
+    // ---- stop test on |r|^2 = |y|^2 - |z|^2, exact residual inside the band
+    const double rn2 = rn2_prev - zk * zk;
+    const double gap = rn2 - tol * tol;
+    const bool need_exact = act && !(fabs(gap) > 1e-12 * yy);
+    bool stop = act && gap < 0.0;
+    if (__any_sync(CDB_FULL_MASK, need_exact)) {
+      double rr = 0.0;
+      if (need_exact)
+        for (int i = gl; i < n; i += G) {
+          double ri = (double)y[i];
+          for (int l = 0; l < kd; l++) ri = fma(-xv[l], __ldg(d64 + ssel[l] * n + i), ri);
+          rr = fma(ri, ri, rr);
+        }
+      rr = gsum<G>(rr);
+      if (need_exact) stop = sqrt(rr) <= tol;
+    }
+    if (act && gl == 0) {
+      st.rn2[sig] = rn2;
+      out_count[sig] = kd;
+    }
+    if (act && (stop || kd >= k_max)) {
+      if (gl == 0) st.status[sig] |= ST_DONE;
+      act = false;
+    }
+    // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16
+    double rr = 0.0, sx = 0.0;
+    if (act) {
+      for (int i0 = 0; i0 < n; i0 += 8 * G) {
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int i = i0 + u * G + gl;
+          acc[u] = i < n ? (double)y[i] : 0.0;
+        }
+        int l = 0;
+        for (; l + 3 < kd; l += 4) {  // 32 loads in flight before the FMAs
+          float v[4][8];
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float *row = d32 + ssel[l + q] * n;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+              const int i = i0 + u * G + gl;
+              v[q][u] = i < n ? __ldg(row + i) : 0.0f;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const double xl = xv[l + q];
+#pragma unroll
+            for (int u = 0; u < 8; u++) acc[u] = fma(-xl, (double)v[q][u], acc[u]);
+          }
+        }
+        for (; l < kd; l++) {
+          const float *row = d32 + ssel[l] * n;
+          const double xl = xv[l];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int i = i0 + u * G + gl;
+            if (i < n) acc[u] = fma(-xl, (double)__ldg(row + i), acc[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int i = i0 + u * G + gl;
+          if (i < n) {
+            st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)acc[u]);
+            rr = fma(acc[u], acc[u], rr);
+          }
+        }
+      }
+      for (int l = gl; l < kd; l += G) sx += fabs(xv[l]);
+    }
+    rr = gsum<G>(rr);
+    sx = gsum<G>(sx);
+    if (act && gl == 0) {
+      st.rt[sig] = sqrt(rr);
+      st.dr[sig] = 0x1p-24 * sx * dmax * 1.0000001;  // |(D64 - D32) x| bound
+      atomicAdd(st.active + iter, 1);
+    }
     __syncwarp();
   }
 }
@@ -890,6 +1182,23 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   // the 2^-15 truncation of the packed epilogue keys
   const double c_err = 2.0 * 0x1p-8 + 0x1p-16 + (double)(n_pad + 16) * 0x1p-23 + 0x1p-15;
   const unsigned ls_grid = (unsigned)((p + ls_wpb - 1) / ls_wpb);
+  // grouped LS kernel: 8-lane groups (4 signals per warp) when the per-signal
+  // state is small, whole warps otherwise; CDB_LS_LEGACY=1 forces ls_step
+  const int64_t grp_bytes = 8 * (kw * kw + 5 * kw);
+  const int lsg_g = 4 * grp_bytes <= 48 * 1024 ? 8 : 32;
+  const int64_t lsg_per_block = 4 * (32 / lsg_g) * grp_bytes;  // 4 warps per block
+  int64_t lsg_smem = lsg_per_block;
+  if (getenv("CDB_LS_LEGACY") || lsg_per_block > 200 * 1024) lsg_smem = 0;
+  const unsigned lsg_grid = (unsigned)((p + 4 * (32 / lsg_g) - 1) / (4 * (32 / lsg_g)));
+  if (lsg_smem > 0) {
+    auto set = [&](const void *f) {
+      return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsg_smem);
+    };
+    if ((e = set((const void *)ls_group_kernel<float, 8>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<double, 8>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<float, 32>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<double, 32>)) != cudaSuccess) return e;
+  }
   for (int it = 0; it < a.k_max; it++) {
     {
     ProfScope _ps("corr_topk", stream);
@@ -913,15 +1222,42 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         note_launch();
       }
       ProfScope _ps(resume ? "ls_resume" : "ls_step", stream);
-      const unsigned grid = resume ? (unsigned)a.num_sms : ls_grid;
-      if (a.ys_f32)
-        ls_step_kernel<float><<<grid, ls_wpb * 32, ls_smem, stream>>>(
-            (const float *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
-            a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
-      else
-        ls_step_kernel<double><<<grid, ls_wpb * 32, ls_smem, stream>>>(
-            (const double *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
-            a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
+      if (lsg_smem > 0) {
+        const unsigned grid = resume ? (unsigned)(a.num_sms * 4) : lsg_grid;
+        if (lsg_g == 8) {
+          if (a.ys_f32)
+            ls_group_kernel<float, 8><<<grid, 128, lsg_smem, stream>>>(
+                (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+          else
+            ls_group_kernel<double, 8><<<grid, 128, lsg_smem, stream>>>(
+                (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+        } else {
+          if (a.ys_f32)
+            ls_group_kernel<float, 32><<<grid, 128, lsg_smem, stream>>>(
+                (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+          else
+            ls_group_kernel<double, 32><<<grid, 128, lsg_smem, stream>>>(
+                (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+        }
+      } else {
+        const unsigned grid = resume ? (unsigned)a.num_sms : ls_grid;
+        if (a.ys_f32)
+          ls_step_kernel<float><<<grid, ls_wpb * 32, ls_smem, stream>>>(
+              (const float *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
+              a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
+        else
+          ls_step_kernel<double><<<grid, ls_wpb * 32, ls_smem, stream>>>(
+              (const double *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
+              a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
+      }
       note_launch();
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
