@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(512, 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
   extern __shared__ __align__(16) double rs[];
   const int n = (int)a.n, T = (int)a.t, kw = (int)a.k_width, Tp = (int)a.t_pad;
+  const int ldl = kw | 1;  // odd L^{-1} row stride: column walks hit distinct banks
   const int64_t P = a.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double *Dt = rs;                 // n x Tp  (columns T..Tp-1 are zero)
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(512, 1)
       const int64_t p = p0 + q;
       double *y = sbase + q * per_sig;
       double *r = y + n;
-      uint32_t *taken = (uint32_t *)(r + n + kw * kw + 5 * kw);
+      uint32_t *taken = (uint32_t *)(r + n + kw * ldl + 5 * kw);
       const bool valid = p < P;
       S[q] = valid ? (int)cs.count(p) : 0;
       kmax[q] = valid ? (int)cs.budget(p, a.k_max, n) : 0;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(512, 1)
         double *y = sbase + q * per_sig;
         double *r = y + n;
         double *lin = r + n;
-        double *zv = lin + kw * kw;
+        double *zv = lin + kw * ldl;
         double *wv = zv + kw;
         double *xv = wv + kw;
         double *gv = xv + kw;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(512, 1)
         __syncwarp();
         for (int l = lane; l < k; l += 32) {
           double accw = 0.0;
-          for (int i = 0; i <= l; i++) accw = fma(lin[l * kw + i], gv[i], accw);
+          for (int i = 0; i <= l; i++) accw = fma(lin[l * ldl + i], gv[i], accw);
           wv[l] = accw;
         }
         __syncwarp();
@@ -208,10 +209,10 @@ __global__ void __launch_bounds__(512, 1)
             v = inv_d;
           } else {
             double accl = 0.0;
-            for (int l = i; l < k; l++) accl = fma(wv[l], lin[l * kw + i], accl);
+            for (int l = i; l < k; l++) accl = fma(wv[l], lin[l * ldl + i], accl);
             v = -accl * inv_d;
           }
-          lin[k * kw + i] = v;
+          lin[k * ldl + i] = v;
         }
         if (lane == 0) zv[k] = zk;
         __syncwarp();
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = lane; i <= k; i += 32) {
           double accx = 0.0;
 #pragma unroll 4
-          for (int l = i; l <= k; l++) accx = fma(lin[l * kw + i], zv[l], accx);
+          for (int l = i; l <= k; l++) accx = fma(lin[l * ldl + i], zv[l], accx);
           xv[i] = accx;
         }
         __syncwarp();
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(512, 1)
         continue;
       }
       double *y = sbase + q * per_sig;
-      double *xv = y + 2 * n + kw * kw + 2 * kw;
+      double *xv = y + 2 * n + kw * ldl + 2 * kw;
       int *sup = (int *)(xv + 2 * kw);
       int64_t *out_sel = a.out_sel + p * kw;
       double *out_coef = a.out_coef + p * kw;
@@ -294,14 +295,17 @@ cudaError_t launch_t(const ResidentArgs &a, const YT *ys, int u, int threads, si
 }  // namespace
 
 int64_t resident_warp_doubles(int64_t n, int64_t kw, int64_t max_cands) {
-  return 2 * n + kw * kw + 6 * kw + ((max_cands + 63) / 64) + 2;
+  return 2 * n + kw * (kw | 1) + 6 * kw + ((max_cands + 63) / 64) + 2;
 }
 
+// Row stride of the transposed dictionary: at least one zero column and the
+// 32*U columns the lane-strided correlation loop reads, rounded to 1 mod 16
+// doubles so a warp walking one column (lane = row) hits distinct banks.
 static int64_t resident_tpad(int64_t t, int64_t max_cands) {
   int64_t u = 1;
   while (32 * u < max_cands) u *= 2;
-  int64_t tp = (t + 1 + 31) / 32 * 32;  // at least one zero column
-  return tp;
+  int64_t tp = t + 1 > 32 * u ? t + 1 : 32 * u;
+  return (tp + 14) / 16 * 16 + 1;
 }
 
 bool resident_fits(int64_t n, int64_t t, int64_t kw, int64_t max_cands, int smem_optin) {
