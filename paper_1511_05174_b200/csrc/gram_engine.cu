@@ -31,26 +31,19 @@
 namespace cdb {
 namespace {
 
-struct GramSmem {
-  double *y;       // n
-  double *alpha0;  // S
-  double *c;       // S    current correlations
-  double *gc;      // S    G[new, C] (this iteration's Gram row slice)
-  double *lr;      // kw*kw  L^{-1} row-major  (lr[l*kw+i])
-  double *lc;      // kw*kw  L^{-1} col-major  (lc[i*kw+l])
-  double *z;       // kw
-  double *w;       // kw
-  double *g;       // kw   G[new, support]
-  double *x;       // kw
-  int64_t *sup;    // kw
-  uint32_t *taken; // (S + 31) / 32
-  double *h;       // kw * S (row i = h_i over candidates) -- smem or global
-};
-
-__host__ __device__ inline int64_t align8(int64_t v) { return (v + 7) & ~int64_t(7); }
-
-__host__ __device__ inline int64_t gram_smem_bytes_no_h(int64_t s, int64_t kw, int64_t n) {
-  return 8 * (n + 3 * s + 2 * kw * kw + 4 * kw) + 8 * kw + 4 * align8((s + 31) / 32);
+// Per-warp shared memory (doubles): L^{-1} twice (row- and column-major,
+// odd row stride so column walks are bank-conflict free), the k-vectors
+// z, w, g, x, the support ids, then H (rows h_i over the candidates, stride
+// max_cands) -- whose first n + 2 S doubles stage y, alpha0 and c while the
+// signal starts.  Correlations, alpha0 and the taken bits live in registers
+// (candidate j = lane + 32 u), so smem per signal is ~8 S k + 16 k^2 bytes.
+__host__ __device__ inline int64_t gram_fixed_doubles(int64_t kw) {
+  return 2 * kw * (kw | 1) + 5 * kw;
+}
+__host__ __device__ inline int64_t gram_region_doubles(int64_t s, int64_t kw, int64_t n,
+                                                       bool h_in_smem) {
+  const int64_t stage = n + 2 * s;
+  return h_in_smem && kw * s > stage ? kw * s : stage;
 }
 
 // alpha0_j = <d_{C_j}, y> for every candidate: the warp streams 8 atom rows
@@ -58,7 +51,7 @@ __host__ __device__ inline int64_t gram_smem_bytes_no_h(int64_t s, int64_t kw, i
 // reduces the 8 partial sums across the warp.
 __device__ __forceinline__ void alpha0_rows(const double *__restrict__ d64, const Cands &cs,
                                             int64_t p, int64_t S, int64_t n, const double *y,
-                                            double *alpha0, double *c, int lane) {
+                                            double *alpha0, int lane) {
   for (int64_t j0 = 0; j0 < S; j0 += 8) {
     const double *rows[8];
 #pragma unroll
@@ -74,19 +67,16 @@ __device__ __forceinline__ void alpha0_rows(const double *__restrict__ d64, cons
 #pragma unroll
     for (int r = 0; r < 8; r++) {
       const double v = warp_sum(acc[r]);
-      if (lane == r && j0 + r < S) {
-        alpha0[j0 + r] = v;
-        c[j0 + r] = v;
-      }
+      if (lane == r && j0 + r < S) alpha0[j0 + r] = v;
     }
   }
 }
 
-// KWT >= k_width and U * 32 >= max_cands are compile-time bounds so every
-// k-loop and candidate loop unrolls (predicated) with independent chains.
+// KWT >= k_width and U * 32 >= max_cands are compile-time bounds (register
+// arrays over this lane's candidates; KWT sizes the lane-per-row loops).
 template <typename YT, int KWT, int U>
-__global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__restrict__ ys,
-                                                       int h_in_smem, int64_t smem_per_warp) {
+__global__ void __launch_bounds__(U <= 8 ? 384 : 256)
+    gram_omp_kernel(GramArgs a, const YT *__restrict__ ys, int h_in_smem, int64_t smem_per_warp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -94,43 +84,38 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   if (local >= a.p) return;
   const int64_t p = a.p_offset + local;
 
-  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands, ldl = kw | 1;
   const int64_t T = a.t;
   const Cands cs = a.cands;
-  unsigned char *base = smem_raw + wib * smem_per_warp;
-  GramSmem s;
-  s.y = (double *)base;
-  s.alpha0 = s.y + n;
-  s.c = s.alpha0 + smax;
-  s.gc = s.c + smax;
-  s.lr = s.gc + smax;
-  s.lc = s.lr + kw * kw;
-  s.z = s.lc + kw * kw;
-  s.w = s.z + kw;
-  s.g = s.w + kw;
-  s.x = s.g + kw;
-  s.sup = (int64_t *)(s.x + kw);
-  s.taken = (uint32_t *)(s.sup + kw);
-  s.h = h_in_smem ? (double *)(base + align8(gram_smem_bytes_no_h(smax, kw, n)))
-                  : a.hwork + local * kw * smax;
+  double *lr = (double *)(smem_raw + wib * smem_per_warp);  // lr[l*ldl+i] = L^{-1}[l][i]
+  double *lc = lr + kw * ldl;                                 // lc[i*ldl+l] = L^{-1}[l][i]
+  double *zv = lc + kw * ldl;
+  double *wv = zv + kw;
+  double *gv = wv + kw;
+  double *xv = gv + kw;
+  int64_t *sup = (int64_t *)(xv + kw);
+  double *region = (double *)(sup + kw);
+  double *h = h_in_smem ? region : a.hwork + local * kw * smax;
+  const YT *yg = ys + p * a.ys_stride;
 
   const int S = (int)cs.count(p);
   const int k_max = (int)cs.budget(p, a.k_max, n);
   int64_t *out_sel = a.out_sel + p * kw;
   double *out_coef = a.out_coef + p * kw;
 
-  // this lane's candidates j = lane + 32u and their atom ids
+  // this lane's candidates j = lane + 32u, their atom ids, unavailable bits
   int cid[U];
+  unsigned tk = 0u;
 #pragma unroll
   for (int u = 0; u < U; u++) {
     const int j = lane + 32 * u;
     cid[u] = j < S ? (int)cs.id(p, j) : 0;
+    if (j >= S) tk |= 1u << u;
   }
-  for (int i = lane; i < n; i += 32) s.y[i] = (double)ys[p * a.ys_stride + i];
-  if (lane < (S + 31) / 32) s.taken[lane] = 0u;
-  for (int w = lane + 32; w < (S + 31) / 32; w += 32) s.taken[w] = 0u;
+  double *y = region;  // staging until the first H row is written
+  for (int i = lane; i < n; i += 32) y[i] = (double)yg[i];
   __syncwarp();
-  const double ynorm = sqrt(dot4_quad(s.y, s.y, n, lane));
+  const double ynorm = sqrt(dot4_quad(y, y, n, lane));  // reference order (_kernels.py:71)
   const double tol = a.eps[p];
 
   int kdone = 0;
@@ -140,145 +125,139 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   bool delegate = false;
 
   if (!(ynorm <= tol) && k_max > 0) {
+    double a0[U], cr[U];
     if (a.alpha0_in) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int j = lane + 32 * u;
-        if (j < S) {
-          const double v = a.alpha0_in[p * smax + j];
-          s.alpha0[j] = v;
-          s.c[j] = v;
-        }
+        a0[u] = j < S ? a.alpha0_in[p * smax + j] : 0.0;
       }
     } else {
-      alpha0_rows(a.d64, cs, p, S, n, s.y, s.alpha0, s.c, lane);
+      double *al = y + n;
+      alpha0_rows(a.d64, cs, p, S, n, y, al, lane);
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int j = lane + 32 * u;
+        a0[u] = j < S ? al[j] : 0.0;
+      }
     }
+#pragma unroll
+    for (int u = 0; u < U; u++) cr[u] = a0[u];
     double yy = 0.0;
-    for (int i = lane; i < n; i += 32) yy = fma(s.y[i], s.y[i], yy);
+    for (int i = lane; i < n; i += 32) yy = fma(y[i], y[i], yy);
     yy = warp_sum(yy);
     double rn2 = yy;
     yy_final = yy;
     const double tol2 = tol * tol;
     const double band = 1e-12 * yy;
-    __syncwarp();
+    int64_t sup0 = 0, sup1 = 0;  // sup[lane], sup[lane + 32]
+    __syncwarp();                // staging is dead from here (H row 0 overwrites it)
 
     for (int k = 0; k < k_max; k++) {
       rn2_final = rn2;
       scans += S - k;
-      // ---- selection: max |c_j| over non-taken, ties -> lowest index
+      // ---- selection: max |c_j| over available candidates, ties -> lowest j
       double best = -1.0;
-      int bestj = -1;
+      unsigned bj = 0xffffffffu;
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const int j = lane + 32 * u;
-        if (j < S && !((s.taken[j >> 5] >> (j & 31)) & 1u)) {
-          const double v = fabs(s.c[j]);
-          if (v > best) {
-            best = v;
-            bestj = j;
-          }
+        const double v = fabs(cr[u]);
+        if (!((tk >> u) & 1u) && v > best) {
+          best = v;
+          bj = lane + 32 * u;
         }
       }
+      double m = best;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(CDB_FULL_MASK, best, o);
-        const int oj = __shfl_xor_sync(CDB_FULL_MASK, bestj, o);
-        if (oj >= 0 && (bestj < 0 || ov > best || (ov == best && oj < bestj))) {
-          best = ov;
-          bestj = oj;
-        }
-      }
-      if (bestj < 0 || best <= 0.0) break;
-      // the winner's atom id from the lane that owns it (no jl / q division)
-      int nid32 = 0;
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+      if (!(m > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
+      const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+      const int ub = bestj >> 5, owner = bestj & 31;
+      int my_id = 0;
+      double my_a0 = 0.0;
 #pragma unroll
       for (int u = 0; u < U; u++)
-        if ((bestj >> 5) == u) nid32 = cid[u];
-      const int64_t nid = __shfl_sync(CDB_FULL_MASK, nid32, bestj & 31);
-      if (lane == 0) {
-        s.taken[bestj >> 5] |= 1u << (bestj & 31);
-        s.sup[k] = nid;
-      }
+        if (u == ub) {
+          my_id = cid[u];
+          my_a0 = a0[u];
+        }
+      const int64_t nid = __shfl_sync(CDB_FULL_MASK, my_id, owner);
+      const double a0_new = __shfl_sync(CDB_FULL_MASK, my_a0, owner);
+      if (lane == owner) tk |= 1u << ub;
       // ---- gathers from Gram row `nid` (independent loads)
       const double *grow = a.gram + nid * T;
-      double gcv[U];
+      double hacc[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) gcv[u] = lane + 32 * u < S ? __ldg(grow + cid[u]) : 0.0;
-      const double gl = lane < k ? __ldg(grow + s.sup[lane]) : 0.0;
-      const double gl2 = lane + 32 < k ? __ldg(grow + s.sup[lane + 32]) : 0.0;
+      for (int u = 0; u < U; u++) hacc[u] = lane + 32 * u < S ? __ldg(grow + cid[u]) : 0.0;
+      const double gl = lane < k ? __ldg(grow + sup0) : 0.0;
+      const double gl2 = lane + 32 < k ? __ldg(grow + sup1) : 0.0;
       const double gnn = __ldg(grow + nid);
-      if (lane < k) s.g[lane] = gl;
-      if (lane + 32 < k) s.g[lane + 32] = gl2;
+      if (lane == k) sup0 = nid;
+      if (lane + 32 == k) sup1 = nid;
+      if (lane == 0) sup[k] = nid;
+      if (lane < k) gv[lane] = gl;
+      if (lane + 32 < k) gv[lane + 32] = gl2;
       __syncwarp();
-      // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l+32)
+      // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l + 32)
 #pragma unroll
       for (int half = 0; half < (KWT + 31) / 32; half++) {
         const int l = lane + 32 * half;
-        if (l < k) {
-          double acc = 0.0;
-#pragma unroll
-          for (int i = 0; i < KWT; i++)
-            if (i <= l) acc = fma(s.lc[i * kw + l], s.g[i], acc);
-          s.w[l] = acc;
-        }
+        double acc = 0.0;
+#pragma unroll 4
+        for (int i = 0; i < k; i++)
+          if (i <= l && l < k) acc = fma(lc[i * ldl + l], gv[i], acc);
+        if (l < k) wv[l] = acc;
       }
       __syncwarp();
       double ww = 0.0, wz = 0.0;
       for (int l = lane; l < k; l += 32) {
-        ww = fma(s.w[l], s.w[l], ww);
-        wz = fma(s.w[l], s.z[l], wz);
+        ww = fma(wv[l], wv[l], ww);
+        wz = fma(wv[l], zv[l], wz);
       }
-      ww = warp_sum(ww);
-      wz = warp_sum(wz);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ww += __shfl_xor_sync(CDB_FULL_MASK, ww, o);
+        wz += __shfl_xor_sync(CDB_FULL_MASK, wz, o);
+      }
       const double d2 = gnn - ww;
       if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
         delegate = true;
         break;
       }
       const double inv_d = 1.0 / sqrt(d2);
-      const double zk = (s.alpha0[bestj] - wz) * inv_d;
+      const double zk = (a0_new - wz) * inv_d;
       // ---- new row of L^{-1}: [-(w^T L^{-1}) / d, 1/d]
 #pragma unroll
       for (int half = 0; half < (KWT + 31) / 32; half++) {
         const int i = lane + 32 * half;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int l = 0; l < k; l++)
+          if (l >= i) acc = fma(wv[l], lr[l * ldl + i], acc);
         if (i <= k) {
-          double v;
-          if (i == k) {
-            v = inv_d;
-          } else {
-            double acc = 0.0;
-#pragma unroll
-            for (int l = 0; l < KWT; l++)
-              if (l >= i && l < k) acc = fma(s.w[l], s.lr[l * kw + i], acc);
-            v = -acc * inv_d;
-          }
-          s.lr[k * kw + i] = v;
-          s.lc[i * kw + k] = v;
+          const double v = i == k ? inv_d : -acc * inv_d;
+          lr[k * ldl + i] = v;
+          lc[i * ldl + k] = v;
         }
       }
-      if (lane == 0) s.z[k] = zk;
+      if (lane == 0) zv[k] = zk;
       // ---- h_k over candidates, correlation update (U independent chains)
-      double hacc[U];
+#pragma unroll 2
+      for (int i = 0; i < k; i++) {
+        const double wi = wv[i];
+        const double *hi = h + i * smax + lane;
 #pragma unroll
-      for (int u = 0; u < U; u++) hacc[u] = gcv[u];
-#pragma unroll
-      for (int i = 0; i < KWT; i++) {
-        if (i < k) {
-          const double wi = s.w[i];
-          const double *hi = s.h + i * smax + lane;
-#pragma unroll
-          for (int u = 0; u < U; u++)
-            if (lane + 32 * u < S) hacc[u] = fma(-wi, hi[32 * u], hacc[u]);
-        }
+        for (int u = 0; u < U; u++)
+          if (lane + 32 * u < S) hacc[u] = fma(-wi, hi[32 * u], hacc[u]);
       }
-      double *hk = s.h + k * smax + lane;
+      double *hk = h + k * smax + lane;
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const int j = lane + 32 * u;
-        if (j < S) {
-          const double h = hacc[u] * inv_d;
-          hk[32 * u] = h;
-          s.c[j] = fma(-zk, h, s.c[j]);
+        if (lane + 32 * u < S) {
+          const double hv = hacc[u] * inv_d;
+          hk[32 * u] = hv;
+          cr[u] = fma(-zk, hv, cr[u]);
         }
       }
       rn2 -= zk * zk;
@@ -291,14 +270,14 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
       if (gap < -band) break;
       for (int i = lane; i < kdone; i += 32) {
         double acc = 0.0;
-        for (int l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
-        s.x[i] = acc;
+        for (int l = i; l < kdone; l++) acc = fma(lr[l * ldl + i], zv[l], acc);
+        xv[i] = acc;
       }
       __syncwarp();
       double rr = 0.0;
       for (int i = lane; i < n; i += 32) {
-        double ri = s.y[i];
-        for (int l = 0; l < kdone; l++) ri = fma(-s.x[l], a.d64[s.sup[l] * n + i], ri);
+        double ri = (double)yg[i];
+        for (int l = 0; l < kdone; l++) ri = fma(-xv[l], a.d64[sup[l] * n + i], ri);
         rr = fma(ri, ri, rr);
       }
       rr = warp_sum(rr);
@@ -314,8 +293,8 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
   __syncwarp();
   for (int i = lane; i < kdone; i += 32) {
     double acc = 0.0;
-    for (int l = i; l < kdone; l++) acc = fma(s.lr[l * kw + i], s.z[l], acc);
-    s.x[i] = acc;
+    for (int l = i; l < kdone; l++) acc = fma(lr[l * ldl + i], zv[l], acc);
+    xv[i] = acc;
   }
   __syncwarp();
   if (kdone > 0) {
@@ -326,16 +305,16 @@ __global__ void __launch_bounds__(256) gram_omp_kernel(GramArgs a, const YT *__r
     } else {
       double rr = 0.0;
       for (int i = lane; i < n; i += 32) {
-        double ri = s.y[i];
-        for (int l = 0; l < kdone; l++) ri = fma(-s.x[l], __ldg(a.d64 + s.sup[l] * n + i), ri);
+        double ri = (double)yg[i];
+        for (int l = 0; l < kdone; l++) ri = fma(-xv[l], __ldg(a.d64 + sup[l] * n + i), ri);
         rr = fma(ri, ri, rr);
       }
       rnorm = sqrt(warp_sum(rr));
     }
   }
   for (int j = lane; j < kw; j += 32) {
-    out_sel[j] = j < kdone ? s.sup[j] : -1;
-    out_coef[j] = j < kdone ? s.x[j] : 0.0;
+    out_sel[j] = j < kdone ? sup[j] : -1;
+    out_coef[j] = j < kdone ? xv[j] : 0.0;
   }
   if (lane == 0) {
     a.out_count[p] = kdone;
@@ -385,8 +364,7 @@ cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int kwt, int u, in
 }  // namespace
 
 int64_t gram_total_smem(int64_t s, int64_t kw, int64_t n, bool h_in_smem) {
-  int64_t b = align8(gram_smem_bytes_no_h(s, kw, n));
-  if (h_in_smem) b += 8 * s * kw;
+  const int64_t b = 8 * (gram_fixed_doubles(kw) + gram_region_doubles(s, kw, n, h_in_smem));
   return (b + 15) & ~int64_t(15);
 }
 
@@ -400,14 +378,14 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   const int64_t per_warp = gram_total_smem(s, kw, n, h_in_smem);
   if (per_warp > max_smem_per_block) return cudaErrorInvalidValue;
   if (kw > 64 || s > 512) return cudaErrorInvalidValue;
+  int u = 1;
+  while (32 * u < s) u *= 2;
   int wpb = (int)(max_smem_per_block / per_warp);
-  if (wpb > 8) wpb = 8;
+  if (wpb > (u <= 8 ? 12 : 8)) wpb = u <= 8 ? 12 : 8;
   if (wpb < 1) wpb = 1;
   const int64_t blocks = (args.p + wpb - 1) / wpb;
   int kwt = 8;
   while (kwt < kw) kwt *= 2;
-  int u = 1;
-  while (32 * u < s) u *= 2;
   note_launch();
   if (ys_f32)
     return launch_gram_y<float>(args, (const float *)ys, kwt, u, h_in_smem ? 1 : 0, per_warp, wpb,
