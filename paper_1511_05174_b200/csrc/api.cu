@@ -358,7 +358,7 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   int64_t chunk = p;
   DevBuf hwork;
   if (!h_smem) {
-    const int64_t per_sig = 8 * max_cands * kw;
+    const int64_t per_sig = 8 * cdb::gram_h_doubles(max_cands, kw);
     chunk = kScratchBudget / per_sig;
     if (chunk < 1) chunk = 1;
     if (chunk > p) chunk = p;

@@ -67,7 +67,9 @@ struct GramArgs {
   const char *tag;       // profiler name
   const double *alpha0_in;  // optional precomputed <d_{C_j}, y> (P x max_cands)
 };
-// Shared-memory bytes per warp of the Gram engine (H in smem or global).
+// Shared-memory bytes per warp of the Gram engine (H in smem or global), and
+// the doubles of one signal's H (global scratch when it does not fit smem).
+int64_t gram_h_doubles(int64_t max_cands, int64_t k_width);
 int64_t gram_total_smem(int64_t max_cands, int64_t k_width, int64_t n, bool h_in_smem);
 cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
                         int num_sms, cudaStream_t stream);

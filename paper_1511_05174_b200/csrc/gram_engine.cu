@@ -3,23 +3,24 @@
 //
 // Same algorithm as the reference kernel (crossdict/_kernels.py:50-168):
 // greedy pick of max |<d_j, r>| over the allowed, not-taken candidates with
-// the lowest index winning ties, exact least squares on the support,
-// residual-norm stop test -- but the least squares is an incremental
-// Cholesky of the support Gram G_SS kept as its explicit inverse factor
-// L^{-1}, and the residual is never materialised.  With q_i the orthonormal
-// basis the reference builds by MGS (_kernels.py:111-137), z_i = q_i^T y
-// (its `qty`) and h_i[j] = d_j^T q_i:
+// the lowest index winning ties, modified Gram-Schmidt least squares,
+// residual-norm stop test, back-substitution for the coefficients -- but
+// the residual and the basis vectors are never materialised.  With q_i the
+// orthonormal basis the reference builds by MGS (_kernels.py:111-137),
+// z_i = q_i^T y (its `qty`) and h_i[j] = q_i^T d_{C_j}:
 //
-//     c_j   = alpha0_j - sum_i z_i h_i[j]            (correlation, fp64)
-//     w     = L^{-1} G[S, new],  d^2 = G_nn - |w|^2  (MGS projection defect)
-//     z_k   = (alpha0_new - w.z) / d
+//     c_j   = alpha0_j - sum_i z_i h_i[j]             (correlation, fp64)
+//     w_i   = q_i^T d_new = h_i[new]                  (MGS coefficients = R[i][k])
+//     d^2   = G_nn - |w|^2                            (projection defect = R[k][k]^2)
+//     z_k   = c_new / d
 //     h_k   = (G[C, new] - sum_i w_i h_i) / d
-//     |r|^2 = |y|^2 - |z|^2                          (stop test, exact band check)
+//     |r|^2 = |y|^2 - |z|^2                           (stop test, exact band check)
+//     R x = z                                         (back-substitution, _kernels.py:159-164)
 //
-// so per iteration a signal touches one Gram row and S*k fp64 values of H
-// held in shared memory, instead of re-reading S atoms of length N.  All
-// arithmetic is fp64; correlations agree with the reference's to ~1e-13
-// relative of |r|, far inside the 1e-6 near-tie band of the parity
+// so per iteration a signal touches one Gram row slice and S*k fp64 values
+// of H held in shared memory, instead of re-reading S atoms of length N.
+// All arithmetic is fp64; correlations agree with the reference's to
+// ~1e-13 relative of |r|, far inside the 1e-6 near-tie band of the parity
 // contract.  Signals whose new atom is within 1e-4 |a| of the span of the
 // support (the reference's rank test is d <= 1e-10 |a|, _kernels.py:126)
 // are delegated to the exact engine, which reproduces the reference bit for
@@ -31,19 +32,29 @@
 namespace cdb {
 namespace {
 
-// Per-warp shared memory (doubles): L^{-1} twice (row- and column-major,
-// odd row stride so column walks are bank-conflict free), the k-vectors
-// z, w, g, x, the support ids, then H (rows h_i over the candidates, stride
-// max_cands) -- whose first n + 2 S doubles stage y, alpha0 and c while the
-// signal starts.  Correlations, alpha0 and the taken bits live in registers
-// (candidate j = lane + 32 u), so smem per signal is ~8 S k + 16 k^2 bytes.
-__host__ __device__ inline int64_t gram_fixed_doubles(int64_t kw) {
-  return 2 * kw * (kw | 1) + 5 * kw;
+// H row layout: row stride HS = 32 U doubles; candidate j = lane + 32 u sits
+// at hslot(j), pairs (u = 2v, 2v + 1) of one lane adjacent so each lane moves
+// its U values with U/2 conflict-free 16-byte accesses.
+template <int U>
+__host__ __device__ __forceinline__ int hslot(int j) {
+  if (U == 1) return j;
+  const int u = j >> 5;
+  return (u >> 1) * 64 + (j & 31) * 2 + (u & 1);
+}
+
+// Per-warp shared memory (doubles): z, 1/d, pick slots, support ids, x
+// (k_width each), then the H rows -- whose first n + S doubles stage y and
+// alpha0 while the signal starts (H in global memory: staging only).
+__host__ __device__ inline int64_t gram_hs(int64_t s) {
+  int64_t u = 1;
+  while (32 * u < s) u *= 2;
+  return 32 * u;
 }
 __host__ __device__ inline int64_t gram_region_doubles(int64_t s, int64_t kw, int64_t n,
                                                        bool h_in_smem) {
-  const int64_t stage = n + 2 * s;
-  return h_in_smem && kw * s > stage ? kw * s : stage;
+  const int64_t stage = n + s;
+  const int64_t hd = kw * gram_hs(s);
+  return h_in_smem && hd > stage ? hd : stage;
 }
 
 // alpha0_j = <d_{C_j}, y> for every candidate: the warp streams 8 atom rows
@@ -72,11 +83,40 @@ __device__ __forceinline__ void alpha0_rows(const double *__restrict__ d64, cons
   }
 }
 
-// KWT >= k_width and U * 32 >= max_cands are compile-time bounds (register
-// arrays over this lane's candidates; KWT sizes the lane-per-row loops).
-template <typename YT, int KWT, int U>
-__global__ void __launch_bounds__(U <= 8 ? 384 : 256)
+// Coefficients by back-substitution R x = z (_kernels.py:159-164), with the
+// MGS factor read out of H: R[i][l] = q_i^T d_{s_l} = h_i[pick_l] (i < l),
+// R[l][l] = d_l.  Column sweep: lane i (and i + 32) accumulates
+// sum_{l > i} R[i][l] x_l.
+template <int U>
+__device__ void back_substitute(const double *h, int kd, const double *zv, const double *iv,
+                                const int *pj, double *xv, int lane) {
+  constexpr int HS = 32 * U;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int l = kd - 1; l >= 0; l--) {
+    const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
+    const double xl = (zv[l] - accl) * iv[l];
+    if (lane == 0) xv[l] = xl;
+    const int sl = hslot<U>(pj[l]);
+    if (lane < l) acc0 = fma(h[lane * HS + sl], xl, acc0);
+    if (lane + 32 < l) acc1 = fma(h[(lane + 32) * HS + sl], xl, acc1);
+  }
+  __syncwarp();
+}
+
+// U * 32 >= max_cands is a compile-time bound (register arrays over this
+// lane's candidates j = lane + 32 u).
+//
+// Per iteration, with j* the pick: w_i = q_i^T d_{j*} = h_i[j*] (the MGS
+// projection coefficients are a column of H), d^2 = G[j*,j*] - |w|^2,
+// z_k = c_{j*} / d, h_k = (G[C, j*] - sum_i w_i h_i) / d, c -= z_k h_k.
+// Every lane reads the w_i it needs as a broadcast out of H while it
+// updates its own candidates, and accumulates |w|^2 redundantly, so an
+// iteration has no triangular solve and a single cross-lane reduction
+// (the argmax).
+template <typename YT, int U>
+__global__ void __launch_bounds__(U <= 8 ? 512 : 256)
     gram_omp_kernel(GramArgs a, const YT *__restrict__ ys, int h_in_smem, int64_t smem_per_warp) {
+  constexpr int HS = 32 * U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -84,18 +124,16 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
   if (local >= a.p) return;
   const int64_t p = a.p_offset + local;
 
-  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands, ldl = kw | 1;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
   const int64_t T = a.t;
   const Cands cs = a.cands;
-  double *lr = (double *)(smem_raw + wib * smem_per_warp);  // lr[l*ldl+i] = L^{-1}[l][i]
-  double *lc = lr + kw * ldl;                                 // lc[i*ldl+l] = L^{-1}[l][i]
-  double *zv = lc + kw * ldl;
-  double *wv = zv + kw;
-  double *gv = wv + kw;
-  double *xv = gv + kw;
-  int64_t *sup = (int64_t *)(xv + kw);
-  double *region = (double *)(sup + kw);
-  double *h = h_in_smem ? region : a.hwork + local * kw * smax;
+  double *zv = (double *)(smem_raw + wib * smem_per_warp);
+  double *iv = zv + kw;              // 1 / d_l
+  int *pj = (int *)(iv + kw);        // candidate index of pick l
+  int64_t *sup = (int64_t *)(iv + 2 * kw);
+  double *xv = (double *)(sup + kw);
+  double *region = xv + kw;
+  double *h = h_in_smem ? region : a.hwork + local * kw * HS;
   const YT *yg = ys + p * a.ys_stride;
 
   const int S = (int)cs.count(p);
@@ -125,12 +163,12 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
   bool delegate = false;
 
   if (!(ynorm <= tol) && k_max > 0) {
-    double a0[U], cr[U];
+    double cr[U];
     if (a.alpha0_in) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int j = lane + 32 * u;
-        a0[u] = j < S ? a.alpha0_in[p * smax + j] : 0.0;
+        cr[u] = j < S ? a.alpha0_in[p * smax + j] : 0.0;
       }
     } else {
       double *al = y + n;
@@ -139,11 +177,9 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int j = lane + 32 * u;
-        a0[u] = j < S ? al[j] : 0.0;
+        cr[u] = j < S ? al[j] : 0.0;
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; u++) cr[u] = a0[u];
     double yy = 0.0;
     for (int i = lane; i < n; i += 32) yy = fma(y[i], y[i], yy);
     yy = warp_sum(yy);
@@ -151,8 +187,7 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
     yy_final = yy;
     const double tol2 = tol * tol;
     const double band = 1e-12 * yy;
-    int64_t sup0 = 0, sup1 = 0;  // sup[lane], sup[lane + 32]
-    __syncwarp();                // staging is dead from here (H row 0 overwrites it)
+    __syncwarp();  // staging is dead from here (H row 0 overwrites it)
 
     for (int k = 0; k < k_max; k++) {
       rn2_final = rn2;
@@ -175,90 +210,66 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
       const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
       const int ub = bestj >> 5, owner = bestj & 31;
       int my_id = 0;
-      double my_a0 = 0.0;
+      double my_c = 0.0;
 #pragma unroll
       for (int u = 0; u < U; u++)
         if (u == ub) {
           my_id = cid[u];
-          my_a0 = a0[u];
+          my_c = cr[u];
         }
       const int64_t nid = __shfl_sync(CDB_FULL_MASK, my_id, owner);
-      const double a0_new = __shfl_sync(CDB_FULL_MASK, my_a0, owner);
+      const double cj = __shfl_sync(CDB_FULL_MASK, my_c, owner);
       if (lane == owner) tk |= 1u << ub;
-      // ---- gathers from Gram row `nid` (independent loads)
+      // ---- Gram row slice G[C, j*] (independent loads), then H update
       const double *grow = a.gram + nid * T;
       double hacc[U];
 #pragma unroll
       for (int u = 0; u < U; u++) hacc[u] = lane + 32 * u < S ? __ldg(grow + cid[u]) : 0.0;
-      const double gl = lane < k ? __ldg(grow + sup0) : 0.0;
-      const double gl2 = lane + 32 < k ? __ldg(grow + sup1) : 0.0;
       const double gnn = __ldg(grow + nid);
-      if (lane == k) sup0 = nid;
-      if (lane + 32 == k) sup1 = nid;
-      if (lane == 0) sup[k] = nid;
-      if (lane < k) gv[lane] = gl;
-      if (lane + 32 < k) gv[lane + 32] = gl2;
-      __syncwarp();
-      // ---- w = L^{-1} G[S, new]   (lane l owns rows l, l + 32)
+      const int bs = hslot<U>(bestj);
+      double ww = 0.0;
+#pragma unroll 2
+      for (int i = 0; i < k; i++) {
+        const double *hi = h + i * HS;
+        const double wi = hi[bs];  // = q_i^T d_{j*}
+        ww = fma(wi, wi, ww);
+        if (U == 1) {
+          hacc[0] = fma(-wi, hi[lane], hacc[0]);
+        } else {
 #pragma unroll
-      for (int half = 0; half < (KWT + 31) / 32; half++) {
-        const int l = lane + 32 * half;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int i = 0; i < k; i++)
-          if (i <= l && l < k) acc = fma(lc[i * ldl + l], gv[i], acc);
-        if (l < k) wv[l] = acc;
-      }
-      __syncwarp();
-      double ww = 0.0, wz = 0.0;
-      for (int l = lane; l < k; l += 32) {
-        ww = fma(wv[l], wv[l], ww);
-        wz = fma(wv[l], zv[l], wz);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ww += __shfl_xor_sync(CDB_FULL_MASK, ww, o);
-        wz += __shfl_xor_sync(CDB_FULL_MASK, wz, o);
+          for (int v = 0; v < U / 2; v++) {
+            const double2 t2 = *(const double2 *)(hi + v * 64 + lane * 2);
+            hacc[2 * v] = fma(-wi, t2.x, hacc[2 * v]);
+            hacc[2 * v + 1] = fma(-wi, t2.y, hacc[2 * v + 1]);
+          }
+        }
       }
       const double d2 = gnn - ww;
       if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
         delegate = true;
         break;
       }
-      const double inv_d = 1.0 / sqrt(d2);
-      const double zk = (a0_new - wz) * inv_d;
-      // ---- new row of L^{-1}: [-(w^T L^{-1}) / d, 1/d]
+      const double inv_d = rsqrt(d2);
+      const double zk = cj * inv_d;  // q_k^T y = q_k^T r = <d_{j*}, r> / d
+      double *hk = h + k * HS;
+      if (U == 1) {
+        const double hv = hacc[0] * inv_d;
+        hk[lane] = hv;
+        cr[0] = fma(-zk, hv, cr[0]);
+      } else {
 #pragma unroll
-      for (int half = 0; half < (KWT + 31) / 32; half++) {
-        const int i = lane + 32 * half;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int l = 0; l < k; l++)
-          if (l >= i) acc = fma(wv[l], lr[l * ldl + i], acc);
-        if (i <= k) {
-          const double v = i == k ? inv_d : -acc * inv_d;
-          lr[k * ldl + i] = v;
-          lc[i * ldl + k] = v;
+        for (int v = 0; v < U / 2; v++) {
+          const double h0 = hacc[2 * v] * inv_d, h1 = hacc[2 * v + 1] * inv_d;
+          *(double2 *)(hk + v * 64 + lane * 2) = make_double2(h0, h1);
+          cr[2 * v] = fma(-zk, h0, cr[2 * v]);
+          cr[2 * v + 1] = fma(-zk, h1, cr[2 * v + 1]);
         }
       }
-      if (lane == 0) zv[k] = zk;
-      // ---- h_k over candidates, correlation update (U independent chains)
-#pragma unroll 2
-      for (int i = 0; i < k; i++) {
-        const double wi = wv[i];
-        const double *hi = h + i * smax + lane;
-#pragma unroll
-        for (int u = 0; u < U; u++)
-          if (lane + 32 * u < S) hacc[u] = fma(-wi, hi[32 * u], hacc[u]);
-      }
-      double *hk = h + k * smax + lane;
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (lane + 32 * u < S) {
-          const double hv = hacc[u] * inv_d;
-          hk[32 * u] = hv;
-          cr[u] = fma(-zk, hv, cr[u]);
-        }
+      if (lane == 0) {
+        zv[k] = zk;
+        iv[k] = inv_d;
+        pj[k] = bestj;
+        sup[k] = nid;
       }
       rn2 -= zk * zk;
       rn2_final = rn2;
@@ -268,12 +279,7 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
       const double gap = rn2 - tol2;
       if (gap > band) continue;
       if (gap < -band) break;
-      for (int i = lane; i < kdone; i += 32) {
-        double acc = 0.0;
-        for (int l = i; l < kdone; l++) acc = fma(lr[l * ldl + i], zv[l], acc);
-        xv[i] = acc;
-      }
-      __syncwarp();
+      back_substitute<U>(h, kdone, zv, iv, pj, xv, lane);
       double rr = 0.0;
       for (int i = lane; i < n; i += 32) {
         double ri = (double)yg[i];
@@ -289,14 +295,9 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
     if (lane == 0) a.status[p] |= ST_DELEGATE;
     return;  // the exact engine rewrites every output of this signal
   }
-  // ---- coefficients x = L^{-T} z (pick order), exact final residual norm
+  // ---- coefficients (pick order), exact final residual norm
   __syncwarp();
-  for (int i = lane; i < kdone; i += 32) {
-    double acc = 0.0;
-    for (int l = i; l < kdone; l++) acc = fma(lr[l * ldl + i], zv[l], acc);
-    xv[i] = acc;
-  }
-  __syncwarp();
+  back_substitute<U>(h, kdone, zv, iv, pj, xv, lane);
   if (kdone > 0) {
     // |r| = sqrt(|y|^2 - |z|^2) is accurate to ~1e-16 |y|^2 / |r|^2 relative;
     // re-materialise the residual exactly only when that is not tight
@@ -324,47 +325,37 @@ __global__ void __launch_bounds__(U <= 8 ? 384 : 256)
   }
 }
 
-template <typename YT, int KWT, int U>
+template <typename YT, int U>
 cudaError_t launch_gram_tu(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
                            int wpb, int64_t blocks, cudaStream_t stream) {
   const int64_t smem = per_warp * wpb;
-  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, KWT, U>,
+  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, U>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  gram_omp_kernel<YT, KWT, U><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
-                                                                            per_warp);
+  gram_omp_kernel<YT, U><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
+                                                                       per_warp);
   return cudaGetLastError();
 }
 
-template <typename YT, int KWT>
-cudaError_t launch_gram_t(const GramArgs &args, const YT *ys, int u, int h_in_smem,
+template <typename YT>
+cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int u, int h_in_smem,
                           int64_t per_warp, int wpb, int64_t blocks, cudaStream_t stream) {
   switch (u) {
-    case 1: return launch_gram_tu<YT, KWT, 1>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
-    case 2: return launch_gram_tu<YT, KWT, 2>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
-    case 4: return launch_gram_tu<YT, KWT, 4>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
-    case 8: return launch_gram_tu<YT, KWT, 8>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
-    case 16: return launch_gram_tu<YT, KWT, 16>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <typename YT>
-cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int kwt, int u, int h_in_smem,
-                          int64_t per_warp, int wpb, int64_t blocks, cudaStream_t stream) {
-  switch (kwt) {
-    case 8: return launch_gram_t<YT, 8>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
-    case 16: return launch_gram_t<YT, 16>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
-    case 32: return launch_gram_t<YT, 32>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
-    case 64: return launch_gram_t<YT, 64>(args, ys, u, h_in_smem, per_warp, wpb, blocks, stream);
+    case 1: return launch_gram_tu<YT, 1>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 2: return launch_gram_tu<YT, 2>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 4: return launch_gram_tu<YT, 4>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 8: return launch_gram_tu<YT, 8>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 16: return launch_gram_tu<YT, 16>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
+int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_cands); }
+
 int64_t gram_total_smem(int64_t s, int64_t kw, int64_t n, bool h_in_smem) {
-  const int64_t b = 8 * (gram_fixed_doubles(kw) + gram_region_doubles(s, kw, n, h_in_smem));
+  const int64_t b = 8 * (5 * kw + gram_region_doubles(s, kw, n, h_in_smem));
   return (b + 15) & ~int64_t(15);
 }
 
@@ -380,17 +371,16 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   if (kw > 64 || s > 512) return cudaErrorInvalidValue;
   int u = 1;
   while (32 * u < s) u *= 2;
+  const int cap = u <= 8 ? 16 : 8;
   int wpb = (int)(max_smem_per_block / per_warp);
-  if (wpb > (u <= 8 ? 12 : 8)) wpb = u <= 8 ? 12 : 8;
+  if (wpb > cap) wpb = cap;
   if (wpb < 1) wpb = 1;
   const int64_t blocks = (args.p + wpb - 1) / wpb;
-  int kwt = 8;
-  while (kwt < kw) kwt *= 2;
   note_launch();
   if (ys_f32)
-    return launch_gram_y<float>(args, (const float *)ys, kwt, u, h_in_smem ? 1 : 0, per_warp, wpb,
+    return launch_gram_y<float>(args, (const float *)ys, u, h_in_smem ? 1 : 0, per_warp, wpb,
                                 blocks, stream);
-  return launch_gram_y<double>(args, (const double *)ys, kwt, u, h_in_smem ? 1 : 0, per_warp, wpb,
+  return launch_gram_y<double>(args, (const double *)ys, u, h_in_smem ? 1 : 0, per_warp, wpb,
                                blocks, stream);
 }
 
