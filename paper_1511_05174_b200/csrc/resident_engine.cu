@@ -23,6 +23,15 @@ constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 // FULL: candidate jl of lane l is atom l + 32u (mode 0) -> compile-time
 // shared-memory offsets in the correlation loop.  R signals per warp share
 // every dictionary element loaded from shared memory (R FMAs per LDS).
+//
+// Per signal (shared memory, doubles): r (n), L^{-1} (k_width rows, odd
+// stride), z, w, g, x (k_width each), support ids.  Taken bits, candidate
+// ids and correlations live in registers.  Per iteration: argmax (fmax
+// butterfly + redux.min for the lowest index among equal maxima), Cholesky
+// append through the Gram row (w = L^{-1} g, d^2 = |d_new|^2 - |w|^2), the
+// new L^{-1} row, and the residual update r -= z_k q_k with
+// q_k = sum_l L^{-1}[k][l] d_{s_l} read from the resident atoms; the
+// coefficients x = L^{-T} z are formed once at the end.
 template <typename YT, int U, bool FULL, int R>
 __global__ void __launch_bounds__(512, 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
@@ -55,33 +64,29 @@ __global__ void __launch_bounds__(512, 1)
   for (int64_t p0 = ((int64_t)blockIdx.x * nwarps + warp) * R; p0 < P;
        p0 += (int64_t)gridDim.x * nwarps * R) {
     // ---- per-signal setup
-    int S[R], kmax[R], kdone[R];
+    int kmax[R], kdone[R], S[R];
     int64_t scans[R];
     double tol[R], rnorm[R];
     bool live[R], delegate[R];
+    unsigned tk[R];  // bit u: candidate lane + 32u taken or beyond S
     int cid[R][U];
 #pragma unroll
     for (int q = 0; q < R; q++) {
       const int64_t p = p0 + q;
-      double *y = sbase + q * per_sig;
-      double *r = y + n;
-      uint32_t *taken = (uint32_t *)(r + n + kw * ldl + 5 * kw);
+      double *r = sbase + q * per_sig;
       const bool valid = p < P;
       S[q] = valid ? (int)cs.count(p) : 0;
       kmax[q] = valid ? (int)cs.budget(p, a.k_max, n) : 0;
+      tk[q] = 0u;
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int jl = lane + 32 * u;
         cid[q][u] = FULL ? jl : (jl < S[q] ? (int)cs.id(p, jl) : Tp - 1);
+        if (jl >= S[q]) tk[q] |= 1u << u;
       }
-      for (int i = lane; i < n; i += 32) {
-        const double v = valid ? (double)ys[p * n + i] : 0.0;
-        y[i] = v;
-        r[i] = v;
-      }
-      for (int w = lane; w < (S[q] + 31) / 32; w += 32) taken[w] = 0u;
+      for (int i = lane; i < n; i += 32) r[i] = valid ? (double)ys[p * n + i] : 0.0;
       __syncwarp();
-      const double ynorm = sqrt(dot4_quad(y, y, n, lane));  // reference order (_kernels.py:71)
+      const double ynorm = sqrt(dot4_quad(r, r, n, lane));  // reference order (_kernels.py:71)
       tol[q] = valid ? eps[p] : 0.0;
       rnorm[q] = ynorm;
       kdone[q] = 0;
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(512, 1)
       for (int i = 0; i < n; i++) {
         double ri[R];
 #pragma unroll
-        for (int q = 0; q < R; q++) ri[q] = sbase[q * per_sig + n + i];
+        for (int q = 0; q < R; q++) ri[q] = sbase[q * per_sig + i];
         const double *row = col + i * Tp;
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -125,52 +130,44 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
       for (int q = 0; q < R; q++) {
         if (!live[q]) continue;
-        const int64_t p = p0 + q;
-        double *y = sbase + q * per_sig;
-        double *r = y + n;
+        double *r = sbase + q * per_sig;
         double *lin = r + n;
         double *zv = lin + kw * ldl;
         double *wv = zv + kw;
-        double *xv = wv + kw;
-        double *gv = xv + kw;
-        int *sup = (int *)(gv + kw);
-        uint32_t *taken = (uint32_t *)(gv + 2 * kw);
+        double *gv = wv + kw;
+        int *sup = (int *)(gv + 2 * kw);
         scans[q] += S[q] - k;
-        double best = -1.0, cbest = 0.0;
-        int bestj = -1;
+        // ---- selection: max |c| over available candidates, ties -> lowest index
+        double best = -1.0;
+        unsigned bj = 0xffffffffu;
 #pragma unroll
         for (int u = 0; u < U; u++) {
-          const int jl = lane + 32 * u;
-          if (jl < S[q] && !((taken[jl >> 5] >> (jl & 31)) & 1u)) {
-            const double v = fabs(acc[q][u]);
-            if (v > best) {
-              best = v;
-              bestj = jl;
-              cbest = acc[q][u];
-            }
+          const double v = fabs(acc[q][u]);
+          if (!((tk[q] >> u) & 1u) && v > best) {
+            best = v;
+            bj = lane + 32 * u;
           }
         }
+        double m = best;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(CDB_FULL_MASK, best, o);
-          const int oj = __shfl_xor_sync(CDB_FULL_MASK, bestj, o);
-          const double oc = __shfl_xor_sync(CDB_FULL_MASK, cbest, o);
-          if (oj >= 0 && (bestj < 0 || ov > best || (ov == best && oj < bestj))) {
-            best = ov;
-            bestj = oj;
-            cbest = oc;
-          }
-        }
-        if (bestj < 0 || best <= 0.0) {  // _kernels.py:104
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+        if (!(m > 0.0)) {  // nothing left, or best <= 0 (_kernels.py:104)
           live[q] = false;
           continue;
         }
-        const int nid = FULL ? bestj : (int)cs.id(p, bestj);
-        if (lane == 0) {
-          taken[bestj >> 5] |= 1u << (bestj & 31);
-          sup[k] = nid;
-        }
-        __syncwarp();
+        const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+        const int ub = bestj >> 5, owner = bestj & 31;
+        double my_c = 0.0;
+        int my_id = 0;
+#pragma unroll
+        for (int u = 0; u < U; u++)
+          if (u == ub) {
+            my_c = acc[q][u];
+            my_id = cid[q][u];
+          }
+        const double cbest = __shfl_sync(CDB_FULL_MASK, my_c, owner);
+        const int nid = FULL ? bestj : __shfl_sync(CDB_FULL_MASK, my_id, owner);
+        if (lane == owner) tk[q] |= 1u << ub;
         // ---- Cholesky append: g_l = <d_{s_l}, d_new> (Gram row gather, or a
         // dot over the resident atoms when no Gram matrix is staged)
         if (gram) {
@@ -184,9 +181,11 @@ __global__ void __launch_bounds__(512, 1)
             gv[l] = g;
           }
         }
+        if (lane == 0) sup[k] = nid;
         __syncwarp();
         for (int l = lane; l < k; l += 32) {
           double accw = 0.0;
+#pragma unroll 4
           for (int i = 0; i <= l; i++) accw = fma(lin[l * ldl + i], gv[i], accw);
           wv[l] = accw;
         }
@@ -201,7 +200,7 @@ __global__ void __launch_bounds__(512, 1)
           live[q] = false;
           continue;
         }
-        const double inv_d = 1.0 / sqrt(d2);
+        const double inv_d = rsqrt(d2);
         const double zk = cbest * inv_d;  // q_k^T y = q_k^T r = <d_new, r> / d
         for (int i = lane; i <= k; i += 32) {
           double v;
@@ -209,6 +208,7 @@ __global__ void __launch_bounds__(512, 1)
             v = inv_d;
           } else {
             double accl = 0.0;
+#pragma unroll 4
             for (int l = i; l < k; l++) accl = fma(wv[l], lin[l * ldl + i], accl);
             v = -accl * inv_d;
           }
@@ -217,20 +217,15 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) zv[k] = zk;
         __syncwarp();
         kdone[q] = k + 1;
-        for (int i = lane; i <= k; i += 32) {
-          double accx = 0.0;
-#pragma unroll 4
-          for (int l = i; l <= k; l++) accx = fma(lin[l * ldl + i], zv[l], accx);
-          xv[i] = accx;
-        }
-        __syncwarp();
-        // ---- residual r = y - D_S x (fp64) and its norm; stop test
+        // ---- residual r -= z_k q_k,  q_k = sum_l L^{-1}[k][l] d_{s_l}; stop test
+        const double *lk = lin + k * ldl;
         double rr = 0.0;
         for (int i = lane; i < n; i += 32) {
-          double rv = y[i];
           const double *row = Dt + i * Tp;
+          double qv = 0.0;
 #pragma unroll 4
-          for (int l = 0; l <= k; l++) rv = fma(-xv[l], row[sup[l]], rv);
+          for (int l = 0; l <= k; l++) qv = fma(lk[l], row[sup[l]], qv);
+          const double rv = fma(-zk, qv, r[i]);
           r[i] = rv;
           rr = fma(rv, rv, rr);
         }
@@ -239,7 +234,7 @@ __global__ void __launch_bounds__(512, 1)
         if (rnorm[q] <= tol[q]) live[q] = false;
       }
     }
-    // ---- outputs
+    // ---- outputs: x = L^{-T} z (pick order)
 #pragma unroll
     for (int q = 0; q < R; q++) {
       const int64_t p = p0 + q;
@@ -248,17 +243,20 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) a.status[p] |= ST_DELEGATE;
         continue;
       }
-      double *y = sbase + q * per_sig;
-      double *xv = y + 2 * n + kw * ldl + 2 * kw;
-      int *sup = (int *)(xv + 2 * kw);
+      double *lin = sbase + q * per_sig + n;
+      double *zv = lin + kw * ldl;
+      int *sup = (int *)(zv + 4 * kw);
       int64_t *out_sel = a.out_sel + p * kw;
       double *out_coef = a.out_coef + p * kw;
+      const int kd = kdone[q];
       for (int j = lane; j < kw; j += 32) {
-        out_sel[j] = j < kdone[q] ? sup[j] : -1;
-        out_coef[j] = j < kdone[q] ? xv[j] : 0.0;
+        double x = 0.0;
+        for (int l = j; l < kd; l++) x = fma(lin[l * ldl + j], zv[l], x);
+        out_sel[j] = j < kd ? sup[j] : -1;
+        out_coef[j] = j < kd ? x : 0.0;
       }
       if (lane == 0) {
-        a.out_count[p] = kdone[q];
+        a.out_count[p] = kd;
         a.out_rnorm[p] = rnorm[q];
         a.out_scans[p] = scans[q];
         a.out_flag[p] = 0;
@@ -295,7 +293,8 @@ cudaError_t launch_t(const ResidentArgs &a, const YT *ys, int u, int threads, si
 }  // namespace
 
 int64_t resident_warp_doubles(int64_t n, int64_t kw, int64_t max_cands) {
-  return 2 * n + kw * (kw | 1) + 6 * kw + ((max_cands + 63) / 64) + 2;
+  (void)max_cands;
+  return n + kw * (kw | 1) + 5 * kw + 1;
 }
 
 // Row stride of the transposed dictionary: at least one zero column and the
