@@ -265,6 +265,162 @@ __global__ void __launch_bounds__(256) alpha0_routed_kernel(
   }
 }
 
+// Shared-memory aggregated routing: a CTA histograms its chunk of signals'
+// (signal, parent) pairs in shared memory and touches each global counter
+// once per parent it saw (instead of once per pair).
+constexpr int kRouteChunk = 1024;  // signals per CTA
+
+__global__ void __launch_bounds__(256) route_count_smem_kernel(
+    const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb, int64_t p, int64_t k1,
+    int t_low, int *__restrict__ count) {
+  extern __shared__ int hist[];
+  for (int b = threadIdx.x; b < t_low; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const int64_t s0 = (int64_t)blockIdx.x * kRouteChunk;
+  const int64_t s1 = s0 + kRouteChunk < p ? s0 + kRouteChunk : p;
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x)
+    for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&hist[blocks[s * k1 + b]], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < t_low; b += blockDim.x)
+    if (hist[b]) atomicAdd(&count[b], hist[b]);
+}
+
+__global__ void __launch_bounds__(256) route_fill_smem_kernel(
+    const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb, int64_t p, int64_t k1,
+    int t_low, unsigned long long *__restrict__ cursor, int64_t *__restrict__ pairs) {
+  extern __shared__ unsigned long long sh[];  // base[t_low] | hist[t_low] (as int)
+  unsigned long long *base = sh;
+  int *hist = (int *)(sh + t_low);
+  for (int b = threadIdx.x; b < t_low; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const int64_t s0 = (int64_t)blockIdx.x * kRouteChunk;
+  const int64_t s1 = s0 + kRouteChunk < p ? s0 + kRouteChunk : p;
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x)
+    for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&hist[blocks[s * k1 + b]], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < t_low; b += blockDim.x) {
+    base[b] = hist[b] ? atomicAdd(&cursor[b], (unsigned long long)hist[b]) : 0ull;
+    hist[b] = 0;
+  }
+  __syncthreads();
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x)
+    for (int64_t b = 0; b < nb[s]; b++) {
+      const int64_t blk = blocks[s * k1 + b];
+      pairs[base[blk] + atomicAdd(&hist[blk], 1)] = s * k1 + b;
+    }
+}
+
+// Warp per routed pair, the parent's QT children held in registers: lane
+// owns the NPL = N/32 coordinates {VW*lane + 32*VW*v + e}, so each signal row
+// is read with coalesced VW-wide loads; QT*NPL fp64 FMAs per lane, then a
+// reduce-scatter butterfly leaves child c's sum in lanes with the matching
+// bits.  A CTA covers 1/split of one parent's pairs.
+template <int QT>
+__device__ __forceinline__ double reduce_scatter(double (&v)[QT], int lane, int &child) {
+  child = 0;
+  int o = 16;
+#pragma unroll
+  for (int h = QT / 2; h >= 1; h >>= 1, o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      const double send = upper ? v[i] : v[i + h];
+      const double keep = upper ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(CDB_FULL_MASK, send, o);
+    }
+    if (upper) child += h;
+  }
+  double r = v[0];
+  for (; o >= 1; o >>= 1) r += __shfl_xor_sync(CDB_FULL_MASK, r, o);
+  return r;
+}
+
+template <typename YT, int QT, int NPL>
+__global__ void __launch_bounds__(128) alpha0_warp_kernel(
+    const double *__restrict__ d64, int n, const YT *__restrict__ ys,
+    const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t k1,
+    int64_t smax, int split, double *__restrict__ alpha0) {
+  constexpr int VW = NPL < 4 ? NPL : 4;  // floats per vector load
+  constexpr int NV = NPL / VW;
+  const int parent = blockIdx.x / split, part = blockIdx.x % split;
+  const int64_t lo = offs[parent], cnt = offs[parent + 1] - lo;
+  const int64_t a = lo + cnt * part / split, b = lo + cnt * (part + 1) / split;
+  if (a >= b) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  double ch[QT][NPL];
+#pragma unroll
+  for (int c = 0; c < QT; c++)
+#pragma unroll
+    for (int v = 0; v < NV; v++)
+#pragma unroll
+      for (int e = 0; e < VW; e++)
+        ch[c][v * VW + e] = __ldg(d64 + ((int64_t)parent * QT + c) * n + VW * lane + 32 * VW * v + e);
+  for (int64_t e0 = a + warp; e0 < b; e0 += nwarps) {
+    const int64_t pr = pairs[e0];
+    const int64_t sig = pr / k1, slot = pr % k1;
+    const YT *y = ys + sig * n;
+    double yv[NPL];
+#pragma unroll
+    for (int v = 0; v < NV; v++) {
+      const int i = VW * lane + 32 * VW * v;
+      if constexpr (sizeof(YT) == 4 && VW == 4) {
+        const float4 f = *reinterpret_cast<const float4 *>(y + i);
+        yv[v * 4 + 0] = f.x;
+        yv[v * 4 + 1] = f.y;
+        yv[v * 4 + 2] = f.z;
+        yv[v * 4 + 3] = f.w;
+      } else if constexpr (sizeof(YT) == 4 && VW == 2) {
+        const float2 f = *reinterpret_cast<const float2 *>(y + i);
+        yv[v * 2 + 0] = f.x;
+        yv[v * 2 + 1] = f.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < VW; e++) yv[v * VW + e] = (double)y[i + e];
+      }
+    }
+    double acc[QT];
+#pragma unroll
+    for (int c = 0; c < QT; c++) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < NPL; t++) s = fma(ch[c][t], yv[t], s);
+      acc[c] = s;
+    }
+    int child;
+    const double r = reduce_scatter<QT>(acc, lane, child);
+    if ((lane & (32 / QT - 1)) == 0) alpha0[sig * smax + slot * QT + child] = r;
+  }
+}
+
+template <typename YT, int QT, int NPL>
+cudaError_t launch_alpha0_warp(const double *d64, int64_t t_low, int64_t n, const YT *ys,
+                               const int64_t *offs, const int64_t *pairs, int64_t k1,
+                               int64_t smax, double *alpha0, cudaStream_t stream) {
+  const int split = 8;
+  alpha0_warp_kernel<YT, QT, NPL><<<(unsigned)(t_low * split), 128, 0, stream>>>(
+      d64, (int)n, ys, offs, pairs, k1, smax, split, alpha0);
+  return cudaGetLastError();
+}
+
+// The register path when the parent's children fit 64 fp64 registers per
+// lane and N is 64, 128 or 256 (else the shared-memory kernel above).
+template <typename YT>
+bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t n, int64_t q, const YT *ys,
+                     const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
+                     double *alpha0, cudaStream_t stream, cudaError_t &err) {
+#define CDB_A0W(QQ, NN)                                                                      \
+  if (q == QQ && n == 32 * NN) {                                                             \
+    err = launch_alpha0_warp<YT, QQ, NN>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0,   \
+                                         stream);                                            \
+    return true;                                                                             \
+  }
+  CDB_A0W(1, 2) CDB_A0W(2, 2) CDB_A0W(4, 2) CDB_A0W(8, 2) CDB_A0W(16, 2)
+  CDB_A0W(1, 4) CDB_A0W(2, 4) CDB_A0W(4, 4) CDB_A0W(8, 4) CDB_A0W(16, 4)
+  CDB_A0W(1, 8) CDB_A0W(2, 8) CDB_A0W(4, 8) CDB_A0W(8, 8)
+#undef CDB_A0W
+  return false;
+}
+
 template <typename YT, int QT>
 cudaError_t launch_alpha0_q(const double *d64, int64_t t_low, int64_t n, const YT *ys,
                             const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
@@ -403,14 +559,29 @@ cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int
   int64_t *pairs = (int64_t *)w;
   cudaError_t e = cudaMemsetAsync(count, 0, t_low * 4, stream);
   if (e != cudaSuccess) return e;
-  route_count_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1, count);
+  const bool smem_route = t_low * 12 <= 48 * 1024;
+  const unsigned rgrid = (unsigned)((p + kRouteChunk - 1) / kRouteChunk);
+  if (smem_route)
+    route_count_smem_kernel<<<rgrid, 256, t_low * 4, stream>>>(blocks, nb, p, k1, (int)t_low,
+                                                               count);
+  else
+    route_count_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1, count);
   route_scan_kernel<<<1, 1024, 0, stream>>>(count, t_low, offs, cursor);
-  route_fill_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1,
-                                                            (unsigned long long *)cursor, pairs);
-  e = ys_f32 ? launch_alpha0<float>(d64, t_low, n, q, (const float *)ys, offs, pairs, k1, smax,
-                                     alpha0, stream)
-             : launch_alpha0<double>(d64, t_low, n, q, (const double *)ys, offs, pairs, k1, smax,
-                                      alpha0, stream);
+  if (smem_route)
+    route_fill_smem_kernel<<<rgrid, 256, t_low * 12, stream>>>(
+        blocks, nb, p, k1, (int)t_low, (unsigned long long *)cursor, pairs);
+  else
+    route_fill_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1,
+                                                              (unsigned long long *)cursor, pairs);
+  bool done = ys_f32 ? try_alpha0_warp<float>(d64, t_low, n, q, (const float *)ys, offs, pairs, k1,
+                                              smax, alpha0, stream, e)
+                     : try_alpha0_warp<double>(d64, t_low, n, q, (const double *)ys, offs, pairs,
+                                               k1, smax, alpha0, stream, e);
+  if (!done)
+    e = ys_f32 ? launch_alpha0<float>(d64, t_low, n, q, (const float *)ys, offs, pairs, k1, smax,
+                                      alpha0, stream)
+               : launch_alpha0<double>(d64, t_low, n, q, (const double *)ys, offs, pairs, k1, smax,
+                                       alpha0, stream);
   if (e != cudaSuccess) return e;
   note_launch(4);
   return cudaGetLastError();
