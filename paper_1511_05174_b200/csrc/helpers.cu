@@ -194,7 +194,7 @@ __global__ void route_fill_kernel(const int64_t *__restrict__ blocks, const int6
   if (s >= p) return;
   for (int64_t b = 0; b < nb[s]; b++) {
     const int64_t pos = (int64_t)atomicAdd(&cursor[blocks[s * k1 + b]], 1ull);
-    pairs[pos] = s * k1 + b;
+    pairs[pos] = (s << 16) | b;  // (signal, slot) pair
   }
 }
 
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(256) alpha0_routed_kernel(
   for (int64_t e0 = lo + 2 * threadIdx.x; e0 < hi; e0 += 2 * blockDim.x) {
     const bool two = e0 + 1 < hi;
     const int64_t pr0 = pairs[e0], pr1 = two ? pairs[e0 + 1] : pr0;
-    const YT *y0 = ys + (pr0 / k1) * n;
-    const YT *y1 = ys + (pr1 / k1) * n;
+    const YT *y0 = ys + (pr0 >> 16) * n;
+    const YT *y1 = ys + (pr1 >> 16) * n;
     double a0[QT], a1[QT];
 #pragma unroll
     for (int c = 0; c < QT; c++) {
@@ -254,11 +254,11 @@ __global__ void __launch_bounds__(256) alpha0_routed_kernel(
         a1[c] = fma(dv, v1, a1[c]);
       }
     }
-    double *o0 = alpha0 + (pr0 / k1) * smax + (pr0 % k1) * QT;
+    double *o0 = alpha0 + (pr0 >> 16) * smax + (pr0 & 0xffff) * QT;
 #pragma unroll
     for (int c = 0; c < QT; c++) o0[c] = a0[c];
     if (two) {
-      double *o1 = alpha0 + (pr1 / k1) * smax + (pr1 % k1) * QT;
+      double *o1 = alpha0 + (pr1 >> 16) * smax + (pr1 & 0xffff) * QT;
 #pragma unroll
       for (int c = 0; c < QT; c++) o1[c] = a1[c];
     }
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256) route_fill_smem_kernel(
   for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x)
     for (int64_t b = 0; b < nb[s]; b++) {
       const int64_t blk = blocks[s * k1 + b];
-      pairs[base[blk] + atomicAdd(&hist[blk], 1)] = s * k1 + b;
+      pairs[base[blk] + atomicAdd(&hist[blk], 1)] = (s << 16) | b;
     }
 }
 
@@ -335,7 +335,10 @@ __device__ __forceinline__ double reduce_scatter(double (&v)[QT], int lane, int 
   return r;
 }
 
-template <typename YT, int QT, int NPL>
+// HV: the parent's children are split over HV warps (QT / HV each), which
+// halves the per-lane registers for QT >= 4 so more warps stay resident; a
+// signal row is then read by HV warps (L1/L2 hits after the first).
+template <typename YT, int QT, int NPL, int HV>
 __global__ void __launch_bounds__(128) alpha0_warp_kernel(
     const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t k1,
@@ -346,20 +349,25 @@ __global__ void __launch_bounds__(128) alpha0_warp_kernel(
   const int64_t lo = offs[parent], cnt = offs[parent + 1] - lo;
   const int64_t a = lo + cnt * part / split, b = lo + cnt * (part + 1) / split;
   if (a >= b) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  double ch[QT][NPL];
+  constexpr int CH = QT / HV;  // children per warp
+  const int lane = threadIdx.x & 31, w0 = threadIdx.x >> 5;
+  const int half = w0 % HV, warp = w0 / HV, nwarps = (blockDim.x >> 5) / HV;
+  double ch[CH][NPL];
 #pragma unroll
-  for (int c = 0; c < QT; c++)
+  for (int c = 0; c < CH; c++)
 #pragma unroll
     for (int v = 0; v < NV; v++)
 #pragma unroll
       for (int e = 0; e < VW; e++)
-        ch[c][v * VW + e] = __ldg(d64 + ((int64_t)parent * QT + c) * n + VW * lane + 32 * VW * v + e);
-  for (int64_t e0 = a + warp; e0 < b; e0 += nwarps) {
-    const int64_t pr = pairs[e0];
-    const int64_t sig = pr / k1, slot = pr % k1;
-    const YT *y = ys + sig * n;
-    double yv[NPL];
+        ch[c][v * VW + e] = __ldg(d64 + ((int64_t)parent * QT + half * CH + c) * n + VW * lane +
+                                  32 * VW * v + e);
+  // warp w takes the contiguous pairs [wa, wb); pair ids arrive 32 at a time
+  // (one coalesced load, then shuffles) and the signal rows of the next two
+  // pairs are loaded while the current two are coded
+  const int64_t per = (b - a + nwarps - 1) / nwarps;
+  const int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
+  auto load_row = [&](int64_t pr, float (&yv)[NPL]) {
+    const YT *y = ys + (pr >> 16) * n;
 #pragma unroll
     for (int v = 0; v < NV; v++) {
       const int i = VW * lane + 32 * VW * v;
@@ -375,20 +383,58 @@ __global__ void __launch_bounds__(128) alpha0_warp_kernel(
         yv[v * 2 + 1] = f.y;
       } else {
 #pragma unroll
-        for (int e = 0; e < VW; e++) yv[v * VW + e] = (double)y[i + e];
+        for (int e = 0; e < VW; e++) yv[v * VW + e] = (float)y[i + e];
       }
     }
-    double acc[QT];
+  };
+  // code two pairs at once: 2 CH independent accumulation chains
+  auto code2 = [&](int64_t pra, const float (&ya)[NPL], int64_t prb, const float (&yb)[NPL],
+                   bool second) {
+    double acc[2 * CH];
 #pragma unroll
-    for (int c = 0; c < QT; c++) {
-      double s = 0.0;
+    for (int c = 0; c < 2 * CH; c++) acc[c] = 0.0;
 #pragma unroll
-      for (int t = 0; t < NPL; t++) s = fma(ch[c][t], yv[t], s);
-      acc[c] = s;
+    for (int t = 0; t < NPL; t++) {
+      const double va = (double)ya[t], vb = (double)yb[t];
+#pragma unroll
+      for (int c = 0; c < CH; c++) {
+        acc[c] = fma(ch[c][t], va, acc[c]);
+        acc[CH + c] = fma(ch[c][t], vb, acc[CH + c]);
+      }
     }
+    // reduce-scatter of both (2 CH values: pair index is the top level)
     int child;
-    const double r = reduce_scatter<QT>(acc, lane, child);
-    if ((lane & (32 / QT - 1)) == 0) alpha0[sig * smax + slot * QT + child] = r;
+    const double r = reduce_scatter<2 * CH>(acc, lane, child);
+    const int pi = child / CH;  // 0: pair a, 1: pair b
+    const int c = half * CH + child % CH;
+    const int64_t pr = pi ? prb : pra;
+    if ((lane & (32 / (2 * CH) - 1)) == 0 && (pi == 0 || second))
+      alpha0[(pr >> 16) * smax + (pr & 0xffff) * QT + c] = r;
+  };
+  for (int64_t e0 = wa; e0 < wb; e0 += 32) {
+    const int m = wb - e0 < 32 ? (int)(wb - e0) : 32;
+    const int64_t mine = lane < m ? pairs[e0 + lane] : 0;
+    float ya[NPL], yb[NPL];
+    int64_t pa = __shfl_sync(CDB_FULL_MASK, (long long)mine, 0);
+    int64_t pb = __shfl_sync(CDB_FULL_MASK, (long long)mine, 1 < m ? 1 : 0);
+    load_row(pa, ya);
+    load_row(pb, yb);
+    for (int j = 0; j < m; j += 2) {
+      float ca[NPL], cb[NPL];
+#pragma unroll
+      for (int t = 0; t < NPL; t++) {
+        ca[t] = ya[t];
+        cb[t] = yb[t];
+      }
+      const int64_t qa = pa, qb = pb;
+      if (j + 2 < m) {
+        pa = __shfl_sync(CDB_FULL_MASK, (long long)mine, j + 2);
+        pb = __shfl_sync(CDB_FULL_MASK, (long long)mine, j + 3 < m ? j + 3 : j + 2);
+        load_row(pa, ya);
+        load_row(pb, yb);
+      }
+      code2(qa, ca, qb, cb, j + 1 < m);
+    }
   }
 }
 
@@ -397,7 +443,8 @@ cudaError_t launch_alpha0_warp(const double *d64, int64_t t_low, int64_t n, cons
                                const int64_t *offs, const int64_t *pairs, int64_t k1,
                                int64_t smax, double *alpha0, cudaStream_t stream) {
   const int split = 8;
-  alpha0_warp_kernel<YT, QT, NPL><<<(unsigned)(t_low * split), 128, 0, stream>>>(
+  constexpr int HV = 1;  // splitting children over 2 warps measured slower (0.76 vs 0.63 ms, cfg 1)
+  alpha0_warp_kernel<YT, QT, NPL, HV><<<(unsigned)(t_low * split), 128, 0, stream>>>(
       d64, (int)n, ys, offs, pairs, k1, smax, split, alpha0);
   return cudaGetLastError();
 }
