@@ -13,34 +13,46 @@ struct Shape4 {
 };
 
 // Block mean of row-major fine patches (crossdict/scaling.py:99-116,
-// downsample_columns), one thread per (signal, coarse cell).
+// downsample_columns).  A CTA stages `spb` signal rows in shared memory with
+// coalesced loads and builds once the fine index of every (coarse cell,
+// in-block offset) -- offsets in row-major order, the summation order the
+// oracle restates -- so the per-output work is `block` shared-memory reads.
 template <typename YT>
-__global__ void downsample_kernel(const YT *__restrict__ ys, int64_t p, int64_t n, Shape4 sh,
-                                  double *__restrict__ out, int64_t n_low) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= p * n_low) return;
-  const int64_t sig = gid / n_low, cell = gid % n_low;
-  int64_t cc[4] = {0, 0, 0, 0};
-  int64_t rem = cell;
-  for (int d = sh.rank - 1; d >= 0; d--) {
-    cc[d] = rem % sh.coarse[d];
-    rem /= sh.coarse[d];
-  }
-  int64_t block = 1;
-  for (int d = 0; d < sh.rank; d++) block *= sh.fac[d];
-  double acc = 0.0;
-  for (int64_t b = 0; b < block; b++) {
-    int64_t off[4] = {0, 0, 0, 0};
-    int64_t r = b;
+__global__ void __launch_bounds__(256) downsample_kernel(const YT *__restrict__ ys, int64_t p,
+                                                         int n, Shape4 sh,
+                                                         double *__restrict__ out, int n_low,
+                                                         int spb) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  int *tab = (int *)dsm;                       // n_low * block fine indices
+  YT *rows = (YT *)(dsm + ((size_t)n * 4 + 15) / 16 * 16);  // spb x n
+  int block = 1;
+  for (int d = 0; d < sh.rank; d++) block *= (int)sh.fac[d];
+  for (int e = threadIdx.x; e < n_low * block; e += blockDim.x) {
+    const int cell = e / block, bo = e % block;
+    int cc[4] = {0, 0, 0, 0}, off[4] = {0, 0, 0, 0};
+    int rem = cell, r = bo;
     for (int d = sh.rank - 1; d >= 0; d--) {
-      off[d] = r % sh.fac[d];
-      r /= sh.fac[d];
+      cc[d] = rem % (int)sh.coarse[d];
+      rem /= (int)sh.coarse[d];
+      off[d] = r % (int)sh.fac[d];
+      r /= (int)sh.fac[d];
     }
-    int64_t idx = 0;
-    for (int d = 0; d < sh.rank; d++) idx = idx * sh.fine[d] + cc[d] * sh.fac[d] + off[d];
-    acc += (double)ys[sig * n + idx];
+    int idx = 0;
+    for (int d = 0; d < sh.rank; d++) idx = idx * (int)sh.fine[d] + cc[d] * (int)sh.fac[d] + off[d];
+    tab[e] = idx;
   }
-  out[sig * n_low + cell] = acc / (double)block;
+  const int64_t s0 = (int64_t)blockIdx.x * spb;
+  const int ns = p - s0 < spb ? (int)(p - s0) : spb;
+  for (int64_t e = threadIdx.x; e < (int64_t)ns * n; e += blockDim.x) rows[e] = ys[s0 * n + e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < ns * n_low; e += blockDim.x) {
+    const int sl = e / n_low, cell = e % n_low;
+    const YT *row = rows + (size_t)sl * n;
+    const int *t = tab + cell * block;
+    double acc = 0.0;
+    for (int b = 0; b < block; b++) acc += (double)row[t[b]];
+    out[(s0 + sl) * n_low + cell] = acc / (double)block;
+  }
 }
 
 // eps_p = rel * ||y_p|| (pursuit.py:437), one warp per signal.
@@ -514,11 +526,26 @@ cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
     sh.fac[d] = factors[d];
     sh.coarse[d] = fine_shape[d] / factors[d];
   }
-  const unsigned g = blocks_for(p * n_low, 256);
-  if (ys_f32)
-    downsample_kernel<float><<<g, 256, 0, stream>>>((const float *)ys, p, n, sh, y_low, n_low);
-  else
-    downsample_kernel<double><<<g, 256, 0, stream>>>((const double *)ys, p, n, sh, y_low, n_low);
+  const int64_t esz = ys_f32 ? 4 : 8;
+  int spb = (int)(32768 / (n * esz));
+  if (spb < 1) spb = 1;
+  const size_t smem = (size_t)(n * 4 + 15) / 16 * 16 + (size_t)spb * n * esz;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const unsigned g = (unsigned)((p + spb - 1) / spb);
+  cudaError_t e;
+  if (ys_f32) {
+    e = cudaFuncSetAttribute(downsample_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    downsample_kernel<float><<<g, 256, smem, stream>>>((const float *)ys, p, (int)n, sh, y_low,
+                                                       (int)n_low, spb);
+  } else {
+    e = cudaFuncSetAttribute(downsample_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    downsample_kernel<double><<<g, 256, smem, stream>>>((const double *)ys, p, (int)n, sh, y_low,
+                                                        (int)n_low, spb);
+  }
   note_launch();
   return cudaGetLastError();
 }
