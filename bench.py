@@ -40,6 +40,15 @@ METRIC = "signals/sec for zero-tree OMP and full OMP at 1/2/4/8 B200; % of roofl
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+def load_traffic():
+    """DRAM bytes per launch of each profiled kernel (tools/ncu_summary.py output)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r1_ncu_traffic.json")) as f:
+            return {k: v for k, v in json.load(f).items() if not k.startswith("_")}
+    except (OSError, ValueError):
+        return {}
+
+
 def load_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -50,19 +59,38 @@ def load_peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+    """SM clocks and throttle reasons sampled during a region: NVML polled
+    every 5 ms from a thread (the data nvidia-smi reports), or nvidia-smi
+    -lms 100 when pynvml is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set(reasons))
         self.proc = None
         self.thread = None
+        self.stop_flag = threading.Event()
+        self.source = None
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.gpu
+            if vis and vis.split(",")[self.gpu].strip().isdigit():
+                idx = int(vis.split(",")[self.gpu])
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.source = "nvml"
+            self.thread = threading.Thread(target=self._poll_nvml, args=(pynvml, h), daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -70,16 +98,36 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.source = "nvidia-smi"
+        self.thread = threading.Thread(target=self._read_smi, daemon=True)
         self.thread.start()
 
-    def _read(self):
+    def _poll_nvml(self, nv, h):
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self.stop_flag.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, smax, {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+            if len(parts) != 6:
+                continue
+            try:
+                rs = {nm for i, nm in enumerate(self.NAMES) if parts[2 + i].lower().startswith("active")}
+                self.samples.append((float(parts[0]), float(parts[1]), rs))
+            except ValueError:
+                continue
 
     def stop(self):
+        self.stop_flag.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -88,21 +136,11 @@ class ClockSampler:
                 self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        sm = []
-        smax = None
-        for s in self.samples:
-            try:
-                sm.append(float(s[0]))
-                smax = float(s[1])
-            except ValueError:
-                continue
-            for i, nm in enumerate(names):
-                if s[2 + i].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [x[0] for x in self.samples]
+        reasons = set().union(*[x[2] for x in self.samples]) if self.samples else set()
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": self.samples[-1][1] if self.samples else None,
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 # ------------------------------------------------------------------ helpers
@@ -139,18 +177,22 @@ def run_oracle_zero_tree(ci, ys_rows, threads):
                                    rel_tol=W.REL_TOL, nthreads=threads)
 
 
-def cpu_rate(ci, threads, budget_s=12.0, max_signals=65536):
-    """Oracle zero-tree sig/s on a bounded sample (calibrated to ~budget_s)."""
-    probe = W.signals(ci, 0, 256)
+def cpu_rate(ci, threads, ys, budget_s=24.0):
+    """Oracle zero-tree sig/s on a bounded sample: whole passes over the
+    config's signals `ys` (the GPU batch) until ~budget_s of CPU time."""
+    probe = ys[:256]
     t0 = time.perf_counter()
     run_oracle_zero_tree(ci, probe, threads)
     rate = 256 / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(max_signals, max(256, rate * budget_s)))
-    ys = W.signals(ci, 0, n)
-    t0 = time.perf_counter()
-    run_oracle_zero_tree(ci, ys, threads)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt
+    target = int(max(256, rate * budget_s))
+    done, dt = 0, 0.0
+    while done < target:
+        m = min(len(ys), target - done)
+        t0 = time.perf_counter()
+        run_oracle_zero_tree(ci, ys[:m], threads)
+        dt += time.perf_counter() - t0
+        done += m
+    return done / dt, done, dt
 
 
 # ------------------------------------------------------------------ reference arm
@@ -277,6 +319,7 @@ def bench_ours(args):
     launches = N.launch_count() - launches0
     clk = clocks.stop()
     engine_full = N.last_run_info()
+    full_scans = ofull["scans"].double().sum().item()
 
     # ---- e2e through the C ABI with pinned host buffers
     yh = torch.from_numpy(ys_host).pin_memory()
@@ -304,38 +347,43 @@ def bench_ours(args):
 
     # ---- roofline of the dominant kernel (zero-tree step), algorithmic flops
     peaks, peaks_kind = load_peaks()
+    traffic_tab = load_traffic()
     low_scans = olo["scans"].double().sum().item()
     high_scans = ohi["scans"].double().sum().item()
     n_low = w.n_signal if phi else w.n_low
-    flops = {
-        "gram_step1": 2.0 * n_low * low_scans + flops_ls(n_low, olo["counts"].cpu().numpy()),
-        "gram_step2": 2.0 * w.n_signal * high_scans + flops_ls(w.n_signal,
-                                                             ohi["counts"].cpu().numpy()),
-    }
+    f_step1 = 2.0 * n_low * low_scans + flops_ls(n_low, olo["counts"].cpu().numpy())
+    f_step2 = 2.0 * w.n_signal * high_scans + flops_ls(w.n_signal, ohi["counts"].cpu().numpy())
+    # algorithmic flops per launch of each OMP kernel (one launch per step per call)
+    flops = {"gram_step1": f_step1, "resident_step1": f_step1, "exact_step1": f_step1,
+             "gram_step2": f_step2, "resident_step2": f_step2, "exact_step2": f_step2}
     dom = max(prof_zt.items(), key=lambda kv: kv[1][0]) if prof_zt else ("none", (1.0, 1))
     dom_name, (dom_ms_total, dom_launches) = dom
     dom_ms = dom_ms_total / max(dom_launches, 1)
     p_emu = peaks["bf16_tflops"] / 6.0
-    dom_flops = flops.get(dom_name, 0.0)
+    dom_flops = flops.get(dom_name, 0.0) * args.steps / max(dom_launches, 1)
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
     roofline = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": p_emu,
-                "unit": "TFLOP/s", "frac": achieved / p_emu if p_emu else None, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / p_emu if p_emu else None,
+                "traffic": traffic_tab.get(dom_name),
                 "basis": "SURVEY §8.0 algorithmic flops 2*N*scans + 4Nk(k-1) + 11Nk per signal "
                          f"(actual scan counts) / mean launch time; peak = {peaks_kind} bf16 "
-                         f"{peaks['bf16_tflops']} TF/s / 6 (3xTF32-emulated fp32, SURVEY §8(d))",
+                         f"{peaks['bf16_tflops']} TF/s / 6 (3xTF32-emulated fp32, SURVEY §8(d)); "
+                         "traffic = DRAM bytes per launch from profiles/r1_ncu_traffic.json",
                 "launch_ms": dom_ms}
-    # full-OMP correlation kernel against the measured bf16 tensor peak
+    # full-OMP correlation kernel against the measured bf16 tensor peak: the
+    # algorithmic correlation flops 2*N*scans (actual scan counts) per launch
     corr = prof_full.get("corr_topk")
     full_roof = None
     if corr:
         c_ms = corr[0] / max(corr[1], 1)
-        # one launch scores every atom of every signal of its chunk
-        c_flops = 2.0 * w.n_signal * w.t_high * P * args.steps * w.k / max(corr[1], 1)
+        c_flops = 2.0 * w.n_signal * full_scans * args.steps / max(corr[1], 1)
         full_roof = {"bound": "tensor", "kernel": "corr_topk",
                      "achieved": c_flops / (c_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
                      "unit": "TFLOP/s",
                      "frac": c_flops / (c_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-                     "traffic": None, "launch_ms": c_ms}
+                     "traffic": traffic_tab.get("corr_topk"), "launch_ms": c_ms,
+                     "basis": "2*N*scans of the full-OMP batch (actual scan counts) / corr_topk "
+                              "time; the bf16 GEMM also scores taken atoms and finished signals"}
 
     zt_value = world * P * args.steps / (zt_ms * 1e-3)
     full_value = world * P * args.steps / (full_ms * 1e-3)
@@ -343,9 +391,10 @@ def bench_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = cpu_threads()
-        rate, n, dt = cpu_rate(ci, threads)
+        rate, n, dt = cpu_rate(ci, threads, ys_host.astype(np.float64))
         cpu = {"value": rate, "unit": "signals/s", "cores": threads, "kind": "port",
-               "sample": f"{n} signals of configs[{ci}] zero-tree OMP in {dt:.1f} s "
+               "sample": f"{n} signals (passes over the {P} benchmark signals) of configs[{ci}] "
+                         f"zero-tree OMP in {dt:.1f} s "
                          f"(oracle/omp_oracle.c restating crossdict's kernel, {threads} threads)"}
 
     if rank == 0:
