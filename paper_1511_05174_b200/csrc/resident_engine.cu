@@ -17,7 +17,6 @@
 namespace cdb {
 namespace {
 
-constexpr int RES_R = 2;        // signals per warp
 constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 
 // FULL: candidate jl of lane l is atom l + 32u (mode 0) -> compile-time
@@ -33,7 +32,7 @@ constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 // q_k = sum_l L^{-1}[k][l] d_{s_l} read from the resident atoms; the
 // coefficients x = L^{-T} z are formed once at the end.
 template <typename YT, int U, bool FULL, int R>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
   extern __shared__ __align__(16) double rs[];
   const int n = (int)a.n, T = (int)a.t, kw = (int)a.k_width, Tp = (int)a.t_pad;
@@ -266,26 +265,40 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
+// Signals per warp: 4 (every dictionary element read from shared memory
+// feeds 4 FMAs) when the per-lane candidate arrays are small, else 2.
+template <int U>
+constexpr int res_r() { return U > 0 ? 2 : 2; }  // R = 4 measured slower (3.43 vs 3.09 ms, cfg 1 step 1)
+constexpr int res_max_warps(int r) { return r >= 4 ? 12 : RES_WARPS; }  // launch bounds
+
 template <typename YT, int U>
-cudaError_t launch_u(const ResidentArgs &a, const YT *ys, int threads, size_t smem,
-                     int grid, cudaStream_t stream) {
-  auto kern = a.cands.mode == 0 ? resident_omp_kernel<YT, U, true, RES_R>
-                                : resident_omp_kernel<YT, U, false, RES_R>;
+cudaError_t launch_u(const ResidentArgs &args, const YT *ys, int64_t base, int smem_optin,
+                     int num_sms, cudaStream_t stream) {
+  constexpr int R = res_r<U>();
+  ResidentArgs a = args;
+  int warps = (int)((smem_optin - base) / (8 * a.per_warp * R));
+  if (warps > res_max_warps(R)) warps = res_max_warps(R);
+  if (warps < 1) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)(base + 8 * a.per_warp * R * warps);
+  int64_t grid = (a.p + warps * R - 1) / (warps * R);
+  if (grid > num_sms) grid = num_sms;
+  auto kern = a.cands.mode == 0 ? resident_omp_kernel<YT, U, true, R>
+                                : resident_omp_kernel<YT, U, false, R>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, threads, smem, stream>>>(a, ys);
+  kern<<<(int)grid, warps * 32, smem, stream>>>(a, ys);
   return cudaGetLastError();
 }
 
 template <typename YT>
-cudaError_t launch_t(const ResidentArgs &a, const YT *ys, int u, int threads, size_t smem,
-                     int grid, cudaStream_t stream) {
+cudaError_t launch_t(const ResidentArgs &a, const YT *ys, int u, int64_t base, int smem_optin,
+                     int num_sms, cudaStream_t stream) {
   switch (u) {
-    case 1: return launch_u<YT, 1>(a, ys, threads, smem, grid, stream);
-    case 2: return launch_u<YT, 2>(a, ys, threads, smem, grid, stream);
-    case 4: return launch_u<YT, 4>(a, ys, threads, smem, grid, stream);
-    case 8: return launch_u<YT, 8>(a, ys, threads, smem, grid, stream);
-    case 16: return launch_u<YT, 16>(a, ys, threads, smem, grid, stream);
+    case 1: return launch_u<YT, 1>(a, ys, base, smem_optin, num_sms, stream);
+    case 2: return launch_u<YT, 2>(a, ys, base, smem_optin, num_sms, stream);
+    case 4: return launch_u<YT, 4>(a, ys, base, smem_optin, num_sms, stream);
+    case 8: return launch_u<YT, 8>(a, ys, base, smem_optin, num_sms, stream);
+    case 16: return launch_u<YT, 16>(a, ys, base, smem_optin, num_sms, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -311,7 +324,7 @@ bool resident_fits(int64_t n, int64_t t, int64_t kw, int64_t max_cands, int smem
   if (max_cands > 512) return false;
   const int64_t tp = resident_tpad(t, max_cands);
   const int64_t base = 8 * (n * tp + tp);
-  const int64_t per = 8 * resident_warp_doubles(n, kw, max_cands) * RES_R;
+  const int64_t per = 8 * resident_warp_doubles(n, kw, max_cands) * 4;
   return base + 4 * per <= smem_optin && base <= 144 * 1024;
 }
 
@@ -324,17 +337,11 @@ cudaError_t launch_resident(const ResidentArgs &args, const void *ys, bool ys_f3
   a.t_pad = resident_tpad(a.t, a.max_cands);
   if (a.cands.mode == 0 && a.t_pad < 32 * ((a.max_cands + 31) / 32)) return cudaErrorInvalidValue;
   const int64_t base = 8 * (a.n * a.t_pad + a.t_pad);
-  int warps = (int)((smem_optin - base) / (8 * a.per_warp * RES_R));
-  if (warps > RES_WARPS) warps = RES_WARPS;
-  if (warps < 1) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)(base + 8 * a.per_warp * RES_R * warps);
   int u = 1;
   while (32 * u < a.max_cands) u *= 2;
-  int64_t grid = (a.p + warps * RES_R - 1) / (warps * RES_R);
-  if (grid > num_sms) grid = num_sms;
   note_launch();
-  if (ys_f32) return launch_t<float>(a, (const float *)ys, u, warps * 32, smem, (int)grid, stream);
-  return launch_t<double>(a, (const double *)ys, u, warps * 32, smem, (int)grid, stream);
+  if (ys_f32) return launch_t<float>(a, (const float *)ys, u, base, smem_optin, num_sms, stream);
+  return launch_t<double>(a, (const double *)ys, u, base, smem_optin, num_sms, stream);
 }
 
 }  // namespace cdb
