@@ -10,12 +10,37 @@
 // as y - D_S x every iteration.  Correlations and |r| are fp64 dots of the
 // same vectors as the reference in a different summation order (~1e-16
 // relative).  Near rank deficiency is delegated to the exact engine.
+#include <cstdlib>
+
 #include "candidates.cuh"
 #include "common.cuh"
 #include "engines.h"
 
 namespace cdb {
 namespace {
+
+// 16-byte shared-memory load (LDS.128; the compiler otherwise splits it)
+__device__ __forceinline__ float4 lds128(const void *p) {
+  float4 v;
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+
+// packed fp32 FMA (FFMA2): two independent fma.rn in one instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  const unsigned long long A = (unsigned long long)__float_as_uint(a.x) |
+                               ((unsigned long long)__float_as_uint(a.y) << 32);
+  const unsigned long long B = (unsigned long long)__float_as_uint(b.x) |
+                               ((unsigned long long)__float_as_uint(b.y) << 32);
+  const unsigned long long C = (unsigned long long)__float_as_uint(c.x) |
+                               ((unsigned long long)__float_as_uint(c.y) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(A), "l"(B), "l"(C));
+  return make_float2(__uint_as_float((unsigned)d), __uint_as_float((unsigned)(d >> 32)));
+}
 
 constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 
@@ -31,7 +56,21 @@ constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 // new L^{-1} row, and the residual update r -= z_k q_k with
 // q_k = sum_l L^{-1}[k][l] d_{s_l} read from the resident atoms; the
 // coefficients x = L^{-T} z are formed once at the end.
-template <typename YT, int U, bool FULL, int R>
+//
+// F32C: the correlations are fp32 dots of an fp32 copy of the resident atoms
+// with an fp32 copy of the residual (half the shared-memory bytes of the
+// fp64 scan, FP32 pipe), certified against the exact fp64 values: with
+// E = (N + 2) 2^-24 max|d| |r| (fp32 accumulation over N terms plus the
+// rounding of both operands), any candidate whose approximate |c| is below
+// max - 2E cannot be the fp64 arg-max.  When exactly one candidate is in
+// the window it is the pick; otherwise the window is re-scored in fp64.  The
+// winner's correlation (z_k = c / d) is always recomputed in fp64.  Layout:
+// the fp32 atoms are interleaved per dimension as [U/4][lane][4] (atoms
+// lane + 32 (4w + c)), one conflict-free 16-byte load per lane per 4 atoms,
+// and accumulated pairwise with FFMA2; the fp32 residual is stored
+// duplicated ({r_i, r_i}) so one 16-byte load feeds two dimensions.
+// F32C requires FULL and U >= 4.
+template <typename YT, int U, bool FULL, int R, bool F32C>
 __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
   extern __shared__ __align__(16) double rs[];
@@ -41,13 +80,22 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double *Dt = rs;                 // n x Tp  (columns T..Tp-1 are zero)
   double *nrm2 = Dt + n * Tp;      // Tp  (|d_j|^2)
-  double *wbase = nrm2 + Tp;
+  const int n2 = (n + 1) & ~1;    // F32C rows (zero row when n is odd)
+  float *Df = (float *)(rs + ((n * Tp + Tp + 1) & ~1));  // F32C: n2 x 32U fp32 (16-B aligned)
+  double *wbase = F32C ? (double *)(Df + n2 * 32 * U) : nrm2 + Tp;
   const int per_sig = (int)a.per_warp;  // doubles of state per signal
+  __shared__ double s_dmax;
 
   for (int e = threadIdx.x; e < n * Tp; e += blockDim.x) {
     const int i = e / Tp, j = e % Tp;
     Dt[e] = j < T ? a.d64[(int64_t)j * n + i] : 0.0;
   }
+  if (F32C)
+    for (int e = threadIdx.x; e < n2 * 32 * U; e += blockDim.x) {
+      const int i = e / (32 * U), rem = e % (32 * U);
+      const int j = (rem % 128) / 4 + 32 * (4 * (rem / 128) + rem % 4);
+      Df[e] = i < n && j < T ? (float)a.d64[(int64_t)j * n + i] : 0.0f;
+    }
   __syncthreads();
   for (int j = threadIdx.x; j < Tp; j += blockDim.x) {
     double sq = 0.0;
@@ -55,6 +103,17 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
     nrm2[j] = sq;
   }
   __syncthreads();
+  if (threadIdx.x < 32) {
+    double mx = 0.0;
+    for (int j = threadIdx.x; j < Tp; j += 32) mx = fmax(mx, nrm2[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(CDB_FULL_MASK, mx, o));
+    if (threadIdx.x == 0) s_dmax = sqrt(mx);
+  }
+  __syncthreads();
+  // |c~ - c| <= e_rel |r|  (F32C certification bound, 1% slack)
+  const double e_rel = (double)(n + 2) * 0x1p-24 * 1.01 * s_dmax;
+  const int r32_off = (n + kw * ldl + 5 * kw + 2) & ~1;  // doubles (even): fp32 residual pairs
 
   const Cands cs = a.cands;
   const double *eps = a.eps;
@@ -83,7 +142,11 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
         cid[q][u] = FULL ? jl : (jl < S[q] ? (int)cs.id(p, jl) : Tp - 1);
         if (jl >= S[q]) tk[q] |= 1u << u;
       }
-      for (int i = lane; i < n; i += 32) r[i] = valid ? (double)ys[p * n + i] : 0.0;
+      for (int i = lane; i < n2; i += 32) {
+        const double v = valid && i < n ? (double)ys[p * n + i] : 0.0;
+        if (i < n) r[i] = v;
+        if (F32C) ((float2 *)(r + r32_off))[i] = make_float2((float)v, (float)v);
+      }
       __syncwarp();
       const double ynorm = sqrt(dot4_quad(r, r, n, lane));  // reference order (_kernels.py:71)
       tol[q] = valid ? eps[p] : 0.0;
@@ -103,26 +166,63 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
       if (!any) break;
       // ---- correlations of this lane's candidates with each live residual
       double acc[R][U];
+      if constexpr (F32C) {
+        float2 af[R][U / 2];
 #pragma unroll
-      for (int q = 0; q < R; q++)
+        for (int q = 0; q < R; q++)
 #pragma unroll
-        for (int u = 0; u < U; u++) acc[q][u] = 0.0;
-      const double *col = FULL ? Dt + lane : Dt;
+          for (int v = 0; v < U / 2; v++) af[q][v] = make_float2(0.0f, 0.0f);
+        const float4 *dcol = (const float4 *)Df + lane;
 #pragma unroll 2
-      for (int i = 0; i < n; i++) {
-        double ri[R];
+        for (int i = 0; i < n2; i += 2) {
+          float4 rq[R];
 #pragma unroll
-        for (int q = 0; q < R; q++) ri[q] = sbase[q * per_sig + i];
-        const double *row = col + i * Tp;
+          for (int q = 0; q < R; q++)
+            rq[q] = lds128((const float4 *)(sbase + q * per_sig + r32_off) + i / 2);
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-          if (FULL) {
-            const double dv = row[32 * u];
+          for (int ii = 0; ii < 2; ii++) {
+            const float4 *row = dcol + (i + ii) * 8 * U;
 #pragma unroll
-            for (int q = 0; q < R; q++) acc[q][u] = fma(dv, ri[q], acc[q][u]);
-          } else {
+            for (int w = 0; w < U / 4; w++) {
+              const float4 d = lds128(row + 32 * w);
 #pragma unroll
-            for (int q = 0; q < R; q++) acc[q][u] = fma(row[cid[q][u]], ri[q], acc[q][u]);
+              for (int q = 0; q < R; q++) {
+                const float2 b = ii ? make_float2(rq[q].z, rq[q].w) : make_float2(rq[q].x, rq[q].y);
+                af[q][2 * w] = ffma2(make_float2(d.x, d.y), b, af[q][2 * w]);
+                af[q][2 * w + 1] = ffma2(make_float2(d.z, d.w), b, af[q][2 * w + 1]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < R; q++)
+#pragma unroll
+          for (int v = 0; v < U / 2; v++) {
+            acc[q][2 * v] = (double)af[q][v].x;
+            acc[q][2 * v + 1] = (double)af[q][v].y;
+          }
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; q++)
+#pragma unroll
+          for (int u = 0; u < U; u++) acc[q][u] = 0.0;
+        const double *col = FULL ? Dt + lane : Dt;
+#pragma unroll 2
+        for (int i = 0; i < n; i++) {
+          double ri[R];
+#pragma unroll
+          for (int q = 0; q < R; q++) ri[q] = sbase[q * per_sig + i];
+          const double *row = col + i * Tp;
+#pragma unroll
+          for (int u = 0; u < U; u++) {
+            if (FULL) {
+              const double dv = row[32 * u];
+#pragma unroll
+              for (int q = 0; q < R; q++) acc[q][u] = fma(dv, ri[q], acc[q][u]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < R; q++) acc[q][u] = fma(row[cid[q][u]], ri[q], acc[q][u]);
+            }
           }
         }
       }
@@ -150,11 +250,49 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
         double m = best;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
-        if (!(m > 0.0)) {  // nothing left, or best <= 0 (_kernels.py:104)
-          live[q] = false;
-          continue;
+        int bestj;
+        double cbest;
+        if constexpr (F32C) {
+          // certification window [m - 2E, m] of the fp32 scan
+          const double thr = m - 2.0 * e_rel * rnorm[q];
+          int cnt = 0;
+#pragma unroll
+          for (int u = 0; u < U; u++)
+            if (!((tk[q] >> u) & 1u) && fabs(acc[q][u]) >= thr) cnt++;
+          cnt = (int)__reduce_add_sync(CDB_FULL_MASK, (unsigned)cnt);
+          if (cnt == 0) {  // nothing available (_kernels.py:104)
+            live[q] = false;
+            continue;
+          }
+          if (cnt > 1) {
+            // re-score the window exactly in fp64 (lane per candidate)
+            best = -1.0;
+            bj = 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+              if (!((tk[q] >> u) & 1u) && fabs(acc[q][u]) >= thr) {
+                const int jj = FULL ? lane + 32 * u : cid[q][u];
+                double c = 0.0;
+                for (int i = 0; i < n; i++) c = fma(Dt[i * Tp + jj], r[i], c);
+                acc[q][u] = c;
+                if (fabs(c) > best) {
+                  best = fabs(c);
+                  bj = lane + 32 * u;
+                }
+              }
+            }
+            m = best;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+          }
+          bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+        } else {
+          if (!(m > 0.0)) {  // nothing left, or best <= 0 (_kernels.py:104)
+            live[q] = false;
+            continue;
+          }
+          bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
         }
-        const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
         const int ub = bestj >> 5, owner = bestj & 31;
         double my_c = 0.0;
         int my_id = 0;
@@ -164,8 +302,18 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
             my_c = acc[q][u];
             my_id = cid[q][u];
           }
-        const double cbest = __shfl_sync(CDB_FULL_MASK, my_c, owner);
+        cbest = __shfl_sync(CDB_FULL_MASK, my_c, owner);
         const int nid = FULL ? bestj : __shfl_sync(CDB_FULL_MASK, my_id, owner);
+        if constexpr (F32C) {
+          // the winner's exact correlation (z_k = c / d); orthogonal break on it
+          double c = 0.0;
+          for (int i = lane; i < n; i += 32) c = fma(Dt[i * Tp + nid], r[i], c);
+          cbest = warp_sum(c);
+          if (!(fabs(cbest) > 0.0)) {  // _kernels.py:104
+            live[q] = false;
+            continue;
+          }
+        }
         if (lane == owner) tk[q] |= 1u << ub;
         // ---- Cholesky append: g_l = <d_{s_l}, d_new> (Gram row gather, or a
         // dot over the resident atoms when no Gram matrix is staged)
@@ -226,6 +374,7 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
           for (int l = 0; l <= k; l++) qv = fma(lk[l], row[sup[l]], qv);
           const double rv = fma(-zk, qv, r[i]);
           r[i] = rv;
+          if (F32C) ((float2 *)(r + r32_off))[i] = make_float2((float)rv, (float)rv);
           rr = fma(rv, rv, rr);
         }
         rnorm[q] = sqrt(warp_sum(rr));
@@ -276,14 +425,28 @@ cudaError_t launch_u(const ResidentArgs &args, const YT *ys, int64_t base, int s
                      int num_sms, cudaStream_t stream) {
   constexpr int R = res_r<U>();
   ResidentArgs a = args;
-  int warps = (int)((smem_optin - base) / (8 * a.per_warp * R));
-  if (warps > res_max_warps(R)) warps = res_max_warps(R);
+  const int max_w = res_max_warps(R);
+  auto warps_for = [&](int64_t b) {
+    int w = (int)((smem_optin - b) / (8 * a.per_warp * R));
+    return w > max_w ? max_w : w;
+  };
+  // fp32 certified scan when the extra fp32 atom copy still leaves as many
+  // warps as the fp64 scan (or a full CTA)
+  const int64_t base32 = base + 16 + 4 * ((a.n + 1) & ~1LL) * 32 * U;
+  const int w64 = warps_for(base), w32 = warps_for(base32);
+  const bool f32c = U >= 4 && a.cands.mode == 0 && !getenv("CDB_RESIDENT_FP64") && w32 >= 8 &&
+                    (w32 >= w64 || w32 >= max_w);
+  const int warps = f32c ? w32 : w64;
   if (warps < 1) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)(base + 8 * a.per_warp * R * warps);
+  const size_t smem = (size_t)((f32c ? base32 : base) + 8 * a.per_warp * R * warps);
   int64_t grid = (a.p + warps * R - 1) / (warps * R);
   if (grid > num_sms) grid = num_sms;
-  auto kern = a.cands.mode == 0 ? resident_omp_kernel<YT, U, true, R>
-                                : resident_omp_kernel<YT, U, false, R>;
+  void (*kern)(ResidentArgs, const YT *);
+  if (a.cands.mode == 0)
+    kern = f32c ? resident_omp_kernel<YT, U, true, R, (U >= 4)>
+                : resident_omp_kernel<YT, U, true, R, false>;
+  else
+    kern = resident_omp_kernel<YT, U, false, R, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<(int)grid, warps * 32, smem, stream>>>(a, ys);
@@ -307,7 +470,8 @@ cudaError_t launch_t(const ResidentArgs &a, const YT *ys, int u, int64_t base, i
 
 int64_t resident_warp_doubles(int64_t n, int64_t kw, int64_t max_cands) {
   (void)max_cands;
-  return n + kw * (kw | 1) + 5 * kw + 1;
+  // ..., fp32 residual pairs at an even offset; even total keeps 16-B alignment
+  return ((n + kw * (kw | 1) + 5 * kw + 2) & ~1LL) + ((n + 1) & ~1LL);
 }
 
 // Row stride of the transposed dictionary: at least one zero column and the
