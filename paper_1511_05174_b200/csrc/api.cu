@@ -3,8 +3,11 @@
 // *_engine.cu / helpers.cu translation units.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <array>
+#include <chrono>
 #include <vector>
 #include <algorithm>
 
@@ -25,8 +28,20 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local int g_last_engine = 0;     // engine the last run_omp used
-thread_local int g_last_delegated = 0;  // signals handed to the exact engine
-thread_local int g_last_rescans = 0;    // inline exact rescans (tensor engine)
+// delegated / rescan counts of the last run_omp live in a persistent device
+// buffer that the kernels count into; only cdb_last_run_info copies them to
+// the host (after a device sync).  No copy is ever queued on the compute
+// stream: a small D2H there would wait behind a pipeline's output copies on
+// the copy engine and stall the next chunk.
+thread_local int *g_diag = nullptr;  // device: [0] delegated, [1] rescans
+int *diag_dev() {
+  if (!g_diag) {
+    cudaMalloc((void **)&g_diag, 2 * sizeof(int));
+    cudaMemset(g_diag, 0, 2 * sizeof(int));
+  }
+  return g_diag;
+}
+void diag_clear(cudaStream_t st) { cudaMemsetAsync(diag_dev(), 0, 2 * sizeof(int), st); }
 std::atomic<int64_t> g_launches{0};
 
 cdb_status fail(cdb_status st, const std::string &msg) {
@@ -167,7 +182,7 @@ constexpr int64_t kScratchBudget = int64_t(4) << 30;  // per-call global scratch
 cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t count,
                      const int64_t *sig_ids, int64_t k_max, int64_t kw, const double *eps,
                      const cdb::Cands &cands, int64_t max_cands, Outs &o, const DevInfo &di,
-                     cudaStream_t st) {
+                     cudaStream_t st, const int *count_dev = nullptr) {
   if (count <= 0) return CDB_OK;
   cdb::ExactArgs a{};
   a.mat_t = d->d64;
@@ -176,6 +191,7 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
   a.ys_stride = d->n;
   a.sig_ids = sig_ids;
   a.p_count = count;
+  a.p_count_dev = count_dev;
   a.k_max = k_max;
   a.k_width = kw;
   a.eps = eps;
@@ -187,7 +203,9 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
   a.out_scans = (int64_t *)o.scans.dev;
   a.out_flag = (uint8_t *)o.flag.dev;
   a.work_stride = cdb::exact_work_stride(d->n, kw, max_cands);
-  int64_t warps = count < (int64_t)di.sms * 8 ? count : (int64_t)di.sms * 8;
+  // a device-side count is usually tiny (delegations are rare): few warps
+  const int64_t wmax = count_dev ? (int64_t)di.sms : (int64_t)di.sms * 8;
+  int64_t warps = count < wmax ? count : wmax;
   const int64_t cap = kScratchBudget / (8 * a.work_stride);
   if (warps > cap) warps = cap < 4 ? 4 : cap;
   warps = (warps + 3) & ~int64_t(3);
@@ -198,24 +216,19 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
   return CDB_OK;
 }
 
-// Signals an engine handed over (status ST_DELEGATE) -> exact engine.
+// Signals an engine handed over (status ST_DELEGATE) -> exact engine.  The
+// count stays on the device: the exact kernel reads it, so nothing here
+// waits for the GPU (a host-buffer pipeline keeps queueing chunks).
 cdb_status finish_delegates(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
                             int64_t k_max, int64_t kw, const double *eps, const cdb::Cands &cands,
                             int64_t max_cands, Outs &o, const uint32_t *status, const DevInfo &di,
                             cudaStream_t st) {
-  DevBuf ids, cnt;
+  DevBuf ids;
   CDB_CUDA(ids.alloc(sizeof(int64_t) * p, st));
-  CDB_CUDA(cnt.alloc(sizeof(int), st));
-  CDB_CUDA(cudaMemsetAsync(cnt.ptr, 0, sizeof(int), st));
-  CDB_CUDA(cdb::launch_collect_delegates(status, p, ids.as<int64_t>(), cnt.as<int>(), st));
-  int h_cnt = 0;
-  CDB_CUDA(cudaMemcpyAsync(&h_cnt, cnt.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CDB_CUDA(cudaStreamSynchronize(st));
-  g_last_delegated = h_cnt;
-  if (h_cnt > 0)
-    return run_exact(d, ys, f32, h_cnt, ids.as<int64_t>(), k_max, kw, eps, cands, max_cands, o,
-                     di, st);
-  return CDB_OK;
+  int *cnt = diag_dev();  // [0]: zeroed by run_omp's diag_clear
+  CDB_CUDA(cdb::launch_collect_delegates(status, p, ids.as<int64_t>(), cnt, st));
+  return run_exact(d, ys, f32, p, ids.as<int64_t>(), k_max, kw, eps, cands, max_cands, o, di, st,
+                   cnt);
 }
 
 cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t p, int64_t k_max,
@@ -228,10 +241,8 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
   int64_t chunk = kScratchBudget / per;
   if (chunk < 128) chunk = 128;
   if (chunk > p) chunk = p;
-  DevBuf work, rescans;
+  DevBuf work;
   CDB_CUDA(work.alloc((size_t)cdb::tensor_state_bytes(chunk, d->n, kw) + 65536, st));
-  CDB_CUDA(rescans.alloc(sizeof(int), st));
-  CDB_CUDA(cudaMemsetAsync(rescans.ptr, 0, sizeof(int), st));
   const size_t ysz = f32 ? 4 : 8;
   for (int64_t off = 0; off < p; off += chunk) {
     cdb::TensorArgs a{};
@@ -248,7 +259,7 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
     a.d16 = d->d16;
     a.d32 = d->d32;
     a.gram = d->gram;
-    a.rescans = rescans.as<int>();
+    a.rescans = diag_dev() + 1;  // zeroed by run_omp's diag_clear
     a.dmax = d->dmax;
     a.out_sel = (int64_t *)o.sel.dev + off * kw;
     a.out_coef = (double *)o.coef.dev + off * kw;
@@ -261,7 +272,6 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
     a.num_sms = di.sms;
     CDB_CUDA(cdb::run_tensor_chunk(a, st));
   }
-  CDB_CUDA(cudaMemcpyAsync(&g_last_rescans, rescans.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
   return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, d->t, o, status.as<uint32_t>(),
                           di, st);
 }
@@ -298,8 +308,7 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   if (engine == CDB_ENGINE_GRAM && (max_cands > 512 || kw > 64))  // beyond the Gram kernel's tiles
     engine = cands.mode == 0 ? CDB_ENGINE_TENSOR : CDB_ENGINE_EXACT;
   g_last_engine = engine;
-  g_last_rescans = 0;
-  g_last_delegated = 0;
+  diag_clear(st);
   if (engine == CDB_ENGINE_EXACT)
     return run_exact(d, ys, f32, p, nullptr, k_max, kw, eps, cands, max_cands, o, di, st);
   if (engine == CDB_ENGINE_TENSOR) return run_tensor(d, ys, f32, p, k_max, kw, eps, cands, o, di, st);
@@ -377,80 +386,158 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
 
 // ---------------------------------------------------------------- host-buffer pipelining
 // Row-major per-signal arrays crossing the host boundary: the batch is coded
-// in chunks; chunk i+1's inputs are copied H2D and chunk i-1's outputs D2H on
-// a copy stream while chunk i computes on the caller's stream (two device
-// buffer sets, events order the reuse).  Requires pinned host memory for the
-// copies to be asynchronous; pageable memory still works (staged by CUDA).
+// in chunks; chunk i+1's inputs go H2D on one copy stream and chunk i-1's
+// outputs D2H on another (PCIe is full duplex) while chunk i computes on the
+// caller's stream.  Two device buffer sets; events order every reuse, and
+// nothing waits on the host until the end, so the GPU never idles between
+// chunks.  Chunk sizes ramp up and down (small first and last chunks) to
+// shrink the copies that cannot overlap compute.  Requires pinned host
+// memory for the copies to be asynchronous; pageable memory still works.
 struct RowArr {
   void *host;        // host base pointer (or device, then passed through)
   size_t row_bytes;  // bytes per signal
   bool out;          // output (D2H) or input (H2D)
 };
 
-cudaStream_t copy_stream() {
-  static thread_local cudaStream_t cs = nullptr;
+cudaStream_t copy_stream(int which) {
+  static thread_local cudaStream_t cs[2] = {nullptr, nullptr};
   static thread_local int dev = -1;
   int cur = 0;
   cudaGetDevice(&cur);
-  if (!cs || dev != cur) {
-    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (!cs[0] || dev != cur) {
+    cudaStreamCreateWithFlags(&cs[0], cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&cs[1], cudaStreamNonBlocking);
     dev = cur;
   }
-  return cs;
+  return cs[which];
+}
+
+// Chunk boundaries: a small first chunk (its H2D cannot overlap compute) and
+// a small last chunk (its D2H cannot), and the rest in as few chunks as fit
+// `kPipeMid` signals -- each call carries ~0.1-0.3 ms of fixed cost (launch
+// gaps, partial waves), so many small chunks lose more than they hide.
+std::vector<int64_t> chunk_bounds(int64_t p) {
+  static const int64_t mid_max = getenv("CDB_PIPE_CHUNK") ? atoll(getenv("CDB_PIPE_CHUNK")) : 90000;
+  static const int64_t edge_max = getenv("CDB_PIPE_EDGE") ? atoll(getenv("CDB_PIPE_EDGE")) : 20000;
+  int64_t edge = p / 5;
+  if (edge > edge_max) edge = edge_max;
+  std::vector<int64_t> b = {0};
+  if (edge < 2048 || p < 4 * edge) {  // too small to bother: two halves
+    b.push_back(p / 2);
+    b.push_back(p);
+    return b;
+  }
+  b.push_back(edge);
+  const int64_t mid = p - 2 * edge;
+  const int64_t nm = (mid + mid_max - 1) / mid_max;
+  for (int64_t i = 1; i < nm; i++) b.push_back(edge + mid * i / nm);
+  b.push_back(p - edge);
+  b.push_back(p);
+  return b;
 }
 
 template <typename Core>
-cdb_status run_pipelined(int64_t p, int64_t chunk, std::vector<RowArr> &arrs, cudaStream_t st,
-                         Core core) {
-  const int64_t nch = (p + chunk - 1) / chunk;
-  cudaStream_t cs = copy_stream();
+cdb_status run_pipelined(int64_t p, std::vector<RowArr> &arrs, cudaStream_t st, Core core) {
+  const std::vector<int64_t> bd = chunk_bounds(p);
+  const int64_t nch = (int64_t)bd.size() - 1;
+  int64_t chunk = 0;
+  for (int64_t i = 0; i < nch; i++) chunk = std::max(chunk, bd[i + 1] - bd[i]);
+  cudaStream_t cin = copy_stream(0), cout = copy_stream(1);
   const size_t na = arrs.size();
   std::vector<DevBuf> bufs(2 * na);
   for (int b = 0; b < 2; b++)
     for (size_t a = 0; a < na; a++)
       CDB_CUDA(bufs[b * na + a].alloc(arrs[a].row_bytes * chunk, st));
-  CDB_CUDA(cudaStreamSynchronize(st));  // buffers allocated before the copy stream uses them
-  cudaEvent_t in_ready[2], done[2];
+  cudaEvent_t ready, in_ready[2], done[2], out_done[2];
+  CDB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   for (int b = 0; b < 2; b++) {
     CDB_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
     CDB_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    CDB_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
   }
+  CDB_CUDA(cudaEventRecord(ready, st));  // buffers allocated (stream-ordered)
+  CDB_CUDA(cudaStreamWaitEvent(cin, ready, 0));
+  CDB_CUDA(cudaStreamWaitEvent(cout, ready, 0));
+  bool out_pending[2] = {false, false};
   auto h2d = [&](int64_t i) -> cudaError_t {
     const int b = (int)(i & 1);
-    const int64_t off = i * chunk, len = std::min(chunk, p - off);
+    const int64_t off = bd[i], len = bd[i + 1] - bd[i];
+    cudaError_t e;
+    if (out_pending[b] && (e = cudaStreamWaitEvent(cin, out_done[b], 0)) != cudaSuccess) return e;
     for (size_t a = 0; a < na; a++) {
       if (arrs[a].out || !arrs[a].host) continue;
-      cudaError_t e = cudaMemcpyAsync(bufs[b * na + a].ptr,
-                                      (const uint8_t *)arrs[a].host + off * arrs[a].row_bytes,
-                                      len * arrs[a].row_bytes, cudaMemcpyHostToDevice, cs);
+      e = cudaMemcpyAsync(bufs[b * na + a].ptr,
+                          (const uint8_t *)arrs[a].host + off * arrs[a].row_bytes,
+                          len * arrs[a].row_bytes, cudaMemcpyHostToDevice, cin);
       if (e != cudaSuccess) return e;
     }
-    return cudaEventRecord(in_ready[b], cs);
+    return cudaEventRecord(in_ready[b], cin);
   };
-  CDB_CUDA(h2d(0));
-  for (int64_t i = 0; i < nch; i++) {
+  static const bool trace = getenv("CDB_PIPE_TRACE") != nullptr;
+  auto now_us = [] {
+    return (double)std::chrono::duration_cast<std::chrono::microseconds>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t_start = now_us();
+  // trace: GPU timestamps of h2d start/end, compute start/end, d2h start/end
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t s_) {
+    if (!trace) return -1;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s_);
+    tev.push_back(e);
+    return (int)tev.size() - 1;
+  };
+  const int t0ev = tmark(st);
+  cdb_status result = CDB_OK;
+  cudaError_t ce = h2d(0);
+  for (int64_t i = 0; i < nch && ce == cudaSuccess && result == CDB_OK; i++) {
     const int b = (int)(i & 1);
-    const int64_t off = i * chunk, len = std::min(chunk, p - off);
-    if (i + 1 < nch) CDB_CUDA(h2d(i + 1));
-    CDB_CUDA(cudaStreamWaitEvent(st, in_ready[b], 0));
+    const int64_t off = bd[i], len = bd[i + 1] - bd[i];
+    if (i + 1 < nch && (ce = h2d(i + 1)) != cudaSuccess) break;
+    if ((ce = cudaStreamWaitEvent(st, in_ready[b], 0)) != cudaSuccess) break;
+    tmark(st);
     std::vector<void *> dev(na);
     for (size_t a = 0; a < na; a++) dev[a] = bufs[b * na + a].ptr;
-    cdb_status s = core(off, len, dev, st);
-    if (s != CDB_OK) return s;
-    CDB_CUDA(cudaEventRecord(done[b], st));
-    CDB_CUDA(cudaStreamWaitEvent(cs, done[b], 0));
-    for (size_t a = 0; a < na; a++) {
+    result = core(off, len, dev, st);
+    if (result != CDB_OK) break;
+    if ((ce = cudaEventRecord(done[b], st)) != cudaSuccess) break;
+    tmark(st);
+    if ((ce = cudaStreamWaitEvent(cout, done[b], 0)) != cudaSuccess) break;
+    for (size_t a = 0; a < na && ce == cudaSuccess; a++) {
       if (!arrs[a].out || !arrs[a].host) continue;
-      CDB_CUDA(cudaMemcpyAsync((uint8_t *)arrs[a].host + off * arrs[a].row_bytes, dev[a],
-                               len * arrs[a].row_bytes, cudaMemcpyDeviceToHost, cs));
+      ce = cudaMemcpyAsync((uint8_t *)arrs[a].host + off * arrs[a].row_bytes, dev[a],
+                           len * arrs[a].row_bytes, cudaMemcpyDeviceToHost, cout);
     }
+    if (ce == cudaSuccess) ce = cudaEventRecord(out_done[b], cout);
+    tmark(cout);
+    out_pending[b] = true;
+    if (trace) fprintf(stderr, "[pipe] chunk %lld len %lld issued at %.0f us\n", (long long)i,
+                       (long long)len, now_us() - t_start);
   }
-  CDB_CUDA(cudaStreamSynchronize(cs));
-  CDB_CUDA(cudaStreamSynchronize(st));
+  cudaError_t e1 = cudaStreamSynchronize(cin), e2 = cudaStreamSynchronize(cout);
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  if (trace) {
+    fprintf(stderr, "[pipe] all done at %.0f us; GPU (compute start, compute end, d2h end) ms:",
+            now_us() - t_start);
+    for (size_t k = 1; k < tev.size(); k++) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, tev[t0ev], tev[k]);
+      fprintf(stderr, " %.3f", ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
+  cudaEventDestroy(ready);
   for (int b = 0; b < 2; b++) {
     cudaEventDestroy(in_ready[b]);
     cudaEventDestroy(done[b]);
+    cudaEventDestroy(out_done[b]);
   }
+  if (result != CDB_OK) return result;
+  for (cudaError_t e : {ce, e1, e2, e3})
+    if (e != cudaSuccess) return fail(CDB_ERR_CUDA, cudaGetErrorString(e));
   return CDB_OK;
 }
 
@@ -561,8 +648,11 @@ int64_t cdb_launch_count(void) { return g_launches.load(); }
 
 void cdb_last_run_info(int *engine, int *delegated, int *rescans) {
   if (engine) *engine = g_last_engine;
-  if (delegated) *delegated = g_last_delegated;
-  if (rescans) *rescans = g_last_rescans;
+  int h[2] = {0, 0};
+  if (g_diag && cudaDeviceSynchronize() == cudaSuccess)
+    cudaMemcpy(h, g_diag, sizeof(h), cudaMemcpyDeviceToHost);
+  if (delegated) *delegated = h[0];
+  if (rescans) *rescans = h[1];
 }
 
 cdb_status cdb_device_info(int *sm_count, int *cc_major, int *cc_minor) {
@@ -675,9 +765,8 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
         {out_count, sizeof(int64_t), true}, {out_rnorm, sizeof(double), true},
         {out_scans, sizeof(int64_t), true}, {out_flag, sizeof(uint8_t), true}};
     if (!mode) arrs[2].host = nullptr;
-    const int64_t chunk = std::max<int64_t>(kPipeMin, (p + 3) / 4);
-    return run_pipelined(p, chunk, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
-                                                 cudaStream_t s2) -> cdb_status {
+    return run_pipelined(p, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
+                                          cudaStream_t s2) -> cdb_status {
       cdb::Cands c{};
       c.mode = mode;
       c.t = dict->t;
@@ -736,15 +825,42 @@ cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int
                     out_count, out_rnorm, out_scans, out_flag, engine, stream);
 }
 
+// Per-step device times of zero-tree calls: events recorded per (chunk) call,
+// read once after the caller's final synchronisation -- no mid-call waits.
+struct StepTimer {
+  std::vector<std::array<cudaEvent_t, 3>> ev;
+  cudaError_t open(cudaStream_t st) {
+    std::array<cudaEvent_t, 3> e{};
+    for (auto &x : e) {
+      cudaError_t r = cudaEventCreate(&x);
+      if (r != cudaSuccess) return r;
+    }
+    ev.push_back(e);
+    return cudaEventRecord(e[0], st);
+  }
+  cudaError_t mark(int i, cudaStream_t st) { return cudaEventRecord(ev.back()[i], st); }
+  void finish(float *step_ms) {  // after the stream was synchronised
+    for (auto &e : ev) {
+      float a = 0.0f, b = 0.0f;
+      if (step_ms && cudaEventElapsedTime(&a, e[0], e[1]) == cudaSuccess &&
+          cudaEventElapsedTime(&b, e[1], e[2]) == cudaSuccess) {
+        step_ms[0] += a;
+        step_ms[1] += b;
+      }
+      for (auto &x : e) cudaEventDestroy(x);
+    }
+    ev.clear();
+  }
+  ~StepTimer() { finish(nullptr); }
+};
+
 static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary *high,
                                  const int64_t *fine_shape, const int64_t *factors, int rank,
                                  const void *ydev, bool f32, int64_t p, int64_t k1,
                                  int64_t k_high, double rel_tol, int phi_mode, Outs &lo, Outs &hi,
-                                 int engine, float *step_ms, const DevInfo &di, cudaStream_t st) {
+                                 int engine, StepTimer *tm, const DevInfo &di, cudaStream_t st) {
   const int64_t n = high->n, q = high->t / low->t;
-  cudaEvent_t ev[3];
-  for (auto &e : ev) CDB_CUDA(cudaEventCreate(&e));
-  CDB_CUDA(cudaEventRecord(ev[0], st));
+  if (tm) CDB_CUDA(tm->open(st));
 
   // ---- step 1: W y (identity) or y (Phi), tolerance relative to it
   DevBuf ylow, eps1, eps2, blocks;
@@ -768,7 +884,7 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
   cdb_status s = run_omp(low, y1, y1_f32, p, k1, k1, eps1.as<double>(), c1, low->t, lo, engine, di,
                          st, "gram_step1");
   if (s != CDB_OK) return s;
-  CDB_CUDA(cudaEventRecord(ev[1], st));
+  if (tm) CDB_CUDA(tm->mark(1, st));
 
   // ---- step 2: restricted to the children of the sorted coarse support
   CDB_CUDA(blocks.alloc(sizeof(int64_t) * p * k1, st));
@@ -802,16 +918,7 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
   s = run_omp(high, ydev, f32, p, k_high, k_high, eps2.as<double>(), c2, k1 * q, hi, engine, di,
               st, "gram_step2", use_route ? alpha0.as<double>() : nullptr);
   if (s != CDB_OK) return s;
-  CDB_CUDA(cudaEventRecord(ev[2], st));
-  CDB_CUDA(cudaEventSynchronize(ev[2]));
-  if (step_ms) {
-    float a = 0.0f, b = 0.0f;
-    CDB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
-    CDB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
-    step_ms[0] += a;
-    step_ms[1] += b;
-  }
-  for (auto &e : ev) cudaEventDestroy(e);
+  if (tm) CDB_CUDA(tm->mark(2, st));
   return CDB_OK;
 }
 
@@ -847,27 +954,31 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
         {high_sel, sizeof(int64_t) * k_high, true}, {high_coef, sizeof(double) * k_high, true},
         {high_count, sizeof(int64_t), true}, {high_rnorm, sizeof(double), true},
         {high_scans, sizeof(int64_t), true}, {high_flag, sizeof(uint8_t), true}};
-    const int64_t chunk = std::max<int64_t>(kPipeMin, (p + 3) / 4);
-    return run_pipelined(p, chunk, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
-                                                 cudaStream_t s2) -> cdb_status {
+    StepTimer tm;
+    cdb_status s = run_pipelined(p, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
+                                                  cudaStream_t s2) -> cdb_status {
       Outs lo, hi;
       dev_outs(lo, dv[1], dv[2], dv[3], dv[4], dv[5], dv[6]);
       dev_outs(hi, dv[7], dv[8], dv[9], dv[10], dv[11], dv[12]);
       return zero_tree_core(low, high, fine_shape, factors, rank, dv[0], f32, len, k1, k_high,
-                            rel_tol, phi_mode, lo, hi, engine, step_ms, di, s2);
+                            rel_tol, phi_mode, lo, hi, engine, step_ms ? &tm : nullptr, di, s2);
     });
+    tm.finish(step_ms);
+    return s;
   }
   InArr y_in;
   CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
   Outs lo, hi;
   CDB_CUDA(lo.bind(p, k1, low_sel, low_coef, low_count, low_rnorm, low_scans, low_flag, st));
   CDB_CUDA(hi.bind(p, k_high, high_sel, high_coef, high_count, high_rnorm, high_scans, high_flag, st));
+  StepTimer tm;
   cdb_status s = zero_tree_core(low, high, fine_shape, factors, rank, y_in.dev, f32, p, k1, k_high,
-                                rel_tol, phi_mode, lo, hi, engine, step_ms, di, st);
+                                rel_tol, phi_mode, lo, hi, engine, step_ms ? &tm : nullptr, di, st);
   if (s != CDB_OK) return s;
   CDB_CUDA(lo.finish(st));
   CDB_CUDA(hi.finish(st));
   CDB_CUDA(cudaStreamSynchronize(st));
+  tm.finish(step_ms);
   return CDB_OK;
 }
 

@@ -27,6 +27,7 @@ struct ExactArgs {
   int64_t ys_stride;     // elements between signal rows
   const int64_t *sig_ids;  // optional: process only these signals
   int64_t p_count;       // number of signals to process (len(sig_ids) or P)
+  const int *p_count_dev;  // optional: the count lives on the device (<= p_count)
   int64_t k_max;         // budget (clipped per signal when cands.clip)
   int64_t k_width;       // output row width
   const double *eps;

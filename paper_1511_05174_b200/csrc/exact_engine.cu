@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
   double *vwork = coefs + kw;         // kw * kw
   uint32_t *taken = (uint32_t *)(vwork + kw * kw);  // bit mask over candidates
 
-  for (int64_t idx = warp_global; idx < a.p_count; idx += n_warps) {
+  const int64_t count = a.p_count_dev ? (int64_t)*a.p_count_dev : a.p_count;
+  for (int64_t idx = warp_global; idx < count; idx += n_warps) {
     const int64_t p = a.sig_ids ? a.sig_ids[idx] : idx;
     const int64_t c = cs.count(p);
     const int64_t k_max = cs.budget(p, a.k_max, n);
