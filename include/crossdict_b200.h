@@ -155,6 +155,14 @@ cdb_status cdb_debug_corr_topk(const cdb_dictionary *dict, const float *rows, in
                                int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
                                void *stream);
 
+/* Host layout helper: rows[j][i] = cols[i][j] for an n x p column batch (the
+ * reference's N x P signal matrix) into p x n rows (the kernel layout; the
+ * copy crossdict makes at pursuit.py:433).  elem_size 4 or 8; blocked and
+ * split over `threads` host threads (<= 0: all cores).  Writing into pinned
+ * memory lets the batch calls pipeline their host copies. */
+cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_size, void *rows,
+                              int threads);
+
 /* Number of kernels this library has launched since load (instrumentation). */
 int64_t cdb_launch_count(void);
 

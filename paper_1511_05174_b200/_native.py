@@ -24,7 +24,7 @@ SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",
            "cdb_dictionary_destroy", "cdb_dictionary_bytes", "cdb_omp_batch",
            "cdb_omp_batch_blocked", "cdb_zero_tree_batch", "cdb_launch_count",
            "cdb_last_run_info", "cdb_profile_enable", "cdb_profile_read",
-           "cdb_debug_corr_topk")
+           "cdb_debug_corr_topk", "cdb_rows_from_cols")
 
 _lib = None
 
@@ -48,6 +48,7 @@ def load():
     lib.cdb_launch_count.restype = I64
     lib.cdb_device_info.argtypes = [P, P, P]
     lib.cdb_last_run_info.argtypes = [P, P, P]
+    lib.cdb_rows_from_cols.argtypes = [P, I64, I64, I32, P, I32]
     lib.cdb_last_run_info.restype = None
     lib.cdb_debug_corr_topk.argtypes = [P, P, I64, P, P, P, I32, P]
     lib.cdb_debug_corr_topk.restype = I32

@@ -206,7 +206,7 @@ def zero_tree_many_arrays(model, ys, *, phi=None):
         return (mk(model.t_low, z, z.reshape(0, k1), np.zeros((0, k1)), np.zeros(0), z),
                 mk(model.t_high, z, z.reshape(0, model.k_high), np.zeros((0, model.k_high)),
                    np.zeros(0), z), {"step1": 0.0, "step2": 0.0})
-    return _solve(model, np.ascontiguousarray(ys.T), phi)
+    return _solve(model, _dev.rows_for_device(ys), phi)
 
 
 def _zero_tree_result(low, high, p, timings, cls):

@@ -8,6 +8,7 @@
 #include <string>
 #include <array>
 #include <chrono>
+#include <thread>
 #include <vector>
 #include <algorithm>
 
@@ -645,6 +646,41 @@ int cdb_profile_read(int max_entries, char *names, int name_len, double *ms, int
 }
 
 int64_t cdb_launch_count(void) { return g_launches.load(); }
+
+cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_size, void *rows,
+                              int threads) {
+  if (!cols || !rows || n < 0 || p < 0 || (elem_size != 4 && elem_size != 8))
+    return fail(CDB_ERR_ARG, "bad rows_from_cols arguments");
+  if (n == 0 || p == 0) return CDB_OK;
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int64_t B = 64;  // 64 x 64 tiles: both sides touch whole cache lines
+  const int64_t tiles_p = (p + B - 1) / B;
+  if (threads > tiles_p) threads = (int)tiles_p;
+  auto work = [&](int tid) {
+    for (int64_t tp = tid; tp < tiles_p; tp += threads) {
+      const int64_t j0 = tp * B, j1 = std::min(p, j0 + B);
+      for (int64_t i0 = 0; i0 < n; i0 += B) {
+        const int64_t i1 = std::min(n, i0 + B);
+        if (elem_size == 4) {
+          const float *src = (const float *)cols;
+          float *dst = (float *)rows;
+          for (int64_t j = j0; j < j1; j++)
+            for (int64_t i = i0; i < i1; i++) dst[j * n + i] = src[i * p + j];
+        } else {
+          const double *src = (const double *)cols;
+          double *dst = (double *)rows;
+          for (int64_t j = j0; j < j1; j++)
+            for (int64_t i = i0; i < i1; i++) dst[j * n + i] = src[i * p + j];
+        }
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto &t : pool) t.join();
+  return CDB_OK;
+}
 
 void cdb_last_run_info(int *engine, int *delegated, int *rescans) {
   if (engine) *engine = g_last_engine;

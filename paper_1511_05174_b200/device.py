@@ -92,10 +92,40 @@ def clear_cache():
         _cache.popitem(last=False)[1][1].close()
 
 
+# Batches at least this large use page-locked host staging: the library then
+# pipelines chunked H2D / compute / D2H; pageable buffers would make every
+# copy host-synchronous (api.cu run_pipelined).
+PIN_MIN = 4096
+
+
+def pinned_empty(shape, dtype):
+    """Page-locked numpy array (torch's caching host allocator keeps the block
+    alive through the array's base and reuses it after release)."""
+    import torch
+    if not torch.cuda.is_available():  # staging only: plain memory is equally correct
+        return np.empty(shape, dtype)
+    t = torch.empty(shape, dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True)
+    return t.numpy()
+
+
+def rows_for_device(ys_cols):
+    """The reference's N x P column batch as contiguous P x N rows -- the copy
+    the drop-in makes anyway -- written into pinned memory for large batches."""
+    ys_cols = np.asarray(ys_cols)
+    n, p = ys_cols.shape
+    if p < PIN_MIN or ys_cols.dtype not in (np.float32, np.float64):
+        return np.ascontiguousarray(ys_cols.T)
+    src = np.ascontiguousarray(ys_cols)
+    dst = pinned_empty((p, n), src.dtype)
+    N.check(N.load().cdb_rows_from_cols(N.ptr(src), n, p, src.itemsize, N.ptr(dst), 0))
+    return dst
+
+
 def _out(p, k):
-    return dict(sel=np.empty((p, k), np.int64), alpha=np.empty((p, k)),
-                counts=np.empty(p, np.int64), rnorm=np.empty(p), scans=np.empty(p, np.int64),
-                flag=np.empty(p, np.uint8))
+    mk = pinned_empty if p >= PIN_MIN else np.empty
+    return dict(sel=mk((p, k), np.int64), alpha=mk((p, k), np.float64),
+                counts=mk((p,), np.int64), rnorm=mk((p,), np.float64),
+                scans=mk((p,), np.int64), flag=mk((p,), np.uint8))
 
 
 def _out_ptrs(o):

@@ -248,7 +248,7 @@ def omp_many_arrays(columns, ys, config, *, allowed_blocks=None, block_q=None):
         return _types.get("BatchSolve", BatchSolve)(
             t, z, z.reshape(0, k_max), np.zeros((0, k_max)), np.zeros(0), z)
 
-    ys_rows = np.ascontiguousarray(ys.T)
+    ys_rows = _dev.rows_for_device(ys)
     if config.residual_tolerance is not None:
         eps = np.full(p_all, float(config.residual_tolerance))
     else:

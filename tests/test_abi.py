@@ -4,6 +4,9 @@ import ctypes
 import os
 import re
 
+import numpy as np
+import pytest
+
 from paper_1511_05174_b200 import _native as N
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
@@ -38,3 +41,18 @@ def test_library_is_sm100a_only():
 
 def test_launch_counter_callable_without_gpu():
     assert N.launch_count() >= 0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(1, 1), (7, 3), (64, 64), (256, 1000), (33, 4097)])
+def test_rows_from_cols_host_transpose(dtype, shape):
+    # cdb_rows_from_cols is host code (no GPU): the N x P -> P x N copy the
+    # drop-in makes (the reference's pursuit.py:433)
+    from paper_1511_05174_b200 import _native as N
+    n, p = shape
+    cols = np.random.default_rng(n * p).standard_normal((n, p)).astype(dtype)
+    rows = np.empty((p, n), dtype)
+    N.check(N.load().cdb_rows_from_cols(N.ptr(cols), n, p, cols.itemsize, N.ptr(rows), 3))
+    assert np.array_equal(rows, cols.T)
+    with pytest.raises(N.NativeError):
+        N.check(N.load().cdb_rows_from_cols(N.ptr(cols), n, p, 2, N.ptr(rows), 1))
