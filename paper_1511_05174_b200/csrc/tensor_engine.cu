@@ -212,6 +212,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int half = ew >> 2;      // M half
     const int row = half * BMH + quarter * 32 + lane;
     uint32_t acc = 0, acc_ph = 0;
+    // chunk-local column ids in registers (opaque to constant folding) so a
+    // key is one LOP3 (mask | id) instead of two
+    uint32_t cid[32];
+    const uint32_t opaque0 = (uint32_t)threadIdx.x >> 16;  // 0 at runtime
+#pragma unroll
+    for (int i = 0; i < 32; i++) cid[i] = opaque0 + (uint32_t)i;
     for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
       float val[NCAND];
       int idx[NCAND];
@@ -229,14 +235,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           sm100::tmem_ld32(tbase + c, v);
-          // branchless chunk top-2 on packed keys: |v| with its low 8 mantissa
-          // bits replaced by the tile-local column (truncation <= 2^-15 rel.)
+          // branchless chunk top-2 on packed keys: |v| with its low 5 mantissa
+          // bits replaced by the chunk-local column (truncation <= 2^-18 rel.)
           uint32_t c1 = 0u, c2 = 0u, rest = 0u;
           const int jbase = tt * BN + c;
           if (jbase + 32 <= t) {
 #pragma unroll
             for (int i = 0; i < 32; i++) {
-              const uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFF00u) | (uint32_t)(c + i);
+              const uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFFE0u) | cid[i];
               const uint32_t m = min(c1, key);
               c1 = max(c1, key);
               rest = max(rest, min(c2, m));
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           } else {
 #pragma unroll
             for (int i = 0; i < 32; i++) {
-              uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFF00u) | (uint32_t)(c + i);
+              uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFFE0u) | cid[i];
               key = (jbase + i < t) ? key : 0u;
               const uint32_t m = min(c1, key);
               c1 = max(c1, key);
@@ -253,11 +259,11 @@ __global__ void __launch_bounds__(THREADS, 1)
               c2 = max(c2, m);
             }
           }
-          dropped = fmaxf(dropped, __uint_as_float(rest & 0xFFFFFF00u));
-          if (c1) list_insert(val, idx, dropped, __uint_as_float(c1 & 0xFFFFFF00u),
-                              tt * BN + (int)(c1 & 0xFFu));
-          if (c2) list_insert(val, idx, dropped, __uint_as_float(c2 & 0xFFFFFF00u),
-                              tt * BN + (int)(c2 & 0xFFu));
+          dropped = fmaxf(dropped, __uint_as_float(rest & 0xFFFFFFE0u));
+          if (c1) list_insert(val, idx, dropped, __uint_as_float(c1 & 0xFFFFFFE0u),
+                              jbase + (int)(c1 & 0x1Fu));
+          if (c2) list_insert(val, idx, dropped, __uint_as_float(c2 & 0xFFFFFFE0u),
+                              jbase + (int)(c2 & 0x1Fu));
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.tempty[acc]);
@@ -1179,7 +1185,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   // rigorous bound of |c~ - <d, r~>| / (|r~| |d|): bf16 rounding of both
   // operands (2u + u^2, u = 2^-8), fp32 accumulation over n_pad terms, and
-  // the 2^-15 truncation of the packed epilogue keys
+  // the truncation of the packed epilogue keys (2^-18; 2^-15 kept as margin)
   const double c_err = 2.0 * 0x1p-8 + 0x1p-16 + (double)(n_pad + 16) * 0x1p-23 + 0x1p-15;
   const unsigned ls_grid = (unsigned)((p + ls_wpb - 1) / ls_wpb);
   // grouped LS kernel: 8-lane groups (4 signals per warp) when the per-signal
