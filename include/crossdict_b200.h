@@ -155,6 +155,41 @@ cdb_status cdb_debug_corr_topk(const cdb_dictionary *dict, const float *rows, in
                                int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
                                void *stream);
 
+/* ---- patch pipeline ends ------------------------------
+ * Geometry: a rank-r (1..4) row-major signal of extents signal_shape, patch
+ * windows of patch_shape at every multiple of stride (crossdict
+ * patchwork.extract_patches, patchwork.py:58-89): P = prod((ext - pe) / st + 1)
+ * positions in row-major order, N = prod(patch_shape).
+ *
+ * cdb_extract_patches: rows_out (P x N fp64, the reference's columns
+ * transposed -- the layout cdb_omp_batch / cdb_zero_tree_batch take) and,
+ * with remove_dc, the per-patch means dc_out (P) subtracted from the rows.
+ * signal fp32 (is_f32) or fp64; every pointer host or device. */
+cdb_status cdb_extract_patches(const void *signal, int is_f32, int rank,
+                               const int64_t *signal_shape, const int64_t *patch_shape,
+                               const int64_t *stride, int remove_dc, double *rows_out,
+                               double *dc_out, void *stream);
+
+/* cdb_reconstruct_aggregate: est_p = D_S x_p (+ dc_p when dc != NULL) from a
+ * solve's sel / coef rows (P x k_width, sel -1 padded; the atoms of `dict`),
+ * then overlap-add averaging into out (signal_shape, fp64): the reference's
+ * `dictionary.atoms @ coef` + aggregate_patches(add_dc) (pipelines.py:246,
+ * patchwork.py:92-122) without the dense T x P coefficient matrix.  Cells no
+ * patch covers are 0; their number goes to *uncovered (host int64). */
+cdb_status cdb_reconstruct_aggregate(const cdb_dictionary *dict, const int64_t *sel,
+                                     const double *coef, int64_t k_width, int64_t p,
+                                     const double *dc, int rank, const int64_t *signal_shape,
+                                     const int64_t *patch_shape, const int64_t *stride,
+                                     double *out, int64_t *uncovered, void *stream);
+
+/* cdb_aggregate_patches: overlap-add averaging of caller patch values
+ * (rows: P x N fp64, the columns transposed; dc != NULL re-adds the means
+ * first) -- crossdict aggregate_patches (patchwork.py:92-122). */
+cdb_status cdb_aggregate_patches(const double *rows, const double *dc, int rank,
+                                 const int64_t *signal_shape, const int64_t *patch_shape,
+                                 const int64_t *stride, double *out, int64_t *uncovered,
+                                 void *stream);
+
 /* Host layout helper: rows[j][i] = cols[i][j] for an n x p column batch (the
  * reference's N x P signal matrix) into p x n rows (the kernel layout; the
  * copy crossdict makes at pursuit.py:433).  elem_size 4 or 8; blocked and

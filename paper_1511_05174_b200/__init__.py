@@ -15,10 +15,13 @@ from .crossscale import (CrossScaleModel, ZeroTreeResult, cross_scale_map, omp_c
                          zero_tree_omp_many)
 from .errors import ConfigError, CrossdictError, DegenerateAtomError, DimensionError, DomainError
 from .install import install, uninstall
+from .patchwork import (PatchGrid, aggregate_patches, extract_patches, patch_count,
+                        reconstruct_aggregate)
+from .pipelines import denoise
 from .pursuit import (BatchSolve, DenseColumns, PursuitConfig, PursuitResult, as_columns, omp,
                       omp_many, omp_many_arrays)
 from .scaling import ScaleSpec, downsample_columns, upsample_columns
-from .tensor import Dictionary, SparseCode, normalize_atoms
+from .tensor import Dictionary, SparseCode, Tensor, as_array, normalize_atoms
 
 
 def set_engine(name: str) -> None:

@@ -647,6 +647,110 @@ int cdb_profile_read(int max_entries, char *names, int name_len, double *ms, int
 
 int64_t cdb_launch_count(void) { return g_launches.load(); }
 
+static cdb_status patch_geometry(int rank, const int64_t *sig, const int64_t *pat,
+                                 const int64_t *str, int64_t &n, int64_t &p, int64_t &cells) {
+  if (rank < 1 || rank > 4 || !sig || !pat || !str) return fail(CDB_ERR_ARG, "bad patch geometry");
+  n = p = cells = 1;
+  for (int d = 0; d < rank; d++) {
+    if (pat[d] < 1 || str[d] < 1 || sig[d] < 1 || pat[d] > sig[d])
+      return fail(CDB_ERR_ARG, "bad patch geometry");
+    n *= pat[d];
+    p *= (sig[d] - pat[d]) / str[d] + 1;
+    cells *= sig[d];
+  }
+  return CDB_OK;
+}
+
+cdb_status cdb_extract_patches(const void *signal, int is_f32, int rank,
+                               const int64_t *signal_shape, const int64_t *patch_shape,
+                               const int64_t *stride, int remove_dc, double *rows_out,
+                               double *dc_out, void *stream) {
+  int64_t n, p, cells;
+  cdb_status s = patch_geometry(rank, signal_shape, patch_shape, stride, n, p, cells);
+  if (s != CDB_OK) return s;
+  if (!signal || !rows_out || (remove_dc && !dc_out)) return fail(CDB_ERR_ARG, "null patch buffer");
+  DevInfo di;
+  if ((s = device_info(di)) != CDB_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  InArr sig;
+  OutArr rows, dc;
+  CDB_CUDA(sig.bind(signal, (is_f32 ? 4 : 8) * cells, st));
+  CDB_CUDA(rows.bind(rows_out, sizeof(double) * p * n, st));
+  if (remove_dc) CDB_CUDA(dc.bind(dc_out, sizeof(double) * p, st));
+  CDB_CUDA(cdb::launch_extract_patches(sig.dev, is_f32 != 0, rank, signal_shape, patch_shape,
+                                       stride, remove_dc, (double *)rows.dev,
+                                       remove_dc ? (double *)dc.dev : nullptr, di.sms, st));
+  CDB_CUDA(rows.finish(st));
+  if (remove_dc) CDB_CUDA(dc.finish(st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  return CDB_OK;
+}
+
+cdb_status cdb_reconstruct_aggregate(const cdb_dictionary *dict, const int64_t *sel,
+                                     const double *coef, int64_t k_width, int64_t p,
+                                     const double *dc, int rank, const int64_t *signal_shape,
+                                     const int64_t *patch_shape, const int64_t *stride,
+                                     double *out, int64_t *uncovered, void *stream) {
+  int64_t n, pp, cells;
+  cdb_status s = patch_geometry(rank, signal_shape, patch_shape, stride, n, pp, cells);
+  if (s != CDB_OK) return s;
+  if (!dict || !out || p != pp || n != dict->n || k_width < 0 || (k_width > 0 && (!sel || !coef)))
+    return fail(CDB_ERR_ARG, "bad reconstruct arguments");
+  DevInfo di;
+  if ((s = device_info(di)) != CDB_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  InArr sel_in, coef_in, dc_in;
+  OutArr out_o;
+  CDB_CUDA(sel_in.bind(sel, sizeof(int64_t) * p * k_width, st));
+  CDB_CUDA(coef_in.bind(coef, sizeof(double) * p * k_width, st));
+  if (dc) CDB_CUDA(dc_in.bind(dc, sizeof(double) * p, st));
+  CDB_CUDA(out_o.bind(out, sizeof(double) * cells, st));
+  DevBuf est, unc;
+  CDB_CUDA(est.alloc(sizeof(double) * p * n, st));
+  CDB_CUDA(unc.alloc(sizeof(unsigned long long), st));
+  CDB_CUDA(cudaMemsetAsync(unc.ptr, 0, sizeof(unsigned long long), st));
+  CDB_CUDA(cdb::launch_reconstruct_aggregate(
+      dict->d64, n, (const int64_t *)sel_in.dev, (const double *)coef_in.dev, k_width, p,
+      dc ? (const double *)dc_in.dev : nullptr, rank, signal_shape, patch_shape, stride,
+      est.as<double>(), (double *)out_o.dev, (unsigned long long *)unc.ptr, di.sms, st));
+  CDB_CUDA(out_o.finish(st));
+  unsigned long long h_unc = 0;
+  CDB_CUDA(cudaMemcpyAsync(&h_unc, unc.ptr, sizeof(h_unc), cudaMemcpyDeviceToHost, st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  if (uncovered) *uncovered = (int64_t)h_unc;
+  return CDB_OK;
+}
+
+cdb_status cdb_aggregate_patches(const double *rows, const double *dc, int rank,
+                                 const int64_t *signal_shape, const int64_t *patch_shape,
+                                 const int64_t *stride, double *out, int64_t *uncovered,
+                                 void *stream) {
+  int64_t n, p, cells;
+  cdb_status s = patch_geometry(rank, signal_shape, patch_shape, stride, n, p, cells);
+  if (s != CDB_OK) return s;
+  if (!rows || !out) return fail(CDB_ERR_ARG, "null patch buffer");
+  DevInfo di;
+  if ((s = device_info(di)) != CDB_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  InArr rows_in, dc_in;
+  OutArr out_o;
+  CDB_CUDA(rows_in.bind(rows, sizeof(double) * p * n, st));
+  if (dc) CDB_CUDA(dc_in.bind(dc, sizeof(double) * p, st));
+  CDB_CUDA(out_o.bind(out, sizeof(double) * cells, st));
+  DevBuf unc;
+  CDB_CUDA(unc.alloc(sizeof(unsigned long long), st));
+  CDB_CUDA(cudaMemsetAsync(unc.ptr, 0, sizeof(unsigned long long), st));
+  CDB_CUDA(cdb::launch_aggregate((const double *)rows_in.dev, dc ? (const double *)dc_in.dev : nullptr,
+                                 rank, signal_shape, patch_shape, stride, (double *)out_o.dev,
+                                 (unsigned long long *)unc.ptr, st));
+  CDB_CUDA(out_o.finish(st));
+  unsigned long long h_unc = 0;
+  CDB_CUDA(cudaMemcpyAsync(&h_unc, unc.ptr, sizeof(h_unc), cudaMemcpyDeviceToHost, st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  if (uncovered) *uncovered = (int64_t)h_unc;
+  return CDB_OK;
+}
+
 cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_size, void *rows,
                               int threads) {
   if (!cols || !rows || n < 0 || p < 0 || (elem_size != 4 && elem_size != 8))

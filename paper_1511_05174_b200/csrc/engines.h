@@ -148,6 +148,20 @@ cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int
                                const int64_t *nb, int64_t p, int64_t k1, int64_t smax,
                                double *alpha0, void *work, cudaStream_t stream);
 int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1);
+
+// ---------------------------------------------------------------- patch pipeline ends
+cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const int64_t *sig,
+                                   const int64_t *pat, const int64_t *str, int remove_dc,
+                                   double *rows, double *dc, int num_sms, cudaStream_t stream);
+cudaError_t launch_reconstruct_aggregate(const double *d64, int64_t n, const int64_t *sel,
+                                         const double *coef, int64_t kw, int64_t p,
+                                         const double *dc, int rank, const int64_t *sig,
+                                         const int64_t *pat, const int64_t *str, double *est,
+                                         double *out, unsigned long long *uncovered, int num_sms,
+                                         cudaStream_t stream);
+cudaError_t launch_aggregate(const double *rows, const double *dc, int rank, const int64_t *sig,
+                             const int64_t *pat, const int64_t *str, double *out,
+                             unsigned long long *uncovered, cudaStream_t stream);
 cudaError_t launch_to_f32(const double *d64, int64_t count, float *d32, cudaStream_t stream);
 cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids,
                                      int *count, cudaStream_t stream);

@@ -1,0 +1,243 @@
+// Patch pipeline ends around the pursuit: the denoise /
+// recovery flow extract_patches -> OMP -> atoms @ coef -> aggregate_patches
+// (crossdict patchwork.py:58-122, pipelines.py:200-253), on the device so the
+// patch rows never leave HBM between the steps.
+//
+//  * extract_rows_kernel: every stride position of a rank <= 4 row-major
+//    signal becomes one row of the P x N patch matrix (the OMP row layout:
+//    the reference's columns transposed), in fp64.  With remove_dc the
+//    per-patch mean is subtracted: summed by one lane in element order and
+//    divided by N -- the order numpy's cols.mean(axis=0) reduces in.
+//  * reconstruct_kernel: est_p = D_S x (+ dc_p) straight from the solve's
+//    (sel, coef) rows -- no dense T x P coefficient matrix.
+//  * aggregate_kernel: overlap-add as a gather, one thread per output cell,
+//    adding the covering patches in ascending patch order (the reference's
+//    accumulation order) and dividing by the coverage count; uncovered cells
+//    are 0 and counted.
+#include "common.cuh"
+#include "engines.h"
+
+namespace cdb {
+namespace {
+
+struct Geom {
+  int rank;
+  int64_t sig[4];   // signal extents
+  int64_t pat[4];   // patch extents
+  int64_t str[4];   // strides
+  int64_t grid[4];  // patch positions per axis
+  int64_t n;        // patch size
+  int64_t p;        // patch count
+  int64_t cells;    // signal size
+};
+
+// linear signal offset of patch element e relative to the patch origin
+__device__ __forceinline__ int64_t elem_offset(const Geom &g, int64_t e) {
+  int64_t off = 0, mul = 1;
+  for (int d = g.rank - 1; d >= 0; d--) {
+    const int64_t u = e % g.pat[d];
+    e /= g.pat[d];
+    off += u * mul;
+    mul *= g.sig[d];
+  }
+  return off;
+}
+
+__device__ __forceinline__ int64_t origin_offset(const Geom &g, int64_t p) {
+  int64_t off = 0, mul = 1;
+  for (int d = g.rank - 1; d >= 0; d--) {
+    const int64_t gi = p % g.grid[d];
+    p /= g.grid[d];
+    off += gi * g.str[d] * mul;
+    mul *= g.sig[d];
+  }
+  return off;
+}
+
+// warp per patch; the patch is staged in shared memory (n doubles per warp)
+template <typename ST>
+__global__ void __launch_bounds__(256) extract_rows_kernel(const ST *__restrict__ sig, Geom g,
+                                                           int remove_dc, double *__restrict__ rows,
+                                                           double *__restrict__ dc) {
+  extern __shared__ double xs[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double *buf = xs + (int64_t)wib * g.n;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < g.p; p += nw) {
+    const int64_t base = origin_offset(g, p);
+    for (int64_t e = lane; e < g.n; e += 32) buf[e] = (double)sig[base + elem_offset(g, e)];
+    __syncwarp();
+    double mean = 0.0;
+    if (remove_dc) {
+      double s = 0.0;
+      if (lane == 0)
+        for (int64_t e = 0; e < g.n; e++) s += buf[e];
+      mean = __shfl_sync(CDB_FULL_MASK, s, 0) / (double)g.n;
+      if (lane == 0) dc[p] = mean;
+    }
+    for (int64_t e = lane; e < g.n; e += 32) rows[p * g.n + e] = remove_dc ? buf[e] - mean : buf[e];
+    __syncwarp();
+  }
+}
+
+// est[p][e] = sum_l coef[p][l] * d[sel[p][l]][e]  (+ dc[p]); warp per patch
+__global__ void __launch_bounds__(256) reconstruct_kernel(const double *__restrict__ d64,
+                                                          int64_t n, const int64_t *__restrict__ sel,
+                                                          const double *__restrict__ coef,
+                                                          int64_t kw, int64_t p,
+                                                          const double *__restrict__ dc,
+                                                          double *__restrict__ est) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p; q += nw) {
+    const int64_t *sq = sel + q * kw;
+    const double *cq = coef + q * kw;
+    for (int64_t e = lane; e < n; e += 32) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < kw; l++) {
+        const int64_t j = sq[l];
+        if (j < 0) break;  // -1 padding after the last pick
+        acc = fma(cq[l], __ldg(d64 + j * n + e), acc);
+      }
+      est[q * n + e] = dc ? acc + dc[q] : acc;
+    }
+  }
+}
+
+// thread per output cell: covering patches in ascending patch index
+// (dc != NULL: the patch values are est + dc_p, added before accumulation as
+// the reference's cols + dc[None, :])
+__global__ void __launch_bounds__(256) aggregate_kernel(const double *__restrict__ est,
+                                                        const double *__restrict__ dc, Geom g,
+                                                        double *__restrict__ out,
+                                                        unsigned long long *__restrict__ uncovered) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= g.cells) return;
+  int64_t xc[4] = {0, 0, 0, 0};
+  {
+    int64_t r = x;
+    for (int d = g.rank - 1; d >= 0; d--) {
+      xc[d] = r % g.sig[d];
+      r /= g.sig[d];
+    }
+  }
+  // per axis: grid indices gi with gi*str <= xc < gi*str + pat, ascending
+  int64_t lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+  bool any = true;
+  for (int d = 0; d < g.rank; d++) {
+    const int64_t a = xc[d] - g.pat[d] + 1;  // smallest origin coordinate
+    int64_t l = a <= 0 ? 0 : (a + g.str[d] - 1) / g.str[d];
+    int64_t h = xc[d] / g.str[d];
+    if (h > g.grid[d] - 1) h = g.grid[d] - 1;
+    lo[d] = l;
+    hi[d] = h;
+    if (l > h) any = false;
+  }
+  double acc = 0.0, w = 0.0;
+  if (any) {
+    int64_t gi[4] = {lo[0], lo[1], lo[2], lo[3]};
+    while (true) {
+      int64_t p = 0, e = 0;
+      for (int d = 0; d < g.rank; d++) {
+        p = p * g.grid[d] + gi[d];
+        e = e * g.pat[d] + (xc[d] - gi[d] * g.str[d]);
+      }
+      acc += dc ? est[p * g.n + e] + dc[p] : est[p * g.n + e];
+      w += 1.0;
+      int d = g.rank - 1;  // odometer, last axis fastest = ascending p
+      while (d >= 0 && ++gi[d] > hi[d]) {
+        gi[d] = lo[d];
+        d--;
+      }
+      if (d < 0) break;
+    }
+  }
+  if (w == 0.0) {
+    atomicAdd(uncovered, 1ull);
+    w = 1.0;
+  }
+  out[x] = acc / w;
+}
+
+cudaError_t make_geom(Geom &g, int rank, const int64_t *sig, const int64_t *pat,
+                      const int64_t *str) {
+  if (rank < 1 || rank > 4) return cudaErrorInvalidValue;
+  g.rank = rank;
+  g.n = 1;
+  g.p = 1;
+  g.cells = 1;
+  for (int d = 0; d < 4; d++) g.sig[d] = g.pat[d] = g.str[d] = g.grid[d] = 1;
+  for (int d = 0; d < rank; d++) {
+    if (pat[d] < 1 || str[d] < 1 || pat[d] > sig[d]) return cudaErrorInvalidValue;
+    g.sig[d] = sig[d];
+    g.pat[d] = pat[d];
+    g.str[d] = str[d];
+    g.grid[d] = (sig[d] - pat[d]) / str[d] + 1;
+    g.n *= pat[d];
+    g.p *= g.grid[d];
+    g.cells *= sig[d];
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const int64_t *sig,
+                                   const int64_t *pat, const int64_t *str, int remove_dc,
+                                   double *rows, double *dc, int num_sms, cudaStream_t stream) {
+  ProfScope _ps("extract_patches", stream);
+  Geom g;
+  cudaError_t e = make_geom(g, rank, sig, pat, str);
+  if (e != cudaSuccess) return e;
+  const size_t smem = 8 * sizeof(double) * (size_t)g.n;  // 8 warps
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  int64_t blocks = (g.p + 7) / 8;
+  if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+  auto kf = extract_rows_kernel<float>;
+  auto kd = extract_rows_kernel<double>;
+  if ((e = cudaFuncSetAttribute(f32 ? (const void *)kf : (const void *)kd,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return e;
+  if (f32)
+    kf<<<(unsigned)blocks, 256, smem, stream>>>((const float *)signal, g, remove_dc, rows, dc);
+  else
+    kd<<<(unsigned)blocks, 256, smem, stream>>>((const double *)signal, g, remove_dc, rows, dc);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reconstruct_aggregate(const double *d64, int64_t n, const int64_t *sel,
+                                         const double *coef, int64_t kw, int64_t p,
+                                         const double *dc, int rank, const int64_t *sig,
+                                         const int64_t *pat, const int64_t *str, double *est,
+                                         double *out, unsigned long long *uncovered, int num_sms,
+                                         cudaStream_t stream) {
+  ProfScope _ps("reconstruct_aggregate", stream);
+  Geom g;
+  cudaError_t e = make_geom(g, rank, sig, pat, str);
+  if (e != cudaSuccess) return e;
+  if (g.n != n || g.p != p) return cudaErrorInvalidValue;
+  int64_t blocks = (p + 7) / 8;
+  if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+  reconstruct_kernel<<<(unsigned)blocks, 256, 0, stream>>>(d64, n, sel, coef, kw, p, dc, est);
+  aggregate_kernel<<<(unsigned)((g.cells + 255) / 256), 256, 0, stream>>>(est, nullptr, g, out,
+                                                                           uncovered);
+  note_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aggregate(const double *rows, const double *dc, int rank, const int64_t *sig,
+                             const int64_t *pat, const int64_t *str, double *out,
+                             unsigned long long *uncovered, cudaStream_t stream) {
+  ProfScope _ps("aggregate", stream);
+  Geom g;
+  cudaError_t e = make_geom(g, rank, sig, pat, str);
+  if (e != cudaSuccess) return e;
+  aggregate_kernel<<<(unsigned)((g.cells + 255) / 256), 256, 0, stream>>>(rows, dc, g, out,
+                                                                           uncovered);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cdb

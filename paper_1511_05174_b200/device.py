@@ -113,6 +113,8 @@ def rows_for_device(ys_cols):
     the drop-in makes anyway -- written into pinned memory for large batches."""
     ys_cols = np.asarray(ys_cols)
     n, p = ys_cols.shape
+    if ys_cols.T.flags.c_contiguous:  # already rows (e.g. extract_patches output)
+        return ys_cols.T
     if p < PIN_MIN or ys_cols.dtype not in (np.float32, np.float64):
         return np.ascontiguousarray(ys_cols.T)
     src = np.ascontiguousarray(ys_cols)
@@ -180,3 +182,63 @@ def zero_tree_raw(low: DeviceDictionary, high: DeviceDictionary, fine_shape, fac
                                          *_out_ptrs(lo), *_out_ptrs(hi), N.ENGINES[engine],
                                          N.ptr(ms), stream))
     return lo, hi, ms
+
+
+# ---------------------------------------------------------------- patch pipeline ends
+def _geom(signal_shape, patch_shape, stride):
+    rank = len(signal_shape)
+    return (rank, np.asarray(signal_shape, np.int64), np.asarray(patch_shape, np.int64),
+            np.asarray(stride, np.int64))
+
+
+def extract_patches_raw(signal, patch_shape, stride, remove_dc, rows=None, dc=None, stream=None):
+    """cdb_extract_patches: rows (P x N fp64) and per-patch means (or None).
+
+    ``signal`` is a numpy array or a CUDA tensor (fp32 / fp64); ``rows`` /
+    ``dc`` may be preallocated (numpy or CUDA tensors)."""
+    shape = tuple(signal.shape)
+    rank, sg, pt, st = _geom(shape, patch_shape, stride)
+    n = int(np.prod(pt))
+    p = int(np.prod([(e - q) // s + 1 for e, q, s in zip(shape, patch_shape, stride)]))
+    if isinstance(signal, np.ndarray):
+        src = np.ascontiguousarray(signal)
+        if src.dtype not in (np.float32, np.float64):
+            src = src.astype(np.float64)
+        f32 = 1 if src.dtype == np.float32 else 0
+    else:
+        import torch
+        src = signal.contiguous()
+        f32 = 1 if src.dtype == torch.float32 else 0
+    if rows is None:
+        rows = (pinned_empty if p >= PIN_MIN else np.empty)((p, n), np.float64)
+    if remove_dc and dc is None:
+        dc = np.empty(p, np.float64)
+    N.check(N.load().cdb_extract_patches(N.ptr(src), f32, rank, N.ptr(sg), N.ptr(pt), N.ptr(st),
+                                         int(bool(remove_dc)), N.ptr(rows),
+                                         N.ptr(dc) if remove_dc else None, stream))
+    return rows, (dc if remove_dc else None)
+
+
+def aggregate_patches_raw(rows, dc, signal_shape, patch_shape, stride, out=None, stream=None):
+    """cdb_aggregate_patches: overlap-averaged signal (fp64) and uncovered count."""
+    rank, sg, pt, st = _geom(signal_shape, patch_shape, stride)
+    if out is None:
+        out = np.empty(tuple(signal_shape), np.float64)
+    unc = np.zeros(1, np.int64)
+    N.check(N.load().cdb_aggregate_patches(N.ptr(rows), N.ptr(dc), rank, N.ptr(sg), N.ptr(pt),
+                                           N.ptr(st), N.ptr(out), N.ptr(unc), stream))
+    return out, int(unc[0])
+
+
+def reconstruct_aggregate_raw(dd: DeviceDictionary, sel, coef, p, dc, signal_shape, patch_shape,
+                              stride, out=None, stream=None):
+    """cdb_reconstruct_aggregate: D_S x (+ dc) per patch, overlap-averaged."""
+    rank, sg, pt, st = _geom(signal_shape, patch_shape, stride)
+    kw = int(sel.shape[1]) if len(sel.shape) > 1 else 0
+    if out is None:
+        out = np.empty(tuple(signal_shape), np.float64)
+    unc = np.zeros(1, np.int64)
+    N.check(N.load().cdb_reconstruct_aggregate(dd.handle, N.ptr(sel), N.ptr(coef), kw, int(p),
+                                               N.ptr(dc), rank, N.ptr(sg), N.ptr(pt), N.ptr(st),
+                                               N.ptr(out), N.ptr(unc), stream))
+    return out, int(unc[0])

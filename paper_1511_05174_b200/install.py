@@ -6,6 +6,7 @@ reference imported them by name -- to this package's B200 implementations:
 * ``crossdict.pursuit.{omp, omp_many, omp_many_arrays}``      (pursuit.py:253-461)
 * ``crossdict.crossscale.{zero_tree_omp, zero_tree_omp_many,
   zero_tree_many_arrays}``                                    (crossscale.py:169-312)
+* ``crossdict.patchwork.{extract_patches, aggregate_patches}`` (patchwork.py:58-122)
 * the re-exports in ``crossdict/__init__.py:12-33`` and the by-name imports
   of the callers ``crossdict.pipelines`` (pipelines.py:214-297) and
   ``crossdict.learn`` (learn.py:245-260).
@@ -22,6 +23,7 @@ import importlib
 
 from . import crossscale as _cs
 from . import errors as _errors
+from . import patchwork as _pw
 from . import pursuit as _pursuit
 
 _saved: dict = {}
@@ -34,9 +36,11 @@ _FUNCS = {
     "zero_tree_omp": _cs.zero_tree_omp,
     "zero_tree_omp_many": _cs.zero_tree_omp_many,
     "zero_tree_many_arrays": _cs.zero_tree_many_arrays,
+    "extract_patches": _pw.extract_patches,
+    "aggregate_patches": _pw.aggregate_patches,
 }
 _MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
-            "crossdict.learn")
+            "crossdict.learn", "crossdict.patchwork")
 
 
 def install(package: str = "crossdict") -> list:
@@ -60,6 +64,12 @@ def install(package: str = "crossdict") -> list:
                 setattr(mod, name, fn)
                 patched.append(f"{modname}.{name}")
     _saved["#types"] = dict(_pursuit._types)
+    _saved["#pwtypes"] = dict(_pw._types)
+    try:
+        ref_pw = importlib.import_module(f"{package}.patchwork")
+        _pw._types.update(PatchGrid=ref_pw.PatchGrid, Tensor=ref_tensor.Tensor)
+    except (ImportError, AttributeError):
+        pass
     _pursuit._types.update(SparseCode=ref_tensor.SparseCode, PursuitResult=ref_pursuit.PursuitResult,
                            BatchSolve=ref_pursuit.BatchSolve, ZeroTreeResult=ref_cs.ZeroTreeResult,
                            pursuit_module=ref_pursuit)
@@ -75,6 +85,9 @@ def uninstall() -> None:
         if key == "#types":
             _pursuit._types.clear()
             _pursuit._types.update(val)
+        elif key == "#pwtypes":
+            _pw._types.clear()
+            _pw._types.update(val)
         elif key == "#errors":
             for n, cls in val.items():
                 setattr(_errors, n, cls)
