@@ -397,6 +397,8 @@ def bench_ours(args):
                          f"zero-tree OMP in {dt:.1f} s "
                          f"(oracle/omp_oracle.c restating crossdict's kernel, {threads} threads)"}
 
+    ends = bench_pipeline_ends(peaks) if rank == 0 and world == 1 else None
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": zt_value, "unit": "signals/s", "n_gpus": world,
@@ -416,6 +418,7 @@ def bench_ours(args):
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_zt.items()},
             "kernels_full_ms_per_step": {k: v[0] / args.steps for k, v in prof_full.items()},
             "cpu_baseline": cpu,
+            "pipeline_ends": ends,
             "e2e": {"value": world * P * args.steps / e2e_total, "unit": "signals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "clocks": clk,
@@ -425,6 +428,72 @@ def bench_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_pipeline_ends(peaks, reps=3):
+    """SURVEY §8 row f2 measurement: the device-resident image recovery chain
+    extract_patches -> zero-tree OMP -> reconstruct + overlap-add on a
+    1024 x 1024 image with configs[0]'s 8 x 8 patches (stride 1, ~1.03 M
+    patches) and model; device times by CUDA events, HBM roofline of the two
+    memory-bound ends (algorithmic bytes: patch rows written/read once, the
+    image read/written once)."""
+    import torch
+    from paper_1511_05174_b200 import device as D
+    from paper_1511_05174_b200 import patchwork as PW
+    w = W.CONFIGS[0]
+    d = W.dictionaries(0)
+    rng = np.random.default_rng(7)
+    img = torch.from_numpy(np.cumsum(rng.standard_normal((1024, 1024)), axis=1) / 32.0).cuda()
+    patch, stride = w.fine_shape, (1, 1)
+    p = PW.patch_count(img.shape, patch, stride)
+    n = w.n_high
+    rows = torch.empty((p, n), dtype=torch.float64, device="cuda")
+    dc = torch.empty(p, dtype=torch.float64, device="cuda")
+    est = torch.empty_like(img)
+    lo, hi = D.device_dictionary(d.low_t), D.device_dictionary(d.high_t)
+
+    def outs(k):
+        return dict(sel=torch.empty((p, k), dtype=torch.int64, device="cuda"),
+                    alpha=torch.empty((p, k), dtype=torch.float64, device="cuda"),
+                    counts=torch.empty(p, dtype=torch.int64, device="cuda"),
+                    rnorm=torch.empty(p, dtype=torch.float64, device="cuda"),
+                    scans=torch.empty(p, dtype=torch.int64, device="cuda"),
+                    flag=torch.empty(p, dtype=torch.uint8, device="cuda"))
+    ol, oh = outs(w.k), outs(w.k)
+    stream = torch.cuda.current_stream()
+
+    def run(ev):
+        ev[0].record(stream)
+        D.extract_patches_raw(img, patch, stride, True, rows, dc)
+        ev[1].record(stream)
+        D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, rows, p, w.k, w.k, W.REL_TOL, False,
+                        "auto", ol, oh)
+        ev[2].record(stream)
+        D.reconstruct_aggregate_raw(hi, oh["sel"], oh["alpha"], p, dc, tuple(img.shape), patch,
+                                    stride, est)
+        ev[3].record(stream)
+
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    run(evs)
+    torch.cuda.synchronize()
+    t = np.zeros(3)
+    for _ in range(reps):
+        run(evs)
+        torch.cuda.synchronize()
+        t += [evs[i].elapsed_time(evs[i + 1]) for i in range(3)]
+    t /= reps
+    cells = img.numel()
+    b_extract = 8.0 * (cells + p * n + p)           # image in, rows + dc out
+    b_recon = 8.0 * (p * n + p + 2 * p * w.k + cells)  # est rows (+dc), codes, image out
+    hbm = peaks["hbm_gbs"]
+    ach = b_extract / (t[0] * 1e-3) / 1e9
+    return {"workload": f"1024x1024 fp64 image, {patch[0]}x{patch[1]} patches stride 1 "
+                        f"({p} patches), configs[0] zero-tree model, K={w.k}, remove_dc",
+            "patches_per_s": p / (t.sum() * 1e-3), "unit": "patches/s",
+            "ms": {"extract_patches": t[0], "zero_tree": t[1], "reconstruct_aggregate": t[2]},
+            "roofline": {"bound": "hbm", "kernel": "extract_patches", "achieved": ach,
+                         "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                         "reconstruct_aggregate_gbs": b_recon / (t[2] * 1e-3) / 1e9}}
 
 
 def main():

@@ -54,28 +54,35 @@ __device__ __forceinline__ int64_t origin_offset(const Geom &g, int64_t p) {
   return off;
 }
 
-// warp per patch; the patch is staged in shared memory (n doubles per warp)
+// warp per patch; the patch is staged in shared memory (n doubles per warp),
+// the cell offsets of a patch relative to its origin are a per-block table
 template <typename ST>
 __global__ void __launch_bounds__(256) extract_rows_kernel(const ST *__restrict__ sig, Geom g,
                                                            int remove_dc, double *__restrict__ rows,
                                                            double *__restrict__ dc) {
   extern __shared__ double xs[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double *buf = xs + (int64_t)wib * g.n;
+  const int n = (int)g.n;
+  int *offs = (int *)(xs + 8 * n);  // n cell offsets (signal size < 2^31)
+  for (int e = threadIdx.x; e < n; e += blockDim.x) offs[e] = (int)elem_offset(g, e);
+  __syncthreads();
+  double *buf = xs + wib * n;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < g.p; p += nw) {
-    const int64_t base = origin_offset(g, p);
-    for (int64_t e = lane; e < g.n; e += 32) buf[e] = (double)sig[base + elem_offset(g, e)];
-    __syncwarp();
-    double mean = 0.0;
-    if (remove_dc) {
-      double s = 0.0;
-      if (lane == 0)
-        for (int64_t e = 0; e < g.n; e++) s += buf[e];
-      mean = __shfl_sync(CDB_FULL_MASK, s, 0) / (double)g.n;
-      if (lane == 0) dc[p] = mean;
+    const ST *src = sig + origin_offset(g, p);
+    double *dst = rows + p * n;
+    if (!remove_dc) {
+      for (int e = lane; e < n; e += 32) dst[e] = (double)src[offs[e]];
+      continue;
     }
-    for (int64_t e = lane; e < g.n; e += 32) rows[p * g.n + e] = remove_dc ? buf[e] - mean : buf[e];
+    for (int e = lane; e < n; e += 32) buf[e] = (double)src[offs[e]];
+    __syncwarp();
+    double s = 0.0;
+    if (lane == 0)
+      for (int e = 0; e < n; e++) s += buf[e];  // numpy's axis-0 order
+    const double mean = __shfl_sync(CDB_FULL_MASK, s, 0) / (double)n;
+    if (lane == 0) dc[p] = mean;
+    for (int e = lane; e < n; e += 32) dst[e] = buf[e] - mean;
     __syncwarp();
   }
 }
@@ -106,45 +113,47 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const double *__restri
 
 // thread per output cell: covering patches in ascending patch index
 // (dc != NULL: the patch values are est + dc_p, added before accumulation as
-// the reference's cols + dc[None, :])
+// the reference's cols + dc[None, :]).  32-bit index math (cells < 2^31).
 __global__ void __launch_bounds__(256) aggregate_kernel(const double *__restrict__ est,
                                                         const double *__restrict__ dc, Geom g,
                                                         double *__restrict__ out,
                                                         unsigned long long *__restrict__ uncovered) {
-  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= g.cells) return;
-  int64_t xc[4] = {0, 0, 0, 0};
+  const int rank = g.rank, n = (int)g.n;
+  int xc[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
   {
-    int64_t r = x;
-    for (int d = g.rank - 1; d >= 0; d--) {
-      xc[d] = r % g.sig[d];
-      r /= g.sig[d];
+    int r = x;
+    for (int d = rank - 1; d >= 0; d--) {
+      xc[d] = r % (int)g.sig[d];
+      r /= (int)g.sig[d];
     }
   }
-  // per axis: grid indices gi with gi*str <= xc < gi*str + pat, ascending
-  int64_t lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
   bool any = true;
-  for (int d = 0; d < g.rank; d++) {
-    const int64_t a = xc[d] - g.pat[d] + 1;  // smallest origin coordinate
-    int64_t l = a <= 0 ? 0 : (a + g.str[d] - 1) / g.str[d];
-    int64_t h = xc[d] / g.str[d];
-    if (h > g.grid[d] - 1) h = g.grid[d] - 1;
+  for (int d = 0; d < rank; d++) {  // grid indices gi with gi*str <= xc < gi*str + pat
+    const int st = (int)g.str[d];
+    const int a = xc[d] - (int)g.pat[d] + 1;
+    const int l = a <= 0 ? 0 : (a + st - 1) / st;
+    int h = xc[d] / st;
+    if (h > (int)g.grid[d] - 1) h = (int)g.grid[d] - 1;
     lo[d] = l;
     hi[d] = h;
     if (l > h) any = false;
   }
   double acc = 0.0, w = 0.0;
   if (any) {
-    int64_t gi[4] = {lo[0], lo[1], lo[2], lo[3]};
+    int gi[4] = {lo[0], lo[1], lo[2], lo[3]};
     while (true) {
-      int64_t p = 0, e = 0;
-      for (int d = 0; d < g.rank; d++) {
+      int64_t p = 0;
+      int e = 0;
+      for (int d = 0; d < rank; d++) {
         p = p * g.grid[d] + gi[d];
-        e = e * g.pat[d] + (xc[d] - gi[d] * g.str[d]);
+        e = e * (int)g.pat[d] + (xc[d] - gi[d] * (int)g.str[d]);
       }
-      acc += dc ? est[p * g.n + e] + dc[p] : est[p * g.n + e];
+      const double v = est[p * n + e];
+      acc += dc ? v + dc[p] : v;
       w += 1.0;
-      int d = g.rank - 1;  // odometer, last axis fastest = ascending p
+      int d = rank - 1;  // odometer, last axis fastest = ascending p
       while (d >= 0 && ++gi[d] > hi[d]) {
         gi[d] = lo[d];
         d--;
@@ -189,10 +198,11 @@ cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const
   Geom g;
   cudaError_t e = make_geom(g, rank, sig, pat, str);
   if (e != cudaSuccess) return e;
-  const size_t smem = 8 * sizeof(double) * (size_t)g.n;  // 8 warps
+  const size_t smem = 8 * sizeof(double) * (size_t)g.n + sizeof(int) * (size_t)g.n;  // 8 warps
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   int64_t blocks = (g.p + 7) / 8;
-  if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+  if (blocks > (int64_t)num_sms * 32) blocks = (int64_t)num_sms * 32;
+  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   auto kf = extract_rows_kernel<float>;
   auto kd = extract_rows_kernel<double>;
   if ((e = cudaFuncSetAttribute(f32 ? (const void *)kf : (const void *)kd,
@@ -221,6 +231,7 @@ cudaError_t launch_reconstruct_aggregate(const double *d64, int64_t n, const int
   int64_t blocks = (p + 7) / 8;
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   reconstruct_kernel<<<(unsigned)blocks, 256, 0, stream>>>(d64, n, sel, coef, kw, p, dc, est);
+  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   aggregate_kernel<<<(unsigned)((g.cells + 255) / 256), 256, 0, stream>>>(est, nullptr, g, out,
                                                                            uncovered);
   note_launch(2);
@@ -234,6 +245,7 @@ cudaError_t launch_aggregate(const double *rows, const double *dc, int rank, con
   Geom g;
   cudaError_t e = make_geom(g, rank, sig, pat, str);
   if (e != cudaSuccess) return e;
+  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   aggregate_kernel<<<(unsigned)((g.cells + 255) / 256), 256, 0, stream>>>(rows, dc, g, out,
                                                                            uncovered);
   note_launch();
