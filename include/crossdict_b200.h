@@ -44,7 +44,9 @@ typedef enum {
     CDB_ERR_ARG = 1,      /* size / pointer argument invalid                   */
     CDB_ERR_CUDA = 2,     /* a CUDA runtime call failed (see cdb_last_error)   */
     CDB_ERR_NOMEM = 3,    /* device or pinned allocation failed                */
-    CDB_ERR_NODEV = 4     /* no sm_100 device available                        */
+    CDB_ERR_NODEV = 4,    /* no sm_100 device available                        */
+    CDB_ERR_FORMAT = 5,   /* malformed .csd file (crossdict FormatError)       */
+    CDB_ERR_CHECKSUM = 6  /* .csd CRC-32 mismatch (crossdict ChecksumError)    */
 } cdb_status;
 
 /* Opaque device-resident dictionary (atoms as rows, T x N). */
@@ -189,6 +191,26 @@ cdb_status cdb_aggregate_patches(const double *rows, const double *dc, int rank,
                                  const int64_t *signal_shape, const int64_t *patch_shape,
                                  const int64_t *stride, double *out, int64_t *uncovered,
                                  void *stream);
+
+/* ---- .csd model files (crossdict fileio.py:216-256) ----
+ * Layout (little-endian): "CSDM", version u32 (=1), scale count u32 (1 or 2),
+ * one record per scale coarse -> fine (patch rank u32, extents u32 x rank,
+ * N, T, K, Q u32, atoms fp64 column-major N x T), CRC-32 of every preceding
+ * byte.  The column-major atom block is exactly the T x N row layout
+ * cdb_dictionary_create takes.
+ *
+ * cdb_csd_read verifies the CRC before parsing (a mismatch refuses the file,
+ * CDB_ERR_CHECKSUM) and every structural rule of the reference loader
+ * (CDB_ERR_FORMAT, message as the reference's).  Call it with atoms == NULL
+ * to get the scale count and the per-scale geometry; then again with one
+ * caller buffer of N*T doubles per scale to receive the atoms (T x N rows). */
+typedef struct {
+    int32_t rank;
+    int64_t extents[4];
+    int64_t n, t, k, q;
+} cdb_csd_scale;
+cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *scales,
+                        double *const *atoms_t);
 
 /* Host layout helper: rows[j][i] = cols[i][j] for an n x p column batch (the
  * reference's N x P signal matrix) into p x n rows (the kernel layout; the

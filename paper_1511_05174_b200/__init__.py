@@ -13,7 +13,9 @@ from . import errors
 from .crossscale import (CrossScaleModel, ZeroTreeResult, cross_scale_map, omp_cost,
                          predicted_speedup, zero_tree_many_arrays, zero_tree_omp,
                          zero_tree_omp_many)
-from .errors import ConfigError, CrossdictError, DegenerateAtomError, DimensionError, DomainError
+from .errors import (ChecksumError, ConfigError, CrossdictError, DegenerateAtomError,
+                     DimensionError, DomainError, FormatError)
+from .fileio import SingleScaleModel, load_model, save_model
 from .install import install, uninstall
 from .patchwork import (PatchGrid, aggregate_patches, extract_patches, patch_count,
                         reconstruct_aggregate)

@@ -751,6 +751,119 @@ cdb_status cdb_aggregate_patches(const double *rows, const double *dc, int rank,
   return CDB_OK;
 }
 
+// ---------------------------------------------------------------- .csd files
+static uint32_t crc32_zlib(const uint8_t *data, size_t len) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; i++) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < len; i++) c = table[(c ^ data[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+static std::string py_tuple(const int64_t *v, int r) {  // Python's tuple repr
+  std::string s = "(";
+  for (int i = 0; i < r; i++) {
+    if (i) s += ", ";
+    s += std::to_string(v[i]);
+  }
+  return s + (r == 1 ? ",)" : ")");
+}
+
+cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *scales,
+                        double *const *atoms_t) {
+  if (!path || !scale_count || !scales) return fail(CDB_ERR_ARG, "bad csd arguments");
+  const std::string P(path);
+  FILE *f = fopen(path, "rb");
+  if (!f) return fail(CDB_ERR_ARG, P + ": cannot open");
+  std::vector<uint8_t> raw;
+  uint8_t chunk[1 << 16];
+  size_t got;
+  while ((got = fread(chunk, 1, sizeof(chunk), f)) > 0) raw.insert(raw.end(), chunk, chunk + got);
+  fclose(f);
+  if (raw.size() < 16) return fail(CDB_ERR_FORMAT, P + ": too short for a model file");
+  uint32_t stored;
+  memcpy(&stored, raw.data() + raw.size() - 4, 4);
+  const size_t body = raw.size() - 4;
+  if (crc32_zlib(raw.data(), body) != stored)
+    return fail(CDB_ERR_CHECKSUM, P + ": CRC-32 mismatch, refusing to load");
+  if (memcmp(raw.data(), "CSDM", 4) != 0)
+    return fail(CDB_ERR_FORMAT, P + ": not a .csd file (bad magic)");
+  size_t pos = 4;
+  auto take = [&](uint32_t &v) -> bool {
+    if (pos + 4 > body) return false;
+    memcpy(&v, raw.data() + pos, 4);
+    pos += 4;
+    return true;
+  };
+  uint32_t version, count;
+  if (!take(version)) return fail(CDB_ERR_FORMAT, P + ": truncated file");
+  if (version != 1)
+    return fail(CDB_ERR_FORMAT, P + ": unsupported version " + std::to_string(version));
+  if (!take(count)) return fail(CDB_ERR_FORMAT, P + ": truncated file");
+  if (count != 1 && count != 2)
+    return fail(CDB_ERR_FORMAT, P + ": scale count " + std::to_string(count) + " not in (1, 2)");
+  for (uint32_t sidx = 0; sidx < count; sidx++) {
+    cdb_csd_scale &sc = scales[sidx];
+    uint32_t rank;
+    if (!take(rank)) return fail(CDB_ERR_FORMAT, P + ": truncated file");
+    if (rank < 1 || rank > 4)
+      return fail(CDB_ERR_FORMAT, P + ": patch rank " + std::to_string(rank) + " outside 1..4");
+    sc.rank = (int32_t)rank;
+    int64_t prod = 1;
+    for (uint32_t d = 0; d < 4; d++) sc.extents[d] = 0;
+    if (pos + 4 * rank > body) return fail(CDB_ERR_FORMAT, P + ": truncated file");
+    for (uint32_t d = 0; d < rank; d++) {
+      uint32_t e;
+      take(e);
+      sc.extents[d] = e;
+      prod *= e;
+    }
+    uint32_t nn, tt, kk, qq;
+    if (pos + 16 > body) return fail(CDB_ERR_FORMAT, P + ": truncated file");
+    take(nn);
+    take(tt);
+    take(kk);
+    take(qq);
+    if ((int64_t)nn != prod)
+      return fail(CDB_ERR_FORMAT, P + ": N=" + std::to_string(nn) +
+                                      " inconsistent with patch shape " +
+                                      py_tuple(sc.extents, (int)rank));
+    sc.n = nn;
+    sc.t = tt;
+    sc.k = kk;
+    sc.q = qq;
+    const size_t bytes = (size_t)8 * nn * tt;
+    if (pos + bytes > body) return fail(CDB_ERR_FORMAT, P + ": truncated atom data");
+    if (atoms_t && atoms_t[sidx]) memcpy(atoms_t[sidx], raw.data() + pos, bytes);
+    pos += bytes;
+  }
+  *scale_count = (int32_t)count;
+  if (count == 2) {
+    const cdb_csd_scale &lo = scales[0], &hi = scales[1];
+    if (hi.q != 0)
+      return fail(CDB_ERR_FORMAT,
+                  P + ": finest scale must have Q=0, got " + std::to_string(hi.q));
+    if (hi.t != lo.q * lo.t)
+      return fail(CDB_ERR_FORMAT, P + ": T_high=" + std::to_string(hi.t) +
+                                      " != Q*T_low=" + std::to_string(lo.q * lo.t));
+    bool bad = lo.rank != hi.rank;
+    for (int d = 0; d < hi.rank && !bad; d++) bad = hi.extents[d] % lo.extents[d] != 0;
+    if (bad)
+      return fail(CDB_ERR_FORMAT, P + ": fine shape " + py_tuple(hi.extents, hi.rank) +
+                                      " not divisible by coarse " +
+                                      py_tuple(lo.extents, lo.rank));
+  }
+  return CDB_OK;
+}
+
 cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_size, void *rows,
                               int threads) {
   if (!cols || !rows || n < 0 || p < 0 || (elem_size != 4 && elem_size != 8))

@@ -28,7 +28,7 @@ from . import pursuit as _pursuit
 
 _saved: dict = {}
 _ERRORS = ("CrossdictError", "DimensionError", "DomainError", "DegenerateAtomError",
-           "ConfigError")
+           "ConfigError", "ChecksumError", "FormatError")
 _FUNCS = {
     "omp": _pursuit.omp,
     "omp_many": _pursuit.omp_many,
@@ -75,7 +75,8 @@ def install(package: str = "crossdict") -> list:
                            pursuit_module=ref_pursuit)
     _saved["#errors"] = {n: getattr(_errors, n) for n in _ERRORS}
     for n in _ERRORS:
-        setattr(_errors, n, getattr(ref_errors, n))
+        if hasattr(ref_errors, n):
+            setattr(_errors, n, getattr(ref_errors, n))
     return patched
 
 
