@@ -115,6 +115,20 @@ cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int
                                  int engine, void *stream);
 
 /*
+ * Ragged block-restricted batched OMP: signal p may use its first nb[p]
+ * block ids of row p of blocks (P x nb_max, ascending within the used
+ * prefix); budget min(k_max, nb[p]*q, N) per signal; outputs k_max wide.
+ * One call for what crossdict's K-SVD coding stage issues as one
+ * cdb_omp_batch_blocked per distinct block count (learn.py:240-262).
+ */
+cdb_status cdb_omp_batch_blocked_ragged(const cdb_dictionary *dict, const void *ys, int ys_is_f32,
+                                        int64_t p, int64_t k_max, const double *eps,
+                                        const int64_t *blocks, int64_t nb_max, const int64_t *nb,
+                                        int64_t q, int64_t *out_sel, double *out_coef,
+                                        int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                                        uint8_t *out_flag, int engine, void *stream);
+
+/*
  * Batched zero-tree OMP.  Replaces crossscale.zero_tree_many_arrays
  * (crossscale.py:235-283) and, with phi_mode != 0, the Phi-composed
  * two-step solve of zero_tree_omp (crossscale.py:169-232) on precomputed

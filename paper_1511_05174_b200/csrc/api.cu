@@ -994,11 +994,14 @@ cdb_status cdb_debug_corr_topk(const cdb_dictionary *d, const float *rows, int64
   return CDB_OK;
 }
 
+// nb != NULL (mode 2): per-signal block counts, budget min(k_max, nb*q, N)
+// per signal (the reference's per-group k_max rule, pursuit.py:423).
 static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_is_f32, int64_t p,
                              int64_t k_max, const double *eps, const int64_t *ids, int64_t stride,
                              int mode, int64_t q, int64_t *out_sel, double *out_coef,
                              int64_t *out_count, double *out_rnorm, int64_t *out_scans,
-                             uint8_t *out_flag, int engine, void *stream) {
+                             uint8_t *out_flag, int engine, void *stream,
+                             const int64_t *nb = nullptr) {
   if (!dict || p < 0 || k_max < 0 || (p > 0 && (!ys || !eps)))
     return fail(CDB_ERR_ARG, "bad omp arguments");
   if (p == 0) return CDB_OK;
@@ -1016,7 +1019,8 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
         {(void *)ids, sizeof(int64_t) * (mode ? stride : 0) + (mode ? 0 : 8), false},
         {out_sel, sizeof(int64_t) * k_max, true}, {out_coef, sizeof(double) * k_max, true},
         {out_count, sizeof(int64_t), true}, {out_rnorm, sizeof(double), true},
-        {out_scans, sizeof(int64_t), true}, {out_flag, sizeof(uint8_t), true}};
+        {out_scans, sizeof(int64_t), true}, {out_flag, sizeof(uint8_t), true},
+        {(void *)nb, sizeof(int64_t), false}};
     if (!mode) arrs[2].host = nullptr;
     return run_pipelined(p, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
                                           cudaStream_t s2) -> cdb_status {
@@ -1027,16 +1031,19 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
       c.stride = stride;
       c.q = q;
       c.nb_fixed = stride;
+      c.nb = nb ? (const int64_t *)dv[9] : nullptr;
+      c.clip = nb ? 1 : 0;
       Outs o;
       dev_outs(o, dv[3], dv[4], dv[5], dv[6], dv[7], dv[8]);
       return run_omp(dict, dv[0], f32, len, k_max, k_max, (const double *)dv[1], c, max_c0, o,
                      engine, di, s2);
     });
   }
-  InArr y_in, e_in, id_in;
+  InArr y_in, e_in, id_in, nb_in;
   CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
   CDB_CUDA(e_in.bind(eps, sizeof(double) * p, st));
   if (mode != 0) CDB_CUDA(id_in.bind(ids, sizeof(int64_t) * p * stride, st));
+  if (nb) CDB_CUDA(nb_in.bind(nb, sizeof(int64_t) * p, st));
   Outs o;
   CDB_CUDA(o.bind(p, k_max, out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, st));
   cdb::Cands c{};
@@ -1045,9 +1052,9 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
   c.ids = (const int64_t *)id_in.dev;
   c.stride = stride;
   c.q = q;
-  c.nb = nullptr;
+  c.nb = nb ? (const int64_t *)nb_in.dev : nullptr;
   c.nb_fixed = stride;
-  c.clip = 0;
+  c.clip = nb ? 1 : 0;
   const int64_t max_c = mode == 0 ? dict->t : (mode == 1 ? stride : stride * q);
   cdb_status s = run_omp(dict, y_in.dev, f32, p, k_max, k_max, (const double *)e_in.dev, c, max_c,
                          o, engine, di, st);
@@ -1066,6 +1073,17 @@ cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f
     return fail(CDB_ERR_ARG, "restricted call without allowed ids");
   return omp_common(dict, ys, ys_is_f32, p, k_max, eps, allowed, s_allowed, restricted ? 1 : 0, 1,
                     out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, engine, stream);
+}
+
+cdb_status cdb_omp_batch_blocked_ragged(const cdb_dictionary *dict, const void *ys, int ys_is_f32,
+                                        int64_t p, int64_t k_max, const double *eps,
+                                        const int64_t *blocks, int64_t nb_max, const int64_t *nb,
+                                        int64_t q, int64_t *out_sel, double *out_coef,
+                                        int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                                        uint8_t *out_flag, int engine, void *stream) {
+  if (p > 0 && (!blocks || !nb || nb_max < 1 || q < 1)) return fail(CDB_ERR_ARG, "bad block arguments");
+  return omp_common(dict, ys, ys_is_f32, p, k_max, eps, blocks, nb_max, 2, q, out_sel, out_coef,
+                    out_count, out_rnorm, out_scans, out_flag, engine, stream, nb);
 }
 
 cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int ys_is_f32,

@@ -242,3 +242,15 @@ def reconstruct_aggregate_raw(dd: DeviceDictionary, sel, coef, p, dc, signal_sha
                                                N.ptr(dc), rank, N.ptr(sg), N.ptr(pt), N.ptr(st),
                                                N.ptr(out), N.ptr(unc), stream))
     return out, int(unc[0])
+
+
+def omp_batch_blocked_ragged_raw(dd: DeviceDictionary, ys, p: int, k_max: int, eps, blocks, nb,
+                                 q: int, engine: str = "auto", out=None, stream=None):
+    """cdb_omp_batch_blocked_ragged: signal p uses the first nb[p] ids of row p."""
+    o = out if out is not None else _out(p, k_max)
+    yptr, f32 = _ys_arg(ys)
+    N.check(N.load().cdb_omp_batch_blocked_ragged(dd.handle, yptr, f32, p, k_max, N.ptr(eps),
+                                                  N.ptr(blocks), int(blocks.shape[1]), N.ptr(nb),
+                                                  int(q), *_out_ptrs(o), N.ENGINES[engine],
+                                                  stream))
+    return o

@@ -7,6 +7,8 @@ reference imported them by name -- to this package's B200 implementations:
 * ``crossdict.crossscale.{zero_tree_omp, zero_tree_omp_many,
   zero_tree_many_arrays}``                                    (crossscale.py:169-312)
 * ``crossdict.patchwork.{extract_patches, aggregate_patches}`` (patchwork.py:58-122)
+* ``crossdict.learn._code_stage`` (learn.py:240-262): K-SVD's coding stage as
+  one ragged block-restricted device call
 * the re-exports in ``crossdict/__init__.py:12-33`` and the by-name imports
   of the callers ``crossdict.pipelines`` (pipelines.py:214-297) and
   ``crossdict.learn`` (learn.py:245-260).
@@ -23,6 +25,7 @@ import importlib
 
 from . import crossscale as _cs
 from . import errors as _errors
+from . import learn as _learn
 from . import patchwork as _pw
 from . import pursuit as _pursuit
 
@@ -38,6 +41,7 @@ _FUNCS = {
     "zero_tree_many_arrays": _cs.zero_tree_many_arrays,
     "extract_patches": _pw.extract_patches,
     "aggregate_patches": _pw.aggregate_patches,
+    "_code_stage": _learn.code_stage,  # crossdict.learn only (learn.py:240-262)
 }
 _MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
             "crossdict.learn", "crossdict.patchwork")

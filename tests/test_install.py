@@ -28,6 +28,12 @@ def test_install_rebinds_and_restores(crossdict):
     try:
         assert "crossdict.pursuit.omp_many_arrays" in patched
         assert "crossdict.pipelines.zero_tree_many_arrays" in patched
+        # K-SVD coding stage and the patch pipeline ends
+        assert "crossdict.learn._code_stage" in patched
+        assert "crossdict.patchwork.extract_patches" in patched
+        assert "crossdict.pipelines.aggregate_patches" in patched
+        import crossdict.learn as cl
+        assert cl._code_stage is b200.learn.code_stage
         assert crossdict.pursuit.omp_many_arrays is b200.omp_many_arrays
         assert crossdict.crossscale.zero_tree_many_arrays is b200.zero_tree_many_arrays
         # validation happens on the host, with the reference's exception classes
