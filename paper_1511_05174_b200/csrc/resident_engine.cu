@@ -44,6 +44,7 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 
 constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 
+
 // FULL: candidate jl of lane l is atom l + 32u (mode 0) -> compile-time
 // shared-memory offsets in the correlation loop.  R signals per warp share
 // every dictionary element loaded from shared memory (R FMAs per LDS).
@@ -71,7 +72,7 @@ constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 // duplicated ({r_i, r_i}) so one 16-byte load feeds two dimensions.
 // F32C requires FULL and U >= 4.
 template <typename YT, int U, bool FULL, int R, bool F32C>
-__global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
+__global__ void __launch_bounds__(R >= 4 ? 384 : (R == 1 ? 768 : 512), 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
   extern __shared__ __align__(16) double rs[];
   const int n = (int)a.n, T = (int)a.t, kw = (int)a.k_width, Tp = (int)a.t_pad;
@@ -417,8 +418,12 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : 512, 1)
 // Signals per warp: 4 (every dictionary element read from shared memory
 // feeds 4 FMAs) when the per-lane candidate arrays are small, else 2.
 template <int U>
-constexpr int res_r() { return U > 0 ? 2 : 2; }  // R = 4 measured slower (3.43 vs 3.09 ms, cfg 1 step 1)
-constexpr int res_max_warps(int r) { return r >= 4 ? 12 : RES_WARPS; }  // launch bounds
+// signals per warp: 1 with 24 warps/SM measured best for cfg 1 step 1
+// (2.76 ms; R = 2 x 16 warps 2.83 ms; R = 4 x 12 warps 3.43 ms): the
+// least-squares tail is latency-bound, so independent warps beat the
+// shared-memory reuse of several signals per warp
+constexpr int res_r() { return U > 0 ? 1 : 1; }
+constexpr int res_max_warps(int r) { return r >= 4 ? 12 : (r == 1 ? 24 : RES_WARPS); }
 
 template <typename YT, int U>
 cudaError_t launch_u(const ResidentArgs &args, const YT *ys, int64_t base, int smem_optin,
