@@ -72,7 +72,7 @@ constexpr int RES_WARPS = 16;   // warps per CTA (512 threads)
 // duplicated ({r_i, r_i}) so one 16-byte load feeds two dimensions.
 // F32C requires FULL and U >= 4.
 template <typename YT, int U, bool FULL, int R, bool F32C>
-__global__ void __launch_bounds__(R >= 4 ? 384 : (R == 1 ? 768 : 512), 1)
+__global__ void __launch_bounds__(R >= 4 ? 384 : (R == 1 ? 1024 : 512), 1)
     resident_omp_kernel(ResidentArgs a, const YT *__restrict__ ys) {
   extern __shared__ __align__(16) double rs[];
   const int n = (int)a.n, T = (int)a.t, kw = (int)a.k_width, Tp = (int)a.t_pad;
@@ -418,12 +418,12 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : (R == 1 ? 768 : 512), 1)
 // Signals per warp: 4 (every dictionary element read from shared memory
 // feeds 4 FMAs) when the per-lane candidate arrays are small, else 2.
 template <int U>
-// signals per warp: 1 with 24 warps/SM measured best for cfg 1 step 1
-// (2.76 ms; R = 2 x 16 warps 2.83 ms; R = 4 x 12 warps 3.43 ms): the
+// signals per warp: 1 with 32 warps/SM measured best for cfg 1 step 1
+// (2.67 ms; 24 warps 2.76; R = 2 x 16 warps 2.83; R = 4 x 12 warps 3.43): the
 // least-squares tail is latency-bound, so independent warps beat the
 // shared-memory reuse of several signals per warp
 constexpr int res_r() { return U > 0 ? 1 : 1; }
-constexpr int res_max_warps(int r) { return r >= 4 ? 12 : (r == 1 ? 24 : RES_WARPS); }
+constexpr int res_max_warps(int r) { return r >= 4 ? 12 : (r == 1 ? 32 : RES_WARPS); }
 
 template <typename YT, int U>
 cudaError_t launch_u(const ResidentArgs &args, const YT *ys, int64_t base, int smem_optin,
