@@ -115,6 +115,22 @@ cdb_status cdb_omp_batch_blocked(const cdb_dictionary *dict, const void *ys, int
                                  int engine, void *stream);
 
 /*
+ * Masked batched OMP (the per-patch mask operators of
+ * crossdict pipelines._recover_operator, pipelines.py:256-322, sensing.py:
+ * 222-231): signal p is measured on the m[p] coordinates rows[p][0..m[p])
+ * (ascending, int32, row stride N) of the atoms, i.e. OMP over the compacted
+ * effective dictionary E_p = D[rows_p, :] with the m[p] measurements in
+ * ys[p][0..m[p]) (fp64, row stride N); budget min(k_max, T, m[p]).  Runs the
+ * exact engine: selections, coefficients and residuals follow the
+ * reference's arithmetic on E_p.
+ */
+cdb_status cdb_omp_batch_masked(const cdb_dictionary *dict, const double *ys,
+                                const int32_t *rows, const int64_t *m, int64_t p, int64_t k_max,
+                                const double *eps, int64_t *out_sel, double *out_coef,
+                                int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                                uint8_t *out_flag, void *stream);
+
+/*
  * Ragged block-restricted batched OMP: signal p may use its first nb[p]
  * block ids of row p of blocks (P x nb_max, ascending within the used
  * prefix); budget min(k_max, nb[p]*q, N) per signal; outputs k_max wide.

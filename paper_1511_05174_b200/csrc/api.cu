@@ -183,7 +183,8 @@ constexpr int64_t kScratchBudget = int64_t(4) << 30;  // per-call global scratch
 cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t count,
                      const int64_t *sig_ids, int64_t k_max, int64_t kw, const double *eps,
                      const cdb::Cands &cands, int64_t max_cands, Outs &o, const DevInfo &di,
-                     cudaStream_t st, const int *count_dev = nullptr) {
+                     cudaStream_t st, const int *count_dev = nullptr,
+                     const int32_t *rows = nullptr, const int64_t *m_sig = nullptr) {
   if (count <= 0) return CDB_OK;
   cdb::ExactArgs a{};
   a.mat_t = d->d64;
@@ -193,6 +194,8 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
   a.sig_ids = sig_ids;
   a.p_count = count;
   a.p_count_dev = count_dev;
+  a.rows = rows;
+  a.m_sig = m_sig;
   a.k_max = k_max;
   a.k_width = kw;
   a.eps = eps;
@@ -1073,6 +1076,41 @@ cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f
     return fail(CDB_ERR_ARG, "restricted call without allowed ids");
   return omp_common(dict, ys, ys_is_f32, p, k_max, eps, allowed, s_allowed, restricted ? 1 : 0, 1,
                     out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, engine, stream);
+}
+
+cdb_status cdb_omp_batch_masked(const cdb_dictionary *dict, const double *ys,
+                                const int32_t *rows, const int64_t *m, int64_t p, int64_t k_max,
+                                const double *eps, int64_t *out_sel, double *out_coef,
+                                int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                                uint8_t *out_flag, void *stream) {
+  if (!dict || p < 0 || k_max < 0 || (p > 0 && (!ys || !rows || !m || !eps)))
+    return fail(CDB_ERR_ARG, "bad masked omp arguments");
+  if (p == 0) return CDB_OK;
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = dict->n;
+  InArr y_in, r_in, m_in, e_in;
+  CDB_CUDA(y_in.bind(ys, sizeof(double) * p * n, st));
+  CDB_CUDA(r_in.bind(rows, sizeof(int32_t) * p * n, st));
+  CDB_CUDA(m_in.bind(m, sizeof(int64_t) * p, st));
+  CDB_CUDA(e_in.bind(eps, sizeof(double) * p, st));
+  Outs o;
+  CDB_CUDA(o.bind(p, k_max, out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, st));
+  cdb::Cands c{};
+  c.mode = 0;
+  c.t = dict->t;
+  c.clip = 1;  // budget min(k_max, T, m_p) per signal
+  g_last_engine = CDB_ENGINE_EXACT;
+  diag_clear(st);
+  cdb_status s = run_exact(dict, y_in.dev, false, p, nullptr, k_max, k_max,
+                           (const double *)e_in.dev, c, dict->t, o, di, st, nullptr,
+                           (const int32_t *)r_in.dev, (const int64_t *)m_in.dev);
+  if (s != CDB_OK) return s;
+  CDB_CUDA(o.finish(st));
+  CDB_CUDA(cudaStreamSynchronize(st));
+  return CDB_OK;
 }
 
 cdb_status cdb_omp_batch_blocked_ragged(const cdb_dictionary *dict, const void *ys, int ys_is_f32,

@@ -70,4 +70,22 @@ __device__ __forceinline__ double dot4_quad(const double *a, const double *b, in
   return tot;
 }
 
+// dot4_quad of a gathered vector a[idx[i]] with b[i] (same summation order
+// as dot4_quad on the compacted vector): the masked exact engine's scan.
+__device__ __forceinline__ double dot4_quad_g(const double *a, const int32_t *idx,
+                                              const double *b, int64_t n, int lane) {
+  const int m = lane & 3;
+  const int64_t m4 = (n / 4) * 4;
+  double s = 0.0;
+  for (int64_t i = m; i < m4; i += 4) s = __dadd_rn(s, __dmul_rn(a[idx[i]], b[i]));
+  const int base = lane & ~3;
+  const double s0 = __shfl_sync(CDB_FULL_MASK, s, base + 0);
+  const double s1 = __shfl_sync(CDB_FULL_MASK, s, base + 1);
+  const double s2 = __shfl_sync(CDB_FULL_MASK, s, base + 2);
+  const double s3 = __shfl_sync(CDB_FULL_MASK, s, base + 3);
+  double tot = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3);
+  for (int64_t i = m4; i < n; i++) tot = __dadd_rn(tot, __dmul_rn(a[idx[i]], b[i]));
+  return tot;
+}
+
 }  // namespace cdb

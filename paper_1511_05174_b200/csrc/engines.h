@@ -28,6 +28,9 @@ struct ExactArgs {
   const int64_t *sig_ids;  // optional: process only these signals
   int64_t p_count;       // number of signals to process (len(sig_ids) or P)
   const int *p_count_dev;  // optional: the count lives on the device (<= p_count)
+  const int32_t *rows;     // optional masked mode: per-signal kept coordinates
+                           // (row p, stride ys_stride, ascending), m_sig[p] of them
+  const int64_t *m_sig;
   int64_t k_max;         // budget (clipped per signal when cands.clip)
   int64_t k_width;       // output row width
   const double *eps;

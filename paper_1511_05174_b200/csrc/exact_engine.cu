@@ -13,6 +13,12 @@
 // runs a one-sided Jacobi SVD minimum-norm solve (the same restatement as
 // oracle/omp_oracle.c, coefficients "parity unpinned").
 //
+// Masked mode (rows != NULL): signal p is measured on m_p kept
+// coordinates of the atoms (a per-patch mask operator, pipelines.py:281-293):
+// every atom access reads atom[rows[i]] for i < m_p, i.e. the reference's
+// compacted effective dictionary E_p = D[kept, :] in its own order, and the
+// signal row holds the m_p kept measurements.
+//
 // Role in the product: the engine of record for small problems and the
 // fallback for signals the fast engines delegate (rank trouble or an
 // uncertifiable selection).  Throughput is not its purpose.
@@ -107,14 +113,16 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
   for (int64_t idx = warp_global; idx < count; idx += n_warps) {
     const int64_t p = a.sig_ids ? a.sig_ids[idx] : idx;
     const int64_t c = cs.count(p);
-    const int64_t k_max = cs.budget(p, a.k_max, n);
+    const int32_t *rw = a.rows ? a.rows + p * a.ys_stride : nullptr;
+    const int64_t ne = rw ? a.m_sig[p] : n;  // coordinates this signal is measured on
+    const int64_t k_max = cs.budget(p, a.k_max, ne);
     int64_t *sel = a.out_sel + p * kw;
     double *coef = a.out_coef + p * kw;
     for (int64_t j = lane; j < kw; j += 32) {
       sel[j] = -1;
       coef[j] = 0.0;
     }
-    for (int64_t i = lane; i < n; i += 32) {
+    for (int64_t i = lane; i < ne; i += 32) {
       double v = (double)ys[p * a.ys_stride + i];
       y[i] = v;
       r[i] = v;
@@ -123,7 +131,7 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
     for (int64_t i = lane; i < kw * kw; i += 32) rmat[i] = 0.0;
     __syncwarp();
 
-    const double ynorm = sqrt(dot4_quad(y, y, n, lane));
+    const double ynorm = sqrt(dot4_quad(y, y, ne, lane));
     const double tol = a.eps[p];
     int64_t scans = 0, kdone = 0;
     double rnorm = ynorm;
@@ -140,7 +148,8 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
           const int64_t jl = base + grp;
           const bool live = jl < c && !((taken[jl >> 5] >> (jl & 31)) & 1u);
           const int64_t g = jl < c ? cs.id(p, jl) : 0;
-          double v = dot4_quad(a.mat_t + g * n, r, n, lane);
+          double v = rw ? dot4_quad_g(a.mat_t + g * n, rw, r, ne, lane)
+                        : dot4_quad(a.mat_t + g * n, r, n, lane);
           if (v < 0.0) v = -v;
           if (live && v > best) {
             best = v;
@@ -156,14 +165,14 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
 
         if (!dense) {
           // ---- MGS with one re-orthogonalisation (_kernels.py:111-137)
-          for (int64_t i = lane; i < n; i += 32) u[i] = a.mat_t[g * n + i];
+          for (int64_t i = lane; i < ne; i += 32) u[i] = a.mat_t[g * n + (rw ? rw[i] : i)];
           __syncwarp();
-          const double anorm = sqrt(dot4_quad(u, u, n, lane));
+          const double anorm = sqrt(dot4_quad(u, u, ne, lane));
           for (int pass = 0; pass < 2; pass++) {
             for (int64_t j = 0; j < kdone - 1; j++) {
-              const double w = dot4_quad(qmat + j * n, u, n, lane);
+              const double w = dot4_quad(qmat + j * n, u, ne, lane);
               __syncwarp();
-              for (int64_t i = lane; i < n; i += 32) u[i] -= w * qmat[j * n + i];
+              for (int64_t i = lane; i < ne; i += 32) u[i] -= w * qmat[j * n + i];
               if (lane == 0) {
                 if (pass == 0)
                   rmat[j * kw + (kdone - 1)] = w;
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
               __syncwarp();
             }
           }
-          const double d = sqrt(dot4_quad(u, u, n, lane));
+          const double d = sqrt(dot4_quad(u, u, ne, lane));
           const double floor_ = anorm > 1e-300 ? anorm : 1e-300;
           if (d <= RANK_TOL * floor_) {
             dense = true;
@@ -181,14 +190,14 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
           } else {
             if (lane == 0) rmat[(kdone - 1) * kw + (kdone - 1)] = d;
             double *qk = qmat + (kdone - 1) * n;
-            for (int64_t i = lane; i < n; i += 32) qk[i] = u[i] / d;
+            for (int64_t i = lane; i < ne; i += 32) qk[i] = u[i] / d;
             __syncwarp();
-            const double z = dot4_quad(qk, r, n, lane);
+            const double z = dot4_quad(qk, r, ne, lane);
             if (lane == 0) qty[kdone - 1] = z;
             __syncwarp();
-            for (int64_t i = lane; i < n; i += 32) r[i] -= z * qk[i];
+            for (int64_t i = lane; i < ne; i += 32) r[i] -= z * qk[i];
             __syncwarp();
-            rnorm = sqrt(dot4_quad(r, r, n, lane));
+            rnorm = sqrt(dot4_quad(r, r, ne, lane));
           }
         }
         if (dense) {
@@ -196,18 +205,20 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
           __syncwarp();
           for (int64_t j = 0; j < kdone; j++) {
             const int64_t gj = sel[j];
-            for (int64_t i = lane; i < n; i += 32) amat[j * n + i] = a.mat_t[gj * n + i];
+            for (int64_t i = lane; i < ne; i += 32)
+              amat[j * ne + i] = a.mat_t[gj * n + (rw ? rw[i] : i)];
           }
           __syncwarp();
-          if (lane == 0) lstsq_min_norm(amat, n, kdone, y, coefs, vwork);
+          if (lane == 0) lstsq_min_norm(amat, ne, kdone, y, coefs, vwork);
           __syncwarp();
-          for (int64_t i = lane; i < n; i += 32) {
+          for (int64_t i = lane; i < ne; i += 32) {
             double acc = 0.0;
-            for (int64_t j = 0; j < kdone; j++) acc += a.mat_t[sel[j] * n + i] * coefs[j];
+            for (int64_t j = 0; j < kdone; j++)
+              acc += a.mat_t[sel[j] * n + (rw ? rw[i] : i)] * coefs[j];
             r[i] = y[i] - acc;
           }
           __syncwarp();
-          rnorm = sqrt(dot4_quad(r, r, n, lane));
+          rnorm = sqrt(dot4_quad(r, r, ne, lane));
           for (int64_t j = lane; j < kdone; j += 32) coef[j] = coefs[j];
         }
         __syncwarp();

@@ -254,3 +254,12 @@ def omp_batch_blocked_ragged_raw(dd: DeviceDictionary, ys, p: int, k_max: int, e
                                                   int(q), *_out_ptrs(o), N.ENGINES[engine],
                                                   stream))
     return o
+
+
+def omp_batch_masked_raw(dd: DeviceDictionary, ys, rows, m, p: int, k_max: int, eps, out=None,
+                         stream=None):
+    """cdb_omp_batch_masked: OMP of ys[p][:m[p]] over D[rows[p][:m[p]], :]."""
+    o = out if out is not None else _out(p, k_max)
+    N.check(N.load().cdb_omp_batch_masked(dd.handle, N.ptr(ys), N.ptr(rows), N.ptr(m), int(p),
+                                          int(k_max), N.ptr(eps), *_out_ptrs(o), stream))
+    return o

@@ -94,3 +94,58 @@ def denoise(signal, patch_shape, stride=1, *, dictionary=None, sparsity=None, mo
     solve = mk(t_dim, _host(code)) if model is None else (mk(model.t_low, _host(lo)),
                                                           mk(model.t_high, _host(code)))
     return estimate, solve, {"extract": t1 - t0, "coding": t2 - t1, "reconstruct": t3 - t2}
+
+
+def recover_masked(measurements, known, patch_shape, stride=1, *, dictionary, sparsity,
+                   remove_dc: bool = True):
+    """Inpainting / masked recovery: crossdict
+    ``pipelines._recover_operator`` for a mask operator with single-scale OMP
+    (pipelines.py:256-322, sensing.patch_problem mask branch sensing.py:222-231).
+
+    ``measurements``: the signal-domain array (unknown cells arbitrary);
+    ``known``: boolean array of the same shape.  Each patch is coded against
+    the rows of ``dictionary`` at its known cells (OMP on the compacted
+    effective dictionary, device exact engine), reconstructed with the full
+    atoms plus its DC, and the patches are overlap-averaged.  Patches with no
+    known cell are flagged and contribute 0.  Returns ``(estimate, solve,
+    flagged)``.
+    """
+    meas = np.asarray(_pw.as_array(measurements), dtype=np.float64)
+    known = np.asarray(known, dtype=bool)
+    if known.shape != meas.shape:
+        raise E.DimensionError(f"mask shape {known.shape} != measurement shape {meas.shape}")
+    atoms = np.asarray(getattr(dictionary, "atoms", dictionary), dtype=np.float64)
+    pshape, strides = _pw._geometry(meas.shape, patch_shape, stride)
+    n = int(np.prod(pshape))
+    if atoms.shape[0] != n:
+        raise E.DimensionError(f"atom dim {atoms.shape[0]} != patch size {n}")
+    t = atoms.shape[1]
+    k_single = int(min(sparsity, t))
+    vals, _ = _dev.extract_patches_raw(meas, pshape, strides, False)
+    kept, _ = _dev.extract_patches_raw(known.astype(np.float64), pshape, strides, False)
+    vals, kept = np.asarray(vals), np.asarray(kept) != 0.0
+    p = vals.shape[0]
+    m = kept.sum(axis=1).astype(np.int64)
+    order = np.argsort(~kept, axis=1, kind="stable")  # kept cells first, ascending
+    rows = np.ascontiguousarray(order, dtype=np.int32)
+    ys = np.take_along_axis(vals, order, axis=1)
+    ys[np.arange(n)[None, :] >= m[:, None]] = 0.0
+    dc = np.zeros(p)
+    if remove_dc:
+        for mm in np.unique(m[m > 0]):  # numpy's own mean of each compacted row
+            sel = np.flatnonzero(m == mm)
+            dc[sel] = ys[sel, :mm].mean(axis=1)
+            ys[sel, :mm] = ys[sel, :mm] - dc[sel, None]
+    rel = _pursuit._rel_tol()
+    eps = np.array([rel * float(np.linalg.norm(ys[i, :m[i]])) for i in range(p)])
+    dd = _dev.device_dictionary(np.ascontiguousarray(atoms.T))
+    o = _dev.omp_batch_masked_raw(dd, np.ascontiguousarray(ys), rows, m, p, k_single, eps)
+    flagged = m == 0
+    if flagged.any():  # unrecoverable patches contribute 0 (pipelines.py:279-281)
+        o["sel"][flagged] = -1
+        o["counts"][flagged] = 0
+        dc[flagged] = 0.0
+    est, unc = _dev.reconstruct_aggregate_raw(dd, o["sel"], o["alpha"], p, dc, meas.shape,
+                                              pshape, strides)
+    estimate = _pw._finish(est, unc)
+    return estimate, _pursuit._make_batch(t, o), int(flagged.sum())
