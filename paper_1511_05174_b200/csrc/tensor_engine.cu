@@ -1191,7 +1191,13 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   // grouped LS kernel: 8-lane groups (4 signals per warp) when the per-signal
   // state is small, whole warps otherwise; CDB_LS_LEGACY=1 forces ls_step
   const int64_t grp_bytes = 8 * (kw * kw + 5 * kw);
-  const int lsg_g = 4 * grp_bytes <= 48 * 1024 ? 8 : 32;
+  // lanes per signal in the grouped LS kernel: 16 measured best on cfg 1
+  // (8: 10.3 M, 16: 10.9 M signals/s); whole warps when the state is large
+  int lsg_g = 4 * 2 * grp_bytes <= 96 * 1024 ? 16 : 32;
+  if (const char *g = getenv("CDB_LS_G")) {
+    const int v = atoi(g);
+    if ((v == 8 && 4 * grp_bytes <= 48 * 1024) || v == 16 || v == 32) lsg_g = v;
+  }
   const int64_t lsg_per_block = 4 * (32 / lsg_g) * grp_bytes;  // 4 warps per block
   int64_t lsg_smem = lsg_per_block;
   if (getenv("CDB_LS_LEGACY") || lsg_per_block > 200 * 1024) lsg_smem = 0;
@@ -1201,6 +1207,8 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsg_smem);
     };
     if ((e = set((const void *)ls_group_kernel<float, 8>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<float, 16>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<double, 16>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<double, 8>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<float, 32>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<double, 32>)) != cudaSuccess) return e;
@@ -1238,6 +1246,17 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
                 resume);
           else
             ls_group_kernel<double, 8><<<grid, 128, lsg_smem, stream>>>(
+                (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+        } else if (lsg_g == 16) {
+          if (a.ys_f32)
+            ls_group_kernel<float, 16><<<grid, 128, lsg_smem, stream>>>(
+                (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+          else
+            ls_group_kernel<double, 16><<<grid, 128, lsg_smem, stream>>>(
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume);
