@@ -319,6 +319,10 @@ struct TensorState {
   int64_t *pending;     // queued signal ids
   int64_t *rs_j;        // rescan result: atom
   double *rs_c;         // rescan result: exact correlation
+  double *rs_pv;        // per pending slot x RS_SPLIT: partial best |c|, atom, c
+  int64_t *rs_pj;
+  double *rs_pc;
+  int *rs_cnt;          // per pending slot: parts done (reset by the last part)
   int64_t debug_sig;    // CDB_LS_DEBUG: printf trace of one signal
 };
 
@@ -948,10 +952,15 @@ __global__ void __launch_bounds__(128) ls_group_kernel(
   }
 }
 
-// Exact fp64 argmax over every non-taken atom for the queued signals: one
-// CTA per signal; the exact residual r = y - D64_S x, the coefficients and a
-// taken-atom bit mask sit in shared memory; each warp streams 8 atom rows at
-// a time with coalesced loads (c_j = <d_j, r>).
+// Exact fp64 argmax over every non-taken atom for the queued signals.  Each
+// signal is split over RS_SPLIT CTAs (latency: a handful of signals per
+// iteration, each a T x N fp64 scan): every part materialises the exact
+// residual r = y - D64_S x and a taken-atom mask in shared memory, scans its
+// 1/RS_SPLIT of the atoms (warps stream 8 rows at a time, coalesced, c_j =
+// <d_j, r>), and publishes (|c|, j, c); the last part to finish reduces the
+// partials (max |c|, lowest index on ties) into rs_j / rs_c.
+constexpr int RS_SPLIT = 16;
+
 template <typename YT>
 __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
                                                      const double *__restrict__ d64,
@@ -963,13 +972,17 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
   __shared__ double sv[8];
   __shared__ int64_t sj[8];
   __shared__ double sc[8];
+  __shared__ int last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t count = st.npending[iter];
   double *y = rsm;                                   // n
   double *x = y + n;                                 // kw
   int64_t *sel = (int64_t *)(x + kw);                // kw
   uint32_t *taken = (uint32_t *)(sel + kw);          // (t + 31) / 32
-  for (int64_t e = blockIdx.x; e < count; e += gridDim.x) {
+  const int64_t per = (t + RS_SPLIT - 1) / RS_SPLIT;
+  for (int64_t w = blockIdx.x; w < count * RS_SPLIT; w += gridDim.x) {
+    const int64_t e = w / RS_SPLIT;
+    const int part = (int)(w % RS_SPLIT);
     const int64_t sig = st.pending[e];
     const int64_t k = iter;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = (double)ys[sig * n + i];
@@ -984,19 +997,20 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
       atomicOr(&taken[j >> 5], 1u << (j & 31));
     }
     __syncthreads();
-    // r = y - D64_S x, exact fp64, once per signal (then plain dots)
+    // r = y - D64_S x, exact fp64 (then plain dots)
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
       double ri = y[i];
       for (int64_t l = 0; l < k; l++) ri = fma(-x[l], __ldg(d64 + sel[l] * n + i), ri);
       y[i] = ri;  // y now holds r
     }
     __syncthreads();
+    const int64_t jlo = part * per, jhi = jlo + per < t ? jlo + per : t;
     double best = -1.0, cbest = 0.0;
     int64_t bestj = -1;
-    for (int64_t j0 = (int64_t)warp * 8; j0 < t; j0 += 64) {
+    for (int64_t j0 = jlo + (int64_t)warp * 8; j0 < jhi; j0 += 64) {
       const double *rows[8];
 #pragma unroll
-      for (int r = 0; r < 8; r++) rows[r] = d64 + (j0 + r < t ? j0 + r : 0) * n;
+      for (int r = 0; r < 8; r++) rows[r] = d64 + (j0 + r < jhi ? j0 + r : jlo) * n;
       double acc[8];
 #pragma unroll
       for (int r = 0; r < 8; r++) acc[r] = 0.0;
@@ -1009,7 +1023,7 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
       for (int r = 0; r < 8; r++) {
         const int64_t j = j0 + r;
         const double cj = warp_sum(acc[r]);
-        if (j < t && !((taken[j >> 5] >> (j & 31)) & 1u)) {
+        if (j < jhi && !((taken[j >> 5] >> (j & 31)) & 1u)) {
           const double v = fabs(cj);
           if (v > best || (v == best && j < bestj)) {
             best = v;
@@ -1026,14 +1040,35 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int w = 1; w < 8; w++)
-        if (sj[w] >= 0 && (bestj < 0 || sv[w] > best || (sv[w] == best && sj[w] < bestj))) {
-          best = sv[w];
-          bestj = sj[w];
-          cbest = sc[w];
+      for (int q = 1; q < 8; q++)
+        if (sj[q] >= 0 && (bestj < 0 || sv[q] > best || (sv[q] == best && sj[q] < bestj))) {
+          best = sv[q];
+          bestj = sj[q];
+          cbest = sc[q];
         }
-      st.rs_j[sig] = bestj;
-      st.rs_c[sig] = cbest;
+      st.rs_pv[e * RS_SPLIT + part] = best;
+      st.rs_pj[e * RS_SPLIT + part] = bestj;
+      st.rs_pc[e * RS_SPLIT + part] = cbest;
+      __threadfence();
+      last = atomicAdd(&st.rs_cnt[e], 1) == RS_SPLIT - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {  // every part published: reduce them
+      __threadfence();
+      double b = -1.0, c = 0.0;
+      int64_t bj = -1;
+      for (int q = 0; q < RS_SPLIT; q++) {
+        const double v = __ldcg(st.rs_pv + e * RS_SPLIT + q);
+        const int64_t j = __ldcg(st.rs_pj + e * RS_SPLIT + q);
+        if (j >= 0 && (bj < 0 || v > b || (v == b && j < bj))) {
+          b = v;
+          bj = j;
+          c = __ldcg(st.rs_pc + e * RS_SPLIT + q);
+        }
+      }
+      st.rs_j[sig] = bj;
+      st.rs_c[sig] = c;
+      st.rs_cnt[e] = 0;
     }
     __syncthreads();
   }
@@ -1097,7 +1132,7 @@ int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw) {
   const int64_t n_pad = (n + BK - 1) / BK * BK;
   const int64_t p_pad = (p + BM - 1) / BM * BM;
   return p_pad * n_pad * 2 + p * kw * kw * 8 + p * kw * 8 + p * 8 * 5 + p * NCAND * 8 + p * 4 +
-         p * 8 * 3 + 4 * 4096 + 16 * 256;
+         p * 8 * 3 + p * (3 * 8 * RS_SPLIT + 4) + 4 * 4096 + 21 * 256;
 }
 
 cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
@@ -1132,12 +1167,17 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   st.pending = (int64_t *)take(p * 8);
   st.rs_j = (int64_t *)take(p * 8);
   st.rs_c = (double *)take(p * 8);
+  st.rs_pv = (double *)take(p * RS_SPLIT * 8);
+  st.rs_pj = (int64_t *)take(p * RS_SPLIT * 8);
+  st.rs_pc = (double *)take(p * RS_SPLIT * 8);
+  st.rs_cnt = (int *)take(p * 4);
   st.rescans = a.rescans;
   st.debug_sig = getenv("CDB_LS_DEBUG") ? atoll(getenv("CDB_LS_DEBUG")) : -1;
   cudaError_t e;
   if ((e = cudaMemsetAsync(st.r16, 0, p_pad * n_pad * 2, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(st.active, 0, (a.k_max + 1) * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(st.npending, 0, (a.k_max + 1) * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(st.rs_cnt, 0, p * 4, stream)) != cudaSuccess) return e;
 
   CUtensorMap tm_a, tm_b;
   if (!make_map(&tm_a, st.r16, p_pad, n_pad, BMH) || !make_map(&tm_b, a.d16, t, n_pad, BN))
