@@ -1074,7 +1074,8 @@ __global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
   }
 }
 
-// Final exact residual norms |y - D64_S x| (the reported rnorm).
+// Final residual norms (the reported rnorm): sqrt(|y|^2 - |z|^2) when that is
+// tight, else the exact |y - D64_S x|.
 template <typename YT>
 __global__ void __launch_bounds__(256) ls_final_kernel(const YT *__restrict__ ys,
                                                        const double *__restrict__ d64, int64_t p,
@@ -1088,6 +1089,13 @@ __global__ void __launch_bounds__(256) ls_final_kernel(const YT *__restrict__ ys
   if (sig >= p || (st.status[sig] & ST_DELEGATE)) return;
   const int64_t kd = out_count[sig];
   if (kd == 0) return;
+  // |r|^2 = |y|^2 - |z|^2 is accurate to ~1e-16 |y|^2 / |r|^2 relative:
+  // re-materialise the residual only when that is not tight (as gram_engine)
+  const double rn2 = st.rn2[sig];
+  if (rn2 > 1e-6 * st.yy[sig]) {
+    if (lane == 0) out_rnorm[sig] = sqrt(rn2);
+    return;
+  }
   const int64_t *sel = out_sel + sig * kw;
   const double *x = out_coef + sig * kw;
   double rr = 0.0;
