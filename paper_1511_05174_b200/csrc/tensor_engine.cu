@@ -214,10 +214,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t acc = 0, acc_ph = 0;
     // chunk-local column ids in registers (opaque to constant folding) so a
     // key is one LOP3 (mask | id) instead of two
-    uint32_t cid[32];
+    uint32_t cid[2][32];
     const uint32_t opaque0 = (uint32_t)threadIdx.x >> 16;  // 0 at runtime
 #pragma unroll
-    for (int i = 0; i < 32; i++) cid[i] = opaque0 + (uint32_t)i;
+    for (int i = 0; i < 64; i++) cid[i >> 5][i & 31] = opaque0 + (uint32_t)i;
     for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
       float val[NCAND];
       int idx[NCAND];
@@ -232,38 +232,43 @@ __global__ void __launch_bounds__(THREADS, 1)
         sm100::tc_fence_after();
         const uint32_t tbase = tmem + (acc * 2 + half) * BN + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          float v[32];
-          sm100::tmem_ld32(tbase + c, v);
-          // branchless chunk top-2 on packed keys: |v| with its low 5 mantissa
-          // bits replaced by the chunk-local column (truncation <= 2^-18 rel.)
+        for (int c = 0; c < BN; c += 64) {
+          float v[2][32];
+          sm100::tmem_ld32(tbase + c, v[0]);
+          sm100::tmem_ld32(tbase + c + 32, v[1]);
+          // branchless top-2 of 64 columns on packed keys: |v| with its low 6
+          // mantissa bits replaced by the column within the 64 (truncation
+          // <= 2^-17 rel., inside c_err); everything else raises `dropped`
           uint32_t c1 = 0u, c2 = 0u, rest = 0u;
           const int jbase = tt * BN + c;
-          if (jbase + 32 <= t) {
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-              const uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFFE0u) | cid[i];
-              const uint32_t m = min(c1, key);
-              c1 = max(c1, key);
-              rest = max(rest, min(c2, m));
-              c2 = max(c2, m);
-            }
-          } else {
+          for (int hh = 0; hh < 2; hh++) {
+            if (jbase + 32 * hh + 32 <= t) {
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-              uint32_t key = (__float_as_uint(v[i]) & 0x7FFFFFE0u) | cid[i];
-              key = (jbase + i < t) ? key : 0u;
-              const uint32_t m = min(c1, key);
-              c1 = max(c1, key);
-              rest = max(rest, min(c2, m));
-              c2 = max(c2, m);
+              for (int i = 0; i < 32; i++) {
+                const uint32_t key = (__float_as_uint(v[hh][i]) & 0x7FFFFFC0u) | cid[hh][i];
+                const uint32_t m = min(c1, key);
+                c1 = max(c1, key);
+                rest = max(rest, min(c2, m));
+                c2 = max(c2, m);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i++) {
+                uint32_t key = (__float_as_uint(v[hh][i]) & 0x7FFFFFC0u) | cid[hh][i];
+                key = (jbase + 32 * hh + i < t) ? key : 0u;
+                const uint32_t m = min(c1, key);
+                c1 = max(c1, key);
+                rest = max(rest, min(c2, m));
+                c2 = max(c2, m);
+              }
             }
           }
-          dropped = fmaxf(dropped, __uint_as_float(rest & 0xFFFFFFE0u));
-          if (c1) list_insert(val, idx, dropped, __uint_as_float(c1 & 0xFFFFFFE0u),
-                              jbase + (int)(c1 & 0x1Fu));
-          if (c2) list_insert(val, idx, dropped, __uint_as_float(c2 & 0xFFFFFFE0u),
-                              jbase + (int)(c2 & 0x1Fu));
+          dropped = fmaxf(dropped, __uint_as_float(rest & 0xFFFFFFC0u));
+          if (c1) list_insert(val, idx, dropped, __uint_as_float(c1 & 0xFFFFFFC0u),
+                              jbase + (int)(c1 & 0x3Fu));
+          if (c2) list_insert(val, idx, dropped, __uint_as_float(c2 & 0xFFFFFFC0u),
+                              jbase + (int)(c2 & 0x3Fu));
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.tempty[acc]);
