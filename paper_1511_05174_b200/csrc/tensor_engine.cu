@@ -689,8 +689,10 @@ __device__ __forceinline__ double gmax(double v) {
   return v;
 }
 
-template <typename YT, int G>
-__global__ void __launch_bounds__(128) ls_group_kernel(
+// YM > 0: N <= YM * G and every lane keeps its YM elements of y
+// (i = gl + G m) in registers for both the re-score and the residual.
+template <typename YT, int G, int YM = 0>
+__global__ void __launch_bounds__(128, 6) ls_group_kernel(
     const YT *__restrict__ ys, const double *__restrict__ d64, const float *__restrict__ d32,
     const double *__restrict__ gram, int64_t p, int64_t t, int n, int64_t n_pad, int k_max,
     int kw, int iter, double c_err, double dmax, TensorState st, int64_t *out_sel,
@@ -742,6 +744,14 @@ __global__ void __launch_bounds__(128) ls_group_kernel(
       }
       for (int i = gl; i < k * kw; i += G) lin[i] = st.linv[sig * kw * kw + i];
     }
+    YT yv[YM > 0 ? YM : 1];
+    if constexpr (YM > 0) {
+#pragma unroll
+      for (int m = 0; m < YM; m++) {
+        const int i = gl + G * m;
+        yv[m] = act && i < n ? y[i] : (YT)0;
+      }
+    }
     __syncwarp();
     double best = -1.0, cbest = 0.0;
     int64_t bestj = -1;
@@ -778,6 +788,21 @@ __global__ void __launch_bounds__(128) ls_group_kernel(
           const double *dj = d64 + j * n;
           double a1 = 0.0, a2 = 0.0, a3 = 0.0;
           int i = gl;
+          if constexpr (YM > 0) {
+#pragma unroll
+            for (int m = 0; m < YM; m += 4) {  // y from registers, 4 atom loads in flight
+              const int i0 = gl + G * m;
+              const double d0 = i0 < n ? __ldg(dj + i0) : 0.0;
+              const double d1 = i0 + G < n ? __ldg(dj + i0 + G) : 0.0;
+              const double d2 = i0 + 2 * G < n ? __ldg(dj + i0 + 2 * G) : 0.0;
+              const double d3 = i0 + 3 * G < n ? __ldg(dj + i0 + 3 * G) : 0.0;
+              acc = fma(d0, (double)yv[m], acc);
+              a1 = fma(d1, (double)yv[m + 1], a1);
+              a2 = fma(d2, (double)yv[m + 2], a2);
+              a3 = fma(d3, (double)yv[m + 3], a3);
+            }
+            i = n;
+          }
           for (; i + 3 * G < n; i += 4 * G) {  // 8 loads in flight
             const double d0 = __ldg(dj + i), d1 = __ldg(dj + i + G), d2 = __ldg(dj + i + 2 * G),
                          d3 = __ldg(dj + i + 3 * G);
@@ -900,12 +925,17 @@ __global__ void __launch_bounds__(128) ls_group_kernel(
     // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16
     double rr = 0.0, sx = 0.0;
     if (act) {
-      for (int i0 = 0; i0 < n; i0 += 8 * G) {
+#pragma unroll
+      for (int i0 = 0; i0 < (YM > 0 ? YM * G : n); i0 += 8 * G) {
+        if (YM > 0 && i0 >= n) break;
         double acc[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) {
           const int i = i0 + u * G + gl;
-          acc[u] = i < n ? (double)y[i] : 0.0;
+          if constexpr (YM > 0)
+            acc[u] = i < n ? (double)yv[i0 / G + u] : 0.0;
+          else
+            acc[u] = i < n ? (double)y[i] : 0.0;
         }
         int l = 0;
         for (; l + 3 < kd; l += 4) {  // 32 loads in flight before the FMAs
@@ -1261,6 +1291,8 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     };
     if ((e = set((const void *)ls_group_kernel<float, 8>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<float, 16>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<float, 16, 16>)) != cudaSuccess) return e;
+    if ((e = set((const void *)ls_group_kernel<double, 16, 16>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<double, 16>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<double, 8>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<float, 32>)) != cudaSuccess) return e;
@@ -1299,6 +1331,17 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
                 resume);
           else
             ls_group_kernel<double, 8><<<grid, 128, lsg_smem, stream>>>(
+                (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+        } else if (lsg_g == 16 && n <= 256) {
+          if (a.ys_f32)
+            ls_group_kernel<float, 16, 16><<<grid, 128, lsg_smem, stream>>>(
+                (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
+                (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
+                resume);
+          else
+            ls_group_kernel<double, 16, 16><<<grid, 128, lsg_smem, stream>>>(
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume);
