@@ -1180,13 +1180,18 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
     for (int d = 0; d < rank; d++) n_low *= fine_shape[d] / factors[d];
     if (n_low != low->n) return fail(CDB_ERR_ARG, "coarse size != low dictionary dim");
     CDB_CUDA(ylow.alloc(sizeof(double) * p * n_low, st));
+    CDB_CUDA(eps1.alloc(sizeof(double) * p, st));
+    CDB_CUDA(eps2.alloc(sizeof(double) * p, st));
+    // downsample + both stopping tolerances in one pass over y
     CDB_CUDA(cdb::launch_downsample(ydev, f32, p, n, fine_shape, factors, rank,
-                                    ylow.as<double>(), n_low, st));
+                                    ylow.as<double>(), n_low, st, rel_tol, eps1.as<double>(),
+                                    eps2.as<double>()));
     y1 = ylow.ptr;
     y1_f32 = false;
+  } else {
+    CDB_CUDA(eps1.alloc(sizeof(double) * p, st));
+    CDB_CUDA(cdb::launch_row_tol(y1, y1_f32, p, low->n, rel_tol, eps1.as<double>(), st));
   }
-  CDB_CUDA(eps1.alloc(sizeof(double) * p, st));
-  CDB_CUDA(cdb::launch_row_tol(y1, y1_f32, p, low->n, rel_tol, eps1.as<double>(), st));
   cdb::Cands c1{};
   c1.mode = 0;
   c1.t = low->t;
@@ -1199,8 +1204,10 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
   CDB_CUDA(blocks.alloc(sizeof(int64_t) * p * k1, st));
   CDB_CUDA(cdb::launch_sort_blocks((const int64_t *)lo.sel.dev, (const int64_t *)lo.count.dev, p,
                                    k1, blocks.as<int64_t>(), st));
-  CDB_CUDA(eps2.alloc(sizeof(double) * p, st));
-  CDB_CUDA(cdb::launch_row_tol(ydev, f32, p, n, rel_tol, eps2.as<double>(), st));
+  if (phi_mode) {  // Phi: step-1 input is y itself, eps2 == eps1 in value
+    CDB_CUDA(eps2.alloc(sizeof(double) * p, st));
+    CDB_CUDA(cdb::launch_row_tol(ydev, f32, p, n, rel_tol, eps2.as<double>(), st));
+  }
   cdb::Cands c2{};
   c2.mode = 2;
   c2.t = high->t;

@@ -137,7 +137,9 @@ cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double 
                                 cudaStream_t stream);
 cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
                               const int64_t *fine_shape, const int64_t *factors, int rank,
-                              double *y_low, int64_t n_low, cudaStream_t stream);
+                              double *y_low, int64_t n_low, cudaStream_t stream,
+                              double rel = 0.0, double *eps_low = nullptr,
+                              double *eps_fine = nullptr);
 cudaError_t launch_row_tol(const void *ys, bool ys_f32, int64_t p, int64_t n, double rel,
                            double *eps, cudaStream_t stream);
 cudaError_t launch_sort_blocks(const int64_t *low_sel, const int64_t *low_count, int64_t p,

@@ -21,7 +21,9 @@ template <typename YT>
 __global__ void __launch_bounds__(256) downsample_kernel(const YT *__restrict__ ys, int64_t p,
                                                          int n, Shape4 sh,
                                                          double *__restrict__ out, int n_low,
-                                                         int spb) {
+                                                         int spb, double rel,
+                                                         double *__restrict__ eps_low,
+                                                         double *__restrict__ eps_fine) {
   extern __shared__ __align__(16) unsigned char dsm[];
   int *tab = (int *)dsm;                       // n_low * block fine indices
   YT *rows = (YT *)(dsm + ((size_t)n * 4 + 15) / 16 * 16);  // spb x n
@@ -52,6 +54,23 @@ __global__ void __launch_bounds__(256) downsample_kernel(const YT *__restrict__ 
     double acc = 0.0;
     for (int b = 0; b < block; b++) acc += (double)row[t[b]];
     out[(s0 + sl) * n_low + cell] = acc / (double)block;
+  }
+  if (!eps_low) return;
+  // fused stopping tolerances rel * |W y| (step 1) and rel * |y| (step 2)
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int sl = warp; sl < ns; sl += blockDim.x >> 5) {
+    const YT *row = rows + (size_t)sl * n;
+    double a = 0.0, b = 0.0;
+    for (int i = lane; i < n; i += 32) a = fma((double)row[i], (double)row[i], a);
+    const double *lo = out + (s0 + sl) * n_low;
+    for (int i = lane; i < n_low; i += 32) b = fma(lo[i], lo[i], b);
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      eps_fine[s0 + sl] = rel * sqrt(a);
+      eps_low[s0 + sl] = rel * sqrt(b);
+    }
   }
 }
 
@@ -515,7 +534,8 @@ inline unsigned blocks_for(int64_t work, int threads) {
 
 cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
                               const int64_t *fine_shape, const int64_t *factors, int rank,
-                              double *y_low, int64_t n_low, cudaStream_t stream) {
+                              double *y_low, int64_t n_low, cudaStream_t stream, double rel,
+                              double *eps_low, double *eps_fine) {
   ProfScope _ps("downsample", stream);
   if (p <= 0) return cudaSuccess;
   if (rank < 1 || rank > 4) return cudaErrorInvalidValue;
@@ -538,13 +558,13 @@ cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
                              (int)smem);
     if (e != cudaSuccess) return e;
     downsample_kernel<float><<<g, 256, smem, stream>>>((const float *)ys, p, (int)n, sh, y_low,
-                                                       (int)n_low, spb);
+                                                       (int)n_low, spb, rel, eps_low, eps_fine);
   } else {
     e = cudaFuncSetAttribute(downsample_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
     downsample_kernel<double><<<g, 256, smem, stream>>>((const double *)ys, p, (int)n, sh, y_low,
-                                                        (int)n_low, spb);
+                                                        (int)n_low, spb, rel, eps_low, eps_fine);
   }
   note_launch();
   return cudaGetLastError();
