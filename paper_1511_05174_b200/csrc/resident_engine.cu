@@ -415,8 +415,287 @@ __global__ void __launch_bounds__(R >= 4 ? 384 : (R == 1 ? 1024 : 512), 1)
   }
 }
 
-// Signals per warp: 4 (every dictionary element read from shared memory
-// feeds 4 FMAs) when the per-lane candidate arrays are small, else 2.
+// ---------------------------------------------------------------- lock-step tensor-core scan
+// Full-dictionary OMP for N <= 32, T <= 256 (the zero-tree step 1 shape):
+// the CTA's 32 warps each own one signal and advance in lock-step, so one
+// iteration's correlations of all 32 signals are the GEMM C = R (32 x 32) .
+// D^T (32 x 256) on the tensor cores (mma.sync m16n8k8 TF32, 3xTF32 split:
+// a_lo b_hi + a_hi b_lo + a_hi b_hi, ~fp32 accuracy) -- every dictionary
+// fragment is read from shared memory once per CTA-iteration instead of once
+// per signal.  Each warp then certifies its pick as the F32C scan does, with
+// E = 2^-15 max|d| |r| (TF32 split residuals, fp32 accumulation in the MMA,
+// fp32 rounding of r: all << 2^-16 relative of sum |r_i d_i| <= |r| |d|),
+// re-scores the window in fp64 when it holds more than one candidate,
+// recomputes the winner's correlation in fp64, and runs the same Cholesky
+// append and residual update as resident_omp_kernel, with the fp64 atoms read
+// from global memory (L1-resident).  Finished signals idle (zero rows) until
+// the CTA's batch of 32 completes.
+constexpr int MM_W = 32;
+constexpr int MM_N = 32;
+constexpr int MM_T = 256;
+constexpr int MM_BS = MM_T + 8;  // B row stride (floats): conflict-free fragment loads
+constexpr int MM_AS = MM_N + 4;  // A row stride
+constexpr int MM_CS = MM_T + 4;  // C row stride
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4],
+                                         const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <typename YT>
+__global__ void __launch_bounds__(1024, 1)
+    resident_mma_kernel(ResidentArgs a, const YT *__restrict__ ys) {
+  constexpr int U = MM_T / 32;
+  extern __shared__ __align__(16) double rs[];
+  __shared__ double s_dmax;
+  const int n = (int)a.n, T = (int)a.t, kw = (int)a.k_width;
+  const int ldl = kw | 1;
+  const int64_t P = a.p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float *Bs = (float *)rs;               // MM_N x MM_BS: Bs[k][j] = d_j[k]
+  float *Ahi = Bs + MM_N * MM_BS;        // MM_W x MM_AS (tf32-rounded floats)
+  float *Alo = Ahi + MM_W * MM_AS;
+  float *Cs = Alo + MM_W * MM_AS;        // MM_W x MM_CS
+  double *nrm2 = (double *)(Cs + MM_W * MM_CS);  // MM_T
+  double *st = nrm2 + MM_T + warp * a.per_warp;
+  double *r = st;
+  double *lin = r + n;
+  double *zv = lin + kw * ldl;
+  double *wv = zv + kw;
+  double *gv = wv + kw;
+  int *sup = (int *)(gv + 2 * kw);
+  const double *d64 = a.d64;
+  const double *gram = a.gram;
+
+  for (int e = threadIdx.x; e < MM_N * MM_T; e += blockDim.x) {
+    const int k = e / MM_T, j = e % MM_T;
+    Bs[k * MM_BS + j] = k < n && j < T ? (float)d64[(int64_t)j * n + k] : 0.0f;
+  }
+  for (int j = threadIdx.x; j < MM_T; j += blockDim.x) {
+    double sq = 0.0;
+    if (j < T)
+      for (int i = 0; i < n; i++) sq = fma(d64[(int64_t)j * n + i], d64[(int64_t)j * n + i], sq);
+    nrm2[j] = sq;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double mx = 0.0;
+    for (int j = threadIdx.x; j < MM_T; j += 32) mx = fmax(mx, nrm2[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(CDB_FULL_MASK, mx, o));
+    if (threadIdx.x == 0) s_dmax = sqrt(mx);
+  }
+  __syncthreads();
+  const double e_rel = 0x1p-15 * 1.01 * s_dmax;  // |c~ - c| <= e_rel |r|
+
+  for (int64_t p0 = (int64_t)blockIdx.x * MM_W; p0 < P; p0 += (int64_t)gridDim.x * MM_W) {
+    const int64_t p = p0 + warp;
+    const bool valid = p < P;
+    const int kmax = valid ? (int)a.cands.budget(p, a.k_max, n) : 0;
+    unsigned tk = 0u;
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (lane + 32 * u >= T) tk |= 1u << u;
+    for (int i = lane; i < n; i += 32) r[i] = valid ? (double)ys[p * n + i] : 0.0;
+    __syncwarp();
+    const double ynorm = sqrt(dot4_quad(r, r, n, lane));  // reference order (_kernels.py:71)
+    const double tol = valid ? a.eps[p] : 0.0;
+    double rnorm = ynorm;
+    int kdone = 0;
+    int64_t scans = 0;
+    bool delegate = false;
+    bool live = valid && !(ynorm <= tol) && kmax > 0;
+    for (int k = 0;; k++) {
+      if (live && k >= kmax) live = false;
+      // this signal's row of A (zeros once finished)
+      for (int i = lane; i < MM_N; i += 32) {
+        const float av = live && i < n ? (float)r[i] : 0.0f;
+        const uint32_t hi = to_tf32(av);
+        Ahi[warp * MM_AS + i] = __uint_as_float(hi);
+        Alo[warp * MM_AS + i] = __uint_as_float(to_tf32(av - __uint_as_float(hi)));
+      }
+      if (!__syncthreads_or(live)) break;
+      {  // ---- C = A B: warp w computes m-tile (w & 1), n-tiles 2 (w >> 1) + {0, 1}
+        const int mt = warp & 1, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+        for (int nn = 0; nn < 2; nn++) {
+          const int nt = (warp >> 1) * 2 + nn;
+          float dd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int ks = 0; ks < MM_N / 8; ks++) {
+            const int k0 = ks * 8;
+            const float *ah = Ahi + (mt * 16 + g) * MM_AS + k0 + tq;
+            const float *al = Alo + (mt * 16 + g) * MM_AS + k0 + tq;
+            const uint32_t ahi[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[8 * MM_AS]),
+                                     __float_as_uint(ah[4]), __float_as_uint(ah[8 * MM_AS + 4])};
+            const uint32_t alo[4] = {__float_as_uint(al[0]), __float_as_uint(al[8 * MM_AS]),
+                                     __float_as_uint(al[4]), __float_as_uint(al[8 * MM_AS + 4])};
+            const float b0 = Bs[(k0 + tq) * MM_BS + nt * 8 + g];
+            const float b1 = Bs[(k0 + tq + 4) * MM_BS + nt * 8 + g];
+            const uint32_t bhi[2] = {to_tf32(b0), to_tf32(b1)};
+            const uint32_t blo[2] = {to_tf32(b0 - __uint_as_float(bhi[0])),
+                                     to_tf32(b1 - __uint_as_float(bhi[1]))};
+            mma_tf32(dd, alo, bhi);
+            mma_tf32(dd, ahi, blo);
+            mma_tf32(dd, ahi, bhi);
+          }
+          float *c0 = Cs + (mt * 16 + g) * MM_CS + nt * 8 + 2 * tq;
+          *(float2 *)c0 = make_float2(dd[0], dd[1]);
+          *(float2 *)(c0 + 8 * MM_CS) = make_float2(dd[2], dd[3]);
+        }
+      }
+      __syncthreads();
+      if (!live) continue;
+      scans += T - k;
+      double acc[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) acc[u] = (double)Cs[warp * MM_CS + lane + 32 * u];
+      // ---- certified selection: max |c| over available atoms, ties -> lowest index
+      double best = -1.0;
+      unsigned bj = 0xffffffffu;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const double v = fabs(acc[u]);
+        if (!((tk >> u) & 1u) && v > best) {
+          best = v;
+          bj = lane + 32 * u;
+        }
+      }
+      double m = best;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+      const double thr = m - 2.0 * e_rel * rnorm;
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (!((tk >> u) & 1u) && fabs(acc[u]) >= thr) cnt++;
+      cnt = (int)__reduce_add_sync(CDB_FULL_MASK, (unsigned)cnt);
+      if (cnt == 0) {  // nothing available (_kernels.py:104)
+        live = false;
+        continue;
+      }
+      if (cnt > 1) {  // re-score the window exactly in fp64 (lane per candidate)
+        best = -1.0;
+        bj = 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          if (!((tk >> u) & 1u) && fabs(acc[u]) >= thr) {
+            const int jj = lane + 32 * u;
+            const double *dj = d64 + (int64_t)jj * n;
+            double c = 0.0;
+            for (int i = 0; i < n; i++) c = fma(__ldg(dj + i), r[i], c);
+            if (fabs(c) > best) {
+              best = fabs(c);
+              bj = jj;
+            }
+          }
+        }
+        m = best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+      }
+      const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+      const int ub = bestj >> 5, owner = bestj & 31;
+      const int nid = bestj;
+      double cbest;
+      {  // the winner's exact correlation (z_k = c / d); orthogonal break on it
+        double c = 0.0;
+        for (int i = lane; i < n; i += 32) c = fma(__ldg(d64 + (int64_t)nid * n + i), r[i], c);
+        cbest = warp_sum(c);
+      }
+      if (!(fabs(cbest) > 0.0)) {  // _kernels.py:104
+        live = false;
+        continue;
+      }
+      if (lane == owner) tk |= 1u << ub;
+      // ---- Cholesky append through the Gram row (as resident_omp_kernel)
+      const double *grow = gram + (int64_t)nid * T;
+      for (int l = lane; l < k; l += 32) gv[l] = __ldg(grow + sup[l]);
+      if (lane == 0) sup[k] = nid;
+      __syncwarp();
+      for (int l = lane; l < k; l += 32) {
+        double accw = 0.0;
+#pragma unroll 4
+        for (int i = 0; i <= l; i++) accw = fma(lin[l * ldl + i], gv[i], accw);
+        wv[l] = accw;
+      }
+      __syncwarp();
+      double ww = 0.0;
+      for (int l = lane; l < k; l += 32) ww = fma(wv[l], wv[l], ww);
+      ww = warp_sum(ww);
+      const double gnn = nrm2[nid];
+      const double d2 = gnn - ww;
+      if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {
+        delegate = true;
+        live = false;
+        continue;
+      }
+      const double inv_d = rsqrt(d2);
+      const double zk = cbest * inv_d;
+      for (int i = lane; i <= k; i += 32) {
+        double v;
+        if (i == k) {
+          v = inv_d;
+        } else {
+          double accl = 0.0;
+#pragma unroll 4
+          for (int l = i; l < k; l++) accl = fma(wv[l], lin[l * ldl + i], accl);
+          v = -accl * inv_d;
+        }
+        lin[k * ldl + i] = v;
+      }
+      if (lane == 0) zv[k] = zk;
+      __syncwarp();
+      kdone = k + 1;
+      // ---- residual r -= z_k q_k,  q_k = sum_l L^{-1}[k][l] d_{s_l}; stop test
+      const double *lk = lin + k * ldl;
+      double rr = 0.0;
+      for (int i = lane; i < n; i += 32) {
+        double qv = 0.0;
+#pragma unroll 4
+        for (int l = 0; l <= k; l++) qv = fma(lk[l], __ldg(d64 + (int64_t)sup[l] * n + i), qv);
+        const double rv = fma(-zk, qv, r[i]);
+        r[i] = rv;
+        rr = fma(rv, rv, rr);
+      }
+      rnorm = sqrt(warp_sum(rr));
+      __syncwarp();
+      if (rnorm <= tol) live = false;
+    }
+    // ---- outputs: x = L^{-T} z (pick order)
+    if (valid) {
+      if (delegate) {
+        if (lane == 0) a.status[p] |= ST_DELEGATE;
+      } else {
+        int64_t *out_sel = a.out_sel + p * kw;
+        double *out_coef = a.out_coef + p * kw;
+        for (int j = lane; j < kw; j += 32) {
+          double x = 0.0;
+          for (int l = j; l < kdone; l++) x = fma(lin[l * ldl + j], zv[l], x);
+          out_sel[j] = j < kdone ? sup[j] : -1;
+          out_coef[j] = j < kdone ? x : 0.0;
+        }
+        if (lane == 0) {
+          a.out_count[p] = kdone;
+          a.out_rnorm[p] = rnorm;
+          a.out_scans[p] = scans;
+          a.out_flag[p] = 0;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int U>
 // signals per warp: 1 with 32 warps/SM measured best for cfg 1 step 1
 // (2.67 ms; 24 warps 2.76; R = 2 x 16 warps 2.83; R = 4 x 12 warps 3.43): the
@@ -505,6 +784,25 @@ cudaError_t launch_resident(const ResidentArgs &args, const void *ys, bool ys_f3
   a.per_warp = resident_warp_doubles(a.n, a.k_width, a.max_cands);
   a.t_pad = resident_tpad(a.t, a.max_cands);
   if (a.cands.mode == 0 && a.t_pad < 32 * ((a.max_cands + 31) / 32)) return cudaErrorInvalidValue;
+  if (a.cands.mode == 0 && a.n <= MM_N && a.t <= MM_T && a.gram && !getenv("CDB_RESIDENT_NO_MMA")) {
+    const size_t smem = sizeof(float) * (MM_N * MM_BS + 2 * MM_W * MM_AS + MM_W * MM_CS) +
+                        sizeof(double) * (MM_T + MM_W * a.per_warp);
+    if ((int64_t)smem <= smem_optin) {
+      int64_t grid = (a.p + MM_W - 1) / MM_W;
+      if (grid > num_sms) grid = num_sms;
+      auto kern = ys_f32 ? (const void *)resident_mma_kernel<float>
+                         : (const void *)resident_mma_kernel<double>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      note_launch();
+      if (ys_f32)
+        resident_mma_kernel<float><<<(int)grid, MM_W * 32, smem, stream>>>(a, (const float *)ys);
+      else
+        resident_mma_kernel<double><<<(int)grid, MM_W * 32, smem, stream>>>(a, (const double *)ys);
+      return cudaGetLastError();
+    }
+  }
   const int64_t base = 8 * (a.n * a.t_pad + a.t_pad);
   int u = 1;
   while (32 * u < a.max_cands) u *= 2;
