@@ -421,6 +421,30 @@ cudaStream_t copy_stream(int which) {
 // `kPipeMid` signals -- each call carries ~0.1-0.3 ms of fixed cost (launch
 // gaps, partial waves), so many small chunks lose more than they hide.
 std::vector<int64_t> chunk_bounds(int64_t p) {
+  if (const char *sched = getenv("CDB_PIPE_SCHEDULE")) {  // "w1,w2,...": relative chunk sizes
+    std::vector<double> w;
+    double tot = 0.0;
+    for (const char *c = sched; *c;) {
+      const double v = atof(c);
+      if (v > 0) {
+        w.push_back(v);
+        tot += v;
+      }
+      while (*c && *c != ',') c++;
+      if (*c == ',') c++;
+    }
+    if (!w.empty()) {
+      std::vector<int64_t> b = {0};
+      double acc = 0.0;
+      for (double x : w) {
+        acc += x;
+        const int64_t e = (int64_t)(p * acc / tot);
+        if (e > b.back()) b.push_back(e);
+      }
+      b.back() = p;
+      return b;
+    }
+  }
   static const int64_t mid_max = getenv("CDB_PIPE_CHUNK") ? atoll(getenv("CDB_PIPE_CHUNK")) : 90000;
   static const int64_t edge_max = getenv("CDB_PIPE_EDGE") ? atoll(getenv("CDB_PIPE_EDGE")) : 20000;
   int64_t edge = p / 5;
