@@ -70,6 +70,17 @@ __device__ __forceinline__ double dot4_quad(const double *a, const double *b, in
   return tot;
 }
 
+// Warp maximum of values v >= 0 (negative inputs count as 0): non-negative
+// IEEE doubles order like their bit patterns, so two redux.max on the high
+// and low words replace a 5-round 64-bit shuffle butterfly.
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+  const unsigned long long b = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mhi = __reduce_max_sync(CDB_FULL_MASK, hi);
+  const unsigned mlo = __reduce_max_sync(CDB_FULL_MASK, hi == mhi ? lo : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+}
+
 // dot4_quad of a gathered vector a[idx[i]] with b[i] (same summation order
 // as dot4_quad on the compacted vector): the masked exact engine's scan.
 __device__ __forceinline__ double dot4_quad_g(const double *a, const int32_t *idx,

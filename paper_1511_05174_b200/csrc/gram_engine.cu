@@ -151,9 +151,15 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
     if (j >= S) tk |= 1u << u;
   }
   double *y = region;  // staging until the first H row is written
-  for (int i = lane; i < n; i += 32) y[i] = (double)yg[i];
+  double yy = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double v = (double)yg[i];
+    y[i] = v;
+    yy = fma(v, v, yy);
+  }
+  yy = warp_sum(yy);
   __syncwarp();
-  const double ynorm = sqrt(dot4_quad(y, y, n, lane));  // reference order (_kernels.py:71)
+  const double ynorm = sqrt(yy);  // early exit |y| <= tol (_kernels.py:71-78)
   const double tol = a.eps[p];
 
   int kdone = 0;
@@ -180,9 +186,6 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
         cr[u] = j < S ? al[j] : 0.0;
       }
     }
-    double yy = 0.0;
-    for (int i = lane; i < n; i += 32) yy = fma(y[i], y[i], yy);
-    yy = warp_sum(yy);
     double rn2 = yy;
     yy_final = yy;
     const double tol2 = tol * tol;
@@ -203,9 +206,7 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
           bj = lane + 32 * u;
         }
       }
-      double m = best;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+      const double m = warp_max_nonneg(best);
       if (!(m > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
       const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
       const int ub = bestj >> 5, owner = bestj & 31;

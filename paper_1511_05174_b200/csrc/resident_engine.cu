@@ -570,9 +570,7 @@ __global__ void __launch_bounds__(1024, 1)
           bj = lane + 32 * u;
         }
       }
-      double m = best;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+      double m = warp_max_nonneg(best);
       const double thr = m - 2.0 * e_rel * rnorm;
       int cnt = 0;
 #pragma unroll
