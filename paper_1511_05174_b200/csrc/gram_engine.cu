@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   int *pj = (int *)(iv + kw);        // candidate index of pick l
   int64_t *sup = (int64_t *)(iv + 2 * kw);
   double *xv = (double *)(sup + kw);
-  double *region = xv + kw;
+  double *region = xv + kw + ((5 * kw) & 1);  // even offset: 16-byte H accesses
   double *h = h_in_smem ? region : a.hwork + local * kw * HS;
   const YT *yg = ys + p * a.ys_stride;
 
@@ -356,7 +356,7 @@ cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int u, int h_in_sm
 int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_cands); }
 
 int64_t gram_total_smem(int64_t s, int64_t kw, int64_t n, bool h_in_smem) {
-  const int64_t b = 8 * (5 * kw + gram_region_doubles(s, kw, n, h_in_smem));
+  const int64_t b = 8 * (((5 * kw + 1) & ~int64_t(1)) + gram_region_doubles(s, kw, n, h_in_smem));
   return (b + 15) & ~int64_t(15);
 }
 

@@ -1,0 +1,92 @@
+"""Seeded random problems across shapes the goldens do not pin: N not a
+multiple of 4 / 32 / 64, T not a multiple of 32, K from 1 to N, fp32 and
+fp64 signals, near-duplicate atoms (delegation to the exact engine), full
+and block-restricted candidates, every engine -- each against the oracle
+(oracle/omp_oracle.c) with the parity contract (tests/parity.py); the exact
+engine bit-identically."""
+
+import numpy as np
+import pytest
+
+from parity import compare
+
+import oracle as O
+from paper_1511_05174_b200 import device as D
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (N, T, K, P)
+    (5, 11, 3, 40), (17, 40, 6, 64), (31, 97, 9, 80), (33, 64, 12, 64),
+    (64, 256, 8, 96), (70, 300, 10, 64), (129, 513, 16, 48), (256, 1000, 20, 32),
+]
+ENGINES = ["exact", "gram", "tensor", "resident", "auto"]
+
+
+def _problem(n, t, k, p, seed, dup):
+    rng = np.random.default_rng(seed)
+    d = rng.standard_normal((t, n))
+    if dup:  # a few near-duplicate atoms: rank trouble for the fast engines
+        d[1] = d[0] + 1e-7 * rng.standard_normal(n)
+        d[t // 2] = d[2] * 0.5 + d[3] * 0.5
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    x = np.zeros((p, t))
+    for i in range(p):
+        sup = rng.choice(t, size=min(k, t), replace=False)
+        x[i, sup] = rng.standard_normal(sup.size)
+    ys = x @ d + 0.01 * rng.standard_normal((p, n))
+    ys[0] = 0.0  # zero signal: immediate exit
+    return d, ys
+
+
+def _oracle(d, ys, k, eps, allowed=None):
+    sel, coef, count, rnorm, scans, flag = O.omp_batch(d, ys, k, eps, allowed)
+    return dict(sel=sel, alpha=coef, counts=count, rnorm=rnorm, scans=scans,
+                flag=np.asarray(flag, bool))
+
+
+def _check(ref, got, d, ys, eps, engine, allowed=None):
+    got["flag"] = got["flag"].astype(bool)
+    if engine == "exact":
+        keep = ~ref["flag"]
+        for key in ("counts", "sel", "scans", "flag"):
+            assert np.array_equal(got[key], ref[key]), key
+        assert np.array_equal(got["alpha"][keep], ref["alpha"][keep])
+        assert np.array_equal(got["rnorm"][keep], ref["rnorm"][keep])
+        return
+    rep = compare(ref, got, d, ys, eps, allowed)
+    assert not rep["bad"], rep["bad"][:3]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("engine", ENGINES)
+def test_random_full(shape, engine):
+    n, t, k, p = shape
+    k = min(k, n, t)
+    for seed, dup, f32 in ((n * t, False, True), (n * t + 1, True, False)):
+        d, ys = _problem(n, t, k, p, seed, dup)
+        if f32:
+            ys = ys.astype(np.float32).astype(np.float64)
+        eps = 1e-3 * np.linalg.norm(ys, axis=1)
+        ref = _oracle(d, ys, k, eps)
+        dd = D.DeviceDictionary(d)
+        got = D.omp_batch_raw(dd, ys.astype(np.float32) if f32 else ys, p, k, eps, None, engine)
+        _check(ref, got, d, ys, eps, engine)
+
+
+@pytest.mark.parametrize("shape", SHAPES[1:6])
+@pytest.mark.parametrize("engine", ["exact", "gram", "resident", "auto"])
+def test_random_blocked(shape, engine):
+    n, t, k, p = shape
+    q = 4
+    t = (t // q) * q
+    nb = 3
+    d, ys = _problem(n, t, k, p, n + t, False)
+    rng = np.random.default_rng(t)
+    blocks = np.sort(np.stack([rng.choice(t // q, size=nb, replace=False) for _ in range(p)]), 1)
+    allowed = (blocks[:, :, None] * q + np.arange(q)[None, None, :]).reshape(p, -1)
+    k_max = min(k, nb * q, n)
+    eps = 1e-3 * np.linalg.norm(ys, axis=1)
+    ref = _oracle(d, ys, k_max, eps, allowed)
+    dd = D.DeviceDictionary(d)
+    got = D.omp_batch_blocked_raw(dd, ys, p, k_max, eps, np.ascontiguousarray(blocks), q, engine)
+    _check(ref, got, d, ys, eps, engine, allowed)
