@@ -987,126 +987,228 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
   }
 }
 
-// Exact fp64 argmax over every non-taken atom for the queued signals.  Each
-// signal is split over RS_SPLIT CTAs (latency: a handful of signals per
-// iteration, each a T x N fp64 scan): every part materialises the exact
-// residual r = y - D64_S x and a taken-atom mask in shared memory, scans its
-// 1/RS_SPLIT of the atoms (warps stream 8 rows at a time, coalesced, c_j =
-// <d_j, r>), and publishes (|c|, j, c); the last part to finish reduces the
-// partials (max |c|, lowest index on ties) into rs_j / rs_c.
-constexpr int RS_SPLIT = 16;
+// Exact fp64 argmax over every non-taken atom for the queued signals.  The
+// queue is cut into groups of RG signals and the atoms into parts; one CTA
+// work item = (group, part): it materialises the RG exact residuals
+// r = y - D64_S x and their taken-atom masks in shared memory, then streams
+// its slice of the fp64 dictionary once for the whole group (each row feeds
+// RG residuals, so the L2 / HBM traffic is 1/RG of a per-signal scan).  A
+// warp pass covers 32/RG rows, i.e. 32 accumulators per lane, folded by a
+// butterfly reduce-scatter (31 shuffles) that leaves lane l the sum of
+// accumulator l.  Each part publishes (|c|, j, c) per signal; the last part of
+// a group to finish reduces the partials (max |c|, lowest index on ties) into
+// rs_j / rs_c.  The part count is chosen on the device from the queue length
+// so that even a handful of queued signals fills the grid.
+constexpr int RS_SPLIT = 16;  // partial slots per signal (buffer sizing)
 
-template <typename YT>
-__global__ void __launch_bounds__(256) rescan_kernel(const YT *__restrict__ ys,
-                                                     const double *__restrict__ d64,
-                                                     const double *__restrict__ gram, int64_t t,
-                                                     int64_t n, int64_t kw, int iter,
+template <int NV>
+__device__ __forceinline__ double fold_lanes(double (&v)[NV], int lane) {
+#pragma unroll
+  for (int off = NV / 2; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int h = 0; h < off; h++) {
+      const double send = up ? v[h] : v[h + off];
+      const double keep = up ? v[h + off] : v[h];
+      v[h] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+template <typename YT, int RG>
+__global__ void __launch_bounds__(512) rescan_kernel(const YT *__restrict__ ys,
+                                                     const double *__restrict__ d64, int64_t p,
+                                                     int64_t t, int64_t n, int64_t kw, int iter,
                                                      TensorState st, const int64_t *out_sel,
                                                      const double *out_coef) {
+  constexpr int ROWS = 32 / RG;
+  constexpr int NW = 16;
   extern __shared__ double rsm[];
-  __shared__ double sv[8];
-  __shared__ int64_t sj[8];
-  __shared__ double sc[8];
+  __shared__ double sv[NW][RG];
+  __shared__ int64_t sj[NW][RG];
+  __shared__ double sc[NW][RG];
   __shared__ int last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t count = st.npending[iter];
-  double *y = rsm;                                   // n
-  double *x = y + n;                                 // kw
-  int64_t *sel = (int64_t *)(x + kw);                // kw
-  uint32_t *taken = (uint32_t *)(sel + kw);          // (t + 31) / 32
-  const int64_t per = (t + RS_SPLIT - 1) / RS_SPLIT;
-  for (int64_t w = blockIdx.x; w < count * RS_SPLIT; w += gridDim.x) {
-    const int64_t e = w / RS_SPLIT;
-    const int part = (int)(w % RS_SPLIT);
-    const int64_t sig = st.pending[e];
-    const int64_t k = iter;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = (double)ys[sig * n + i];
-    for (int64_t i = threadIdx.x; i < (t + 31) / 32; i += blockDim.x) taken[i] = 0u;
-    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
-      x[i] = out_coef[sig * kw + i];
-      sel[i] = out_sel[sig * kw + i];
+  if (count == 0) return;
+  const int64_t tw = (t + 31) / 32;
+  double *r = rsm;                                     // RG x n
+  double *x = r + RG * n;                              // RG x kw
+  int64_t *sel = (int64_t *)(x + RG * kw);             // RG x kw
+  uint32_t *taken = (uint32_t *)(sel + RG * kw);       // RG x tw
+  const int64_t groups = (count + RG - 1) / RG;
+  int64_t nparts = (2 * (int64_t)gridDim.x + groups - 1) / groups;
+  if (nparts < 16) nparts = 16;
+  if (nparts > (t + 63) / 64) nparts = (t + 63) / 64;
+  if (nparts > p * RS_SPLIT / count) nparts = p * RS_SPLIT / count;
+  if (nparts < 1) nparts = 1;
+  const int64_t per = (t + nparts - 1) / nparts;
+  const int64_t k = iter;
+  for (int64_t w = blockIdx.x; w < groups * nparts; w += gridDim.x) {
+    const int64_t g = w / nparts, part = w % nparts;
+    const int64_t e0 = g * RG;
+    const int ng = (int)(count - e0 < RG ? count - e0 : RG);
+    for (int64_t i = threadIdx.x; i < RG * tw; i += blockDim.x) taken[i] = 0u;
+    for (int64_t i = threadIdx.x; i < RG * kw; i += blockDim.x) {
+      const int s = (int)(i / kw);
+      const int64_t l = i % kw;
+      const bool ok = s < ng && l < k;
+      const int64_t sig = ok ? st.pending[e0 + s] : 0;
+      x[i] = ok ? out_coef[sig * kw + l] : 0.0;
+      sel[i] = ok ? out_sel[sig * kw + l] : 0;
     }
     __syncthreads();
-    if (threadIdx.x < k) {
-      const int64_t j = sel[threadIdx.x];
-      atomicOr(&taken[j >> 5], 1u << (j & 31));
+    for (int i = threadIdx.x; i < ng * (int)k; i += blockDim.x) {
+      const int s = i / (int)k;
+      const int64_t j = sel[s * kw + i % (int)k];
+      atomicOr(&taken[s * tw + (j >> 5)], 1u << (j & 31));
     }
-    __syncthreads();
-    // r = y - D64_S x, exact fp64 (then plain dots)
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      double ri = y[i];
-      for (int64_t l = 0; l < k; l++) ri = fma(-x[l], __ldg(d64 + sel[l] * n + i), ri);
-      y[i] = ri;  // y now holds r
+    // r_s = y_s - D64_S x_s, exact fp64 (zero for the unused group slots)
+    for (int64_t i = threadIdx.x; i < RG * n; i += blockDim.x) {
+      const int s = (int)(i / n);
+      const int64_t c = i % n;
+      double ri = 0.0;
+      if (s < ng) {
+        const int64_t sig = st.pending[e0 + s];
+        ri = (double)ys[sig * n + c];
+        for (int64_t l = 0; l < k; l++)
+          ri = fma(-x[s * kw + l], __ldg(d64 + sel[s * kw + l] * n + c), ri);
+      }
+      r[i] = ri;
     }
     __syncthreads();
     const int64_t jlo = part * per, jhi = jlo + per < t ? jlo + per : t;
     double best = -1.0, cbest = 0.0;
     int64_t bestj = -1;
-    for (int64_t j0 = jlo + (int64_t)warp * 8; j0 < jhi; j0 += 64) {
-      const double *rows[8];
+    const int my_s = lane % RG, my_row = lane / RG;
+    for (int64_t j0 = jlo + (int64_t)warp * ROWS; j0 < jhi; j0 += NW * ROWS) {
+      const double *rows[ROWS];
 #pragma unroll
-      for (int r = 0; r < 8; r++) rows[r] = d64 + (j0 + r < jhi ? j0 + r : jlo) * n;
-      double acc[8];
+      for (int q = 0; q < ROWS; q++) rows[q] = d64 + (j0 + q < jhi ? j0 + q : jlo) * n;
+      double acc[32];
 #pragma unroll
-      for (int r = 0; r < 8; r++) acc[r] = 0.0;
+      for (int q = 0; q < 32; q++) acc[q] = 0.0;
+#pragma unroll(RG == 8 ? 2 : 1)
       for (int64_t i = lane; i < n; i += 32) {
-        const double ri = y[i];
+        double dv[ROWS], rv[RG];
 #pragma unroll
-        for (int r = 0; r < 8; r++) acc[r] = fma(__ldg(rows[r] + i), ri, acc[r]);
+        for (int q = 0; q < ROWS; q++) dv[q] = __ldg(rows[q] + i);
+#pragma unroll
+        for (int s = 0; s < RG; s++) rv[s] = r[s * n + i];
+#pragma unroll
+        for (int q = 0; q < ROWS; q++)
+#pragma unroll
+          for (int s = 0; s < RG; s++) acc[q * RG + s] = fma(dv[q], rv[s], acc[q * RG + s]);
       }
-#pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int64_t j = j0 + r;
-        const double cj = warp_sum(acc[r]);
-        if (j < jhi && !((taken[j >> 5] >> (j & 31)) & 1u)) {
-          const double v = fabs(cj);
-          if (v > best || (v == best && j < bestj)) {
-            best = v;
-            bestj = j;
-            cbest = cj;
-          }
+      const double cj = fold_lanes<32>(acc, lane);
+      const int64_t j = j0 + my_row;
+      if (my_s < ng && j < jhi && !((taken[my_s * tw + (j >> 5)] >> (j & 31)) & 1u)) {
+        const double v = fabs(cj);
+        if (v > best || (v == best && j < bestj)) {
+          best = v;
+          bestj = j;
+          cbest = cj;
         }
       }
     }
-    if (lane == 0) {
-      sv[warp] = best;
-      sj[warp] = bestj;
-      sc[warp] = cbest;
+    // lanes sharing my_s: lane ^ RG, ^ 2RG, ...
+#pragma unroll
+    for (int off = RG; off < 32; off <<= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+      const int64_t oj = __shfl_xor_sync(0xffffffffu, bestj, off);
+      const double oc = __shfl_xor_sync(0xffffffffu, cbest, off);
+      if (oj >= 0 && (bestj < 0 || ov > best || (ov == best && oj < bestj))) {
+        best = ov;
+        bestj = oj;
+        cbest = oc;
+      }
+    }
+    if (lane < RG) {
+      sv[warp][lane] = best;
+      sj[warp][lane] = bestj;
+      sc[warp][lane] = cbest;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int q = 1; q < 8; q++)
-        if (sj[q] >= 0 && (bestj < 0 || sv[q] > best || (sv[q] == best && sj[q] < bestj))) {
-          best = sv[q];
-          bestj = sj[q];
-          cbest = sc[q];
-        }
-      st.rs_pv[e * RS_SPLIT + part] = best;
-      st.rs_pj[e * RS_SPLIT + part] = bestj;
-      st.rs_pc[e * RS_SPLIT + part] = cbest;
-      __threadfence();
-      last = atomicAdd(&st.rs_cnt[e], 1) == RS_SPLIT - 1;
-    }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {  // every part published: reduce them
-      __threadfence();
+    if (threadIdx.x < ng) {
+      const int s = threadIdx.x;
       double b = -1.0, c = 0.0;
       int64_t bj = -1;
-      for (int q = 0; q < RS_SPLIT; q++) {
-        const double v = __ldcg(st.rs_pv + e * RS_SPLIT + q);
-        const int64_t j = __ldcg(st.rs_pj + e * RS_SPLIT + q);
+      for (int q = 0; q < NW; q++)
+        if (sj[q][s] >= 0 && (bj < 0 || sv[q][s] > b || (sv[q][s] == b && sj[q][s] < bj))) {
+          b = sv[q][s];
+          bj = sj[q][s];
+          c = sc[q][s];
+        }
+      const int64_t slot = (e0 + s) * nparts + part;
+      st.rs_pv[slot] = b;
+      st.rs_pj[slot] = bj;
+      st.rs_pc[slot] = c;
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st.rs_cnt[g], 1) == (int)nparts - 1;
+    __syncthreads();
+    if (last && threadIdx.x < ng) {  // every part of the group published: reduce
+      __threadfence();
+      const int64_t e = e0 + threadIdx.x;
+      double b = -1.0, c = 0.0;
+      int64_t bj = -1;
+      for (int64_t q = 0; q < nparts; q++) {
+        const double v = __ldcg(st.rs_pv + e * nparts + q);
+        const int64_t j = __ldcg(st.rs_pj + e * nparts + q);
         if (j >= 0 && (bj < 0 || v > b || (v == b && j < bj))) {
           b = v;
           bj = j;
-          c = __ldcg(st.rs_pc + e * RS_SPLIT + q);
+          c = __ldcg(st.rs_pc + e * nparts + q);
         }
       }
+      const int64_t sig = st.pending[e];
       st.rs_j[sig] = bj;
       st.rs_c[sig] = c;
-      st.rs_cnt[e] = 0;
     }
+    if (last && threadIdx.x == 0) st.rs_cnt[g] = 0;
     __syncthreads();
   }
+}
+
+
+// Signals per rescan group: as many as fit 200 KB of shared memory (r, x,
+// sel, taken per signal), at most 8.
+size_t rescan_smem(int rg, int64_t t, int64_t n, int64_t kw) {
+  return (size_t)rg * (8 * n + 16 * kw + 4 * ((t + 31) / 32)) + 64;
+}
+
+template <typename YT>
+cudaError_t launch_rescan_t(const TensorArgs &a, const TensorState &st, int64_t t, int64_t n,
+                            int64_t kw, int it, cudaStream_t stream) {
+  const size_t lim = 200 * 1024;
+  int rg = 8;
+  while (rg > 1 && rescan_smem(rg, t, n, kw) > lim) rg >>= 1;
+  const size_t sm = rescan_smem(rg, t, n, kw);
+  if (sm > 227 * 1024) return cudaErrorInvalidValue;
+  const void *f = rg == 8   ? (const void *)rescan_kernel<YT, 8>
+                  : rg == 4 ? (const void *)rescan_kernel<YT, 4>
+                  : rg == 2 ? (const void *)rescan_kernel<YT, 2>
+                            : (const void *)rescan_kernel<YT, 1>;
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  const int per_sm = sm <= 100 * 1024 ? 2 : 1;
+  const unsigned grid = (unsigned)(a.num_sms * per_sm);
+  const YT *ys = (const YT *)a.ys;
+  switch (rg) {
+    case 8: rescan_kernel<YT, 8><<<grid, 512, sm, stream>>>(ys, a.d64, a.p, t, n, kw, it, st, a.out_sel, a.out_coef); break;
+    case 4: rescan_kernel<YT, 4><<<grid, 512, sm, stream>>>(ys, a.d64, a.p, t, n, kw, it, st, a.out_sel, a.out_coef); break;
+    case 2: rescan_kernel<YT, 2><<<grid, 512, sm, stream>>>(ys, a.d64, a.p, t, n, kw, it, st, a.out_sel, a.out_coef); break;
+    default: rescan_kernel<YT, 1><<<grid, 512, sm, stream>>>(ys, a.d64, a.p, t, n, kw, it, st, a.out_sel, a.out_coef); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rescan(const TensorArgs &a, const TensorState &st, int64_t t, int64_t n,
+                          int64_t kw, int it, cudaStream_t stream) {
+  return a.ys_f32 ? launch_rescan_t<float>(a, st, t, n, kw, it, stream)
+                  : launch_rescan_t<double>(a, st, t, n, kw, it, stream);
 }
 
 // Final residual norms (the reported rnorm): sqrt(|y|^2 - |z|^2) when that is
@@ -1311,13 +1413,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     for (int resume = 0; resume < 2; resume++) {
       if (resume) {
         ProfScope _ps("rescan", stream);
-        const size_t rs_smem = 8 * (n + 2 * kw) + 4 * ((t + 31) / 32) + 64;
-        if (a.ys_f32)
-          rescan_kernel<float><<<(unsigned)a.num_sms, 256, rs_smem, stream>>>(
-              (const float *)a.ys, a.d64, a.gram, t, n, kw, it, st, a.out_sel, a.out_coef);
-        else
-          rescan_kernel<double><<<(unsigned)a.num_sms, 256, rs_smem, stream>>>(
-              (const double *)a.ys, a.d64, a.gram, t, n, kw, it, st, a.out_sel, a.out_coef);
+        if ((e = launch_rescan(a, st, t, n, kw, it, stream)) != cudaSuccess) return e;
         note_launch();
       }
       ProfScope _ps(resume ? "ls_resume" : "ls_step", stream);
