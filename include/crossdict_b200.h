@@ -131,6 +131,35 @@ cdb_status cdb_omp_batch_masked(const cdb_dictionary *dict, const double *ys,
                                 uint8_t *out_flag, void *stream);
 
 /*
+ * Coded batched OMP (general form; crossdict
+ * pipelines._recover_operator pipelines.py:256-322 with sensing.patch_problem
+ * sensing.py:205-279, and the Phi zero-tree steps of crossscale.zero_tree_omp
+ * crossscale.py:194-222 per patch): signal p is measured through its own
+ * operator with m[p] <= m_stride outputs.  Effective row i of signal p sums
+ * the atom coordinates rows[(p*m_stride + i)*fan + u], u < fan (fan 1: a
+ * gather -- masks, channel mosaics, angular sampling; fan F: a binary
+ * temporal code), in numpy's order for the reference's
+ * E_p = phi_p.apply_matrix(D): sum_order 0 = sequential over the listed
+ * sources (the list ends at the first -1; C-contiguous columns), 1 =
+ * numpy's pairwise_sum over all fan slots, -1 slots being 0.0 (the frame
+ * axis contiguous: zero-tree step-2 columns, or a single column; fan <= 128).  ys is
+ * P x m_stride fp64 (first m[p] used).  blocks (P x nb_max, ascending, or
+ * NULL for all T atoms; nb NULL -> nb_max each) restricts the candidates to
+ * blocks*q + [0,q) in that order -- the reference's local OMP over
+ * D_high[:, allowed] -- and outputs are global atom ids.  Budget
+ * min(k_max, candidates, m[p]) per signal.  Exact engine: selections,
+ * coefficients, residuals and scans follow the reference's arithmetic.
+ * m_stride <= N.  Host or device pointers.
+ */
+cdb_status cdb_omp_batch_coded(const cdb_dictionary *dict, const double *ys, int64_t m_stride,
+                               const int32_t *rows, int64_t fan, int sum_order,
+                               const int64_t *m, int64_t p,
+                               int64_t k_max, const double *eps, const int64_t *blocks,
+                               int64_t nb_max, const int64_t *nb, int64_t q, int64_t *out_sel,
+                               double *out_coef, int64_t *out_count, double *out_rnorm,
+                               int64_t *out_scans, uint8_t *out_flag, void *stream);
+
+/*
  * Ragged block-restricted batched OMP: signal p may use its first nb[p]
  * block ids of row p of blocks (P x nb_max, ascending within the used
  * prefix); budget min(k_max, nb[p]*q, N) per signal; outputs k_max wide.

@@ -19,7 +19,8 @@ from .fileio import SingleScaleModel, load_model, save_model
 from .install import install, uninstall
 from .patchwork import (PatchGrid, aggregate_patches, extract_patches, patch_count,
                         reconstruct_aggregate)
-from .pipelines import denoise
+from .pipelines import denoise, recover_masked, recover_operator
+from . import sensing
 from .pursuit import (BatchSolve, DenseColumns, PursuitConfig, PursuitResult, as_columns, omp,
                       omp_many, omp_many_arrays)
 from .scaling import ScaleSpec, downsample_columns, upsample_columns

@@ -184,18 +184,22 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
                      const int64_t *sig_ids, int64_t k_max, int64_t kw, const double *eps,
                      const cdb::Cands &cands, int64_t max_cands, Outs &o, const DevInfo &di,
                      cudaStream_t st, const int *count_dev = nullptr,
-                     const int32_t *rows = nullptr, const int64_t *m_sig = nullptr) {
+                     const int32_t *rows = nullptr, const int64_t *m_sig = nullptr,
+                     int fan = 1, int64_t m_stride = 0, int sum_order = 0) {
   if (count <= 0) return CDB_OK;
   cdb::ExactArgs a{};
   a.mat_t = d->d64;
   a.t = d->t;
   a.n = d->n;
-  a.ys_stride = d->n;
+  a.ys_stride = rows ? m_stride : d->n;
   a.sig_ids = sig_ids;
   a.p_count = count;
   a.p_count_dev = count_dev;
   a.rows = rows;
   a.m_sig = m_sig;
+  a.fan = fan;
+  a.sum_order = sum_order;
+  a.rows_stride = m_stride * fan;
   a.k_max = k_max;
   a.k_width = kw;
   a.eps = eps;
@@ -1102,39 +1106,69 @@ cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f
                     out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, engine, stream);
 }
 
-cdb_status cdb_omp_batch_masked(const cdb_dictionary *dict, const double *ys,
-                                const int32_t *rows, const int64_t *m, int64_t p, int64_t k_max,
-                                const double *eps, int64_t *out_sel, double *out_coef,
-                                int64_t *out_count, double *out_rnorm, int64_t *out_scans,
-                                uint8_t *out_flag, void *stream) {
-  if (!dict || p < 0 || k_max < 0 || (p > 0 && (!ys || !rows || !m || !eps)))
-    return fail(CDB_ERR_ARG, "bad masked omp arguments");
+cdb_status cdb_omp_batch_coded(const cdb_dictionary *dict, const double *ys, int64_t m_stride,
+                               const int32_t *rows, int64_t fan, int sum_order,
+                               const int64_t *m, int64_t p,
+                               int64_t k_max, const double *eps, const int64_t *blocks,
+                               int64_t nb_max, const int64_t *nb, int64_t q, int64_t *out_sel,
+                               double *out_coef, int64_t *out_count, double *out_rnorm,
+                               int64_t *out_scans, uint8_t *out_flag, void *stream) {
+  if (!dict || p < 0 || k_max < 0 || fan < 1 || fan > 1024 || sum_order < 0 ||
+      sum_order > 1 || (sum_order == 1 && fan > 128) ||
+      (p > 0 && (!ys || !rows || !m || !eps || m_stride < 1 || m_stride > dict->n)))
+    return fail(CDB_ERR_ARG, "bad coded omp arguments");
+  if (blocks && (nb_max < 1 || q < 1 || nb_max * q > dict->t))
+    return fail(CDB_ERR_ARG, "bad block arguments");
   if (p == 0) return CDB_OK;
   DevInfo di;
   cdb_status s0 = device_info(di);
   if (s0 != CDB_OK) return s0;
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t n = dict->n;
-  InArr y_in, r_in, m_in, e_in;
-  CDB_CUDA(y_in.bind(ys, sizeof(double) * p * n, st));
-  CDB_CUDA(r_in.bind(rows, sizeof(int32_t) * p * n, st));
+  InArr y_in, r_in, m_in, e_in, b_in, nb_in;
+  CDB_CUDA(y_in.bind(ys, sizeof(double) * p * m_stride, st));
+  CDB_CUDA(r_in.bind(rows, sizeof(int32_t) * p * m_stride * fan, st));
   CDB_CUDA(m_in.bind(m, sizeof(int64_t) * p, st));
   CDB_CUDA(e_in.bind(eps, sizeof(double) * p, st));
   Outs o;
   CDB_CUDA(o.bind(p, k_max, out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, st));
   cdb::Cands c{};
-  c.mode = 0;
   c.t = dict->t;
-  c.clip = 1;  // budget min(k_max, T, m_p) per signal
+  c.clip = 1;  // budget min(k_max, candidates, m_p) per signal
+  int64_t max_cands = dict->t;
+  if (blocks) {
+    CDB_CUDA(b_in.bind(blocks, sizeof(int64_t) * p * nb_max, st));
+    if (nb) CDB_CUDA(nb_in.bind(nb, sizeof(int64_t) * p, st));
+    c.mode = 2;
+    c.ids = (const int64_t *)b_in.dev;
+    c.stride = nb_max;
+    c.q = q;
+    c.nb = nb ? (const int64_t *)nb_in.dev : nullptr;
+    c.nb_fixed = nb_max;
+    max_cands = nb_max * q;
+  } else {
+    c.mode = 0;
+  }
   g_last_engine = CDB_ENGINE_EXACT;
   diag_clear(st);
   cdb_status s = run_exact(dict, y_in.dev, false, p, nullptr, k_max, k_max,
-                           (const double *)e_in.dev, c, dict->t, o, di, st, nullptr,
-                           (const int32_t *)r_in.dev, (const int64_t *)m_in.dev);
+                           (const double *)e_in.dev, c, max_cands, o, di, st, nullptr,
+                           (const int32_t *)r_in.dev, (const int64_t *)m_in.dev, (int)fan,
+                           m_stride, sum_order);
   if (s != CDB_OK) return s;
   CDB_CUDA(o.finish(st));
   CDB_CUDA(cudaStreamSynchronize(st));
   return CDB_OK;
+}
+
+cdb_status cdb_omp_batch_masked(const cdb_dictionary *dict, const double *ys,
+                                const int32_t *rows, const int64_t *m, int64_t p, int64_t k_max,
+                                const double *eps, int64_t *out_sel, double *out_coef,
+                                int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                                uint8_t *out_flag, void *stream) {
+  if (!dict) return fail(CDB_ERR_ARG, "bad masked omp arguments");
+  return cdb_omp_batch_coded(dict, ys, dict->n, rows, 1, 0, m, p, k_max, eps, nullptr, 0, nullptr,
+                             0, out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag,
+                             stream);
 }
 
 cdb_status cdb_omp_batch_blocked_ragged(const cdb_dictionary *dict, const void *ys, int ys_is_f32,

@@ -99,4 +99,63 @@ __device__ __forceinline__ double dot4_quad_g(const double *a, const int32_t *id
   return tot;
 }
 
+// Element i of a coded effective atom (per-patch measurement operators, SURVEY
+// row f3).  ord 0: the sequential sum of atom[idx[i*fan + u]] over the listed
+// sources (-1 ends the list; fan 1 = a gather: masks, mosaics, angular
+// sampling), which is numpy's frame-axis sum of a temporal code applied to
+// C-contiguous columns (sensing.py:89-91; the zero-coded frames add +-0).
+// ord 1: numpy's pairwise_sum over exactly `fan` slots (slot -1 = 0.0), the
+// order numpy takes when the frame axis is the contiguous one -- the step-2
+// columns d_high.atoms_t[allowed0].T of zero_tree_omp (crossscale.py:215) or
+// a single column.  fan <= 128 in that mode (one 8-accumulator block).
+__device__ __forceinline__ double eff_at(const double *atom, const int32_t *idx, int fan, int ord,
+                                         int64_t i) {
+  if (fan == 1) return atom[idx[i]];
+  const int32_t *q = idx + i * fan;
+  if (ord == 0) {
+    double e = atom[q[0]];
+    for (int u = 1; u < fan; u++) {
+      const int32_t s = q[u];
+      if (s < 0) break;
+      e = __dadd_rn(e, atom[s]);
+    }
+    return e;
+  }
+  auto v = [&](int u) { return q[u] >= 0 ? atom[q[u]] : 0.0; };
+  if (fan < 8) {
+    double res = 0.0;
+    for (int u = 0; u < fan; u++) res = __dadd_rn(res, v(u));
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) r[j] = v(j);
+  int u = 8;
+  for (; u < fan - (fan % 8); u += 8)
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], v(u + j));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; u < fan; u++) res = __dadd_rn(res, v(u));
+  return res;
+}
+
+// dot4_quad of a coded vector (eff_at) with b[i]: the masked / coded exact
+// engine's scan, same summation order as dot4_quad on the compacted vector.
+__device__ __forceinline__ double dot4_quad_c(const double *a, const int32_t *idx, int fan,
+                                              int ord, const double *b, int64_t n, int lane) {
+  const int m = lane & 3;
+  const int64_t m4 = (n / 4) * 4;
+  double s = 0.0;
+  for (int64_t i = m; i < m4; i += 4) s = __dadd_rn(s, __dmul_rn(eff_at(a, idx, fan, ord, i), b[i]));
+  const int base = lane & ~3;
+  const double s0 = __shfl_sync(CDB_FULL_MASK, s, base + 0);
+  const double s1 = __shfl_sync(CDB_FULL_MASK, s, base + 1);
+  const double s2 = __shfl_sync(CDB_FULL_MASK, s, base + 2);
+  const double s3 = __shfl_sync(CDB_FULL_MASK, s, base + 3);
+  double tot = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3);
+  for (int64_t i = m4; i < n; i++) tot = __dadd_rn(tot, __dmul_rn(eff_at(a, idx, fan, ord, i), b[i]));
+  return tot;
+}
+
 }  // namespace cdb

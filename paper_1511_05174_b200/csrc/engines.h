@@ -28,9 +28,13 @@ struct ExactArgs {
   const int64_t *sig_ids;  // optional: process only these signals
   int64_t p_count;       // number of signals to process (len(sig_ids) or P)
   const int *p_count_dev;  // optional: the count lives on the device (<= p_count)
-  const int32_t *rows;     // optional masked mode: per-signal kept coordinates
-                           // (row p, stride ys_stride, ascending), m_sig[p] of them
+  const int32_t *rows;     // optional coded mode: per-signal effective rows, m_sig[p]
+                           // of them, each `fan` source coordinates (row p at
+                           // rows + p * rows_stride; see eff_at in common.cuh)
   const int64_t *m_sig;
+  int fan;
+  int sum_order;           // eff_at ord: 0 sequential list, 1 numpy pairwise slots
+  int64_t rows_stride;
   int64_t k_max;         // budget (clipped per signal when cands.clip)
   int64_t k_width;       // output row width
   const double *eps;

@@ -13,11 +13,13 @@
 // runs a one-sided Jacobi SVD minimum-norm solve (the same restatement as
 // oracle/omp_oracle.c, coefficients "parity unpinned").
 //
-// Masked mode (rows != NULL): signal p is measured on m_p kept
-// coordinates of the atoms (a per-patch mask operator, pipelines.py:281-293):
-// every atom access reads atom[rows[i]] for i < m_p, i.e. the reference's
-// compacted effective dictionary E_p = D[kept, :] in its own order, and the
-// signal row holds the m_p kept measurements.
+// Coded mode (rows != NULL): signal p is measured through its
+// own patch operator with m_p outputs (pipelines.py:256-322, sensing.
+// patch_problem): every atom access reads the effective element eff_at(atom,
+// rows_p, fan, i) for i < m_p -- atom[rows[i]] for a mask / mosaic / angular
+// gather, the ordered sum of the coded frames for a temporal code -- i.e. the
+// reference's effective dictionary E_p = phi_p.apply_matrix(D) in its own
+// arithmetic, and the signal row holds the m_p measurements.
 //
 // Role in the product: the engine of record for small problems and the
 // fallback for signals the fast engines delegate (rank trouble or an
@@ -113,7 +115,8 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
   for (int64_t idx = warp_global; idx < count; idx += n_warps) {
     const int64_t p = a.sig_ids ? a.sig_ids[idx] : idx;
     const int64_t c = cs.count(p);
-    const int32_t *rw = a.rows ? a.rows + p * a.ys_stride : nullptr;
+    const int32_t *rw = a.rows ? a.rows + p * a.rows_stride : nullptr;
+    const int fan = a.fan, ord = a.sum_order;
     const int64_t ne = rw ? a.m_sig[p] : n;  // coordinates this signal is measured on
     const int64_t k_max = cs.budget(p, a.k_max, ne);
     int64_t *sel = a.out_sel + p * kw;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
           const int64_t jl = base + grp;
           const bool live = jl < c && !((taken[jl >> 5] >> (jl & 31)) & 1u);
           const int64_t g = jl < c ? cs.id(p, jl) : 0;
-          double v = rw ? dot4_quad_g(a.mat_t + g * n, rw, r, ne, lane)
+          double v = rw ? dot4_quad_c(a.mat_t + g * n, rw, fan, ord, r, ne, lane)
                         : dot4_quad(a.mat_t + g * n, r, n, lane);
           if (v < 0.0) v = -v;
           if (live && v > best) {
@@ -165,7 +168,8 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
 
         if (!dense) {
           // ---- MGS with one re-orthogonalisation (_kernels.py:111-137)
-          for (int64_t i = lane; i < ne; i += 32) u[i] = a.mat_t[g * n + (rw ? rw[i] : i)];
+          for (int64_t i = lane; i < ne; i += 32)
+            u[i] = rw ? eff_at(a.mat_t + g * n, rw, fan, ord, i) : a.mat_t[g * n + i];
           __syncwarp();
           const double anorm = sqrt(dot4_quad(u, u, ne, lane));
           for (int pass = 0; pass < 2; pass++) {
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
           for (int64_t j = 0; j < kdone; j++) {
             const int64_t gj = sel[j];
             for (int64_t i = lane; i < ne; i += 32)
-              amat[j * ne + i] = a.mat_t[gj * n + (rw ? rw[i] : i)];
+              amat[j * ne + i] = rw ? eff_at(a.mat_t + gj * n, rw, fan, ord, i) : a.mat_t[gj * n + i];
           }
           __syncwarp();
           if (lane == 0) lstsq_min_norm(amat, ne, kdone, y, coefs, vwork);
@@ -214,7 +218,8 @@ __global__ void __launch_bounds__(256) exact_omp_kernel(ExactArgs a, const YT *_
           for (int64_t i = lane; i < ne; i += 32) {
             double acc = 0.0;
             for (int64_t j = 0; j < kdone; j++)
-              acc += a.mat_t[sel[j] * n + (rw ? rw[i] : i)] * coefs[j];
+              acc += (rw ? eff_at(a.mat_t + sel[j] * n, rw, fan, ord, i) : a.mat_t[sel[j] * n + i]) *
+                     coefs[j];
             r[i] = y[i] - acc;
           }
           __syncwarp();

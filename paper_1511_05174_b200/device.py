@@ -263,3 +263,21 @@ def omp_batch_masked_raw(dd: DeviceDictionary, ys, rows, m, p: int, k_max: int, 
     N.check(N.load().cdb_omp_batch_masked(dd.handle, N.ptr(ys), N.ptr(rows), N.ptr(m), int(p),
                                           int(k_max), N.ptr(eps), *_out_ptrs(o), stream))
     return o
+
+
+def omp_batch_coded_raw(dd: DeviceDictionary, ys, rows, m, p: int, k_max: int, eps,
+                        blocks=None, nb=None, q: int = 1, pairwise: bool = False, out=None,
+                        stream=None):
+    """cdb_omp_batch_coded: OMP of ys[p][:m[p]] over the coded effective
+    dictionary of rows (P x M x fan int32, -1 padded; ``pairwise``: numpy's
+    pairwise order over all fan slots), optionally restricted to the ragged
+    blocks (P x nb_max, nb[p] used)."""
+    o = out if out is not None else _out(p, k_max)
+    m_stride, fan = int(rows.shape[1]), int(rows.shape[2])
+    nb_max = int(blocks.shape[1]) if blocks is not None else 0
+    N.check(N.load().cdb_omp_batch_coded(dd.handle, N.ptr(ys), m_stride, N.ptr(rows), fan,
+                                         1 if pairwise else 0, N.ptr(m), int(p), int(k_max), N.ptr(eps),
+                                         N.ptr(blocks) if blocks is not None else None, nb_max,
+                                         N.ptr(nb) if nb is not None else None, int(q),
+                                         *_out_ptrs(o), stream))
+    return o

@@ -9,6 +9,9 @@ reference imported them by name -- to this package's B200 implementations:
 * ``crossdict.patchwork.{extract_patches, aggregate_patches}`` (patchwork.py:58-122)
 * ``crossdict.learn._code_stage`` (learn.py:240-262): K-SVD's coding stage as
   one ragged block-restricted device call
+* ``crossdict.pipelines._recover_operator`` (pipelines.py:258-322): operator
+  recovery (masks, mosaics, temporal codes, angular sampling) with every
+  patch coded in one coded-rows device call per step
 * the re-exports in ``crossdict/__init__.py:12-33`` and the by-name imports
   of the callers ``crossdict.pipelines`` (pipelines.py:214-297) and
   ``crossdict.learn`` (learn.py:245-260).
@@ -27,6 +30,7 @@ from . import crossscale as _cs
 from . import errors as _errors
 from . import learn as _learn
 from . import patchwork as _pw
+from . import pipelines as _pipelines
 from . import pursuit as _pursuit
 
 _saved: dict = {}
@@ -42,6 +46,7 @@ _FUNCS = {
     "extract_patches": _pw.extract_patches,
     "aggregate_patches": _pw.aggregate_patches,
     "_code_stage": _learn.code_stage,  # crossdict.learn only (learn.py:240-262)
+    "_recover_operator": _pipelines.recover_operator_stage,  # crossdict.pipelines only
 }
 _MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
             "crossdict.learn", "crossdict.patchwork")

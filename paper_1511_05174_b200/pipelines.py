@@ -11,6 +11,8 @@ memory).  Single-scale OMP (``dictionary`` + ``sparsity``) or zero-tree
 from __future__ import annotations
 
 import time
+from dataclasses import dataclass, field
+from typing import Optional
 
 import numpy as np
 
@@ -18,6 +20,7 @@ from . import device as _dev
 from . import errors as E
 from . import patchwork as _pw
 from . import pursuit as _pursuit
+from . import sensing as _sensing
 
 
 def _outs(p, k, dev):
@@ -96,6 +99,167 @@ def denoise(signal, patch_shape, stride=1, *, dictionary=None, sparsity=None, mo
     return estimate, solve, {"extract": t1 - t0, "coding": t2 - t1, "reconstruct": t3 - t2}
 
 
+@dataclass
+class RecoveryMetrics:
+    """Per-run instrumentation (pipelines.RecoveryMetrics, pipelines.py:80-96;
+    the fields the operator path fills)."""
+
+    method: str
+    patch_count: int = 0
+    residual_norms: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    scan_count_step1: int = 0
+    scan_count_step2: int = 0
+    nesting_ok_fraction: Optional[float] = None
+    flagged_patches: int = 0
+    coding_time_s: float = 0.0
+    aggregate_time_s: float = 0.0
+
+
+def _default_stride(patch_shape, signal_shape):
+    return tuple(ext if pe == ext else max(1, pe // 2) for pe, ext in zip(patch_shape, signal_shape))
+
+
+def recover_operator(measurements, phi, patch_shape, stride=None, *, dictionary=None,
+                     sparsity=None, model=None, remove_dc=None, signal_shape=None):
+    """Patch recovery through a structured measurement operator (SURVEY §8
+    row f3): crossdict ``pipelines._recover_operator`` (pipelines.py:258-322)
+    with ``sensing.patch_problem`` (sensing.py:205-279) for masks, channel
+    mosaics, temporal codes and angular sampling, coding every patch in ONE
+    batched exact-engine call per step (``cdb_omp_batch_coded``) instead of
+    one scalar ``omp`` / ``zero_tree_omp(phi=sub_op)`` per patch.
+
+    ``dictionary`` + ``sparsity``: method "omp-single" (OMP on phi_p D, budget
+    min(sparsity, T, m_p)).  ``model`` (CrossScaleModel): method "zerotree",
+    the Phi form of zero_tree_omp per patch (crossscale.py:194-222): step 1 on
+    phi_p U D_low with budget min(k_low, m_p, T_low), step 2 on phi_p D_high
+    restricted to the step-1 blocks with budget min(k_high, nb Q, m_p).
+    ``remove_dc`` defaults to on for masks only (and is refused otherwise).
+    Returns ``(estimate, metrics, codes)``: the overlap-averaged estimate
+    (Tensor), a RecoveryMetrics, and the device outputs (``{"step1", "step2"}``
+    for zero-tree, ``{"code"}`` otherwise).
+    """
+    if (dictionary is None) == (model is None):
+        raise E.ConfigError("pass exactly one of dictionary= (with sparsity=) or model=")
+    if phi is None or phi.kind == "identity":
+        raise E.ConfigError("identity measurements: use pipelines.denoise")
+    meas = np.asarray(_pw.as_array(measurements), dtype=np.float64)
+    sig_shape = _sensing.signal_shape_for(phi, meas.shape, signal_shape)
+    pshape = tuple(int(e) for e in patch_shape)
+    if len(pshape) != len(sig_shape):
+        raise E.DimensionError(f"patch rank {len(pshape)} != signal rank {len(sig_shape)}")
+    if stride is None:
+        stride = _default_stride(pshape, sig_shape)
+    pshape, strides = _pw._geometry(sig_shape, pshape, stride)
+    if remove_dc is None:
+        remove_dc = phi.kind == "mask"
+    if remove_dc and phi.kind != "mask":
+        raise E.ConfigError(f"DC removal is only supported for mask measurements, not {phi.kind}")
+    n = int(np.prod(pshape))
+    if phi.input_dim != int(np.prod(sig_shape)):
+        raise E.DimensionError(f"operator input dim {phi.input_dim} != signal size "
+                               f"{int(np.prod(sig_shape))}")
+    ys, rows, m = _sensing.coded_problems(phi, meas, sig_shape, pshape, strides)
+    p = ys.shape[0]
+
+    def slot_rows():
+        if phi.kind != "temporal-code":
+            return rows
+        return _sensing.coded_problems(phi, meas, sig_shape, pshape, strides, slots=True)[1]
+
+    dc = np.zeros(p)
+    if remove_dc:
+        for mm in np.unique(m[m > 0]):  # numpy's own mean of each compacted row
+            sel = np.flatnonzero(m == mm)
+            dc[sel] = ys[sel, :mm].mean(axis=1)
+            ys[sel, :mm] = ys[sel, :mm] - dc[sel, None]
+    ynorm = np.array([float(np.linalg.norm(ys[i, :m[i]])) for i in range(p)])
+    eps = _pursuit._rel_tol() * ynorm
+    empty = m == 0  # unrecoverable patch: skipped, contributes 0 (pipelines.py:279-281)
+    metrics = RecoveryMetrics("zerotree" if model is not None else "omp-single", patch_count=p)
+    t0 = time.perf_counter()
+    if dictionary is not None:
+        atoms = np.asarray(getattr(dictionary, "atoms", dictionary), dtype=np.float64)
+        if atoms.shape[0] != n:
+            raise E.DimensionError(f"atom dim {atoms.shape[0]} != patch size {n}")
+        dd = _dev.device_dictionary(np.ascontiguousarray(atoms.T))
+        k = int(min(sparsity, atoms.shape[1]))
+        pw = atoms.shape[1] == 1  # one column: numpy reduces the frame axis pairwise
+        code = _dev.omp_batch_coded_raw(dd, ys, slot_rows() if pw else rows, m, p, k, eps,
+                                        pairwise=pw)
+        metrics.scan_count_step1 = int(code["scans"].sum())
+        codes = {"code": code}
+    else:
+        if model.d_high.atom_dim != n:
+            raise E.DimensionError(f"model fine size {model.d_high.atom_dim} != patch size {n}")
+        dlow = _dev.device_dictionary(np.ascontiguousarray(model.upsampled_low_atoms.T))
+        dd = _dev.device_dictionary(model.d_high.atoms_t)
+        pw1 = model.t_low == 1
+        s1 = _dev.omp_batch_coded_raw(dlow, ys, slot_rows() if pw1 else rows, m, p, model.k_low,
+                                      eps, pairwise=pw1)
+        c1 = np.asarray(s1["counts"])
+        kb = max(int(c1.max()) if p else 0, 1)
+        blocks = np.sort(np.where(np.arange(s1["sel"].shape[1])[None, :] < c1[:, None],
+                                  s1["sel"], np.iinfo(np.int64).max), axis=1)[:, :kb]
+        blocks = np.ascontiguousarray(np.where(blocks == np.iinfo(np.int64).max, 0, blocks))
+        # step 2 applies phi to d_high.atoms_t[allowed0].T (crossscale.py:215): the
+        # frame axis is the contiguous one, so numpy sums it pairwise
+        code = _dev.omp_batch_coded_raw(dd, ys, slot_rows(), m, p, model.k_high, eps, blocks,
+                                        np.ascontiguousarray(c1, dtype=np.int64), model.q,
+                                        pairwise=True)
+        s1_empty = (c1 == 0) & ~empty & (ynorm > 0)  # step1_empty (crossscale.py:204)
+        code["rnorm"][c1 == 0] = ynorm[c1 == 0]  # _zero_result (crossscale.py:139-148)
+        metrics.scan_count_step1 = int(s1["scans"].sum())
+        metrics.scan_count_step2 = int(code["scans"].sum())
+        live = ~empty
+        hs, hc = code["sel"], code["counts"]
+        ok = [set((hs[i, :hc[i]] // model.q).tolist()) <= set(s1["sel"][i, :c1[i]].tolist())
+              for i in np.flatnonzero(live)]
+        metrics.nesting_ok_fraction = float(np.mean(ok)) if ok else 1.0
+        metrics.flagged_patches += int(s1_empty.sum())
+        codes = {"step1": s1, "step2": code}
+    metrics.coding_time_s = time.perf_counter() - t0
+    metrics.flagged_patches += int(empty.sum())
+    resid = np.asarray(code["rnorm"], dtype=np.float64).copy()
+    resid[empty] = 0.0
+    metrics.residual_norms = resid
+    if empty.any():
+        code["sel"][empty] = -1
+        code["counts"][empty] = 0
+        dc[empty] = 0.0
+    t1 = time.perf_counter()
+    est, unc = _dev.reconstruct_aggregate_raw(dd, code["sel"], code["alpha"], p, dc, sig_shape,
+                                              pshape, strides)
+    metrics.aggregate_time_s = time.perf_counter() - t1
+    return _pw._finish(est, unc), metrics, codes
+
+
+def recover_operator_stage(meas, phi, sig_shape, patch_shape, stride, config, metrics):
+    """Drop-in for crossdict ``pipelines._recover_operator`` (pipelines.py:
+    258-322): same arguments, fills the caller's RecoveryMetrics, returns
+    ``(estimate, metrics)``; every patch is coded in one device call per
+    step (see :func:`recover_operator`)."""
+    t0 = time.perf_counter()
+    if config.method == "zerotree":
+        kw = dict(model=config.model)
+    else:
+        d = config.fine_dictionary()
+        kw = dict(dictionary=d.atoms, sparsity=config.resolved_sparsity())
+    est, met, _ = recover_operator(meas, phi, patch_shape, stride, remove_dc=config.remove_dc,
+                                   signal_shape=sig_shape, **kw)
+    total = time.perf_counter() - t0
+    metrics.patch_count = met.patch_count
+    metrics.coding_time_s = met.coding_time_s
+    metrics.aggregate_time_s = met.aggregate_time_s
+    metrics.prep_time_s = total - met.coding_time_s - met.aggregate_time_s
+    metrics.residual_norms = met.residual_norms
+    metrics.scan_count_step1 += met.scan_count_step1
+    metrics.scan_count_step2 += met.scan_count_step2
+    if config.method == "zerotree":
+        metrics.nesting_ok_fraction = met.nesting_ok_fraction
+    metrics.flagged_patches += met.flagged_patches
+    return est, metrics
+
+
 def recover_masked(measurements, known, patch_shape, stride=1, *, dictionary, sparsity,
                    remove_dc: bool = True):
     """Inpainting / masked recovery: crossdict
@@ -115,37 +279,8 @@ def recover_masked(measurements, known, patch_shape, stride=1, *, dictionary, sp
     if known.shape != meas.shape:
         raise E.DimensionError(f"mask shape {known.shape} != measurement shape {meas.shape}")
     atoms = np.asarray(getattr(dictionary, "atoms", dictionary), dtype=np.float64)
-    pshape, strides = _pw._geometry(meas.shape, patch_shape, stride)
-    n = int(np.prod(pshape))
-    if atoms.shape[0] != n:
-        raise E.DimensionError(f"atom dim {atoms.shape[0]} != patch size {n}")
-    t = atoms.shape[1]
-    k_single = int(min(sparsity, t))
-    vals, _ = _dev.extract_patches_raw(meas, pshape, strides, False)
-    kept, _ = _dev.extract_patches_raw(known.astype(np.float64), pshape, strides, False)
-    vals, kept = np.asarray(vals), np.asarray(kept) != 0.0
-    p = vals.shape[0]
-    m = kept.sum(axis=1).astype(np.int64)
-    order = np.argsort(~kept, axis=1, kind="stable")  # kept cells first, ascending
-    rows = np.ascontiguousarray(order, dtype=np.int32)
-    ys = np.take_along_axis(vals, order, axis=1)
-    ys[np.arange(n)[None, :] >= m[:, None]] = 0.0
-    dc = np.zeros(p)
-    if remove_dc:
-        for mm in np.unique(m[m > 0]):  # numpy's own mean of each compacted row
-            sel = np.flatnonzero(m == mm)
-            dc[sel] = ys[sel, :mm].mean(axis=1)
-            ys[sel, :mm] = ys[sel, :mm] - dc[sel, None]
-    rel = _pursuit._rel_tol()
-    eps = np.array([rel * float(np.linalg.norm(ys[i, :m[i]])) for i in range(p)])
-    dd = _dev.device_dictionary(np.ascontiguousarray(atoms.T))
-    o = _dev.omp_batch_masked_raw(dd, np.ascontiguousarray(ys), rows, m, p, k_single, eps)
-    flagged = m == 0
-    if flagged.any():  # unrecoverable patches contribute 0 (pipelines.py:279-281)
-        o["sel"][flagged] = -1
-        o["counts"][flagged] = 0
-        dc[flagged] = 0.0
-    est, unc = _dev.reconstruct_aggregate_raw(dd, o["sel"], o["alpha"], p, dc, meas.shape,
-                                              pshape, strides)
-    estimate = _pw._finish(est, unc)
-    return estimate, _pursuit._make_batch(t, o), int(flagged.sum())
+    phi = _sensing.mask_from_tensor(known)
+    estimate, metrics, codes = recover_operator(meas, phi, patch_shape, stride,
+                                                dictionary=atoms, sparsity=sparsity,
+                                                remove_dc=remove_dc, signal_shape=meas.shape)
+    return estimate, _pursuit._make_batch(atoms.shape[1], codes["code"]), metrics.flagged_patches

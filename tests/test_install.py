@@ -32,6 +32,8 @@ def test_install_rebinds_and_restores(crossdict):
         assert "crossdict.learn._code_stage" in patched
         assert "crossdict.patchwork.extract_patches" in patched
         assert "crossdict.pipelines.aggregate_patches" in patched
+        # operator recovery
+        assert "crossdict.pipelines._recover_operator" in patched
         import crossdict.learn as cl
         assert cl._code_stage is b200.learn.code_stage
         assert crossdict.pursuit.omp_many_arrays is b200.omp_many_arrays
