@@ -27,6 +27,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -1173,6 +1174,237 @@ __global__ void __launch_bounds__(512) rescan_kernel(const YT *__restrict__ ys,
 }
 
 
+// ---------------------------------------------------------------- tiled rescan
+// For large dictionaries (T*N >= 2^22: every group of the kernel above would
+// stream the whole fp64 dictionary from HBM) the queued rescans of one
+// iteration are computed as the fp64 GEMM C = R D64^T over all queued
+// residuals R at once, tiled 64 signals x 128 atoms per CTA (8 x 8 register
+// blocking: 2 B of shared-memory traffic per FMA, i.e. FP64-pipe bound), with
+// the masked argmax fused into the epilogue: each tile publishes
+// (max |c|, lowest atom, c) per signal, and the last atom tile of a signal
+// tile to finish reduces the partials into rs_j / rs_c.  Work items run
+// signal-tile-fastest so the CTAs sharing an atom tile are co-resident and
+// the dictionary is read from HBM about once per iteration.  Queues longer
+// than `cap` signals run in several passes (a pass past the queue's end
+// exits at once).
+constexpr int RT_S = 64, RT_A = 128, RT_K = 16;
+
+template <typename YT>
+__global__ void __launch_bounds__(256) rescan_residual_kernel(
+    const YT *__restrict__ ys, const double *__restrict__ d64, int64_t t, int64_t n, int64_t kw,
+    int iter, TensorState st, const int64_t *out_sel, const double *out_coef, int64_t base,
+    int64_t cap, double *__restrict__ rbuf, uint32_t *__restrict__ tbits) {
+  extern __shared__ double rrs[];
+  double *x = rrs;                       // kw
+  int64_t *sel = (int64_t *)(x + kw);    // kw
+  const int64_t count = st.npending[iter];
+  const int64_t end = count < base + cap ? count : base + cap;
+  const int64_t tw = (t + 31) / 32;
+  const int64_t k = iter;
+  for (int64_t e = base + blockIdx.x; e < end; e += gridDim.x) {
+    const int64_t sig = st.pending[e], slot = e - base;
+    for (int64_t l = threadIdx.x; l < k; l += blockDim.x) {
+      x[l] = out_coef[sig * kw + l];
+      sel[l] = out_sel[sig * kw + l];
+    }
+    uint32_t *tb = tbits + slot * tw;
+    for (int64_t i = threadIdx.x; i < tw; i += blockDim.x) tb[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x < k) {
+      const int64_t j = sel[threadIdx.x];
+      atomicOr(&tb[j >> 5], 1u << (j & 31));
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      double ri = (double)ys[sig * n + i];
+      for (int64_t l = 0; l < k; l++) ri = fma(-x[l], __ldg(d64 + sel[l] * n + i), ri);
+      rbuf[slot * n + i] = ri;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) rescan_tile_kernel(
+    const double *__restrict__ d64, int64_t t, int64_t n, int iter, TensorState st, int64_t base,
+    int64_t cap, const double *__restrict__ rbuf, const uint32_t *__restrict__ tbits,
+    double *__restrict__ pv, int *__restrict__ pj, double *__restrict__ pc, int *tcnt) {
+  constexpr int SA = RT_S + 1, SB = RT_A + 1;  // padded rows: conflict-free transposed stores
+  extern __shared__ double tsm[];
+  double *As = tsm;                // RT_K x SA   residual chunk, k-major
+  double *Bs = As + RT_K * SA;     // RT_K x SB   atom chunk, k-major
+  __shared__ int last;
+  int64_t count = st.npending[iter] - base;
+  if (count > cap) count = cap;
+  if (count <= 0) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t s_tiles = (count + RT_S - 1) / RT_S, a_tiles = (t + RT_A - 1) / RT_A;
+  const int64_t tw = (t + 31) / 32;
+  for (int64_t w = blockIdx.x; w < s_tiles * a_tiles; w += gridDim.x) {
+    const int64_t stile = w % s_tiles, at = w / s_tiles;
+    const int64_t s0 = stile * RT_S, a0 = at * RT_A;
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+      for (int j = 0; j < 8; j++) acc[i][j] = 0.0;
+    for (int64_t k0 = 0; k0 < n; k0 += RT_K) {
+#pragma unroll
+      for (int q = 0; q < RT_S * RT_K / 128; q++) {
+        const int idx = tid + 128 * q, s = idx / RT_K, kk = idx % RT_K;
+        As[kk * SA + s] =
+            (s0 + s < count && k0 + kk < n) ? rbuf[(s0 + s) * n + k0 + kk] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < RT_A * RT_K / 128; q++) {
+        const int idx = tid + 128 * q, a = idx / RT_K, kk = idx % RT_K;
+        Bs[kk * SB + a] =
+            (a0 + a < t && k0 + kk < n) ? __ldg(d64 + (a0 + a) * n + k0 + kk) : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int kk = 0; kk < RT_K; kk++) {
+        double av[8], bv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) av[i] = As[kk * SA + ty + 8 * i];
+#pragma unroll
+        for (int j = 0; j < 8; j++) bv[j] = Bs[kk * SB + tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+#pragma unroll
+          for (int j = 0; j < 8; j++) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+    // ---- masked argmax: my 8 atoms (ascending), then across the 16 tx lanes
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const int64_t s = s0 + ty + 8 * i;
+      double best = -1.0, cb = 0.0;
+      int bj = -1;
+      if (s < count) {
+        const uint32_t *tb = tbits + s * tw;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int64_t a = a0 + tx + 16 * j;
+          if (a < t && !((__ldg(tb + (a >> 5)) >> (a & 31)) & 1u)) {
+            const double v = fabs(acc[i][j]);
+            if (v > best) {
+              best = v;
+              bj = (int)a;
+              cb = acc[i][j];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+        const double oc = __shfl_xor_sync(0xffffffffu, cb, off);
+        if (oj >= 0 && (bj < 0 || ov > best || (ov == best && oj < bj))) {
+          best = ov;
+          bj = oj;
+          cb = oc;
+        }
+      }
+      if (tx == 0 && s < count) {
+        pv[s * a_tiles + at] = best;
+        pj[s * a_tiles + at] = bj;
+        pc[s * a_tiles + at] = cb;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&tcnt[stile], 1) == (int)a_tiles - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      for (int si = tid; si < RT_S; si += blockDim.x) {
+        const int64_t s = s0 + si;
+        if (s >= count) break;
+        double b = -1.0, c = 0.0;
+        int bjj = -1;
+        for (int64_t q = 0; q < a_tiles; q++) {
+          const double v = __ldcg(pv + s * a_tiles + q);
+          const int j = __ldcg(pj + s * a_tiles + q);
+          if (j >= 0 && (bjj < 0 || v > b || (v == b && j < bjj))) {
+            b = v;
+            bjj = j;
+            c = __ldcg(pc + s * a_tiles + q);
+          }
+        }
+        const int64_t sig = st.pending[base + s];
+        st.rs_j[sig] = bjj;
+        st.rs_c[sig] = c;
+      }
+      if (tid == 0) tcnt[stile] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+// Buffers of the tiled rescan (stream-ordered allocations, freed at the end
+// of the chunk).
+struct TileRescan {
+  int64_t cap = 0, a_tiles = 0;
+  double *r = nullptr, *pv = nullptr, *pc = nullptr;
+  uint32_t *tb = nullptr;
+  int *pj = nullptr, *cnt = nullptr;
+  void *mem = nullptr;
+  cudaStream_t stream = nullptr;
+  ~TileRescan() {
+    if (mem) cudaFreeAsync(mem, stream);
+  }
+};
+
+bool rescan_tiled(int64_t t, int64_t n) {
+  const char *m = getenv("CDB_RESCAN");
+  if (m && !strcmp(m, "tile")) return true;
+  if (m && !strcmp(m, "group")) return false;
+  return t * n >= (int64_t(1) << 22);
+}
+
+cudaError_t tile_rescan_alloc(TileRescan &tr, int64_t p, int64_t t, int64_t n,
+                              cudaStream_t stream) {
+  int64_t cap = (int64_t(256) << 20) / (8 * n);
+  cap = cap / RT_S * RT_S;
+  if (cap < RT_S) cap = RT_S;
+  if (cap > p) cap = (p + RT_S - 1) / RT_S * RT_S;
+  tr.cap = cap;
+  tr.a_tiles = (t + RT_A - 1) / RT_A;
+  const int64_t tw = (t + 31) / 32;
+  auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+  const int64_t b_r = al(cap * n * 8), b_tb = al(cap * tw * 4), b_p = al(cap * tr.a_tiles * 8),
+                b_j = al(cap * tr.a_tiles * 4), b_c = al((cap / RT_S + 1) * 4);
+  tr.stream = stream;
+  cudaError_t e = cudaMallocAsync(&tr.mem, b_r + b_tb + 2 * b_p + b_j + b_c, stream);
+  if (e != cudaSuccess) return e;
+  uint8_t *w = (uint8_t *)tr.mem;
+  tr.r = (double *)w;
+  tr.tb = (uint32_t *)(w += b_r);
+  tr.pv = (double *)(w += b_tb);
+  tr.pc = (double *)(w += b_p);
+  tr.pj = (int *)(w += b_p);
+  tr.cnt = (int *)(w += b_j);
+  return cudaMemsetAsync(tr.cnt, 0, b_c, stream);
+}
+
+template <typename YT>
+cudaError_t launch_rescan_tiled_t(const TensorArgs &a, const TensorState &st, TileRescan &tr,
+                                  int64_t t, int64_t n, int64_t kw, int it, cudaStream_t stream) {
+  const size_t tsm = sizeof(double) * RT_K * ((RT_S + 1) + (RT_A + 1));
+  const size_t rsm = 16 * (size_t)kw;
+  for (int64_t base = 0; base < a.p; base += tr.cap) {
+    rescan_residual_kernel<YT><<<(unsigned)(a.num_sms * 4), 256, rsm, stream>>>(
+        (const YT *)a.ys, a.d64, t, n, kw, it, st, a.out_sel, a.out_coef, base, tr.cap, tr.r,
+        tr.tb);
+    note_launch();
+    rescan_tile_kernel<<<(unsigned)(a.num_sms * 3), 128, tsm, stream>>>(
+        a.d64, t, n, it, st, base, tr.cap, tr.r, tr.tb, tr.pv, tr.pj, tr.pc, tr.cnt);
+    note_launch();
+  }
+  return cudaGetLastError();
+}
+
 // Signals per rescan group: as many as fit 200 KB of shared memory (r, x,
 // sel, taken per signal), at most 8.
 size_t rescan_smem(int rg, int64_t t, int64_t n, int64_t kw) {
@@ -1400,6 +1632,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     if ((e = set((const void *)ls_group_kernel<float, 32>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<double, 32>)) != cudaSuccess) return e;
   }
+  const bool tiled = rescan_tiled(t, n);
+  TileRescan tr;
+  if (tiled && (e = tile_rescan_alloc(tr, p, t, n, stream)) != cudaSuccess) return e;
   for (int it = 0; it < a.k_max; it++) {
     {
     ProfScope _ps("corr_topk", stream);
@@ -1413,7 +1648,12 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     for (int resume = 0; resume < 2; resume++) {
       if (resume) {
         ProfScope _ps("rescan", stream);
-        if ((e = launch_rescan(a, st, t, n, kw, it, stream)) != cudaSuccess) return e;
+        if (tiled)
+          e = a.ys_f32 ? launch_rescan_tiled_t<float>(a, st, tr, t, n, kw, it, stream)
+                       : launch_rescan_tiled_t<double>(a, st, tr, t, n, kw, it, stream);
+        else
+          e = launch_rescan(a, st, t, n, kw, it, stream);
+        if (e != cudaSuccess) return e;
         note_launch();
       }
       ProfScope _ps(resume ? "ls_resume" : "ls_step", stream);

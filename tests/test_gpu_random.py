@@ -90,3 +90,20 @@ def test_random_blocked(shape, engine):
     dd = D.DeviceDictionary(d)
     got = D.omp_batch_blocked_raw(dd, ys, p, k_max, eps, np.ascontiguousarray(blocks), q, engine)
     _check(ref, got, d, ys, eps, engine, allowed)
+
+
+def test_tiled_rescan_matches_oracle(monkeypatch):
+    """The tensor engine's tiled fp64 rescan (the large-dictionary path),
+    forced on shapes whose bf16 scans leave picks uncertified."""
+    from paper_1511_05174_b200 import _native as N
+    monkeypatch.setenv("CDB_RESCAN", "tile")
+    rescans = 0
+    for n, t, k, p in ((129, 513, 16, 160), (256, 1000, 20, 200), (70, 300, 10, 130)):
+        d, ys = _problem(n, t, k, p, n + t + 5, True)
+        ys += 0.2 * np.random.default_rng(n).standard_normal(ys.shape)  # noisy: near ties
+        eps = 1e-4 * np.linalg.norm(ys, axis=1)
+        ref = _oracle(d, ys, k, eps)
+        got = D.omp_batch_raw(D.DeviceDictionary(d), ys, p, k, eps, None, "tensor")
+        rescans += N.last_run_info()[2]
+        _check(ref, got, d, ys, eps, "tensor")
+    assert rescans > 0
