@@ -306,9 +306,17 @@ __global__ void to_bf16_rows(const float *__restrict__ rows, int64_t p, int64_t 
 }
 
 // ---------------------------------------------------------------- LS side
+// L^{-1} layout (shared and global): row stride kwp = kw rounded up to 16,
+// element (l, i) at l * kwp + (i ^ (l & 15)).  Lanes walking a column (fixed
+// i, l = lane) hit 16 distinct banks; lanes walking a row stay inside one
+// aligned 128-byte block.
+__device__ __forceinline__ int64_t lsw(int64_t l, int64_t i, int64_t kwp) {
+  return l * kwp + (i ^ (l & 15));
+}
+
 struct TensorState {
   __nv_bfloat16 *r16;   // Ppad x n_pad   GEMM operand  bf16(r~), r~ = y - D32_S x
-  double *linv;         // P x kw x kw    L^{-1} row-major
+  double *linv;         // P x kw x kwp   L^{-1}, swizzled rows (lsw)
   double *z;            // P x kw         q_i^T y
   double *rn2;          // P   |y|^2 - |z|^2   (= |r|^2 up to rounding)
   double *yy;           // P   |y|^2
@@ -427,6 +435,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
                           double *gv, double *zv, const double *y, int lane, double g0, double g1,
                           double rn2_prev, double tol, double yy) {
   const int64_t k = iter;
+  const int64_t ldl = (kw + 15) & ~int64_t(15);  // L^{-1} row stride (see lsw)
   const double *grow = gram + bestj * t;
   const double gnn = __ldg(grow + bestj);
   if (lane < k) gv[lane] = g0;
@@ -435,7 +444,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
   __syncwarp();
   for (int64_t l = lane; l < k; l += 32) {
     double acc = 0.0;
-    for (int64_t i = 0; i <= l; i++) acc = fma(lin[l * kw + i], gv[i], acc);
+    for (int64_t i = 0; i <= l; i++) acc = fma(lin[lsw(l, i, ldl)], gv[i], acc);
     wv[l] = acc;
   }
   __syncwarp();
@@ -456,11 +465,11 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
       v = inv_d;
     } else {
       double acc = 0.0;
-      for (int64_t l = i; l < k; l++) acc = fma(wv[l], lin[l * kw + i], acc);
+      for (int64_t l = i; l < k; l++) acc = fma(wv[l], lin[lsw(l, i, ldl)], acc);
       v = -acc * inv_d;
     }
-    lin[k * kw + i] = v;
-    st.linv[sig * kw * kw + k * kw + i] = v;
+    lin[lsw(k, i, ldl)] = v;
+    st.linv[sig * kw * ldl + lsw(k, i, ldl)] = v;
   }
   if (lane == 0) {
     zv[k] = zk;
@@ -472,7 +481,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
   const int64_t kd = k + 1;
   for (int64_t i = lane; i < kd; i += 32) {
     double acc = 0.0;
-    for (int64_t l = i; l < kd; l++) acc = fma(lin[l * kw + i], zv[l], acc);
+    for (int64_t l = i; l < kd; l++) acc = fma(lin[lsw(l, i, ldl)], zv[l], acc);
     xv[i] = acc;
     out_coef[sig * kw + i] = acc;
   }
@@ -564,9 +573,10 @@ __global__ void __launch_bounds__(256, 3) ls_step_kernel(
     int64_t *out_sel, double *out_coef, int64_t *out_count, int64_t *out_scans, int resume) {
   extern __shared__ double lsm[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t per_warp = kw * kw + 5 * kw + n;
+  const int64_t ldl = (kw + 15) & ~int64_t(15);
+  const int64_t per_warp = kw * ldl + 5 * kw + n;
   double *lin = lsm + wib * per_warp;  // L^{-1} rows (row-major)
-  double *wv = lin + kw * kw;          // w
+  double *wv = lin + kw * ldl;         // w
   double *xv = wv + kw;                // x (current coefficients)
   double *gv = xv + kw;                // G[new, S]
   double *zv = gv + kw;                // z
@@ -597,7 +607,7 @@ __global__ void __launch_bounds__(256, 3) ls_step_kernel(
       zv[i] = st.z[sig * kw + i];
       ssel[i] = sel[i];
     }
-    for (int64_t i = lane; i < k * kw; i += 32) lin[i] = st.linv[sig * kw * kw + i];
+    for (int64_t i = lane; i < k * ldl; i += 32) lin[i] = st.linv[sig * kw * ldl + i];
     __syncwarp();
     double best = -1.0, cbest = 0.0, bg0 = 0.0, bg1 = 0.0;
     int64_t bestj = -1;
@@ -703,9 +713,10 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gi = lane / G, gl = lane % G;
   const unsigned gbits = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (gi * G);
-  const int per_group = kw * kw + 5 * kw;
+  const int ldl = (kw + 15) & ~15;  // L^{-1} row stride (see lsw)
+  const int per_group = kw * ldl + 5 * kw;
   double *lin = lsm + (wib * NG + gi) * per_group;
-  double *wv = lin + kw * kw;
+  double *wv = lin + kw * ldl;
   double *xv = wv + kw;
   double *gv = xv + kw;
   double *zv = gv + kw;
@@ -743,7 +754,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
         zv[i] = st.z[sig * kw + i];
         ssel[i] = sel[i];
       }
-      for (int i = gl; i < k * kw; i += G) lin[i] = st.linv[sig * kw * kw + i];
+      for (int i = gl; i < k * ldl; i += G) lin[i] = st.linv[sig * kw * ldl + i];
     }
     YT yv[YM > 0 ? YM : 1];
     if constexpr (YM > 0) {
@@ -854,7 +865,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     if (act)
       for (int l = gl; l < k; l += G) {
         double acc = 0.0;
-        for (int i = 0; i <= l; i++) acc = fma(lin[l * kw + i], gv[i], acc);
+        for (int i = 0; i <= l; i++) acc = fma(lin[lsw(l, i, ldl)], gv[i], acc);
         wv[l] = acc;
       }
     __syncwarp();
@@ -876,11 +887,11 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
           v = inv_d;
         } else {
           double acc = 0.0;
-          for (int l = i; l < k; l++) acc = fma(wv[l], lin[l * kw + i], acc);
+          for (int l = i; l < k; l++) acc = fma(wv[l], lin[lsw(l, i, ldl)], acc);
           v = -acc * inv_d;
         }
-        lin[k * kw + i] = v;
-        st.linv[sig * kw * kw + k * kw + i] = v;
+        lin[lsw(k, i, ldl)] = v;
+        st.linv[sig * kw * ldl + lsw(k, i, ldl)] = v;
       }
       if (gl == 0) {
         zv[k] = zk;
@@ -894,7 +905,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     if (act)
       for (int i = gl; i < kd; i += G) {
         double acc = 0.0;
-        for (int l = i; l < kd; l++) acc = fma(lin[l * kw + i], zv[l], acc);
+        for (int l = i; l < kd; l++) acc = fma(lin[lsw(l, i, ldl)], zv[l], acc);
         xv[i] = acc;
         out_coef[sig * kw + i] = acc;
       }
@@ -1175,8 +1186,8 @@ __global__ void __launch_bounds__(512) rescan_kernel(const YT *__restrict__ ys,
 
 
 // ---------------------------------------------------------------- tiled rescan
-// For large dictionaries (T*N >= 2^22: every group of the kernel above would
-// stream the whole fp64 dictionary from HBM) the queued rescans of one
+// For large dictionaries (every group of the kernel above would stream the
+// whole fp64 dictionary from HBM or L2; see rescan_tiled) the queued rescans of one
 // iteration are computed as the fp64 GEMM C = R D64^T over all queued
 // residuals R at once, tiled 64 signals x 128 atoms per CTA (8 x 8 register
 // blocking: 2 B of shared-memory traffic per FMA, i.e. FP64-pipe bound), with
@@ -1356,11 +1367,13 @@ struct TileRescan {
   }
 };
 
-bool rescan_tiled(int64_t t, int64_t n) {
+// Tiled when the dictionary is large, or mid-sized with long supports (the
+// queue then holds hundreds of signals per iteration); CDB_RESCAN=tile|group.
+bool rescan_tiled(int64_t t, int64_t n, int64_t k_max) {
   const char *m = getenv("CDB_RESCAN");
   if (m && !strcmp(m, "tile")) return true;
   if (m && !strcmp(m, "group")) return false;
-  return t * n >= (int64_t(1) << 22);
+  return t * n >= (int64_t(1) << 22) || (t * n >= (int64_t(1) << 20) && k_max >= 32);
 }
 
 cudaError_t tile_rescan_alloc(TileRescan &tr, int64_t p, int64_t t, int64_t n,
@@ -1508,7 +1521,7 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols_pad, 
 int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw) {
   const int64_t n_pad = (n + BK - 1) / BK * BK;
   const int64_t p_pad = (p + BM - 1) / BM * BM;
-  return p_pad * n_pad * 2 + p * kw * kw * 8 + p * kw * 8 + p * 8 * 5 + p * NCAND * 8 + p * 4 +
+  return p_pad * n_pad * 2 + p * kw * ((kw + 15) & ~int64_t(15)) * 8 + p * kw * 8 + p * 8 * 5 + p * NCAND * 8 + p * 4 +
          p * 8 * 3 + p * (3 * 8 * RS_SPLIT + 4) + 4 * 4096 + 21 * 256;
 }
 
@@ -1525,7 +1538,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   };
   TensorState st{};
   st.r16 = (__nv_bfloat16 *)take(p_pad * n_pad * 2);
-  st.linv = (double *)take(p * kw * kw * 8);
+  st.linv = (double *)take(p * kw * ((kw + 15) & ~int64_t(15)) * 8);
   st.z = (double *)take(p * kw * 8);
   st.rn2 = (double *)take(p * 8);
   st.yy = (double *)take(p * 8);
@@ -1588,7 +1601,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     const int c = atoi(cap);
     if (c > 0 && (unsigned)c < corr_grid) corr_grid = (unsigned)c;
   }
-  const int64_t ls_per_warp = (int64_t)sizeof(double) * (kw * kw + 5 * kw + n);
+  const int64_t ls_per_warp = (int64_t)sizeof(double) * (kw * ((kw + 15) & ~int64_t(15)) + 5 * kw + n);
   int ls_wpb = (int)((160 * 1024) / ls_per_warp);
   if (ls_wpb > 8) ls_wpb = 8;
   if (ls_wpb < 1) ls_wpb = 1;
@@ -1607,7 +1620,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   const unsigned ls_grid = (unsigned)((p + ls_wpb - 1) / ls_wpb);
   // grouped LS kernel: 8-lane groups (4 signals per warp) when the per-signal
   // state is small, whole warps otherwise; CDB_LS_LEGACY=1 forces ls_step
-  const int64_t grp_bytes = 8 * (kw * kw + 5 * kw);
+  const int64_t grp_bytes = 8 * (kw * ((kw + 15) & ~int64_t(15)) + 5 * kw);
   // lanes per signal in the grouped LS kernel: 16 measured best on cfg 1
   // (8: 10.3 M, 16: 10.9 M signals/s); whole warps when the state is large
   int lsg_g = 4 * 2 * grp_bytes <= 96 * 1024 ? 16 : 32;
@@ -1632,7 +1645,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     if ((e = set((const void *)ls_group_kernel<float, 32>)) != cudaSuccess) return e;
     if ((e = set((const void *)ls_group_kernel<double, 32>)) != cudaSuccess) return e;
   }
-  const bool tiled = rescan_tiled(t, n);
+  const bool tiled = rescan_tiled(t, n, a.k_max);
   TileRescan tr;
   if (tiled && (e = tile_rescan_alloc(tr, p, t, n, stream)) != cudaSuccess) return e;
   for (int it = 0; it < a.k_max; it++) {
