@@ -422,6 +422,7 @@ __device__ __forceinline__ double exact_corr(const double *__restrict__ d64,
 }
 
 constexpr uint32_t ST_RESCAN = 4u;  // pick needs the exact full rescan
+constexpr uint32_t ST_RESID = 8u;   // split mode: the next scan operand is still to be built
 
 // Append atom `bestj` (exact correlation cbest) to the signal's support:
 // Cholesky update through the Gram row, coefficients, stop test, and the
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     const YT *__restrict__ ys, const double *__restrict__ d64, const float *__restrict__ d32,
     const double *__restrict__ gram, int64_t p, int64_t t, int n, int64_t n_pad, int k_max,
     int kw, int iter, double c_err, double dmax, TensorState st, int64_t *out_sel,
-    double *out_coef, int64_t *out_count, int64_t *out_scans, int resume) {
+    double *out_coef, int64_t *out_count, int64_t *out_scans, int resume, int split) {
   constexpr int NG = 32 / G;
   extern __shared__ double lsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -935,8 +936,9 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
       act = false;
     }
     // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16
+    //      (split mode: left to resid_split_kernel, flagged ST_RESID)
     double rr = 0.0, sx = 0.0;
-    if (act) {
+    if (act && !split) {
 #pragma unroll
       for (int i0 = 0; i0 < (YM > 0 ? YM * G : n); i0 += 8 * G) {
         if (YM > 0 && i0 >= n) break;
@@ -991,11 +993,110 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     rr = gsum<G>(rr);
     sx = gsum<G>(sx);
     if (act && gl == 0) {
-      st.rt[sig] = sqrt(rr);
-      st.dr[sig] = 0x1p-24 * sx * dmax * 1.0000001;  // |(D64 - D32) x| bound
+      if (split) {
+        st.status[sig] |= ST_RESID;
+      } else {
+        st.rt[sig] = sqrt(rr);
+        st.dr[sig] = 0x1p-24 * sx * dmax * 1.0000001;  // |(D64 - D32) x| bound
+      }
       atomicAdd(st.active + iter, 1);
     }
     __syncwarp();
+  }
+}
+
+// Split-mode scan operand (large N): r~ = y - D32_S x -> bf16 for every signal
+// flagged ST_RESID, one CTA per signal -- 8 elements x 4 atom rows = 32 loads
+// in flight per thread, so the kd x N fp32 row stream runs near HBM speed
+// instead of at the LS kernel's occupancy (its per-signal L^{-1} state allows
+// only a few signals per SM).  Same arithmetic as the fused path.
+template <typename YT, int BT>
+__global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ ys,
+                                                          const float *__restrict__ d32, int64_t p,
+                                                          int64_t n, int64_t n_pad, int64_t kw,
+                                                          double dmax, TensorState st,
+                                                          const int64_t *out_sel,
+                                                          const double *out_coef,
+                                                          const int64_t *out_count) {
+  extern __shared__ double xsm[];
+  double *xv = xsm;                         // kw
+  int64_t *ssel = (int64_t *)(xv + kw);     // kw
+  __shared__ double red[2][BT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t sig = blockIdx.x; sig < p; sig += gridDim.x) {
+    if (!(st.status[sig] & ST_RESID)) continue;  // uniform across the CTA
+    const int kd = (int)out_count[sig];
+    for (int l = tid; l < kd; l += blockDim.x) {
+      xv[l] = out_coef[sig * kw + l];
+      ssel[l] = out_sel[sig * kw + l];
+    }
+    __syncthreads();
+    const YT *y = ys + sig * n;
+    double rr = 0.0;
+    for (int64_t i0 = 0; i0 < n; i0 += 8 * BT) {
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int64_t i = i0 + u * BT + tid;
+        acc[u] = i < n ? (double)y[i] : 0.0;
+      }
+      int l = 0;
+      for (; l + 3 < kd; l += 4) {
+        float v[4][8];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const float *row = d32 + ssel[l + q] * n;
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int64_t i = i0 + u * BT + tid;
+            v[q][u] = i < n ? __ldg(row + i) : 0.0f;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const double xl = xv[l + q];
+#pragma unroll
+          for (int u = 0; u < 8; u++) acc[u] = fma(-xl, (double)v[q][u], acc[u]);
+        }
+      }
+      for (; l < kd; l++) {
+        const float *row = d32 + ssel[l] * n;
+        const double xl = xv[l];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int64_t i = i0 + u * BT + tid;
+          if (i < n) acc[u] = fma(-xl, (double)__ldg(row + i), acc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int64_t i = i0 + u * BT + tid;
+        if (i < n) {
+          st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)acc[u]);
+          rr = fma(acc[u], acc[u], rr);
+        }
+      }
+    }
+    double sx = 0.0;
+    for (int l = tid; l < kd; l += blockDim.x) sx += fabs(xv[l]);
+    rr = warp_sum(rr);
+    sx = warp_sum(sx);
+    if (lane == 0) {
+      red[0][warp] = rr;
+      red[1][warp] = sx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < BT / 32; w++) {
+        a += red[0][w];
+        b += red[1][w];
+      }
+      st.rt[sig] = sqrt(a);
+      st.dr[sig] = 0x1p-24 * b * dmax * 1.0000001;  // |(D64 - D32) x| bound
+      st.status[sig] &= ~ST_RESID;
+    }
+    __syncthreads();
   }
 }
 
@@ -1646,6 +1747,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     if ((e = set((const void *)ls_group_kernel<double, 32>)) != cudaSuccess) return e;
   }
   const bool tiled = rescan_tiled(t, n, a.k_max);
+  // large N: build the scan operand in its own kernel (CDB_LS_SPLIT=0|1 overrides)
+  int split = n > 256 ? 1 : 0;
+  if (const char *v = getenv("CDB_LS_SPLIT")) split = atoi(v) ? 1 : 0;
   TileRescan tr;
   if (tiled && (e = tile_rescan_alloc(tr, p, t, n, stream)) != cudaSuccess) return e;
   for (int it = 0; it < a.k_max; it++) {
@@ -1677,45 +1781,45 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
             ls_group_kernel<float, 8><<<grid, 128, lsg_smem, stream>>>(
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
           else
             ls_group_kernel<double, 8><<<grid, 128, lsg_smem, stream>>>(
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
         } else if (lsg_g == 16 && n <= 256) {
           if (a.ys_f32)
             ls_group_kernel<float, 16, 16><<<grid, 128, lsg_smem, stream>>>(
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
           else
             ls_group_kernel<double, 16, 16><<<grid, 128, lsg_smem, stream>>>(
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
         } else if (lsg_g == 16) {
           if (a.ys_f32)
             ls_group_kernel<float, 16><<<grid, 128, lsg_smem, stream>>>(
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
           else
             ls_group_kernel<double, 16><<<grid, 128, lsg_smem, stream>>>(
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
         } else {
           if (a.ys_f32)
             ls_group_kernel<float, 32><<<grid, 128, lsg_smem, stream>>>(
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
           else
             ls_group_kernel<double, 32><<<grid, 128, lsg_smem, stream>>>(
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
-                resume);
+                resume, split);
         }
       } else {
         const unsigned grid = resume ? (unsigned)a.num_sms : ls_grid;
@@ -1728,6 +1832,32 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
               (const double *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
               a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
       }
+      note_launch();
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (split && lsg_smem > 0 && it + 1 < a.k_max) {  // the next scan's operand
+      ProfScope _ps("ls_resid", stream);
+      const size_t xs = 16 * (size_t)kw;
+      // threads per signal: N / 8 (8 elements each), 64..256
+      const int bt = n >= 2048 ? 256 : (n >= 1024 ? 128 : 64);
+      const unsigned g = (unsigned)(a.num_sms * (2048 / bt));
+#define CDB_RESID(BT_)                                                                          \
+  if (a.ys_f32)                                                                                 \
+    resid_split_kernel<float, BT_><<<g, BT_, xs, stream>>>((const float *)a.ys, a.d32, p, n,    \
+                                                           n_pad, kw, a.dmax, st, a.out_sel,    \
+                                                           a.out_coef, a.out_count);            \
+  else                                                                                          \
+    resid_split_kernel<double, BT_><<<g, BT_, xs, stream>>>((const double *)a.ys, a.d32, p, n,  \
+                                                            n_pad, kw, a.dmax, st, a.out_sel,   \
+                                                            a.out_coef, a.out_count);
+      if (bt == 256) {
+        CDB_RESID(256)
+      } else if (bt == 128) {
+        CDB_RESID(128)
+      } else {
+        CDB_RESID(64)
+      }
+#undef CDB_RESID
       note_launch();
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }

@@ -107,3 +107,15 @@ def test_tiled_rescan_matches_oracle(monkeypatch):
         rescans += N.last_run_info()[2]
         _check(ref, got, d, ys, eps, "tensor")
     assert rescans > 0
+
+
+def test_split_residual_matches_oracle(monkeypatch):
+    """The tensor engine's split-mode scan operand (resid_split_kernel, the
+    large-N path), forced on shapes below its default threshold."""
+    monkeypatch.setenv("CDB_LS_SPLIT", "1")
+    for n, t, k, p in ((129, 513, 16, 96), (256, 1000, 20, 64), (33, 64, 12, 64)):
+        d, ys = _problem(n, t, k, p, n * t + 3, False)
+        eps = 1e-3 * np.linalg.norm(ys, axis=1)
+        ref = _oracle(d, ys, k, eps)
+        got = D.omp_batch_raw(D.DeviceDictionary(d), ys, p, k, eps, None, "tensor")
+        _check(ref, got, d, ys, eps, "tensor")
