@@ -160,6 +160,27 @@ cdb_status cdb_omp_batch_coded(const cdb_dictionary *dict, const double *ys, int
                                int64_t *out_scans, uint8_t *out_flag, void *stream);
 
 /*
+ * K-SVD dictionary-update stage (SURVEY §8 row f1 follow-on; crossdict
+ * learn._update_stage, learn.py:169-199): sequential rank-one refits of the
+ * T atoms.  y_rows / e_rows: M x N fp64 signal and residual rows (e = y - D X
+ * on entry, updated in place); d_rows: T x N atom rows (updated in place);
+ * the code matrix X as a per-atom CSR: the users of atom j are
+ * atom_sig[atom_ptr[j] .. atom_ptr[j+1]) (ascending signal ids) with values
+ * vals[...] (updated in place; dead atoms' entries zeroed); nnz =
+ * atom_ptr[T]; max_users = max_j |users_j|.  An atom with fewer than
+ * `threshold` users is re-seeded from the not-yet-taken signal with the
+ * largest residual norm; the others take the leading singular triple of
+ * E_j (sign: largest-magnitude entry of the atom positive; the reference's
+ * LAPACK sign is arbitrary).  *replaced = number of re-seeded atoms.
+ * N <= ~160 (the Gram matrix of the update lives in shared memory up to
+ * there, in global memory beyond).  Host or device pointers.
+ */
+cdb_status cdb_ksvd_update(int64_t n, int64_t m, int64_t t, const double *y_rows, double *e_rows,
+                           double *d_rows, const int64_t *atom_ptr, const int64_t *atom_sig,
+                           double *vals, int64_t nnz, int64_t max_users, int64_t threshold,
+                           int64_t *replaced, void *stream);
+
+/*
  * Ragged block-restricted batched OMP: signal p may use its first nb[p]
  * block ids of row p of blocks (P x nb_max, ascending within the used
  * prefix); budget min(k_max, nb[p]*q, N) per signal; outputs k_max wide.

@@ -127,6 +127,30 @@ struct OutArr {
   }
 };
 
+// An array read and written on the device: copied in, and back when host-resident.
+struct IoArr {
+  void *host = nullptr;
+  void *dev = nullptr;
+  size_t bytes = 0;
+  DevBuf buf;
+  cudaError_t bind(void *p, size_t nbytes, cudaStream_t s) {
+    bytes = nbytes;
+    if (!p || is_device_ptr(p)) {
+      dev = p;
+      return cudaSuccess;
+    }
+    host = p;
+    cudaError_t e = buf.alloc(nbytes, s);
+    if (e != cudaSuccess) return e;
+    dev = buf.ptr;
+    return cudaMemcpyAsync(dev, p, nbytes, cudaMemcpyHostToDevice, s);
+  }
+  cudaError_t finish(cudaStream_t s) {
+    if (!host || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s);
+  }
+};
+
 struct Outs {
   OutArr sel, coef, count, rnorm, scans, flag;
   cudaError_t bind(int64_t p, int64_t kw, int64_t *s, double *c, int64_t *cnt, double *rn,
@@ -1353,6 +1377,60 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   CDB_CUDA(hi.finish(st));
   CDB_CUDA(cudaStreamSynchronize(st));
   tm.finish(step_ms);
+  return CDB_OK;
+}
+
+cdb_status cdb_ksvd_update(int64_t n, int64_t m, int64_t t, const double *y_rows, double *e_rows,
+                           double *d_rows, const int64_t *atom_ptr, const int64_t *atom_sig,
+                           double *vals, int64_t nnz, int64_t max_users, int64_t threshold,
+                           int64_t *replaced, void *stream) {
+  if (n < 1 || m < 1 || t < 1 || nnz < 0 || max_users < 0 || max_users > m || !y_rows ||
+      !e_rows || !d_rows || !atom_ptr || (nnz > 0 && (!atom_sig || !vals)) || !replaced)
+    return fail(CDB_ERR_ARG, "bad K-SVD update arguments");
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  InArr y_in, p_in, s_in;
+  IoArr e_io, d_io, v_io;
+  OutArr r_out;
+  CDB_CUDA(y_in.bind(y_rows, sizeof(double) * m * n, st));
+  CDB_CUDA(p_in.bind(atom_ptr, sizeof(int64_t) * (t + 1), st));
+  CDB_CUDA(s_in.bind(atom_sig, sizeof(int64_t) * (nnz > 0 ? nnz : 1), st));
+  CDB_CUDA(e_io.bind(e_rows, sizeof(double) * m * n, st));
+  CDB_CUDA(d_io.bind(d_rows, sizeof(double) * t * n, st));
+  CDB_CUDA(v_io.bind(vals, sizeof(double) * (nnz > 0 ? nnz : 1), st));
+  CDB_CUDA(r_out.bind(replaced, sizeof(int64_t), st));
+  const int64_t budget = (200 * 1024) / 8 - 4 * n - 32 - 33 * n;  // see ksvd_update_smem
+  if (budget < 64) return fail(CDB_ERR_ARG, "signal dimension too large for the update kernel");
+  const int64_t smem_b = n * n <= budget ? n * n : budget;
+  DevBuf ej, bg, taken;
+  CDB_CUDA(ej.alloc(sizeof(double) * (max_users > 0 ? max_users : 1) * n, st));
+  CDB_CUDA(bg.alloc(n * n > smem_b ? sizeof(double) * n * n : 16, st));
+  CDB_CUDA(taken.alloc(sizeof(uint32_t) * ((m + 31) / 32), st));
+  CDB_CUDA(cudaMemsetAsync(taken.ptr, 0, sizeof(uint32_t) * ((m + 31) / 32), st));
+  cdb::KsvdArgs a{};
+  a.y = (const double *)y_in.dev;
+  a.e = (double *)e_io.dev;
+  a.d = (double *)d_io.dev;
+  a.ptr = (const int64_t *)p_in.dev;
+  a.sig = (const int64_t *)s_in.dev;
+  a.val = (double *)v_io.dev;
+  a.n = n;
+  a.m = m;
+  a.t = t;
+  a.threshold = threshold;
+  a.smem_b = smem_b;
+  a.ej = ej.as<double>();
+  a.bglob = bg.as<double>();
+  a.taken = taken.as<uint32_t>();
+  a.replaced = (int64_t *)r_out.dev;
+  CDB_CUDA(cdb::launch_ksvd_update(a, cdb::ksvd_update_smem(n, smem_b), st));
+  CDB_CUDA(e_io.finish(st));
+  CDB_CUDA(d_io.finish(st));
+  CDB_CUDA(v_io.finish(st));
+  CDB_CUDA(r_out.finish(st));
+  CDB_CUDA(cudaStreamSynchronize(st));
   return CDB_OK;
 }
 

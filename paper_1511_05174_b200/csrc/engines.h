@@ -175,4 +175,22 @@ cudaError_t launch_to_f32(const double *d64, int64_t count, float *d32, cudaStre
 cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids,
                                      int *count, cudaStream_t stream);
 
+// K-SVD update stage (ksvd_engine.cu): one persistent CTA over the atoms.
+struct KsvdArgs {
+  const double *y;        // M x N signal rows
+  double *e;              // M x N residual rows (in/out)
+  double *d;              // T x N atom rows (in/out)
+  const int64_t *ptr;     // T + 1: users of atom j are sig[ptr[j] .. ptr[j+1])
+  const int64_t *sig;     // ascending signal ids per atom
+  double *val;            // code entries x[j, sig] (in/out)
+  int64_t n, m, t, threshold;
+  int64_t smem_b;         // doubles of shared memory for the Gram matrix
+  double *ej;             // scratch: max users x N
+  double *bglob;          // scratch: N x N (Gram matrix beyond smem_b)
+  uint32_t *taken;        // M bits, zeroed
+  int64_t *replaced;      // out
+};
+size_t ksvd_update_smem(int64_t n, int64_t smem_b);
+cudaError_t launch_ksvd_update(const KsvdArgs &a, size_t smem, cudaStream_t stream);
+
 }  // namespace cdb

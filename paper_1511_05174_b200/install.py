@@ -8,7 +8,8 @@ reference imported them by name -- to this package's B200 implementations:
   zero_tree_many_arrays}``                                    (crossscale.py:169-312)
 * ``crossdict.patchwork.{extract_patches, aggregate_patches}`` (patchwork.py:58-122)
 * ``crossdict.learn._code_stage`` (learn.py:240-262): K-SVD's coding stage as
-  one ragged block-restricted device call
+  one ragged block-restricted device call, and ``crossdict.learn._update_stage``
+  (learn.py:169-199): the rank-one dictionary refits in one device call
 * ``crossdict.pipelines._recover_operator`` (pipelines.py:258-322): operator
   recovery (masks, mosaics, temporal codes, angular sampling) with every
   patch coded in one coded-rows device call per step
@@ -46,6 +47,7 @@ _FUNCS = {
     "extract_patches": _pw.extract_patches,
     "aggregate_patches": _pw.aggregate_patches,
     "_code_stage": _learn.code_stage,  # crossdict.learn only (learn.py:240-262)
+    "_update_stage": _learn.update_stage,  # crossdict.learn only (learn.py:169-199)
     "_recover_operator": _pipelines.recover_operator_stage,  # crossdict.pipelines only
 }
 _MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
