@@ -398,6 +398,7 @@ def bench_ours(args):
                          f"(oracle/omp_oracle.c restating crossdict's kernel, {threads} threads)"}
 
     ends = bench_pipeline_ends(peaks) if rank == 0 and world == 1 else None
+    ksvd = bench_ksvd_update(args.no_cpu) if rank == 0 and world == 1 else None
 
     if rank == 0:
         line = {
@@ -419,6 +420,7 @@ def bench_ours(args):
             "kernels_full_ms_per_step": {k: v[0] / args.steps for k, v in prof_full.items()},
             "cpu_baseline": cpu,
             "pipeline_ends": ends,
+            "ksvd_update": ksvd,
             "e2e": {"value": world * P * args.steps / e2e_total, "unit": "signals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "clocks": clk,
@@ -428,6 +430,39 @@ def bench_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_ksvd_update(no_cpu=False):
+    """SURVEY §8 row f1 follow-on: K-SVD's dictionary-update stage
+    (learn._update_stage) on the device -- one call through the public
+    learn.update_stage (host E = Y - D X, transfers, the device atom loop) --
+    beside the oracle's restatement of the reference stage (numpy + LAPACK,
+    the box's host) on the same seeded problem: N=64, T=256, M=20000, K=8,
+    two dead atoms."""
+    import time as _t
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle"))
+    import ksvd_oracle as KO
+    from paper_1511_05174_b200 import _native as NN
+    from paper_1511_05174_b200.learn import update_stage
+    y, d, x = KO.problem(64, 256, 20000, 8, 7, (3, 4))
+    update_stage(y, d.copy(), x.copy(), 2)  # warm-up
+    d1, x1 = d.copy(), x.copy()
+    NN.profile_enable(True)
+    t0 = _t.perf_counter()
+    rep = update_stage(y, d1, x1, 2)[0]
+    t1 = _t.perf_counter()
+    prof = NN.profile_read()
+    NN.profile_enable(False)
+    out = {"workload": "N=64, T=256, M=20000 signals, K=8, 2 dead atoms (seeded)",
+           "replaced": rep, "call_ms": (t1 - t0) * 1e3,
+           "kernel_ms": prof.get("ksvd_update", (0.0,))[0]}
+    if not no_cpu:
+        d2, x2 = d.copy(), x.copy()
+        t2 = _t.perf_counter()
+        KO.update_stage(y, d2, x2, 2)
+        out["cpu_reference_ms"] = (_t.perf_counter() - t2) * 1e3
+        out["cpu_kind"] = "port (oracle/ksvd_oracle.py: the reference stage's numpy/LAPACK calls)"
+    return out
 
 
 def bench_pipeline_ends(peaks, reps=3):

@@ -36,6 +36,7 @@ METRICS = {
 # kernel-name fragment -> profiler tag used by bench.py (csrc ProfScope names)
 TAGS = {
     "resident_omp": "resident_step1",
+    "resident_mma": "resident_step1",
     "gram_omp": "gram_step2",
     "alpha0_warp": "route_alpha0",
     "downsample": "downsample",
