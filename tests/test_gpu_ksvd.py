@@ -49,3 +49,22 @@ def test_update_stage_matches_oracle(n, t, m, k, dead, thr):
     d1, x1 = d.copy(), x.copy()
     rep, e = KO.update_stage(y, d1, x1, thr)
     _compare(y, d, x, thr, d1, x1, e, rep)
+
+
+def test_update_stage_every_atom_dead():
+    """threshold above every atom's user count: all atoms re-seeded, each from
+    a different worst-coded signal (learn.py:179-191), codes zeroed."""
+    y, d, x = KO.problem(12, 10, 60, 2, 5)
+    d1, x1 = d.copy(), x.copy()
+    rep, e = KO.update_stage(y, d1, x1, 10 ** 6)
+    _compare(y, d, x, 10 ** 6, d1, x1, e, rep)
+    assert rep == 10
+
+
+def test_update_stage_zero_codes():
+    """An all-zero code matrix: E = Y, every atom dead at threshold 1."""
+    y, d, x = KO.problem(9, 6, 40, 2, 6)
+    x[:] = 0.0
+    d1, x1 = d.copy(), x.copy()
+    rep, e = KO.update_stage(y, d1, x1, 1)
+    _compare(y, d, x, 1, d1, x1, e, rep)

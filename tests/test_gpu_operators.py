@@ -132,3 +132,25 @@ def test_recover_operator_stage_fills_reference_metrics():
     assert np.array_equal(met.residual_norms, g["resid"])
     assert met.flagged_patches == int(g["flagged"]) and met.patch_count == g["resid"].size
     np.testing.assert_allclose(np.asarray(est), g["estimate"], rtol=0, atol=1e-12)
+
+
+def test_angular_zero_tree_vs_oracle():
+    """Angular sampling with zero-tree coding (the view axes coarsened by 1)."""
+    rng = np.random.default_rng(21)
+    spatial, grid, kept = (7, 6), (2, 2), np.array([1, 4])
+    patch = (4, 4, 2, 2)
+    n = int(np.prod(patch))
+    fac = (2, 2, 1, 1)
+    dl = rng.standard_normal((n // 4, 10))
+    dh = rng.standard_normal((n, 30))
+    g = dict(kind="angular-sample", view_grid=np.array(grid), kept=kept,
+             sig_shape=np.array(spatial + grid), patch=np.array(patch),
+             stride=np.array((3, 2, 1, 1)), meas=rng.standard_normal(spatial + (kept.size,)),
+             method="zerotree", d_low=dl / np.linalg.norm(dl, axis=0),
+             d_high=dh / np.linalg.norm(dh, axis=0), factors=np.array(fac), k_low=3, k_high=5)
+    ref = OO.recover(g, rel=1e-3)
+    est, met, _ = _run(g, rel=1e-3)
+    assert met.flagged_patches == ref["flagged"]
+    assert (met.scan_count_step1, met.scan_count_step2) == (ref["scans1"], ref["scans2"])
+    assert np.array_equal(met.residual_norms, ref["resid"])
+    np.testing.assert_allclose(np.asarray(est), ref["estimate"], rtol=0, atol=1e-10)
