@@ -1,5 +1,6 @@
 """BASELINE configs at their FULL sizes, checked through size-independent
-properties (the CPU oracle cannot run them whole): zero-tree nesting, the
+properties (the CPU oracle cannot run them whole) -- configs 0-4, cfg 4 at one
+GPU's shard of its 1M signals: zero-tree nesting, the
 reference's scan-count formula (pursuit.py:18-20), the stop rule, residual
 consistency and least-squares optimality on samples, and the parity contract
 against the oracle on a seeded random subset."""
@@ -160,3 +161,99 @@ def test_pipelined_host_buffers_match_device_buffers(kind):
     for a, b in pairs:
         for k in ("sel", "counts", "scans", "alpha", "rnorm"):
             assert np.array_equal(a[k], b[k]), k
+
+
+# configs 2-4 at their per-GPU sizes (cfg 4: one of 8 shards of 1M); oracle
+# subsets sized so the CPU restatement finishes in seconds
+BIG = {2: dict(p=None, sub_zt=96, sub_full=24), 3: dict(p=None, sub_zt=96, sub_full=48),
+       4: dict(p=125000, sub_zt=32, sub_full=4)}
+
+
+def _fast_signals(ci, count, seed=0):
+    """Signals with the BASELINE generator's distribution (K distinct parents,
+    one child each, N(0,1) coefficients, noise sigma; Phi for the CS config),
+    built on the device -- the seeded stream of workloads.signals takes
+    minutes at cfg 4's full size.  Returned as fp32-exact fp64 rows."""
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    rng = np.random.default_rng([seed, 77, ci])
+    parents = np.argpartition(rng.random((count, w.t_low)), w.k, axis=1)[:, : w.k]
+    atoms = torch.from_numpy(parents * w.q + rng.integers(0, w.q, size=(count, w.k))).cuda()
+    coefs = torch.from_numpy(rng.standard_normal((count, w.k))).cuda()
+    dh = torch.from_numpy(np.array(d.high_t)).cuda()
+    x = torch.zeros((count, w.n_high), dtype=torch.float64, device="cuda")
+    for j in range(w.k):
+        x += coefs[:, j, None] * dh[atoms[:, j]]
+    if w.measurements:
+        x = x @ torch.from_numpy(np.array(d.phi)).cuda().T
+    x += w.sigma * torch.from_numpy(rng.standard_normal(tuple(x.shape))).cuda()
+    return x.float().double().cpu().numpy()
+
+
+def _nested(low_sel, low_cnt, high_sel, high_cnt, q):
+    k1, k2 = low_sel.shape[1], high_sel.shape[1]
+    ok = True
+    for s in range(0, low_sel.shape[0], 20000):
+        ls, hs = low_sel[s:s + 20000], high_sel[s:s + 20000]
+        lv = np.arange(k1)[None, :] < low_cnt[s:s + 20000, None]
+        hv = np.arange(k2)[None, :] < high_cnt[s:s + 20000, None]
+        par = np.where(hv, hs // q, -7)
+        hit = ((par[:, :, None] == np.where(lv, ls, -9)[:, None, :]).any(axis=2)) | ~hv
+        ok &= bool(hit.all())
+    return ok
+
+
+@pytest.mark.parametrize("ci", [2, 3, 4])
+def test_zero_tree_full_size_big(ci):
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    P = BIG[ci]["p"] or w.signals
+    ys = _fast_signals(ci, P)
+    phi = bool(w.measurements)
+    lo_t, hi_t = (d.e_low_t, d.e_high_t) if phi else (d.low_t, d.high_t)
+    k1 = min(w.k, w.n_signal, w.t_low) if phi else w.k
+    low, high, _ = D.zero_tree_raw(D.device_dictionary(lo_t), D.device_dictionary(hi_t),
+                                   None if phi else w.fine_shape, None if phi else w.factors,
+                                   ys.astype(np.float32), P, k1, w.k, W.REL_TOL, phi, "auto")
+    low, high = _host(low), _host(high)
+    assert _nested(low["sel"], low["counts"], high["sel"], high["counts"], w.q)
+    assert np.array_equal(low["scans"], _scan_formula(w.t_low, low["counts"]))
+    nbq = low["counts"].astype(np.int64) * w.q
+    c2 = high["counts"].astype(np.int64)
+    assert np.array_equal(high["scans"], nbq * c2 - c2 * (c2 - 1) // 2)
+    eps2 = W.REL_TOL * np.linalg.norm(ys, axis=1)
+    _check_stop(high, eps2, np.minimum(np.minimum(w.k, nbq), ys.shape[1]))
+    rng = np.random.default_rng(20 + ci)
+    idx = np.sort(rng.choice(P, size=BIG[ci]["sub_zt"], replace=False))
+    _check_ls(hi_t, ys, high, eps2, idx[:64])
+    if phi:
+        rl, rh = O.zero_tree_phi_many(lo_t, hi_t, k1, w.k, ys[idx], rel_tol=W.REL_TOL, nthreads=8)
+    else:
+        rl, rh = O.zero_tree_many_arrays(lo_t, hi_t, w.fine_shape, w.factors, w.k, w.k, ys[idx],
+                                         rel_tol=W.REL_TOL, nthreads=8)
+    same1 = np.mean([np.array_equal(low["sel"][p], rl["sel"][i]) for i, p in enumerate(idx)])
+    assert same1 > 0.95
+    agree = np.mean([np.array_equal(high["sel"][p], rh["sel"][i]) for i, p in enumerate(idx)])
+    assert agree > 0.9
+
+
+@pytest.mark.parametrize("ci", [2, 3, 4])
+def test_full_omp_full_size_big(ci):
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    P = BIG[ci]["p"] or w.signals
+    ys = _fast_signals(ci, P, 1)
+    hi_t = d.e_high_t if w.measurements else d.high_t
+    eps = W.REL_TOL * np.linalg.norm(ys, axis=1)
+    sol = _host(D.omp_batch_raw(D.device_dictionary(hi_t), ys.astype(np.float32), P, w.k, eps,
+                                None, "auto"))
+    assert np.array_equal(sol["scans"], _scan_formula(w.t_high, sol["counts"]))
+    _check_stop(sol, eps, w.k)
+    rng = np.random.default_rng(30 + ci)
+    idx = np.sort(rng.choice(P, size=BIG[ci]["sub_full"], replace=False))
+    _check_ls(hi_t, ys, sol, eps, idx)
+    ref = O.omp_many_arrays(hi_t, ys[idx], w.k, rel_tol=W.REL_TOL, nthreads=8)
+    got = {k: v[idx] for k, v in sol.items()}
+    got["flag"] = got["flag"].astype(bool)
+    rep = compare(ref, got, hi_t, ys[idx], eps[idx])
+    assert not rep["bad"], rep["bad"][:3]
