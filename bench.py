@@ -245,9 +245,17 @@ def bench_ours(args):
     from paper_1511_05174_b200 import device as D
 
     rank, world, local = dist_env()
+    # CDB_BENCH_SMOKE=1: launcher smoke test on a box with fewer GPUs than ranks
+    # (ranks share devices round-robin, gloo process group; timings meaningless)
+    smoke = os.environ.get("CDB_BENCH_SMOKE") == "1"
+    if smoke:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if smoke:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ci = args.config
     w = W.CONFIGS[ci]
     P = args.signals or w.signals
