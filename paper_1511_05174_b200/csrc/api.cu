@@ -201,6 +201,7 @@ cdb_status device_info(DevInfo &di) {
 }
 
 constexpr int64_t kGramSmemLimit = 100 * 1024;       // per-warp smem for H in smem
+constexpr int64_t kGramPreferBytes = 24 * 1024;      // auto: gram over resident below this
 constexpr int64_t kScratchBudget = int64_t(4) << 30;  // per-call global scratch cap
 
 // Run the exact engine over `count` signals (all, or the ids in sig_ids).
@@ -308,6 +309,14 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
                           di, st);
 }
 
+// The Gram engine beats the resident one when its per-signal state is small
+// (>= ~13 signals per SM: cfg 0 full 32.7 vs 28.3 M/s, both steps of cfg 0's
+// zero-tree); with a larger H (cfg 1 step 1: 32 KB per signal) resident wins.
+bool gram_preferred(const cdb_dictionary *d, int64_t max_cands, int64_t kw) {
+  return d->gram && max_cands > 0 && max_cands <= 512 && kw <= 64 &&
+         cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramPreferBytes;
+}
+
 // The OMP driver shared by every entry point: picks the engine.
 //   exact  : any problem (reference restatement)
 //   gram   : Gram matrix available; H (max_cands x k) kept in smem when it fits
@@ -322,8 +331,9 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit;
   const bool resident = cdb::resident_fits(d->n, d->t, kw, max_cands, di.smem_optin);
   if (engine == CDB_ENGINE_RESIDENT && !resident) engine = CDB_ENGINE_AUTO;  // a preference
+  const bool gram_small = gram_preferred(d, max_cands, kw);
   if (engine == CDB_ENGINE_AUTO) {
-    if (resident && max_cands > 0)
+    if (resident && max_cands > 0 && !gram_small)
       engine = CDB_ENGINE_RESIDENT;
     else if (!d->gram || max_cands <= 0)
       engine = CDB_ENGINE_EXACT;
@@ -1302,7 +1312,8 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
   DevBuf alpha0, rwork;
   const bool high_resident =
       cdb::resident_fits(high->n, high->t, k_high, k1 * q, di.smem_optin) &&
-      (engine == CDB_ENGINE_AUTO || engine == CDB_ENGINE_RESIDENT);
+      (engine == CDB_ENGINE_RESIDENT ||
+       (engine == CDB_ENGINE_AUTO && !gram_preferred(high, k1 * q, k_high)));
   const bool use_route = high->gram && !high_resident && engine != CDB_ENGINE_EXACT &&
                          high->t / q == low->t && 8 * q * n <= 192 * 1024 && k1 < 65536 &&
                          (q == 1 || q == 2 || q == 4 || q == 8 || q == 16);

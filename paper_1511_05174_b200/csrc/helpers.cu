@@ -397,7 +397,9 @@ __global__ void __launch_bounds__(128) alpha0_warp_kernel(
   // pairs are loaded while the current two are coded
   const int64_t per = (b - a + nwarps - 1) / nwarps;
   const int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
-  auto load_row = [&](int64_t pr, float (&yv)[NPL]) {
+  // signal values are staged in the input type: fp32 rows stay fp32 (exact),
+  // fp64 rows are never rounded
+  auto load_row = [&](int64_t pr, YT (&yv)[NPL]) {
     const YT *y = ys + (pr >> 16) * n;
 #pragma unroll
     for (int v = 0; v < NV; v++) {
@@ -414,12 +416,12 @@ __global__ void __launch_bounds__(128) alpha0_warp_kernel(
         yv[v * 2 + 1] = f.y;
       } else {
 #pragma unroll
-        for (int e = 0; e < VW; e++) yv[v * VW + e] = (float)y[i + e];
+        for (int e = 0; e < VW; e++) yv[v * VW + e] = y[i + e];
       }
     }
   };
   // code two pairs at once: 2 CH independent accumulation chains
-  auto code2 = [&](int64_t pra, const float (&ya)[NPL], int64_t prb, const float (&yb)[NPL],
+  auto code2 = [&](int64_t pra, const YT (&ya)[NPL], int64_t prb, const YT (&yb)[NPL],
                    bool second) {
     double acc[2 * CH];
 #pragma unroll
@@ -445,13 +447,13 @@ __global__ void __launch_bounds__(128) alpha0_warp_kernel(
   for (int64_t e0 = wa; e0 < wb; e0 += 32) {
     const int m = wb - e0 < 32 ? (int)(wb - e0) : 32;
     const int64_t mine = lane < m ? pairs[e0 + lane] : 0;
-    float ya[NPL], yb[NPL];
+    YT ya[NPL], yb[NPL];
     int64_t pa = __shfl_sync(CDB_FULL_MASK, (long long)mine, 0);
     int64_t pb = __shfl_sync(CDB_FULL_MASK, (long long)mine, 1 < m ? 1 : 0);
     load_row(pa, ya);
     load_row(pb, yb);
     for (int j = 0; j < m; j += 2) {
-      float ca[NPL], cb[NPL];
+      YT ca[NPL], cb[NPL];
 #pragma unroll
       for (int t = 0; t < NPL; t++) {
         ca[t] = ya[t];
