@@ -46,9 +46,12 @@ __host__ __device__ __forceinline__ int hslot(int j) {
 // (k_width each), then the H rows -- whose first n + S doubles stage y and
 // alpha0 while the signal starts (H in global memory: staging only).
 __host__ __device__ inline int64_t gram_hs(int64_t s) {
-  int64_t u = 1;
-  while (32 * u < s) u *= 2;
-  return 32 * u;
+  // U = 6 and 12 (even: the paired layout) trim H for S in (128, 192] and
+  // (256, 384] -- e.g. cfg 3's step 2 (S = 384): 74 instead of 98 KB per signal
+  const int64_t us[7] = {1, 2, 4, 6, 8, 12, 16};
+  for (int i = 0; i < 7; i++)
+    if (32 * us[i] >= s) return 32 * us[i];
+  return 32 * 16;
 }
 __host__ __device__ inline int64_t gram_region_doubles(int64_t s, int64_t kw, int64_t n,
                                                        bool h_in_smem) {
@@ -345,7 +348,9 @@ cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int u, int h_in_sm
     case 1: return launch_gram_tu<YT, 1>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
     case 2: return launch_gram_tu<YT, 2>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
     case 4: return launch_gram_tu<YT, 4>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 6: return launch_gram_tu<YT, 6>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
     case 8: return launch_gram_tu<YT, 8>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+    case 12: return launch_gram_tu<YT, 12>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
     case 16: return launch_gram_tu<YT, 16>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
   }
   return cudaErrorInvalidValue;
@@ -370,8 +375,7 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   const int64_t per_warp = gram_total_smem(s, kw, n, h_in_smem);
   if (per_warp > max_smem_per_block) return cudaErrorInvalidValue;
   if (kw > 64 || s > 512) return cudaErrorInvalidValue;
-  int u = 1;
-  while (32 * u < s) u *= 2;
+  const int u = (int)(gram_hs(s) / 32);
   const int cap = u <= 8 ? 16 : 8;
   int wpb = (int)(max_smem_per_block / per_warp);
   if (wpb > cap) wpb = cap;

@@ -119,3 +119,21 @@ def test_split_residual_matches_oracle(monkeypatch):
         ref = _oracle(d, ys, k, eps)
         got = D.omp_batch_raw(D.DeviceDictionary(d), ys, p, k, eps, None, "tensor")
         _check(ref, got, d, ys, eps, "tensor")
+
+
+@pytest.mark.parametrize("nb,q,k", [(15, 12, 14), (28, 12, 20), (9, 20, 12)])
+def test_gram_candidate_widths(nb, q, k):
+    """Block-restricted sets whose width lands on the Gram engine's U = 6 and
+    U = 12 H layouts (S in (128, 192] and (256, 384]) and U = 8 (S = 180)."""
+    n, p = 64, 40
+    t = 40 * q
+    d, ys = _problem(n, t, k, p, nb * q + k, False)
+    rng = np.random.default_rng(nb)
+    blocks = np.sort(np.stack([rng.choice(t // q, size=nb, replace=False) for _ in range(p)]), 1)
+    allowed = (blocks[:, :, None] * q + np.arange(q)[None, None, :]).reshape(p, -1)
+    k_max = min(k, nb * q, n)
+    eps = 1e-3 * np.linalg.norm(ys, axis=1)
+    ref = _oracle(d, ys, k_max, eps, allowed)
+    got = D.omp_batch_blocked_raw(D.DeviceDictionary(d), ys, p, k_max, eps,
+                                  np.ascontiguousarray(blocks), q, "gram")
+    _check(ref, got, d, ys, eps, "gram", allowed)
