@@ -470,6 +470,24 @@ def bench_ksvd_update(no_cpu=False):
         KO.update_stage(y, d2, x2, 2)
         out["cpu_reference_ms"] = (_t.perf_counter() - t2) * 1e3
         out["cpu_kind"] = "port (oracle/ksvd_oracle.py: the reference stage's numpy/LAPACK calls)"
+    # whole training iterations (row f1): learn.ksvd, codes / residual / refits on the device
+    from paper_1511_05174_b200 import learn as LL
+    cfg = LL.TrainConfig(256, 8, iterations=3, seed=0)
+    LL.ksvd(y[:, :2000], LL.TrainConfig(256, 8, iterations=1, seed=0))  # warm-up
+    t3 = _t.perf_counter()
+    _, _, rep_d = LL.ksvd(y, cfg)
+    train = {"workload": "K-SVD, N=64, T=256, M=20000, K=8, 3 iterations (seeded data)",
+             "device_s": _t.perf_counter() - t3,
+             "objective_per_iteration": [float(v) for v in rep_d.objective_per_iteration]}
+    if not no_cpu:
+        thr = len(os.sched_getaffinity(0))
+        t4 = _t.perf_counter()
+        _, _, _, post, _ = KO.train(y, 256, 8, 3, seed=0, nthreads=thr)
+        train["cpu_reference_s"] = _t.perf_counter() - t4
+        train["cpu_kind"] = (f"port (oracle: C coding kernel on {thr} threads + the reference "
+                             "update stage's numpy/LAPACK calls)")
+        train["cpu_objective_per_iteration"] = [float(v) for v in post]
+    out["training"] = train
     return out
 
 

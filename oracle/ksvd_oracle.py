@@ -79,3 +79,97 @@ def problem(n, t, m, k, seed, dead=()):
     d = dt + 0.1 * rng.standard_normal((n, t))
     d /= np.linalg.norm(d, axis=0)
     return y, d, x
+
+
+_INIT_COHERENCE_CAP = 0.7
+_DUPLICATE_COHERENCE = 0.99
+
+
+def init_atoms(y, t, init, rng):
+    """learn._init_atoms (learn.py:98-128)."""
+    n, m = y.shape
+    if init == "random-unit":
+        g = rng.standard_normal((n, t))
+        return g / np.linalg.norm(g, axis=0)
+    norms = np.linalg.norm(y, axis=0)
+    order = rng.permutation(np.flatnonzero(norms > 0))
+    atoms = np.empty((t, n))
+    filled = 0
+    used = np.zeros(order.size, dtype=bool)
+    for pos, c in enumerate(order):
+        v = y[:, c] / norms[c]
+        if filled and np.abs(atoms[:filled] @ v).max() > _INIT_COHERENCE_CAP:
+            continue
+        atoms[filled] = v
+        filled += 1
+        used[pos] = True
+        if filled == t:
+            break
+    for pos, c in enumerate(order):
+        if filled == t:
+            break
+        if not used[pos]:
+            atoms[filled] = y[:, c] / norms[c]
+            filled += 1
+    while filled < t:
+        v = rng.standard_normal(n)
+        atoms[filled] = v / np.linalg.norm(v)
+        filled += 1
+    return np.ascontiguousarray(atoms.T)
+
+
+def cleanup_duplicates(y, d, e):
+    """learn._cleanup_duplicates (learn.py:201-228)."""
+    t = d.shape[1]
+    gram = np.abs(d.T @ d)
+    np.fill_diagonal(gram, 0.0)
+    resid_norms = np.linalg.norm(e, axis=0)
+    taken = set()
+    replaced = 0
+    for j in range(t):
+        if gram[:j, j].max(initial=0.0) <= _DUPLICATE_COHERENCE:
+            continue
+        rn = resid_norms.copy()
+        if taken:
+            rn[list(taken)] = -1.0
+        worst = int(np.argmax(rn))
+        taken.add(worst)
+        cn = np.linalg.norm(y[:, worst])
+        if cn > 0:
+            d[:, j] = y[:, worst] / cn
+        gram[j, :] = 0.0
+        gram[:, j] = 0.0
+        replaced += 1
+    return replaced
+
+
+def train(y, t, k, iterations, seed=0, threshold=1, init="data-columns", rel_tol=1e-6,
+          blocks=None, q=None, nthreads=1):
+    """learn._ksvd_core (learn.py:265-288) with the C kernel restatement for
+    the coding stage (full, or block-restricted with a rectangular block
+    list); returns (d, x, pre, post, replaced)."""
+    import oracle as O
+    n, m = y.shape
+    rng = np.random.default_rng(seed)
+    d = init_atoms(y, t, init, rng)
+    ys_rows = np.ascontiguousarray(y.T)
+    pre, post, replaced = [], [], 0
+    x = None
+    for it in range(iterations):
+        if blocks is None:
+            r = O.omp_many_arrays(np.ascontiguousarray(d.T), ys_rows, k, rel_tol=rel_tol,
+                                  nthreads=nthreads)
+        else:
+            r = O.omp_many_arrays(np.ascontiguousarray(d.T), ys_rows, k, rel_tol=rel_tol,
+                                  allowed_blocks=blocks, block_q=q, nthreads=nthreads)
+        x = np.zeros((t, m))
+        for p in range(m):
+            c = int(r["counts"][p])
+            x[r["sel"][p, :c], p] = r["alpha"][p, :c]
+        pre.append(float(np.linalg.norm(y - d @ x)))
+        rep, e = update_stage(y, d, x, threshold)
+        replaced += rep
+        post.append(float(np.linalg.norm(e)))
+        if it + 1 < iterations:
+            replaced += cleanup_duplicates(y, d, e)
+    return d, x, np.array(pre), np.array(post), replaced

@@ -9,7 +9,9 @@ reference imported them by name -- to this package's B200 implementations:
 * ``crossdict.patchwork.{extract_patches, aggregate_patches}`` (patchwork.py:58-122)
 * ``crossdict.learn._code_stage`` (learn.py:240-262): K-SVD's coding stage as
   one ragged block-restricted device call, and ``crossdict.learn._update_stage``
-  (learn.py:169-199): the rank-one dictionary refits in one device call
+  (learn.py:169-199): the rank-one dictionary refits in one device call, and
+  ``crossdict.learn._ksvd_core`` (learn.py:265-288): the whole training loop
+  with codes, residual and refits kept on the device
 * ``crossdict.pipelines._recover_operator`` (pipelines.py:258-322): operator
   recovery (masks, mosaics, temporal codes, angular sampling) with every
   patch coded in one coded-rows device call per step
@@ -36,7 +38,7 @@ from . import pursuit as _pursuit
 
 _saved: dict = {}
 _ERRORS = ("CrossdictError", "DimensionError", "DomainError", "DegenerateAtomError",
-           "ConfigError", "ChecksumError", "FormatError")
+           "DegenerateDataError", "ConfigError", "ChecksumError", "FormatError")
 _FUNCS = {
     "omp": _pursuit.omp,
     "omp_many": _pursuit.omp_many,
@@ -48,6 +50,7 @@ _FUNCS = {
     "aggregate_patches": _pw.aggregate_patches,
     "_code_stage": _learn.code_stage,  # crossdict.learn only (learn.py:240-262)
     "_update_stage": _learn.update_stage,  # crossdict.learn only (learn.py:169-199)
+    "_ksvd_core": _learn.ksvd_core,  # crossdict.learn only (learn.py:265-288)
     "_recover_operator": _pipelines.recover_operator_stage,  # crossdict.pipelines only
 }
 _MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
@@ -75,6 +78,13 @@ def install(package: str = "crossdict") -> list:
                 setattr(mod, name, fn)
                 patched.append(f"{modname}.{name}")
     _saved["#types"] = dict(_pursuit._types)
+    _saved["#learntypes"] = dict(_learn._types)
+    try:
+        ref_learn = importlib.import_module(f"{package}.learn")
+        _learn._types.update(TrainReport=ref_learn.TrainReport, report_log=ref_learn.report_log,
+                             Dictionary=ref_tensor.Dictionary)
+    except (ImportError, AttributeError):
+        pass
     _saved["#pwtypes"] = dict(_pw._types)
     try:
         ref_pw = importlib.import_module(f"{package}.patchwork")
@@ -100,6 +110,9 @@ def uninstall() -> None:
         elif key == "#pwtypes":
             _pw._types.clear()
             _pw._types.update(val)
+        elif key == "#learntypes":
+            _learn._types.clear()
+            _learn._types.update(val)
         elif key == "#errors":
             for n, cls in val.items():
                 setattr(_errors, n, cls)

@@ -33,7 +33,8 @@ def _compare(y, d0, x0, thr, d_ref, x_ref, e_ref, rep_ref):
     assert np.abs(e - e_ref).max() <= TOL * max(np.abs(y).max(), 1.0)
 
 
-@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "ksvd_*.npz"))),
+@pytest.mark.parametrize("path", sorted(p for p in glob.glob(os.path.join(GOLD, "ksvd_*.npz"))
+                                         if "ksvd_train_" not in p),
                          ids=lambda p: os.path.basename(p)[5:-4])
 def test_update_stage_matches_reference(path):
     g = np.load(path)

@@ -31,6 +31,7 @@ def test_install_rebinds_and_restores(crossdict):
         # K-SVD coding stage and the patch pipeline ends
         assert "crossdict.learn._code_stage" in patched
         assert "crossdict.learn._update_stage" in patched
+        assert "crossdict.learn._ksvd_core" in patched
         assert "crossdict.patchwork.extract_patches" in patched
         assert "crossdict.pipelines.aggregate_patches" in patched
         # operator recovery
