@@ -348,3 +348,33 @@ def ksvd_constrained(samples, per_sample_allowed_support, config: TrainConfig, *
     if all(len(s) == t for s in sets):
         return ksvd_core(y, config, None, None)
     return ksvd_core(y, config, sets, block_hint)
+
+
+def train_cross_scale(samples, scale, t_low: int, t_high: int, k_low: int, k_high: int,
+                      iterations: int = 20, seed: int = 0, dead_atom_threshold: int = 1,
+                      init: str = "data-columns"):
+    """Two-step cross-scale training (learn.py:334-379): K-SVD on the
+    block-averaged samples, then block-restricted K-SVD at full resolution
+    (each sample confined to its coarse support's children; an empty coarse
+    code gets block 1 as placeholder).  Returns ``(model, (low, high))``."""
+    from .crossscale import CrossScaleModel, cross_scale_map
+    from .scaling import downsample_columns
+    y = _validate_samples(samples)
+    if t_low < 1 or t_high % t_low:
+        raise E.ConfigError(f"t_high={t_high} must be a positive multiple of t_low={t_low}")
+    q = t_high // t_low
+    if y.shape[0] != scale.fine_size:
+        raise E.DimensionError(f"sample length {y.shape[0]} != fine patch size {scale.fine_size}")
+    y_low = downsample_columns(y, scale)
+    cfg_low = TrainConfig(t_low, k_low, iterations, seed, dead_atom_threshold, init)
+    d_low, codes_low, report_low = ksvd(y_low, cfg_low)
+    blocks_list, allowed_sets = [], []
+    for code in codes_low:
+        sup = code.support if code.support else (1,)
+        blocks_list.append([i - 1 for i in sup])
+        allowed_sets.append(cross_scale_map(sup, q, t_high))
+    cfg_high = TrainConfig(t_high, k_high, iterations, seed, dead_atom_threshold, init)
+    d_high, _, report_high = ksvd_constrained(y, allowed_sets, cfg_high,
+                                              block_hint=(blocks_list, q))
+    model = CrossScaleModel(d_low, d_high, scale, k_low, k_high)
+    return model, (report_low, report_high)

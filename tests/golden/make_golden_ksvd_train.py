@@ -18,7 +18,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
 
 import crossdict.pursuit as cpursuit  # noqa: E402
-from crossdict.learn import TrainConfig, ksvd, ksvd_constrained  # noqa: E402
+from crossdict.learn import TrainConfig, ksvd, ksvd_constrained, train_cross_scale  # noqa: E402
+from crossdict.scaling import ScaleSpec  # noqa: E402
 
 
 def data(n, t, m, k, seed):
@@ -63,6 +64,15 @@ def main():
     d3, codes3, rep3 = ksvd_constrained(y3, sets, cfg3, block_hint=(blocks, 3))
     save("blocked", y3, d3, codes3, rep3, t=30, k=3, iterations=3, seed=3, threshold=1,
          blocks=np.array(blocks), q=3)
+    # two-scale training (learn.py:334-379): 4 x 4 patches, 2 x 2 blocks
+    y4 = data(16, 32, 260, 3, 8)
+    model, (rl, rh) = train_cross_scale(y4, ScaleSpec((4, 4), (2, 2)), 8, 32, 2, 4,
+                                        iterations=3, seed=4)
+    np.savez_compressed(os.path.join(HERE, "train_cross_scale.npz"), y=y4, d_low=model.d_low.atoms,
+                        d_high=model.d_high.atoms, pre_low=np.array(rl.objective_pre_update),
+                        post_low=np.array(rl.objective_per_iteration),
+                        pre_high=np.array(rh.objective_pre_update),
+                        post_high=np.array(rh.objective_per_iteration))
     print("wrote ksvd training goldens")
 
 

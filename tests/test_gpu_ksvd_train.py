@@ -47,3 +47,24 @@ def test_ksvd_training_matches_reference(path):
         for i, v in c.entries:
             x[i - 1, p] = v
     assert np.abs(x - g["x"] * sgn[:, None]).max() <= 1e-8 * max(1.0, np.abs(g["x"]).max())
+
+
+def test_train_cross_scale_matches_reference():
+    """Two-scale training (learn.py:334-379) on the device loop vs the
+    reference's run: both objective traces and both dictionaries."""
+    from paper_1511_05174_b200.scaling import ScaleSpec
+    g = np.load(os.path.join(GOLD, "train_cross_scale.npz"))
+    old = pursuit.REL_RESIDUAL_TOL
+    pursuit.REL_RESIDUAL_TOL = 1e-6
+    try:
+        model, (rl, rh) = L.train_cross_scale(g["y"], ScaleSpec((4, 4), (2, 2)), 8, 32, 2, 4,
+                                              iterations=3, seed=4)
+    finally:
+        pursuit.REL_RESIDUAL_TOL = old
+    for got, key in ((rl.objective_pre_update, "pre_low"), (rl.objective_per_iteration, "post_low"),
+                     (rh.objective_pre_update, "pre_high"),
+                     (rh.objective_per_iteration, "post_high")):
+        np.testing.assert_allclose(got, g[key], rtol=1e-8)
+    for d, ref in ((model.d_low.atoms, g["d_low"]), (model.d_high.atoms, g["d_high"])):
+        sgn = np.sign(np.sum(d * ref, axis=0))
+        assert np.abs(d - ref * sgn).max() <= 1e-8
