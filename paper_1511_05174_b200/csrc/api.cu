@@ -22,6 +22,7 @@ struct cdb_dictionary {
   void *d16 = nullptr;     // T x n_pad bf16 (tensor-core operand)
   float *d32 = nullptr;    // T x N fp32 (residual materialisation of the scan operand)
   double dmax = 0.0;       // largest atom norm
+  double emax = 0.0;       // largest |bf16(d_j) - d_j| (tensor-engine certification)
   int64_t bytes = 0;
 };
 
@@ -294,6 +295,7 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
     a.gram = d->gram;
     a.rescans = diag_dev() + 1;  // zeroed by run_omp's diag_clear
     a.dmax = d->dmax;
+    a.emax = d->emax;
     a.out_sel = (int64_t *)o.sel.dev + off * kw;
     a.out_coef = (double *)o.coef.dev + off * kw;
     a.out_count = (int64_t *)o.count.dev + off;
@@ -1022,6 +1024,10 @@ cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
     if (cdb::launch_row_norm_max(d->d64, t, n, dm, st) != cudaSuccess ||
         cudaMemcpyAsync(&d->dmax, dm, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
       return cleanup(CDB_ERR_CUDA, "dmax kernel");
+    if (cudaStreamSynchronize(st) != cudaSuccess ||
+        cdb::launch_quant_err_max(d->d64, d->d16, t, n, d->n_pad, dm, st) != cudaSuccess ||
+        cudaMemcpyAsync(&d->emax, dm, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return cleanup(CDB_ERR_CUDA, "quantisation-error kernel");
     cudaFreeAsync(dm, st);
   }
   const double gb = 8.0 * (double)t * (double)t;

@@ -118,6 +118,7 @@ struct TensorArgs {
   const float *d32;      // T x N fp32 atoms (residual materialisation)
   const double *gram;
   double dmax;           // max atom norm (error bound)
+  double emax;           // max |bf16(d_j) - d_j| (error bound)
   int *rescans;          // device counter of inline exact rescans
   int64_t *out_sel;
   double *out_coef;
@@ -137,6 +138,8 @@ cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *
                             cudaStream_t stream);
 
 // ---------------------------------------------------------------- helpers
+cudaError_t launch_quant_err_max(const double *d64, const void *d16, int64_t t, int64_t n,
+                                 int64_t n_pad, double *out, cudaStream_t stream);
 cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double *out,
                                 cudaStream_t stream);
 cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,

@@ -182,6 +182,24 @@ __global__ void row_norm_max_kernel(const double *__restrict__ d, int64_t t, int
   if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(sqrt(acc)));
 }
 
+// max over atoms of |bf16(d_j) - d_j| (the tensor engine's operand rounding,
+// measured exactly; the certification bound charges it instead of u |d|)
+__global__ void quant_err_max_kernel(const double *__restrict__ d, const __nv_bfloat16 *__restrict__ d16,
+                                     int64_t t, int64_t n, int64_t n_pad,
+                                     unsigned long long *__restrict__ out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= t) return;
+  double acc = 0.0;
+  for (int64_t i = lane; i < n; i += 32) {
+    const double e = (double)__bfloat162float(d16[w * n_pad + i]) - d[w * n + i];
+    acc = fma(e, e, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0)
+    atomicMax(out, (unsigned long long)__double_as_longlong(sqrt(acc) * (1.0 + 1e-12)));
+}
+
 // ---- zero-tree step-2 routing: (signal, slot) pairs grouped by parent block
 __global__ void route_count_kernel(const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb,
                                    int64_t p, int64_t k1, int *__restrict__ count) {
@@ -635,6 +653,16 @@ cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double 
   if (e != cudaSuccess) return e;
   row_norm_max_kernel<<<blocks_for(t * 32, 256), 256, 0, stream>>>(d64, t, n,
                                                                      (unsigned long long *)out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_err_max(const double *d64, const void *d16, int64_t t, int64_t n,
+                                 int64_t n_pad, double *out, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), stream);
+  if (e != cudaSuccess) return e;
+  quant_err_max_kernel<<<blocks_for(t * 32, 256), 256, 0, stream>>>(
+      d64, (const __nv_bfloat16 *)d16, t, n, n_pad, (unsigned long long *)out);
   note_launch();
   return cudaGetLastError();
 }

@@ -306,6 +306,14 @@ __global__ void to_bf16_rows(const float *__restrict__ rows, int64_t p, int64_t 
 }
 
 // ---------------------------------------------------------------- LS side
+// Store the bf16 scan operand element of r~ and return its squared rounding error.
+__device__ __forceinline__ double put_r16(__nv_bfloat16 *dst, double v) {
+  const __nv_bfloat16 b = __float2bfloat16_rn((float)v);
+  *dst = b;
+  const double e = (double)__bfloat162float(b) - v;
+  return e * e;
+}
+
 // L^{-1} layout (shared and global): row stride kwp = kw rounded up to 16,
 // element (l, i) at l * kwp + (i ^ (l & 15)).  Lanes walking a column (fixed
 // i, l = lane) hit 16 distinct banks; lanes walking a row stay inside one
@@ -322,6 +330,8 @@ struct TensorState {
   double *yy;           // P   |y|^2
   double *rt;           // P   |r~|  (operand of the bf16 scan)
   double *dr;           // P   bound on |r~ - r|
+  double *rq;           // P   |bf16(r~) - r~| (the scan operand's rounding, exact)
+  double emax;          // max_j |bf16(d_j) - d_j| (the dictionary operand's rounding)
   double *tol;          // P
   uint32_t *status;     // P   ST_DONE | ST_DELEGATE
   const int *cand_idx;
@@ -352,13 +362,14 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
   const int lane = threadIdx.x & 31;
   if (sig >= p) return;
   const YT *y = ys + sig * n;
-  double yy = 0.0;
+  double yy = 0.0, q2 = 0.0;
   for (int64_t i = lane; i < n; i += 32) {
     const double v = (double)y[i];
-    st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)v);
+    q2 += put_r16(st.r16 + sig * n_pad + i, v);
     yy = fma(v, v, yy);
   }
   yy = warp_sum(yy);
+  q2 = warp_sum(q2);
   // |y| in the reference's _dot4 order (_kernels.py:27-47,71): lanes 0-3
   // run the four accumulator chains, the tail is added last
   const int64_t m4 = (n / 4) * 4;
@@ -387,6 +398,7 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
     st.rn2[sig] = yy;
     st.rt[sig] = sqrt(yy);
     st.dr[sig] = 0.0;
+    st.rq[sig] = sqrt(q2) * (1.0 + 1e-12);
     st.status[sig] = ynorm <= tol ? ST_DONE : 0u;
     out_count[sig] = 0;
     out_rnorm[sig] = ynorm;
@@ -512,7 +524,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
   }
   // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16.
   // 8 elements per lane per pass: each support atom row is read coalesced.
-  double rr = 0.0, sx = 0.0;
+  double rr = 0.0, sx = 0.0, q2 = 0.0;
   for (int64_t i0 = 0; i0 < n; i0 += 256) {
     double acc[8];
 #pragma unroll
@@ -548,7 +560,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
     for (int u = 0; u < 8; u++) {
       const int64_t i = i0 + u * 32 + lane;
       if (i < n) {
-        st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)acc[u]);
+        q2 += put_r16(st.r16 + sig * n_pad + i, acc[u]);
         rr = fma(acc[u], acc[u], rr);
       }
     }
@@ -556,7 +568,9 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
   for (int64_t l = lane; l < kd; l += 32) sx += fabs(xv[l]);
   rr = warp_sum(rr);
   sx = warp_sum(sx);
+  q2 = warp_sum(q2);
   if (lane == 0) {
+    st.rq[sig] = sqrt(q2) * (1.0 + 1e-12);
     st.rt[sig] = sqrt(rr);
     st.dr[sig] = 0x1p-24 * sx * dmax * 1.0000001;  // |(D64 - D32) x| bound
     atomicAdd(st.active + iter, 1);
@@ -629,7 +643,8 @@ __global__ void __launch_bounds__(256, 3) ls_step_kernel(
           if (ssel[i] == cidx) cidx = -1;
         if (cidx < 0) cval = -1.0f;
       }
-      const double E = (c_err * rt + drs) * dmax;
+      const double rq = st.rq[sig];  // E: rigorous bound of |c~ - <d, r>| (see c_err)
+      const double E = (c_err * (rt + rq) * 1.0079 + rq + drs) * dmax + st.emax * (rt + rq);
       double best_apx = (double)cval;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
@@ -782,7 +797,8 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
           if (ssel[i] == cidx) cidx = -1;
         if (cidx < 0) cval = -1.0f;
       }
-      const double E = (c_err * rt + drs) * dmax;
+      const double rq = st.rq[sig];  // E: rigorous bound of |c~ - <d, r>| (see c_err)
+      const double E = (c_err * (rt + rq) * 1.0079 + rq + drs) * dmax + st.emax * (rt + rq);
       const double best_apx = gmax<G>((double)cval);
       const bool rescore = act && cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
       const unsigned rm = (__ballot_sync(CDB_FULL_MASK, rescore) & gbits) >> (gi * G);
@@ -937,7 +953,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     }
     // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16
     //      (split mode: left to resid_split_kernel, flagged ST_RESID)
-    double rr = 0.0, sx = 0.0;
+    double rr = 0.0, sx = 0.0, q2 = 0.0;
     if (act && !split) {
 #pragma unroll
       for (int i0 = 0; i0 < (YM > 0 ? YM * G : n); i0 += 8 * G) {
@@ -983,7 +999,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
         for (int u = 0; u < 8; u++) {
           const int i = i0 + u * G + gl;
           if (i < n) {
-            st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)acc[u]);
+            q2 += put_r16(st.r16 + sig * n_pad + i, acc[u]);
             rr = fma(acc[u], acc[u], rr);
           }
         }
@@ -992,10 +1008,12 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     }
     rr = gsum<G>(rr);
     sx = gsum<G>(sx);
+    q2 = gsum<G>(q2);
     if (act && gl == 0) {
       if (split) {
         st.status[sig] |= ST_RESID;
       } else {
+        st.rq[sig] = sqrt(q2) * (1.0 + 1e-12);
         st.rt[sig] = sqrt(rr);
         st.dr[sig] = 0x1p-24 * sx * dmax * 1.0000001;  // |(D64 - D32) x| bound
       }
@@ -1021,7 +1039,7 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
   extern __shared__ double xsm[];
   double *xv = xsm;                         // kw
   int64_t *ssel = (int64_t *)(xv + kw);     // kw
-  __shared__ double red[2][BT / 32];
+  __shared__ double red[3][BT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t sig = blockIdx.x; sig < p; sig += gridDim.x) {
     if (!(st.status[sig] & ST_RESID)) continue;  // uniform across the CTA
@@ -1032,7 +1050,7 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
     }
     __syncthreads();
     const YT *y = ys + sig * n;
-    double rr = 0.0;
+    double rr = 0.0, q2 = 0.0;
     for (int64_t i0 = 0; i0 < n; i0 += 8 * BT) {
       double acc[8];
 #pragma unroll
@@ -1072,7 +1090,7 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
       for (int u = 0; u < 8; u++) {
         const int64_t i = i0 + u * BT + tid;
         if (i < n) {
-          st.r16[sig * n_pad + i] = __float2bfloat16_rn((float)acc[u]);
+          q2 += put_r16(st.r16 + sig * n_pad + i, acc[u]);
           rr = fma(acc[u], acc[u], rr);
         }
       }
@@ -1081,17 +1099,21 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
     for (int l = tid; l < kd; l += blockDim.x) sx += fabs(xv[l]);
     rr = warp_sum(rr);
     sx = warp_sum(sx);
+    q2 = warp_sum(q2);
     if (lane == 0) {
       red[0][warp] = rr;
       red[1][warp] = sx;
+      red[2][warp] = q2;
     }
     __syncthreads();
     if (tid == 0) {
-      double a = 0.0, b = 0.0;
+      double a = 0.0, b = 0.0, c = 0.0;
       for (int w = 0; w < BT / 32; w++) {
         a += red[0][w];
         b += red[1][w];
+        c += red[2][w];
       }
+      st.rq[sig] = sqrt(c) * (1.0 + 1e-12);
       st.rt[sig] = sqrt(a);
       st.dr[sig] = 0x1p-24 * b * dmax * 1.0000001;  // |(D64 - D32) x| bound
       st.status[sig] &= ~ST_RESID;
@@ -1622,7 +1644,7 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols_pad, 
 int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw) {
   const int64_t n_pad = (n + BK - 1) / BK * BK;
   const int64_t p_pad = (p + BM - 1) / BM * BM;
-  return p_pad * n_pad * 2 + p * kw * ((kw + 15) & ~int64_t(15)) * 8 + p * kw * 8 + p * 8 * 5 + p * NCAND * 8 + p * 4 +
+  return p_pad * n_pad * 2 + p * kw * ((kw + 15) & ~int64_t(15)) * 8 + p * kw * 8 + p * 8 * 6 + p * NCAND * 8 + p * 4 +
          p * 8 * 3 + p * (3 * 8 * RS_SPLIT + 4) + 4 * 4096 + 21 * 256;
 }
 
@@ -1645,6 +1667,8 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   st.yy = (double *)take(p * 8);
   st.rt = (double *)take(p * 8);
   st.dr = (double *)take(p * 8);
+  st.rq = (double *)take(p * 8);
+  st.emax = a.emax;
   st.tol = (double *)take(p * 8);
   st.status = a.status;
   int *cidx = (int *)take(p * NCAND * 4);
@@ -1714,10 +1738,14 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     e = cudaFuncSetAttribute(ls_step_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)ls_smem);
   if (e != cudaSuccess) return e;
-  // rigorous bound of |c~ - <d, r~>| / (|r~| |d|): bf16 rounding of both
-  // operands (2u + u^2, u = 2^-8), fp32 accumulation over n_pad terms, and
-  // the truncation of the packed epilogue keys (2^-18; 2^-15 kept as margin)
-  const double c_err = 2.0 * 0x1p-8 + 0x1p-16 + (double)(n_pad + 16) * 0x1p-23 + 0x1p-15;
+  // E = c_err (|r~| + rq)(1 + 2^-7) dmax + emax (|r~| + rq) + dmax (rq + dr):
+  // the bf16 operands' rounding is charged exactly as measured -- emax =
+  // max_j |bf16(d_j) - d_j| (dictionary), rq = |bf16(r~) - r~| (per signal,
+  // per iteration), via <d^, r^> - <d, r~> = <d^ - d, r^> + <d, r^ - r~> --
+  // and c_err covers the fp32 accumulation over n_pad terms and the
+  // truncation of the packed epilogue keys (2^-18; 2^-15 kept as margin),
+  // relative to |d^| |r^| <= dmax (1 + 2^-8) (|r~| + rq).
+  const double c_err = (double)(n_pad + 16) * 0x1p-23 + 0x1p-15;
   const unsigned ls_grid = (unsigned)((p + ls_wpb - 1) / ls_wpb);
   // grouped LS kernel: 8-lane groups (4 signals per warp) when the per-signal
   // state is small, whole warps otherwise; CDB_LS_LEGACY=1 forces ls_step
