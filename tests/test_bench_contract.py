@@ -1,0 +1,44 @@
+"""bench.py keeps the driver's JSON contract: one line on stdout with the
+required keys -- the reference arm on CPU here, our arm on the B200."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+        "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, timeout):
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py")] + args, cwd=REPO,
+                         capture_output=True, text=True, timeout=timeout, check=True)
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "3"], 600)
+    assert BASE <= set(d) and d["impl"] == "reference"
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["warmup"] >= 3
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+    assert d["cpu_baseline"]["kind"] in ("port", "reference")
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert "workload" in d["config"]
+
+
+@pytest.mark.gpu
+def test_our_arm_line():
+    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu"], 900)
+    assert BASE <= set(d) and d.get("impl", "ours") != "reference"
+    assert d["value"] > 0 and d["scaling"] == "weak" and "workload" in d["config"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
+    assert 0 < d["roofline"]["frac"] <= 1
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["gpu_launches"] > 0
+    e2e = d["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
