@@ -1338,7 +1338,7 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
                          (q == 1 || q == 2 || q == 4 || q == 8 || q == 16);
   if (use_route) {
     CDB_CUDA(alpha0.alloc(sizeof(double) * p * k1 * q, st));
-    CDB_CUDA(rwork.alloc((size_t)cdb::route_work_bytes(low->t, p, k1), st));
+    CDB_CUDA(rwork.alloc((size_t)cdb::route_work_bytes(low->t, p, k1, n, f32), st));
     CDB_CUDA(cdb::launch_route_alpha0(high->d64, low->t, n, q, ydev, f32, blocks.as<int64_t>(),
                                       (const int64_t *)lo.count.dev, p, k1, k1 * q,
                                       alpha0.as<double>(), rwork.ptr, st));

@@ -159,7 +159,7 @@ cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int
                                const void *ys, bool ys_f32, const int64_t *blocks,
                                const int64_t *nb, int64_t p, int64_t k1, int64_t smax,
                                double *alpha0, void *work, cudaStream_t stream);
-int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1);
+int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1, int64_t n, bool ys_f32);
 
 // ---------------------------------------------------------------- patch pipeline ends
 cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const int64_t *sig,

@@ -201,11 +201,16 @@ __global__ void quant_err_max_kernel(const double *__restrict__ d, const __nv_bf
 }
 
 // ---- zero-tree step-2 routing: (signal, slot) pairs grouped by parent block
+// Buckets are (signal block, parent): signals [sb*SB, (sb+1)*SB) x the T_low
+// parents, so the alpha0 kernels sweep one L2-sized block of signal rows at a
+// time (bucket = sb * t_low + parent).
 __global__ void route_count_kernel(const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb,
-                                   int64_t p, int64_t k1, int *__restrict__ count) {
+                                   int64_t p, int64_t k1, int64_t t_low, int64_t sbs,
+                                   int *__restrict__ count) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= p) return;
-  for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&count[blocks[s * k1 + b]], 1);
+  const int64_t off = (s / sbs) * t_low;
+  for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&count[off + blocks[s * k1 + b]], 1);
 }
 
 // exclusive scan of count[0..m) into offs[0..m] and cursor copy (one CTA)
@@ -237,12 +242,14 @@ __global__ void route_scan_kernel(const int *__restrict__ count, int64_t m,
 }
 
 __global__ void route_fill_kernel(const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb,
-                                  int64_t p, int64_t k1, unsigned long long *__restrict__ cursor,
+                                  int64_t p, int64_t k1, int64_t t_low, int64_t sbs,
+                                  unsigned long long *__restrict__ cursor,
                                   int64_t *__restrict__ pairs) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= p) return;
+  const int64_t off = (s / sbs) * t_low;
   for (int64_t b = 0; b < nb[s]; b++) {
-    const int64_t pos = (int64_t)atomicAdd(&cursor[blocks[s * k1 + b]], 1ull);
+    const int64_t pos = (int64_t)atomicAdd(&cursor[off + blocks[s * k1 + b]], 1ull);
     pairs[pos] = (s << 16) | b;  // (signal, slot) pair
   }
 }
@@ -255,10 +262,10 @@ template <typename YT, int QT>
 __global__ void __launch_bounds__(256) alpha0_routed_kernel(
     const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t k1,
-    int64_t smax, double *__restrict__ alpha0) {
+    int64_t smax, int64_t t_low, double *__restrict__ alpha0) {
   extern __shared__ double child[];  // QT x n
-  const int64_t parent = blockIdx.x;
-  const int64_t lo = offs[parent], hi = offs[parent + 1];
+  const int64_t bucket = blockIdx.x, parent = bucket % t_low;
+  const int64_t lo = offs[bucket], hi = offs[bucket + 1];
   if (lo == hi) return;
   for (int e = threadIdx.x; e < QT * n; e += blockDim.x) child[e] = d64[parent * QT * n + e];
   __syncthreads();
@@ -318,10 +325,13 @@ __global__ void __launch_bounds__(256) alpha0_routed_kernel(
 // (signal, parent) pairs in shared memory and touches each global counter
 // once per parent it saw (instead of once per pair).
 constexpr int kRouteChunk = 1024;  // signals per CTA
+}  // namespace
+int64_t route_block_signals(int64_t p, int64_t n, bool ys_f32);
+namespace {
 
 __global__ void __launch_bounds__(256) route_count_smem_kernel(
     const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb, int64_t p, int64_t k1,
-    int t_low, int *__restrict__ count) {
+    int t_low, int64_t sbs, int *__restrict__ count) {
   extern __shared__ int hist[];
   for (int b = threadIdx.x; b < t_low; b += blockDim.x) hist[b] = 0;
   __syncthreads();
@@ -330,13 +340,14 @@ __global__ void __launch_bounds__(256) route_count_smem_kernel(
   for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x)
     for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&hist[blocks[s * k1 + b]], 1);
   __syncthreads();
+  const int64_t off = (s0 / sbs) * t_low;  // the chunk lies in one signal block
   for (int b = threadIdx.x; b < t_low; b += blockDim.x)
-    if (hist[b]) atomicAdd(&count[b], hist[b]);
+    if (hist[b]) atomicAdd(&count[off + b], hist[b]);
 }
 
 __global__ void __launch_bounds__(256) route_fill_smem_kernel(
     const int64_t *__restrict__ blocks, const int64_t *__restrict__ nb, int64_t p, int64_t k1,
-    int t_low, unsigned long long *__restrict__ cursor, int64_t *__restrict__ pairs) {
+    int t_low, int64_t sbs, unsigned long long *__restrict__ cursor, int64_t *__restrict__ pairs) {
   extern __shared__ unsigned long long sh[];  // base[t_low] | hist[t_low] (as int)
   unsigned long long *base = sh;
   int *hist = (int *)(sh + t_low);
@@ -347,8 +358,9 @@ __global__ void __launch_bounds__(256) route_fill_smem_kernel(
   for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x)
     for (int64_t b = 0; b < nb[s]; b++) atomicAdd(&hist[blocks[s * k1 + b]], 1);
   __syncthreads();
+  const int64_t off = (s0 / sbs) * t_low;
   for (int b = threadIdx.x; b < t_low; b += blockDim.x) {
-    base[b] = hist[b] ? atomicAdd(&cursor[b], (unsigned long long)hist[b]) : 0ull;
+    base[b] = hist[b] ? atomicAdd(&cursor[off + b], (unsigned long long)hist[b]) : 0ull;
     hist[b] = 0;
   }
   __syncthreads();
@@ -391,11 +403,12 @@ template <typename YT, int QT, int NPL, int HV>
 __global__ void __launch_bounds__(128) alpha0_warp_kernel(
     const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t k1,
-    int64_t smax, int split, double *__restrict__ alpha0) {
+    int64_t smax, int split, int t_low, double *__restrict__ alpha0) {
   constexpr int VW = NPL < 4 ? NPL : 4;  // floats per vector load
   constexpr int NV = NPL / VW;
-  const int parent = blockIdx.x / split, part = blockIdx.x % split;
-  const int64_t lo = offs[parent], cnt = offs[parent + 1] - lo;
+  const int bucket = blockIdx.x / split, part = blockIdx.x % split;
+  const int parent = bucket % t_low;
+  const int64_t lo = offs[bucket], cnt = offs[bucket + 1] - lo;
   const int64_t a = lo + cnt * part / split, b = lo + cnt * (part + 1) / split;
   if (a >= b) return;
   constexpr int CH = QT / HV;  // children per warp
@@ -490,26 +503,26 @@ __global__ void __launch_bounds__(128) alpha0_warp_kernel(
 }
 
 template <typename YT, int QT, int NPL>
-cudaError_t launch_alpha0_warp(const double *d64, int64_t t_low, int64_t n, const YT *ys,
-                               const int64_t *offs, const int64_t *pairs, int64_t k1,
-                               int64_t smax, double *alpha0, cudaStream_t stream) {
+cudaError_t launch_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t n,
+                               const YT *ys, const int64_t *offs, const int64_t *pairs,
+                               int64_t k1, int64_t smax, double *alpha0, cudaStream_t stream) {
   const int split = 8;
   constexpr int HV = 1;  // splitting children over 2 warps measured slower (0.76 vs 0.63 ms, cfg 1)
-  alpha0_warp_kernel<YT, QT, NPL, HV><<<(unsigned)(t_low * split), 128, 0, stream>>>(
-      d64, (int)n, ys, offs, pairs, k1, smax, split, alpha0);
+  alpha0_warp_kernel<YT, QT, NPL, HV><<<(unsigned)(buckets * split), 128, 0, stream>>>(
+      d64, (int)n, ys, offs, pairs, k1, smax, split, (int)t_low, alpha0);
   return cudaGetLastError();
 }
 
 // The register path when the parent's children fit 64 fp64 registers per
 // lane and N is 64, 128 or 256 (else the shared-memory kernel above).
 template <typename YT>
-bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t n, int64_t q, const YT *ys,
-                     const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
-                     double *alpha0, cudaStream_t stream, cudaError_t &err) {
+bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t n, int64_t q,
+                     const YT *ys, const int64_t *offs, const int64_t *pairs, int64_t k1,
+                     int64_t smax, double *alpha0, cudaStream_t stream, cudaError_t &err) {
 #define CDB_A0W(QQ, NN)                                                                      \
   if (q == QQ && n == 32 * NN) {                                                             \
-    err = launch_alpha0_warp<YT, QQ, NN>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0,   \
-                                         stream);                                            \
+    err = launch_alpha0_warp<YT, QQ, NN>(d64, t_low, buckets, n, ys, offs, pairs, k1, smax,  \
+                                         alpha0, stream);                                    \
     return true;                                                                             \
   }
   CDB_A0W(1, 2) CDB_A0W(2, 2) CDB_A0W(4, 2) CDB_A0W(8, 2) CDB_A0W(16, 2)
@@ -520,29 +533,28 @@ bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t n, int64_t q, con
 }
 
 template <typename YT, int QT>
-cudaError_t launch_alpha0_q(const double *d64, int64_t t_low, int64_t n, const YT *ys,
-                            const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
-                            double *alpha0, cudaStream_t stream) {
+cudaError_t launch_alpha0_q(const double *d64, int64_t t_low, int64_t buckets, int64_t n,
+                            const YT *ys, const int64_t *offs, const int64_t *pairs, int64_t k1,
+                            int64_t smax, double *alpha0, cudaStream_t stream) {
   const size_t smem = sizeof(double) * QT * n;
   cudaError_t e = cudaFuncSetAttribute(alpha0_routed_kernel<YT, QT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  alpha0_routed_kernel<YT, QT><<<(unsigned)t_low, 256, smem, stream>>>(d64, (int)n, ys, offs,
-                                                                      pairs, k1, smax, alpha0);
+  alpha0_routed_kernel<YT, QT><<<(unsigned)buckets, 256, smem, stream>>>(
+      d64, (int)n, ys, offs, pairs, k1, smax, t_low, alpha0);
   return cudaGetLastError();
 }
 
 template <typename YT>
-cudaError_t launch_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q, const YT *ys,
-                          const int64_t *offs, const int64_t *pairs, int64_t k1, int64_t smax,
-                          double *alpha0, cudaStream_t stream) {
-  switch (q) {
-    case 1: return launch_alpha0_q<YT, 1>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
-    case 2: return launch_alpha0_q<YT, 2>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
-    case 4: return launch_alpha0_q<YT, 4>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
-    case 8: return launch_alpha0_q<YT, 8>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
-    case 16: return launch_alpha0_q<YT, 16>(d64, t_low, n, ys, offs, pairs, k1, smax, alpha0, stream);
-  }
+cudaError_t launch_alpha0(const double *d64, int64_t t_low, int64_t buckets, int64_t n, int64_t q,
+                          const YT *ys, const int64_t *offs, const int64_t *pairs, int64_t k1,
+                          int64_t smax, double *alpha0, cudaStream_t stream) {
+#define CDB_A0Q(QQ)                                                                            \
+  case QQ:                                                                                     \
+    return launch_alpha0_q<YT, QQ>(d64, t_low, buckets, n, ys, offs, pairs, k1, smax, alpha0,  \
+                                   stream);
+  switch (q) { CDB_A0Q(1) CDB_A0Q(2) CDB_A0Q(4) CDB_A0Q(8) CDB_A0Q(16) }
+#undef CDB_A0Q
   return cudaErrorInvalidValue;
 }
 
@@ -672,48 +684,67 @@ cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int
                                const int64_t *nb, int64_t p, int64_t k1, int64_t smax,
                                double *alpha0, void *work, cudaStream_t stream) {
   ProfScope _ps("route_alpha0", stream);
-  // work: count int[t_low] | offs int64[t_low+1] | cursor u64[t_low] | pairs int64[p*k1]
+  // buckets = (signal block, parent); work: count int[m] | offs int64[m+1] |
+  // cursor u64[m] | pairs int64[p*k1], m = blocks * t_low
+  const int64_t sbs = route_block_signals(p, n, ys_f32);
+  const int64_t m = ((p + sbs - 1) / sbs) * t_low;
   uint8_t *w = (uint8_t *)work;
   int *count = (int *)w;
-  w += ((t_low * 4 + 255) / 256) * 256;
+  w += ((m * 4 + 255) / 256) * 256;
   int64_t *offs = (int64_t *)w;
-  w += (((t_low + 1) * 8 + 255) / 256) * 256;
+  w += (((m + 1) * 8 + 255) / 256) * 256;
   int64_t *cursor = (int64_t *)w;
-  w += ((t_low * 8 + 255) / 256) * 256;
+  w += ((m * 8 + 255) / 256) * 256;
   int64_t *pairs = (int64_t *)w;
-  cudaError_t e = cudaMemsetAsync(count, 0, t_low * 4, stream);
+  cudaError_t e = cudaMemsetAsync(count, 0, m * 4, stream);
   if (e != cudaSuccess) return e;
   const bool smem_route = t_low * 12 <= 48 * 1024;
   const unsigned rgrid = (unsigned)((p + kRouteChunk - 1) / kRouteChunk);
   if (smem_route)
-    route_count_smem_kernel<<<rgrid, 256, t_low * 4, stream>>>(blocks, nb, p, k1, (int)t_low,
+    route_count_smem_kernel<<<rgrid, 256, t_low * 4, stream>>>(blocks, nb, p, k1, (int)t_low, sbs,
                                                                count);
   else
-    route_count_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1, count);
-  route_scan_kernel<<<1, 1024, 0, stream>>>(count, t_low, offs, cursor);
+    route_count_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1, t_low, sbs,
+                                                               count);
+  route_scan_kernel<<<1, 1024, 0, stream>>>(count, m, offs, cursor);
   if (smem_route)
     route_fill_smem_kernel<<<rgrid, 256, t_low * 12, stream>>>(
-        blocks, nb, p, k1, (int)t_low, (unsigned long long *)cursor, pairs);
+        blocks, nb, p, k1, (int)t_low, sbs, (unsigned long long *)cursor, pairs);
   else
-    route_fill_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(blocks, nb, p, k1,
-                                                              (unsigned long long *)cursor, pairs);
-  bool done = ys_f32 ? try_alpha0_warp<float>(d64, t_low, n, q, (const float *)ys, offs, pairs, k1,
-                                              smax, alpha0, stream, e)
-                     : try_alpha0_warp<double>(d64, t_low, n, q, (const double *)ys, offs, pairs,
-                                               k1, smax, alpha0, stream, e);
+    route_fill_kernel<<<blocks_for(p, 256), 256, 0, stream>>>(
+        blocks, nb, p, k1, t_low, sbs, (unsigned long long *)cursor, pairs);
+  bool done = ys_f32 ? try_alpha0_warp<float>(d64, t_low, m, n, q, (const float *)ys, offs, pairs,
+                                              k1, smax, alpha0, stream, e)
+                     : try_alpha0_warp<double>(d64, t_low, m, n, q, (const double *)ys, offs,
+                                               pairs, k1, smax, alpha0, stream, e);
   if (!done)
-    e = ys_f32 ? launch_alpha0<float>(d64, t_low, n, q, (const float *)ys, offs, pairs, k1, smax,
-                                      alpha0, stream)
-               : launch_alpha0<double>(d64, t_low, n, q, (const double *)ys, offs, pairs, k1, smax,
-                                       alpha0, stream);
+    e = ys_f32 ? launch_alpha0<float>(d64, t_low, m, n, q, (const float *)ys, offs, pairs, k1,
+                                      smax, alpha0, stream)
+               : launch_alpha0<double>(d64, t_low, m, n, q, (const double *)ys, offs, pairs, k1,
+                                       smax, alpha0, stream);
   if (e != cudaSuccess) return e;
   note_launch(4);
   return cudaGetLastError();
 }
 
-int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1) {
-  return ((t_low * 4 + 255) / 256) * 256 + (((t_low + 1) * 8 + 255) / 256) * 256 +
-         ((t_low * 8 + 255) / 256) * 256 + p * k1 * 8 + 256;
+// Signals per routing block: ~48 MB of signal rows stay L2-resident while
+// every parent of the block is coded (measured on cfg 1, 100k signals:
+// 8 MB 0.79 ms, 16 MB 0.685, 32 MB 0.637, 40-64 MB 0.627-0.629, one block
+// 0.68); a multiple of the 1024-signal routing chunk; CDB_ROUTE_SB overrides
+// (0 = one block).
+int64_t route_block_signals(int64_t p, int64_t n, bool ys_f32) {
+  int64_t sbs = (int64_t(48) << 20) / ((ys_f32 ? 4 : 8) * (n > 0 ? n : 1));
+  if (const char *v = getenv("CDB_ROUTE_SB")) sbs = atoll(v);
+  if (sbs <= 0) return p > 0 ? ((p + kRouteChunk - 1) / kRouteChunk) * kRouteChunk : kRouteChunk;
+  sbs = (sbs / kRouteChunk) * kRouteChunk;
+  return sbs < kRouteChunk ? kRouteChunk : sbs;
+}
+
+int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1, int64_t n, bool ys_f32) {
+  const int64_t sbs = route_block_signals(p, n, ys_f32);
+  const int64_t m = ((p + sbs - 1) / sbs) * t_low;
+  return ((m * 4 + 255) / 256) * 256 + (((m + 1) * 8 + 255) / 256) * 256 +
+         ((m * 8 + 255) / 256) * 256 + p * k1 * 8 + 256;
 }
 
 }  // namespace cdb
