@@ -73,25 +73,32 @@ def _raise(status):
     N.check(status)
 
 
+# install(): the reference's model / dictionary classes, so the drop-in
+# load_model returns the caller's own types
+_types: dict = {}
+
+
 def load_model(path, stage: bool = False):
     """Load a .csd file -> CrossScaleModel or SingleScaleModel (fileio.py:216-256).
 
     ``stage=True`` also creates the device dictionaries now (cached for the
     pursuit calls that follow)."""
     recs = _read(path)
+    dict_cls = _types.get("Dictionary", Dictionary)
     dicts = []
     for shape, atoms_t, k, q in recs:
-        d = Dictionary(np.asarray(atoms_t).T)  # validates unit norms as the reference
+        d = dict_cls(np.asarray(atoms_t).T)  # validates unit norms as the reference
         dicts.append((shape, d, k, q))
     if stage:
         for _, d, _, _ in dicts:
-            _dev.device_dictionary(d.atoms_t)
+            _dev.device_dictionary(np.ascontiguousarray(d.atoms_t))
     if len(dicts) == 1:
         shape, d, k, _ = dicts[0]
-        return SingleScaleModel(d, shape, k)
+        return _types.get("SingleScaleModel", SingleScaleModel)(d, shape, k)
     (coarse, d_low, k_low, _), (fine, d_high, k_high, _) = dicts
     factors = tuple(f // c for f, c in zip(fine, coarse))
-    return CrossScaleModel(d_low, d_high, ScaleSpec(fine, factors), k_low, k_high)
+    scale = _types.get("ScaleSpec", ScaleSpec)(fine, factors)
+    return _types.get("CrossScaleModel", CrossScaleModel)(d_low, d_high, scale, k_low, k_high)
 
 
 def _pack_record(buf: bytearray, patch_shape, dictionary: Dictionary, k: int, q: int):

@@ -7,6 +7,8 @@ reference imported them by name -- to this package's B200 implementations:
 * ``crossdict.crossscale.{zero_tree_omp, zero_tree_omp_many,
   zero_tree_many_arrays}``                                    (crossscale.py:169-312)
 * ``crossdict.patchwork.{extract_patches, aggregate_patches}`` (patchwork.py:58-122)
+* ``crossdict.fileio.load_model`` (fileio.py:216-256): the native CRC-checked
+  .csd reader, returning the reference's model classes
 * ``crossdict.learn._code_stage`` (learn.py:240-262): K-SVD's coding stage as
   one ragged block-restricted device call, and ``crossdict.learn._update_stage``
   (learn.py:169-199): the rank-one dictionary refits in one device call, and
@@ -31,6 +33,7 @@ import importlib
 
 from . import crossscale as _cs
 from . import errors as _errors
+from . import fileio as _fileio
 from . import learn as _learn
 from . import patchwork as _pw
 from . import pipelines as _pipelines
@@ -51,10 +54,11 @@ _FUNCS = {
     "_code_stage": _learn.code_stage,  # crossdict.learn only (learn.py:240-262)
     "_update_stage": _learn.update_stage,  # crossdict.learn only (learn.py:169-199)
     "_ksvd_core": _learn.ksvd_core,  # crossdict.learn only (learn.py:265-288)
+    "load_model": _fileio.load_model,  # .csd models (fileio.py:216-256)
     "_recover_operator": _pipelines.recover_operator_stage,  # crossdict.pipelines only
 }
 _MODULES = ("crossdict.pursuit", "crossdict.crossscale", "crossdict", "crossdict.pipelines",
-            "crossdict.learn", "crossdict.patchwork")
+            "crossdict.learn", "crossdict.patchwork", "crossdict.fileio")
 
 
 def install(package: str = "crossdict") -> list:
@@ -79,6 +83,16 @@ def install(package: str = "crossdict") -> list:
                 patched.append(f"{modname}.{name}")
     _saved["#types"] = dict(_pursuit._types)
     _saved["#learntypes"] = dict(_learn._types)
+    _saved["#fiotypes"] = dict(_fileio._types)
+    try:
+        ref_fio = importlib.import_module(f"{package}.fileio")
+        ref_scaling = importlib.import_module(f"{package}.scaling")
+        _fileio._types.update(Dictionary=ref_tensor.Dictionary,
+                              SingleScaleModel=ref_fio.SingleScaleModel,
+                              CrossScaleModel=ref_cs.CrossScaleModel,
+                              ScaleSpec=ref_scaling.ScaleSpec)
+    except (ImportError, AttributeError):
+        pass
     try:
         ref_learn = importlib.import_module(f"{package}.learn")
         _learn._types.update(TrainReport=ref_learn.TrainReport, report_log=ref_learn.report_log,
@@ -113,6 +127,9 @@ def uninstall() -> None:
         elif key == "#learntypes":
             _learn._types.clear()
             _learn._types.update(val)
+        elif key == "#fiotypes":
+            _fileio._types.clear()
+            _fileio._types.update(val)
         elif key == "#errors":
             for n, cls in val.items():
                 setattr(_errors, n, cls)

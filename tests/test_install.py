@@ -32,6 +32,14 @@ def test_install_rebinds_and_restores(crossdict):
         assert "crossdict.learn._code_stage" in patched
         assert "crossdict.learn._update_stage" in patched
         assert "crossdict.learn._ksvd_core" in patched
+        # .csd loading through the native reader, reference types out
+        assert "crossdict.fileio.load_model" in patched
+        gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+        m = crossdict.fileio.load_model(os.path.join(gold, "csd_cross.csd"))
+        assert isinstance(m, crossdict.crossscale.CrossScaleModel)
+        assert isinstance(m.d_high, crossdict.tensor.Dictionary)
+        m1 = crossdict.fileio.load_model(os.path.join(gold, "csd_single.csd"))
+        assert type(m1).__name__ == "SingleScaleModel" and type(m1).__module__.startswith("crossdict")
         assert "crossdict.patchwork.extract_patches" in patched
         assert "crossdict.pipelines.aggregate_patches" in patched
         # operator recovery
