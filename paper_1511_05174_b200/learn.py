@@ -316,10 +316,15 @@ def ksvd_core(y, config: TrainConfig, allowed_sets, block_hint):
                 y, d, torch.linalg.norm(e, dim=1).cpu().numpy())
     sel_h, coef_h = o["sel"].cpu().numpy(), o["alpha"].cpu().numpy()
     sc = _pursuit._types["SparseCode"]
-    codes = []
-    for p in range(m):
-        keep = (sel_h[p] >= 0) & (coef_h[p] != 0.0)
-        codes.append(sc.from_arrays(t, (sel_h[p][keep] + 1).tolist(), coef_h[p][keep]))
+    # entries sorted by atom per sample, vectorised (the reference's
+    # _codes_from_matrix order, learn.py:231-237); only the objects are per sample
+    keep = (sel_h >= 0) & (coef_h != 0.0)
+    key = np.where(keep, sel_h, np.iinfo(np.int64).max)
+    order = np.argsort(key, axis=1, kind="stable")
+    ids = (np.take_along_axis(sel_h, order, axis=1) + 1).tolist()
+    vals = np.take_along_axis(coef_h, order, axis=1).tolist()
+    cnt = keep.sum(axis=1).tolist()
+    codes = [sc(t, tuple(zip(ids[p][:cnt[p]], vals[p][:cnt[p]]))) for p in range(m)]
     report.wall_clock = time.perf_counter() - start
     _types.get("report_log", report_log).append(report)
     return _types.get("Dictionary", _tensor.Dictionary)(d), codes, report
