@@ -314,11 +314,17 @@ __global__ void __launch_bounds__(KT, 1) ksvd_update_kernel(KsvdArgs a) {
       for (int64_t i = tid; i < n; i += KT) uv[i] = v[i];
       __syncthreads();
       double s2 = 0.0;
-      for (int64_t c = tid; c < u; c += KT) {
-        double s = 0.0;
-        for (int64_t i = 0; i < n; i++) s = fma(ej[c * n + i], uv[i], s);
-        a.val[b0 + c] = s;  // scratch: E_j^T u
-        s2 = fma(s, s, s2);
+      {  // a warp per user row: coalesced, lanes over the coordinates
+        const int lane = tid & 31, wp = tid >> 5;
+        for (int64_t c = wp; c < u; c += KT / 32) {
+          double s = 0.0;
+          for (int64_t i = lane; i < n; i += 32) s = fma(ej[c * n + i], uv[i], s);
+          s = warp_sum(s);
+          if (lane == 0) {
+            a.val[b0 + c] = s;  // scratch: E_j^T u
+            s2 = fma(s, s, s2);
+          }
+        }
       }
       const double nr = sqrt(block_sum(s2, red));
       for (int64_t c = tid; c < u; c += KT) a.val[b0 + c] /= nr;
