@@ -407,6 +407,7 @@ def bench_ours(args):
 
     ends = bench_pipeline_ends(peaks) if rank == 0 and world == 1 else None
     ksvd = bench_ksvd_update(args.no_cpu) if rank == 0 and world == 1 else None
+    oprec = bench_operator_recovery(args.no_cpu) if rank == 0 and world == 1 else None
 
     if rank == 0:
         line = {
@@ -429,6 +430,7 @@ def bench_ours(args):
             "cpu_baseline": cpu,
             "pipeline_ends": ends,
             "ksvd_update": ksvd,
+            "operator_recovery": oprec,
             "e2e": {"value": world * P * args.steps / e2e_total, "unit": "signals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "clocks": clk,
@@ -438,6 +440,49 @@ def bench_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_operator_recovery(no_cpu=False):
+    """per-patch operator recovery (pipelines._recover_operator)
+    through the public recover_operator -- a 512 x 512 x 3 image behind a
+    random channel mosaic, 8 x 8 x 3 patches at stride 2 (64 009 patches),
+    single-scale OMP with K = 6 over 384 atoms -- beside the oracle's
+    restatement of the reference (per-patch numpy + the C kernel, 1 thread)
+    on a 96 x 96 crop of the same problem."""
+    import time as _t
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle"))
+    from paper_1511_05174_b200 import sensing as S
+    from paper_1511_05174_b200.pipelines import recover_operator
+    rng = np.random.default_rng(3)
+    h = w = 512
+    c = 3
+    img = np.cumsum(rng.standard_normal((h, w, c)), axis=0) / 8
+    a = rng.integers(1, c + 1, size=h * w)
+    op = S.make_channel_mosaic(h * w, c, a)
+    coded = op.apply(img.ravel()).reshape(h, w)
+    patch, stride = (8, 8, 3), (2, 2, 1)
+    d = rng.standard_normal((192, 384))
+    d /= np.linalg.norm(d, axis=0)
+    recover_operator(coded, op, patch, stride, dictionary=d, sparsity=6)  # warm-up
+    t0 = _t.perf_counter()
+    _, met, _ = recover_operator(coded, op, patch, stride, dictionary=d, sparsity=6)
+    el = _t.perf_counter() - t0
+    out = {"workload": "512x512x3 image, random channel mosaic, 8x8x3 patches stride 2, "
+                       "K=6 over 384 atoms (exact engine, coded rows)",
+           "patches": met.patch_count, "ms": el * 1e3, "patches_per_s": met.patch_count / el}
+    if not no_cpu:
+        import operator_oracle as OO
+        hs = 96
+        g = dict(kind="channel-mosaic", assignment=a.reshape(h, w)[:hs, :hs].ravel(), channels=c,
+                 sig_shape=np.array((hs, hs, c)), patch=np.array(patch), stride=np.array(stride),
+                 meas=coded[:hs, :hs], method="omp-single", atoms=d, k=6)
+        t1 = _t.perf_counter()
+        OO.recover(g)
+        pc = ((hs - 8) // 2 + 1) ** 2
+        out["cpu_reference_patches_per_s"] = pc / (_t.perf_counter() - t1)
+        out["cpu_kind"] = ("port (oracle/operator_oracle.py: the reference's per-patch "
+                           "slicing + the C kernel restatement, 1 thread, 96x96 crop)")
+    return out
 
 
 def bench_ksvd_update(no_cpu=False):

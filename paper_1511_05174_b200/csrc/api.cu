@@ -205,6 +205,13 @@ constexpr int64_t kGramSmemLimit = 100 * 1024;       // per-warp smem for H in s
 constexpr int64_t kGramPreferBytes = 24 * 1024;      // auto: gram over resident below this
 constexpr int64_t kScratchBudget = int64_t(4) << 30;  // per-call global scratch cap
 
+// Warps per SM for exact-engine launches: the kernel is latency-bound (a warp
+// per signal), so as many as its registers allow (CDB_EXACT_WPS overrides).
+int64_t exact_warps_per_sm() {
+  static const int64_t w = getenv("CDB_EXACT_WPS") ? atoll(getenv("CDB_EXACT_WPS")) : 16;
+  return w > 0 ? w : 16;
+}
+
 // Run the exact engine over `count` signals (all, or the ids in sig_ids).
 cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t count,
                      const int64_t *sig_ids, int64_t k_max, int64_t kw, const double *eps,
@@ -238,7 +245,7 @@ cdb_status run_exact(const cdb_dictionary *d, const void *ys, bool f32, int64_t 
   a.out_flag = (uint8_t *)o.flag.dev;
   a.work_stride = cdb::exact_work_stride(d->n, kw, max_cands);
   // a device-side count is usually tiny (delegations are rare): few warps
-  const int64_t wmax = count_dev ? (int64_t)di.sms : (int64_t)di.sms * 8;
+  const int64_t wmax = count_dev ? (int64_t)di.sms : (int64_t)di.sms * exact_warps_per_sm();
   int64_t warps = count < wmax ? count : wmax;
   const int64_t cap = kScratchBudget / (8 * a.work_stride);
   if (warps > cap) warps = cap < 4 ? 4 : cap;
