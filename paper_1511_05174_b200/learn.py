@@ -18,6 +18,7 @@ binds this function as ``crossdict.learn._code_stage``.
 
 from __future__ import annotations
 
+import math
 import time
 from dataclasses import dataclass, field
 
@@ -61,11 +62,32 @@ def code_stage(d, y, k, allowed_sets, block_hint):
                                               _pursuit.ENGINE)
         solve = _pursuit._make_batch(t, o)
         return [solve.result(p) for p in range(m)]
-    return [
-        _pursuit.omp(d, y[:, p], PursuitConfig(min(k, len(allowed_sets[p])),
-                                               allowed_support=frozenset(allowed_sets[p])))
-        for p in range(m)
-    ]
+    # arbitrary per-sample sets (the reference runs one scalar omp per sample,
+    # learn.py:258-261): ONE ragged call with Q = 1 -- the "blocks" are the
+    # sorted allowed atom ids, the budget min(k, |set|, N) per sample
+    n, t = d.shape
+    if m == 0:
+        return []
+    for s_ in allowed_sets:
+        if min(k, len(s_)) > min(n, t):
+            raise E.ConfigError(f"sparsity_budget {min(k, len(s_))} exceeds min(N, T) = {min(n, t)}")
+    sizes = np.array([len(s_) for s_ in allowed_sets], dtype=np.int64)
+    width = max(1, int(sizes.max()))
+    ids = np.zeros((m, width), dtype=np.int64)
+    for p, s_ in enumerate(allowed_sets):
+        srt = np.sort(np.fromiter(s_, dtype=np.int64, count=len(s_))) - 1
+        if srt.size and (srt[0] < 0 or srt[-1] >= t):
+            raise E.DomainError("allowed_support index outside [1, T]")
+        ids[p, :srt.size] = srt
+    ys_rows = np.ascontiguousarray(y.T)
+    # scalar omp's tolerance: REL * np.linalg.norm(y_p) = REL * sqrt(y_p . y_p)
+    eps = _pursuit._rel_tol() * np.array([math.sqrt(r.dot(r)) for r in ys_rows])
+    k_out = int(max(1, min(k, width, n)))
+    dd = _dev.device_dictionary(np.ascontiguousarray(d.T))
+    o = _dev.omp_batch_blocked_ragged_raw(dd, ys_rows, m, k_out, eps, ids, sizes, 1,
+                                          _pursuit.ENGINE)
+    solve = _pursuit._make_batch(t, o)
+    return [solve.result(p) for p in range(m)]
 
 
 def update_stage(y, d, x, threshold: int):

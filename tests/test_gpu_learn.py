@@ -44,3 +44,32 @@ def test_explicit_allowed_sets_coding_stage():
     k = int(G["k"])
     sets = [set(int(j) for j in row if j >= 0) for row in G["sets_list"]]
     _check(code_stage(G["d"], G["y"][:, :24], k, sets, None), "sets", k)
+
+
+def test_code_stage_arbitrary_sets_batched():
+    """Per-sample allowed sets without a block hint (learn.py:258-261: one
+    scalar omp per sample in the reference) run as ONE ragged device call;
+    each sample matches the oracle's restricted OMP over its sorted set."""
+    import math
+
+    import oracle as O
+    from parity import compare
+    from paper_1511_05174_b200.learn import code_stage
+    rng = np.random.default_rng(17)
+    n, t, m, k = 24, 60, 50, 5
+    d = rng.standard_normal((n, t))
+    d /= np.linalg.norm(d, axis=0)
+    y = rng.standard_normal((n, m))
+    sets = [frozenset((rng.choice(t, size=int(rng.integers(3, 30)), replace=False) + 1).tolist())
+            for _ in range(m)]
+    res = code_stage(d, y, k, sets, None)
+    for p in range(m):
+        allowed = np.array(sorted(sets[p]), dtype=np.int64)[None, :] - 1
+        kp = min(k, len(sets[p]))
+        eps = np.array([1e-6 * math.sqrt(y[:, p].dot(y[:, p]))])
+        sel, coef, cnt, rn, sc, fl = O.omp_batch(np.ascontiguousarray(d.T), y[:, p][None, :], kp,
+                                                 eps, allowed)
+        got = res[p]
+        assert list(got.selected) == (sel[0, :cnt[0]] + 1).tolist()
+        assert got.atom_scan_count == int(sc[0])
+        np.testing.assert_allclose(got.residual_norm, rn[0], rtol=1e-9)
