@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t opaque0 = (uint32_t)threadIdx.x >> 16;  // 0 at runtime
 #pragma unroll
     for (int i = 0; i < 64; i++) cid[i >> 5][i & 31] = opaque0 + (uint32_t)i;
+    const uint32_t k63 = 63u + opaque0;  // kept in a register
     for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
       float val[NCAND];
       int idx[NCAND];
@@ -246,12 +247,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int hh = 0; hh < 2; hh++) {
             if (jbase + 32 * hh + 32 <= t) {
 #pragma unroll
-              for (int i = 0; i < 32; i++) {
-                const uint32_t key = (__float_as_uint(v[hh][i]) & 0x7FFFFFC0u) | cid[hh][i];
-                const uint32_t m = min(c1, key);
-                c1 = max(c1, key);
-                rest = max(rest, min(c2, m));
-                c2 = max(c2, m);
+              for (int i = 0; i < 32; i += 2) {
+                // (bits | 63) & (0x7FFFFFC0 | id) == (bits & 0x7FFFFFC0) | id: one LOP3
+                // (63 in a register, the id folded into the immediate)
+                uint32_t ka, kb;
+                asm("lop3.b32 %0, %1, %2, %3, 0xA8;"
+                    : "=r"(ka)
+                    : "r"(__float_as_uint(v[hh][i])), "r"(k63), "r"(0x7FFFFFC0u | (uint32_t)(32 * hh + i)));
+                asm("lop3.b32 %0, %1, %2, %3, 0xA8;"
+                    : "=r"(kb)
+                    : "r"(__float_as_uint(v[hh][i + 1])), "r"(k63),
+                      "r"(0x7FFFFFC0u | (uint32_t)(32 * hh + i + 1)));
+                // merge the sorted pair (hi, lo) into (c1 >= c2) and `rest`:
+                // c2' = max(min(c1,hi), c2, lo), third = max(min(c1,lo), min(c2,hi))
+                const uint32_t hi = max(ka, kb), lo = min(ka, kb);
+                const uint32_t n2 = max(max(min(c1, hi), c2), lo);
+                rest = max(max(rest, min(c1, lo)), min(c2, hi));
+                c1 = max(c1, hi);
+                c2 = n2;
               }
             } else {
 #pragma unroll
