@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(1024, 1)
   double *wv = zv + kw;
   double *gv = wv + kw;
   int *sup = (int *)(gv + 2 * kw);
+  int *soff = sup + kw;  // sup[l] * n: 32-bit row offsets of the support atoms
   const double *d64 = a.d64;
   const double *gram = a.gram;
 
@@ -618,7 +619,10 @@ __global__ void __launch_bounds__(1024, 1)
       // ---- Cholesky append through the Gram row (as resident_omp_kernel)
       const double *grow = gram + (int64_t)nid * T;
       for (int l = lane; l < k; l += 32) gv[l] = __ldg(grow + sup[l]);
-      if (lane == 0) sup[k] = nid;
+      if (lane == 0) {
+        sup[k] = nid;
+        soff[k] = nid * n;
+      }
       __syncwarp();
       for (int l = lane; l < k; l += 32) {
         double accw = 0.0;
@@ -659,8 +663,9 @@ __global__ void __launch_bounds__(1024, 1)
       double rr = 0.0;
       for (int i = lane; i < n; i += 32) {
         double qv = 0.0;
+        const double *dbase = d64 + i;  // + soff[l]: one address add per term
 #pragma unroll 4
-        for (int l = 0; l <= k; l++) qv = fma(lk[l], __ldg(d64 + (int64_t)sup[l] * n + i), qv);
+        for (int l = 0; l <= k; l++) qv = fma(lk[l], __ldg(dbase + soff[l]), qv);
         const double rv = fma(-zk, qv, r[i]);
         r[i] = rv;
         rr = fma(rv, rv, rr);
