@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(1024, 1)
         const float av = live && i < n ? (float)r[i] : 0.0f;
         const uint32_t hi = to_tf32(av);
         Ahi[warp * MM_AS + i] = __uint_as_float(hi);
-        Alo[warp * MM_AS + i] = __uint_as_float(to_tf32(av - __uint_as_float(hi)));
+        Alo[warp * MM_AS + i] = av - __uint_as_float(hi);  // unrounded (see blo)
       }
       if (!__syncthreads_or(live)) break;
       {  // ---- C = A B: warp w computes m-tile (w & 1), n-tiles 2 (w >> 1) + {0, 1}
@@ -543,8 +543,10 @@ __global__ void __launch_bounds__(1024, 1)
             const float b0 = Bs[(k0 + tq) * MM_BS + nt * 8 + g];
             const float b1 = Bs[(k0 + tq + 4) * MM_BS + nt * 8 + g];
             const uint32_t bhi[2] = {to_tf32(b0), to_tf32(b1)};
-            const uint32_t blo[2] = {to_tf32(b0 - __uint_as_float(bhi[0])),
-                                     to_tf32(b1 - __uint_as_float(bhi[1]))};
+            // the low part enters the MMA unrounded: the tensor core drops its
+            // low 13 mantissa bits, <= 2^-21 |b|, far inside E (2^-15)
+            const uint32_t blo[2] = {__float_as_uint(b0 - __uint_as_float(bhi[0])),
+                                     __float_as_uint(b1 - __uint_as_float(bhi[1]))};
             mma_tf32(dd, alo, bhi);
             mma_tf32(dd, ahi, blo);
             mma_tf32(dd, ahi, bhi);
