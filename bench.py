@@ -352,6 +352,26 @@ def bench_ours(args):
     e2e_total = float(t.item())
     h2d = P * w.n_signal * 4
     d2h = sum(v.numel() * v.element_size() for o in (hlo, hhi) for v in o.values())
+    # full OMP end to end: the same C-ABI call with pinned host signals,
+    # tolerances and outputs (the library pipelines chunked H2D / compute / D2H)
+    hfull = outs(w.k, "cpu", True)
+    hfull_n = npv(hfull)
+    eps_h = eps_full.cpu().numpy()
+    D.omp_batch_raw(hi, yh_n, P, w.k, eps_h, None, "auto", hfull_n)
+    e2e_full_total = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        D.omp_batch_raw(hi, yh_n, P, w.k, eps_h, None, "auto", hfull_n)
+        e2e_full_total += time.perf_counter() - t0
+    t = torch.tensor([e2e_full_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_full_total = float(t.item())
+    d2h_full = sum(v.numel() * v.element_size() for v in hfull.values())
 
     # ---- roofline of the dominant kernel (zero-tree step), algorithmic flops
     peaks, peaks_kind = load_peaks()
@@ -423,7 +443,10 @@ def bench_ours(args):
                        "signals_per_gpu": P, "l2": "flushed between steps (256 MiB write)"},
             "full_omp": {"value": full_value, "unit": "signals/s",
                          "ms_per_step": full_ms / args.steps, "engine": engine_full[0],
-                         "roofline": full_roof},
+                         "roofline": full_roof,
+                         "e2e": {"value": world * P * args.steps / e2e_full_total,
+                                 "unit": "signals/s", "h2d_bytes_per_step": h2d + P * 8,
+                                 "d2h_bytes_per_step": d2h_full}},
             "roofline": roofline,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_zt.items()},
             "kernels_full_ms_per_step": {k: v[0] / args.steps for k, v in prof_full.items()},

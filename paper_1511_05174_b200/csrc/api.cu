@@ -467,7 +467,9 @@ cudaStream_t copy_stream(int which) {
 // a small last chunk (its D2H cannot), and the rest in as few chunks as
 // possible -- each call carries ~0.1-0.3 ms of fixed cost (launch gaps,
 // partial waves), so many small chunks lose more than they hide.
-std::vector<int64_t> chunk_bounds(int64_t p) {
+// kind 0: zero-tree calls; kind 1: OMP batches (the tensor engine's 16-
+// iteration chunks carry more fixed cost, so fewer, larger chunks).
+std::vector<int64_t> chunk_bounds(int64_t p, int kind) {
   if (const char *sched = getenv("CDB_PIPE_SCHEDULE")) {  // "w1,w2,...": relative chunk sizes
     std::vector<double> w;
     double tot = 0.0;
@@ -493,13 +495,18 @@ std::vector<int64_t> chunk_bounds(int64_t p) {
     }
   }
   if (p >= 50000 && !getenv("CDB_PIPE_CHUNK") && !getenv("CDB_PIPE_EDGE")) {
-    // measured best for 100k (5.85 vs 6.0 ms, three runs each): ~9.5% first
-    // chunk (its H2D is exposed), two middle chunks, ~10% last (exposed D2H)
-    const double w[4] = {0.0947, 0.4262, 0.3789, 0.1002};
+    // measured best for 100k: zero-tree ~9.5% first chunk (its H2D is
+    // exposed), two middle chunks, ~10% last (5.85 vs 6.0 ms for [20k, 60k,
+    // 20k]); full OMP 15% / 85% (8.96 vs 9.20 ms for [20k, 60k, 20k], 10.6 ms
+    // with the zero-tree ramp)
+    static const double wz[4] = {0.0947, 0.4262, 0.3789, 0.1002};
+    static const double wo[2] = {0.15, 0.85};
+    const double *w = kind == 0 ? wz : wo;
+    const int nw = kind == 0 ? 4 : 2;
     std::vector<int64_t> b = {0};
     double acc = 0.0;
-    for (double x : w) {
-      acc += x;
+    for (int i = 0; i < nw; i++) {
+      acc += w[i];
       b.push_back((int64_t)(p * acc));
     }
     b.back() = p;
@@ -525,8 +532,9 @@ std::vector<int64_t> chunk_bounds(int64_t p) {
 }
 
 template <typename Core>
-cdb_status run_pipelined(int64_t p, std::vector<RowArr> &arrs, cudaStream_t st, Core core) {
-  const std::vector<int64_t> bd = chunk_bounds(p);
+cdb_status run_pipelined(int64_t p, std::vector<RowArr> &arrs, cudaStream_t st, Core core,
+                          int kind = 0) {
+  const std::vector<int64_t> bd = chunk_bounds(p, kind);
   const int64_t nch = (int64_t)bd.size() - 1;
   int64_t chunk = 0;
   for (int64_t i = 0; i < nch; i++) chunk = std::max(chunk, bd[i + 1] - bd[i]);
@@ -1128,7 +1136,7 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
       dev_outs(o, dv[3], dv[4], dv[5], dv[6], dv[7], dv[8]);
       return run_omp(dict, dv[0], f32, len, k_max, k_max, (const double *)dv[1], c, max_c0, o,
                      engine, di, s2);
-    });
+    }, 1);
   }
   InArr y_in, e_in, id_in, nb_in;
   CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));
