@@ -116,7 +116,7 @@ __device__ void back_substitute(const double *h, int kd, const double *zv, const
 // updates its own candidates, and accumulates |w|^2 redundantly, so an
 // iteration has no triangular solve and a single cross-lane reduction
 // (the argmax).
-template <typename YT, int U>
+template <typename YT, int U, bool HSM>
 __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
     gram_omp_kernel(GramArgs a, const YT *__restrict__ ys, int h_in_smem, int64_t smem_per_warp) {
   constexpr int HS = 32 * U;
@@ -136,7 +136,10 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   int64_t *sup = (int64_t *)(iv + 2 * kw);
   double *xv = (double *)(sup + kw);
   double *region = xv + kw + ((5 * kw) & 1);  // even offset: 16-byte H accesses
-  double *h = h_in_smem ? region : a.hwork + local * kw * HS;
+  // HSM: H in shared memory, known at compile time so its accesses are LDS/STS
+  // rather than generic loads
+  double *h = HSM ? region : a.hwork + local * kw * HS;
+  (void)h_in_smem;
   const YT *yg = ys + p * a.ys_stride;
 
   const int S = (int)cs.count(p);
@@ -225,7 +228,10 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       const double cj = __shfl_sync(CDB_FULL_MASK, my_c, owner);
       if (lane == owner) tk |= 1u << ub;
       // ---- Gram row slice G[C, j*] (independent loads), then H update
-      const double *grow = a.gram + nid * T;
+      // 32-bit row offset when the Gram matrix has < 2^31 entries
+      const double *grow = a.gram + (T * T < (int64_t(1) << 31)
+                                         ? (int64_t)((uint32_t)nid * (uint32_t)T)
+                                         : nid * T);
       double hacc[U];
 #pragma unroll
       for (int u = 0; u < U; u++) hacc[u] = lane + 32 * u < S ? __ldg(grow + cid[u]) : 0.0;
@@ -329,16 +335,23 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   }
 }
 
+template <typename YT, int U, bool HSM>
+cudaError_t launch_gram_tuh(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
+                            int wpb, int64_t blocks, cudaStream_t stream) {
+  const int64_t smem = per_warp * wpb;
+  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, U, HSM>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gram_omp_kernel<YT, U, HSM><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
+                                                                            per_warp);
+  return cudaGetLastError();
+}
+
 template <typename YT, int U>
 cudaError_t launch_gram_tu(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
                            int wpb, int64_t blocks, cudaStream_t stream) {
-  const int64_t smem = per_warp * wpb;
-  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, U>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  gram_omp_kernel<YT, U><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
-                                                                       per_warp);
-  return cudaGetLastError();
+  return h_in_smem ? launch_gram_tuh<YT, U, true>(args, ys, h_in_smem, per_warp, wpb, blocks, stream)
+                   : launch_gram_tuh<YT, U, false>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
 }
 
 template <typename YT>
