@@ -610,7 +610,8 @@ __global__ void __launch_bounds__(1024, 1)
       double cbest;
       {  // the winner's exact correlation (z_k = c / d); orthogonal break on it
         double c = 0.0;
-        for (int i = lane; i < n; i += 32) c = fma(__ldg(d64 + (int64_t)nid * n + i), r[i], c);
+        const double *drow = d64 + (uint32_t)(nid * n);  // T * n < 2^31 here (T <= 256)
+        for (int i = lane; i < n; i += 32) c = fma(__ldg(drow + i), r[i], c);
         cbest = warp_sum(c);
       }
       if (!(fabs(cbest) > 0.0)) {  // _kernels.py:104
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(1024, 1)
       }
       if (lane == owner) tk |= 1u << ub;
       // ---- Cholesky append through the Gram row (as resident_omp_kernel)
-      const double *grow = gram + (int64_t)nid * T;
+      const double *grow = gram + (uint32_t)(nid * T);  // T <= 256: 32-bit offsets
       for (int l = lane; l < k; l += 32) gv[l] = __ldg(grow + sup[l]);
       if (lane == 0) {
         sup[k] = nid;
