@@ -513,12 +513,109 @@ cudaError_t launch_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets
   return cudaGetLastError();
 }
 
+// Q = 8 on the fp64 tensor cores: a warp codes 8 pairs at once as one 8x8
+// tile C[child][pair] = sum_k D[child][k] y_pair[k] of m8n8k4 DMMA steps.
+// Lane (r = lane>>2, j = lane&3) supplies A[r][j] = child r and B[j][r] =
+// pair r at coordinate 16 t + 4 j + e of step 4 t + e -- the same k
+// permutation on both sides -- so each pair row is read with one 16-B load
+// per 16 coordinates and no cross-lane reduction is needed.
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename YT, int NT>  // NT = N / 16
+__global__ void __launch_bounds__(128) alpha0_mma_kernel(
+    const double *__restrict__ d64, int n, const YT *__restrict__ ys,
+    const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t smax, int split,
+    int t_low, double *__restrict__ alpha0) {
+  const int bucket = blockIdx.x / split, part = blockIdx.x % split;
+  const int parent = bucket % t_low;
+  const int64_t lo = offs[bucket], cnt = offs[bucket + 1] - lo;
+  const int64_t a = lo + cnt * part / split, b = lo + cnt * (part + 1) / split;
+  if (a >= b) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int r = lane >> 2, j = lane & 3;
+  double ch[4 * NT];
+  {
+    const double *src = d64 + ((int64_t)parent * 8 + r) * n + 4 * j;
+#pragma unroll
+    for (int t = 0; t < NT; t++) {
+      const double2 u = __ldg(reinterpret_cast<const double2 *>(src + 16 * t));
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(src + 16 * t + 2));
+      ch[4 * t + 0] = u.x;
+      ch[4 * t + 1] = u.y;
+      ch[4 * t + 2] = v.x;
+      ch[4 * t + 3] = v.y;
+    }
+  }
+  // warp w takes a contiguous run of whole 8-pair tiles
+  const int64_t per = ((b - a + 8 * nwarps - 1) / (8 * nwarps)) * 8;
+  const int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
+  for (int64_t e0 = wa; e0 < wb; e0 += 8) {
+    const int m = wb - e0 < 8 ? (int)(wb - e0) : 8;
+    const int64_t pr = pairs[e0 + (r < m ? r : m - 1)];
+    const YT *y = ys + (pr >> 16) * n + 4 * j;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < NT; t++) {
+      double yv[4];
+      if constexpr (sizeof(YT) == 4) {
+        const float4 f = *reinterpret_cast<const float4 *>(y + 16 * t);
+        yv[0] = f.x;
+        yv[1] = f.y;
+        yv[2] = f.z;
+        yv[3] = f.w;
+      } else {
+        const double2 u = *reinterpret_cast<const double2 *>(y + 16 * t);
+        const double2 v = *reinterpret_cast<const double2 *>(y + 16 * t + 2);
+        yv[0] = u.x;
+        yv[1] = u.y;
+        yv[2] = v.x;
+        yv[3] = v.y;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; e++) dmma_8x8x4(c0, c1, ch[4 * t + e], yv[e]);
+    }
+    // lane holds child r of pairs 2j and 2j + 1 (pair q's id sits in lane 4q)
+    const int64_t p0 = __shfl_sync(CDB_FULL_MASK, (long long)pr, 8 * j);
+    const int64_t p1 = __shfl_sync(CDB_FULL_MASK, (long long)pr, 8 * j + 4);
+    if (2 * j < m) alpha0[(p0 >> 16) * smax + (p0 & 0xffff) * 8 + r] = c0;
+    if (2 * j + 1 < m) alpha0[(p1 >> 16) * smax + (p1 & 0xffff) * 8 + r] = c1;
+  }
+}
+
+// CDB_A0_MMA=0 keeps the FFMA warp kernel for Q = 8
+bool alpha0_mma_enabled() {
+  static const int on = [] {
+    const char *v = getenv("CDB_A0_MMA");
+    return v ? atoi(v) : 1;
+  }();
+  return on != 0;
+}
+
 // The register path when the parent's children fit 64 fp64 registers per
 // lane and N is 64, 128 or 256 (else the shared-memory kernel above).
 template <typename YT>
 bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t n, int64_t q,
                      const YT *ys, const int64_t *offs, const int64_t *pairs, int64_t k1,
                      int64_t smax, double *alpha0, cudaStream_t stream, cudaError_t &err) {
+  if (q == 8 && (n == 64 || n == 128 || n == 256) && alpha0_mma_enabled()) {
+    const int split = 8;
+    const unsigned grid = (unsigned)(buckets * split);
+    if (n == 64)
+      alpha0_mma_kernel<YT, 4><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                         split, (int)t_low, alpha0);
+    else if (n == 128)
+      alpha0_mma_kernel<YT, 8><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                         split, (int)t_low, alpha0);
+    else
+      alpha0_mma_kernel<YT, 16><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                          split, (int)t_low, alpha0);
+    err = cudaGetLastError();
+    return true;
+  }
 #define CDB_A0W(QQ, NN)                                                                      \
   if (q == QQ && n == 32 * NN) {                                                             \
     err = launch_alpha0_warp<YT, QQ, NN>(d64, t_low, buckets, n, ys, offs, pairs, k1, smax,  \
