@@ -586,6 +586,70 @@ __global__ void __launch_bounds__(128) alpha0_mma_kernel(
   }
 }
 
+// The same tiles for any N (a multiple of 16) and Q = 8 CT: the children
+// are read per step from L1 (a bucket's CTAs share one parent, Q N fp64),
+// each 16-B pair load feeding CT child tiles.
+template <typename YT, int CT>
+__global__ void __launch_bounds__(128) alpha0_mma_l1_kernel(
+    const double *__restrict__ d64, int n, const YT *__restrict__ ys,
+    const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t smax, int split,
+    int t_low, double *__restrict__ alpha0) {
+  constexpr int QT = 8 * CT;
+  const int bucket = blockIdx.x / split, part = blockIdx.x % split;
+  const int parent = bucket % t_low;
+  const int64_t lo = offs[bucket], cnt = offs[bucket + 1] - lo;
+  const int64_t a = lo + cnt * part / split, b = lo + cnt * (part + 1) / split;
+  if (a >= b) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int r = lane >> 2, j = lane & 3, nt = n >> 4;
+  const double *dc = d64 + ((int64_t)parent * QT + r) * n + 4 * j;
+  const int64_t per = ((b - a + 8 * nwarps - 1) / (8 * nwarps)) * 8;
+  const int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
+  for (int64_t e0 = wa; e0 < wb; e0 += 8) {
+    const int m = wb - e0 < 8 ? (int)(wb - e0) : 8;
+    const int64_t pr = pairs[e0 + (r < m ? r : m - 1)];
+    const YT *y = ys + (pr >> 16) * n + 4 * j;
+    double c[CT][2];
+#pragma unroll
+    for (int ct = 0; ct < CT; ct++) c[ct][0] = c[ct][1] = 0.0;
+#pragma unroll 4
+    for (int t = 0; t < nt; t++) {
+      double yv[4];
+      if constexpr (sizeof(YT) == 4) {
+        const float4 f = *reinterpret_cast<const float4 *>(y + 16 * t);
+        yv[0] = f.x;
+        yv[1] = f.y;
+        yv[2] = f.z;
+        yv[3] = f.w;
+      } else {
+        const double2 u = *reinterpret_cast<const double2 *>(y + 16 * t);
+        const double2 v = *reinterpret_cast<const double2 *>(y + 16 * t + 2);
+        yv[0] = u.x;
+        yv[1] = u.y;
+        yv[2] = v.x;
+        yv[3] = v.y;
+      }
+#pragma unroll
+      for (int ct = 0; ct < CT; ct++) {
+        const double2 u = __ldg(reinterpret_cast<const double2 *>(dc + (int64_t)ct * 8 * n + 16 * t));
+        const double2 v =
+            __ldg(reinterpret_cast<const double2 *>(dc + (int64_t)ct * 8 * n + 16 * t + 2));
+        dmma_8x8x4(c[ct][0], c[ct][1], u.x, yv[0]);
+        dmma_8x8x4(c[ct][0], c[ct][1], u.y, yv[1]);
+        dmma_8x8x4(c[ct][0], c[ct][1], v.x, yv[2]);
+        dmma_8x8x4(c[ct][0], c[ct][1], v.y, yv[3]);
+      }
+    }
+    const int64_t p0 = __shfl_sync(CDB_FULL_MASK, (long long)pr, 8 * j);
+    const int64_t p1 = __shfl_sync(CDB_FULL_MASK, (long long)pr, 8 * j + 4);
+#pragma unroll
+    for (int ct = 0; ct < CT; ct++) {
+      if (2 * j < m) alpha0[(p0 >> 16) * smax + (p0 & 0xffff) * QT + ct * 8 + r] = c[ct][0];
+      if (2 * j + 1 < m) alpha0[(p1 >> 16) * smax + (p1 & 0xffff) * QT + ct * 8 + r] = c[ct][1];
+    }
+  }
+}
+
 // CDB_A0_MMA=0 keeps the FFMA warp kernel for Q = 8
 bool alpha0_mma_enabled() {
   static const int on = [] {
@@ -613,6 +677,18 @@ bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t 
     else
       alpha0_mma_kernel<YT, 16><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
                                                           split, (int)t_low, alpha0);
+    err = cudaGetLastError();
+    return true;
+  }
+  if ((q == 8 || q == 16) && n % 16 == 0 && q * n <= 16384 && alpha0_mma_enabled()) {
+    const int split = 8;
+    const unsigned grid = (unsigned)(buckets * split);
+    if (q == 8)
+      alpha0_mma_l1_kernel<YT, 1><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                            split, (int)t_low, alpha0);
+    else
+      alpha0_mma_l1_kernel<YT, 2><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                            split, (int)t_low, alpha0);
     err = cudaGetLastError();
     return true;
   }
