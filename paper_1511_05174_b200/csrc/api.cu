@@ -676,6 +676,16 @@ cudaEvent_t prof_event() {
 namespace cdb {
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+bool prof_active() { return g_prof_on.load(std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("CDB_PDL");
+    return v ? atoi(v) != 0 : true;
+  }();
+  return on;
+}
+
 void prof_begin(const char *name, cudaStream_t stream) {
   if (!g_prof_on.load(std::memory_order_relaxed)) return;
   ProfRec r{name, prof_event(), prof_event()};

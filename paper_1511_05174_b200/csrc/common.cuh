@@ -26,6 +26,12 @@ constexpr double GRAM_DELEGATE_D2 = 1e-8;
 template <typename T>
 __device__ __forceinline__ double ld_f64(const T *p) { return (double)(*p); }
 
+// Programmatic dependent launch (no-ops when the grid was launched without it)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CDB_FULL_MASK, v, o);

@@ -1,5 +1,6 @@
 // Internal engine interfaces (host side) of the crossdict B200 library.
 #pragma once
+#include <utility>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -13,6 +14,27 @@ void note_launch(int n = 1);
 // stream around each kernel launch, summed per kernel name.
 void prof_begin(const char *name, cudaStream_t stream);
 void prof_end(const char *name, cudaStream_t stream);
+bool prof_active();  // per-kernel events are being recorded
+bool pdl_enabled();  // CDB_PDL (default 1): programmatic dependent launch
+
+// Launch `kern` with the programmatic-stream-serialization attribute when
+// `pdl`: the kernel may start while its predecessor drains, and must call
+// griddep_wait() before reading the predecessor's output.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block,
+                     size_t smem, cudaStream_t stream, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 struct ProfScope {
   const char *name;
   cudaStream_t stream;

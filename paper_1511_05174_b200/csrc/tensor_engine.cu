@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                      int n_kchunks, int64_t m_tiles, const int *__restrict__ active,
                      int *__restrict__ cand_idx, float *__restrict__ cand_val,
                      float *__restrict__ cand_drop) {
+  griddep_wait();  // the previous kernel's residuals and active count (PDL)
+  griddep_launch();
   if (active && *active == 0) return;  // every signal already finished
   using Smem = typename std::conditional<A_RES, CorrSmemRes, CorrSmemStr>::type;
   constexpr int NST = A_RES ? RES_BSTAGES : STR_STAGES;
@@ -738,6 +740,8 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
     int kw, int iter, double c_err, double dmax, TensorState st, int64_t *out_sel,
     double *out_coef, int64_t *out_count, int64_t *out_scans, int resume, int split) {
   constexpr int NG = 32 / G;
+  griddep_wait();  // the scan's candidates (PDL)
+  griddep_launch();
   extern __shared__ double lsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gi = lane / G, gl = lane % G;
@@ -1788,6 +1792,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     if ((e = set((const void *)ls_group_kernel<double, 32>)) != cudaSuccess) return e;
   }
   const bool tiled = rescan_tiled(t, n, a.k_max);
+  // programmatic dependent launch for the scan / least-squares pairs (not
+  // while per-kernel events are recorded: they would time the overlap)
+  const bool pdl = pdl_enabled() && !prof_active();
   // large N: build the scan operand in its own kernel (CDB_LS_SPLIT=0|1 overrides)
   int split = n > 256 ? 1 : 0;
   if (const char *v = getenv("CDB_LS_SPLIT")) split = atoi(v) ? 1 : 0;
@@ -1797,9 +1804,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     {
     ProfScope _ps("corr_topk", stream);
     auto kern = a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>;
-    kern<<<corr_grid, THREADS, corr_smem, stream>>>(tm_a, tm_b, p, t, (int)(n_pad / BK), m_tiles,
-                                                    it ? st.active + it - 1 : nullptr, cidx, cval,
-                                                    cdrop);
+    e = launch_k(pdl, kern, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
+                 (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, cidx, cval, cdrop);
+    if (e != cudaSuccess) return e;
     }
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1819,45 +1826,45 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         const unsigned grid = resume ? (unsigned)(a.num_sms * 4) : lsg_grid;
         if (lsg_g == 8) {
           if (a.ys_f32)
-            ls_group_kernel<float, 8><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<float, 8>, grid, 128, lsg_smem, stream,
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
           else
-            ls_group_kernel<double, 8><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<double, 8>, grid, 128, lsg_smem, stream,
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
         } else if (lsg_g == 16 && n <= 256) {
           if (a.ys_f32)
-            ls_group_kernel<float, 16, 16><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<float, 16, 16>, grid, 128, lsg_smem, stream,
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
           else
-            ls_group_kernel<double, 16, 16><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<double, 16, 16>, grid, 128, lsg_smem, stream,
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
         } else if (lsg_g == 16) {
           if (a.ys_f32)
-            ls_group_kernel<float, 16><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<float, 16>, grid, 128, lsg_smem, stream,
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
           else
-            ls_group_kernel<double, 16><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<double, 16>, grid, 128, lsg_smem, stream,
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
         } else {
           if (a.ys_f32)
-            ls_group_kernel<float, 32><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<float, 32>, grid, 128, lsg_smem, stream,
                 (const float *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
           else
-            ls_group_kernel<double, 32><<<grid, 128, lsg_smem, stream>>>(
+            e = launch_k(pdl, ls_group_kernel<double, 32>, grid, 128, lsg_smem, stream,
                 (const double *)a.ys, a.d64, a.d32, a.gram, p, t, (int)n, n_pad, (int)a.k_max,
                 (int)kw, it, c_err, a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans,
                 resume, split);
@@ -1873,6 +1880,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
               (const double *)a.ys, a.d64, a.d32, a.gram, p, t, n, n_pad, a.k_max, kw, it, c_err,
               a.dmax, st, a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
       }
+      if (e != cudaSuccess) return e;
       note_launch();
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
