@@ -39,6 +39,7 @@ TAGS = {
     "resident_mma": "resident_step1",
     "gram_omp": "gram_step2",
     "alpha0_warp": "route_alpha0",
+    "alpha0_mma": "route_alpha0",
     "downsample": "downsample",
     "corr_topk": "corr_topk",
     "ls_group": "ls_step",

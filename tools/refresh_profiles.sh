@@ -9,7 +9,7 @@ python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err || { echo "bench
 tail -1 gpurun_out/bench.json | cut -c1-300
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-for k in resident_mma gram_omp alpha0_warp downsample corr_topk ls_group; do
+for k in resident_mma gram_omp alpha0_mma downsample corr_topk ls_group; do
   ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o gpurun_out/full_$k \
       python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full_$k.log 2>&1
 done
