@@ -11,6 +11,7 @@ import pytest
 from parity import compare
 
 import oracle as O
+from paper_1511_05174_b200 import _native as N
 from paper_1511_05174_b200 import device as D
 
 pytestmark = pytest.mark.gpu
@@ -111,3 +112,35 @@ def test_random_zero_tree_phi(m, t_low, q, k1, k2):
     lo, hi, ms = D.zero_tree_raw(D.DeviceDictionary(e_low), D.DeviceDictionary(e_high), None, None,
                                  ys, ys.shape[0], kb, k2, 1e-3, True, "auto")
     _check_zt(e_low, e_high, q, ys, _dev_outs(lo), _dev_outs(hi), rl, rh, kb)
+
+
+# Q and N that select each routed-alpha0 kernel (the Gram engine for step 2
+# forced, so alpha0 always comes from the routing): the DMMA tiles with the
+# children in registers (Q = 8, N <= 256), from L1 (Q = 8 above N = 256,
+# Q = 16), and the FFMA warp kernel (Q = 4).
+ROUTED = [  # fine_shape, factors, T_low, Q, k_low, k_high, P
+    ((8, 16), (2, 2), 20, 8, 4, 8, 64),
+    ((8, 8, 8), (2, 2, 2), 24, 8, 4, 8, 64),
+    ((16, 16), (2, 2), 12, 16, 4, 8, 64),
+    ((8, 8), (2, 2), 16, 4, 4, 6, 64),
+]
+
+
+@pytest.mark.parametrize("case", ROUTED)
+@pytest.mark.parametrize("f32", [True, False])
+def test_routed_alpha0_kernels(case, f32):
+    fine, fac, t_low, q, k1, k2, p = case
+    d_low, d_high = _model(fine, fac, t_low, q, 7 * t_low + q)
+    ys = _signals(d_high, q, k1, p, t_low + 1)
+    if f32:
+        ys = ys.astype(np.float32).astype(np.float64)
+    rl, rh = O.zero_tree_many_arrays(d_low, d_high, fine, fac, k1, k2, ys, rel_tol=1e-3)
+    N.profile_enable(True)
+    lo, hi, ms = D.zero_tree_raw(D.DeviceDictionary(d_low), D.DeviceDictionary(d_high), fine, fac,
+                                 ys.astype(np.float32) if f32 else ys, p, k1, k2, 1e-3, False,
+                                 "gram")
+    prof = N.profile_read()
+    N.profile_enable(False)
+    assert "route_alpha0" in prof, sorted(prof)
+    yl = O.downsample_rows(ys, fine, fac)
+    _check_zt(d_low, d_high, q, ys, _dev_outs(lo), _dev_outs(hi), rl, rh, k1, yl)
