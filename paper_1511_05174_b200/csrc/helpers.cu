@@ -525,11 +525,28 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Pull the next tile's pair rows into L1 while the current tile is coded
+// (the rows are L2-resident; this hides the L2 latency of the next tile).
+// Used by the register-children kernel (cfg 1: 0.451 -> 0.423 ms); the L1
+// kernel measured slower with it (its children compete for L1).
+template <typename YT>
+__device__ __forceinline__ void prefetch_tile(const int64_t *__restrict__ pairs,
+                                              const YT *__restrict__ ys, int n, int64_t e1,
+                                              int64_t wb, int r, int j, int len) {
+  if (e1 >= wb) return;
+  const int mn = wb - e1 < 8 ? (int)(wb - e1) : 8;
+  const int64_t pn = pairs[e1 + (r < mn ? r : mn - 1)];
+  const char *row = reinterpret_cast<const char *>(ys + (pn >> 16) * n);
+  const int bytes = len * (int)sizeof(YT);
+  for (int o = j * 128; o < bytes; o += 4 * 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(row + o));
+}
+
 template <typename YT, int NT>  // NT = N / 16
 __global__ void __launch_bounds__(128) alpha0_mma_kernel(
     const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t smax, int split,
-    int t_low, double *__restrict__ alpha0) {
+    int t_low, double *__restrict__ alpha0, int pf) {
   const int bucket = blockIdx.x / split, part = blockIdx.x % split;
   const int parent = bucket % t_low;
   const int64_t lo = offs[bucket], cnt = offs[bucket + 1] - lo;
@@ -557,6 +574,7 @@ __global__ void __launch_bounds__(128) alpha0_mma_kernel(
     const int m = wb - e0 < 8 ? (int)(wb - e0) : 8;
     const int64_t pr = pairs[e0 + (r < m ? r : m - 1)];
     const YT *y = ys + (pr >> 16) * n + 4 * j;
+    if (pf) prefetch_tile(pairs, ys, n, e0 + 8, wb, r, j, 16 * NT);
     double c0 = 0.0, c1 = 0.0;
 #pragma unroll
     for (int t = 0; t < NT; t++) {
@@ -593,7 +611,7 @@ template <typename YT, int CT>
 __global__ void __launch_bounds__(128) alpha0_mma_l1_kernel(
     const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t smax, int split,
-    int t_low, double *__restrict__ alpha0) {
+    int t_low, double *__restrict__ alpha0, int pf) {
   constexpr int QT = 8 * CT;
   const int bucket = blockIdx.x / split, part = blockIdx.x % split;
   const int parent = bucket % t_low;
@@ -609,6 +627,7 @@ __global__ void __launch_bounds__(128) alpha0_mma_l1_kernel(
     const int m = wb - e0 < 8 ? (int)(wb - e0) : 8;
     const int64_t pr = pairs[e0 + (r < m ? r : m - 1)];
     const YT *y = ys + (pr >> 16) * n + 4 * j;
+    if (pf) prefetch_tile(pairs, ys, n, e0 + 8, wb, r, j, n);
     double c[CT][2];
 #pragma unroll
     for (int ct = 0; ct < CT; ct++) c[ct][0] = c[ct][1] = 0.0;
@@ -665,18 +684,22 @@ template <typename YT>
 bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t n, int64_t q,
                      const YT *ys, const int64_t *offs, const int64_t *pairs, int64_t k1,
                      int64_t smax, double *alpha0, cudaStream_t stream, cudaError_t &err) {
+  static const int pf = [] {
+    const char *v = getenv("CDB_A0_PF");
+    return v ? atoi(v) : 1;
+  }();
   if (q == 8 && (n == 64 || n == 128 || n == 256) && alpha0_mma_enabled()) {
     const int split = 8;
     const unsigned grid = (unsigned)(buckets * split);
     if (n == 64)
       alpha0_mma_kernel<YT, 4><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
-                                                         split, (int)t_low, alpha0);
+                                                         split, (int)t_low, alpha0, pf);
     else if (n == 128)
       alpha0_mma_kernel<YT, 8><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
-                                                         split, (int)t_low, alpha0);
+                                                         split, (int)t_low, alpha0, pf);
     else
       alpha0_mma_kernel<YT, 16><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
-                                                          split, (int)t_low, alpha0);
+                                                          split, (int)t_low, alpha0, pf);
     err = cudaGetLastError();
     return true;
   }
@@ -685,10 +708,10 @@ bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t 
     const unsigned grid = (unsigned)(buckets * split);
     if (q == 8)
       alpha0_mma_l1_kernel<YT, 1><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
-                                                            split, (int)t_low, alpha0);
+                                                            split, (int)t_low, alpha0, 0);
     else
       alpha0_mma_l1_kernel<YT, 2><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
-                                                            split, (int)t_low, alpha0);
+                                                            split, (int)t_low, alpha0, 0);
     err = cudaGetLastError();
     return true;
   }
