@@ -526,20 +526,21 @@ __global__ void __launch_bounds__(1024, 1)
       }
       if (!__syncthreads_or(live)) break;
       {  // ---- C = A B: warp w computes m-tile (w & 1), n-tiles 2 (w >> 1) + {0, 1}
+        // (k-steps outer: each A fragment is loaded once for both n-tiles)
         const int mt = warp & 1, g = lane >> 2, tq = lane & 3;
+        float dd[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
 #pragma unroll
-        for (int nn = 0; nn < 2; nn++) {
-          const int nt = (warp >> 1) * 2 + nn;
-          float dd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int ks = 0; ks < MM_N / 8; ks++) {
+          const int k0 = ks * 8;
+          const float *ah = Ahi + (mt * 16 + g) * MM_AS + k0 + tq;
+          const float *al = Alo + (mt * 16 + g) * MM_AS + k0 + tq;
+          const uint32_t ahi[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[8 * MM_AS]),
+                                   __float_as_uint(ah[4]), __float_as_uint(ah[8 * MM_AS + 4])};
+          const uint32_t alo[4] = {__float_as_uint(al[0]), __float_as_uint(al[8 * MM_AS]),
+                                   __float_as_uint(al[4]), __float_as_uint(al[8 * MM_AS + 4])};
 #pragma unroll
-          for (int ks = 0; ks < MM_N / 8; ks++) {
-            const int k0 = ks * 8;
-            const float *ah = Ahi + (mt * 16 + g) * MM_AS + k0 + tq;
-            const float *al = Alo + (mt * 16 + g) * MM_AS + k0 + tq;
-            const uint32_t ahi[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[8 * MM_AS]),
-                                     __float_as_uint(ah[4]), __float_as_uint(ah[8 * MM_AS + 4])};
-            const uint32_t alo[4] = {__float_as_uint(al[0]), __float_as_uint(al[8 * MM_AS]),
-                                     __float_as_uint(al[4]), __float_as_uint(al[8 * MM_AS + 4])};
+          for (int nn = 0; nn < 2; nn++) {
+            const int nt = (warp >> 1) * 2 + nn;
             const float b0 = Bs[(k0 + tq) * MM_BS + nt * 8 + g];
             const float b1 = Bs[(k0 + tq + 4) * MM_BS + nt * 8 + g];
             const uint32_t bhi[2] = {to_tf32(b0), to_tf32(b1)};
@@ -547,13 +548,17 @@ __global__ void __launch_bounds__(1024, 1)
             // low 13 mantissa bits, <= 2^-21 |b|, far inside E (2^-15)
             const uint32_t blo[2] = {__float_as_uint(b0 - __uint_as_float(bhi[0])),
                                      __float_as_uint(b1 - __uint_as_float(bhi[1]))};
-            mma_tf32(dd, alo, bhi);
-            mma_tf32(dd, ahi, blo);
-            mma_tf32(dd, ahi, bhi);
+            mma_tf32(dd[nn], alo, bhi);
+            mma_tf32(dd[nn], ahi, blo);
+            mma_tf32(dd[nn], ahi, bhi);
           }
+        }
+#pragma unroll
+        for (int nn = 0; nn < 2; nn++) {
+          const int nt = (warp >> 1) * 2 + nn;
           float *c0 = Cs + (mt * 16 + g) * MM_CS + nt * 8 + 2 * tq;
-          *(float2 *)c0 = make_float2(dd[0], dd[1]);
-          *(float2 *)(c0 + 8 * MM_CS) = make_float2(dd[2], dd[3]);
+          *(float2 *)c0 = make_float2(dd[nn][0], dd[nn][1]);
+          *(float2 *)(c0 + 8 * MM_CS) = make_float2(dd[nn][2], dd[nn][3]);
         }
       }
       __syncthreads();
