@@ -564,37 +564,43 @@ __global__ void __launch_bounds__(1024, 1)
       __syncthreads();
       if (!live) continue;
       scans += T - k;
-      double acc[U];
+      float acc[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) acc[u] = (double)Cs[warp * MM_CS + lane + 32 * u];
+      for (int u = 0; u < U; u++) acc[u] = Cs[warp * MM_CS + lane + 32 * u];
       // ---- certified selection: max |c| over available atoms, ties -> lowest index
-      double best = -1.0;
+      // (in fp32 on the fp32 correlations: the max of non-negative floats is a
+      // REDUX on their bits; the window threshold is rounded down, so the
+      // window can only grow -- a larger window is re-scored exactly)
+      float bestf = -1.0f;
       unsigned bj = 0xffffffffu;
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const double v = fabs(acc[u]);
-        if (!((tk >> u) & 1u) && v > best) {
-          best = v;
+        const float v = fabsf(acc[u]);
+        if (!((tk >> u) & 1u) && v > bestf) {
+          bestf = v;
           bj = lane + 32 * u;
         }
       }
-      double m = warp_max_nonneg(best);
-      const double thr = m - 2.0 * e_rel * rnorm;
+      const unsigned key = bestf >= 0.0f ? __float_as_uint(bestf) : 0u;
+      const unsigned mkey = __reduce_max_sync(CDB_FULL_MASK, key);
+      double m = (double)__uint_as_float(mkey);
+      const float thr = __double2float_rd(m - 2.0 * e_rel * rnorm);
+      unsigned cand = bestf >= 0.0f && key == mkey ? bj : 0xffffffffu;
       int cnt = 0;
 #pragma unroll
       for (int u = 0; u < U; u++)
-        if (!((tk >> u) & 1u) && fabs(acc[u]) >= thr) cnt++;
+        if (!((tk >> u) & 1u) && fabsf(acc[u]) >= thr) cnt++;
       cnt = (int)__reduce_add_sync(CDB_FULL_MASK, (unsigned)cnt);
       if (cnt == 0) {  // nothing available (_kernels.py:104)
         live = false;
         continue;
       }
       if (cnt > 1) {  // re-score the window exactly in fp64 (lane per candidate)
-        best = -1.0;
+        double best = -1.0;
         bj = 0xffffffffu;
 #pragma unroll
         for (int u = 0; u < U; u++) {
-          if (!((tk >> u) & 1u) && fabs(acc[u]) >= thr) {
+          if (!((tk >> u) & 1u) && fabsf(acc[u]) >= thr) {
             const int jj = lane + 32 * u;
             const double *dj = d64 + (int64_t)jj * n;
             double c = 0.0;
@@ -608,8 +614,9 @@ __global__ void __launch_bounds__(1024, 1)
         m = best;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(CDB_FULL_MASK, m, o));
+        cand = best == m ? bj : 0xffffffffu;
       }
-      const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+      const int bestj = (int)__reduce_min_sync(CDB_FULL_MASK, cand);
       const int ub = bestj >> 5, owner = bestj & 31;
       const int nid = bestj;
       double cbest;
