@@ -639,11 +639,18 @@ __global__ void __launch_bounds__(1024, 1)
         soff[k] = nid * n;
       }
       __syncwarp();
-      for (int l = lane; l < k; l += 32) {
+      // w = L^{-1} g and the new L^{-1} row: two lanes per row, each summing
+      // half of it (halves the warp's trip count of the triangular loops)
+      for (int l0 = 0; l0 < k; l0 += 16) {
+        const int l = l0 + (lane >> 1), h = lane & 1;
         double accw = 0.0;
-#pragma unroll 4
-        for (int i = 0; i <= l; i++) accw = fma(lin[l * ldl + i], gv[i], accw);
-        wv[l] = accw;
+        if (l < k) {
+          const int mid = (l + 1) >> 1;
+          const int i1 = h ? l + 1 : mid;
+          for (int i = h ? mid : 0; i < i1; i++) accw = fma(lin[l * ldl + i], gv[i], accw);
+        }
+        accw += __shfl_xor_sync(CDB_FULL_MASK, accw, 1);
+        if (l < k && h == 0) wv[l] = accw;
       }
       __syncwarp();
       double ww = 0.0;
@@ -658,17 +665,16 @@ __global__ void __launch_bounds__(1024, 1)
       }
       const double inv_d = rsqrt(d2);
       const double zk = cbest * inv_d;
-      for (int i = lane; i <= k; i += 32) {
-        double v;
-        if (i == k) {
-          v = inv_d;
-        } else {
-          double accl = 0.0;
-#pragma unroll 4
-          for (int l = i; l < k; l++) accl = fma(wv[l], lin[l * ldl + i], accl);
-          v = -accl * inv_d;
+      for (int i0 = 0; i0 <= k; i0 += 16) {
+        const int i = i0 + (lane >> 1), h = lane & 1;
+        double accl = 0.0;
+        if (i < k) {
+          const int mid = (i + k) >> 1;
+          const int l1 = h ? k : mid;
+          for (int l = h ? mid : i; l < l1; l++) accl = fma(wv[l], lin[l * ldl + i], accl);
         }
-        lin[k * ldl + i] = v;
+        accl += __shfl_xor_sync(CDB_FULL_MASK, accl, 1);
+        if (i <= k && h == 0) lin[k * ldl + i] = i == k ? inv_d : -accl * inv_d;
       }
       if (lane == 0) zv[k] = zk;
       __syncwarp();
