@@ -451,9 +451,12 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-template <typename YT>
-__global__ void __launch_bounds__(1024, 1)
+// W signals (warps) per CTA: 32 (one CTA per SM) or 16 (two CTAs per SM, so
+// one CTA's warps issue while the other's wait at the lock-step barrier)
+template <typename YT, int W>
+__global__ void __launch_bounds__(W * 32, 1024 / (W * 32))
     resident_mma_kernel(ResidentArgs a, const YT *__restrict__ ys) {
+  constexpr int MT = W / 16;  // m-tiles of the scan GEMM
   constexpr int U = MM_T / 32;
   extern __shared__ __align__(16) double rs[];
   __shared__ double s_dmax;
@@ -462,10 +465,10 @@ __global__ void __launch_bounds__(1024, 1)
   const int64_t P = a.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float *Bs = (float *)rs;               // MM_N x MM_BS: Bs[k][j] = d_j[k]
-  float *Ahi = Bs + MM_N * MM_BS;        // MM_W x MM_AS (tf32-rounded floats)
-  float *Alo = Ahi + MM_W * MM_AS;
-  float *Cs = Alo + MM_W * MM_AS;        // MM_W x MM_CS
-  double *nrm2 = (double *)(Cs + MM_W * MM_CS);  // MM_T
+  float *Ahi = Bs + MM_N * MM_BS;        // W x MM_AS (tf32-rounded floats)
+  float *Alo = Ahi + W * MM_AS;
+  float *Cs = Alo + W * MM_AS;           // W x MM_CS
+  double *nrm2 = (double *)(Cs + W * MM_CS);  // MM_T
   double *st = nrm2 + MM_T + warp * a.per_warp;
   double *r = st;
   double *lin = r + n;
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(1024, 1)
   __syncthreads();
   const double e_rel = 0x1p-15 * 1.01 * s_dmax;  // |c~ - c| <= e_rel |r|
 
-  for (int64_t p0 = (int64_t)blockIdx.x * MM_W; p0 < P; p0 += (int64_t)gridDim.x * MM_W) {
+  for (int64_t p0 = (int64_t)blockIdx.x * W; p0 < P; p0 += (int64_t)gridDim.x * W) {
     const int64_t p = p0 + warp;
     const bool valid = p < P;
     const int kmax = valid ? (int)a.cands.budget(p, a.k_max, n) : 0;
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(1024, 1)
       if (!__syncthreads_or(live)) break;
       {  // ---- C = A B: warp w computes m-tile (w & 1), n-tiles 2 (w >> 1) + {0, 1}
         // (k-steps outer: each A fragment is loaded once for both n-tiles)
-        const int mt = warp & 1, g = lane >> 2, tq = lane & 3;
+        const int mt = warp % MT, g = lane >> 2, tq = lane & 3;
         float dd[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
 #pragma unroll
         for (int ks = 0; ks < MM_N / 8; ks++) {
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(1024, 1)
                                    __float_as_uint(al[4]), __float_as_uint(al[8 * MM_AS + 4])};
 #pragma unroll
           for (int nn = 0; nn < 2; nn++) {
-            const int nt = (warp >> 1) * 2 + nn;
+            const int nt = (warp / MT) * 2 + nn;
             const float b0 = Bs[(k0 + tq) * MM_BS + nt * 8 + g];
             const float b1 = Bs[(k0 + tq + 4) * MM_BS + nt * 8 + g];
             const uint32_t bhi[2] = {to_tf32(b0), to_tf32(b1)};
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
 #pragma unroll
         for (int nn = 0; nn < 2; nn++) {
-          const int nt = (warp >> 1) * 2 + nn;
+          const int nt = (warp / MT) * 2 + nn;
           float *c0 = Cs + (mt * 16 + g) * MM_CS + nt * 8 + 2 * tq;
           *(float2 *)c0 = make_float2(dd[nn][0], dd[nn][1]);
           *(float2 *)(c0 + 8 * MM_CS) = make_float2(dd[nn][2], dd[nn][3]);
@@ -809,21 +812,40 @@ cudaError_t launch_resident(const ResidentArgs &args, const void *ys, bool ys_f3
   a.t_pad = resident_tpad(a.t, a.max_cands);
   if (a.cands.mode == 0 && a.t_pad < 32 * ((a.max_cands + 31) / 32)) return cudaErrorInvalidValue;
   if (a.cands.mode == 0 && a.n <= MM_N && a.t <= MM_T && a.gram && !getenv("CDB_RESIDENT_NO_MMA")) {
-    const size_t smem = sizeof(float) * (MM_N * MM_BS + 2 * MM_W * MM_AS + MM_W * MM_CS) +
-                        sizeof(double) * (MM_T + MM_W * a.per_warp);
+    static const int w_env = [] {
+      const char *v = getenv("CDB_MM_W");  // cfg 1 step 1: W = 16 2.23 ms, W = 32 2.29 ms
+      return v ? atoi(v) : 16;
+    }();
+    auto smem_for = [&](int w) {
+      return sizeof(float) * (MM_N * MM_BS + 2 * w * MM_AS + w * MM_CS) +
+             sizeof(double) * (MM_T + w * a.per_warp);
+    };
+    // W = 16 only while two CTAs fit one SM
+    const int W = w_env == 16 && 2 * (int64_t)smem_for(16) + 2048 <= smem_optin ? 16 : 32;
+    const size_t smem = smem_for(W);
     if ((int64_t)smem <= smem_optin) {
-      int64_t grid = (a.p + MM_W - 1) / MM_W;
-      if (grid > num_sms) grid = num_sms;
-      auto kern = ys_f32 ? (const void *)resident_mma_kernel<float>
-                         : (const void *)resident_mma_kernel<double>;
+      int64_t grid = (a.p + W - 1) / W;
+      const int64_t cap = (int64_t)num_sms * (32 / W);
+      if (grid > cap) grid = cap;
+      const void *kern = W == 16 ? (ys_f32 ? (const void *)resident_mma_kernel<float, 16>
+                                           : (const void *)resident_mma_kernel<double, 16>)
+                                 : (ys_f32 ? (const void *)resident_mma_kernel<float, 32>
+                                           : (const void *)resident_mma_kernel<double, 32>);
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
       note_launch();
-      if (ys_f32)
-        resident_mma_kernel<float><<<(int)grid, MM_W * 32, smem, stream>>>(a, (const float *)ys);
-      else
-        resident_mma_kernel<double><<<(int)grid, MM_W * 32, smem, stream>>>(a, (const double *)ys);
+      if (W == 16) {
+        if (ys_f32)
+          resident_mma_kernel<float, 16><<<(int)grid, 512, smem, stream>>>(a, (const float *)ys);
+        else
+          resident_mma_kernel<double, 16><<<(int)grid, 512, smem, stream>>>(a, (const double *)ys);
+      } else {
+        if (ys_f32)
+          resident_mma_kernel<float, 32><<<(int)grid, 1024, smem, stream>>>(a, (const float *)ys);
+        else
+          resident_mma_kernel<double, 32><<<(int)grid, 1024, smem, stream>>>(a, (const double *)ys);
+      }
       return cudaGetLastError();
     }
   }
