@@ -1359,7 +1359,8 @@ static cdb_status zero_tree_core(const cdb_dictionary *low, const cdb_dictionary
       (engine == CDB_ENGINE_RESIDENT ||
        (engine == CDB_ENGINE_AUTO && !gram_preferred(high, k1 * q, k_high)));
   const bool use_route = high->gram && !high_resident && engine != CDB_ENGINE_EXACT &&
-                         high->t / q == low->t && 8 * q * n <= 192 * 1024 && k1 < 65536 &&
+                         high->t / q == low->t &&
+                         (8 * q * n <= 192 * 1024 || cdb::route_alpha0_dmma(q, n)) && k1 < 65536 &&
                          (q == 1 || q == 2 || q == 4 || q == 8 || q == 16);
   if (use_route) {
     CDB_CUDA(alpha0.alloc(sizeof(double) * p * k1 * q, st));

@@ -177,6 +177,7 @@ cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *
                                cudaStream_t stream);
 cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad,
                            void *d16, cudaStream_t stream);
+bool route_alpha0_dmma(int64_t q, int64_t n);
 cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q,
                                const void *ys, bool ys_f32, const int64_t *blocks,
                                const int64_t *nb, int64_t p, int64_t k1, int64_t smax,

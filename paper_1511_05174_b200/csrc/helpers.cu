@@ -703,7 +703,7 @@ bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t 
     err = cudaGetLastError();
     return true;
   }
-  if ((q == 8 || q == 16) && n % 16 == 0 && q * n <= 16384 && alpha0_mma_enabled()) {
+  if ((q == 8 || q == 16) && n % 16 == 0 && alpha0_mma_enabled()) {
     const int split = 8;
     const unsigned grid = (unsigned)(buckets * split);
     if (q == 8)
@@ -873,6 +873,12 @@ cudaError_t launch_quant_err_max(const double *d64, const void *d16, int64_t t, 
       d64, (const __nv_bfloat16 *)d16, t, n, n_pad, (unsigned long long *)out);
   note_launch();
   return cudaGetLastError();
+}
+
+// the DMMA tiles take any N (a multiple of 16) for Q in {8, 16}: above the
+// L1 size the children stream from L2, still 8 pairs per read
+bool route_alpha0_dmma(int64_t q, int64_t n) {
+  return (q == 8 || q == 16) && n % 16 == 0 && alpha0_mma_enabled();
 }
 
 cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q,
