@@ -26,6 +26,8 @@
 // are delegated to the exact engine, which reproduces the reference bit for
 // bit, including the dense minimum-norm mode.
 #include "candidates.cuh"
+#include <cstdlib>
+
 #include "common.cuh"
 #include "engines.h"
 
@@ -392,6 +394,10 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   const int cap = u <= 8 ? 16 : 8;
   int wpb = (int)(max_smem_per_block / per_warp);
   if (wpb > cap) wpb = cap;
+  // H in global memory: 3-warp CTAs keep more of the in-flight H rows in L2
+  // (cfg 4 step 2: 178 ms vs 194 ms for 6-8 warps, 188 ms for 2)
+  if (!h_in_smem && wpb > 3) wpb = 3;
+  if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) < wpb ? atoi(v) : wpb;
   if (wpb < 1) wpb = 1;
   const int64_t blocks = (args.p + wpb - 1) / wpb;
   note_launch();
