@@ -392,12 +392,12 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   if (kw > 64 || s > 512) return cudaErrorInvalidValue;
   const int u = (int)(gram_hs(s) / 32);
   const int cap = u <= 8 ? 16 : 8;
-  int wpb = (int)(max_smem_per_block / per_warp);
-  if (wpb > cap) wpb = cap;
+  int max_w = (int)(max_smem_per_block / per_warp);
+  if (max_w > cap) max_w = cap;
   // H in global memory: 3-warp CTAs keep more of the in-flight H rows in L2
   // (cfg 4 step 2: 178 ms vs 194 ms for 6-8 warps, 188 ms for 2)
-  if (!h_in_smem && wpb > 3) wpb = 3;
-  if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) < wpb ? atoi(v) : wpb;
+  int wpb = !h_in_smem && max_w > 3 ? 3 : max_w;
+  if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) < max_w ? atoi(v) : max_w;
   if (wpb < 1) wpb = 1;
   const int64_t blocks = (args.p + wpb - 1) / wpb;
   note_launch();
