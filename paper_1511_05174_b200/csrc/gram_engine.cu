@@ -394,9 +394,7 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   const int cap = u <= 8 ? 16 : 8;
   int max_w = (int)(max_smem_per_block / per_warp);
   if (max_w > cap) max_w = cap;
-  // H in global memory: 3-warp CTAs keep more of the in-flight H rows in L2
-  // (cfg 4 step 2: 178 ms vs 194 ms for 6-8 warps, 188 ms for 2)
-  int wpb = !h_in_smem && max_w > 3 ? 3 : max_w;
+  int wpb = max_w;
   if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) < max_w ? atoi(v) : max_w;
   if (wpb < 1) wpb = 1;
   const int64_t blocks = (args.p + wpb - 1) / wpb;
