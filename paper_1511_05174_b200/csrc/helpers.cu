@@ -542,7 +542,7 @@ __device__ __forceinline__ void prefetch_tile(const int64_t *__restrict__ pairs,
     asm volatile("prefetch.global.L1 [%0];" ::"l"(row + o));
 }
 
-template <typename YT, int NT>  // NT = N / 16
+template <typename YT, int NT, int QT = 8>  // NT = N / 16; QT = 4: rows 4-7 of A are zero
 __global__ void __launch_bounds__(128) alpha0_mma_kernel(
     const double *__restrict__ d64, int n, const YT *__restrict__ ys,
     const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t smax, int split,
@@ -556,15 +556,16 @@ __global__ void __launch_bounds__(128) alpha0_mma_kernel(
   const int r = lane >> 2, j = lane & 3;
   double ch[4 * NT];
   {
-    const double *src = d64 + ((int64_t)parent * 8 + r) * n + 4 * j;
+    const double *src = d64 + ((int64_t)parent * QT + (r < QT ? r : 0)) * n + 4 * j;
 #pragma unroll
     for (int t = 0; t < NT; t++) {
       const double2 u = __ldg(reinterpret_cast<const double2 *>(src + 16 * t));
       const double2 v = __ldg(reinterpret_cast<const double2 *>(src + 16 * t + 2));
-      ch[4 * t + 0] = u.x;
-      ch[4 * t + 1] = u.y;
-      ch[4 * t + 2] = v.x;
-      ch[4 * t + 3] = v.y;
+      const bool live = r < QT;
+      ch[4 * t + 0] = live ? u.x : 0.0;
+      ch[4 * t + 1] = live ? u.y : 0.0;
+      ch[4 * t + 2] = live ? v.x : 0.0;
+      ch[4 * t + 3] = live ? v.y : 0.0;
     }
   }
   // warp w takes a contiguous run of whole 8-pair tiles
@@ -599,8 +600,8 @@ __global__ void __launch_bounds__(128) alpha0_mma_kernel(
     // lane holds child r of pairs 2j and 2j + 1 (pair q's id sits in lane 4q)
     const int64_t p0 = __shfl_sync(CDB_FULL_MASK, (long long)pr, 8 * j);
     const int64_t p1 = __shfl_sync(CDB_FULL_MASK, (long long)pr, 8 * j + 4);
-    if (2 * j < m) alpha0[(p0 >> 16) * smax + (p0 & 0xffff) * 8 + r] = c0;
-    if (2 * j + 1 < m) alpha0[(p1 >> 16) * smax + (p1 & 0xffff) * 8 + r] = c1;
+    if (r < QT && 2 * j < m) alpha0[(p0 >> 16) * smax + (p0 & 0xffff) * QT + r] = c0;
+    if (r < QT && 2 * j + 1 < m) alpha0[(p1 >> 16) * smax + (p1 & 0xffff) * QT + r] = c1;
   }
 }
 
@@ -688,6 +689,18 @@ bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t 
     const char *v = getenv("CDB_A0_PF");
     return v ? atoi(v) : 1;
   }();
+  if (q == 4 && (n == 64 || n == 128) && alpha0_mma_enabled()) {
+    const int split = 8;
+    const unsigned grid = (unsigned)(buckets * split);
+    if (n == 64)
+      alpha0_mma_kernel<YT, 4, 4><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                            split, (int)t_low, alpha0, pf);
+    else
+      alpha0_mma_kernel<YT, 8, 4><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                            split, (int)t_low, alpha0, pf);
+    err = cudaGetLastError();
+    return true;
+  }
   if (q == 8 && (n == 64 || n == 128 || n == 256) && alpha0_mma_enabled()) {
     const int split = 8;
     const unsigned grid = (unsigned)(buckets * split);
