@@ -1040,6 +1040,285 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
   }
 }
 
+// ---------------------------------------------------------------- wide LS step
+// Long supports (kw > 32: cfg 4, K = 64) make L^{-1} too large to stage in
+// shared memory (32 KB per signal left the grouped kernel 4 signals per SM,
+// 5.4 ms per 111 k-signal launch on cfg 4 step 1).  Here one warp owns one
+// signal and nothing per-signal is staged: L^{-1} stays in global memory as
+// packed rows (row l holds l+1 entries at l(l+1)/2), read twice per
+// iteration with coalesced row loads --
+//   w = L^{-1} g      lanes own columns i, accumulate one partial per row,
+//                     and a butterfly reduce-scatter (31 fp64 shuffles per
+//                     32 rows) leaves lane l holding w_l;
+//   v = L^{-T} w      lanes own columns i, rows l streamed with w_l broadcast,
+// and the support's k-vectors (ids, coefficients, Gram row) live in
+// registers, lane i holding entries i, i + 32, ...  The coefficients are
+// updated in place, x_k = [x_{k-1}; 0] + z_k [-v / d; 1 / d] (the new row of
+// L^{-1} is [-v^T / d, 1 / d]), so z never needs re-reading.  Certification,
+// delegation, the stop rule and the scan counts are those of ls_step_kernel;
+// the next scan operand is built by resid_split_kernel.
+__device__ __forceinline__ int64_t lpk(int l) { return (int64_t)l * (l + 1) / 2; }
+
+// 32 per-lane partials acc[m] (m = row within the block) -> lane l returns
+// the warp-wide sum of partial l.
+__device__ __forceinline__ double reduce_scatter32(double (&acc)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int m = 0; m < o; m++) {
+      const double send = hi ? acc[m] : acc[m + o];
+      const double keep = hi ? acc[m + o] : acc[m];
+      acc[m] = keep + __shfl_xor_sync(CDB_FULL_MASK, send, o);
+    }
+  }
+  return acc[0];
+}
+
+template <typename YT, int KR>
+__global__ void __launch_bounds__(128) ls_wide_kernel(
+    const YT *__restrict__ ys, const double *__restrict__ d64, const double *__restrict__ gram,
+    int64_t p, int64_t t, int n, int k_max, int kw, int iter, double c_err, double dmax,
+    TensorState st, int64_t *out_sel, double *out_coef, int64_t *out_count, int64_t *out_scans,
+    int resume) {
+  griddep_wait();  // the scan's candidates (PDL)
+  griddep_launch();
+  __shared__ double wsm[4][32 * KR];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int k = iter;
+  const int64_t kp = (int64_t)kw * (kw + 1) / 2;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t count = resume ? (int64_t)st.npending[iter] : p;
+  double *wl = wsm[wib];
+
+  for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; e < count; e += nw) {
+    const int64_t sig = resume ? st.pending[e] : e;
+    if (!resume && (st.status[sig] & (ST_DONE | ST_DELEGATE))) continue;
+    int64_t *sel = out_sel + sig * kw;
+    double *xo = out_coef + sig * kw;
+    double *lin = st.linv + sig * kp;
+    const YT *y = ys + sig * (int64_t)n;
+    int64_t sv[KR];
+    double xv[KR];
+#pragma unroll
+    for (int r = 0; r < KR; r++) {
+      const int i = lane + 32 * r;
+      sv[r] = i < k ? sel[i] : -1;
+      xv[r] = i < k ? xo[i] : 0.0;
+    }
+    int cidx = -1;
+    float cval = -1.0f;
+    if (!resume && lane < NCAND) {
+      cidx = st.cand_idx[sig * NCAND + lane];
+      cval = st.cand_val[sig * NCAND + lane];
+    }
+    const double rn2_prev = st.rn2[sig], tol = st.tol[sig], yy = st.yy[sig];
+    double best = -1.0, cbest = 0.0;
+    int64_t bestj = -1;
+    double bg[KR];
+#pragma unroll
+    for (int r = 0; r < KR; r++) bg[r] = 0.0;
+    if (resume) {
+      bestj = st.rs_j[sig];
+      cbest = st.rs_c[sig];
+      best = fabs(cbest);
+      if (lane == 0) st.status[sig] &= ~ST_RESCAN;
+      if (bestj >= 0) {
+        const double *grow = gram + bestj * t;
+#pragma unroll
+        for (int r = 0; r < KR; r++) bg[r] = sv[r] >= 0 ? __ldg(grow + sv[r]) : 0.0;
+      }
+    } else {
+      // ---- candidates: drop taken atoms (support ids are spread over the lanes)
+#pragma unroll
+      for (int c = 0; c < NCAND; c++) {
+        const int j = __shfl_sync(CDB_FULL_MASK, cidx, c);
+        bool hit = false;
+#pragma unroll
+        for (int r = 0; r < KR; r++) hit |= (j >= 0 && sv[r] == j);
+        if (__any_sync(CDB_FULL_MASK, hit) && lane == c) {
+          cidx = -1;
+          cval = -1.0f;
+        }
+      }
+      const float cdrop = st.cand_drop[sig];
+      const double rt = st.rt[sig], drs = st.dr[sig], rq = st.rq[sig];
+      const double E = (c_err * (rt + rq) * 1.0079 + rq + drs) * dmax + st.emax * (rt + rq);
+      double best_apx = (double)cval;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        best_apx = fmax(best_apx, __shfl_xor_sync(CDB_FULL_MASK, best_apx, o));
+      const bool rescore = cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
+      const unsigned rmask = __ballot_sync(CDB_FULL_MASK, rescore);
+      double unscored = rescore || cidx < 0 ? -1.0 : (double)cval;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        unscored = fmax(unscored, __shfl_xor_sync(CDB_FULL_MASK, unscored, o));
+      unscored = fmax(unscored, (double)cdrop);
+      for (unsigned m = rmask; m; m &= m - 1) {
+        const int64_t j = __shfl_sync(CDB_FULL_MASK, cidx, __ffs(m) - 1);
+        // exact c_j = <d_j, y> - G[j, S] x  (fp64)
+        const double *dj = d64 + j * n;
+        const double *gj = gram + j * t;
+        double g[KR];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < KR; r++) g[r] = sv[r] >= 0 ? __ldg(gj + sv[r]) : 0.0;
+        int i = lane;
+        for (; i + 96 < n; i += 128) {
+          const double e0 = __ldg(dj + i), e1 = __ldg(dj + i + 32), e2 = __ldg(dj + i + 64),
+                       e3 = __ldg(dj + i + 96);
+          a0 = fma(e0, (double)y[i], a0);
+          a1 = fma(e1, (double)y[i + 32], a1);
+          a2 = fma(e2, (double)y[i + 64], a2);
+          a3 = fma(e3, (double)y[i + 96], a3);
+        }
+        for (; i < n; i += 32) a0 = fma(__ldg(dj + i), (double)y[i], a0);
+        double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+        for (int r = 0; r < KR; r++) acc = fma(-g[r], xv[r], acc);
+        const double cj = warp_sum(acc);
+        const double v = fabs(cj);
+        if (v > best || (v == best && j < bestj)) {
+          best = v;
+          bestj = j;
+          cbest = cj;
+#pragma unroll
+          for (int r = 0; r < KR; r++) bg[r] = g[r];
+        }
+      }
+      if (bestj < 0 || !(unscored + E < best)) {
+        // uncertifiable: queue for the exact rescan, resume later
+        if (lane == 0) {
+          st.status[sig] |= ST_RESCAN;
+          st.pending[atomicAdd(st.npending + iter, 1)] = sig;
+          atomicAdd(st.rescans, 1);
+        }
+        continue;
+      }
+    }
+    if (lane == 0) out_scans[sig] += t - k;  // scans += c - k (_kernels.py:91)
+    if (bestj < 0 || best <= 0.0) {          // orthogonal break (_kernels.py:104)
+      if (lane == 0) st.status[sig] |= ST_DONE;
+      continue;
+    }
+    // ---- w = L^{-1} g   (g = G[S, new]; lane-owned columns, reduce-scatter per 32 rows)
+    double w[KR];
+#pragma unroll
+    for (int b = 0; b < KR; b++) {
+      w[b] = 0.0;
+      if (32 * b >= k) continue;  // warp-uniform
+      double acc[32];
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int l = 32 * b + m;
+        double a = 0.0;
+        if (l < k) {
+          const double *row = lin + lpk(l);
+#pragma unroll
+          for (int r = 0; r <= b; r++) {
+            const int i = lane + 32 * r;
+            if (i <= l) a = fma(row[i], bg[r], a);
+          }
+        }
+        acc[m] = a;
+      }
+      w[b] = reduce_scatter32(acc, lane);
+      wl[32 * b + lane] = w[b];
+    }
+    __syncwarp();
+    double ww = 0.0;
+#pragma unroll
+    for (int b = 0; b < KR; b++)
+      if (lane + 32 * b < k) ww = fma(w[b], w[b], ww);
+    ww = warp_sum(ww);
+    const double gnn = __ldg(gram + bestj * t + bestj);
+    const double d2 = gnn - ww;
+    if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: the exact engine decides
+      if (lane == 0) st.status[sig] |= ST_DELEGATE;
+      __syncwarp();
+      continue;
+    }
+    const double inv_d = 1.0 / sqrt(d2);
+    const double zk = cbest * inv_d;  // q_k^T y = q_k^T r = <d_new, r> / d
+    // ---- v = L^{-T} w (rows streamed, w_l broadcast from shared memory)
+    double v[KR];
+#pragma unroll
+    for (int r = 0; r < KR; r++) v[r] = 0.0;
+    int l = 0;
+    for (; l + 3 < k; l += 4) {
+      const double w0 = wl[l], w1 = wl[l + 1], w2 = wl[l + 2], w3 = wl[l + 3];
+      const double *r0 = lin + lpk(l);
+#pragma unroll
+      for (int r = 0; r < KR; r++) {
+        const int i = lane + 32 * r;
+        const double *rw = r0;
+        if (i <= l) v[r] = fma(rw[i], w0, v[r]);
+        rw += l + 1;
+        if (i <= l + 1) v[r] = fma(rw[i], w1, v[r]);
+        rw += l + 2;
+        if (i <= l + 2) v[r] = fma(rw[i], w2, v[r]);
+        rw += l + 3;
+        if (i <= l + 3) v[r] = fma(rw[i], w3, v[r]);
+      }
+    }
+    for (; l < k; l++) {
+      const double wv = wl[l];
+      const double *rw = lin + lpk(l);
+#pragma unroll
+      for (int r = 0; r < KR; r++) {
+        const int i = lane + 32 * r;
+        if (i <= l) v[r] = fma(rw[i], wv, v[r]);
+      }
+    }
+    // ---- append row k of L^{-1}, update x, record the pick
+    double *nrow = lin + lpk(k);
+#pragma unroll
+    for (int r = 0; r < KR; r++) {
+      const int i = lane + 32 * r;
+      if (i < k) {
+        const double u = -v[r] * inv_d;
+        nrow[i] = u;
+        xv[r] = fma(zk, u, xv[r]);
+        xo[i] = xv[r];
+      } else if (i == k) {
+        nrow[i] = inv_d;
+        xv[r] = zk * inv_d;
+        xo[i] = xv[r];
+        sv[r] = bestj;
+        sel[i] = bestj;
+      }
+    }
+    if (lane == 0) st.z[sig * kw + k] = zk;
+    const int kd = k + 1;
+    // ---- stop test on |r|^2 = |y|^2 - |z|^2, exact residual inside the band
+    const double rn2 = rn2_prev - zk * zk;
+    const double gap = rn2 - tol * tol;
+    bool stop = gap < 0.0;
+    if (!(fabs(gap) > 1e-12 * yy)) {
+      __syncwarp();  // x and the ids written above by the other lanes
+      double rr = 0.0;
+      for (int i = lane; i < n; i += 32) {
+        double ri = (double)y[i];
+        for (int s = 0; s < kd; s++) ri = fma(-xo[s], __ldg(d64 + sel[s] * n + i), ri);
+        rr = fma(ri, ri, rr);
+      }
+      stop = sqrt(warp_sum(rr)) <= tol;
+    }
+    if (lane == 0) {
+      st.rn2[sig] = rn2;
+      out_count[sig] = kd;
+      if (stop || kd >= k_max) {
+        st.status[sig] |= ST_DONE;
+      } else {
+        st.status[sig] |= ST_RESID;
+        atomicAdd(st.active + iter, 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Split-mode scan operand (large N): r~ = y - D32_S x -> bf16 for every signal
 // flagged ST_RESID, one CTA per signal -- 8 elements x 4 atom rows = 32 loads
 // in flight per thread, so the kd x N fp32 row stream runs near HBM speed
@@ -1798,6 +2077,12 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   // large N: build the scan operand in its own kernel (CDB_LS_SPLIT=0|1 overrides)
   int split = n > 256 ? 1 : 0;
   if (const char *v = getenv("CDB_LS_SPLIT")) split = atoi(v) ? 1 : 0;
+  // long supports: the wide LS kernel (L^{-1} in global memory, warp per signal);
+  // CDB_LS_WIDE=0|1 overrides
+  int wide_kr = kw <= 32 ? 1 : (kw <= 64 ? 2 : (kw <= 128 ? 4 : 0));
+  bool wide = kw > 32 && wide_kr > 0;
+  if (const char *v = getenv("CDB_LS_WIDE")) wide = atoi(v) != 0 && wide_kr > 0;
+  if (wide) split = 1;
   TileRescan tr;
   if (tiled && (e = tile_rescan_alloc(tr, p, t, n, stream)) != cudaSuccess) return e;
   for (int it = 0; it < a.k_max; it++) {
@@ -1822,7 +2107,19 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         note_launch();
       }
       ProfScope _ps(resume ? "ls_resume" : "ls_step", stream);
-      if (lsg_smem > 0) {
+      if (wide) {
+        const unsigned grid = resume ? (unsigned)(a.num_sms * 8) : (unsigned)((p + 3) / 4);
+#define CDB_WIDE(YT_, KR_)                                                                      \
+  e = launch_k(pdl, ls_wide_kernel<YT_, KR_>, grid, 128, 0, stream, (const YT_ *)a.ys, a.d64,   \
+               a.gram, p, t, (int)n, (int)a.k_max, (int)kw, it, c_err, a.dmax, st, a.out_sel,   \
+               a.out_coef, a.out_count, a.out_scans, resume);
+        if (a.ys_f32) {
+          if (wide_kr == 1) { CDB_WIDE(float, 1) } else if (wide_kr == 2) { CDB_WIDE(float, 2) } else { CDB_WIDE(float, 4) }
+        } else {
+          if (wide_kr == 1) { CDB_WIDE(double, 1) } else if (wide_kr == 2) { CDB_WIDE(double, 2) } else { CDB_WIDE(double, 4) }
+        }
+#undef CDB_WIDE
+      } else if (lsg_smem > 0) {
         const unsigned grid = resume ? (unsigned)(a.num_sms * 4) : lsg_grid;
         if (lsg_g == 8) {
           if (a.ys_f32)
@@ -1884,7 +2181,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       note_launch();
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    if (split && lsg_smem > 0 && it + 1 < a.k_max) {  // the next scan's operand
+    if (split && (wide || lsg_smem > 0) && it + 1 < a.k_max) {  // the next scan's operand
       ProfScope _ps("ls_resid", stream);
       const size_t xs = 16 * (size_t)kw;
       // threads per signal: N / 8 (8 elements each), 64..256

@@ -193,3 +193,60 @@ def signals_at(cfg_index: int, ids, seed: int = 0) -> np.ndarray:
         ys, _, _ = signal_block(cfg_index, int(b), seed)
         out[sel] = ys[ids[sel] - b * BLOCK]
     return out
+
+
+#: signals per device-generation block (``signals_device``)
+DEVICE_BLOCK = 65536
+
+
+def _block_seed(seed: int, cfg_index: int, block: int) -> int:
+    return int(np.random.default_rng([seed, 3, cfg_index, block]).integers(0, 2**62))
+
+
+def signals_device(cfg_index: int, start: int, stop: int, seed: int = 0, device="cuda"):
+    """Signals ``start:stop`` of the config's DEVICE stream, as fp32 ROWS on ``device``.
+
+    Same distribution as ``signal_block`` (K distinct parents uniform over
+    T_low, one uniform child each, N(0,1) coefficients, sigma noise; Phi for
+    the CS config), drawn with torch's device generator in independent blocks
+    of ``DEVICE_BLOCK`` signals seeded from ``(seed, cfg, block)`` -- so any rank
+    generates just its own shard and the stream does not depend on the
+    sharding.  At cfg 4's full size (1M x 4096) the host stream
+    (``signals``) takes ~12 min; this takes seconds.  It is a different
+    stream from ``signals``: parity tests copy the rows they check back to
+    the host and feed exactly those to the oracle.
+    """
+    import torch
+    w = CONFIGS[cfg_index]
+    d = dictionaries(cfg_index, seed)
+    dev = torch.device(device)
+    dh = torch.from_numpy(np.array(d.high_t)).to(dev)
+    phi_t = torch.from_numpy(np.array(d.phi)).to(dev).T.contiguous() if w.measurements else None
+    out = torch.empty((max(stop - start, 0), w.n_signal), dtype=torch.float32, device=dev)
+    if stop <= start:
+        return out
+    sub = max(1, min(DEVICE_BLOCK, (512 << 20) // (8 * w.n_high)))
+    for b in range(start // DEVICE_BLOCK, (stop - 1) // DEVICE_BLOCK + 1):
+        g = torch.Generator(device=dev)
+        g.manual_seed(_block_seed(seed, cfg_index, b))
+        parents = torch.topk(torch.rand((DEVICE_BLOCK, w.t_low), generator=g, device=dev), w.k,
+                             dim=1, largest=False).indices
+        atoms = parents * w.q + torch.randint(0, w.q, (DEVICE_BLOCK, w.k), generator=g, device=dev)
+        coefs = torch.randn((DEVICE_BLOCK, w.k), generator=g, device=dev, dtype=torch.float64)
+        lo = max(start - b * DEVICE_BLOCK, 0)
+        hi = min(stop - b * DEVICE_BLOCK, DEVICE_BLOCK)
+        for s in range(0, DEVICE_BLOCK, sub):
+            e = min(s + sub, DEVICE_BLOCK)
+            # noise is drawn for every sub-block so the stream is independent of lo/hi
+            noise = torch.randn((e - s, w.n_signal), generator=g, device=dev, dtype=torch.float64)
+            if e <= lo or s >= hi:
+                continue
+            x = torch.zeros((e - s, w.n_high), dtype=torch.float64, device=dev)
+            for j in range(w.k):
+                x += coefs[s:e, j, None] * dh[atoms[s:e, j]]
+            if phi_t is not None:
+                x = x @ phi_t
+            x += w.sigma * noise
+            a, z = max(lo, s), min(hi, e)
+            out[b * DEVICE_BLOCK + a - start: b * DEVICE_BLOCK + z - start] = x[a - s: z - s].float()
+    return out
