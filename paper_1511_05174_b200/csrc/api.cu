@@ -415,21 +415,17 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   g.status = status.as<uint32_t>();
   g.tag = tag;
   g.alpha0_in = alpha0;
-  int64_t chunk = p;
   DevBuf hwork;
-  if (!h_smem) {
-    const int64_t per_sig = 8 * cdb::gram_h_doubles(max_cands, kw);
-    chunk = kScratchBudget / per_sig;
-    if (chunk < 1) chunk = 1;
-    if (chunk > p) chunk = p;
-    CDB_CUDA(hwork.alloc((size_t)per_sig * chunk, st));
+  if (!h_smem) {  // streamed H: one L2-resident slot per persistent warp
+    const cdb::GramStreamPlan pl = cdb::gram_stream_plan(max_cands, kw, d->n, alpha0 == nullptr,
+                                                         di.smem_optin, di.sms);
+    if (!pl.ok) return fail(CDB_ERR_ARG, "Gram engine: no shared-memory plan for this H");
+    CDB_CUDA(hwork.alloc((size_t)(8 * pl.warps * (pl.slot_doubles > 0 ? pl.slot_doubles : 1)), st));
     g.hwork = hwork.as<double>();
   }
-  for (int64_t off = 0; off < p; off += chunk) {
-    g.p_offset = off;
-    g.p = (p - off) < chunk ? (p - off) : chunk;
-    CDB_CUDA(cdb::launch_gram(g, ys, f32, di.smem_optin, di.sms, st));
-  }
+  g.p_offset = 0;
+  g.p = p;
+  CDB_CUDA(cdb::launch_gram(g, ys, f32, di.smem_optin, di.sms, st));
   return finish_delegates(d, ys, f32, p, k_max, kw, eps, cands, max_cands, o,
                           status.as<uint32_t>(), di, st);
 }

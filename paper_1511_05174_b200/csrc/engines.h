@@ -103,6 +103,16 @@ int64_t gram_h_doubles(int64_t max_cands, int64_t k_width);
 int64_t gram_total_smem(int64_t max_cands, int64_t k_width, int64_t n, bool h_in_smem);
 cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int max_smem_per_block,
                         int num_sms, cudaStream_t stream);
+// Streamed H (H larger than a warp's shared memory): persistent warps, the
+// first nr rows of each warp's H in shared memory, the rest in a per-warp
+// global slot of slot_doubles (args.hwork = warps * slot_doubles doubles).
+struct GramStreamPlan {
+  bool ok;
+  int wpb, nr;
+  int64_t per_warp_smem, warps, slot_doubles;
+};
+GramStreamPlan gram_stream_plan(int64_t max_cands, int64_t k_width, int64_t n, bool stage_y,
+                                int max_smem_per_block, int num_sms);
 
 // ---------------------------------------------------------------- resident
 struct ResidentArgs {

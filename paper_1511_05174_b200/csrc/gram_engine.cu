@@ -61,6 +61,10 @@ __host__ __device__ inline int64_t gram_region_doubles(int64_t s, int64_t kw, in
   const int64_t hd = kw * gram_hs(s);
   return h_in_smem && hd > stage ? hd : stage;
 }
+// Streamed H (see gram_omp_kernel): default warps per SM (CDB_GRAM_WPB overrides).
+// cfg 4 step 2 (1M signals): 2 / 3 / 4 / 6 / 8 warps -> 1019 / 767 / 816 / 1169 /
+// 1365 ms; at 3, 444 slots x (64 - 18 smem rows) x 4 KB = 84 MB stay in L2.
+constexpr int kStreamWarpsPerSm = 3;
 
 // alpha0_j = <d_{C_j}, y> for every candidate: the warp streams 8 atom rows
 // at a time with coalesced loads (lane i reads element i of each row) and
@@ -92,20 +96,51 @@ __device__ __forceinline__ void alpha0_rows(const double *__restrict__ d64, cons
 // MGS factor read out of H: R[i][l] = q_i^T d_{s_l} = h_i[pick_l] (i < l),
 // R[l][l] = d_l.  Column sweep: lane i (and i + 32) accumulates
 // sum_{l > i} R[i][l] x_l.
+// H rows: rows i < nr at hs + i HS (shared memory), the rest at hg + i HS.
 template <int U>
-__device__ void back_substitute(const double *h, int kd, const double *zv, const double *iv,
-                                const int *pj, double *xv, int lane) {
-  constexpr int HS = 32 * U;
+__device__ __forceinline__ const double *hrow(const double *hs, const double *hg, int nr, int i) {
+  return (i < nr ? hs : hg) + (int64_t)i * (32 * U);
+}
+
+template <int U>
+__device__ void back_substitute(const double *hs, const double *hg, int nr, int kd,
+                                const double *zv, const double *iv, const int *pj, double *xv,
+                                int lane) {
+  const double *h0 = hrow<U>(hs, hg, nr, lane);
+  const double *h1 = hrow<U>(hs, hg, nr, lane + 32);
   double acc0 = 0.0, acc1 = 0.0;
   for (int l = kd - 1; l >= 0; l--) {
     const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
     const double xl = (zv[l] - accl) * iv[l];
     if (lane == 0) xv[l] = xl;
     const int sl = hslot<U>(pj[l]);
-    if (lane < l) acc0 = fma(h[lane * HS + sl], xl, acc0);
-    if (lane + 32 < l) acc1 = fma(h[(lane + 32) * HS + sl], xl, acc1);
+    if (lane < l) acc0 = fma(h0[sl], xl, acc0);
+    if (lane + 32 < l) acc1 = fma(h1[sl], xl, acc1);
   }
   __syncwarp();
+}
+
+// hacc -= sum_{i in [i0, i1)} w_i h_i, ww += |w|^2 over those rows (w_i = h_i[bs]).
+template <int U, int UNR>
+__device__ __forceinline__ void h_sweep(const double *h, int i0, int i1, int bs, int lane,
+                                        double (&hacc)[U], double &ww) {
+  constexpr int HS = 32 * U;
+#pragma unroll UNR
+  for (int i = i0; i < i1; i++) {
+    const double *hi = h + (int64_t)i * HS;
+    const double wi = hi[bs];  // = q_i^T d_{j*}
+    ww = fma(wi, wi, ww);
+    if (U == 1) {
+      hacc[0] = fma(-wi, hi[lane], hacc[0]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < U / 2; v++) {
+        const double2 t2 = *(const double2 *)(hi + v * 64 + lane * 2);
+        hacc[2 * v] = fma(-wi, t2.x, hacc[2 * v]);
+        hacc[2 * v + 1] = fma(-wi, t2.y, hacc[2 * v + 1]);
+      }
+    }
+  }
 }
 
 // U * 32 >= max_cands is a compile-time bound (register arrays over this
@@ -118,17 +153,23 @@ __device__ void back_substitute(const double *h, int kd, const double *zv, const
 // updates its own candidates, and accumulates |w|^2 redundantly, so an
 // iteration has no triangular solve and a single cross-lane reduction
 // (the argmax).
+//
+// HSM (H fits shared memory): one warp per signal.  Otherwise (cfg 4's step
+// 2: S = 512, K = 64, 256 KB of H per signal) the warps are persistent and
+// each owns one H slot: its first `nr` rows in shared memory (the oldest
+// rows, read by every later iteration: rows < nr carry
+// sum_{i<nr} (k_max - i) of the sum_i (k_max - i) row reads) and the rest in
+// a per-warp global slot sized so that all slots stay L2-resident -- a
+// streamed H is then read from L2, not HBM.
 template <typename YT, int U, bool HSM>
 __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
-    gram_omp_kernel(GramArgs a, const YT *__restrict__ ys, int h_in_smem, int64_t smem_per_warp) {
+    gram_omp_kernel(GramArgs a, const YT *__restrict__ ys, int h_rows_smem, int64_t smem_per_warp) {
   constexpr int HS = 32 * U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int64_t local = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (local >= a.p) return;
-  const int64_t p = a.p_offset + local;
-
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
   const int64_t T = a.t;
   const Cands cs = a.cands;
@@ -139,9 +180,13 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   double *xv = (double *)(sup + kw);
   double *region = xv + kw + ((5 * kw) & 1);  // even offset: 16-byte H accesses
   // HSM: H in shared memory, known at compile time so its accesses are LDS/STS
-  // rather than generic loads
-  double *h = HSM ? region : a.hwork + local * kw * HS;
-  (void)h_in_smem;
+  // rather than generic loads; else rows >= nr in this warp's global slot
+  const int nr = HSM ? kw : h_rows_smem;
+  double *hs = region;
+  double *hg = HSM ? region : a.hwork + gw * (int64_t)(kw - nr) * HS - (int64_t)nr * HS;
+
+  for (int64_t local = gw; local < a.p; local += nwarps) {
+  const int64_t p = a.p_offset + local;
   const YT *yg = ys + p * a.ys_stride;
 
   const int S = (int)cs.count(p);
@@ -158,11 +203,12 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
     cid[u] = j < S ? (int)cs.id(p, j) : 0;
     if (j >= S) tk |= 1u << u;
   }
-  double *y = region;  // staging until the first H row is written
+  double *y = region;  // staging until the first H row is written (in-kernel alpha0 only)
+  const bool stage = a.alpha0_in == nullptr;
   double yy = 0.0;
   for (int i = lane; i < n; i += 32) {
     const double v = (double)yg[i];
-    y[i] = v;
+    if (stage) y[i] = v;
     yy = fma(v, v, yy);
   }
   yy = warp_sum(yy);
@@ -240,21 +286,11 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       const double gnn = __ldg(grow + nid);
       const int bs = hslot<U>(bestj);
       double ww = 0.0;
-#pragma unroll 2
-      for (int i = 0; i < k; i++) {
-        const double *hi = h + i * HS;
-        const double wi = hi[bs];  // = q_i^T d_{j*}
-        ww = fma(wi, wi, ww);
-        if (U == 1) {
-          hacc[0] = fma(-wi, hi[lane], hacc[0]);
-        } else {
-#pragma unroll
-          for (int v = 0; v < U / 2; v++) {
-            const double2 t2 = *(const double2 *)(hi + v * 64 + lane * 2);
-            hacc[2 * v] = fma(-wi, t2.x, hacc[2 * v]);
-            hacc[2 * v + 1] = fma(-wi, t2.y, hacc[2 * v + 1]);
-          }
-        }
+      if (HSM) {
+        h_sweep<U, 2>(hs, 0, k, bs, lane, hacc, ww);
+      } else {
+        h_sweep<U, 2>(hs, 0, k < nr ? k : nr, bs, lane, hacc, ww);
+        if (k > nr) h_sweep<U, 4>(hg, nr, k, bs, lane, hacc, ww);
       }
       const double d2 = gnn - ww;
       if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
@@ -263,7 +299,7 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       }
       const double inv_d = rsqrt(d2);
       const double zk = cj * inv_d;  // q_k^T y = q_k^T r = <d_{j*}, r> / d
-      double *hk = h + k * HS;
+      double *hk = (HSM || k < nr ? hs : hg) + (int64_t)k * HS;
       if (U == 1) {
         const double hv = hacc[0] * inv_d;
         hk[lane] = hv;
@@ -291,7 +327,7 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       const double gap = rn2 - tol2;
       if (gap > band) continue;
       if (gap < -band) break;
-      back_substitute<U>(h, kdone, zv, iv, pj, xv, lane);
+      back_substitute<U>(hs, hg, nr, kdone, zv, iv, pj, xv, lane);
       double rr = 0.0;
       for (int i = lane; i < n; i += 32) {
         double ri = (double)yg[i];
@@ -305,11 +341,12 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
 
   if (delegate) {
     if (lane == 0) a.status[p] |= ST_DELEGATE;
-    return;  // the exact engine rewrites every output of this signal
+    __syncwarp();
+    continue;  // the exact engine rewrites every output of this signal
   }
   // ---- coefficients (pick order), exact final residual norm
   __syncwarp();
-  back_substitute<U>(h, kdone, zv, iv, pj, xv, lane);
+  back_substitute<U>(hs, hg, nr, kdone, zv, iv, pj, xv, lane);
   if (kdone > 0) {
     // |r| = sqrt(|y|^2 - |z|^2) is accurate to ~1e-16 |y|^2 / |r|^2 relative;
     // re-materialise the residual exactly only when that is not tight
@@ -335,6 +372,8 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
     a.out_scans[p] = scans;
     a.out_flag[p] = 0;
   }
+  __syncwarp();  // the next signal re-stages the shared region
+  }
 }
 
 template <typename YT, int U, bool HSM>
@@ -352,8 +391,9 @@ cudaError_t launch_gram_tuh(const GramArgs &args, const YT *ys, int h_in_smem, i
 template <typename YT, int U>
 cudaError_t launch_gram_tu(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
                            int wpb, int64_t blocks, cudaStream_t stream) {
-  return h_in_smem ? launch_gram_tuh<YT, U, true>(args, ys, h_in_smem, per_warp, wpb, blocks, stream)
-                   : launch_gram_tuh<YT, U, false>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+  return args.hwork == nullptr
+             ? launch_gram_tuh<YT, U, true>(args, ys, h_in_smem, per_warp, wpb, blocks, stream)
+             : launch_gram_tuh<YT, U, false>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
 }
 
 template <typename YT>
@@ -375,6 +415,31 @@ cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int u, int h_in_sm
 
 int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_cands); }
 
+GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
+                                int max_smem_per_block, int num_sms) {
+  GramStreamPlan pl{};
+  const int64_t hs = gram_hs(s);
+  int wpb = kStreamWarpsPerSm;
+  if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) > 0 ? atoi(v) : wpb;
+  if (wpb > 32) wpb = 32;
+  const int64_t fixed = 8 * ((5 * kw + 1) & ~int64_t(1));
+  int64_t per_warp = ((int64_t)max_smem_per_block / wpb) & ~int64_t(15);
+  // shared memory only holds whole H rows (plus the y / alpha0 staging if needed)
+  int64_t region = per_warp - fixed;
+  int64_t nr = region > 0 ? region / (8 * hs) : 0;
+  if (nr > kw) nr = kw;
+  const int64_t need = stage_y ? n + s : 0;
+  int64_t rd = nr * hs > need ? nr * hs : need;
+  per_warp = (fixed + 8 * rd + 15) & ~int64_t(15);
+  pl.ok = per_warp <= max_smem_per_block / wpb && per_warp > fixed;
+  pl.wpb = wpb;
+  pl.nr = (int)nr;
+  pl.per_warp_smem = per_warp;
+  pl.warps = (int64_t)num_sms * wpb;
+  pl.slot_doubles = (kw - nr) * hs;
+  return pl;
+}
+
 int64_t gram_total_smem(int64_t s, int64_t kw, int64_t n, bool h_in_smem) {
   const int64_t b = 8 * (((5 * kw + 1) & ~int64_t(1)) + gram_region_doubles(s, kw, n, h_in_smem));
   return (b + 15) & ~int64_t(15);
@@ -387,9 +452,21 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   if (args.p <= 0) return cudaSuccess;
   const int64_t s = args.max_cands, kw = args.k_width, n = args.n;
   const bool h_in_smem = args.hwork == nullptr;
+  if (kw > 64 || s > 512) return cudaErrorInvalidValue;
+  if (!h_in_smem) {  // streamed H: persistent warps, one block per SM
+    const GramStreamPlan pl = gram_stream_plan(s, kw, n, args.alpha0_in == nullptr,
+                                               max_smem_per_block, num_sms);
+    if (!pl.ok) return cudaErrorInvalidValue;
+    const int u = (int)(gram_hs(s) / 32);
+    note_launch();
+    if (ys_f32)
+      return launch_gram_y<float>(args, (const float *)ys, u, pl.nr, pl.per_warp_smem, pl.wpb,
+                                  num_sms, stream);
+    return launch_gram_y<double>(args, (const double *)ys, u, pl.nr, pl.per_warp_smem, pl.wpb,
+                                 num_sms, stream);
+  }
   const int64_t per_warp = gram_total_smem(s, kw, n, h_in_smem);
   if (per_warp > max_smem_per_block) return cudaErrorInvalidValue;
-  if (kw > 64 || s > 512) return cudaErrorInvalidValue;
   const int u = (int)(gram_hs(s) / 32);
   const int cap = u <= 8 ? 16 : 8;
   int max_w = (int)(max_smem_per_block / per_warp);
@@ -400,10 +477,10 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
   const int64_t blocks = (args.p + wpb - 1) / wpb;
   note_launch();
   if (ys_f32)
-    return launch_gram_y<float>(args, (const float *)ys, u, h_in_smem ? 1 : 0, per_warp, wpb,
-                                blocks, stream);
-  return launch_gram_y<double>(args, (const double *)ys, u, h_in_smem ? 1 : 0, per_warp, wpb,
-                               blocks, stream);
+    return launch_gram_y<float>(args, (const float *)ys, u, (int)kw, per_warp, wpb, blocks,
+                                stream);
+  return launch_gram_y<double>(args, (const double *)ys, u, (int)kw, per_warp, wpb, blocks,
+                               stream);
 }
 
 }  // namespace cdb
