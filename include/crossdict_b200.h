@@ -291,6 +291,13 @@ typedef struct {
 } cdb_csd_scale;
 cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *scales,
                         double *const *atoms_t);
+/* The same parse over an in-memory file image (read the file once, parse the
+ * header, size the buffers, parse the same bytes again: no window for the file
+ * to change between the calls).  capacity[s] (optional): doubles available in
+ * atoms_t[s]; a scale larger than its buffer is refused (CDB_ERR_ARG). */
+cdb_status cdb_csd_parse(const uint8_t *data, int64_t size, const char *name,
+                         int32_t *scale_count, cdb_csd_scale *scales, double *const *atoms_t,
+                         const int64_t *capacity);
 
 /* Host layout helper: rows[j][i] = cols[i][j] for an n x p column batch (the
  * reference's N x P signal matrix) into p x n rows (the kernel layout; the

@@ -25,7 +25,7 @@ SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",
            "cdb_omp_batch_blocked", "cdb_zero_tree_batch", "cdb_launch_count",
            "cdb_last_run_info", "cdb_profile_enable", "cdb_profile_read",
            "cdb_debug_corr_topk", "cdb_rows_from_cols", "cdb_extract_patches",
-           "cdb_reconstruct_aggregate", "cdb_aggregate_patches", "cdb_csd_read",
+           "cdb_reconstruct_aggregate", "cdb_aggregate_patches", "cdb_csd_read", "cdb_csd_parse",
            "cdb_omp_batch_blocked_ragged", "cdb_omp_batch_masked", "cdb_omp_batch_coded", "cdb_ksvd_update")
 
 _lib = None
@@ -55,6 +55,7 @@ def load():
     lib.cdb_reconstruct_aggregate.argtypes = [P, P, P, I64, I64, P, I32, P, P, P, P, P, P]
     lib.cdb_aggregate_patches.argtypes = [P, P, I32, P, P, P, P, P, P]
     lib.cdb_csd_read.argtypes = [ctypes.c_char_p, P, P, P]
+    lib.cdb_csd_parse.argtypes = [P, I64, ctypes.c_char_p, P, P, P, P]
     lib.cdb_omp_batch_masked.argtypes = [P, P, P, P, I64, I64, P, P, P, P, P, P, P, P]
     lib.cdb_ksvd_update.argtypes = [I64, I64, I64, P, P, P, P, P, P, I64, I64, I64, P, P]
     lib.cdb_omp_batch_coded.argtypes = [P, P, I64, P, I64, I32, P, I64, I64, P, P, I64, P, I64,

@@ -24,6 +24,7 @@ struct cdb_dictionary {
   double dmax = 0.0;       // largest atom norm
   double emax = 0.0;       // largest |bf16(d_j) - d_j| (tensor-engine certification)
   int64_t bytes = 0;
+  int device = -1;         // CUDA device holding the arrays
 };
 
 namespace {
@@ -35,13 +36,21 @@ thread_local int g_last_engine = 0;     // engine the last run_omp used
 // the host (after a device sync).  No copy is ever queued on the compute
 // stream: a small D2H there would wait behind a pipeline's output copies on
 // the copy engine and stall the next chunk.
-thread_local int *g_diag = nullptr;  // device: [0] delegated, [1] rescans
+// per thread and per device: [0] delegated, [1] rescans
+constexpr int kMaxDevices = 64;
+thread_local int *g_diag_per_dev[kMaxDevices] = {};
+thread_local int *g_diag = nullptr;  // the current device's counters
 int *diag_dev() {
-  if (!g_diag) {
-    cudaMalloc((void **)&g_diag, 2 * sizeof(int));
-    cudaMemset(g_diag, 0, 2 * sizeof(int));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int *&slot = g_diag_per_dev[dev];
+  if (!slot) {
+    cudaMalloc((void **)&slot, 2 * sizeof(int));
+    cudaMemset(slot, 0, 2 * sizeof(int));
   }
-  return g_diag;
+  g_diag = slot;
+  return slot;
 }
 void diag_clear(cudaStream_t st) { cudaMemsetAsync(diag_dev(), 0, 2 * sizeof(int), st); }
 std::atomic<int64_t> g_launches{0};
@@ -527,6 +536,25 @@ std::vector<int64_t> chunk_bounds(int64_t p, int kind) {
   return b;
 }
 
+// A dictionary is usable only on the device it was staged on.
+cdb_status check_device(const cdb_dictionary *d) {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (d && d->device != dev)
+    return fail(CDB_ERR_ARG, "dictionary was staged on device " + std::to_string(d->device) +
+                                 ", current device is " + std::to_string(dev));
+  return CDB_OK;
+}
+
+// The pipeline copies every array with explicit H2D / D2H kinds, so it is
+// taken only when every array given is host memory (mixed host / device
+// argument sets go through the per-array staging of OutArr instead).
+bool all_host(const std::vector<RowArr> &arrs) {
+  for (const RowArr &a : arrs)
+    if (a.host && is_device_ptr(a.host)) return false;
+  return true;
+}
+
 template <typename Core>
 cdb_status run_pipelined(int64_t p, std::vector<RowArr> &arrs, cudaStream_t st, Core core,
                           int kind = 0) {
@@ -878,17 +906,18 @@ static std::string py_tuple(const int64_t *v, int r) {  // Python's tuple repr
   return s + (r == 1 ? ",)" : ")");
 }
 
-cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *scales,
-                        double *const *atoms_t) {
-  if (!path || !scale_count || !scales) return fail(CDB_ERR_ARG, "bad csd arguments");
-  const std::string P(path);
-  FILE *f = fopen(path, "rb");
-  if (!f) return fail(CDB_ERR_ARG, P + ": cannot open");
-  std::vector<uint8_t> raw;
-  uint8_t chunk[1 << 16];
-  size_t got;
-  while ((got = fread(chunk, 1, sizeof(chunk), f)) > 0) raw.insert(raw.end(), chunk, chunk + got);
-  fclose(f);
+namespace {
+// Parse one in-memory .csd image.  atoms_t[s] (when given) receives scale s's
+// T x N rows; capacity[s] (doubles, when given) must cover them.
+cdb_status csd_parse(const uint8_t *raw_data, size_t raw_size, const std::string &P,
+                     int32_t *scale_count, cdb_csd_scale *scales, double *const *atoms_t,
+                     const int64_t *capacity) {
+  struct {
+    const uint8_t *p;
+    size_t n;
+    const uint8_t *data() const { return p; }
+    size_t size() const { return n; }
+  } raw{raw_data, raw_size};
   if (raw.size() < 16) return fail(CDB_ERR_FORMAT, P + ": too short for a model file");
   uint32_t stored;
   memcpy(&stored, raw.data() + raw.size() - 4, 4);
@@ -925,7 +954,8 @@ cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *s
       uint32_t e;
       take(e);
       sc.extents[d] = e;
-      prod *= e;
+      if (__builtin_mul_overflow(prod, (int64_t)e, &prod))
+        return fail(CDB_ERR_FORMAT, P + ": patch shape overflows");
     }
     uint32_t nn, tt, kk, qq;
     if (pos + 16 > body) return fail(CDB_ERR_FORMAT, P + ": truncated file");
@@ -941,9 +971,15 @@ cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *s
     sc.t = tt;
     sc.k = kk;
     sc.q = qq;
-    const size_t bytes = (size_t)8 * nn * tt;
-    if (pos + bytes > body) return fail(CDB_ERR_FORMAT, P + ": truncated atom data");
-    if (atoms_t && atoms_t[sidx]) memcpy(atoms_t[sidx], raw.data() + pos, bytes);
+    uint64_t elems, bytes;
+    if (__builtin_mul_overflow((uint64_t)nn, (uint64_t)tt, &elems) ||
+        __builtin_mul_overflow(elems, (uint64_t)8, &bytes) || bytes > body - pos)
+      return fail(CDB_ERR_FORMAT, P + ": truncated atom data");
+    if (atoms_t && atoms_t[sidx]) {
+      if (capacity && (capacity[sidx] < 0 || (uint64_t)capacity[sidx] < elems))
+        return fail(CDB_ERR_ARG, P + ": atom buffer too small for scale " + std::to_string(sidx));
+      memcpy(atoms_t[sidx], raw.data() + pos, bytes);
+    }
     pos += bytes;
   }
   *scale_count = (int32_t)count;
@@ -963,6 +999,29 @@ cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *s
                                       py_tuple(lo.extents, lo.rank));
   }
   return CDB_OK;
+}
+}  // namespace
+
+cdb_status cdb_csd_read(const char *path, int32_t *scale_count, cdb_csd_scale *scales,
+                        double *const *atoms_t) {
+  if (!path || !scale_count || !scales) return fail(CDB_ERR_ARG, "bad csd arguments");
+  const std::string P(path);
+  FILE *f = fopen(path, "rb");
+  if (!f) return fail(CDB_ERR_ARG, P + ": cannot open");
+  std::vector<uint8_t> raw;
+  uint8_t chunk[1 << 16];
+  size_t got;
+  while ((got = fread(chunk, 1, sizeof(chunk), f)) > 0) raw.insert(raw.end(), chunk, chunk + got);
+  fclose(f);
+  return csd_parse(raw.data(), raw.size(), P, scale_count, scales, atoms_t, nullptr);
+}
+
+cdb_status cdb_csd_parse(const uint8_t *data, int64_t size, const char *name,
+                         int32_t *scale_count, cdb_csd_scale *scales, double *const *atoms_t,
+                         const int64_t *capacity) {
+  if (!data || size < 0 || !scale_count || !scales) return fail(CDB_ERR_ARG, "bad csd arguments");
+  return csd_parse(data, (size_t)size, name ? std::string(name) : std::string("<memory>"),
+                   scale_count, scales, atoms_t, capacity);
 }
 
 cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_size, void *rows,
@@ -1003,8 +1062,9 @@ cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_s
 void cdb_last_run_info(int *engine, int *delegated, int *rescans) {
   if (engine) *engine = g_last_engine;
   int h[2] = {0, 0};
-  if (g_diag && cudaDeviceSynchronize() == cudaSuccess)
-    cudaMemcpy(h, g_diag, sizeof(h), cudaMemcpyDeviceToHost);
+  int *diag = g_diag ? diag_dev() : nullptr;
+  if (diag && cudaDeviceSynchronize() == cudaSuccess)
+    cudaMemcpy(h, diag, sizeof(h), cudaMemcpyDeviceToHost);
   if (delegated) *delegated = h[0];
   if (rescans) *rescans = h[1];
 }
@@ -1030,6 +1090,7 @@ cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
   if (s0 != CDB_OK) return s0;
   cudaStream_t st = (cudaStream_t)stream;
   auto *d = new cdb_dictionary();
+  cudaGetDevice(&d->device);
   d->t = t;
   d->n = n;
   d->n_pad = (n + 63) / 64 * 64;
@@ -1113,6 +1174,7 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
   DevInfo di;
   cdb_status s0 = device_info(di);
   if (s0 != CDB_OK) return s0;
+  if ((s0 = check_device(dict)) != CDB_OK) return s0;
   cudaStream_t st = (cudaStream_t)stream;
   const bool f32 = ys_is_f32 != 0;
   const int64_t n = dict->n;
@@ -1127,6 +1189,7 @@ static cdb_status omp_common(const cdb_dictionary *dict, const void *ys, int ys_
         {out_scans, sizeof(int64_t), true}, {out_flag, sizeof(uint8_t), true},
         {(void *)nb, sizeof(int64_t), false}};
     if (!mode) arrs[2].host = nullptr;
+    if (all_host(arrs))
     return run_pipelined(p, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
                                           cudaStream_t s2) -> cdb_status {
       cdb::Cands c{};
@@ -1390,6 +1453,7 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   DevInfo di;
   cdb_status s0 = device_info(di);
   if (s0 != CDB_OK) return s0;
+  if ((s0 = check_device(low)) != CDB_OK || (s0 = check_device(high)) != CDB_OK) return s0;
   cudaStream_t st = (cudaStream_t)stream;
   const bool f32 = ys_is_f32 != 0;
   const int64_t n = high->n;
@@ -1404,17 +1468,19 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
         {high_sel, sizeof(int64_t) * k_high, true}, {high_coef, sizeof(double) * k_high, true},
         {high_count, sizeof(int64_t), true}, {high_rnorm, sizeof(double), true},
         {high_scans, sizeof(int64_t), true}, {high_flag, sizeof(uint8_t), true}};
-    StepTimer tm;
-    cdb_status s = run_pipelined(p, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
-                                                  cudaStream_t s2) -> cdb_status {
-      Outs lo, hi;
-      dev_outs(lo, dv[1], dv[2], dv[3], dv[4], dv[5], dv[6]);
-      dev_outs(hi, dv[7], dv[8], dv[9], dv[10], dv[11], dv[12]);
-      return zero_tree_core(low, high, fine_shape, factors, rank, dv[0], f32, len, k1, k_high,
-                            rel_tol, phi_mode, lo, hi, engine, step_ms ? &tm : nullptr, di, s2);
-    });
-    tm.finish(step_ms);
-    return s;
+    if (all_host(arrs)) {
+      StepTimer tm;
+      cdb_status s = run_pipelined(p, arrs, st, [&](int64_t, int64_t len, std::vector<void *> &dv,
+                                                    cudaStream_t s2) -> cdb_status {
+        Outs lo, hi;
+        dev_outs(lo, dv[1], dv[2], dv[3], dv[4], dv[5], dv[6]);
+        dev_outs(hi, dv[7], dv[8], dv[9], dv[10], dv[11], dv[12]);
+        return zero_tree_core(low, high, fine_shape, factors, rank, dv[0], f32, len, k1, k_high,
+                              rel_tol, phi_mode, lo, hi, engine, step_ms ? &tm : nullptr, di, s2);
+      });
+      tm.finish(step_ms);
+      return s;
+    }
   }
   InArr y_in;
   CDB_CUDA(y_in.bind(ys, (f32 ? 4 : 8) * p * n, st));

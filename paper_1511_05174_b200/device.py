@@ -61,11 +61,20 @@ class DeviceDictionary:
 _cache: "OrderedDict[tuple, tuple]" = OrderedDict()
 
 
+def _current_device() -> int:
+    try:
+        import torch
+        return torch.cuda.current_device() if torch.cuda.is_available() else -1
+    except Exception:
+        return -1
+
+
 def device_dictionary(atoms_t: np.ndarray) -> DeviceDictionary:
-    """Cached device staging of a T x N atom-row matrix."""
+    """Cached device staging of a T x N atom-row matrix (per CUDA device)."""
     atoms_t = np.asarray(atoms_t)
+    dev = _current_device()
     if not atoms_t.flags.writeable:
-        key = ("ro", id(atoms_t), atoms_t.shape)
+        key = ("ro", dev, id(atoms_t), atoms_t.shape)
         hit = _cache.get(key)
         if hit is not None and hit[0]() is atoms_t:
             _cache.move_to_end(key)
@@ -79,7 +88,7 @@ def device_dictionary(atoms_t: np.ndarray) -> DeviceDictionary:
         flat = data.reshape(-1)
         sample = tuple(float(flat[i]) for i in (0, flat.size // 3, flat.size // 2, flat.size - 1)) \
             if flat.size else ()
-        key = ("rw", data.shape, sample)
+        key = ("rw", dev, data.shape, sample)
         hit = _cache.get(key)
         if hit is not None and np.array_equal(hit[2], data):
             _cache.move_to_end(key)
@@ -140,29 +149,74 @@ def _out(p, k):
                 scans=mk((p,), np.int64), flag=mk((p,), np.uint8))
 
 
+_OUT_DTYPES = (("sel", np.int64), ("alpha", np.float64), ("counts", np.int64),
+               ("rnorm", np.float64), ("scans", np.int64), ("flag", np.uint8))
+
+
+def _is_tensor(a) -> bool:
+    return hasattr(a, "data_ptr") and hasattr(a, "is_contiguous")
+
+
+def _check_tensor(a, dtypes, name):
+    import torch
+    allowed = [getattr(torch, np.dtype(d).name) for d in dtypes]
+    if a.dtype not in allowed:
+        raise TypeError(f"{name}: tensor dtype {a.dtype}, expected one of {allowed}")
+    if not a.is_contiguous():
+        raise TypeError(f"{name}: tensor must be contiguous")
+
+
+def _arg(a, dtype, name):
+    """(keepalive, pointer) of an input array: numpy arrays are converted to a
+    C-contiguous ``dtype`` copy when needed (the caller keeps the returned
+    object alive across the C call); tensors must already match."""
+    if a is None:
+        return None, None
+    if _is_tensor(a):
+        _check_tensor(a, (dtype,), name)
+        return a, N.ptr(a)
+    c = np.ascontiguousarray(a, dtype=dtype)
+    return c, N.ptr(c)
+
+
 def _out_ptrs(o):
-    return [N.ptr(o[k]) for k in ("sel", "alpha", "counts", "rnorm", "scans", "flag")]
+    ptrs = []
+    for k, dt in _OUT_DTYPES:
+        a = o[k]
+        if _is_tensor(a):
+            _check_tensor(a, (dt,), k)
+        elif not (isinstance(a, np.ndarray) and a.dtype == dt and a.flags.c_contiguous
+                  and a.flags.writeable):
+            raise TypeError(f"output {k!r} must be a writeable C-contiguous {np.dtype(dt).name} array")
+        ptrs.append(N.ptr(a))
+    return ptrs
 
 
 def _ys_arg(ys):
-    """(pointer, is_f32) for fp64/fp32 signal rows (numpy or CUDA tensor)."""
-    if isinstance(ys, np.ndarray):
-        if ys.dtype == np.float32:
-            return N.ptr(np.ascontiguousarray(ys)), 1
-        return N.ptr(np.ascontiguousarray(ys, dtype=np.float64)), 0
-    import torch  # device tensor
-    return N.ptr(ys), 1 if ys.dtype == torch.float32 else 0
+    """(keepalive, pointer, is_f32) for fp32/fp64 signal rows (numpy or tensor).
+    Other numpy dtypes are converted to fp64; tensors must be contiguous fp32
+    or fp64 (read as raw rows by the library)."""
+    if _is_tensor(ys):
+        _check_tensor(ys, (np.float32, np.float64), "ys")
+        import torch
+        return ys, N.ptr(ys), 1 if ys.dtype == torch.float32 else 0
+    ys = np.asarray(ys)
+    c = np.ascontiguousarray(ys, dtype=np.float32 if ys.dtype == np.float32 else np.float64)
+    return c, N.ptr(c), 1 if c.dtype == np.float32 else 0
 
 
 def omp_batch_raw(dd: DeviceDictionary, ys, p: int, k_max: int, eps, allowed=None,
                   engine: str = "auto", out=None, stream=None):
     """cdb_omp_batch: signals as rows; returns the BatchSolve arrays (dict)."""
     o = out if out is not None else _out(p, k_max)
-    yptr, f32 = _ys_arg(ys)
+    yk, yptr, f32 = _ys_arg(ys)
+    ek, eptr = _arg(eps, np.float64, "eps")
+    ak, aptr = _arg(allowed, np.int64, "allowed")
     s = 0 if allowed is None else int(allowed.shape[1])
-    N.check(N.load().cdb_omp_batch(dd.handle, yptr, f32, p, k_max, N.ptr(eps), N.ptr(allowed), s,
+    N.check(N.load().cdb_omp_batch(dd.handle, yptr, f32, p, k_max, eptr, aptr, s,
                                    0 if allowed is None else 1, *_out_ptrs(o),
                                    N.ENGINES[engine], stream))
+    del yk, ek, ak
     return o
 
 
@@ -170,10 +224,13 @@ def omp_batch_blocked_raw(dd: DeviceDictionary, ys, p: int, k_max: int, eps, blo
                           engine: str = "auto", out=None, stream=None):
     """cdb_omp_batch_blocked: allowed = blocks * q + [0, q)."""
     o = out if out is not None else _out(p, k_max)
-    yptr, f32 = _ys_arg(ys)
-    N.check(N.load().cdb_omp_batch_blocked(dd.handle, yptr, f32, p, k_max, N.ptr(eps),
-                                           N.ptr(blocks), int(blocks.shape[1]), int(q),
+    yk, yptr, f32 = _ys_arg(ys)
+    ek, eptr = _arg(eps, np.float64, "eps")
+    bk, bptr = _arg(blocks, np.int64, "blocks")
+    N.check(N.load().cdb_omp_batch_blocked(dd.handle, yptr, f32, p, k_max, eptr, bptr,
+                                           int(blocks.shape[1]), int(q),
                                            *_out_ptrs(o), N.ENGINES[engine], stream))
+    del yk, ek, bk
     return o
 
 
@@ -186,11 +243,12 @@ def zero_tree_raw(low: DeviceDictionary, high: DeviceDictionary, fine_shape, fac
     fs = np.asarray(fine_shape if fine_shape is not None else [1], dtype=np.int64)
     fa = np.asarray(factors if factors is not None else [1], dtype=np.int64)
     ms = np.zeros(2, np.float32)
-    yptr, f32 = _ys_arg(ys)
+    yk, yptr, f32 = _ys_arg(ys)
     N.check(N.load().cdb_zero_tree_batch(low.handle, high.handle, N.ptr(fs), N.ptr(fa), int(fs.size),
                                          yptr, f32, p, k1, k_high, float(rel_tol), int(phi_mode),
                                          *_out_ptrs(lo), *_out_ptrs(hi), N.ENGINES[engine],
                                          N.ptr(ms), stream))
+    del yk
     return lo, hi, ms
 
 
@@ -258,11 +316,15 @@ def omp_batch_blocked_ragged_raw(dd: DeviceDictionary, ys, p: int, k_max: int, e
                                  q: int, engine: str = "auto", out=None, stream=None):
     """cdb_omp_batch_blocked_ragged: signal p uses the first nb[p] ids of row p."""
     o = out if out is not None else _out(p, k_max)
-    yptr, f32 = _ys_arg(ys)
-    N.check(N.load().cdb_omp_batch_blocked_ragged(dd.handle, yptr, f32, p, k_max, N.ptr(eps),
-                                                  N.ptr(blocks), int(blocks.shape[1]), N.ptr(nb),
+    yk, yptr, f32 = _ys_arg(ys)
+    ek, eptr = _arg(eps, np.float64, "eps")
+    bk, bptr = _arg(blocks, np.int64, "blocks")
+    nk, nptr = _arg(nb, np.int64, "nb")
+    N.check(N.load().cdb_omp_batch_blocked_ragged(dd.handle, yptr, f32, p, k_max, eptr, bptr,
+                                                  int(blocks.shape[1]), nptr,
                                                   int(q), *_out_ptrs(o), N.ENGINES[engine],
                                                   stream))
+    del yk, ek, bk, nk
     return o
 
 
@@ -270,8 +332,12 @@ def omp_batch_masked_raw(dd: DeviceDictionary, ys, rows, m, p: int, k_max: int, 
                          stream=None):
     """cdb_omp_batch_masked: OMP of ys[p][:m[p]] over D[rows[p][:m[p]], :]."""
     o = out if out is not None else _out(p, k_max)
-    N.check(N.load().cdb_omp_batch_masked(dd.handle, N.ptr(ys), N.ptr(rows), N.ptr(m), int(p),
-                                          int(k_max), N.ptr(eps), *_out_ptrs(o), stream))
+    keep = [_arg(ys, np.float64, "ys"), _arg(rows, np.int32, "rows"), _arg(m, np.int64, "m"),
+            _arg(eps, np.float64, "eps")]
+    (_, yptr), (_, rptr), (_, mptr), (_, eptr) = keep
+    N.check(N.load().cdb_omp_batch_masked(dd.handle, yptr, rptr, mptr, int(p),
+                                          int(k_max), eptr, *_out_ptrs(o), stream))
+    del keep
     return o
 
 
@@ -285,9 +351,12 @@ def omp_batch_coded_raw(dd: DeviceDictionary, ys, rows, m, p: int, k_max: int, e
     o = out if out is not None else _out(p, k_max)
     m_stride, fan = int(rows.shape[1]), int(rows.shape[2])
     nb_max = int(blocks.shape[1]) if blocks is not None else 0
-    N.check(N.load().cdb_omp_batch_coded(dd.handle, N.ptr(ys), m_stride, N.ptr(rows), fan,
-                                         1 if pairwise else 0, N.ptr(m), int(p), int(k_max), N.ptr(eps),
-                                         N.ptr(blocks) if blocks is not None else None, nb_max,
-                                         N.ptr(nb) if nb is not None else None, int(q),
-                                         *_out_ptrs(o), stream))
+    keep = [_arg(ys, np.float64, "ys"), _arg(rows, np.int32, "rows"), _arg(m, np.int64, "m"),
+            _arg(eps, np.float64, "eps"), _arg(blocks, np.int64, "blocks"),
+            _arg(nb, np.int64, "nb")]
+    (_, yptr), (_, rptr), (_, mptr), (_, eptr), (_, bptr), (_, nptr) = keep
+    N.check(N.load().cdb_omp_batch_coded(dd.handle, yptr, m_stride, rptr, fan,
+                                         1 if pairwise else 0, mptr, int(p), int(k_max), eptr,
+                                         bptr, nb_max, nptr, int(q), *_out_ptrs(o), stream))
+    del keep
     return o

@@ -46,13 +46,18 @@ class _Scale(ctypes.Structure):
 
 def _read(path):
     lib = N.load()
+    raw = Path(path).read_bytes()  # read once (as the reference): both parses see these bytes
+    data = np.frombuffer(raw, dtype=np.uint8)
+    name = str(path).encode()
     count = ctypes.c_int32()
     scales = (_Scale * 2)()
-    st = lib.cdb_csd_read(str(path).encode(), ctypes.byref(count), scales, None)
-    _raise(st)
+    _raise(lib.cdb_csd_parse(N.ptr(data) if data.size else ctypes.c_char_p(b""), data.size, name,
+                             ctypes.byref(count), scales, None, None))
     bufs = [np.empty((scales[i].t, scales[i].n), np.float64) for i in range(count.value)]
     arr = (ctypes.c_void_p * 2)(*[b.ctypes.data for b in bufs], *([None] * (2 - len(bufs))))
-    _raise(lib.cdb_csd_read(str(path).encode(), ctypes.byref(count), scales, arr))
+    cap = np.array([b.size for b in bufs] + [0] * (2 - len(bufs)), dtype=np.int64)
+    _raise(lib.cdb_csd_parse(N.ptr(data) if data.size else ctypes.c_char_p(b""), data.size, name,
+                             ctypes.byref(count), scales, arr, N.ptr(cap)))
     out = []
     for i in range(count.value):
         s = scales[i]

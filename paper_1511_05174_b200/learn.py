@@ -42,6 +42,12 @@ def code_stage(d, y, k, allowed_sets, block_hint):
     if block_hint is not None:
         blocks_list, q = block_hint
         n, t = d.shape
+        # the reference reaches omp_many's block checks (pursuit.py:414-420)
+        if q is None or q < 1 or t % q:
+            raise E.ConfigError("block_q must be a positive divisor of T")
+        for b in blocks_list:
+            if len(b) and (min(b) < 0 or max(b) >= t // q):
+                raise E.DomainError("block id outside [0, T/Q)")
         nb = np.array([len(b) for b in blocks_list], dtype=np.int64)
         nb_max = max(1, int(nb.max()) if m else 1)
         blocks = np.zeros((m, nb_max), dtype=np.int64)
