@@ -1,22 +1,28 @@
 #!/usr/bin/env python
 """Benchmark: signals/s of zero-tree OMP (headline) and full OMP on B200.
 
-Workload: BASELINE.json configs[1] ("video": N=256 fine / 32 coarse, T_high=2048,
-T_low=256, Q=8, K=16, 100,000 signals, sigma=0.01, fp32 inputs, stop at K or
-|r| <= 1e-3 |y|) -- the largest config whose metric fits one GPU comfortably.
-Synthetic, seeded (paper_1511_05174_b200.workloads); each rank codes its
-own 100,000-signal shard of the deterministic stream (weak scaling, no
-data-path collective: signals are independent).
+Workload: BASELINE.json configs[4] ("large": N=4096 fine / 512 coarse,
+T_high=16384, T_low=2048, Q=8, K=64, 1,000,000 signals, sigma=0.01, fp32
+inputs, stop at K or |r| <= 1e-3 |y|) -- the config the 1/2/4/8-GPU sweep
+is quoted on; its 16.4 GB of signals fit one B200.  Synthetic and seeded:
+the signals are drawn on the device (paper_1511_05174_b200.workloads.
+signals_device, the BASELINE generator in 65,536-signal blocks), so every
+rank generates just its own shard.
 
-A step = one pass of the hot path over the whole batch.  `value` times the
-step through the C ABI with the inputs resident in HBM (CUDA events on the
-launching stream, L2 flushed between steps); `e2e` times the same C-ABI call
-with pinned HOST buffers (H2D of the inputs and D2H of every output inside
-the timed region).  `--impl reference` times the reference algorithm on the
-host cores (oracle/, the C restatement of crossdict's kernel, all threads)
-on a bounded sample of the same workload.
+A step = one pass of the hot path over all 1,000,000 signals.  With N GPUs
+the signals are partitioned into N contiguous shards (strong scaling; the
+dictionary is replicated; no collective on the data path).  `value` times the
+step through the C ABI with inputs resident in HBM (CUDA events on the
+launching stream, L2 flushed between steps, max over ranks); `e2e` times the
+same C-ABI call with pinned HOST buffers (H2D of the signals and D2H of every
+output inside the timed region) plus, for N > 1, the NCCL gather of all
+outputs to rank 0; `e2e_api` times the Python drop-in
+(crossscale.zero_tree_many_arrays) on a pageable N x P fp64 column batch.
+`--impl reference` times the reference itself (crossdict's numba kernel from
+baseline/_ref, forked processes on all host cores) on a bounded sample.
 
-Run:  python bench.py [--gpus N --steps K --warmup W]   (torchrun for N > 1)
+Run:  python bench.py [--gpus N --steps K --warmup W]
+      (N > 1 without torchrun: the script launches torchrun itself)
 """
 
 from __future__ import annotations
@@ -38,15 +44,19 @@ from paper_1511_05174_b200 import workloads as W  # noqa: E402
 
 METRIC = "signals/sec for zero-tree OMP and full OMP at 1/2/4/8 B200; % of roofline"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+REF_PATH = os.path.join(REPO, "baseline", "_ref")
 
 
 def load_traffic():
-    """DRAM bytes per launch of each profiled kernel (tools/ncu_summary.py output)."""
-    try:
-        with open(os.path.join(REPO, "profiles", "r1_ncu_traffic.json")) as f:
-            return {k: v for k, v in json.load(f).items() if not k.startswith("_")}
-    except (OSError, ValueError):
-        return {}
+    """DRAM bytes per launch of each profiled kernel (profiles/*_ncu_traffic.json)."""
+    out = {}
+    for name in ("r1_ncu_traffic.json", "r2_ncu_traffic.json"):
+        try:
+            with open(os.path.join(REPO, "profiles", name)) as f:
+                out.update({k: v for k, v in json.load(f).items() if not k.startswith("_")})
+        except (OSError, ValueError):
+            pass
+    return out
 
 
 def load_peaks():
@@ -165,34 +175,173 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def run_oracle_zero_tree(ci, ys_rows, threads):
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import oracle as O
+def model_arrays(ci):
+    """(low_t, high_t, k1, fine_shape, factors, phi) of a config's zero-tree model."""
     w = W.CONFIGS[ci]
     d = W.dictionaries(ci)
     if w.measurements:
-        return O.zero_tree_phi_many(d.e_low_t, d.e_high_t, w.k, w.k, ys_rows, rel_tol=W.REL_TOL,
+        return d.e_low_t, d.e_high_t, min(w.k, w.n_signal, w.t_low), None, None, True
+    return d.low_t, d.high_t, w.k, w.fine_shape, w.factors, False
+
+
+# ---- the reference itself: crossdict (baseline/_ref) in forked processes
+_REF = {}
+
+
+def reference_available():
+    """crossdict importable from baseline/_ref (its numba kernel needs numba)."""
+    if "mod" in _REF:
+        return _REF["mod"] is not None
+    try:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/cdb_numba_cache")
+        if os.path.isdir(REF_PATH) and REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        import crossdict.crossscale as cs
+        import crossdict.pursuit as cp
+        import crossdict.scaling as sc
+        import crossdict.tensor as ct
+        _REF["mod"] = (cs, cp, sc, ct)
+    except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+        _REF["mod"] = None
+        _REF["why"] = f"{type(e).__name__}: {e}"
+    return _REF["mod"] is not None
+
+
+def _ref_model(ci):
+    cs, cp, sc, ct = _REF["mod"]
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    cp.REL_RESIDUAL_TOL = W.REL_TOL  # BASELINE stopping rule (BASELINE.md §2)
+    if w.measurements:  # cfg 3: batched OMP on the effective dictionaries
+        return ("phi", np.ascontiguousarray(d.e_low_t.T), np.ascontiguousarray(d.e_high_t.T),
+                min(w.k, w.n_signal, w.t_low), w.k, w.q)
+    return ("zt", cs.CrossScaleModel(ct.Dictionary(np.ascontiguousarray(d.low_t.T)),
+                                     ct.Dictionary(np.ascontiguousarray(d.high_t.T)),
+                                     sc.ScaleSpec(w.fine_shape, w.factors), w.k, w.k))
+
+
+def _ref_solve(model, cols):
+    """crossdict's zero-tree solve of the N x P column batch (its public API)."""
+    cs, cp, _, _ = _REF["mod"]
+    if model[0] == "zt":
+        return cs.zero_tree_many_arrays(model[1], cols)
+    _, e_low, e_high, k1, k2, q = model
+    low = cp.omp_many_arrays(e_low, cols, cp.PursuitConfig(k1))
+    blocks = np.sort(low.sel, axis=1)
+    return low, cp.omp_many_arrays(e_high, cols, cp.PursuitConfig(k2), allowed_blocks=blocks,
+                                   block_q=q), {}
+
+
+_FORK = {}
+
+
+def _ref_worker(bounds):
+    from threadpoolctl import threadpool_limits
+    lo, hi = bounds
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        _ref_solve(_FORK["model"], _FORK["cols"][:, lo:hi])
+        return time.perf_counter() - t0
+
+
+def reference_rate(ci, cols, procs):
+    """crossdict on `procs` forked processes, signals split contiguously;
+    returns (signals/s, seconds) with the time = max over processes of the
+    solver-call wall time."""
+    import multiprocessing as mp
+    p = cols.shape[1]
+    procs = max(1, min(procs, p))
+    _FORK["cols"] = cols
+    if "model" not in _FORK or _FORK.get("ci") != ci:
+        _FORK["model"] = _ref_model(ci)
+        _FORK["ci"] = ci
+    cuts = np.linspace(0, p, procs + 1).astype(int)
+    bounds = [(int(cuts[i]), int(cuts[i + 1])) for i in range(procs)]
+    if procs == 1:
+        dt = _ref_worker(bounds[0])
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            dt = max(pool.map(_ref_worker, bounds))
+    return p / dt, dt
+
+
+def reference_warm(ci, cols):
+    """JIT-compile crossdict's kernel in this process (forked children inherit it)."""
+    _FORK["model"] = _ref_model(ci)
+    _FORK["ci"] = ci
+    _ref_solve(_FORK["model"], cols[:, :1])
+
+
+def reference_cpu_baseline(ci, cols, threads, budget_s):
+    """Single-core rate, then a multi-process sample of about budget_s."""
+    reference_warm(ci, cols)
+    r1, _ = reference_rate(ci, cols[:, : min(2, cols.shape[1])], 1)
+    per_proc = int(max(1, min(cols.shape[1] // threads, round(r1 * budget_s))))
+    m = min(cols.shape[1], per_proc * threads)
+    rate, dt = reference_rate(ci, cols[:, :m], threads)
+    return {"value": rate, "unit": "signals/s", "cores": threads, "kind": "reference",
+            "single_core_value": r1,
+            "sample": f"{m} signals of configs[{ci}] zero-tree OMP in {dt:.1f} s: crossdict "
+                      f"(baseline/_ref, numba omp_batch_kernel) zero_tree_many_arrays on "
+                      f"{threads} forked processes, time = max over processes; single-core "
+                      f"rate from 2 signals on one process"}
+
+
+# ---- the C restatement of the reference kernel (oracle/), secondary figure
+def run_oracle_zero_tree(ci, ys_rows, threads):
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    low_t, high_t, k1, fs, fa, phi = model_arrays(ci)
+    w = W.CONFIGS[ci]
+    if phi:
+        return O.zero_tree_phi_many(low_t, high_t, k1, w.k, ys_rows, rel_tol=W.REL_TOL,
                                     nthreads=threads)
-    return O.zero_tree_many_arrays(d.low_t, d.high_t, w.fine_shape, w.factors, w.k, w.k, ys_rows,
-                                   rel_tol=W.REL_TOL, nthreads=threads)
+    return O.zero_tree_many_arrays(low_t, high_t, fs, fa, w.k, w.k, ys_rows, rel_tol=W.REL_TOL,
+                                   nthreads=threads)
 
 
-def cpu_rate(ci, threads, ys, budget_s=24.0):
-    """Oracle zero-tree sig/s on a bounded sample: whole passes over the
-    config's signals `ys` (the GPU batch) until ~budget_s of CPU time."""
-    probe = ys[:256]
+def port_rate(ci, ys_rows, threads, budget_s):
+    """oracle/omp_oracle.c on `threads` host threads over a bounded sample."""
+    probe = ys_rows[: min(len(ys_rows), max(threads, 16))]
     t0 = time.perf_counter()
     run_oracle_zero_tree(ci, probe, threads)
-    rate = 256 / max(time.perf_counter() - t0, 1e-6)
-    target = int(max(256, rate * budget_s))
-    done, dt = 0, 0.0
-    while done < target:
-        m = min(len(ys), target - done)
-        t0 = time.perf_counter()
-        run_oracle_zero_tree(ci, ys[:m], threads)
-        dt += time.perf_counter() - t0
-        done += m
-    return done / dt, done, dt
+    rate = len(probe) / max(time.perf_counter() - t0, 1e-6)
+    m = int(min(len(ys_rows), max(len(probe), rate * budget_s)))
+    t0 = time.perf_counter()
+    run_oracle_zero_tree(ci, ys_rows[:m], threads)
+    dt = time.perf_counter() - t0
+    return {"value": m / dt, "unit": "signals/s", "cores": threads, "kind": "port",
+            "sample": f"{m} signals in {dt:.1f} s (oracle/omp_oracle.c restating crossdict's "
+                      f"kernel, {threads} threads)"}
+
+
+def cpu_baseline(ci, ys_host):
+    """The reference (crossdict, forked processes) on the benchmark's own
+    signals, with the C port as a secondary figure; the port alone when
+    crossdict cannot be imported."""
+    threads = cpu_threads()
+    if reference_available():
+        cpu = reference_cpu_baseline(ci, np.ascontiguousarray(ys_host.T), threads, 15.0)
+        cpu["port"] = port_rate(ci, ys_host, threads, 10.0)
+    else:
+        cpu = port_rate(ci, ys_host, threads, 15.0)
+        cpu["note"] = f"crossdict unavailable: {_REF.get('why')}"
+    return cpu
+
+
+def cpu_baseline_subprocess(ci, ys_host):
+    """Run cpu_baseline in a fresh interpreter (its worker processes fork from
+    a parent without CUDA or torch threads)."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "ys.npy")
+        np.save(path, ys_host)
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--config", str(ci),
+                              "--cpu-sample", path], capture_output=True, text=True)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    if out.returncode != 0 or not lines:
+        return {"error": (out.stderr or out.stdout)[-500:]}
+    return json.loads(lines[-1])
 
 
 # ------------------------------------------------------------------ reference arm
@@ -201,34 +350,56 @@ def bench_reference(args):
     if rank != 0:
         return 0
     ci = args.config
-    threads = cpu_threads()
     w = W.CONFIGS[ci]
-    # bounded per-step sample so that warmup + steps finish within minutes
-    probe = W.signals(ci, 0, 256)
-    t0 = time.perf_counter()
-    run_oracle_zero_tree(ci, probe, threads)
-    rate = 256 / max(time.perf_counter() - t0, 1e-6)
-    sample = int(min(w.signals, max(256, rate * 4.0)))
-    ys = W.signals(ci, 0, sample)
-    for _ in range(args.warmup):
-        run_oracle_zero_tree(ci, ys[: min(sample, 512)], threads)
-    times = []
-    for _ in range(args.steps):
+    threads = cpu_threads()
+    budget = min(8.0, 150.0 / max(1, args.steps + args.warmup))
+    use_ref = reference_available()
+    # a pool of seeded signals of the workload (host stream, same distribution
+    # as the GPU arm's device stream)
+    pool_n = min(w.signals, max(4 * threads, 64))
+    ys = W.signals(ci, 0, pool_n)
+    cols = np.ascontiguousarray(ys.T)
+    if use_ref:
+        reference_warm(ci, cols)
+        r1, _ = reference_rate(ci, cols[:, :2], 1)
+        per_proc = max(1, int(round(r1 * budget)))
+        sample = per_proc * threads
+        if sample > pool_n:
+            ys = W.signals(ci, 0, sample)
+            cols = np.ascontiguousarray(ys.T)
+        for _ in range(args.warmup):  # untimed: one signal per process
+            reference_rate(ci, cols[:, :threads], threads)
+        times = [reference_rate(ci, cols[:, :sample], threads)[1] for _ in range(args.steps)]
+        kind = "reference"
+        desc = (f"{sample} signals of configs[{ci}] per step: crossdict (baseline/_ref) "
+                f"zero_tree_many_arrays, numba kernel, {threads} forked processes, time = max "
+                f"over processes; single-core {r1:.2f} signals/s")
+    else:
         t0 = time.perf_counter()
-        run_oracle_zero_tree(ci, ys, threads)
-        times.append(time.perf_counter() - t0)
+        run_oracle_zero_tree(ci, ys[:threads], threads)
+        rate = threads / max(time.perf_counter() - t0, 1e-6)
+        sample = int(min(len(ys), max(threads, rate * budget)))
+        for _ in range(args.warmup):
+            run_oracle_zero_tree(ci, ys[:threads], threads)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run_oracle_zero_tree(ci, ys[:sample], threads)
+            times.append(time.perf_counter() - t0)
+        kind = "port"
+        desc = (f"{sample} signals of configs[{ci}] per step (oracle/omp_oracle.c, {threads} "
+                f"threads; crossdict unavailable: {_REF.get('why')})")
     value = sample * len(times) / sum(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "signals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator, fp32-exact inputs)",
         "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP",
                    "signals_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "signals/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} signals of configs[{ci}] per step "
-                                   f"(oracle/omp_oracle.c, {threads} threads)"},
+        "cpu_baseline": {"value": value, "unit": "signals/s", "cores": threads, "kind": kind,
+                         "sample": desc},
         "e2e": {"value": value, "unit": "signals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -237,12 +408,24 @@ def bench_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def _outs(torch, p, k, dev="cuda", pin=False):
+    mk = (lambda shape, dt: torch.empty(shape, dtype=dt, device=dev, pin_memory=pin))
+    return dict(sel=mk((p, k), torch.int64), alpha=mk((p, k), torch.float64),
+                counts=mk((p,), torch.int64), rnorm=mk((p,), torch.float64),
+                scans=mk((p,), torch.int64), flag=mk((p,), torch.uint8))
+
+
+def _nbytes(o):
+    return sum(v.numel() * v.element_size() for v in o.values())
+
+
 def bench_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_1511_05174_b200 import _native as N
     from paper_1511_05174_b200 import device as D
+    from paper_1511_05174_b200 import sharding as SH
 
     rank, world, local = dist_env()
     # CDB_BENCH_SMOKE=1: launcher smoke test on a box with fewer GPUs than ranks
@@ -258,29 +441,20 @@ def bench_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ci = args.config
     w = W.CONFIGS[ci]
-    P = args.signals or w.signals
-    phi = bool(w.measurements)
-    d = W.dictionaries(ci)
-    low_t = d.e_low_t if phi else d.low_t
-    high_t = d.e_high_t if phi else d.high_t
-    k1 = min(w.k, w.n_signal, w.t_low) if phi else w.k
-    fs = None if phi else w.fine_shape
-    fa = None if phi else w.factors
+    total = args.num_signals or w.signals
+    s0, s1 = SH.shard_range(total, rank, world)
+    P = s1 - s0
+    low_t, high_t, k1, fs, fa, phi = model_arrays(ci)
 
-    ys_host = W.signals(ci, rank * P, (rank + 1) * P).astype(np.float32)
-    yd = torch.from_numpy(ys_host).cuda()
-    eps_full = torch.from_numpy(
-        W.REL_TOL * np.linalg.norm(ys_host.astype(np.float64), axis=1)).cuda()
+    t_gen = time.perf_counter()
+    yd = W.signals_device(ci, s0, s1)  # fp32 rows in HBM
+    eps_full = (W.REL_TOL * torch.linalg.vector_norm(yd.double(), dim=1)).contiguous()
     lo = D.device_dictionary(low_t)
     hi = D.device_dictionary(high_t)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
 
-    def outs(k, dev="cuda", pin=False):
-        mk = (lambda shape, dt: torch.empty(shape, dtype=dt, device=dev, pin_memory=pin))
-        return dict(sel=mk((P, k), torch.int64), alpha=mk((P, k), torch.float64),
-                    counts=mk((P,), torch.int64), rnorm=mk((P,), torch.float64),
-                    scans=mk((P,), torch.int64), flag=mk((P,), torch.uint8))
-
-    olo, ohi, ofull = outs(k1), outs(w.k), outs(w.k)
+    olo, ohi, ofull = _outs(torch, P, k1), _outs(torch, P, w.k), _outs(torch, P, w.k)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
@@ -290,28 +464,37 @@ def bench_ours(args):
     def full_step():
         D.omp_batch_raw(hi, yd, P, w.k, eps_full, None, "auto", ofull)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     def timed(step, k_steps):
-        total = 0.0
+        total_ms = 0.0
         for _ in range(k_steps):
             flush.zero_()
             torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
+            barrier()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
             step()
             b.record(stream)
             torch.cuda.synchronize()
-            total += a.elapsed_time(b)
-        t = torch.tensor([total], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+            total_ms += a.elapsed_time(b)
+        return max_over_ranks(total_ms)
 
     for _ in range(args.warmup):
         zt_step()
-        full_step()
+    # full OMP warm-up on a slice (allocations, one-time attributes)
+    wm = min(P, 16384)
+    D.omp_batch_raw(hi, yd[:wm], wm, w.k, eps_full[:wm], None, "auto",
+                    {k: v[:wm] for k, v in ofull.items()})
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -321,148 +504,191 @@ def bench_ours(args):
     zt_ms = timed(zt_step, args.steps)
     prof_zt = N.profile_read()
     N.profile_enable(True)
-    full_ms = timed(full_step, args.steps)
+    full_ms = timed(full_step, args.full_steps)
     prof_full = N.profile_read()
     N.profile_enable(False)
     launches = N.launch_count() - launches0
     clk = clocks.stop()
     engine_full = N.last_run_info()
-    full_scans = ofull["scans"].double().sum().item()
+    zt_value = total * args.steps / (zt_ms * 1e-3)
+    full_value = total * args.full_steps / (full_ms * 1e-3)
 
-    # ---- e2e through the C ABI with pinned host buffers
-    yh = torch.from_numpy(ys_host).pin_memory()
-    hlo, hhi = outs(k1, "cpu", True), outs(w.k, "cpu", True)
-    # numpy views so the library sees host pointers
+    # ---- e2e through the C ABI: pinned host signals in, host outputs out,
+    # plus the NCCL gather of every output to rank 0 when N > 1
+    yh = torch.empty((P, w.n_signal), dtype=torch.float32, pin_memory=True)
+    yh.copy_(yd)
+    hlo, hhi = _outs(torch, P, k1, "cpu", True), _outs(torch, P, w.k, "cpu", True)
+
     def npv(o):
         return {k: v.numpy() for k, v in o.items()}
-    hlo_n, hhi_n, yh_n = npv(hlo), npv(hhi), yh.numpy()
-    D.zero_tree_raw(lo, hi, fs, fa, yh_n, P, k1, w.k, W.REL_TOL, phi, "auto", hlo_n, hhi_n)
-    e2e_total = 0.0
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        D.zero_tree_raw(lo, hi, fs, fa, yh_n, P, k1, w.k, W.REL_TOL, phi, "auto", hlo_n, hhi_n)
-        e2e_total += time.perf_counter() - t0
-    t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_total = float(t.item())
-    h2d = P * w.n_signal * 4
-    d2h = sum(v.numel() * v.element_size() for o in (hlo, hhi) for v in o.values())
-    # full OMP end to end: the same C-ABI call with pinned host signals,
-    # tolerances and outputs (the library pipelines chunked H2D / compute / D2H)
-    hfull = outs(w.k, "cpu", True)
-    hfull_n = npv(hfull)
-    eps_h = eps_full.cpu().numpy()
-    D.omp_batch_raw(hi, yh_n, P, w.k, eps_h, None, "auto", hfull_n)
-    e2e_full_total = 0.0
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        D.omp_batch_raw(hi, yh_n, P, w.k, eps_h, None, "auto", hfull_n)
-        e2e_full_total += time.perf_counter() - t0
-    t = torch.tensor([e2e_full_total], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_full_total = float(t.item())
-    d2h_full = sum(v.numel() * v.element_size() for v in hfull.values())
 
-    # ---- roofline of the dominant kernel (zero-tree step), algorithmic flops
+    hlo_n, hhi_n, yh_n = npv(hlo), npv(hhi), yh.numpy()
+
+    gdev = None if smoke else "cuda"  # NCCL gathers device tensors; gloo host ones
+
+    def e2e_step():
+        D.zero_tree_raw(lo, hi, fs, fa, yh_n, P, k1, w.k, W.REL_TOL, phi, "auto", hlo_n, hhi_n)
+        if world > 1:
+            SH.gather_solutions(hlo_n, total, device=gdev)
+            SH.gather_solutions(hhi_n, total, device=gdev)
+
+    e2e_step()  # warm (pinned staging, pipeline buffers)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    e2e_total = 0.0
+    for _ in range(e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_total += time.perf_counter() - t0
+    e2e_total = max_over_ranks(e2e_total)
+    h2d = total * w.n_signal * 4
+    d2h = (_nbytes(hlo) + _nbytes(hhi)) * world
+    del yh
+
+    # ---- e2e through the Python drop-in on the reference's layout (rank 0, N = 1)
+    e2e_api = None
+    if rank == 0 and world == 1 and not args.no_api:
+        e2e_api = bench_dropin(torch, ci, yd, args.api_signals)
+
+    # ---- roofline of the dominant kernel and of the whole step
     peaks, peaks_kind = load_peaks()
     traffic_tab = load_traffic()
+    n_low = w.n_signal if phi else w.n_low
+    c_low = olo["counts"].cpu().numpy()
+    c_high = ohi["counts"].cpu().numpy()
     low_scans = olo["scans"].double().sum().item()
     high_scans = ohi["scans"].double().sum().item()
-    n_low = w.n_signal if phi else w.n_low
-    f_step1 = 2.0 * n_low * low_scans + flops_ls(n_low, olo["counts"].cpu().numpy())
-    f_step2 = 2.0 * w.n_signal * high_scans + flops_ls(w.n_signal, ohi["counts"].cpu().numpy())
-    # algorithmic flops per launch of each OMP kernel (one launch per step per call)
-    flops = {"gram_step1": f_step1, "resident_step1": f_step1, "exact_step1": f_step1,
-             "gram_step2": f_step2, "resident_step2": f_step2, "exact_step2": f_step2}
-    dom = max(prof_zt.items(), key=lambda kv: kv[1][0]) if prof_zt else ("none", (1.0, 1))
-    dom_name, (dom_ms_total, dom_launches) = dom
-    dom_ms = dom_ms_total / max(dom_launches, 1)
+    f_step1 = 2.0 * n_low * low_scans + flops_ls(n_low, c_low)
+    f_step2 = 2.0 * w.n_signal * high_scans + flops_ls(w.n_signal, c_high)
     p_emu = peaks["bf16_tflops"] / 6.0
-    dom_flops = flops.get(dom_name, 0.0) * args.steps / max(dom_launches, 1)
+    dom_name, (dom_total, dom_launches) = max(prof_zt.items(), key=lambda kv: kv[1][0])
+    dom_ms = dom_total / max(dom_launches, 1)
+    # algorithmic flops of one launch of the dominant kernel (SURVEY §8(d) cost
+    # model on this rank's actual scan counts)
+    step_kernels = {"gram_step2": f_step2, "resident_step2": f_step2, "exact_step2": f_step2,
+                    "gram_step1": f_step1, "resident_step1": f_step1, "exact_step1": f_step1,
+                    "corr_topk": 2.0 * n_low * low_scans}
+    dom_flops = step_kernels.get(dom_name, 0.0) * args.steps / max(dom_launches, 1)
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
-    roofline = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": p_emu,
-                "unit": "TFLOP/s", "frac": achieved / p_emu if p_emu else None,
-                "traffic": traffic_tab.get(dom_name),
-                "basis": "SURVEY §8.0 algorithmic flops 2*N*scans + 4Nk(k-1) + 11Nk per signal "
-                         f"(actual scan counts) / mean launch time; peak = {peaks_kind} bf16 "
-                         f"{peaks['bf16_tflops']} TF/s / 6 (3xTF32-emulated fp32, SURVEY §8(d)); "
-                         "traffic = DRAM bytes per launch from profiles/r1_ncu_traffic.json",
-                "launch_ms": dom_ms}
-    # full-OMP correlation kernel against the measured bf16 tensor peak: the
-    # algorithmic correlation flops 2*N*scans (actual scan counts) per launch
+    step_tf = (f_step1 + f_step2) * world / (zt_ms / args.steps * 1e-3) / 1e12
+    roofline = {
+        "bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": p_emu,
+        "unit": "TFLOP/s", "frac": achieved / p_emu, "traffic": traffic_tab.get(dom_name),
+        "launch_ms": dom_ms, "share_of_step": dom_total / max(sum(v[0] for v in prof_zt.values()),
+                                                              1e-9),
+        "step": {"achieved": step_tf, "frac": step_tf / p_emu,
+                 "flops_per_signal": (f_step1 + f_step2) / P},
+        "basis": "SURVEY §8.0/§8(d) algorithmic flops 2*N*scans + 4Nk(k-1) + 11Nk per signal of "
+                 "the kernel's step (actual scan counts) / its mean launch time; peak = "
+                 f"{peaks_kind} bf16 {peaks['bf16_tflops']} TF/s / 6 (P_emu, 3xTF32-emulated "
+                 "fp32); the Gram formulation of step 2 does ~1/128 of the scan flops, so frac "
+                 "can exceed 1; traffic = ncu DRAM bytes per launch (profiles/)"}
     corr = prof_full.get("corr_topk")
     full_roof = None
     if corr:
+        full_scans = ofull["scans"].double().sum().item()
         c_ms = corr[0] / max(corr[1], 1)
-        c_flops = 2.0 * w.n_signal * full_scans * args.steps / max(corr[1], 1)
+        c_flops = 2.0 * w.n_signal * full_scans * args.full_steps / max(corr[1], 1)
         full_roof = {"bound": "tensor", "kernel": "corr_topk",
                      "achieved": c_flops / (c_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
                      "unit": "TFLOP/s",
                      "frac": c_flops / (c_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-                     "traffic": traffic_tab.get("corr_topk"), "launch_ms": c_ms,
+                     "traffic": traffic_tab.get("corr_topk_full"), "launch_ms": c_ms,
                      "basis": "2*N*scans of the full-OMP batch (actual scan counts) / corr_topk "
-                              "time; the bf16 GEMM also scores taken atoms and finished signals"}
-
-    zt_value = world * P * args.steps / (zt_ms * 1e-3)
-    full_value = world * P * args.steps / (full_ms * 1e-3)
+                              "time, against the measured bf16 peak it runs on"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = cpu_threads()
-        rate, n, dt = cpu_rate(ci, threads, ys_host.astype(np.float64))
-        cpu = {"value": rate, "unit": "signals/s", "cores": threads, "kind": "port",
-               "sample": f"{n} signals (passes over the {P} benchmark signals) of configs[{ci}] "
-                         f"zero-tree OMP in {dt:.1f} s "
-                         f"(oracle/omp_oracle.c restating crossdict's kernel, {threads} threads)"}
+        cpu = cpu_baseline_subprocess(ci, yd[: min(P, 8192)].double().cpu().numpy())
 
-    ends = bench_pipeline_ends(peaks) if rank == 0 and world == 1 else None
-    ksvd = bench_ksvd_update(args.no_cpu) if rank == 0 and world == 1 else None
-    oprec = bench_operator_recovery(args.no_cpu) if rank == 0 and world == 1 else None
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras["pipeline_ends"] = bench_pipeline_ends(peaks)
+        extras["ksvd_update"] = bench_ksvd_update(args.no_cpu)
+        extras["operator_recovery"] = bench_operator_recovery(args.no_cpu)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": zt_value, "unit": "signals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": zt_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": zt_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE generator, fp32 inputs, fp64 dictionaries)",
-            "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP: N={w.n_high}, "
-                                   f"N_low={w.n_low}, T_high={w.t_high}, T_low={w.t_low}, "
-                                   f"Q={w.q}, K={w.k}, {P} signals per GPU, stop K or "
-                                   f"|r|<=1e-3|y|",
-                       "signals_per_gpu": P, "l2": "flushed between steps (256 MiB write)"},
-            "full_omp": {"value": full_value, "unit": "signals/s",
-                         "ms_per_step": full_ms / args.steps, "engine": engine_full[0],
-                         "roofline": full_roof,
-                         "e2e": {"value": world * P * args.steps / e2e_full_total,
-                                 "unit": "signals/s", "h2d_bytes_per_step": h2d + P * 8,
-                                 "d2h_bytes_per_step": d2h_full}},
+            "data": "synthetic (seeded BASELINE generator drawn on the device, fp32 inputs, "
+                    "fp64 dictionaries)",
+            "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP: "
+                                   f"N={w.n_high}, N_low={w.n_low}, T_high={w.t_high}, "
+                                   f"T_low={w.t_low}, Q={w.q}, K={w.k}, {total:,} signals "
+                                   f"split over {world} GPU(s), stop K or |r|<=1e-3|y|",
+                       "signals": total, "signals_per_gpu": P,
+                       "parallelism": f"signal shards x{world}, dictionary replicated",
+                       "l2": "flushed between steps (256 MiB write); inputs 16.4 GB > L2"},
+            "full_omp": {"value": full_value, "unit": "signals/s", "steps": args.full_steps,
+                         "ms_per_step": full_ms / args.full_steps, "engine": engine_full[0],
+                         "exact_rescans": engine_full[2], "roofline": full_roof,
+                         "note": f"{args.full_steps} timed pass(es) over all {total:,} signals "
+                                 "(one pass is ~10x a zero-tree step)"},
             "roofline": roofline,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_zt.items()},
-            "kernels_full_ms_per_step": {k: v[0] / args.steps for k, v in prof_full.items()},
+            "kernels_full_ms_per_step": {k: v[0] / args.full_steps for k, v in prof_full.items()},
             "cpu_baseline": cpu,
-            "pipeline_ends": ends,
-            "ksvd_update": ksvd,
-            "operator_recovery": oprec,
-            "e2e": {"value": world * P * args.steps / e2e_total, "unit": "signals/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": total * e2e_steps / e2e_total, "unit": "signals/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "what": "C-ABI cdb_zero_tree_batch on pinned host rows (chunked H2D / "
+                            "compute / D2H pipeline) + NCCL gather of all outputs to rank 0 "
+                            "when N > 1; wall clock, max over ranks; byte counts whole-job"},
+            "e2e_api": e2e_api,
+            "gen_s": t_gen,
             "clocks": clk,
             "gpu_launches": launches,
+            **extras,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_dropin(torch, ci, yd, count):
+    """zero_tree_many_arrays through the Python drop-in (the call a crossdict
+    user makes) on an N x P fp64 column batch in pageable host memory -- the
+    reference's layout -- over the first `count` benchmark signals."""
+    from paper_1511_05174_b200 import crossscale as C
+    from paper_1511_05174_b200 import pursuit as PU
+    from paper_1511_05174_b200.scaling import ScaleSpec
+    from paper_1511_05174_b200.tensor import Dictionary
+    w = W.CONFIGS[ci]
+    if w.measurements:
+        return None
+    d = W.dictionaries(ci)
+    m = int(min(count, yd.shape[0]))
+    cols = yd[:m].T.contiguous().double().cpu().numpy()  # N x P fp64, pageable
+    model = C.CrossScaleModel(Dictionary(np.ascontiguousarray(d.low_t.T)),
+                              Dictionary(np.ascontiguousarray(d.high_t.T)),
+                              ScaleSpec(w.fine_shape, w.factors), w.k, w.k)
+    old = PU.REL_RESIDUAL_TOL
+    PU.REL_RESIDUAL_TOL = W.REL_TOL
+    try:
+        # warm call (dictionary staging, pinned staging buffers), then the timed call
+        t0 = time.perf_counter()
+        C.zero_tree_many_arrays(model, cols)
+        first = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        low, high, tim = C.zero_tree_many_arrays(model, cols)
+        dt = time.perf_counter() - t0
+    finally:
+        PU.REL_RESIDUAL_TOL = old
+    return {"value": m / dt, "unit": "signals/s", "signals": m, "seconds": dt,
+            "first_call_s": first, "device_s": tim, "h2d_bytes_per_step": m * w.n_high * 8,
+            "d2h_bytes_per_step": int(sum(a.nbytes for a in (low.sel, low.alpha, low.counts,
+                                                             low.rnorm, low.scans, high.sel,
+                                                             high.alpha, high.counts,
+                                                             high.rnorm, high.scans))),
+            "what": "paper_1511_05174_b200.crossscale.zero_tree_many_arrays(model, ys) with ys "
+                    "an N x P fp64 pageable numpy array, returning BatchSolve objects; includes "
+                    "the N x P -> P x N transpose into pinned memory and all copies"}
 
 
 def bench_operator_recovery(no_cpu=False):
@@ -625,16 +851,43 @@ def bench_pipeline_ends(peaks, reps=3):
                          "reconstruct_aggregate_gbs": b_recon / (t[2] * 1e-3) / 1e9}}
 
 
+def self_launch(args):
+    """`--gpus N` without torchrun: run this script under torchrun, N ranks."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator init (nranks) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--signals", type=int, default=0, help="signals per GPU (default: config's)")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--num-signals", type=int, default=0,
+                    help="total signals over all GPUs (default: the config's)")
+    ap.add_argument("--full-steps", type=int, default=1, help="timed full-OMP passes")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="timed e2e passes (<= steps)")
+    ap.add_argument("--api-signals", type=int, default=131072, help="signals of the e2e_api leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-api", action="store_true", help="skip the e2e_api leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the f-row legs")
+    ap.add_argument("--cpu-sample", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_sample:  # internal: the cpu_baseline leg in a clean process
+        print(json.dumps(cpu_baseline(args.config, np.load(args.cpu_sample))), flush=True)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
     if args.impl == "reference":
         return bench_reference(args)
     return bench_ours(args)

@@ -110,3 +110,35 @@ def golden_dict(g, prefix=""):
     flag[g[prefix + "flag"]] = True
     return dict(counts=g[prefix + "counts"], sel=g[prefix + "sel"], alpha=g[prefix + "alpha"],
                 rnorm=g[prefix + "rnorm"], scans=g[prefix + "scans"], flag=flag)
+
+
+def check_zero_tree(d_low_t, d_high_t, q, ys, low, high, rl, rh, yl=None, min_same=0.9):
+    """The contract on a zero-tree batch: step 1 against the oracle's step 1
+    (eps = 1e-3 |W y|), step 2 on the signals whose step-1 support equals the
+    oracle's (their candidate sets are then identical; allowed = the oracle's
+    sorted blocks x Q), and the nesting invariant (crossscale.py:224).
+    ``low``/``high`` hold the device outputs of exactly these signals."""
+    p = ys.shape[0]
+    y1 = yl if yl is not None else ys
+    eps1 = 1e-3 * np.linalg.norm(y1, axis=1)
+    rep1 = compare(rl, low, d_low_t, y1, eps1)
+    assert not rep1["bad"], ("step1", rep1["bad"][:3])
+    same = np.array([np.array_equal(low["sel"][i], rl["sel"][i]) for i in range(p)])
+    assert same.mean() >= min_same, same.mean()  # enough signals for a step-2 check
+    idx = np.flatnonzero(same)
+    eps2 = 1e-3 * np.linalg.norm(ys, axis=1)
+    allowed = []
+    for i in idx:
+        c = int(rl["counts"][i])
+        b = np.sort(rl["sel"][i, :c])
+        allowed.append((b[:, None] * q + np.arange(q)[None, :]).ravel())
+
+    def sub(o):
+        return {k: np.asarray(v)[idx] for k, v in o.items() if np.ndim(v) >= 1 and len(v) == p}
+
+    rep2 = compare(sub(rh), sub(high), d_high_t, ys[idx], eps2[idx], allowed if idx.size else None)
+    assert not rep2["bad"], ("step2", rep2["bad"][:3])
+    for i in range(p):
+        parents = set(np.asarray(low["sel"][i, :int(low["counts"][i])]).tolist())
+        assert all(int(j) // q in parents for j in high["sel"][i, :int(high["counts"][i])])
+    return rep1, rep2

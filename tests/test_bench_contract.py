@@ -26,18 +26,23 @@ def test_reference_arm_line():
     assert BASE <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["warmup"] >= 3
     assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
-    assert d["cpu_baseline"]["kind"] in ("port", "reference")
+    # crossdict itself when baseline/_ref is installed, else the C port
+    has_ref = os.path.isdir(os.path.join(REPO, "baseline", "_ref", "crossdict"))
+    assert d["cpu_baseline"]["kind"] == ("reference" if has_ref else "port")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
 
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu"], 900)
+    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu", "--no-extras"], 1200)
     assert BASE <= set(d) and d.get("impl", "ours") != "reference"
-    assert d["value"] > 0 and d["scaling"] == "weak" and "workload" in d["config"]
+    assert d["value"] > 0 and d["scaling"] == "strong" and "workload" in d["config"]
+    assert d["config"]["signals"] == 1_000_000 and "configs[4]" in d["config"]["workload"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
-    assert 0 < d["roofline"]["frac"] <= 1
+    assert d["roofline"]["frac"] > 0 and 0 < d["roofline"]["step"]["frac"] <= 1
+    assert d["full_omp"]["value"] > 0
+    assert d["e2e_api"]["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["gpu_launches"] > 0
     e2e = d["e2e"]

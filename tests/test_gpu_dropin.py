@@ -1,0 +1,194 @@
+"""The public drop-in entry points on the GPU -- what a crossdict caller
+imports -- against the reference's golden outputs: omp (pursuit.py:253-300),
+omp_many_arrays (pursuit.py:388-441), omp_many (444-461), zero_tree_omp
+(crossscale.py:169-232), zero_tree_many_arrays (235-283) and
+zero_tree_omp_many (286-312).  Inputs are pageable N x P fp64 column batches
+(the reference's layout; the drop-in makes the P x N row copy, pinned for
+large batches); results are checked for their types, 1-based codes, pick
+order, timings, and the parity contract against the goldens."""
+
+import numpy as np
+import pytest
+
+from conftest import edge_names, load_golden
+from parity import batch_dict, check_zero_tree, compare, golden_dict
+
+import paper_1511_05174_b200 as P
+from paper_1511_05174_b200 import pursuit as PU
+from paper_1511_05174_b200 import workloads as W
+from paper_1511_05174_b200.crossscale import ZeroTreeResult
+from paper_1511_05174_b200.pursuit import BatchSolve, PursuitResult
+
+pytestmark = pytest.mark.gpu
+
+OMP_EDGES = [n for n in edge_names() if not n.startswith("edge_zt")]
+ZT_EDGES = [n for n in edge_names() if n.startswith("edge_zt")]
+
+
+@pytest.fixture
+def rel_tol():
+    old = PU.REL_RESIDUAL_TOL
+
+    def set_(v):
+        PU.REL_RESIDUAL_TOL = float(v)
+    yield set_
+    PU.REL_RESIDUAL_TOL = old
+
+
+def _config(g):
+    k = int(g["k"])
+    tol = float(g["tol"])
+    return PU.PursuitConfig(k, residual_tolerance=tol if tol >= 0 else None)
+
+
+def _eps(g, ys_rows):
+    if g["tol"] >= 0:
+        return np.full(ys_rows.shape[0], float(g["tol"]))
+    return float(g["rel"]) * np.linalg.norm(ys_rows, axis=1)
+
+
+def _allowed(g):
+    if "blocks" not in g:
+        return None
+    q = int(g["q"])
+    return (g["blocks"][:, :, None] * q + np.arange(q)[None, None, :]).reshape(len(g["blocks"]), -1)
+
+
+def _check_batch(s, p, k_width):
+    assert isinstance(s, BatchSolve)
+    assert s.counts.shape == (p,) and s.counts.dtype == np.int64
+    assert s.sel.shape == (p, k_width) and s.sel.dtype == np.int64
+    assert s.alpha.shape == (p, k_width) and s.alpha.dtype == np.float64
+    assert s.rnorm.dtype == np.float64 and s.scans.dtype == np.int64
+    assert isinstance(s.rank_deficient, frozenset)
+
+
+@pytest.mark.parametrize("name", OMP_EDGES)
+def test_omp_many_arrays_edges(name, rel_tol):
+    g = load_golden(name)
+    rel_tol(g["rel"])
+    ys_rows = g["ys_rows"]
+    cols = np.array(ys_rows.T)  # pageable N x P fp64
+    kw = {}
+    if "blocks" in g:
+        kw = dict(allowed_blocks=g["blocks"], block_q=int(g["q"]))
+    s = P.omp_many_arrays(np.ascontiguousarray(g["mat_t"].T), cols, _config(g), **kw)
+    _check_batch(s, ys_rows.shape[0], g["sel"].shape[1])
+    rep = compare(golden_dict(g), batch_dict(s), g["mat_t"], ys_rows, _eps(g, ys_rows),
+                  _allowed(g))
+    assert not rep["bad"], rep["bad"][:3]
+
+
+@pytest.mark.parametrize("name", ["edge_batch", "edge_ties", "edge_scans", "edge_mixed",
+                                  "edge_rank_deficient"])
+def test_scalar_omp_and_omp_many_edges(name, rel_tol):
+    g = load_golden(name)
+    rel_tol(g["rel"])
+    ys_rows = g["ys_rows"]
+    d = np.ascontiguousarray(g["mat_t"].T)
+    ref = golden_dict(g)
+    many = P.omp_many(d, np.array(ys_rows.T), _config(g))
+    assert len(many) == ys_rows.shape[0]
+    for p in range(min(ys_rows.shape[0], 12)):
+        r = P.omp(d, ys_rows[p], _config(g))
+        assert isinstance(r, PursuitResult)
+        c = int(ref["counts"][p])
+        for res in (r, many[p]):
+            assert res.iterations == c and res.atom_scan_count == int(ref["scans"][p])
+            assert res.selected == tuple(int(j) + 1 for j in ref["sel"][p, :c])  # pick order
+            assert res.code.support == tuple(sorted(res.selected))           # sorted, 1-based
+            assert res.rank_deficient == bool(ref["flag"][p])
+            if not ref["flag"][p]:
+                got = dict(res.code.entries)
+                for i, j in enumerate(res.selected):
+                    assert got[j] == pytest.approx(ref["alpha"][p, i], rel=1e-9, abs=1e-12)
+                assert res.residual_norm == pytest.approx(ref["rnorm"][p], rel=1e-9, abs=1e-12)
+
+
+def _zt_model(low_t, high_t, fine_shape, factors, k_low, k_high):
+    return P.CrossScaleModel(P.Dictionary(np.ascontiguousarray(low_t.T)),
+                             P.Dictionary(np.ascontiguousarray(high_t.T)),
+                             P.ScaleSpec(tuple(int(e) for e in fine_shape),
+                                         tuple(int(f) for f in factors)),
+                             int(k_low), int(k_high))
+
+
+def _check_zt_api(model, q, ys_rows, rl, rh, low_t, high_t, fine_shape, factors):
+    low, high, tim = P.zero_tree_many_arrays(model, np.array(ys_rows.T))
+    _check_batch(low, ys_rows.shape[0], model.k_low)
+    _check_batch(high, ys_rows.shape[0], model.k_high)
+    assert set(tim) == {"step1", "step2"} and all(v >= 0.0 for v in tim.values())
+    import oracle as O
+    yl = O.downsample_rows(ys_rows, tuple(fine_shape), tuple(factors))
+    check_zero_tree(low_t, high_t, q, ys_rows, batch_dict(low), batch_dict(high), rl, rh, yl,
+                    min_same=0.75)
+    return low, high
+
+
+@pytest.mark.parametrize("name", ZT_EDGES)
+def test_zero_tree_api_edges(name, rel_tol):
+    g = load_golden(name)
+    rel_tol(g["rel"])
+    model = _zt_model(g["low_t"], g["high_t"], g["fine_shape"], g["factors"], g["k_low"],
+                      g["k_high"])
+    ys = g["ys_rows"]
+    rl, rh = golden_dict(g, "low_"), golden_dict(g, "high_")
+    low, high = _check_zt_api(model, model.q, ys, rl, rh, g["low_t"], g["high_t"],
+                              g["fine_shape"], g["factors"])
+    # the per-signal entry points agree with the batch
+    many = P.zero_tree_omp_many(model, np.array(ys.T))
+    assert len(many) == ys.shape[0]
+    for p in range(min(ys.shape[0], 8)):
+        r = P.zero_tree_omp(model, ys[p])
+        for res in (r, many[p]):
+            assert isinstance(res, ZeroTreeResult)
+            assert res.code_low.support == tuple(sorted(int(j) + 1 for j in
+                                                        low.sel[p, :low.counts[p]]))
+            assert res.code_high.support == tuple(sorted(int(j) + 1 for j in
+                                                         high.sel[p, :high.counts[p]]))
+            assert res.scan_counts == {"step1": int(low.scans[p]), "step2": int(high.scans[p])}
+            assert res.residual_norm == pytest.approx(float(high.rnorm[p]), rel=1e-12)
+            assert set(res.timings) == {"step1", "step2"}
+
+
+@pytest.mark.parametrize("ci", [0, 1, 2, 4])
+def test_zero_tree_api_configs(ci, rel_tol):
+    rel_tol(W.REL_TOL)
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    g = load_golden(f"cfg{ci}_zt")
+    ys = W.signals_at(ci, g["ids"])
+    model = _zt_model(d.low_t, d.high_t, w.fine_shape, w.factors, w.k, w.k)
+    _check_zt_api(model, w.q, ys, golden_dict(g, "low_"), golden_dict(g, "high_"), d.low_t,
+                  d.high_t, w.fine_shape, w.factors)
+
+
+def test_zero_tree_api_large_batch_pinned_path(rel_tol):
+    """>= 4096 signals: the drop-in stages rows in pinned memory and the library
+    pipelines the host copies; results equal the small-batch path's."""
+    rel_tol(W.REL_TOL)
+    ci = 1
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    ys = W.signals(ci, 0, 40_000)
+    model = _zt_model(d.low_t, d.high_t, w.fine_shape, w.factors, w.k, w.k)
+    low, high, tim = P.zero_tree_many_arrays(model, np.array(ys.T))
+    lo2, hi2, _ = P.zero_tree_many_arrays(model, np.array(ys[:3000].T))
+    for a, b in ((low, lo2), (high, hi2)):
+        assert np.array_equal(a.sel[:3000], b.sel) and np.array_equal(a.counts[:3000], b.counts)
+        assert np.array_equal(a.alpha[:3000], b.alpha)
+    assert tim["step1"] > 0 and tim["step2"] > 0
+
+
+@pytest.mark.parametrize("ci", [0, 1, 3])
+def test_omp_many_arrays_configs(ci, rel_tol):
+    rel_tol(W.REL_TOL)
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    g = load_golden(f"cfg{ci}_full")
+    ys = W.signals_at(ci, g["ids"])
+    hi_t = d.e_high_t if w.measurements else d.high_t
+    s = P.omp_many_arrays(np.ascontiguousarray(hi_t.T), np.array(ys.T), PU.PursuitConfig(w.k))
+    _check_batch(s, ys.shape[0], w.k)
+    rep = compare(golden_dict(g), batch_dict(s), hi_t, ys, W.REL_TOL * np.linalg.norm(ys, axis=1))
+    assert not rep["bad"], rep["bad"][:3]

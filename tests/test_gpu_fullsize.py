@@ -1,25 +1,49 @@
-"""BASELINE configs at their FULL sizes, checked through size-independent
-properties (the CPU oracle cannot run them whole) -- configs 0-4, cfg 4 at one
-GPU's shard of its 1M signals: zero-tree nesting, the
-reference's scan-count formula (pursuit.py:18-20), the stop rule, residual
-consistency and least-squares optimality on samples, and the parity contract
-against the oracle on a seeded random subset."""
+"""BASELINE configs at their FULL sizes -- cfg 4 at its whole 1,000,000
+signals on one GPU -- checked with the parity contract of the north star on
+seeded subsets of the sizes SURVEY §8(d) sets (cfg 1: all 100,000 zero-tree
+and 16,384 full-OMP signals; cfg 2: 16,384 / 2,048; cfg 3: 8,192 / 4,096;
+cfg 4: 2,048 / 64), plus size-independent properties on the whole batch:
+zero-tree nesting, the reference's scan-count formula (pursuit.py:18-20), the
+stop rule, residual consistency and least-squares optimality on samples.
+
+No agreement rates: every signal of a subset either matches the oracle
+(supports in pick order, coefficients within 1e-4, counts / scans) or is
+excused by the contract (oracle top-two gap < 1e-6 at the first divergence,
+or the 1e-5 stop band); zero-tree step 2 is compared on the signals whose
+step-1 support matched (tests/parity.py).  The oracle is oracle/omp_oracle.c
+on the host's threads, fed exactly the fp32 rows the GPU consumed."""
+
+import os
 
 import numpy as np
 import pytest
 import torch
 
-from parity import compare
+from parity import check_zero_tree, compare
 
 import oracle as O
 from paper_1511_05174_b200 import device as D
 from paper_1511_05174_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
+THREADS = max(1, len(os.sched_getaffinity(0)))
+
+# subset sizes (zero-tree, full OMP): SURVEY §8(d) / BASELINE.md §2
+SUBSETS = {0: (10_000, 10_000), 1: (100_000, 16_384), 2: (16_384, 2_048), 3: (8_192, 4_096),
+           4: (2_048, 64)}
 
 
 def _host(o):
     return {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in o.items()}
+
+
+def _outs(p, k):
+    return dict(sel=torch.empty((p, k), dtype=torch.int64, device="cuda"),
+                alpha=torch.empty((p, k), dtype=torch.float64, device="cuda"),
+                counts=torch.empty(p, dtype=torch.int64, device="cuda"),
+                rnorm=torch.empty(p, dtype=torch.float64, device="cuda"),
+                scans=torch.empty(p, dtype=torch.int64, device="cuda"),
+                flag=torch.empty(p, dtype=torch.uint8, device="cuda"))
 
 
 def _scan_formula(t, counts):
@@ -27,79 +51,129 @@ def _scan_formula(t, counts):
     return t * c - c * (c - 1) // 2
 
 
-def _check_ls(mat_t, ys, sol, eps, idx):
+def _check_ls(mat_t, ys, sol, idx):
     for p in idx:
         c = int(sol["counts"][p])
+        y = ys[p] if ys.ndim == 2 else None
         if c == 0:
-            assert sol["rnorm"][p] == pytest.approx(np.linalg.norm(ys[p]), rel=1e-12)
+            assert sol["rnorm"][p] == pytest.approx(np.linalg.norm(y), rel=1e-12)
             continue
         A = mat_t[sol["sel"][p, :c]].T
-        r = ys[p] - A @ sol["alpha"][p, :c]
-        assert abs(np.linalg.norm(r) - sol["rnorm"][p]) <= 1e-9 * np.linalg.norm(ys[p])
+        r = y - A @ sol["alpha"][p, :c]
+        assert abs(np.linalg.norm(r) - sol["rnorm"][p]) <= 1e-9 * np.linalg.norm(y)
         # least-squares optimality: residual orthogonal to the support
-        assert np.abs(A.T @ r).max() <= 1e-9 * np.linalg.norm(ys[p])
+        assert np.abs(A.T @ r).max() <= 1e-9 * np.linalg.norm(y)
 
 
 def _check_stop(sol, eps, budget):
+    """Every signal ended by the stop rule (_kernels.py:156; within the
+    contract's 1e-5 stop band), its budget, or the rank-deficient path."""
     c = sol["counts"]
-    stopped = (sol["rnorm"] <= eps * (1 + 1e-9)) | (c == budget)
-    assert stopped.mean() > 0.9999
+    ok = (sol["rnorm"] <= eps * (1 + 1e-5)) | (c == budget) | (sol["flag"] != 0)
+    assert ok.all(), np.flatnonzero(~ok)[:10]
 
 
-@pytest.mark.parametrize("ci", [0, 1])
+def _nested(low_sel, low_cnt, high_sel, high_cnt, q):
+    k1, k2 = low_sel.shape[1], high_sel.shape[1]
+    ok = True
+    for s in range(0, low_sel.shape[0], 20000):
+        ls, hs = low_sel[s:s + 20000], high_sel[s:s + 20000]
+        lv = np.arange(k1)[None, :] < low_cnt[s:s + 20000, None]
+        hv = np.arange(k2)[None, :] < high_cnt[s:s + 20000, None]
+        par = np.where(hv, hs // q, -7)
+        hit = ((par[:, :, None] == np.where(lv, ls, -9)[:, None, :]).any(axis=2)) | ~hv
+        ok &= bool(hit.all())
+    return ok
+
+
+def _signals(ci, p):
+    """(device fp32 rows, host fp64 view fetcher): cfg 0/1 from the host stream
+    the goldens use, cfg 2-4 from the device stream (cfg 4: 16 GB)."""
+    if ci <= 1:
+        ys = W.signals(ci, 0, p)
+        return torch.from_numpy(ys.astype(np.float32)).cuda()
+    return W.signals_device(ci, 0, p)
+
+
+def _rows(yd, idx):
+    return yd[torch.from_numpy(np.asarray(idx)).cuda()].double().cpu().numpy()
+
+
+def _subset(ci, p, count, seed):
+    if count >= p:
+        return np.arange(p)
+    rng = np.random.default_rng([seed, ci])
+    idx = np.sort(rng.choice(p, size=count, replace=False))
+    if ci == 4:  # rows past 2^31 / N elements exercise the 64-bit offsets
+        idx[-1] = p - 1
+    return idx
+
+
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4])
 def test_zero_tree_full_size(ci):
     w = W.CONFIGS[ci]
     d = W.dictionaries(ci)
     P = w.signals
-    ys = W.signals(ci, 0, P)
-    low, high, _ = D.zero_tree_raw(D.device_dictionary(d.low_t), D.device_dictionary(d.high_t),
-                                   w.fine_shape, w.factors, ys.astype(np.float32), P, w.k, w.k,
-                                   W.REL_TOL, False, "auto")
-    # nesting (crossscale.py:224): every fine atom is a child of a coarse pick
-    for p in range(P):
-        cl, ch = int(low["counts"][p]), int(high["counts"][p])
-        parents = set(low["sel"][p, :cl].tolist())
-        assert all(int(j) // w.q in parents for j in high["sel"][p, :ch])
-    # scan counts: step 1 scans T_low per pick, step 2 scans nb*Q candidates
+    yd = _signals(ci, P)
+    phi = bool(w.measurements)
+    lo_t, hi_t = (d.e_low_t, d.e_high_t) if phi else (d.low_t, d.high_t)
+    k1 = min(w.k, w.n_signal, w.t_low) if phi else w.k
+    low, high = _outs(P, k1), _outs(P, w.k)
+    D.zero_tree_raw(D.device_dictionary(lo_t), D.device_dictionary(hi_t),
+                    None if phi else w.fine_shape, None if phi else w.factors, yd, P, k1, w.k,
+                    W.REL_TOL, phi, "auto", low, high)
+    low, high = _host(low), _host(high)
+    # whole-batch properties
+    assert _nested(low["sel"], low["counts"], high["sel"], high["counts"], w.q)
     assert np.array_equal(low["scans"], _scan_formula(w.t_low, low["counts"]))
     nbq = low["counts"].astype(np.int64) * w.q
     c2 = high["counts"].astype(np.int64)
     assert np.array_equal(high["scans"], nbq * c2 - c2 * (c2 - 1) // 2)
-    eps2 = W.REL_TOL * np.linalg.norm(ys, axis=1)
-    _check_stop(high, eps2, np.minimum(w.k, nbq))
-    rng = np.random.default_rng(ci)
-    idx = rng.choice(P, size=256, replace=False)
-    _check_ls(d.high_t, ys, high, eps2, idx)
-    # parity contract vs the oracle on the random subset
-    rl, rh = O.zero_tree_many_arrays(d.low_t, d.high_t, w.fine_shape, w.factors, w.k, w.k,
-                                     ys[idx], rel_tol=W.REL_TOL, nthreads=8)
-    sub = {k: v[idx] for k, v in high.items()}
-    sub["flag"] = sub["flag"].astype(bool)
-    same1 = np.array([np.array_equal(low["sel"][p], rl["sel"][i]) for i, p in enumerate(idx)])
-    assert same1.mean() > 0.99
-    agree = np.mean([np.array_equal(sub["sel"][i], rh["sel"][i]) for i in range(len(idx))])
-    assert agree > 0.98
+    ynorm = torch.linalg.vector_norm(yd.double(), dim=1).cpu().numpy()
+    _check_stop(high, W.REL_TOL * ynorm, np.minimum(np.minimum(w.k, nbq), w.n_signal))
+    # the contract on the SURVEY-sized subset
+    idx = _subset(ci, P, SUBSETS[ci][0], 20)
+    ys = _rows(yd, idx)
+    if phi:
+        rl, rh = O.zero_tree_phi_many(lo_t, hi_t, k1, w.k, ys, rel_tol=W.REL_TOL,
+                                      nthreads=THREADS)
+        yl = None
+    else:
+        rl, rh = O.zero_tree_many_arrays(lo_t, hi_t, w.fine_shape, w.factors, w.k, w.k, ys,
+                                         rel_tol=W.REL_TOL, nthreads=THREADS)
+        yl = O.downsample_rows(ys, w.fine_shape, w.factors)
+
+    def sub(o):
+        s = {k: v[idx] for k, v in o.items()}
+        s["flag"] = s["flag"].astype(bool)
+        return s
+
+    check_zero_tree(lo_t, hi_t, w.q, ys, sub(low), sub(high), rl, rh, yl)
+    _check_ls(hi_t, ys, sub(high), range(min(64, len(idx))))
 
 
-@pytest.mark.parametrize("ci", [0, 1])
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4])
 def test_full_omp_full_size(ci):
     w = W.CONFIGS[ci]
     d = W.dictionaries(ci)
     P = w.signals
-    ys = W.signals(ci, 0, P)
-    eps = W.REL_TOL * np.linalg.norm(ys, axis=1)
-    sol = D.omp_batch_raw(D.device_dictionary(d.high_t), ys.astype(np.float32), P, w.k, eps, None,
-                          "auto")
+    yd = _signals(ci, P)
+    hi_t = d.e_high_t if w.measurements else d.high_t
+    eps_d = (W.REL_TOL * torch.linalg.vector_norm(yd.double(), dim=1)).contiguous()
+    sol = _outs(P, w.k)
+    D.omp_batch_raw(D.device_dictionary(hi_t), yd, P, w.k, eps_d, None, "auto", sol)
+    sol = _host(sol)
+    eps = eps_d.cpu().numpy()
     assert np.array_equal(sol["scans"], _scan_formula(w.t_high, sol["counts"]))
     _check_stop(sol, eps, w.k)
-    rng = np.random.default_rng(10 + ci)
-    idx = rng.choice(P, size=256, replace=False)
-    _check_ls(d.high_t, ys, sol, eps, idx)
-    ref = O.omp_many_arrays(d.high_t, ys[idx], w.k, rel_tol=W.REL_TOL, nthreads=8)
+    idx = _subset(ci, P, SUBSETS[ci][1], 30)
+    ys = _rows(yd, idx)
+    ref = O.omp_many_arrays(hi_t, ys, w.k, rel_tol=W.REL_TOL, nthreads=THREADS)
     got = {k: v[idx] for k, v in sol.items()}
     got["flag"] = got["flag"].astype(bool)
-    rep = compare(ref, got, d.high_t, ys[idx], eps[idx])
+    rep = compare(ref, got, hi_t, ys, W.REL_TOL * np.linalg.norm(ys, axis=1))
     assert not rep["bad"], rep["bad"][:3]
+    _check_ls(hi_t, ys, got, range(min(64, len(idx))))
 
 
 def test_device_resident_inputs_match_host_inputs():
@@ -113,13 +187,7 @@ def test_device_resident_inputs_match_host_inputs():
     a_low, a_high, _ = D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, ys, len(ys), w.k, w.k,
                                        W.REL_TOL, False, "auto")
     yd = torch.from_numpy(ys).cuda()
-    mk = lambda k: dict(sel=torch.empty((len(ys), k), dtype=torch.int64, device="cuda"),
-                        alpha=torch.empty((len(ys), k), dtype=torch.float64, device="cuda"),
-                        counts=torch.empty(len(ys), dtype=torch.int64, device="cuda"),
-                        rnorm=torch.empty(len(ys), dtype=torch.float64, device="cuda"),
-                        scans=torch.empty(len(ys), dtype=torch.int64, device="cuda"),
-                        flag=torch.empty(len(ys), dtype=torch.uint8, device="cuda"))
-    ol, oh = mk(w.k), mk(w.k)
+    ol, oh = _outs(len(ys), w.k), _outs(len(ys), w.k)
     D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, yd, len(ys), w.k, w.k, W.REL_TOL, False,
                     "auto", ol, oh)
     ol, oh = _host(ol), _host(oh)
@@ -138,16 +206,10 @@ def test_pipelined_host_buffers_match_device_buffers(kind):
     ys = W.signals(ci, 0, P).astype(np.float32)
     lo, hi = D.device_dictionary(d.low_t), D.device_dictionary(d.high_t)
     yd = torch.from_numpy(ys).cuda()
-    mk = lambda k: dict(sel=torch.empty((P, k), dtype=torch.int64, device="cuda"),
-                        alpha=torch.empty((P, k), dtype=torch.float64, device="cuda"),
-                        counts=torch.empty(P, dtype=torch.int64, device="cuda"),
-                        rnorm=torch.empty(P, dtype=torch.float64, device="cuda"),
-                        scans=torch.empty(P, dtype=torch.int64, device="cuda"),
-                        flag=torch.empty(P, dtype=torch.uint8, device="cuda"))
     if kind == "zt":
         h_low, h_high, ms_h = D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, ys, P, w.k, w.k,
                                               W.REL_TOL, False, "auto")
-        d_low, d_high = mk(w.k), mk(w.k)
+        d_low, d_high = _outs(P, w.k), _outs(P, w.k)
         D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, yd, P, w.k, w.k, W.REL_TOL, False, "auto",
                         d_low, d_high)
         pairs = [(h_low, _host(d_low)), (h_high, _host(d_high))]
@@ -155,7 +217,7 @@ def test_pipelined_host_buffers_match_device_buffers(kind):
     else:
         eps = W.REL_TOL * np.linalg.norm(ys.astype(np.float64), axis=1)
         h = D.omp_batch_raw(hi, ys, P, w.k, eps, None, "auto")
-        dd = mk(w.k)
+        dd = _outs(P, w.k)
         D.omp_batch_raw(hi, yd, P, w.k, torch.from_numpy(eps).cuda(), None, "auto", dd)
         pairs = [(h, _host(dd))]
     for a, b in pairs:
@@ -163,97 +225,21 @@ def test_pipelined_host_buffers_match_device_buffers(kind):
             assert np.array_equal(a[k], b[k]), k
 
 
-# configs 2-4 at their per-GPU sizes (cfg 4: one of 8 shards of 1M); oracle
-# subsets sized so the CPU restatement finishes in seconds
-BIG = {2: dict(p=None, sub_zt=96, sub_full=24), 3: dict(p=None, sub_zt=96, sub_full=48),
-       4: dict(p=125000, sub_zt=32, sub_full=4)}
-
-
-def _fast_signals(ci, count, seed=0):
-    """Signals with the BASELINE generator's distribution (K distinct parents,
-    one child each, N(0,1) coefficients, noise sigma; Phi for the CS config),
-    built on the device -- the seeded stream of workloads.signals takes
-    minutes at cfg 4's full size.  Returned as fp32-exact fp64 rows."""
+def test_mixed_host_device_arguments():
+    # host signals with device outputs (and the reverse) take the staged path,
+    # not the host pipeline: same results as all-device arguments
+    ci = 1
     w = W.CONFIGS[ci]
     d = W.dictionaries(ci)
-    rng = np.random.default_rng([seed, 77, ci])
-    parents = np.argpartition(rng.random((count, w.t_low)), w.k, axis=1)[:, : w.k]
-    atoms = torch.from_numpy(parents * w.q + rng.integers(0, w.q, size=(count, w.k))).cuda()
-    coefs = torch.from_numpy(rng.standard_normal((count, w.k))).cuda()
-    dh = torch.from_numpy(np.array(d.high_t)).cuda()
-    x = torch.zeros((count, w.n_high), dtype=torch.float64, device="cuda")
-    for j in range(w.k):
-        x += coefs[:, j, None] * dh[atoms[:, j]]
-    if w.measurements:
-        x = x @ torch.from_numpy(np.array(d.phi)).cuda().T
-    x += w.sigma * torch.from_numpy(rng.standard_normal(tuple(x.shape))).cuda()
-    return x.float().double().cpu().numpy()
-
-
-def _nested(low_sel, low_cnt, high_sel, high_cnt, q):
-    k1, k2 = low_sel.shape[1], high_sel.shape[1]
-    ok = True
-    for s in range(0, low_sel.shape[0], 20000):
-        ls, hs = low_sel[s:s + 20000], high_sel[s:s + 20000]
-        lv = np.arange(k1)[None, :] < low_cnt[s:s + 20000, None]
-        hv = np.arange(k2)[None, :] < high_cnt[s:s + 20000, None]
-        par = np.where(hv, hs // q, -7)
-        hit = ((par[:, :, None] == np.where(lv, ls, -9)[:, None, :]).any(axis=2)) | ~hv
-        ok &= bool(hit.all())
-    return ok
-
-
-@pytest.mark.parametrize("ci", [2, 3, 4])
-def test_zero_tree_full_size_big(ci):
-    w = W.CONFIGS[ci]
-    d = W.dictionaries(ci)
-    P = BIG[ci]["p"] or w.signals
-    ys = _fast_signals(ci, P)
-    phi = bool(w.measurements)
-    lo_t, hi_t = (d.e_low_t, d.e_high_t) if phi else (d.low_t, d.high_t)
-    k1 = min(w.k, w.n_signal, w.t_low) if phi else w.k
-    low, high, _ = D.zero_tree_raw(D.device_dictionary(lo_t), D.device_dictionary(hi_t),
-                                   None if phi else w.fine_shape, None if phi else w.factors,
-                                   ys.astype(np.float32), P, k1, w.k, W.REL_TOL, phi, "auto")
-    low, high = _host(low), _host(high)
-    assert _nested(low["sel"], low["counts"], high["sel"], high["counts"], w.q)
-    assert np.array_equal(low["scans"], _scan_formula(w.t_low, low["counts"]))
-    nbq = low["counts"].astype(np.int64) * w.q
-    c2 = high["counts"].astype(np.int64)
-    assert np.array_equal(high["scans"], nbq * c2 - c2 * (c2 - 1) // 2)
-    eps2 = W.REL_TOL * np.linalg.norm(ys, axis=1)
-    _check_stop(high, eps2, np.minimum(np.minimum(w.k, nbq), ys.shape[1]))
-    rng = np.random.default_rng(20 + ci)
-    idx = np.sort(rng.choice(P, size=BIG[ci]["sub_zt"], replace=False))
-    _check_ls(hi_t, ys, high, eps2, idx[:64])
-    if phi:
-        rl, rh = O.zero_tree_phi_many(lo_t, hi_t, k1, w.k, ys[idx], rel_tol=W.REL_TOL, nthreads=8)
-    else:
-        rl, rh = O.zero_tree_many_arrays(lo_t, hi_t, w.fine_shape, w.factors, w.k, w.k, ys[idx],
-                                         rel_tol=W.REL_TOL, nthreads=8)
-    same1 = np.mean([np.array_equal(low["sel"][p], rl["sel"][i]) for i, p in enumerate(idx)])
-    assert same1 > 0.95
-    agree = np.mean([np.array_equal(high["sel"][p], rh["sel"][i]) for i, p in enumerate(idx)])
-    assert agree > 0.9
-
-
-@pytest.mark.parametrize("ci", [2, 3, 4])
-def test_full_omp_full_size_big(ci):
-    w = W.CONFIGS[ci]
-    d = W.dictionaries(ci)
-    P = BIG[ci]["p"] or w.signals
-    ys = _fast_signals(ci, P, 1)
-    hi_t = d.e_high_t if w.measurements else d.high_t
-    eps = W.REL_TOL * np.linalg.norm(ys, axis=1)
-    sol = _host(D.omp_batch_raw(D.device_dictionary(hi_t), ys.astype(np.float32), P, w.k, eps,
-                                None, "auto"))
-    assert np.array_equal(sol["scans"], _scan_formula(w.t_high, sol["counts"]))
-    _check_stop(sol, eps, w.k)
-    rng = np.random.default_rng(30 + ci)
-    idx = np.sort(rng.choice(P, size=BIG[ci]["sub_full"], replace=False))
-    _check_ls(hi_t, ys, sol, eps, idx)
-    ref = O.omp_many_arrays(hi_t, ys[idx], w.k, rel_tol=W.REL_TOL, nthreads=8)
-    got = {k: v[idx] for k, v in sol.items()}
-    got["flag"] = got["flag"].astype(bool)
-    rep = compare(ref, got, hi_t, ys[idx], eps[idx])
-    assert not rep["bad"], rep["bad"][:3]
+    P = 40_000
+    ys = W.signals(ci, 0, P).astype(np.float32)
+    lo, hi = D.device_dictionary(d.low_t), D.device_dictionary(d.high_t)
+    a_low, a_high = _outs(P, w.k), _outs(P, w.k)
+    D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, torch.from_numpy(ys).cuda(), P, w.k, w.k,
+                    W.REL_TOL, False, "auto", a_low, a_high)
+    b_low, b_high = _outs(P, w.k), _outs(P, w.k)
+    D.zero_tree_raw(lo, hi, w.fine_shape, w.factors, ys, P, w.k, w.k, W.REL_TOL, False, "auto",
+                    b_low, b_high)
+    for a, b in ((a_low, b_low), (a_high, b_high)):
+        for k in ("sel", "counts", "scans", "alpha", "rnorm"):
+            assert torch.equal(a[k], b[k]), k

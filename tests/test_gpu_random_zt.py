@@ -8,7 +8,7 @@ plus the nesting invariant (crossscale.py:224)."""
 import numpy as np
 import pytest
 
-from parity import compare
+from parity import check_zero_tree
 
 import oracle as O
 from paper_1511_05174_b200 import _native as N
@@ -56,26 +56,7 @@ def _signals(d_high, q, k, p, seed):
 
 
 def _check_zt(d_low_t, d_high_t, q, ys, low, high, rl, rh, k1, yl=None):
-    p = ys.shape[0]
-    eps1 = 1e-3 * np.linalg.norm(yl if yl is not None else ys, axis=1)
-    rep = compare(rl, low, d_low_t, yl if yl is not None else ys, eps1)
-    assert not rep["bad"], ("step1", rep["bad"][:3])
-    same = np.array([np.array_equal(low["sel"][i], rl["sel"][i]) for i in range(p)])
-    assert same.mean() > 0.9
-    idx = np.flatnonzero(same)
-    eps2 = 1e-3 * np.linalg.norm(ys, axis=1)
-    allowed = []
-    for i in idx:
-        c = int(rl["counts"][i])
-        b = np.sort(rl["sel"][i, :c])
-        allowed.append((b[:, None] * q + np.arange(q)[None, :]).ravel())
-    def sub(o):
-        return {k2: np.asarray(v)[idx] for k2, v in o.items() if np.ndim(v) >= 1 and len(v) == p}
-    rep = compare(sub(rh), sub(high), d_high_t, ys[idx], eps2[idx], allowed if idx.size else None)
-    assert not rep["bad"], ("step2", rep["bad"][:3])
-    for i in range(p):
-        parents = set(low["sel"][i, :int(low["counts"][i])].tolist())
-        assert all(int(j) // q in parents for j in high["sel"][i, :int(high["counts"][i])])
+    check_zero_tree(d_low_t, d_high_t, q, ys, low, high, rl, rh, yl)
 
 
 def _dev_outs(o):
