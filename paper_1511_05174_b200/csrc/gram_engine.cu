@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "engines.h"
+#include "sm100.cuh"
 
 namespace cdb {
 namespace {
@@ -65,6 +66,14 @@ __host__ __device__ inline int64_t gram_region_doubles(int64_t s, int64_t kw, in
 // cfg 4 step 2 (1M signals): 2 / 3 / 4 / 6 / 8 warps -> 1019 / 767 / 816 / 1169 /
 // 1365 ms; at 3, 444 slots x (64 - 18 smem rows) x 4 KB = 84 MB stay in L2.
 constexpr int kStreamWarpsPerSm = 3;
+// TMEM rows for the streamed H: at most 4 warps per CTA (one TMEM lane
+// quarter each).
+// Measured SLOWER than reading those rows from L2 (cfg 4, 1M: 1091 / 884 ms
+// at 3 / 4 warps vs 768 ms), so opt-in only: CDB_GRAM_TMEM=1.
+inline bool gram_stream_tmem(int wpb) {
+  const char *v = getenv("CDB_GRAM_TMEM");
+  return wpb <= 4 && v && atoi(v) != 0;
+}
 
 // alpha0_j = <d_{C_j}, y> for every candidate: the warp streams 8 atom rows
 // at a time with coalesced loads (lane i reads element i of each row) and
@@ -102,22 +111,68 @@ __device__ __forceinline__ const double *hrow(const double *hs, const double *hg
   return (i < nr ? hs : hg) + (int64_t)i * (32 * U);
 }
 
-template <int U>
-__device__ void back_substitute(const double *hs, const double *hg, int nr, int kd,
-                                const double *zv, const double *iv, const int *pj, double *xv,
-                                int lane) {
-  const double *h0 = hrow<U>(hs, hg, nr, lane);
-  const double *h1 = hrow<U>(hs, hg, nr, lane + 32);
+// TMEM rows (TMR): rows [nr, nr + ntr) live in the warp's TMEM lane quarter,
+// slot-major: candidate j = lane + 32 u, row nr + t at columns 32 u + 2 t
+// (lo, hi words).  A warp-wide load of the 32 columns of slot u gives every
+// lane its slot-u values of all TMEM rows; for the column R[., l] the owner
+// lane of pick l publishes its 16 values through `tcol` (shared memory).
+template <int U, bool TMR>
+__device__ void back_substitute(const double *hs, const double *hg, int nr, int ntr,
+                                uint32_t tbase, double *tcol, int kd, const double *zv,
+                                const double *iv, const int *pj, double *xv, int lane) {
+  const int i0 = lane, i1 = lane + 32;
+  const bool t0 = TMR && i0 >= nr && i0 < nr + ntr, t1 = TMR && i1 >= nr && i1 < nr + ntr;
+  const double *h0 = hrow<U>(hs, hg, nr, i0);
+  const double *h1 = hrow<U>(hs, hg, nr, i1);
   double acc0 = 0.0, acc1 = 0.0;
   for (int l = kd - 1; l >= 0; l--) {
     const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
     const double xl = (zv[l] - accl) * iv[l];
     if (lane == 0) xv[l] = xl;
     const int sl = hslot<U>(pj[l]);
-    if (lane < l) acc0 = fma(h0[sl], xl, acc0);
-    if (lane + 32 < l) acc1 = fma(h1[sl], xl, acc1);
+    double r0 = 0.0, r1 = 0.0;
+    if (TMR && l > nr) {  // some row i < l lives in TMEM
+      uint32_t v[32];
+      sm100::tmem_ld32u(tbase + 32u * (uint32_t)(pj[l] >> 5), v);
+      sm100::tmem_wait_ld();
+      if (lane == (pj[l] & 31)) {
+#pragma unroll
+        for (int t = 0; t < 16; t++) tcol[t] = __hiloint2double((int)v[2 * t + 1], (int)v[2 * t]);
+      }
+      __syncwarp();
+      if (t0) r0 = tcol[i0 - nr];
+      if (t1) r1 = tcol[i1 - nr];
+      __syncwarp();
+    }
+    if (lane < l) acc0 = fma(t0 ? r0 : h0[sl], xl, acc0);
+    if (lane + 32 < l) acc1 = fma(t1 ? r1 : h1[sl], xl, acc1);
   }
   __syncwarp();
+}
+
+// The TMEM rows' share of the H sweep: w_t = H[j*][nr + t] from the owner
+// lane's slot-ub columns, then hacc[u] -= sum_t w_t h_{nr+t}[lane + 32 u].
+template <int U>
+__device__ __forceinline__ void tm_sweep(uint32_t tbase, int tr, int ub, int owner,
+                                         double (&hacc)[U], double &ww) {
+  uint32_t v[32];
+  sm100::tmem_ld32u(tbase + 32u * (uint32_t)ub, v);
+  sm100::tmem_wait_ld();
+  double w[16];
+#pragma unroll
+  for (int t = 0; t < 16; t++) {
+    const double mine = __hiloint2double((int)v[2 * t + 1], (int)v[2 * t]);
+    w[t] = __shfl_sync(CDB_FULL_MASK, mine, owner);
+    if (t < tr) ww = fma(w[t], w[t], ww);
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    sm100::tmem_ld32u(tbase + 32u * (uint32_t)u, v);
+    sm100::tmem_wait_ld();
+#pragma unroll
+    for (int t = 0; t < 16; t++)
+      if (t < tr) hacc[u] = fma(-w[t], __hiloint2double((int)v[2 * t + 1], (int)v[2 * t]), hacc[u]);
+  }
 }
 
 // hacc -= sum_{i in [i0, i1)} w_i h_i, ww += |w|^2 over those rows (w_i = h_i[bs]).
@@ -161,10 +216,15 @@ __device__ __forceinline__ void h_sweep(const double *h, int i0, int i1, int bs,
 // sum_{i<nr} (k_max - i) of the sum_i (k_max - i) row reads) and the rest in
 // a per-warp global slot sized so that all slots stay L2-resident -- a
 // streamed H is then read from L2, not HBM.
-template <typename YT, int U, bool HSM>
+//
+// HM == 2 (TMR) adds 16 TMEM rows per warp between the shared-memory and the
+// global rows (each warp of the <= 4-warp CTA owns one TMEM lane quarter, 64 KB),
+// so fewer rows stream from L2.
+template <typename YT, int U, int HM>
 __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
     gram_omp_kernel(GramArgs a, const YT *__restrict__ ys, int h_rows_smem, int64_t smem_per_warp) {
   constexpr int HS = 32 * U;
+  constexpr bool HSM = HM == 1, TMR = HM == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -178,12 +238,27 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   int *pj = (int *)(iv + kw);        // candidate index of pick l
   int64_t *sup = (int64_t *)(iv + 2 * kw);
   double *xv = (double *)(sup + kw);
-  double *region = xv + kw + ((5 * kw) & 1);  // even offset: 16-byte H accesses
+  double *tcol = xv + kw;                     // TMR: one TMEM column, 16 doubles
+  double *region = tcol + (HSM ? 0 : 16) + ((5 * kw) & 1);  // even: 16-byte H accesses
   // HSM: H in shared memory, known at compile time so its accesses are LDS/STS
-  // rather than generic loads; else rows >= nr in this warp's global slot
+  // rather than generic loads; else rows >= nr (+ TMEM rows) in this warp's global slot
   const int nr = HSM ? kw : h_rows_smem;
+  const int ntr = TMR ? (kw - nr < 16 ? kw - nr : 16) : 0;
   double *hs = region;
-  double *hg = HSM ? region : a.hwork + gw * (int64_t)(kw - nr) * HS - (int64_t)nr * HS;
+  double *hg = HSM ? region
+                   : a.hwork + gw * (int64_t)(kw - nr - ntr) * HS - (int64_t)(nr + ntr) * HS;
+  __shared__ uint32_t tm_base_s;
+  uint32_t tbase = 0;
+  if (TMR) {
+    if (wib == 0) sm100::tmem_alloc(&tm_base_s, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    tbase = tm_base_s + ((uint32_t)(32 * (wib & 3)) << 16);
+#pragma unroll 1
+    for (int c = 0; c < 16; c++) sm100::tmem_st32_zero(tbase + 32u * c);  // finite unused rows
+    sm100::tmem_wait_st();
+  }
 
   for (int64_t local = gw; local < a.p; local += nwarps) {
   const int64_t p = a.p_offset + local;
@@ -280,6 +355,8 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       const double *grow = a.gram + (T * T < (int64_t(1) << 31)
                                          ? (int64_t)((uint32_t)nid * (uint32_t)T)
                                          : nid * T);
+      // (loading the slice into separate registers, added after the sweep,
+      // measured slower: 766 -> 802 ms per 1M on cfg 4)
       double hacc[U];
 #pragma unroll
       for (int u = 0; u < U; u++) hacc[u] = lane + 32 * u < S ? __ldg(grow + cid[u]) : 0.0;
@@ -290,7 +367,8 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
         h_sweep<U, 2>(hs, 0, k, bs, lane, hacc, ww);
       } else {
         h_sweep<U, 2>(hs, 0, k < nr ? k : nr, bs, lane, hacc, ww);
-        if (k > nr) h_sweep<U, 4>(hg, nr, k, bs, lane, hacc, ww);
+        if (TMR && k > nr) tm_sweep<U>(tbase, k - nr < ntr ? k - nr : ntr, ub, owner, hacc, ww);
+        if (k > nr + ntr) h_sweep<U, 4>(hg, nr + ntr, k, bs, lane, hacc, ww);
       }
       const double d2 = gnn - ww;
       if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
@@ -299,8 +377,18 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       }
       const double inv_d = rsqrt(d2);
       const double zk = cj * inv_d;  // q_k^T y = q_k^T r = <d_{j*}, r> / d
+      const bool in_tm = TMR && k >= nr && k < nr + ntr;
       double *hk = (HSM || k < nr ? hs : hg) + (int64_t)k * HS;
-      if (U == 1) {
+      if (in_tm) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const double hv = hacc[u] * inv_d;
+          sm100::tmem_st2(tbase + 32u * u + 2u * (uint32_t)(k - nr),
+                          (uint32_t)__double2loint(hv), (uint32_t)__double2hiint(hv));
+          cr[u] = fma(-zk, hv, cr[u]);
+        }
+        sm100::tmem_wait_st();
+      } else if (U == 1) {
         const double hv = hacc[0] * inv_d;
         hk[lane] = hv;
         cr[0] = fma(-zk, hv, cr[0]);
@@ -327,7 +415,7 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
       const double gap = rn2 - tol2;
       if (gap > band) continue;
       if (gap < -band) break;
-      back_substitute<U>(hs, hg, nr, kdone, zv, iv, pj, xv, lane);
+      back_substitute<U, TMR>(hs, hg, nr, ntr, tbase, tcol, kdone, zv, iv, pj, xv, lane);
       double rr = 0.0;
       for (int i = lane; i < n; i += 32) {
         double ri = (double)yg[i];
@@ -346,7 +434,7 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   }
   // ---- coefficients (pick order), exact final residual norm
   __syncwarp();
-  back_substitute<U>(hs, hg, nr, kdone, zv, iv, pj, xv, lane);
+  back_substitute<U, TMR>(hs, hg, nr, ntr, tbase, tcol, kdone, zv, iv, pj, xv, lane);
   if (kdone > 0) {
     // |r| = sqrt(|y|^2 - |z|^2) is accurate to ~1e-16 |y|^2 / |r|^2 relative;
     // re-materialise the residual exactly only when that is not tight
@@ -374,26 +462,33 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   }
   __syncwarp();  // the next signal re-stages the shared region
   }
+  if (TMR) {
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (wib == 0) sm100::tmem_dealloc(tm_base_s, 512);
+  }
 }
 
-template <typename YT, int U, bool HSM>
+template <typename YT, int U, int HM>
 cudaError_t launch_gram_tuh(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
                             int wpb, int64_t blocks, cudaStream_t stream) {
   const int64_t smem = per_warp * wpb;
-  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, U, HSM>,
+  cudaError_t e = cudaFuncSetAttribute(gram_omp_kernel<YT, U, HM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  gram_omp_kernel<YT, U, HSM><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
-                                                                            per_warp);
+  gram_omp_kernel<YT, U, HM><<<(unsigned)blocks, wpb * 32, smem, stream>>>(args, ys, h_in_smem,
+                                                                           per_warp);
   return cudaGetLastError();
 }
 
 template <typename YT, int U>
 cudaError_t launch_gram_tu(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
                            int wpb, int64_t blocks, cudaStream_t stream) {
-  return args.hwork == nullptr
-             ? launch_gram_tuh<YT, U, true>(args, ys, h_in_smem, per_warp, wpb, blocks, stream)
-             : launch_gram_tuh<YT, U, false>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+  if (args.hwork == nullptr)
+    return launch_gram_tuh<YT, U, 1>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+  if (gram_stream_tmem(wpb))
+    return launch_gram_tuh<YT, U, 2>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
+  return launch_gram_tuh<YT, U, 0>(args, ys, h_in_smem, per_warp, wpb, blocks, stream);
 }
 
 template <typename YT>
@@ -422,7 +517,7 @@ GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
   int wpb = kStreamWarpsPerSm;
   if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) > 0 ? atoi(v) : wpb;
   if (wpb > 32) wpb = 32;
-  const int64_t fixed = 8 * ((5 * kw + 1) & ~int64_t(1));
+  const int64_t fixed = 8 * ((5 * kw + 16 + 1) & ~int64_t(1));  // + the TMEM column scratch
   int64_t per_warp = ((int64_t)max_smem_per_block / wpb) & ~int64_t(15);
   // shared memory only holds whole H rows (plus the y / alpha0 staging if needed)
   int64_t region = per_warp - fixed;
@@ -436,7 +531,8 @@ GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
   pl.nr = (int)nr;
   pl.per_warp_smem = per_warp;
   pl.warps = (int64_t)num_sms * wpb;
-  pl.slot_doubles = (kw - nr) * hs;
+  const int64_t ntr = gram_stream_tmem(wpb) ? (kw - nr < 16 ? kw - nr : 16) : 0;
+  pl.slot_doubles = (kw - nr - ntr) * hs;
   return pl;
 }
 

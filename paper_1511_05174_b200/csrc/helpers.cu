@@ -43,33 +43,47 @@ __global__ void __launch_bounds__(256) downsample_kernel(const YT *__restrict__ 
     for (int d = 0; d < sh.rank; d++) idx = idx * (int)sh.fine[d] + cc[d] * (int)sh.fac[d] + off[d];
     tab[e] = idx;
   }
-  const int64_t s0 = (int64_t)blockIdx.x * spb;
-  const int ns = p - s0 < spb ? (int)(p - s0) : spb;
-  for (int64_t e = threadIdx.x; e < (int64_t)ns * n; e += blockDim.x) rows[e] = ys[s0 * n + e];
-  __syncthreads();
-  for (int e = threadIdx.x; e < ns * n_low; e += blockDim.x) {
-    const int sl = e / n_low, cell = e % n_low;
-    const YT *row = rows + (size_t)sl * n;
-    const int *t = tab + cell * block;
-    double acc = 0.0;
-    for (int b = 0; b < block; b++) acc += (double)row[t[b]];
-    out[(s0 + sl) * n_low + cell] = acc / (double)block;
-  }
-  if (!eps_low) return;
-  // fused stopping tolerances rel * |W y| (step 1) and rel * |y| (step 2)
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int sl = warp; sl < ns; sl += blockDim.x >> 5) {
-    const YT *row = rows + (size_t)sl * n;
-    double a = 0.0, b = 0.0;
-    for (int i = lane; i < n; i += 32) a = fma((double)row[i], (double)row[i], a);
-    const double *lo = out + (s0 + sl) * n_low;
-    for (int i = lane; i < n_low; i += 32) b = fma(lo[i], lo[i], b);
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (lane == 0) {
-      eps_fine[s0 + sl] = rel * sqrt(a);
-      eps_low[s0 + sl] = rel * sqrt(b);
+  // persistent CTAs: the index table is built once, then groups of spb
+  // signals are staged with 16-byte loads (rows are 16-byte aligned when
+  // n * sizeof(YT) is a multiple of 16)
+  const bool vec = ((size_t)n * sizeof(YT)) % 16 == 0;
+  constexpr int VE = 16 / sizeof(YT);
+  for (int64_t s0 = (int64_t)blockIdx.x * spb; s0 < p; s0 += (int64_t)gridDim.x * spb) {
+    const int ns = p - s0 < spb ? (int)(p - s0) : spb;
+    __syncthreads();  // the previous group's rows are consumed
+    if (vec) {
+      const int4 *src = (const int4 *)(ys + s0 * n);
+      int4 *dst = (int4 *)rows;
+      const int64_t nv = (int64_t)ns * n / VE;
+      for (int64_t e = threadIdx.x; e < nv; e += blockDim.x) dst[e] = __ldcs(src + e);
+    } else {
+      for (int64_t e = threadIdx.x; e < (int64_t)ns * n; e += blockDim.x) rows[e] = ys[s0 * n + e];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < ns * n_low; e += blockDim.x) {
+      const int sl = e / n_low, cell = e % n_low;
+      const YT *row = rows + (size_t)sl * n;
+      const int *t = tab + cell * block;
+      double acc = 0.0;
+      for (int b = 0; b < block; b++) acc += (double)row[t[b]];
+      out[(s0 + sl) * n_low + cell] = acc / (double)block;
+    }
+    if (!eps_low) continue;
+    // fused stopping tolerances rel * |W y| (step 1) and rel * |y| (step 2)
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int sl = warp; sl < ns; sl += blockDim.x >> 5) {
+      const YT *row = rows + (size_t)sl * n;
+      double a = 0.0, b = 0.0;
+      for (int i = lane; i < n; i += 32) a = fma((double)row[i], (double)row[i], a);
+      const double *lo = out + (s0 + sl) * n_low;
+      for (int i = lane; i < n_low; i += 32) b = fma(lo[i], lo[i], b);
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == 0) {
+        eps_fine[s0 + sl] = rel * sqrt(a);
+        eps_low[s0 + sl] = rel * sqrt(b);
+      }
     }
   }
 }
@@ -792,7 +806,12 @@ cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
   if (spb < 1) spb = 1;
   const size_t smem = (size_t)(n * 4 + 15) / 16 * 16 + (size_t)spb * n * esz;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  const unsigned g = (unsigned)((p + spb - 1) / spb);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = (int)((200 * 1024) / (smem + 1024)) < 8 ? (int)((200 * 1024) / (smem + 1024)) : 8;
+  const int64_t groups = (p + spb - 1) / spb;
+  const unsigned g = (unsigned)(groups < (int64_t)sms * per_sm ? groups : (int64_t)sms * per_sm);
   cudaError_t e;
   if (ys_f32) {
     e = cudaFuncSetAttribute(downsample_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,

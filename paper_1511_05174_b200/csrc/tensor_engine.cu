@@ -1059,6 +1059,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
 // the next scan operand is built by resid_split_kernel.
 __device__ __forceinline__ int64_t lpk(int l) { return (int64_t)l * (l + 1) / 2; }
 
+
 // 32 per-lane partials acc[m] (m = row within the block) -> lane l returns
 // the warp-wide sum of partial l.
 __device__ __forceinline__ double reduce_scatter32(double (&acc)[32], int lane) {
@@ -1075,8 +1076,8 @@ __device__ __forceinline__ double reduce_scatter32(double (&acc)[32], int lane) 
   return acc[0];
 }
 
-template <typename YT, int KR>
-__global__ void __launch_bounds__(128) ls_wide_kernel(
+template <typename YT, int KR, int MB>
+__global__ void __launch_bounds__(128, MB) ls_wide_kernel(
     const YT *__restrict__ ys, const double *__restrict__ d64, const double *__restrict__ gram,
     int64_t p, int64_t t, int n, int k_max, int kw, int iter, double c_err, double dmax,
     TensorState st, int64_t *out_sel, double *out_coef, int64_t *out_count, int64_t *out_scans,
@@ -1098,6 +1099,17 @@ __global__ void __launch_bounds__(128) ls_wide_kernel(
     double *xo = out_coef + sig * kw;
     double *lin = st.linv + sig * kp;
     const YT *y = ys + sig * (int64_t)n;
+    // the L^{-1} rows and the signal are needed only after the candidate
+    // loads and the re-scores: start pulling them into L1 now
+    {
+      const char *lb = (const char *)lin;
+      const int64_t lbytes = lpk(k) * 8;
+      for (int64_t o = (int64_t)lane * 128; o < lbytes; o += 32 * 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(lb + o));
+      const char *yb = (const char *)y;
+      for (int64_t o = (int64_t)lane * 128; o < (int64_t)n * (int64_t)sizeof(YT); o += 32 * 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(yb + o));
+    }
     int64_t sv[KR];
     double xv[KR];
 #pragma unroll
@@ -1115,7 +1127,7 @@ __global__ void __launch_bounds__(128) ls_wide_kernel(
     const double rn2_prev = st.rn2[sig], tol = st.tol[sig], yy = st.yy[sig];
     double best = -1.0, cbest = 0.0;
     int64_t bestj = -1;
-    double bg[KR];
+    double bg[KR], bgnn = 1.0;
 #pragma unroll
     for (int r = 0; r < KR; r++) bg[r] = 0.0;
     if (resume) {
@@ -1127,6 +1139,7 @@ __global__ void __launch_bounds__(128) ls_wide_kernel(
         const double *grow = gram + bestj * t;
 #pragma unroll
         for (int r = 0; r < KR; r++) bg[r] = sv[r] >= 0 ? __ldg(grow + sv[r]) : 0.0;
+        bgnn = __ldg(grow + bestj);
       }
     } else {
       // ---- candidates: drop taken atoms (support ids are spread over the lanes)
@@ -1164,6 +1177,7 @@ __global__ void __launch_bounds__(128) ls_wide_kernel(
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
         for (int r = 0; r < KR; r++) g[r] = sv[r] >= 0 ? __ldg(gj + sv[r]) : 0.0;
+        const double gjj = __ldg(gj + j);
         int i = lane;
         for (; i + 96 < n; i += 128) {
           const double e0 = __ldg(dj + i), e1 = __ldg(dj + i + 32), e2 = __ldg(dj + i + 64),
@@ -1183,6 +1197,7 @@ __global__ void __launch_bounds__(128) ls_wide_kernel(
           best = v;
           bestj = j;
           cbest = cj;
+          bgnn = gjj;
 #pragma unroll
           for (int r = 0; r < KR; r++) bg[r] = g[r];
         }
@@ -1232,7 +1247,7 @@ __global__ void __launch_bounds__(128) ls_wide_kernel(
     for (int b = 0; b < KR; b++)
       if (lane + 32 * b < k) ww = fma(w[b], w[b], ww);
     ww = warp_sum(ww);
-    const double gnn = __ldg(gram + bestj * t + bestj);
+    const double gnn = bgnn;
     const double d2 = gnn - ww;
     if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: the exact engine decides
       if (lane == 0) st.status[sig] |= ST_DELEGATE;
@@ -1412,6 +1427,153 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
       st.rq[sig] = sqrt(c) * (1.0 + 1e-12);
       st.rt[sig] = sqrt(a);
       st.dr[sig] = 0x1p-24 * b * dmax * 1.0000001;  // |(D64 - D32) x| bound
+      st.status[sig] &= ~ST_RESID;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ float4 ldg_nc_f4(const float4 *p) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// fp32 split-mode scan operand: the same r~ = y - D32_S x, accumulated in
+// fp32 with 16-byte loads (V float4 per thread per atom row, 8 rows in
+// flight), packed bf16 stores.  The scan's error budget charges the fp32
+// arithmetic exactly (dr below): with u = 2^-24 and g = (k+1) u / (1 - (k+1) u)
+// the FMA chain y32 - sum_l x32_l d32_l has |r~ - r| <= |y32 - y| +
+// sum_l |x32_l d32_l - x_l d_l| + g (|y32| + sum_l |x32_l| |d32_l|), so
+//   |r~ - r| <= (u + g (1 + u)) |y| + (2.0001 u + g (1 + u)^2) sum_l |x_l| dmax.
+// Needs n == 4 * BT * V.
+template <typename YT, int BT, int V>
+__global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys,
+                                                        const float *__restrict__ d32, int64_t p,
+                                                        int64_t n, int64_t n_pad, int64_t kw,
+                                                        double dmax, TensorState st,
+                                                        const int64_t *out_sel,
+                                                        const double *out_coef,
+                                                        const int64_t *out_count) {
+  extern __shared__ double xsm[];
+  float *xf = (float *)xsm;                         // kw fp32 coefficients
+  const float **rows = (const float **)(xsm + kw);  // kw row pointers
+  __shared__ double red[3][BT / 32];
+  __shared__ double sxs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t sig = blockIdx.x; sig < p; sig += gridDim.x) {
+    if (!(st.status[sig] & ST_RESID)) continue;  // uniform across the CTA
+    const int kd = (int)out_count[sig];
+    double sx = 0.0;
+    for (int l = tid; l < kd; l += BT) {
+      const double x = out_coef[sig * kw + l];
+      xf[l] = (float)x;
+      rows[l] = d32 + out_sel[sig * kw + l] * n;
+      sx += fabs(x);
+    }
+    sx = warp_sum(sx);
+    if (lane == 0) red[1][warp] = sx;
+    __syncthreads();
+    float4 acc[V];
+    const YT *y = ys + sig * n;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      const int64_t i = 4 * (tid + (int64_t)v * BT);
+      acc[v] = make_float4((float)y[i], (float)y[i + 1], (float)y[i + 2], (float)y[i + 3]);
+    }
+    // software-pipelined over groups of G rows: the next group's loads are
+    // issued before the current group's FMAs (G * V 16-byte loads in flight)
+    constexpr int G = 8;
+    int l = 0;
+    if (kd >= G) {
+      float4 cur[G][V];
+#pragma unroll
+      for (int q = 0; q < G; q++)
+#pragma unroll
+        for (int v = 0; v < V; v++) cur[q][v] = ldg_nc_f4((const float4 *)rows[q] + tid + v * BT);
+      for (; l + G - 1 < kd; l += G) {
+        float4 nxt[G][V];
+        const bool more = l + 2 * G - 1 < kd;
+        if (more) {
+#pragma unroll
+          for (int q = 0; q < G; q++)
+#pragma unroll
+            for (int v = 0; v < V; v++)
+              nxt[q][v] = ldg_nc_f4((const float4 *)rows[l + G + q] + tid + v * BT);
+        }
+#pragma unroll
+        for (int q = 0; q < G; q++) {
+          const float xl = -xf[l + q];
+#pragma unroll
+          for (int v = 0; v < V; v++) {
+            acc[v].x = fmaf(xl, cur[q][v].x, acc[v].x);
+            acc[v].y = fmaf(xl, cur[q][v].y, acc[v].y);
+            acc[v].z = fmaf(xl, cur[q][v].z, acc[v].z);
+            acc[v].w = fmaf(xl, cur[q][v].w, acc[v].w);
+          }
+        }
+        if (more) {
+#pragma unroll
+          for (int q = 0; q < G; q++)
+#pragma unroll
+            for (int v = 0; v < V; v++) cur[q][v] = nxt[q][v];
+        }
+      }
+    }
+    for (; l < kd; l++) {
+      const float xl = -xf[l];
+#pragma unroll
+      for (int v = 0; v < V; v++) {
+        const float4 t = __ldg((const float4 *)rows[l] + tid + v * BT);
+        acc[v].x = fmaf(xl, t.x, acc[v].x);
+        acc[v].y = fmaf(xl, t.y, acc[v].y);
+        acc[v].z = fmaf(xl, t.z, acc[v].z);
+        acc[v].w = fmaf(xl, t.w, acc[v].w);
+      }
+    }
+    float rr = 0.0f, q2 = 0.0f;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      const float e[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
+      __nv_bfloat16 b[4];
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        b[c] = __float2bfloat16_rn(e[c]);
+        const float d = __bfloat162float(b[c]) - e[c];  // exact in fp32
+        q2 = fmaf(d, d, q2);
+        rr = fmaf(e[c], e[c], rr);
+      }
+      __nv_bfloat162 lo, hi;
+      lo.x = b[0];
+      lo.y = b[1];
+      hi.x = b[2];
+      hi.y = b[3];
+      uint2 pk;
+      pk.x = *(uint32_t *)&lo;
+      pk.y = *(uint32_t *)&hi;
+      *(uint2 *)(st.r16 + sig * n_pad + 4 * (tid + (int64_t)v * BT)) = pk;
+    }
+    const double rrd = warp_sum((double)rr), q2d = warp_sum((double)q2);
+    if (lane == 0) {
+      red[0][warp] = rrd;
+      red[2][warp] = q2d;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0, c = 0.0;
+      for (int w = 0; w < BT / 32; w++) {
+        a += red[0][w];
+        b += red[1][w];
+        c += red[2][w];
+      }
+      // fp32 sums of n squares: relative error <= n u; margins 2^-10 cover n <= 2^14
+      st.rq[sig] = sqrt(c) * (1.0 + 0x1p-10);
+      st.rt[sig] = sqrt(a) * (1.0 + 0x1p-10);
+      const double u = 0x1p-24, g = (kd + 1) * u / (1.0 - (kd + 1) * u);
+      st.dr[sig] = (u + g * (1.0 + u)) * sqrt(st.yy[sig]) * 1.0000001 +
+                   (2.0001 * u + g * (1.0 + u) * (1.0 + u)) * b * dmax * 1.0000001;
       st.status[sig] &= ~ST_RESID;
     }
     __syncthreads();
@@ -2109,16 +2271,24 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       ProfScope _ps(resume ? "ls_resume" : "ls_step", stream);
       if (wide) {
         const unsigned grid = resume ? (unsigned)(a.num_sms * 8) : (unsigned)((p + 3) / 4);
+        // blocks per SM the register budget targets (CDB_LSW_MINB=4|5|6 for A/B)
+        // (cfg 4 step 1 per 1M: 4 / 5 / 6 -> 514 / 462 / 472 ms)
+        static const int lsw_mb = getenv("CDB_LSW_MINB") ? atoi(getenv("CDB_LSW_MINB")) : 5;
+#define CDB_WIDE_MB(YT_, KR_, MB_)                                                              \
+  e = launch_k(pdl, ls_wide_kernel<YT_, KR_, MB_>, grid, 128, 0, stream, (const YT_ *)a.ys,     \
+               a.d64, a.gram, p, t, (int)n, (int)a.k_max, (int)kw, it, c_err, a.dmax, st,       \
+               a.out_sel, a.out_coef, a.out_count, a.out_scans, resume);
 #define CDB_WIDE(YT_, KR_)                                                                      \
-  e = launch_k(pdl, ls_wide_kernel<YT_, KR_>, grid, 128, 0, stream, (const YT_ *)a.ys, a.d64,   \
-               a.gram, p, t, (int)n, (int)a.k_max, (int)kw, it, c_err, a.dmax, st, a.out_sel,   \
-               a.out_coef, a.out_count, a.out_scans, resume);
+  if (lsw_mb == 5) { CDB_WIDE_MB(YT_, KR_, 5) }                                                 \
+  else if (lsw_mb == 6) { CDB_WIDE_MB(YT_, KR_, 6) }                                            \
+  else { CDB_WIDE_MB(YT_, KR_, 4) }
         if (a.ys_f32) {
           if (wide_kr == 1) { CDB_WIDE(float, 1) } else if (wide_kr == 2) { CDB_WIDE(float, 2) } else { CDB_WIDE(float, 4) }
         } else {
           if (wide_kr == 1) { CDB_WIDE(double, 1) } else if (wide_kr == 2) { CDB_WIDE(double, 2) } else { CDB_WIDE(double, 4) }
         }
 #undef CDB_WIDE
+#undef CDB_WIDE_MB
       } else if (lsg_smem > 0) {
         const unsigned grid = resume ? (unsigned)(a.num_sms * 4) : lsg_grid;
         if (lsg_g == 8) {
@@ -2187,6 +2357,31 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       // threads per signal: N / 8 (8 elements each), 64..256
       const int bt = n >= 2048 ? 256 : (n >= 1024 ? 128 : 64);
       const unsigned g = (unsigned)(a.num_sms * (2048 / bt));
+      // fp32 vectorised operand build when n = 4 * BT * V (CDB_RESID_F32=0: fp64 kernel)
+      static const bool f32_ok = !(getenv("CDB_RESID_F32") && atoi(getenv("CDB_RESID_F32")) == 0);
+      const size_t xs32 = 16 * (size_t)kw;
+#define CDB_RESID32(BT_, V_)                                                                    \
+  if (a.ys_f32)                                                                                 \
+    resid_f32_kernel<float, BT_, V_><<<g, BT_, xs32, stream>>>(                                 \
+        (const float *)a.ys, a.d32, p, n, n_pad, kw, a.dmax, st, a.out_sel, a.out_coef,         \
+        a.out_count);                                                                           \
+  else                                                                                          \
+    resid_f32_kernel<double, BT_, V_><<<g, BT_, xs32, stream>>>(                                \
+        (const double *)a.ys, a.d32, p, n, n_pad, kw, a.dmax, st, a.out_sel, a.out_coef,        \
+        a.out_count);
+      bool done32 = false;
+      if (f32_ok) {
+        done32 = true;
+        // N = 4096 (cfg 4 full OMP) stays on the fp64 kernel: measured 1988 vs
+        // 6287 ms per 250 k signals (register-bound) and 37% more exact rescans
+        // from the looser fp32 bound
+        if (n == 4 * 64 * 2) { CDB_RESID32(64, 2) }
+        else if (n == 4 * 128 * 2) { CDB_RESID32(128, 2) }
+        else if (n == 4 * 64 * 1) { CDB_RESID32(64, 1) }
+        else done32 = false;
+      }
+#undef CDB_RESID32
+      if (!done32) {
 #define CDB_RESID(BT_)                                                                          \
   if (a.ys_f32)                                                                                 \
     resid_split_kernel<float, BT_><<<g, BT_, xs, stream>>>((const float *)a.ys, a.d32, p, n,    \
@@ -2202,6 +2397,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         CDB_RESID(128)
       } else {
         CDB_RESID(64)
+      }
       }
 #undef CDB_RESID
       note_launch();
