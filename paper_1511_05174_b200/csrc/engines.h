@@ -108,6 +108,8 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
 // global slot of slot_doubles (args.hwork = warps * slot_doubles doubles).
 struct GramStreamPlan {
   bool ok;
+  bool cta;   // CTA per signal (gram_cta_kernel): warps = CTAs, per_warp_smem = per CTA
+  int cpt;    // cta: candidates per thread
   int wpb, nr;
   int64_t per_warp_smem, warps, slot_doubles;
 };

@@ -66,6 +66,8 @@ __host__ __device__ inline int64_t gram_region_doubles(int64_t s, int64_t kw, in
 // cfg 4 step 2 (1M signals): 2 / 3 / 4 / 6 / 8 warps -> 1019 / 767 / 816 / 1169 /
 // 1365 ms; at 3, 444 slots x (64 - 18 smem rows) x 4 KB = 84 MB stay in L2.
 constexpr int kStreamWarpsPerSm = 3;
+// cfg 4 step 2 per 1M signals: 2 / 3 CTAs per SM -> 729 / 1002 ms (warp kernel: 767)
+constexpr int kStreamCtasPerSm = 2;
 // TMEM rows for the streamed H: at most 4 warps per CTA (one TMEM lane
 // quarter each).
 // Measured SLOWER than reading those rows from L2 (cfg 4, 1M: 1091 / 884 ms
@@ -469,6 +471,332 @@ __global__ void __launch_bounds__(U <= 8 ? 512 : 256)
   }
 }
 
+// ---------------------------------------------------------------- CTA per signal
+// Streamed H with a precomputed alpha0 (cfg 4's step 2: S = 512, K = 64): one
+// 128-thread CTA per signal, thread t owning the CPT contiguous candidates
+// [t CPT, t CPT + CPT).  Against the warp-per-signal kernel the per-iteration
+// chain (Gram row gather, H sweep) is spread over 4 warps: each row's sweep
+// is 2 x 16-byte loads per thread and 8 rows of the L2-resident part are in
+// flight per thread, at the cost of one CTA barrier per iteration (the
+// arg-max exchange, double-buffered by iteration parity; it also publishes
+// row k-1 of H to every thread).  Same arithmetic as gram_omp_kernel.
+// H rows [0, nr) in shared memory, the rest in the CTA's global slot.
+template <int CPT>
+__device__ void back_sub_rows(const double *hs, const double *hg, int nr, int stride, int kd,
+                              const double *zv, const double *iv, const int *pj, double *xv,
+                              int lane) {
+  const double *h0 = (lane < nr ? hs : hg) + (int64_t)lane * stride;
+  const double *h1 = (lane + 32 < nr ? hs : hg) + (int64_t)(lane + 32) * stride;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int l = kd - 1; l >= 0; l--) {
+    const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
+    const double xl = (zv[l] - accl) * iv[l];
+    if (lane == 0) xv[l] = xl;
+    const int sl = pj[l];
+    if (lane < l) acc0 = fma(h0[sl], xl, acc0);
+    if (lane + 32 < l) acc1 = fma(h1[sl], xl, acc1);
+  }
+  __syncwarp();
+}
+
+template <typename YT, int CPT>
+__global__ void __launch_bounds__(128) gram_cta_kernel(GramArgs a, const YT *__restrict__ ys,
+                                                        int nr) {
+  constexpr int NT = 128, NW = NT / 32;
+  constexpr int SP = NT * CPT;  // H row stride (doubles)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
+  const int64_t T = a.t;
+  const Cands cs = a.cands;
+  double *zv = (double *)smem_raw;
+  double *iv = zv + kw;
+  int64_t *sup = (int64_t *)(iv + kw);
+  double *xv = (double *)(sup + kw);
+  int *pj = (int *)(xv + kw);               // kw ints in kw doubles of space
+  double *xb = xv + 2 * kw;                 // exchange: [2][NW] x {|c|, c}
+  int64_t *xi = (int64_t *)(xb + 4 * NW);   // exchange: [2][NW] x {j, atom}
+  double *red = (double *)(xi + 4 * NW);    // NW partial sums + 2 flags
+  double *hs = red + NW + 2;
+  hs += ((uintptr_t)hs & 15) ? 1 : 0;       // 16-byte aligned rows
+  double *hg = a.hwork + (int64_t)blockIdx.x * (kw - nr) * SP - (int64_t)nr * SP;
+  const bool q8 = cs.mode == 2 && cs.q % CPT == 0;  // a thread's candidates are contiguous atoms
+
+  for (int64_t local = blockIdx.x; local < a.p; local += gridDim.x) {
+    const int64_t p = a.p_offset + local;
+    const YT *yg = ys + p * a.ys_stride;
+    const int S = (int)cs.count(p);
+    const int k_max = (int)cs.budget(p, a.k_max, n);
+    int cid[CPT];
+    unsigned tk = 0u;
+#pragma unroll
+    for (int c = 0; c < CPT; c++) {
+      const int j = tid * CPT + c;
+      cid[c] = j < S ? (int)cs.id(p, j) : 0;
+      if (j >= S) tk |= 1u << c;
+    }
+    double yy = 0.0;
+    for (int i = tid; i < n; i += NT) {
+      const double v = (double)yg[i];
+      yy = fma(v, v, yy);
+    }
+    yy = warp_sum(yy);
+    if (lane == 0) red[warp] = yy;
+    __syncthreads();
+    yy = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) yy += red[w];
+    const double ynorm = sqrt(yy);  // early exit |y| <= tol (_kernels.py:71-78)
+    const double tol = a.eps[p];
+    int kdone = 0;
+    int64_t scans = 0;
+    double rnorm = ynorm, rn2_final = 0.0;
+    bool delegate = false;
+    if (!(ynorm <= tol) && k_max > 0) {
+      double cr[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; c++) {
+        const int j = tid * CPT + c;
+        cr[c] = j < S ? a.alpha0_in[p * smax + j] : 0.0;
+      }
+      double rn2 = yy;
+      const double tol2 = tol * tol, band = 1e-12 * yy;
+      for (int k = 0; k < k_max; k++) {
+        rn2_final = rn2;
+        scans += S - k;
+        // ---- arg-max: thread, warp, then the 4 warps through shared memory
+        double best = -1.0;
+        int bc = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; c++) {
+          const double v = fabs(cr[c]);
+          if (!((tk >> c) & 1u) && v > best) {
+            best = v;
+            bc = c;
+          }
+        }
+        const unsigned bj = best >= 0.0 ? (unsigned)(tid * CPT + bc) : 0xffffffffu;
+        const double m = warp_max_nonneg(best);
+        const unsigned wj = __reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+        const int src = __ffs(__ballot_sync(CDB_FULL_MASK, bj == wj)) - 1;
+        double myc = 0.0;
+        int myid = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; c++)
+          if (c == bc) {
+            myc = cr[c];
+            myid = cid[c];
+          }
+        const double wc = __shfl_sync(CDB_FULL_MASK, myc, src < 0 ? 0 : src);
+        const int wid = __shfl_sync(CDB_FULL_MASK, myid, src < 0 ? 0 : src);
+        const int par = k & 1;
+        if (lane == 0) {
+          xb[(par * NW + warp) * 2] = m;
+          xb[(par * NW + warp) * 2 + 1] = wc;
+          xi[(par * NW + warp) * 2] = (int64_t)wj;
+          xi[(par * NW + warp) * 2 + 1] = wid;
+        }
+        __syncthreads();  // also publishes row k-1 of H
+        double gm = -1.0, cj = 0.0;
+        int64_t gj = 0xffffffffll, nid = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+          const double mw = xb[(par * NW + w) * 2];
+          const int64_t jw = xi[(par * NW + w) * 2];
+          if (mw > gm || (mw == gm && jw < gj)) {
+            gm = mw;
+            gj = jw;
+            cj = xb[(par * NW + w) * 2 + 1];
+            nid = xi[(par * NW + w) * 2 + 1];
+          }
+        }
+        if (!(gm > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
+        const int bestj = (int)gj;
+        if (tid == bestj / CPT) tk |= 1u << (bestj % CPT);
+        // ---- Gram row slice, H sweep
+        // the slice (an HBM gather) lands in its own registers and is added
+        // after the sweep, so its latency overlaps the sweep
+        const double *grow = a.gram + nid * T;
+        double gsl[CPT], hacc[CPT];
+        if (q8 && tid * CPT + CPT <= S) {
+          const double2 *g2 = (const double2 *)(grow + cid[0]);
+#pragma unroll
+          for (int c = 0; c < CPT / 2; c++) {
+            const double2 t2 = __ldg(g2 + c);
+            gsl[2 * c] = t2.x;
+            gsl[2 * c + 1] = t2.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPT; c++) gsl[c] = tid * CPT + c < S ? __ldg(grow + cid[c]) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; c++) hacc[c] = 0.0;
+        const double gnn = __ldg(grow + nid);
+        double ww = 0.0;
+        const int ks = k < nr ? k : nr;
+#pragma unroll 4
+        for (int i = 0; i < ks; i++) {
+          const double *hi = hs + i * SP;
+          const double wi = hi[bestj];
+          ww = fma(wi, wi, ww);
+#pragma unroll
+          for (int c = 0; c < CPT / 2; c++) {
+            const double2 t2 = *(const double2 *)(hi + tid * CPT + 2 * c);
+            hacc[2 * c] = fma(-wi, t2.x, hacc[2 * c]);
+            hacc[2 * c + 1] = fma(-wi, t2.y, hacc[2 * c + 1]);
+          }
+        }
+        // L2-resident rows in blocks of RB, software-pipelined: block b+1's
+        // 3 RB loads are issued before block b's FMAs (a plain unrolled loop
+        // with a runtime bound let ptxas serialise them: one row in flight)
+        constexpr int RB = 8;
+        int i = nr;
+        if (i + RB <= k) {
+          double wc[RB];
+          double2 hc[RB][CPT / 2];
+#pragma unroll
+          for (int q = 0; q < RB; q++) {
+            const double *hi = hg + (int64_t)(i + q) * SP;
+            wc[q] = hi[bestj];
+#pragma unroll
+            for (int c = 0; c < CPT / 2; c++) hc[q][c] = ((const double2 *)(hi + tid * CPT))[c];
+          }
+          for (; i + RB <= k; i += RB) {
+            double wn[RB];
+            double2 hn[RB][CPT / 2];
+            const bool more = i + 2 * RB <= k;
+            if (more) {
+#pragma unroll
+              for (int q = 0; q < RB; q++) {
+                const double *hi = hg + (int64_t)(i + RB + q) * SP;
+                wn[q] = hi[bestj];
+#pragma unroll
+                for (int c = 0; c < CPT / 2; c++) hn[q][c] = ((const double2 *)(hi + tid * CPT))[c];
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+              ww = fma(wc[q], wc[q], ww);
+#pragma unroll
+              for (int c = 0; c < CPT / 2; c++) {
+                hacc[2 * c] = fma(-wc[q], hc[q][c].x, hacc[2 * c]);
+                hacc[2 * c + 1] = fma(-wc[q], hc[q][c].y, hacc[2 * c + 1]);
+              }
+            }
+            if (more) {
+#pragma unroll
+              for (int q = 0; q < RB; q++) {
+                wc[q] = wn[q];
+#pragma unroll
+                for (int c = 0; c < CPT / 2; c++) hc[q][c] = hn[q][c];
+              }
+            }
+          }
+        }
+        for (; i < k; i++) {
+          const double *hi = hg + (int64_t)i * SP;
+          const double wi = hi[bestj];
+          ww = fma(wi, wi, ww);
+#pragma unroll
+          for (int c = 0; c < CPT / 2; c++) {
+            const double2 t2 = ((const double2 *)(hi + tid * CPT))[c];
+            hacc[2 * c] = fma(-wi, t2.x, hacc[2 * c]);
+            hacc[2 * c + 1] = fma(-wi, t2.y, hacc[2 * c + 1]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; c++) hacc[c] += gsl[c];
+        const double d2 = gnn - ww;  // identical in every thread (same w_i, same order)
+        if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
+          delegate = true;
+          break;
+        }
+        const double inv_d = rsqrt(d2);
+        const double zk = cj * inv_d;
+        double *hk = (k < nr ? hs : hg) + (int64_t)k * SP + tid * CPT;
+#pragma unroll
+        for (int c = 0; c < CPT / 2; c++) {
+          const double h0 = hacc[2 * c] * inv_d, h1 = hacc[2 * c + 1] * inv_d;
+          *(double2 *)(hk + 2 * c) = make_double2(h0, h1);
+          cr[2 * c] = fma(-zk, h0, cr[2 * c]);
+          cr[2 * c + 1] = fma(-zk, h1, cr[2 * c + 1]);
+        }
+        if (tid == 0) {
+          zv[k] = zk;
+          iv[k] = inv_d;
+          pj[k] = bestj;
+          sup[k] = nid;
+        }
+        rn2 -= zk * zk;
+        rn2_final = rn2;
+        kdone = k + 1;
+        // ---- stop test (_kernels.py:156), exact residual inside the band
+        const double gap = rn2 - tol2;
+        if (gap > band) continue;
+        if (gap < -band) break;
+        __syncthreads();  // row k and the pick in place
+        if (warp == 0) {
+          back_sub_rows<CPT>(hs, hg, nr, SP, kdone, zv, iv, pj, xv, lane);
+          double rr = 0.0;
+          for (int i = lane; i < n; i += 32) {
+            double ri = (double)yg[i];
+            for (int l = 0; l < kdone; l++) ri = fma(-xv[l], a.d64[sup[l] * n + i], ri);
+            rr = fma(ri, ri, rr);
+          }
+          rr = warp_sum(rr);
+          if (lane == 0) red[NW] = sqrt(rr) <= tol ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        if (red[NW] != 0.0) break;
+      }
+    }
+    __syncthreads();  // H, z, picks complete
+    if (delegate) {
+      if (tid == 0) a.status[p] |= ST_DELEGATE;
+    } else if (warp == 0) {
+      back_sub_rows<CPT>(hs, hg, nr, SP, kdone, zv, iv, pj, xv, lane);
+      if (kdone > 0) {
+        if (rn2_final > 1e-6 * yy) {
+          rnorm = sqrt(rn2_final);
+        } else {
+          double rr = 0.0;
+          for (int i = lane; i < n; i += 32) {
+            double ri = (double)yg[i];
+            for (int l = 0; l < kdone; l++) ri = fma(-xv[l], __ldg(a.d64 + sup[l] * n + i), ri);
+            rr = fma(ri, ri, rr);
+          }
+          rnorm = sqrt(warp_sum(rr));
+        }
+      }
+      int64_t *out_sel = a.out_sel + p * kw;
+      double *out_coef = a.out_coef + p * kw;
+      for (int j = lane; j < kw; j += 32) {
+        out_sel[j] = j < kdone ? sup[j] : -1;
+        out_coef[j] = j < kdone ? xv[j] : 0.0;
+      }
+      if (lane == 0) {
+        a.out_count[p] = kdone;
+        a.out_rnorm[p] = rnorm;
+        a.out_scans[p] = scans;
+        a.out_flag[p] = 0;
+      }
+    }
+    __syncthreads();  // the next signal reuses the shared state
+  }
+}
+
+template <typename YT, int CPT>
+cudaError_t go_cta(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
+                   cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(gram_cta_kernel<YT, CPT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pl.per_warp_smem);
+  if (e != cudaSuccess) return e;
+  gram_cta_kernel<YT, CPT><<<(unsigned)pl.warps, 128, pl.per_warp_smem, stream>>>(args, ys, pl.nr);
+  return cudaGetLastError();
+}
+
 template <typename YT, int U, int HM>
 cudaError_t launch_gram_tuh(const GramArgs &args, const YT *ys, int h_in_smem, int64_t per_warp,
                             int wpb, int64_t blocks, cudaStream_t stream) {
@@ -513,6 +841,29 @@ int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_
 GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
                                 int max_smem_per_block, int num_sms) {
   GramStreamPlan pl{};
+  const char *cv = getenv("CDB_GRAM_CTA");
+  if (!stage_y && s <= 512 && kw <= 64 && !(cv && atoi(cv) == 0)) {
+    // CTA per signal (gram_cta_kernel): cps CTAs per SM share its shared memory
+    int cps = kStreamCtasPerSm;
+    if (const char *v = getenv("CDB_GRAM_CPS")) cps = atoi(v) > 0 ? atoi(v) : cps;
+    const int cpt = s <= 256 ? 2 : 4;
+    const int64_t sp = 128 * cpt;
+    const int64_t fixed = 8 * (5 * kw + 9 * 4 + 2 + 2);
+    int64_t per_cta = (int64_t)(228 * 1024) / cps - 1024;
+    if (per_cta > max_smem_per_block) per_cta = max_smem_per_block;
+    int64_t nr = (per_cta - fixed) / (8 * sp);
+    if (nr > kw) nr = kw;
+    if (nr < 0) nr = 0;
+    pl.ok = per_cta > fixed;
+    pl.cta = true;
+    pl.cpt = cpt;
+    pl.wpb = 4;
+    pl.nr = (int)nr;
+    pl.per_warp_smem = (fixed + 8 * nr * sp + 15) & ~int64_t(15);  // per CTA
+    pl.warps = (int64_t)num_sms * cps;                                // CTAs
+    pl.slot_doubles = (kw - nr) * sp;
+    return pl;
+  }
   const int64_t hs = gram_hs(s);
   int wpb = kStreamWarpsPerSm;
   if (const char *v = getenv("CDB_GRAM_WPB")) wpb = atoi(v) > 0 ? atoi(v) : wpb;
@@ -553,6 +904,14 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
     const GramStreamPlan pl = gram_stream_plan(s, kw, n, args.alpha0_in == nullptr,
                                                max_smem_per_block, num_sms);
     if (!pl.ok) return cudaErrorInvalidValue;
+    if (pl.cta) {  // CTA per signal
+      note_launch();
+      if (ys_f32)
+        return pl.cpt == 2 ? go_cta<float, 2>(args, (const float *)ys, pl, stream)
+                           : go_cta<float, 4>(args, (const float *)ys, pl, stream);
+      return pl.cpt == 2 ? go_cta<double, 2>(args, (const double *)ys, pl, stream)
+                         : go_cta<double, 4>(args, (const double *)ys, pl, stream);
+    }
     const int u = (int)(gram_hs(s) / 32);
     note_launch();
     if (ys_f32)

@@ -1,1 +1,2 @@
-for cfg in ${CFGS:-"3 1" "3 0" "4 1"}; do set -- $cfg; echo "WPB=$1 TMEM=$2"; CDB_GRAM_WPB=$1 CDB_GRAM_TMEM=$2 python tools/probe_big.py 4 1000000 zt 1 2>&1 | tail -1 | grep -o "gram_step2[^)]*)"; done
+# step-2 Gram kernel variants on cfg 4 (1M signals), 2 runs each
+for v in ${VARIANTS:-"CDB_GRAM_CPS=2" "CDB_GRAM_CPS=3" "CDB_GRAM_CTA=0"}; do echo "$v"; env $v python tools/probe_big.py 4 1000000 zt 2 2>&1 | tail -2 | grep -o "gram_step2[^)]*)"; done
