@@ -88,6 +88,92 @@ __global__ void __launch_bounds__(256) downsample_kernel(const YT *__restrict__ 
   }
 }
 
+// Direct block means (no staging): one thread per coarse cell reads its
+// `block` fine entries straight from HBM (each fine entry is read exactly once
+// over the CTA, so the sectors are fully used) and the fine / coarse squared
+// norms are reduced per signal in a fixed order (deterministic tolerances).
+// spi = 256 / n_low signals per CTA pass when n_low < 256, else one signal
+// with n_low / 256 cells per thread.
+template <typename YT, int VW>
+__global__ void __launch_bounds__(256) downsample_direct_kernel(
+    const YT *__restrict__ ys, int64_t p, int n, int n_low, int block,
+    const int *__restrict__ tab_g, double *__restrict__ out, double rel,
+    double *__restrict__ eps_low, double *__restrict__ eps_fine) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  int *tab = (int *)dsm;  // n_low * block fine indices
+  __shared__ double r_yy[256], r_yl[256];
+  for (int e = threadIdx.x; e < n_low * block; e += blockDim.x) tab[e] = tab_g[e];
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const int spi = n_low < 256 ? 256 / n_low : 1;
+  const int tps = n_low < 256 ? n_low : 256;  // threads per signal
+  const double inv_b = 1.0 / (double)block;
+  for (int64_t s0 = (int64_t)blockIdx.x * spi; s0 < p; s0 += (int64_t)gridDim.x * spi) {
+    double yy = 0.0, yl = 0.0;
+    const int sl = tid / tps;
+    const int64_t sig = s0 + sl;
+    if (sl < spi && sig < p) {
+      const YT *y = ys + sig * n;
+      for (int cell = tid % tps; cell < n_low; cell += tps) {
+        const int *t = tab + cell * block;
+        double acc = 0.0;
+        if constexpr (VW == 2) {  // the last axis' factor-2 pairs are adjacent: 8-byte loads
+          for (int b = 0; b < block; b += 2) {
+            const float2 v2 = __ldcs((const float2 *)(y + t[b]));
+            const double v0 = (double)v2.x, v1 = (double)v2.y;
+            acc += v0;
+            acc += v1;
+            yy = fma(v0, v0, yy);
+            yy = fma(v1, v1, yy);
+          }
+        } else {
+          for (int b = 0; b < block; b++) {
+            const double v = (double)__ldcs(y + t[b]);
+            acc += v;
+            yy = fma(v, v, yy);
+          }
+        }
+        const double m = acc * inv_b;
+        out[sig * n_low + cell] = m;
+        yl = fma(m, m, yl);
+      }
+    }
+    if (!eps_low) continue;
+    r_yy[tid] = yy;
+    r_yl[tid] = yl;
+    __syncthreads();
+    if (tid < spi && s0 + tid < p) {
+      double a = 0.0, b = 0.0;
+      for (int q = tid * tps; q < (tid + 1) * tps; q++) {
+        a += r_yy[q];
+        b += r_yl[q];
+      }
+      eps_fine[s0 + tid] = rel * sqrt(a);
+      eps_low[s0 + tid] = rel * sqrt(b);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void downsample_table_kernel(Shape4 sh, int n_low, int *__restrict__ tab) {
+  int block = 1;
+  for (int d = 0; d < sh.rank; d++) block *= (int)sh.fac[d];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_low * block; e += gridDim.x * blockDim.x) {
+    const int cell = e / block, bo = e % block;
+    int cc[4] = {0, 0, 0, 0}, off[4] = {0, 0, 0, 0};
+    int rem = cell, r = bo;
+    for (int d = sh.rank - 1; d >= 0; d--) {
+      cc[d] = rem % (int)sh.coarse[d];
+      rem /= (int)sh.coarse[d];
+      off[d] = r % (int)sh.fac[d];
+      r /= (int)sh.fac[d];
+    }
+    int idx = 0;
+    for (int d = 0; d < sh.rank; d++) idx = idx * (int)sh.fine[d] + cc[d] * (int)sh.fac[d] + off[d];
+    tab[e] = idx;
+  }
+}
+
 // eps_p = rel * ||y_p|| (pursuit.py:437), one warp per signal.
 template <typename YT>
 __global__ void row_tol_kernel(const YT *__restrict__ ys, int64_t p, int64_t n, double rel,
@@ -800,6 +886,38 @@ cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
     sh.fine[d] = fine_shape[d];
     sh.fac[d] = factors[d];
     sh.coarse[d] = fine_shape[d] / factors[d];
+  }
+  int block = 1;
+  for (int d = 0; d < rank; d++) block *= (int)factors[d];
+  static const bool direct = !(getenv("CDB_DOWNSAMPLE_STAGED") && atoi(getenv("CDB_DOWNSAMPLE_STAGED")));
+  if (direct && n_low * block <= 48 * 1024 / 4) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int *tab = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&tab, sizeof(int) * n_low * block, stream);
+    if (e != cudaSuccess) return e;
+    downsample_table_kernel<<<(unsigned)((n_low * block + 255) / 256), 256, 0, stream>>>(sh, (int)n_low, tab);
+    const int spi = n_low < 256 ? (int)(256 / n_low) : 1;
+    const int64_t groups = (p + spi - 1) / spi;
+    const unsigned g = (unsigned)(groups < (int64_t)sms * 8 ? groups : (int64_t)sms * 8);
+    const size_t smem = sizeof(int) * n_low * block;
+    // fp32 rows with a last-axis factor of 2 (every BASELINE config): pair loads
+    const bool pairs = ys_f32 && factors[rank - 1] == 2 && fine_shape[rank - 1] % 2 == 0;
+    if (pairs)
+      downsample_direct_kernel<float, 2><<<g, 256, smem, stream>>>(
+          (const float *)ys, p, (int)n, (int)n_low, block, tab, y_low, rel, eps_low, eps_fine);
+    else if (ys_f32)
+      downsample_direct_kernel<float, 1><<<g, 256, smem, stream>>>(
+          (const float *)ys, p, (int)n, (int)n_low, block, tab, y_low, rel, eps_low, eps_fine);
+    else
+      downsample_direct_kernel<double, 1><<<g, 256, smem, stream>>>(
+          (const double *)ys, p, (int)n, (int)n_low, block, tab, y_low, rel, eps_low, eps_fine);
+    note_launch();
+    note_launch();
+    e = cudaGetLastError();
+    cudaFreeAsync(tab, stream);
+    return e;
   }
   const int64_t esz = ys_f32 ? 4 : 8;
   int spb = (int)(32768 / (n * esz));

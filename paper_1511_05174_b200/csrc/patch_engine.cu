@@ -63,26 +63,42 @@ __global__ void __launch_bounds__(256) extract_rows_kernel(const ST *__restrict_
   extern __shared__ double xs[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = (int)g.n;
-  int *offs = (int *)(xs + 8 * n);  // n cell offsets (signal size < 2^31)
+  const int nwarps = blockDim.x >> 5;
+  int *offs = (int *)(xs + (size_t)nwarps * (remove_dc ? 33 : 1) * n);  // n cell offsets
   for (int e = threadIdx.x; e < n; e += blockDim.x) offs[e] = (int)elem_offset(g, e);
   __syncthreads();
-  double *buf = xs + wib * n;
+  double *buf = xs + (size_t)wib * (remove_dc ? 33 : 1) * n;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < g.p; p += nw) {
-    const ST *src = sig + origin_offset(g, p);
-    double *dst = rows + p * n;
-    if (!remove_dc) {
+  if (!remove_dc) {
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < g.p; p += nw) {
+      const ST *src = sig + origin_offset(g, p);
+      double *dst = rows + p * n;
       for (int e = lane; e < n; e += 32) dst[e] = (double)src[offs[e]];
-      continue;
     }
-    for (int e = lane; e < n; e += 32) buf[e] = (double)src[offs[e]];
+    return;
+  }
+  // remove_dc: the mean of each patch is numpy's sequential axis-0 sum, so
+  // a warp takes 32 patches at a time, stages them as buf[e][q] (row stride
+  // 33: few bank conflicts), and lane q sums patch q in element order -- 32
+  // sequential sums in parallel -- before the rows go out coalesced.
+  const int64_t nw32 = nw * 32;
+  for (int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * 32; p0 < g.p; p0 += nw32) {
+    const int np = g.p - p0 < 32 ? (int)(g.p - p0) : 32;
+    for (int q = 0; q < np; q++) {
+      const ST *src = sig + origin_offset(g, p0 + q);
+      for (int e = lane; e < n; e += 32) buf[e * 33 + q] = (double)src[offs[e]];
+    }
     __syncwarp();
     double s = 0.0;
-    if (lane == 0)
-      for (int e = 0; e < n; e++) s += buf[e];  // numpy's axis-0 order
-    const double mean = __shfl_sync(CDB_FULL_MASK, s, 0) / (double)n;
-    if (lane == 0) dc[p] = mean;
-    for (int e = lane; e < n; e += 32) dst[e] = buf[e] - mean;
+    if (lane < np)
+      for (int e = 0; e < n; e++) s += buf[e * 33 + lane];  // numpy's axis-0 order
+    const double mean = s / (double)n;
+    if (lane < np) dc[p0 + lane] = mean;
+    for (int q = 0; q < np; q++) {
+      const double mq = __shfl_sync(CDB_FULL_MASK, mean, q);
+      double *dst = rows + (p0 + q) * n;
+      for (int e = lane; e < n; e += 32) dst[e] = buf[e * 33 + q] - mq;
+    }
     __syncwarp();
   }
 }
@@ -198,9 +214,14 @@ cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const
   Geom g;
   cudaError_t e = make_geom(g, rank, sig, pat, str);
   if (e != cudaSuccess) return e;
-  const size_t smem = 8 * sizeof(double) * (size_t)g.n + sizeof(int) * (size_t)g.n;  // 8 warps
+  // 8 warps; remove_dc stages 32 patches per warp
+  const size_t per_warp = (remove_dc ? 33 : 1) * sizeof(double) * (size_t)g.n;
+  int warps = 8;
+  while (warps > 1 && warps * per_warp + sizeof(int) * (size_t)g.n > 200 * 1024) warps /= 2;
+  const size_t smem = warps * per_warp + sizeof(int) * (size_t)g.n;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  int64_t blocks = (g.p + 7) / 8;
+  const int64_t per_block = (int64_t)warps * (remove_dc ? 32 : 1);
+  int64_t blocks = (g.p + per_block - 1) / per_block;
   if (blocks > (int64_t)num_sms * 32) blocks = (int64_t)num_sms * 32;
   if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   auto kf = extract_rows_kernel<float>;
@@ -210,9 +231,9 @@ cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const
       cudaSuccess)
     return e;
   if (f32)
-    kf<<<(unsigned)blocks, 256, smem, stream>>>((const float *)signal, g, remove_dc, rows, dc);
+    kf<<<(unsigned)blocks, 32 * warps, smem, stream>>>((const float *)signal, g, remove_dc, rows, dc);
   else
-    kd<<<(unsigned)blocks, 256, smem, stream>>>((const double *)signal, g, remove_dc, rows, dc);
+    kd<<<(unsigned)blocks, 32 * warps, smem, stream>>>((const double *)signal, g, remove_dc, rows, dc);
   note_launch();
   return cudaGetLastError();
 }
