@@ -109,6 +109,7 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
 struct GramStreamPlan {
   bool ok;
   bool cta;   // CTA per signal (gram_cta_kernel): warps = CTAs, per_warp_smem = per CTA
+  bool reg;   // H on chip (gram_reg_kernel, cta too): nr = register rows
   int cpt;    // cta: candidates per thread
   int wpb, nr;
   int64_t per_warp_smem, warps, slot_doubles;

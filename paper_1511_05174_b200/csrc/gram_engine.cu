@@ -786,6 +786,342 @@ __global__ void __launch_bounds__(128) gram_cta_kernel(GramArgs a, const YT *__r
   }
 }
 
+// ---------------------------------------------------------------- on-chip H
+// cfg 4's step 2 (S = 512, K = 64: 256 KB of fp64 H per signal) with the whole
+// H on chip: one 512-thread CTA per SM codes one signal at a time, thread t
+// owning candidate t and its H column -- rows [0, R) in registers (the oldest
+// rows, which take most of the sum_i (k_max - i) row reads), rows [R, kw) in
+// shared memory, private to the thread (no bank conflicts, no barriers).  The
+// streamed kernels above re-read those rows from L2 and, at 1M signals, from
+// HBM (ncu: 0.5 MB of DRAM reads per signal); here the per-iteration H traffic
+// is register and shared-memory bandwidth only, and the one remaining global
+// access is the Gram row slice G[j*, C] (one 8-byte load per thread).
+//
+// Per iteration: warp arg-max (redux) -> each warp's winner publishes
+// {|c|, c, d^2, G_jj, index, atom} and its H column w into a per-warp slot
+// (double-buffered by iteration parity) -> one CTA barrier -> every thread
+// picks the global winner from the 16 slots (strict '>' in warp order: the
+// lowest index wins ties) and issues its Gram load -> sweep
+// h_k = (G[j*, t] - sum_i w_i h_i[t]) / d, c_t -= z_k h_k.  d^2 = G_jj - |w|^2
+// uses s_t = sum_i h_i[t]^2, kept incrementally by the owner in the order the
+// other Gram kernels sum |w|^2.  The winner also files its column as column k
+// of R (R[i][k] = h_i[j*]) for the back-substitution R x = z
+// (_kernels.py:159-164).
+// Register rows are filled 8 at a time: row k < R is written to a per-thread
+// staging slot (shared memory) and, when its block of 8 is complete, the 8
+// staged rows move into hr[8 b, 8 b + 8) under a warp-uniform switch -- every
+// register index stays static (a dynamic hr[k] write costs R selects).
+template <int R>
+__device__ __forceinline__ void load_block(double (&hr)[R], int b, const double *st) {
+#pragma unroll
+  for (int bb = 0; bb < R / 8; bb++) {
+    if (bb == b) {
+#pragma unroll
+      for (int u = 0; u < 8; u++) hr[8 * bb + u] = st[u * 512];
+    }
+  }
+}
+
+// dst[i] = src[(i - r0) * 512] for i in [r0, k): a thread's shared-memory H
+// rows, four loads in flight before the stores.
+__device__ __forceinline__ void copy_col(double *dst, const double *src, int r0, int k) {
+  int i = r0;
+  for (; i + 3 < k; i += 4) {
+    const double v0 = src[(int64_t)(i - r0) * 512], v1 = src[(int64_t)(i + 1 - r0) * 512];
+    const double v2 = src[(int64_t)(i + 2 - r0) * 512], v3 = src[(int64_t)(i + 3 - r0) * 512];
+    dst[i] = v0;
+    dst[i + 1] = v1;
+    dst[i + 2] = v2;
+    dst[i + 3] = v3;
+  }
+  for (; i < k; i++) dst[i] = src[(int64_t)(i - r0) * 512];
+}
+
+// The full register blocks of a thread's H column (rows [0, kb)) -> dst.
+template <int R>
+__device__ __forceinline__ void put_regs(double *dst, const double (&hr)[R], int kb) {
+#pragma unroll
+  for (int b = 0; b < R / 8; b++) {
+    if (8 * b + 8 <= kb) {
+#pragma unroll
+      for (int u = 0; u < 8; u += 2)
+        *(double2 *)(dst + 8 * b + u) = make_double2(hr[8 * b + u], hr[8 * b + u + 1]);
+    }
+  }
+}
+
+// Column l of R (R[i][l] = h_i[p_l], i < l) filed by the thread that owns
+// pick l, once per signal: register rows, staged rows of the open block,
+// shared-memory rows (all immutable once written).
+template <int R>
+__device__ __forceinline__ void file_col(double *rm, int kw, int l, const double (&hr)[R],
+                                         const double *stg, const double *hsm, int kdone) {
+  if (l < 0) return;
+  double *col = rm + (int64_t)l * kw;
+  const int kr = kdone < R ? kdone : R, kb = kr & ~7;
+#pragma unroll
+  for (int i = 0; i < R; i++)
+    if (i < l && i < kb) col[i] = hr[i];
+  for (int i = kb; i < l && i < kr; i++) col[i] = stg[(i & 7) * 512];
+  if (l > R) copy_col(col, hsm, R, l);
+}
+
+// Back-substitution R x = z (_kernels.py:159-164) with column l of R at
+// rm + l kw; lane i (and i + 32) accumulates sum_{l > i} R[i][l] x_l -- the
+// order of back_sub_rows.
+__device__ __forceinline__ void back_sub_cols(const double *rm, int kw, int kd, const double *zv,
+                                              const double *iv, double *xv, int lane) {
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int l = kd - 1; l >= 0; l--) {
+    const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
+    const double xl = (zv[l] - accl) * iv[l];
+    if (lane == 0) xv[l] = xl;
+    const double *col = rm + (int64_t)l * kw;
+    if (lane < l) acc0 = fma(col[lane], xl, acc0);
+    if (lane + 32 < l) acc1 = fma(col[lane + 32], xl, acc1);
+  }
+  __syncwarp();
+}
+
+template <typename YT, int R>
+__global__ void __launch_bounds__(512, 1) gram_reg_kernel(GramArgs a, const YT *__restrict__ ys) {
+  constexpr int NT = 512, NW = NT / 32;
+  static_assert(R % 8 == 0, "register rows come in blocks of 8");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
+  const int64_t T = a.t;
+  const Cands cs = a.cands;
+  const int nsr = kw > R ? kw - R : 0;             // shared-memory rows
+  constexpr int SL = 6 + R;                         // slot: 6 header doubles + register rows of w
+  double *hsm = (double *)smem_raw;                 // nsr x NT, column t private to thread t
+  // staging rows of the open register block: the first 8 shared-memory rows,
+  // unused while k < R (R is a multiple of 8, the last block moves at k = R - 1)
+  double *stg = hsm;
+  double *slots = hsm + (int64_t)(nsr > 8 ? nsr : 8) * NT;  // [2][NW][SL]
+  double *rm = a.hwork + (int64_t)blockIdx.x * kw * kw;  // kw x kw (global): column l of R at rm + l kw
+  double *zv = slots + 2 * NW * SL;
+  double *iv = zv + kw;
+  double *xv = iv + kw;
+  int64_t *sup = (int64_t *)(xv + kw);
+  double *red = (double *)(sup + kw);               // NW
+  auto cta_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    __syncthreads();  // red reuse
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) s += red[w];
+    return s;
+  };
+
+  for (int64_t local = blockIdx.x; local < a.p; local += gridDim.x) {
+    const int64_t p = a.p_offset + local;
+    const YT *yg = ys + p * a.ys_stride;
+    const int S = (int)cs.count(p);
+    const int k_max = (int)cs.budget(p, a.k_max, n);
+    const bool valid = t < S;
+    const int64_t cid = valid ? cs.id(p, t) : 0;
+    double yy = 0.0;
+    for (int i = t; i < n; i += NT) {
+      const double v = (double)yg[i];
+      yy = fma(v, v, yy);
+    }
+    yy = cta_sum(yy);
+    const double ynorm = sqrt(yy);  // early exit |y| <= tol (_kernels.py:71-78)
+    const double tol = a.eps[p];
+    int kdone = 0;
+    int64_t scans = 0;
+    double rnorm = ynorm, rn2_final = 0.0;
+    bool delegate = false;
+    double hr[R];
+    int mypick = -1;  // the iteration this thread's candidate was picked at
+    if (!(ynorm <= tol) && k_max > 0) {
+#pragma unroll
+      for (int i = 0; i < R; i++) hr[i] = 0.0;
+      double c = valid ? a.alpha0_in[p * smax + t] : 0.0;
+      const double gjj = valid ? __ldg(a.gram + cid * T + cid) : 1.0;
+      double s2 = 0.0;  // sum_i h_i[t]^2
+      bool taken = !valid;
+      double rn2 = yy;
+      const double tol2 = tol * tol, band = 1e-12 * yy;
+      int k = 0;
+      for (;;) {  // iterations; leaves the inner loop only to stop or to test the band
+      bool check = false;
+      for (; k < k_max; k++) {
+        rn2_final = rn2;
+        scans += S - k;
+        const int par = k & 1;
+        double *sbase = slots + par * NW * SL;
+        // ---- warp arg-max; the warp's winner publishes its column
+        const double v = taken ? 0.0 : fabs(c);
+        const double m = warp_max_nonneg(v);
+        const unsigned wj = __reduce_min_sync(CDB_FULL_MASK, v == m ? (unsigned)t : 0xffffffffu);
+        if ((unsigned)t == wj) {
+          double *sl = sbase + warp * SL;
+          sl[0] = m;
+          sl[1] = c;
+          sl[2] = gjj - s2;
+          sl[3] = gjj;
+          ((int64_t *)sl)[4] = (cid << 16) | t;
+          put_regs<R>(sl + 6, hr, (k < R ? k : R) & ~7);  // other rows: read in place
+        }
+        __syncthreads();
+        // ---- global winner: lane w reads slot w; strict '>' in warp order
+        // (lowest index on ties) = the first slot holding the maximum
+        const double mw = lane < NW ? sbase[lane * SL] : 0.0;
+        const double gm = warp_max_nonneg(mw);
+        if (!(gm > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
+        const int gw = __ffs(__ballot_sync(CDB_FULL_MASK, lane < NW && mw == gm)) - 1;
+        const double *ws = sbase + gw * SL;
+        const int64_t packed = ((const int64_t *)ws)[4];
+        const int bestj = (int)(packed & 0xffff);
+        const int64_t nid = packed >> 16;
+        const double g = valid ? __ldg(a.gram + nid * T + cid) : 0.0;
+        const double cj = ws[1], d2 = ws[2], gnn = ws[3];
+        const double *w = ws + 6;
+        // ---- sweep: sum_i w_i h_i[t] (register blocks, staged rows, smem rows)
+        const int kr = k < R ? k : R, kb = kr & ~7;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int b = 0; b < R / 8; b++) {
+          if (8 * b + 8 <= kb) {
+            const double2 w0 = *(const double2 *)(w + 8 * b), w1 = *(const double2 *)(w + 8 * b + 2);
+            const double2 w2 = *(const double2 *)(w + 8 * b + 4), w3 = *(const double2 *)(w + 8 * b + 6);
+            a0 = fma(w0.x, hr[8 * b], a0);
+            a1 = fma(w0.y, hr[8 * b + 1], a1);
+            a2 = fma(w1.x, hr[8 * b + 2], a2);
+            a3 = fma(w1.y, hr[8 * b + 3], a3);
+            a0 = fma(w2.x, hr[8 * b + 4], a0);
+            a1 = fma(w2.y, hr[8 * b + 5], a1);
+            a2 = fma(w3.x, hr[8 * b + 6], a2);
+            a3 = fma(w3.y, hr[8 * b + 7], a3);
+          }
+        }
+        // staged and shared-memory rows: w_i read from the winner's own column
+        for (int i = kb; i < kr; i++) a0 = fma(stg[(i & 7) * NT + bestj], stg[(i & 7) * NT + t], a0);
+        {
+          const double *hc = hsm + t, *wc = hsm + bestj;
+          int i = R;
+          for (; i + 3 < k; i += 4) {
+            const int64_t o = (int64_t)(i - R) * NT;
+            a0 = fma(wc[o], hc[o], a0);
+            a1 = fma(wc[o + NT], hc[o + NT], a1);
+            a2 = fma(wc[o + 2 * NT], hc[o + 2 * NT], a2);
+            a3 = fma(wc[o + 3 * NT], hc[o + 3 * NT], a3);
+          }
+          for (; i < k; i++) a0 = fma(wc[(int64_t)(i - R) * NT], hc[(int64_t)(i - R) * NT], a0);
+        }
+        if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
+          delegate = true;
+          break;
+        }
+        const double inv_d = rsqrt(d2);
+        const double zk = cj * inv_d;  // q_k^T y = <d_{j*}, r> / d
+        const double hk = valid ? (g - ((a0 + a1) + (a2 + a3))) * inv_d : 0.0;
+        if ((unsigned)t == (unsigned)bestj) {
+          taken = true;
+          mypick = k;
+          zv[k] = zk;
+          iv[k] = inv_d;
+          sup[k] = nid;
+        }
+        if (k < R) {
+          stg[(k & 7) * NT + t] = hk;
+          if ((k & 7) == 7) load_block<R>(hr, k >> 3, stg + t);
+        } else {
+          hsm[(int64_t)(k - R) * NT + t] = hk;
+        }
+        c = fma(-zk, hk, c);
+        s2 = fma(hk, hk, s2);
+        rn2 -= zk * zk;
+        rn2_final = rn2;
+        kdone = k + 1;
+        // ---- stop test (_kernels.py:156), exact residual inside the band
+        const double gap = rn2 - tol2;
+        if (gap > band) continue;
+        if (gap < -band) break;
+        check = true;
+        break;
+      }
+      if (!check) break;
+      file_col<R>(rm, kw, mypick, hr, stg + t, hsm + t, kdone);
+      __syncthreads();  // R and the picks in place
+      if (warp == 0) back_sub_cols(rm, kw, kdone, zv, iv, xv, lane);
+      __syncthreads();
+      double rr = 0.0;
+      for (int i = t; i < n; i += NT) {
+        double ri = (double)yg[i];
+        for (int l = 0; l < kdone; l++) ri = fma(-xv[l], a.d64[sup[l] * n + i], ri);
+        rr = fma(ri, ri, rr);
+      }
+      rr = cta_sum(rr);
+      if (sqrt(rr) <= tol) break;
+      k++;
+      }
+    }
+    __syncthreads();  // R, z, picks complete
+    if (delegate) {
+      if (t == 0) a.status[p] |= ST_DELEGATE;
+      __syncthreads();
+      continue;
+    }
+    file_col<R>(rm, kw, mypick, hr, stg + t, hsm + t, kdone);
+    __syncthreads();
+    if (warp == 0) back_sub_cols(rm, kw, kdone, zv, iv, xv, lane);
+    __syncthreads();
+    if (kdone > 0) {
+      if (rn2_final > 1e-6 * yy) {
+        rnorm = sqrt(rn2_final);
+      } else {
+        double rr = 0.0;
+        for (int i = t; i < n; i += NT) {
+          double ri = (double)yg[i];
+          for (int l = 0; l < kdone; l++) ri = fma(-xv[l], __ldg(a.d64 + sup[l] * n + i), ri);
+          rr = fma(ri, ri, rr);
+        }
+        rnorm = sqrt(cta_sum(rr));
+      }
+    }
+    int64_t *out_sel = a.out_sel + p * kw;
+    double *out_coef = a.out_coef + p * kw;
+    for (int j = t; j < kw; j += NT) {
+      out_sel[j] = j < kdone ? sup[j] : -1;
+      out_coef[j] = j < kdone ? xv[j] : 0.0;
+    }
+    if (t == 0) {
+      a.out_count[p] = kdone;
+      a.out_rnorm[p] = rnorm;
+      a.out_scans[p] = scans;
+      a.out_flag[p] = 0;
+    }
+    __syncthreads();  // the next signal reuses the shared state
+  }
+}
+
+template <typename YT, int R>
+cudaError_t go_reg(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
+                   cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(gram_reg_kernel<YT, R>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pl.per_warp_smem);
+  if (e != cudaSuccess) return e;
+  gram_reg_kernel<YT, R><<<(unsigned)pl.warps, 512, pl.per_warp_smem, stream>>>(args, ys);
+  return cudaGetLastError();
+}
+
+template <typename YT>
+cudaError_t go_reg_r(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
+                     cudaStream_t stream) {
+  switch (pl.nr) {
+    case 16: return go_reg<YT, 16>(args, ys, pl, stream);
+    case 24: return go_reg<YT, 24>(args, ys, pl, stream);
+    case 32: return go_reg<YT, 32>(args, ys, pl, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <typename YT, int CPT>
 cudaError_t go_cta(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
                    cudaStream_t stream) {
@@ -841,6 +1177,33 @@ int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_
 GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
                                 int max_smem_per_block, int num_sms) {
   GramStreamPlan pl{};
+  // on-chip H (gram_reg_kernel): one 512-thread CTA per SM, R register rows.
+  // Opt-in (CDB_GRAM_REG=1): measured on cfg 4 (65,536 signals) at 49.8 / 50.8 /
+  // 53.7 ms for R = 16 / 24 / 32 against 47.7 ms for the streamed CTA kernel --
+  // one signal per SM leaves the per-iteration chain (arg-max, barrier, Gram
+  // row load from HBM) exposed (ncu: issue 39%, stalls wait / short-scoreboard
+  // / barrier), which costs what the L2 row traffic it removes saved.
+  const char *rv = getenv("CDB_GRAM_REG");
+  if (!stage_y && s <= 512 && kw <= 64 && rv && atoi(rv) != 0) {
+    int r = 16;
+    if (const char *v = getenv("CDB_GRAM_R")) r = atoi(v);
+    if (r != 16 && r != 24 && r != 32) r = 16;
+    const int64_t nsr = kw > r ? kw - r : 0;
+    const int64_t sl = 6 + r;
+    const int64_t dbl = (nsr > 8 ? nsr : 8) * 512 + 2 * 16 * sl + 4 * kw + 16;
+    pl.per_warp_smem = (8 * dbl + 15) & ~int64_t(15);  // per CTA
+    pl.ok = pl.per_warp_smem <= max_smem_per_block;
+    if (pl.ok) {
+      pl.reg = true;
+      pl.cta = true;
+      pl.wpb = 16;
+      pl.nr = r;
+      pl.warps = num_sms;  // CTAs
+      pl.slot_doubles = kw * kw;  // the CTA's R matrix
+      return pl;
+    }
+    pl = GramStreamPlan{};
+  }
   const char *cv = getenv("CDB_GRAM_CTA");
   if (!stage_y && s <= 512 && kw <= 64 && !(cv && atoi(cv) == 0)) {
     // CTA per signal (gram_cta_kernel): cps CTAs per SM share its shared memory
@@ -904,6 +1267,11 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
     const GramStreamPlan pl = gram_stream_plan(s, kw, n, args.alpha0_in == nullptr,
                                                max_smem_per_block, num_sms);
     if (!pl.ok) return cudaErrorInvalidValue;
+    if (pl.reg) {  // H on chip, CTA per signal
+      note_launch();
+      return ys_f32 ? go_reg_r<float>(args, (const float *)ys, pl, stream)
+                    : go_reg_r<double>(args, (const double *)ys, pl, stream);
+    }
     if (pl.cta) {  // CTA per signal
       note_launch();
       if (ys_f32)
