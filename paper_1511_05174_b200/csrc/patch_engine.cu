@@ -14,6 +14,8 @@
 //    adding the covering patches in ascending patch order (the reference's
 //    accumulation order) and dividing by the coverage count; uncovered cells
 //    are 0 and counted.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "engines.h"
 
@@ -103,7 +105,75 @@ __global__ void __launch_bounds__(256) extract_rows_kernel(const ST *__restrict_
   }
 }
 
-// est[p][e] = sum_l coef[p][l] * d[sel[p][l]][e]  (+ dc[p]); warp per patch
+// Segment extraction: a warp takes up to 32 consecutive patches of one
+// patch row (same grid index on every axis but the last).  Their union is
+// (n / pl) signal rows of W = (np - 1) s + pl contiguous cells -- read once
+// into shared memory (coalesced), instead of n cells per patch.  Lane q sums
+// patch q in element order (numpy's axis-0 order, as extract_rows_kernel),
+// and the np x n output rows, contiguous in HBM, go out as 16-byte stores.
+// toff[e] = tile offset of element e for patch 0 (patch q adds q s).
+template <typename ST>
+__global__ void __launch_bounds__(512) extract_seg_kernel(const ST *__restrict__ sig, Geom g,
+                                                          int remove_dc, int wmax,
+                                                          double *__restrict__ rows,
+                                                          double *__restrict__ dc) {
+  extern __shared__ double xs[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const int n = (int)g.n, rank = g.rank;
+  const int pl = (int)g.pat[rank - 1], nrow = n / pl, st = (int)g.str[rank - 1];
+  const int64_t gl = g.grid[rank - 1], segs = (gl + 31) / 32, tasks = (g.p / gl) * segs;
+  int *toff = (int *)xs;                           // n
+  int *roff = toff + n;                            // nrow signal offsets of the tile rows
+  double *tile = xs + ((2 * n + 1) / 2 + 1) / 2 * 2 + (size_t)wib * (nrow * wmax + 32);
+  double *mean = tile + nrow * wmax;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) toff[e] = (e / pl) * wmax + e % pl;
+  for (int r = threadIdx.x; r < nrow; r += blockDim.x) roff[r] = (int)elem_offset(g, (int64_t)r * pl);
+  __syncthreads();
+  for (int64_t task = (int64_t)blockIdx.x * nwb + wib; task < tasks; task += (int64_t)gridDim.x * nwb) {
+    const int64_t rowp = task / segs, si = task % segs;
+    const int64_t p0 = rowp * gl + si * 32;
+    const int np = (int)(gl - si * 32 < 32 ? gl - si * 32 : 32);
+    const int w = (np - 1) * st + pl;
+    const ST *src = sig + origin_offset(g, p0);
+    for (int idx = lane; idx < nrow * w; idx += 32) {
+      const int r = idx / w, x = idx - r * w;
+      tile[r * wmax + x] = (double)src[roff[r] + x];
+    }
+    __syncwarp();
+    double mq = 0.0;
+    if (remove_dc) {
+      double s = 0.0;
+      if (lane < np)
+        for (int e = 0; e < n; e++) s += tile[toff[e] + lane * st];  // numpy's axis-0 order
+      mq = s / (double)n;
+      if (lane < np) dc[p0 + lane] = mq;
+      mean[lane] = mq;
+      __syncwarp();
+    }
+    double *dst = rows + p0 * n;
+    const int tot = np * n;
+    if ((n & 1) == 0) {  // pairs of elements of one patch: 16-byte stores
+      for (int idx = 2 * lane; idx < tot; idx += 64) {
+        const int q = idx / n, e = idx - q * n;
+        const double t0 = tile[toff[e] + q * st], t1 = tile[toff[e + 1] + q * st];
+        *(double2 *)(dst + idx) =
+            remove_dc ? make_double2(t0 - mean[q], t1 - mean[q]) : make_double2(t0, t1);
+      }
+    } else {
+      for (int idx = lane; idx < tot; idx += 32) {
+        const int q = idx / n, e = idx - q * n;
+        const double v = tile[toff[e] + q * st];
+        dst[idx] = remove_dc ? v - mean[q] : v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// est[p][e] = sum_l coef[p][l] * d[sel[p][l]][e]  (+ dc[p]); warp per patch.
+// The patch's codes are loaded once (lane l holds pick l) and broadcast by
+// shuffles; each lane then runs the reference-order fma chain for its
+// elements with coalesced atom-row loads.
 __global__ void __launch_bounds__(256) reconstruct_kernel(const double *__restrict__ d64,
                                                           int64_t n, const int64_t *__restrict__ sel,
                                                           const double *__restrict__ coef,
@@ -115,6 +185,27 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const double *__restri
   for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p; q += nw) {
     const int64_t *sq = sel + q * kw;
     const double *cq = coef + q * kw;
+    const double dq = dc ? dc[q] : 0.0;
+    if (kw <= 32 && n <= 64 && (int64_t)n * 65536 < ((int64_t)1 << 31)) {
+      const int64_t jl = lane < kw ? sq[lane] : -1;
+      const int js = (int)jl * (int)n;  // row offset (T n < 2^31)
+      const double cs = lane < kw ? cq[lane] : 0.0;
+      // picks before the first -1 (the reference breaks there)
+      const unsigned neg = __ballot_sync(CDB_FULL_MASK, lane < kw && jl < 0);
+      const int kv = neg ? __ffs(neg) - 1 : (int)kw;
+      const int e0 = lane, e1 = lane + 32;
+      const int c0 = e0 < n ? e0 : (int)n - 1, c1 = e1 < n ? e1 : (int)n - 1;
+      double a0 = 0.0, a1 = 0.0;
+      for (int l = 0; l < kv; l++) {
+        const double cl = __shfl_sync(CDB_FULL_MASK, cs, l);
+        const double *row = d64 + __shfl_sync(CDB_FULL_MASK, js, l);
+        a0 = fma(cl, __ldg(row + c0), a0);
+        a1 = fma(cl, __ldg(row + c1), a1);
+      }
+      if (e0 < n) est[q * n + e0] = dc ? a0 + dq : a0;
+      if (e1 < n) est[q * n + e1] = dc ? a1 + dq : a1;
+      continue;
+    }
     for (int64_t e = lane; e < n; e += 32) {
       double acc = 0.0;
       for (int64_t l = 0; l < kw; l++) {
@@ -122,7 +213,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const double *__restri
         if (j < 0) break;  // -1 padding after the last pick
         acc = fma(cq[l], __ldg(d64 + j * n + e), acc);
       }
-      est[q * n + e] = dc ? acc + dc[q] : acc;
+      est[q * n + e] = dc ? acc + dq : acc;
     }
   }
 }
@@ -159,22 +250,38 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const double *__restrict
   double acc = 0.0, w = 0.0;
   if (any) {
     int gi[4] = {lo[0], lo[1], lo[2], lo[3]};
-    while (true) {
-      int64_t p = 0;
-      int e = 0;
-      for (int d = 0; d < rank; d++) {
-        p = p * g.grid[d] + gi[d];
-        e = e * (int)g.pat[d] + (xc[d] - gi[d] * (int)g.str[d]);
+    bool more = true;
+    while (more) {
+      // up to 8 covering patches in ascending p: their loads in flight
+      // together, accumulated in order
+      int off[8], pp[8];  // cells < 2^31 and P n < 2^31 (checked at launch)
+      int m = 0;
+      while (more && m < 8) {
+        int p = 0, e = 0;
+        for (int d = 0; d < rank; d++) {
+          p = p * (int)g.grid[d] + gi[d];
+          e = e * (int)g.pat[d] + (xc[d] - gi[d] * (int)g.str[d]);
+        }
+        off[m] = p * n + e;
+        pp[m] = p;
+        m++;
+        int d = rank - 1;  // odometer, last axis fastest = ascending p
+        while (d >= 0 && ++gi[d] > hi[d]) {
+          gi[d] = lo[d];
+          d--;
+        }
+        more = d >= 0;
       }
-      const double v = est[p * n + e];
-      acc += dc ? v + dc[p] : v;
-      w += 1.0;
-      int d = rank - 1;  // odometer, last axis fastest = ascending p
-      while (d >= 0 && ++gi[d] > hi[d]) {
-        gi[d] = lo[d];
-        d--;
-      }
-      if (d < 0) break;
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < m) v[u] = __ldg(est + off[u]) + (dc ? __ldg(dc + pp[u]) : 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < m) {
+          acc += v[u];
+          w += 1.0;
+        }
     }
   }
   if (w == 0.0) {
@@ -214,6 +321,38 @@ cudaError_t launch_extract_patches(const void *signal, bool f32, int rank, const
   Geom g;
   cudaError_t e = make_geom(g, rank, sig, pat, str);
   if (e != cudaSuccess) return e;
+  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
+  {  // segment path: 32 patches of a patch row share one tile (CDB_EXTRACT_SEG=0: off)
+    const int pl = (int)g.pat[rank - 1], st = (int)g.str[rank - 1];
+    const int64_t wmax = 31 * (int64_t)st + pl, nrow = g.n / pl;
+    const size_t head = (size_t)(((2 * g.n + 1) / 2 + 1) / 2 * 2) * sizeof(double);
+    const size_t per_w = (size_t)(nrow * wmax + 32) * sizeof(double);
+    const char *sv = getenv("CDB_EXTRACT_SEG");
+    if (!(sv && atoi(sv) == 0) && nrow * wmax <= 2048 && wmax < (1 << 20)) {
+      int warps = 16;
+      while (warps > 1 && head + warps * per_w > 160 * 1024) warps /= 2;
+      const size_t smem = head + warps * per_w;
+      const int64_t gl = g.grid[rank - 1];
+      const int64_t tasks = (g.p / gl) * ((gl + 31) / 32);
+      int64_t blocks = (tasks + warps - 1) / warps;
+      const int per_sm = (int)((200 * 1024) / smem) < 1 ? 1 : (int)((200 * 1024) / smem);
+      if (blocks > (int64_t)num_sms * per_sm) blocks = (int64_t)num_sms * per_sm;
+      auto sf = extract_seg_kernel<float>;
+      auto sd = extract_seg_kernel<double>;
+      if ((e = cudaFuncSetAttribute(f32 ? (const void *)sf : (const void *)sd,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+          cudaSuccess)
+        return e;
+      if (f32)
+        sf<<<(unsigned)blocks, 32 * warps, smem, stream>>>((const float *)signal, g, remove_dc,
+                                                            (int)wmax, rows, dc);
+      else
+        sd<<<(unsigned)blocks, 32 * warps, smem, stream>>>((const double *)signal, g, remove_dc,
+                                                            (int)wmax, rows, dc);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   // 8 warps; remove_dc stages 32 patches per warp
   const size_t per_warp = (remove_dc ? 33 : 1) * sizeof(double) * (size_t)g.n;
   int warps = 8;
@@ -249,10 +388,11 @@ cudaError_t launch_reconstruct_aggregate(const double *d64, int64_t n, const int
   cudaError_t e = make_geom(g, rank, sig, pat, str);
   if (e != cudaSuccess) return e;
   if (g.n != n || g.p != p) return cudaErrorInvalidValue;
+  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
+  if (p * n >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   int64_t blocks = (p + 7) / 8;
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   reconstruct_kernel<<<(unsigned)blocks, 256, 0, stream>>>(d64, n, sel, coef, kw, p, dc, est);
-  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   aggregate_kernel<<<(unsigned)((g.cells + 255) / 256), 256, 0, stream>>>(est, nullptr, g, out,
                                                                            uncovered);
   note_launch(2);
@@ -266,7 +406,7 @@ cudaError_t launch_aggregate(const double *rows, const double *dc, int rank, con
   Geom g;
   cudaError_t e = make_geom(g, rank, sig, pat, str);
   if (e != cudaSuccess) return e;
-  if (g.cells >= (int64_t)1 << 31) return cudaErrorInvalidValue;
+  if (g.cells >= (int64_t)1 << 31 || g.p * g.n >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   aggregate_kernel<<<(unsigned)((g.cells + 255) / 256), 256, 0, stream>>>(rows, dc, g, out,
                                                                            uncovered);
   note_launch();
