@@ -1543,7 +1543,22 @@ cdb_status cdb_ksvd_update(int64_t n, int64_t m, int64_t t, const double *y_rows
   a.bglob = bg.as<double>();
   a.taken = taken.as<uint32_t>();
   a.replaced = (int64_t *)r_out.dev;
+  DevBuf prof;
+  const bool kprof = getenv("CDB_KSVD_PROF") != nullptr;
+  if (kprof) {
+    CDB_CUDA(prof.alloc(16 * sizeof(long long), st));
+    CDB_CUDA(cudaMemsetAsync(prof.ptr, 0, 16 * sizeof(long long), st));
+    a.prof = (long long *)prof.ptr;
+  }
   CDB_CUDA(cdb::launch_ksvd_update(a, cdb::ksvd_update_smem(n, smem_b), st));
+  if (kprof) {
+    long long hp[16];
+    CDB_CUDA(cudaMemcpyAsync(hp, prof.ptr, sizeof(hp), cudaMemcpyDeviceToHost, st));
+    CDB_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "ksvd phases (k cycles):");
+    for (int i = 0; i < 13; i++) fprintf(stderr, " %d:%.0f", i, hp[i] * 1e-3);
+    fprintf(stderr, "\n");
+  }
   CDB_CUDA(e_io.finish(st));
   CDB_CUDA(d_io.finish(st));
   CDB_CUDA(v_io.finish(st));

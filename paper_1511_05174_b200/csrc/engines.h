@@ -228,6 +228,7 @@ struct KsvdArgs {
   double *bglob;          // scratch: N x N (Gram matrix beyond smem_b)
   uint32_t *taken;        // M bits, zeroed
   int64_t *replaced;      // out
+  long long *prof;        // optional phase times (ns, 16 slots; CDB_KSVD_PROF=1)
 };
 size_t ksvd_update_smem(int64_t n, int64_t smem_b);
 cudaError_t launch_ksvd_update(const KsvdArgs &a, size_t smem, cudaStream_t stream);
