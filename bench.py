@@ -48,7 +48,9 @@ REF_PATH = os.path.join(REPO, "baseline", "_ref")
 
 
 def load_traffic():
-    """DRAM bytes per launch of each profiled kernel (profiles/*_ncu_traffic.json)."""
+    """ncu DRAM traffic of each profiled kernel: round 2 (profiles/r2_ncu_traffic.json,
+    configs[4] captures) as bytes per unit (signal) of a captured launch; round-1
+    entries (bytes per configs[1] launch) only for kernels round 2 did not capture."""
     out = {}
     for name in ("r1_ncu_traffic.json", "r2_ncu_traffic.json"):
         try:
@@ -57,6 +59,14 @@ def load_traffic():
         except (OSError, ValueError):
             pass
     return out
+
+
+def traffic_per_launch(entry, units_per_launch):
+    """DRAM bytes of one launch: a round-2 per-unit figure times the units the
+    launch processes, or a round-1 per-launch figure as is."""
+    if isinstance(entry, dict):
+        return entry["bytes_per_unit"] * units_per_launch
+    return entry
 
 
 def load_peaks():
@@ -575,7 +585,9 @@ def bench_ours(args):
     step_tf = (f_step1 + f_step2) * world / (zt_ms / args.steps * 1e-3) / 1e12
     roofline = {
         "bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": p_emu,
-        "unit": "TFLOP/s", "frac": achieved / p_emu, "traffic": traffic_tab.get(dom_name),
+        "unit": "TFLOP/s", "frac": achieved / p_emu,
+        "traffic": (traffic_per_launch(traffic_tab[dom_name], P * args.steps / max(dom_launches, 1))
+                    if dom_name in traffic_tab else None),
         "launch_ms": dom_ms, "share_of_step": dom_total / max(sum(v[0] for v in prof_zt.values()),
                                                               1e-9),
         "step": {"achieved": step_tf, "frac": step_tf / p_emu,
@@ -584,7 +596,8 @@ def bench_ours(args):
                  "the kernel's step (actual scan counts) / its mean launch time; peak = "
                  f"{peaks_kind} bf16 {peaks['bf16_tflops']} TF/s / 6 (P_emu, 3xTF32-emulated "
                  "fp32); the Gram formulation of step 2 does ~1/128 of the scan flops, so frac "
-                 "can exceed 1; traffic = ncu DRAM bytes per launch (profiles/)"}
+                 "can exceed 1; traffic = ncu DRAM bytes per launch (profiles/r2_ncu_traffic.json: "
+                 "bytes per signal of a 65,536-signal capture x the signals of this launch)"}
     corr = prof_full.get("corr_topk")
     full_roof = None
     if corr:
@@ -595,7 +608,9 @@ def bench_ours(args):
                      "achieved": c_flops / (c_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
                      "unit": "TFLOP/s",
                      "frac": c_flops / (c_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-                     "traffic": traffic_tab.get("corr_topk_full"), "launch_ms": c_ms,
+                     "traffic": (traffic_per_launch(traffic_tab["corr_topk_full"],
+                                                    P * args.full_steps * w.k / max(corr[1], 1))
+                                 if "corr_topk_full" in traffic_tab else None), "launch_ms": c_ms,
                      "basis": "2*N*scans of the full-OMP batch (actual scan counts) / corr_topk "
                               "time, against the measured bf16 peak it runs on"}
 
