@@ -110,6 +110,7 @@ struct GramStreamPlan {
   bool ok;
   bool cta;   // CTA per signal (gram_cta_kernel): warps = CTAs, per_warp_smem = per CTA
   bool reg;   // H on chip (gram_reg_kernel, cta too): nr = register rows
+  bool tma;   // cta: rows [nr, k) streamed through a shared-memory ring by bulk copies
   int cpt;    // cta: candidates per thread
   int wpb, nr;
   int64_t per_warp_smem, warps, slot_doubles;

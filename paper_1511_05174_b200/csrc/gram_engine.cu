@@ -786,6 +786,284 @@ __global__ void __launch_bounds__(128) gram_cta_kernel(GramArgs a, const YT *__r
   }
 }
 
+// ---------------------------------------------------------------- TMA-streamed rows
+// gram_cta_kernel with the L2-resident rows streamed by the bulk-copy engine:
+// the rows [nr, k) an iteration re-reads go through a ring of RS shared-memory
+// slots (4 KB each: the whole row of the signal), issued by one thread right
+// after the arg-max barrier -- before the Gram gather and the shared-memory
+// rows' sweep, so their L2 latency hides behind that work -- and refilled as
+// the sweep frees them (full / empty mbarriers per slot).  The row sweep order
+// and arithmetic are gram_cta_kernel's, so the results are bit-identical; the
+// register pipeline of 8 in-flight rows (252 registers) is gone.
+constexpr int kRingSlots = 8;
+
+template <typename YT, int CPT>
+__global__ void __launch_bounds__(128) gram_tma_kernel(GramArgs a, const YT *__restrict__ ys,
+                                                        int nr) {
+  constexpr int NT = 128, NW = NT / 32, RS = kRingSlots;
+  constexpr int SP = NT * CPT;  // H row stride (doubles)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
+  const int64_t T = a.t;
+  const Cands cs = a.cands;
+  double *zv = (double *)smem_raw;
+  double *iv = zv + kw;
+  int64_t *sup = (int64_t *)(iv + kw);
+  double *xv = (double *)(sup + kw);
+  int *pj = (int *)(xv + kw);
+  double *xb = xv + 2 * kw;                 // exchange: [2][NW] x {|c|, c}
+  int64_t *xi = (int64_t *)(xb + 4 * NW);   // exchange: [2][NW] x {j, atom}
+  double *red = (double *)(xi + 4 * NW);    // NW partial sums + 2 flags
+  double *hs = red + NW + 2;
+  hs += ((uintptr_t)hs & 15) ? 1 : 0;       // 16-byte aligned rows
+  double *ring = hs + (int64_t)nr * SP;     // RS x SP
+  uint64_t *full = (uint64_t *)(ring + (int64_t)RS * SP);
+  uint64_t *empty = full + RS;
+  double *hg = a.hwork + (int64_t)blockIdx.x * (kw - nr) * SP - (int64_t)nr * SP;
+  const bool q8 = cs.mode == 2 && cs.q % CPT == 0;
+  if (tid == 0) {
+    for (int r = 0; r < RS; r++) {
+      sm100::mbar_init(&full[r], 1);
+      sm100::mbar_init(&empty[r], NT);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t qbase = 0;  // ring uses so far (CTA-uniform)
+  auto issue = [&](uint32_t q, int row) {  // tid 0: row -> slot q % RS once it is free
+    const uint32_t sl = q % RS, ph = (q / RS) & 1;
+    sm100::mbar_wait(&empty[sl], ph ^ 1);
+    sm100::mbar_expect_tx(&full[sl], (uint32_t)(SP * sizeof(double)));
+    sm100::bulk_load(ring + (int64_t)sl * SP, hg + (int64_t)row * SP, (uint32_t)(SP * sizeof(double)),
+                     &full[sl]);
+  };
+
+  for (int64_t local = blockIdx.x; local < a.p; local += gridDim.x) {
+    const int64_t p = a.p_offset + local;
+    const YT *yg = ys + p * a.ys_stride;
+    const int S = (int)cs.count(p);
+    const int k_max = (int)cs.budget(p, a.k_max, n);
+    int cid[CPT];
+    unsigned tk = 0u;
+#pragma unroll
+    for (int c = 0; c < CPT; c++) {
+      const int j = tid * CPT + c;
+      cid[c] = j < S ? (int)cs.id(p, j) : 0;
+      if (j >= S) tk |= 1u << c;
+    }
+    double yy = 0.0;
+    for (int i = tid; i < n; i += NT) {
+      const double v = (double)yg[i];
+      yy = fma(v, v, yy);
+    }
+    yy = warp_sum(yy);
+    if (lane == 0) red[warp] = yy;
+    __syncthreads();
+    yy = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) yy += red[w];
+    const double ynorm = sqrt(yy);  // early exit |y| <= tol (_kernels.py:71-78)
+    const double tol = a.eps[p];
+    int kdone = 0;
+    int64_t scans = 0;
+    double rnorm = ynorm, rn2_final = 0.0;
+    bool delegate = false;
+    if (!(ynorm <= tol) && k_max > 0) {
+      double cr[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; c++) {
+        const int j = tid * CPT + c;
+        cr[c] = j < S ? a.alpha0_in[p * smax + j] : 0.0;
+      }
+      double rn2 = yy;
+      const double tol2 = tol * tol, band = 1e-12 * yy;
+      for (int k = 0; k < k_max; k++) {
+        rn2_final = rn2;
+        scans += S - k;
+        // ---- arg-max: thread, warp, then the 4 warps through shared memory
+        double best = -1.0;
+        int bc = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; c++) {
+          const double v = fabs(cr[c]);
+          if (!((tk >> c) & 1u) && v > best) {
+            best = v;
+            bc = c;
+          }
+        }
+        const unsigned bj = best >= 0.0 ? (unsigned)(tid * CPT + bc) : 0xffffffffu;
+        const double m = warp_max_nonneg(best);
+        const unsigned wj = __reduce_min_sync(CDB_FULL_MASK, best == m ? bj : 0xffffffffu);
+        const int src = __ffs(__ballot_sync(CDB_FULL_MASK, bj == wj)) - 1;
+        double myc = 0.0;
+        int myid = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; c++)
+          if (c == bc) {
+            myc = cr[c];
+            myid = cid[c];
+          }
+        const double wc = __shfl_sync(CDB_FULL_MASK, myc, src < 0 ? 0 : src);
+        const int wid = __shfl_sync(CDB_FULL_MASK, myid, src < 0 ? 0 : src);
+        const int par = k & 1;
+        if (lane == 0) {
+          xb[(par * NW + warp) * 2] = m;
+          xb[(par * NW + warp) * 2 + 1] = wc;
+          xi[(par * NW + warp) * 2] = (int64_t)wj;
+          xi[(par * NW + warp) * 2 + 1] = wid;
+        }
+        __syncthreads();  // also publishes row k-1 of H (shared memory or, fenced, the L2 slot)
+        double gm = -1.0, cj = 0.0;
+        int64_t gj = 0xffffffffll, nid = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+          const double mw = xb[(par * NW + w) * 2];
+          const int64_t jw = xi[(par * NW + w) * 2];
+          if (mw > gm || (mw == gm && jw < gj)) {
+            gm = mw;
+            gj = jw;
+            cj = xb[(par * NW + w) * 2 + 1];
+            nid = xi[(par * NW + w) * 2 + 1];
+          }
+        }
+        if (!(gm > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
+        const int bestj = (int)gj;
+        // ---- the L2 rows of this iteration start streaming now
+        const int nl = k > nr ? k - nr : 0;
+        if (tid == 0)
+          for (int j = 0; j < nl && j < RS; j++) issue(qbase + j, nr + j);
+        if (tid == bestj / CPT) tk |= 1u << (bestj % CPT);
+        // ---- Gram row slice (HBM gather, lands after the sweep), H sweep
+        const double *grow = a.gram + nid * T;
+        double gsl[CPT], hacc[CPT];
+        if (q8 && tid * CPT + CPT <= S) {
+          const double2 *g2 = (const double2 *)(grow + cid[0]);
+#pragma unroll
+          for (int c = 0; c < CPT / 2; c++) {
+            const double2 t2 = __ldg(g2 + c);
+            gsl[2 * c] = t2.x;
+            gsl[2 * c + 1] = t2.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPT; c++) gsl[c] = tid * CPT + c < S ? __ldg(grow + cid[c]) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; c++) hacc[c] = 0.0;
+        const double gnn = __ldg(grow + nid);
+        double ww = 0.0;
+        const int ks = k < nr ? k : nr;
+#pragma unroll 4
+        for (int i = 0; i < ks; i++) {
+          const double *hi = hs + i * SP;
+          const double wi = hi[bestj];
+          ww = fma(wi, wi, ww);
+#pragma unroll
+          for (int c = 0; c < CPT / 2; c++) {
+            const double2 t2 = *(const double2 *)(hi + tid * CPT + 2 * c);
+            hacc[2 * c] = fma(-wi, t2.x, hacc[2 * c]);
+            hacc[2 * c + 1] = fma(-wi, t2.y, hacc[2 * c + 1]);
+          }
+        }
+        for (int j = 0; j < nl; j++) {  // ring rows, same order and arithmetic
+          const uint32_t q = qbase + j, sl = q % RS, ph = (q / RS) & 1;
+          sm100::mbar_wait(&full[sl], ph);
+          const double *hi = ring + (int64_t)sl * SP;
+          const double wi = hi[bestj];
+          ww = fma(wi, wi, ww);
+#pragma unroll
+          for (int c = 0; c < CPT / 2; c++) {
+            const double2 t2 = *(const double2 *)(hi + tid * CPT + 2 * c);
+            hacc[2 * c] = fma(-wi, t2.x, hacc[2 * c]);
+            hacc[2 * c + 1] = fma(-wi, t2.y, hacc[2 * c + 1]);
+          }
+          sm100::mbar_arrive(&empty[sl]);
+          if (tid == 0 && j + RS < nl) issue(q + RS, nr + j + RS);
+        }
+        qbase += nl;
+#pragma unroll
+        for (int c = 0; c < CPT; c++) hacc[c] += gsl[c];
+        const double d2 = gnn - ww;  // identical in every thread (same w_i, same order)
+        if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
+          delegate = true;
+          break;
+        }
+        const double inv_d = rsqrt(d2);
+        const double zk = cj * inv_d;
+        double *hk = (k < nr ? hs : hg) + (int64_t)k * SP + tid * CPT;
+#pragma unroll
+        for (int c = 0; c < CPT / 2; c++) {
+          const double h0 = hacc[2 * c] * inv_d, h1 = hacc[2 * c + 1] * inv_d;
+          *(double2 *)(hk + 2 * c) = make_double2(h0, h1);
+          cr[2 * c] = fma(-zk, h0, cr[2 * c]);
+          cr[2 * c + 1] = fma(-zk, h1, cr[2 * c + 1]);
+        }
+        if (k >= nr) sm100::fence_proxy_async_global();  // row k is read back by the bulk copies
+        if (tid == 0) {
+          zv[k] = zk;
+          iv[k] = inv_d;
+          pj[k] = bestj;
+          sup[k] = nid;
+        }
+        rn2 -= zk * zk;
+        rn2_final = rn2;
+        kdone = k + 1;
+        // ---- stop test (_kernels.py:156), exact residual inside the band
+        const double gap = rn2 - tol2;
+        if (gap > band) continue;
+        if (gap < -band) break;
+        __syncthreads();  // row k and the pick in place
+        if (warp == 0) {
+          back_sub_rows<CPT>(hs, hg, nr, SP, kdone, zv, iv, pj, xv, lane);
+          double rr = 0.0;
+          for (int i = lane; i < n; i += 32) {
+            double ri = (double)yg[i];
+            for (int l = 0; l < kdone; l++) ri = fma(-xv[l], a.d64[sup[l] * n + i], ri);
+            rr = fma(ri, ri, rr);
+          }
+          rr = warp_sum(rr);
+          if (lane == 0) red[NW] = sqrt(rr) <= tol ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        if (red[NW] != 0.0) break;
+      }
+    }
+    __syncthreads();  // H, z, picks complete
+    if (delegate) {
+      if (tid == 0) a.status[p] |= ST_DELEGATE;
+    } else if (warp == 0) {
+      back_sub_rows<CPT>(hs, hg, nr, SP, kdone, zv, iv, pj, xv, lane);
+      if (kdone > 0) {
+        if (rn2_final > 1e-6 * yy) {
+          rnorm = sqrt(rn2_final);
+        } else {
+          double rr = 0.0;
+          for (int i = lane; i < n; i += 32) {
+            double ri = (double)yg[i];
+            for (int l = 0; l < kdone; l++) ri = fma(-xv[l], __ldg(a.d64 + sup[l] * n + i), ri);
+            rr = fma(ri, ri, rr);
+          }
+          rnorm = sqrt(warp_sum(rr));
+        }
+      }
+      int64_t *out_sel = a.out_sel + p * kw;
+      double *out_coef = a.out_coef + p * kw;
+      for (int j = lane; j < kw; j += 32) {
+        out_sel[j] = j < kdone ? sup[j] : -1;
+        out_coef[j] = j < kdone ? xv[j] : 0.0;
+      }
+      if (lane == 0) {
+        a.out_count[p] = kdone;
+        a.out_rnorm[p] = rnorm;
+        a.out_scans[p] = scans;
+        a.out_flag[p] = 0;
+      }
+    }
+    __syncthreads();  // the next signal reuses the shared state
+  }
+}
+
 // ---------------------------------------------------------------- on-chip H
 // cfg 4's step 2 (S = 512, K = 64: 256 KB of fp64 H per signal) with the whole
 // H on chip: one 512-thread CTA per SM codes one signal at a time, thread t
@@ -1123,6 +1401,17 @@ cudaError_t go_reg_r(const GramArgs &args, const YT *ys, const GramStreamPlan &p
 }
 
 template <typename YT, int CPT>
+cudaError_t go_tma(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
+                   cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(gram_tma_kernel<YT, CPT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pl.per_warp_smem);
+  if (e != cudaSuccess) return e;
+  gram_tma_kernel<YT, CPT><<<(unsigned)pl.warps, 128, pl.per_warp_smem, stream>>>(args, ys, pl.nr);
+  return cudaGetLastError();
+}
+
+template <typename YT, int CPT>
 cudaError_t go_cta(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
                    cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(gram_cta_kernel<YT, CPT>,
@@ -1214,15 +1503,26 @@ GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
     const int64_t fixed = 8 * (5 * kw + 9 * 4 + 2 + 2);
     int64_t per_cta = (int64_t)(228 * 1024) / cps - 1024;
     if (per_cta > max_smem_per_block) per_cta = max_smem_per_block;
-    int64_t nr = (per_cta - fixed) / (8 * sp);
+    // TMA-streamed rows (opt-in CDB_GRAM_TMA=1; a ring of kRingSlots rows + its
+    // mbarriers comes out of the shared rows).  Measured on cfg 4 (65,536
+    // signals, bit-identical results): 102.3 ms against 47.8 ms for the
+    // register-pipelined kernel -- 8 ring slots (32 KB) keep half the bytes in
+    // flight of its 16 rows x 128 threads of registers, the bulk-copy latency is
+    // longer than an L2 load's, and every refill waits for the whole CTA.
+    const char *tv = getenv("CDB_GRAM_TMA");
+    const bool tma = tv && atoi(tv) != 0;
+    const int64_t ring = tma ? kRingSlots * 8 * sp + 16 * kRingSlots + 16 : 0;
+    int64_t nr = (per_cta - fixed - ring) / (8 * sp);
     if (nr > kw) nr = kw;
     if (nr < 0) nr = 0;
-    pl.ok = per_cta > fixed;
+    pl.ok = per_cta > fixed + ring;
+    pl.tma = tma && nr < kw;
+    if (!pl.tma && tma) nr = (per_cta - fixed) / (8 * sp) > kw ? kw : (per_cta - fixed) / (8 * sp);
     pl.cta = true;
     pl.cpt = cpt;
     pl.wpb = 4;
     pl.nr = (int)nr;
-    pl.per_warp_smem = (fixed + 8 * nr * sp + 15) & ~int64_t(15);  // per CTA
+    pl.per_warp_smem = (fixed + 8 * nr * sp + (pl.tma ? ring : 0) + 15) & ~int64_t(15);  // per CTA
     pl.warps = (int64_t)num_sms * cps;                                // CTAs
     pl.slot_doubles = (kw - nr) * sp;
     return pl;
@@ -1271,6 +1571,14 @@ cudaError_t launch_gram(const GramArgs &args, const void *ys, bool ys_f32, int m
       note_launch();
       return ys_f32 ? go_reg_r<float>(args, (const float *)ys, pl, stream)
                     : go_reg_r<double>(args, (const double *)ys, pl, stream);
+    }
+    if (pl.cta && pl.tma) {  // CTA per signal, L2 rows streamed by bulk copies
+      note_launch();
+      if (ys_f32)
+        return pl.cpt == 2 ? go_tma<float, 2>(args, (const float *)ys, pl, stream)
+                           : go_tma<float, 4>(args, (const float *)ys, pl, stream);
+      return pl.cpt == 2 ? go_tma<double, 2>(args, (const double *)ys, pl, stream)
+                         : go_tma<double, 4>(args, (const double *)ys, pl, stream);
     }
     if (pl.cta) {  // CTA per signal
       note_launch();

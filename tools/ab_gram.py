@@ -19,9 +19,8 @@ def outs(k):
                 counts=torch.empty(P, dtype=torch.int64, device='cuda'), rnorm=torch.empty(P, dtype=torch.float64, device='cuda'),
                 scans=torch.empty(P, dtype=torch.int64, device='cuda'), flag=torch.empty(P, dtype=torch.uint8, device='cuda'))
 res = {}
-for label, env in (("stream", {"CDB_GRAM_REG": "0"}), ("reg32", {"CDB_GRAM_REG": "1", "CDB_GRAM_R": "32"}),
-                   ("reg24", {"CDB_GRAM_REG": "1", "CDB_GRAM_R": "24"}), ("reg16", {"CDB_GRAM_REG": "1", "CDB_GRAM_R": "16"})):
-    for k in ("CDB_GRAM_REG", "CDB_GRAM_R"):
+for label, env in (("stream", {"CDB_GRAM_TMA": "0"}), ("tma", {})):
+    for k in ("CDB_GRAM_REG", "CDB_GRAM_R", "CDB_GRAM_TMA"):
         os.environ.pop(k, None)
     os.environ.update(env)
     ol, oh = outs(k1), outs(w.k)
@@ -41,6 +40,7 @@ for label, r in res.items():
     same_sel = (r["sel"] == base["sel"]).all(axis=1).mean()
     nz = base["alpha"] != 0
     rel = np.abs(r["alpha"] - base["alpha"])[nz] / np.abs(base["alpha"][nz])
+    print(f"{label}: bitwise equal sel/alpha/rnorm: {(r['sel']==base['sel']).all()} {(r['alpha']==base['alpha']).all()} {(r['rnorm']==base['rnorm']).all()}")
     print(f"{label}: rows with identical sel {same_sel:.5f}, counts equal {(r['counts']==base['counts']).mean():.5f}, "
           f"scans equal {(r['scans']==base['scans']).mean():.5f}, coef max rel diff (same-sel rows) "
           f"{np.max(np.abs(r['alpha']-base['alpha'])[(r['sel']==base['sel']).all(axis=1)]) if same_sel>0 else -1:.3e}, "
