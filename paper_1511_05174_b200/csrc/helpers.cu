@@ -1,6 +1,7 @@
 // Small memory-bound kernels around the OMP engines.
 #include <cuda_bf16.h>
 
+#include <cstdint>
 #include "common.cuh"
 #include "engines.h"
 
@@ -139,6 +140,30 @@ __global__ void __launch_bounds__(256) downsample_direct_kernel(
       }
     }
     if (!eps_low) continue;
+    if (tps % 32 == 0) {
+      // warp butterflies, then the warps of a signal in order (fixed order:
+      // deterministic; a serial 256-term sum by one thread left the CTA
+      // waiting at the barrier)
+      yy = warp_sum(yy);
+      yl = warp_sum(yl);
+      const int lane = tid & 31, warp = tid >> 5, wps = tps / 32;
+      if (lane == 0) {
+        r_yy[warp] = yy;
+        r_yl[warp] = yl;
+      }
+      __syncthreads();
+      if (tid < spi && s0 + tid < p) {
+        double a = 0.0, b = 0.0;
+        for (int q = tid * wps; q < (tid + 1) * wps; q++) {
+          a += r_yy[q];
+          b += r_yl[q];
+        }
+        eps_fine[s0 + tid] = rel * sqrt(a);
+        eps_low[s0 + tid] = rel * sqrt(b);
+      }
+      __syncthreads();
+      continue;
+    }
     r_yy[tid] = yy;
     r_yl[tid] = yl;
     __syncthreads();
@@ -208,6 +233,38 @@ __global__ void sort_blocks_kernel(const int64_t *__restrict__ sel, const int64_
     out[j] = v;
   }
   for (int64_t i = nb; i < k1; i++) out[i] = 0;
+}
+
+// Warp per signal (k1 <= 64): the coarse support ids are distinct, so each
+// value's output slot is its rank (the count of smaller ids), found against
+// all nb values broadcast by shuffles; the row is read and written coalesced
+// (the thread-per-signal insertion sort above walks global memory k1^2 / 2
+// times).
+__global__ void __launch_bounds__(256) sort_blocks_warp_kernel(const int64_t *__restrict__ sel,
+                                                               const int64_t *__restrict__ cnt,
+                                                               int64_t p, int64_t k1,
+                                                               int64_t *__restrict__ blocks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= p) return;
+  const int nb = (int)cnt[s];
+  const int64_t *in = sel + s * k1;
+  int64_t *out = blocks + s * k1;
+  const int64_t v0 = lane < nb ? in[lane] : INT64_MAX, v1 = lane + 32 < nb ? in[lane + 32] : INT64_MAX;
+  int r0 = 0, r1 = 0;
+  for (int q = 0; q < nb && q < 32; q++) {
+    const int64_t u = __shfl_sync(CDB_FULL_MASK, v0, q);
+    r0 += u < v0;
+    r1 += u < v1;
+  }
+  for (int q = 32; q < nb; q++) {
+    const int64_t u = __shfl_sync(CDB_FULL_MASK, v1, q - 32);
+    r0 += u < v0;
+    r1 += u < v1;
+  }
+  if (lane < nb) out[r0] = v0;
+  if (lane + 32 < nb) out[r1] = v1;
+  for (int i = nb + lane; i < k1; i += 32) out[i] = 0;
 }
 
 // G = D D^T in fp64 (T x T), 64x64 tiles, 16x16 threads with 4x4 outputs.
@@ -965,7 +1022,11 @@ cudaError_t launch_sort_blocks(const int64_t *low_sel, const int64_t *low_count,
                                int64_t k1, int64_t *blocks, cudaStream_t stream) {
   ProfScope _ps("sort_blocks", stream);
   if (p <= 0) return cudaSuccess;
-  sort_blocks_kernel<<<blocks_for(p, 128), 128, 0, stream>>>(low_sel, low_count, p, k1, blocks);
+  if (k1 <= 64)
+    sort_blocks_warp_kernel<<<(unsigned)((p * 32 + 255) / 256), 256, 0, stream>>>(low_sel, low_count,
+                                                                                 p, k1, blocks);
+  else
+    sort_blocks_kernel<<<blocks_for(p, 128), 128, 0, stream>>>(low_sel, low_count, p, k1, blocks);
   note_launch();
   return cudaGetLastError();
 }

@@ -1449,7 +1449,7 @@ __device__ __forceinline__ float4 ldg_nc_f4(const float4 *p) {
 // sum_l |x32_l d32_l - x_l d_l| + g (|y32| + sum_l |x32_l| |d32_l|), so
 //   |r~ - r| <= (u + g (1 + u)) |y| + (2.0001 u + g (1 + u)^2) sum_l |x_l| dmax.
 // Needs n == 4 * BT * V.
-template <typename YT, int BT, int V>
+template <typename YT, int BT, int V, int G>
 __global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys,
                                                         const float *__restrict__ d32, int64_t p,
                                                         int64_t n, int64_t n_pad, int64_t kw,
@@ -1485,7 +1485,6 @@ __global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys
     }
     // software-pipelined over groups of G rows: the next group's loads are
     // issued before the current group's FMAs (G * V 16-byte loads in flight)
-    constexpr int G = 8;
     int l = 0;
     if (kd >= G) {
       float4 cur[G][V];
@@ -2360,15 +2359,20 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       // fp32 vectorised operand build when n = 4 * BT * V (CDB_RESID_F32=0: fp64 kernel)
       static const bool f32_ok = !(getenv("CDB_RESID_F32") && atoi(getenv("CDB_RESID_F32")) == 0);
       const size_t xs32 = 16 * (size_t)kw;
-#define CDB_RESID32(BT_, V_)                                                                    \
+      static const int rg = getenv("CDB_RESID_G") ? atoi(getenv("CDB_RESID_G")) : 8;
+#define CDB_RESID32G(BT_, V_, G_)                                                               \
   if (a.ys_f32)                                                                                 \
-    resid_f32_kernel<float, BT_, V_><<<g, BT_, xs32, stream>>>(                                 \
+    resid_f32_kernel<float, BT_, V_, G_><<<g, BT_, xs32, stream>>>(                             \
         (const float *)a.ys, a.d32, p, n, n_pad, kw, a.dmax, st, a.out_sel, a.out_coef,         \
         a.out_count);                                                                           \
   else                                                                                          \
-    resid_f32_kernel<double, BT_, V_><<<g, BT_, xs32, stream>>>(                                \
+    resid_f32_kernel<double, BT_, V_, G_><<<g, BT_, xs32, stream>>>(                            \
         (const double *)a.ys, a.d32, p, n, n_pad, kw, a.dmax, st, a.out_sel, a.out_coef,        \
         a.out_count);
+#define CDB_RESID32(BT_, V_)                                                                    \
+  if (rg == 4) { CDB_RESID32G(BT_, V_, 4) }                                                     \
+  else if (rg == 6) { CDB_RESID32G(BT_, V_, 6) }                                                \
+  else { CDB_RESID32G(BT_, V_, 8) }
       bool done32 = false;
       if (f32_ok) {
         done32 = true;
@@ -2381,6 +2385,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         else done32 = false;
       }
 #undef CDB_RESID32
+#undef CDB_RESID32G
       if (!done32) {
 #define CDB_RESID(BT_)                                                                          \
   if (a.ys_f32)                                                                                 \
