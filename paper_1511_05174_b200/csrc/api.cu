@@ -424,6 +424,7 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   g.status = status.as<uint32_t>();
   g.tag = tag;
   g.alpha0_in = alpha0;
+  g.prefetch_runner = getenv("CDB_GRAM_PF") ? atoi(getenv("CDB_GRAM_PF")) : 0;
   DevBuf hwork;
   if (!h_smem) {  // streamed H: one L2-resident slot per persistent warp
     const cdb::GramStreamPlan pl = cdb::gram_stream_plan(max_cands, kw, d->n, alpha0 == nullptr,

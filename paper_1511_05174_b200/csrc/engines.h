@@ -96,6 +96,7 @@ struct GramArgs {
   double *hwork;         // optional global H storage when it does not fit smem
   const char *tag;       // profiler name
   const double *alpha0_in;  // optional precomputed <d_{C_j}, y> (P x max_cands)
+  int prefetch_runner;      // CTA kernel: L2-prefetch the runner-up's Gram slice
 };
 // Shared-memory bytes per warp of the Gram engine (H in smem or global), and
 // the doubles of one signal's H (global scratch when it does not fit smem).

@@ -77,6 +77,27 @@ inline bool gram_stream_tmem(int wpb) {
   return wpb <= 4 && v && atoi(v) != 0;
 }
 
+// sum_i y_i^2 over this thread's share (i = tid, tid + nt, ...) with eight
+// loads in flight: the per-signal prologue otherwise waits one HBM round trip
+// per element (4096 / 128 = 32 of them per thread for cfg 4).
+template <typename YT>
+__device__ __forceinline__ double row_sumsq(const YT *__restrict__ y, int n, int tid, int nt) {
+  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int i = tid;
+  for (; i + 7 * nt < n; i += 8 * nt) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) v[u] = (double)__ldg(y + i + u * nt);
+#pragma unroll
+    for (int u = 0; u < 8; u++) s[u] = fma(v[u], v[u], s[u]);
+  }
+  for (; i < n; i += nt) {
+    const double v = (double)__ldg(y + i);
+    s[0] = fma(v, v, s[0]);
+  }
+  return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+}
+
 // alpha0_j = <d_{C_j}, y> for every candidate: the warp streams 8 atom rows
 // at a time with coalesced loads (lane i reads element i of each row) and
 // reduces the 8 partial sums across the warp.
@@ -488,13 +509,27 @@ __device__ void back_sub_rows(const double *hs, const double *hg, int nr, int st
   const double *h0 = (lane < nr ? hs : hg) + (int64_t)lane * stride;
   const double *h1 = (lane + 32 < nr ? hs : hg) + (int64_t)(lane + 32) * stride;
   double acc0 = 0.0, acc1 = 0.0;
-  for (int l = kd - 1; l >= 0; l--) {
-    const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
-    const double xl = (zv[l] - accl) * iv[l];
-    if (lane == 0) xv[l] = xl;
-    const int sl = pj[l];
-    if (lane < l) acc0 = fma(h0[sl], xl, acc0);
-    if (lane + 32 < l) acc1 = fma(h1[sl], xl, acc1);
+  // steps in blocks of 8: the block's R entries (L2 for rows >= nr) are loaded
+  // before its dependent chain, so each block waits for one round trip, not 8
+  for (int l0 = kd - 1; l0 >= 0; l0 -= 8) {
+    double r0[8], r1[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int l = l0 - u;
+      const int sl = l >= 0 ? pj[l] : 0;
+      r0[u] = l >= 0 && lane < l ? h0[sl] : 0.0;
+      r1[u] = l >= 0 && lane + 32 < l ? h1[sl] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int l = l0 - u;
+      if (l < 0) break;
+      const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
+      const double xl = (zv[l] - accl) * iv[l];
+      if (lane == 0) xv[l] = xl;
+      if (lane < l) acc0 = fma(r0[u], xl, acc0);
+      if (lane + 32 < l) acc1 = fma(r1[u], xl, acc1);
+    }
   }
   __syncwarp();
 }
@@ -535,11 +570,7 @@ __global__ void __launch_bounds__(128) gram_cta_kernel(GramArgs a, const YT *__r
       cid[c] = j < S ? (int)cs.id(p, j) : 0;
       if (j >= S) tk |= 1u << c;
     }
-    double yy = 0.0;
-    for (int i = tid; i < n; i += NT) {
-      const double v = (double)yg[i];
-      yy = fma(v, v, yy);
-    }
+    double yy = row_sumsq(yg, n, tid, NT);
     yy = warp_sum(yy);
     if (lane == 0) red[warp] = yy;
     __syncthreads();
@@ -613,6 +644,23 @@ __global__ void __launch_bounds__(128) gram_cta_kernel(GramArgs a, const YT *__r
         if (!(gm > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
         const int bestj = (int)gj;
         if (tid == bestj / CPT) tk |= 1u << (bestj % CPT);
+        if (a.prefetch_runner) {
+          // the best other warp's candidate often wins the next iteration: pull
+          // its Gram row slice toward L2 now (the next gather then misses less)
+          double g2 = -1.0;
+          int64_t n2 = -1;
+#pragma unroll
+          for (int w = 0; w < NW; w++) {
+            const double mw = xb[(par * NW + w) * 2];
+            const int64_t jw = xi[(par * NW + w) * 2];
+            if (jw != gj && mw > g2) {
+              g2 = mw;
+              n2 = xi[(par * NW + w) * 2 + 1];
+            }
+          }
+          if (n2 >= 0 && g2 > 0.0 && tid * CPT < S)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.gram + n2 * T + cid[0]));
+        }
         // ---- Gram row slice, H sweep
         // the slice (an HBM gather) lands in its own registers and is added
         // after the sweep, so its latency overlaps the sweep
@@ -852,11 +900,7 @@ __global__ void __launch_bounds__(128) gram_tma_kernel(GramArgs a, const YT *__r
       cid[c] = j < S ? (int)cs.id(p, j) : 0;
       if (j >= S) tk |= 1u << c;
     }
-    double yy = 0.0;
-    for (int i = tid; i < n; i += NT) {
-      const double v = (double)yg[i];
-      yy = fma(v, v, yy);
-    }
+    double yy = row_sumsq(yg, n, tid, NT);
     yy = warp_sum(yy);
     if (lane == 0) red[warp] = yy;
     __syncthreads();
@@ -1150,13 +1194,25 @@ __device__ __forceinline__ void file_col(double *rm, int kw, int l, const double
 __device__ __forceinline__ void back_sub_cols(const double *rm, int kw, int kd, const double *zv,
                                               const double *iv, double *xv, int lane) {
   double acc0 = 0.0, acc1 = 0.0;
-  for (int l = kd - 1; l >= 0; l--) {
-    const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
-    const double xl = (zv[l] - accl) * iv[l];
-    if (lane == 0) xv[l] = xl;
-    const double *col = rm + (int64_t)l * kw;
-    if (lane < l) acc0 = fma(col[lane], xl, acc0);
-    if (lane + 32 < l) acc1 = fma(col[lane + 32], xl, acc1);
+  for (int l0 = kd - 1; l0 >= 0; l0 -= 8) {  // a block's columns loaded ahead of its chain
+    double r0[8], r1[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int l = l0 - u;
+      const double *col = rm + (int64_t)(l >= 0 ? l : 0) * kw;
+      r0[u] = l >= 0 && lane < l ? col[lane] : 0.0;
+      r1[u] = l >= 0 && lane + 32 < l ? col[lane + 32] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int l = l0 - u;
+      if (l < 0) break;
+      const double accl = __shfl_sync(CDB_FULL_MASK, l < 32 ? acc0 : acc1, l & 31);
+      const double xl = (zv[l] - accl) * iv[l];
+      if (lane == 0) xv[l] = xl;
+      if (lane < l) acc0 = fma(r0[u], xl, acc0);
+      if (lane + 32 < l) acc1 = fma(r1[u], xl, acc1);
+    }
   }
   __syncwarp();
 }
@@ -1201,12 +1257,7 @@ __global__ void __launch_bounds__(512, 1) gram_reg_kernel(GramArgs a, const YT *
     const int k_max = (int)cs.budget(p, a.k_max, n);
     const bool valid = t < S;
     const int64_t cid = valid ? cs.id(p, t) : 0;
-    double yy = 0.0;
-    for (int i = t; i < n; i += NT) {
-      const double v = (double)yg[i];
-      yy = fma(v, v, yy);
-    }
-    yy = cta_sum(yy);
+    double yy = cta_sum(row_sumsq(yg, n, t, NT));
     const double ynorm = sqrt(yy);  // early exit |y| <= tol (_kernels.py:71-78)
     const double tol = a.eps[p];
     int kdone = 0;
@@ -1378,6 +1429,290 @@ __global__ void __launch_bounds__(512, 1) gram_reg_kernel(GramArgs a, const YT *
   }
 }
 
+// Two candidates per thread (256 threads, 8 warps: per-candidate overhead
+// and the w broadcasts halve, the CTA barrier spans 8 warps): thread t owns
+// candidates 2t and 2t + 1 -- one 16-byte shared-memory access per H row, one
+// 16-byte Gram load per iteration for Q even.  Same arithmetic and order per
+// candidate as gram_reg_kernel (row stride 512 in both).
+template <int R>
+__device__ __forceinline__ void load_block2(double (&h0)[R], double (&h1)[R], int b, const double *st) {
+#pragma unroll
+  for (int bb = 0; bb < R / 8; bb++) {
+    if (bb == b) {
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const double2 v = *(const double2 *)(st + u * 512);
+        h0[8 * bb + u] = v.x;
+        h1[8 * bb + u] = v.y;
+      }
+    }
+  }
+}
+template <int R>
+__device__ __forceinline__ void put_regs_sel(double *dst, const double (&h0)[R], const double (&h1)[R],
+                                             bool second, int kb) {
+#pragma unroll
+  for (int b = 0; b < R / 8; b++) {
+    if (8 * b + 8 <= kb) {
+#pragma unroll
+      for (int u = 0; u < 8; u += 2)
+        *(double2 *)(dst + 8 * b + u) =
+            second ? make_double2(h1[8 * b + u], h1[8 * b + u + 1]) : make_double2(h0[8 * b + u], h0[8 * b + u + 1]);
+    }
+  }
+}
+
+template <typename YT, int R>
+__global__ void __launch_bounds__(256, 1) gram_reg2_kernel(GramArgs a, const YT *__restrict__ ys) {
+  constexpr int NT = 256, NW = NT / 32, NC = 512;
+  static_assert(R % 8 == 0, "register rows come in blocks of 8");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int n = (int)a.n, kw = (int)a.k_width, smax = (int)a.max_cands;
+  const int64_t T = a.t;
+  const Cands cs = a.cands;
+  const int nsr = kw > R ? kw - R : 0;
+  constexpr int SL = 6 + R;
+  double *hsm = (double *)smem_raw;                 // nsr x NC; thread t owns entries 2t, 2t + 1
+  double *stg = hsm;                                // staging rows of the open register block
+  double *slots = hsm + (int64_t)(nsr > 8 ? nsr : 8) * NC;  // [2][NW][SL]
+  double *rm = a.hwork + (int64_t)blockIdx.x * kw * kw;
+  double *zv = slots + 2 * NW * SL;
+  double *iv = zv + kw;
+  double *xv = iv + kw;
+  int64_t *sup = (int64_t *)(xv + kw);
+  double *red = (double *)(sup + kw);
+  auto cta_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) s += red[w];
+    return s;
+  };
+  const int j0 = 2 * t;
+  const bool pairs = cs.mode == 2 && (cs.q & 1) == 0;  // 2t, 2t + 1 adjacent atoms
+
+  for (int64_t local = blockIdx.x; local < a.p; local += gridDim.x) {
+    const int64_t p = a.p_offset + local;
+    const YT *yg = ys + p * a.ys_stride;
+    const int S = (int)cs.count(p);
+    const int k_max = (int)cs.budget(p, a.k_max, n);
+    const bool va = j0 < S, vb = j0 + 1 < S;
+    const int64_t cid0 = va ? cs.id(p, j0) : 0, cid1 = vb ? cs.id(p, j0 + 1) : 0;
+    double yy = cta_sum(row_sumsq(yg, n, t, NT));
+    const double ynorm = sqrt(yy);  // early exit |y| <= tol (_kernels.py:71-78)
+    const double tol = a.eps[p];
+    int kdone = 0;
+    int64_t scans = 0;
+    double rnorm = ynorm, rn2_final = 0.0;
+    bool delegate = false;
+    double h0[R], h1[R];
+    int pick0 = -1, pick1 = -1;
+    if (!(ynorm <= tol) && k_max > 0) {
+#pragma unroll
+      for (int i = 0; i < R; i++) h0[i] = h1[i] = 0.0;
+      double c0 = va ? a.alpha0_in[p * smax + j0] : 0.0, c1 = vb ? a.alpha0_in[p * smax + j0 + 1] : 0.0;
+      const double g00 = va ? __ldg(a.gram + cid0 * T + cid0) : 1.0;
+      const double g11 = vb ? __ldg(a.gram + cid1 * T + cid1) : 1.0;
+      double s0 = 0.0, s1 = 0.0;
+      bool tk0 = !va, tk1 = !vb;
+      double rn2 = yy;
+      const double tol2 = tol * tol, band = 1e-12 * yy;
+      int k = 0;
+      for (;;) {
+      bool check = false;
+      for (; k < k_max; k++) {
+        rn2_final = rn2;
+        scans += S - k;
+        const int par = k & 1;
+        double *sbase = slots + par * NW * SL;
+        // ---- thread best of two (lower index on ties), warp arg-max, publication
+        const double a_ = tk0 ? 0.0 : fabs(c0), b_ = tk1 ? 0.0 : fabs(c1);
+        const bool sec = b_ > a_;
+        const double v = sec ? b_ : a_;
+        const unsigned jt = (unsigned)(j0 + (sec ? 1 : 0));
+        const double m = warp_max_nonneg(v);
+        const unsigned wj = __reduce_min_sync(CDB_FULL_MASK, v == m ? jt : 0xffffffffu);
+        if (jt == wj) {
+          double *sl = sbase + warp * SL;
+          sl[0] = m;
+          sl[1] = sec ? c1 : c0;
+          sl[2] = sec ? g11 - s1 : g00 - s0;
+          sl[3] = sec ? g11 : g00;
+          ((int64_t *)sl)[4] = ((sec ? cid1 : cid0) << 16) | (int64_t)jt;
+          put_regs_sel<R>(sl + 6, h0, h1, sec, (k < R ? k : R) & ~7);
+        }
+        __syncthreads();
+        const double mw = lane < NW ? sbase[lane * SL] : 0.0;
+        const double gm = warp_max_nonneg(mw);
+        if (!(gm > 0.0)) break;  // nothing left, or best <= 0 (_kernels.py:104)
+        const int gw = __ffs(__ballot_sync(CDB_FULL_MASK, lane < NW && mw == gm)) - 1;
+        const double *ws = sbase + gw * SL;
+        const int64_t packed = ((const int64_t *)ws)[4];
+        const int bestj = (int)(packed & 0xffff);
+        const int64_t nid = packed >> 16;
+        double gA = 0.0, gB = 0.0;
+        if (pairs && vb) {
+          const double2 g2 = __ldg((const double2 *)(a.gram + nid * T + cid0));
+          gA = g2.x;
+          gB = g2.y;
+        } else {
+          gA = va ? __ldg(a.gram + nid * T + cid0) : 0.0;
+          gB = vb ? __ldg(a.gram + nid * T + cid1) : 0.0;
+        }
+        const double cj = ws[1], d2 = ws[2], gnn = ws[3];
+        const double *w = ws + 6;
+        // ---- sweep
+        const int kr = k < R ? k : R, kb = kr & ~7;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int b = 0; b < R / 8; b++) {
+          if (8 * b + 8 <= kb) {
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              const double2 wv = *(const double2 *)(w + 8 * b + u);
+              a0 = fma(wv.x, h0[8 * b + u], a0);
+              b0 = fma(wv.x, h1[8 * b + u], b0);
+              a1 = fma(wv.y, h0[8 * b + u + 1], a1);
+              b1 = fma(wv.y, h1[8 * b + u + 1], b1);
+            }
+          }
+        }
+        for (int i = kb; i < kr; i++) {
+          const double wi = stg[(i & 7) * NC + bestj];
+          const double2 hv = *(const double2 *)(stg + (i & 7) * NC + j0);
+          a0 = fma(wi, hv.x, a0);
+          b0 = fma(wi, hv.y, b0);
+        }
+        {
+          int i = R;
+          for (; i + 1 < k; i += 2) {
+            const int64_t o = (int64_t)(i - R) * NC;
+            const double w0 = hsm[o + bestj], w1 = hsm[o + NC + bestj];
+            const double2 x0 = *(const double2 *)(hsm + o + j0), x1 = *(const double2 *)(hsm + o + NC + j0);
+            a0 = fma(w0, x0.x, a0);
+            b0 = fma(w0, x0.y, b0);
+            a1 = fma(w1, x1.x, a1);
+            b1 = fma(w1, x1.y, b1);
+          }
+          if (i < k) {
+            const int64_t o = (int64_t)(i - R) * NC;
+            const double w0 = hsm[o + bestj];
+            const double2 x0 = *(const double2 *)(hsm + o + j0);
+            a0 = fma(w0, x0.x, a0);
+            b0 = fma(w0, x0.y, b0);
+          }
+        }
+        if (!(d2 > GRAM_DELEGATE_D2 * gnn)) {  // near rank deficiency: exact engine decides
+          delegate = true;
+          break;
+        }
+        const double inv_d = rsqrt(d2);
+        const double zk = cj * inv_d;  // q_k^T y = <d_{j*}, r> / d
+        const double hA = va ? (gA - (a0 + a1)) * inv_d : 0.0;
+        const double hB = vb ? (gB - (b0 + b1)) * inv_d : 0.0;
+        if ((bestj >> 1) == t) {
+          if (bestj & 1) {
+            tk1 = true;
+            pick1 = k;
+          } else {
+            tk0 = true;
+            pick0 = k;
+          }
+          zv[k] = zk;
+          iv[k] = inv_d;
+          sup[k] = nid;
+        }
+        if (k < R) {
+          *(double2 *)(stg + (k & 7) * NC + j0) = make_double2(hA, hB);
+          if ((k & 7) == 7) load_block2<R>(h0, h1, k >> 3, stg + j0);
+        } else {
+          *(double2 *)(hsm + (int64_t)(k - R) * NC + j0) = make_double2(hA, hB);
+        }
+        c0 = fma(-zk, hA, c0);
+        c1 = fma(-zk, hB, c1);
+        s0 = fma(hA, hA, s0);
+        s1 = fma(hB, hB, s1);
+        rn2 -= zk * zk;
+        rn2_final = rn2;
+        kdone = k + 1;
+        const double gap = rn2 - tol2;  // stop test (_kernels.py:156)
+        if (gap > band) continue;
+        if (gap < -band) break;
+        check = true;
+        break;
+      }
+      if (!check) break;
+      file_col<R>(rm, kw, pick0, h0, stg + j0, hsm + j0, kdone);
+      file_col<R>(rm, kw, pick1, h1, stg + j0 + 1, hsm + j0 + 1, kdone);
+      __syncthreads();
+      if (warp == 0) back_sub_cols(rm, kw, kdone, zv, iv, xv, lane);
+      __syncthreads();
+      double rr = 0.0;
+      for (int i = t; i < n; i += NT) {
+        double ri = (double)yg[i];
+        for (int l = 0; l < kdone; l++) ri = fma(-xv[l], a.d64[sup[l] * n + i], ri);
+        rr = fma(ri, ri, rr);
+      }
+      rr = cta_sum(rr);
+      if (sqrt(rr) <= tol) break;
+      k++;
+      }
+    }
+    __syncthreads();
+    if (delegate) {
+      if (t == 0) a.status[p] |= ST_DELEGATE;
+      __syncthreads();
+      continue;
+    }
+    file_col<R>(rm, kw, pick0, h0, stg + j0, hsm + j0, kdone);
+    file_col<R>(rm, kw, pick1, h1, stg + j0 + 1, hsm + j0 + 1, kdone);
+    __syncthreads();
+    if (warp == 0) back_sub_cols(rm, kw, kdone, zv, iv, xv, lane);
+    __syncthreads();
+    if (kdone > 0) {
+      if (rn2_final > 1e-6 * yy) {
+        rnorm = sqrt(rn2_final);
+      } else {
+        double rr = 0.0;
+        for (int i = t; i < n; i += NT) {
+          double ri = (double)yg[i];
+          for (int l = 0; l < kdone; l++) ri = fma(-xv[l], __ldg(a.d64 + sup[l] * n + i), ri);
+          rr = fma(ri, ri, rr);
+        }
+        rnorm = sqrt(cta_sum(rr));
+      }
+    }
+    int64_t *out_sel = a.out_sel + p * kw;
+    double *out_coef = a.out_coef + p * kw;
+    for (int j = t; j < kw; j += NT) {
+      out_sel[j] = j < kdone ? sup[j] : -1;
+      out_coef[j] = j < kdone ? xv[j] : 0.0;
+    }
+    if (t == 0) {
+      a.out_count[p] = kdone;
+      a.out_rnorm[p] = rnorm;
+      a.out_scans[p] = scans;
+      a.out_flag[p] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename YT, int R>
+cudaError_t go_reg2(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
+                    cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(gram_reg2_kernel<YT, R>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pl.per_warp_smem);
+  if (e != cudaSuccess) return e;
+  gram_reg2_kernel<YT, R><<<(unsigned)pl.warps, 256, pl.per_warp_smem, stream>>>(args, ys);
+  return cudaGetLastError();
+}
+
 template <typename YT, int R>
 cudaError_t go_reg(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
                    cudaStream_t stream) {
@@ -1392,6 +1727,11 @@ cudaError_t go_reg(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
 template <typename YT>
 cudaError_t go_reg_r(const GramArgs &args, const YT *ys, const GramStreamPlan &pl,
                      cudaStream_t stream) {
+  if (pl.cpt == 2) switch (pl.nr) {
+      case 16: return go_reg2<YT, 16>(args, ys, pl, stream);
+      case 24: return go_reg2<YT, 24>(args, ys, pl, stream);
+      case 32: return go_reg2<YT, 32>(args, ys, pl, stream);
+    }
   switch (pl.nr) {
     case 16: return go_reg<YT, 16>(args, ys, pl, stream);
     case 24: return go_reg<YT, 24>(args, ys, pl, stream);
@@ -1466,17 +1806,20 @@ int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_
 GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
                                 int max_smem_per_block, int num_sms) {
   GramStreamPlan pl{};
-  // on-chip H (gram_reg_kernel): one 512-thread CTA per SM, R register rows.
-  // Opt-in (CDB_GRAM_REG=1): measured on cfg 4 (65,536 signals) at 49.8 / 50.8 /
-  // 53.7 ms for R = 16 / 24 / 32 against 47.7 ms for the streamed CTA kernel --
-  // one signal per SM leaves the per-iteration chain (arg-max, barrier, Gram
-  // row load from HBM) exposed (ncu: issue 39%, stalls wait / short-scoreboard
-  // / barrier), which costs what the L2 row traffic it removes saved.
+  // on-chip H, one CTA per SM holding one signal's whole H: registers (R rows)
+  // + shared memory.  Default: gram_reg2_kernel (256 threads, two candidates
+  // per thread, R = 24): cfg 4 step 2, 131,072 signals: 87.8 ms against 93.8 ms
+  // for the streamed CTA kernel below (CDB_GRAM_REG=0) and 99.8 ms for
+  // gram_reg_kernel (one candidate per thread, CDB_GRAM_REG=1; R = 16 / 24 / 32:
+  // CDB_GRAM_R).  One signal per SM leaves its per-iteration chain (arg-max,
+  // barrier, Gram-row gather from HBM) exposed; what it saves is the L2 row
+  // traffic of the streamed kernel.
   const char *rv = getenv("CDB_GRAM_REG");
-  if (!stage_y && s <= 512 && kw <= 64 && rv && atoi(rv) != 0) {
-    int r = 16;
+  const int regmode = rv ? atoi(rv) : 2;
+  if (!stage_y && s <= 512 && kw <= 64 && regmode != 0) {
+    int r = regmode == 2 ? 24 : 16;
     if (const char *v = getenv("CDB_GRAM_R")) r = atoi(v);
-    if (r != 16 && r != 24 && r != 32) r = 16;
+    if (r != 16 && r != 24 && r != 32) r = regmode == 2 ? 24 : 16;
     const int64_t nsr = kw > r ? kw - r : 0;
     const int64_t sl = 6 + r;
     const int64_t dbl = (nsr > 8 ? nsr : 8) * 512 + 2 * 16 * sl + 4 * kw + 16;
@@ -1485,7 +1828,8 @@ GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
     if (pl.ok) {
       pl.reg = true;
       pl.cta = true;
-      pl.wpb = 16;
+      pl.cpt = regmode == 2 ? 2 : 1;
+      pl.wpb = pl.cpt == 2 ? 8 : 16;
       pl.nr = r;
       pl.warps = num_sms;  // CTAs
       pl.slot_doubles = kw * kw;  // the CTA's R matrix
