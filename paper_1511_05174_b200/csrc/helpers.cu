@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(128) alpha0_mma_l1_kernel(
     double c[CT][2];
 #pragma unroll
     for (int ct = 0; ct < CT; ct++) c[ct][0] = c[ct][1] = 0.0;
-#pragma unroll 4
+#pragma unroll 8
     for (int t = 0; t < nt; t++) {
       double yv[4];
       if constexpr (sizeof(YT) == 4) {
