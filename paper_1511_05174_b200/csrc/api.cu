@@ -346,7 +346,9 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
                    Outs &o, int engine, const DevInfo &di, cudaStream_t st,
                    const char *tag = nullptr, const double *alpha0 = nullptr) {
   if (p <= 0) return CDB_OK;
-  const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit;
+  static const bool force_onchip = getenv("CDB_GRAM_ONCHIP") && atoi(getenv("CDB_GRAM_ONCHIP")) != 0;
+  const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit &&
+                      !(force_onchip && alpha0 && max_cands > 128);
   const bool resident = cdb::resident_fits(d->n, d->t, kw, max_cands, di.smem_optin);
   if (engine == CDB_ENGINE_RESIDENT && !resident) engine = CDB_ENGINE_AUTO;  // a preference
   const bool gram_small = gram_preferred(d, max_cands, kw);
