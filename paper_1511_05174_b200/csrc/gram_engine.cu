@@ -1567,17 +1567,24 @@ __global__ void __launch_bounds__(256, 1) gram_reg2_kernel(GramArgs a, const YT 
         const double *w = ws + 6;
         // ---- sweep
         const int kr = k < R ? k : R, kb = kr & ~7;
+        // 8 fma chains (4 per candidate): the sweep is bound by fp64 latency
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        double a2 = 0.0, a3 = 0.0, b2 = 0.0, b3 = 0.0;
 #pragma unroll
         for (int b = 0; b < R / 8; b++) {
           if (8 * b + 8 <= kb) {
 #pragma unroll
-            for (int u = 0; u < 8; u += 2) {
+            for (int u = 0; u < 8; u += 4) {
               const double2 wv = *(const double2 *)(w + 8 * b + u);
+              const double2 wx = *(const double2 *)(w + 8 * b + u + 2);
               a0 = fma(wv.x, h0[8 * b + u], a0);
               b0 = fma(wv.x, h1[8 * b + u], b0);
               a1 = fma(wv.y, h0[8 * b + u + 1], a1);
               b1 = fma(wv.y, h1[8 * b + u + 1], b1);
+              a2 = fma(wx.x, h0[8 * b + u + 2], a2);
+              b2 = fma(wx.x, h1[8 * b + u + 2], b2);
+              a3 = fma(wx.y, h0[8 * b + u + 3], a3);
+              b3 = fma(wx.y, h1[8 * b + u + 3], b3);
             }
           }
         }
@@ -1589,6 +1596,21 @@ __global__ void __launch_bounds__(256, 1) gram_reg2_kernel(GramArgs a, const YT 
         }
         {
           int i = R;
+          for (; i + 3 < k; i += 4) {
+            const int64_t o = (int64_t)(i - R) * NC;
+            const double w0 = hsm[o + bestj], w1 = hsm[o + NC + bestj];
+            const double w2 = hsm[o + 2 * NC + bestj], w3 = hsm[o + 3 * NC + bestj];
+            const double2 x0 = *(const double2 *)(hsm + o + j0), x1 = *(const double2 *)(hsm + o + NC + j0);
+            const double2 x2 = *(const double2 *)(hsm + o + 2 * NC + j0), x3 = *(const double2 *)(hsm + o + 3 * NC + j0);
+            a0 = fma(w0, x0.x, a0);
+            b0 = fma(w0, x0.y, b0);
+            a1 = fma(w1, x1.x, a1);
+            b1 = fma(w1, x1.y, b1);
+            a2 = fma(w2, x2.x, a2);
+            b2 = fma(w2, x2.y, b2);
+            a3 = fma(w3, x3.x, a3);
+            b3 = fma(w3, x3.y, b3);
+          }
           for (; i + 1 < k; i += 2) {
             const int64_t o = (int64_t)(i - R) * NC;
             const double w0 = hsm[o + bestj], w1 = hsm[o + NC + bestj];
@@ -1612,8 +1634,8 @@ __global__ void __launch_bounds__(256, 1) gram_reg2_kernel(GramArgs a, const YT 
         }
         const double inv_d = rsqrt(d2);
         const double zk = cj * inv_d;  // q_k^T y = <d_{j*}, r> / d
-        const double hA = va ? (gA - (a0 + a1)) * inv_d : 0.0;
-        const double hB = vb ? (gB - (b0 + b1)) * inv_d : 0.0;
+        const double hA = va ? (gA - ((a0 + a1) + (a2 + a3))) * inv_d : 0.0;
+        const double hB = vb ? (gB - ((b0 + b1) + (b2 + b3))) * inv_d : 0.0;
         if ((bestj >> 1) == t) {
           if (bestj & 1) {
             tk1 = true;
