@@ -1179,6 +1179,19 @@ __global__ void __launch_bounds__(128, MB) ls_wide_kernel(
         for (int r = 0; r < KR; r++) g[r] = sv[r] >= 0 ? __ldg(gj + sv[r]) : 0.0;
         const double gjj = __ldg(gj + j);
         int i = lane;
+        if (n == 512) {  // cfg 4 step 1: all 16 atom loads of a lane in flight at once
+          double e[16];
+#pragma unroll
+          for (int q = 0; q < 16; q++) e[q] = __ldg(dj + lane + 32 * q);
+#pragma unroll
+          for (int q = 0; q < 16; q += 4) {
+            a0 = fma(e[q], (double)y[lane + 32 * q], a0);
+            a1 = fma(e[q + 1], (double)y[lane + 32 * (q + 1)], a1);
+            a2 = fma(e[q + 2], (double)y[lane + 32 * (q + 2)], a2);
+            a3 = fma(e[q + 3], (double)y[lane + 32 * (q + 3)], a3);
+          }
+          i = n;
+        }
         for (; i + 96 < n; i += 128) {
           const double e0 = __ldg(dj + i), e1 = __ldg(dj + i + 32), e2 = __ldg(dj + i + 64),
                        e3 = __ldg(dj + i + 96);
