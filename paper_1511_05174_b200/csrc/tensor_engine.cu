@@ -1476,15 +1476,31 @@ __global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys
   __shared__ double red[3][BT / 32];
   __shared__ double sxs;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the next signal's status, count and (thread l < kw) code entry are loaded
+  // one signal ahead, so a signal starts without three dependent round trips
+  auto meta = [&](int64_t s, uint32_t &stt, int &kd, double &x, int64_t &sel) {
+    stt = s < p ? st.status[s] : 0u;
+    kd = s < p ? (int)out_count[s] : 0;
+    x = s < p && tid < kw ? out_coef[s * kw + tid] : 0.0;
+    sel = s < p && tid < kw ? out_sel[s * kw + tid] : 0;
+  };
+  uint32_t n_st;
+  int n_kd;
+  double n_x;
+  int64_t n_sel;
+  meta(blockIdx.x, n_st, n_kd, n_x, n_sel);
   for (int64_t sig = blockIdx.x; sig < p; sig += gridDim.x) {
-    if (!(st.status[sig] & ST_RESID)) continue;  // uniform across the CTA
-    const int kd = (int)out_count[sig];
+    const uint32_t c_st = n_st;
+    const int kd = n_kd;
+    const double cx = n_x;
+    const int64_t csel = n_sel;
+    meta(sig + gridDim.x, n_st, n_kd, n_x, n_sel);
+    if (!(c_st & ST_RESID)) continue;  // uniform across the CTA
     double sx = 0.0;
-    for (int l = tid; l < kd; l += BT) {
-      const double x = out_coef[sig * kw + l];
-      xf[l] = (float)x;
-      rows[l] = d32 + out_sel[sig * kw + l] * n;
-      sx += fabs(x);
+    if (tid < kd) {  // kw <= BT (64 or 128 threads, K <= 64)
+      xf[tid] = (float)cx;
+      rows[tid] = d32 + csel * n;
+      sx = fabs(cx);
     }
     sx = warp_sum(sx);
     if (lane == 0) red[1][warp] = sx;
@@ -2387,7 +2403,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   else if (rg == 6) { CDB_RESID32G(BT_, V_, 6) }                                                \
   else { CDB_RESID32G(BT_, V_, 8) }
       bool done32 = false;
-      if (f32_ok) {
+      if (f32_ok && kw <= 64) {  // one code entry per thread (BT >= 64)
         done32 = true;
         // N = 4096 (cfg 4 full OMP) stays on the fp64 kernel: measured 1988 vs
         // 6287 ms per 250 k signals (register-bound) and 37% more exact rescans
