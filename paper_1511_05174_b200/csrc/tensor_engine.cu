@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                      const __grid_constant__ CUtensorMap tm_b, int64_t p, int64_t t,
                      int n_kchunks, int64_t m_tiles, const int *__restrict__ active,
                      int *__restrict__ cand_idx, float *__restrict__ cand_val,
-                     float *__restrict__ cand_drop) {
+                     float *__restrict__ cand_drop, int nsplit) {
   griddep_wait();  // the previous kernel's residuals and active count (PDL)
   griddep_launch();
   if (active && *active == 0) return;  // every signal already finished
@@ -101,6 +101,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                        ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t_tiles = (int)((t + BN - 1) / BN);
+  // work item = (signal tile mt, dictionary part q of nsplit): items of one
+  // signal tile are adjacent, so the CTAs in flight share few signal tiles
+  // (their A stays in L2) and stream the same dictionary parts together
+  const int tpq = (t_tiles + nsplit - 1) / nsplit;
+  const int64_t n_items = m_tiles * nsplit;
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tm_a);
@@ -127,7 +132,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t s = 0, ph = 0, aph = 0;
-      for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int64_t mt = item / nsplit;
+        const int tt0 = (int)(item % nsplit) * tpq, tt1 = tt0 + tpq < t_tiles ? tt0 + tpq : t_tiles;
         const int row0 = (int)(mt * BM);
         if constexpr (A_RES) {
           sm100::mbar_wait(&sm.aempty, aph ^ 1);
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               sm100::tma_load_2d(sm.a[kc][h], &tm_a, &sm.afull, kc * BK, row0 + h * BMH);
           aph ^= 1;
         }
-        for (int tt = 0; tt < t_tiles; tt++) {
+        for (int tt = tt0; tt < tt1; tt++) {
           for (int kc = 0; kc < n_kchunks; kc++) {
             sm100::mbar_wait(&sm.empty[s], ph ^ 1);
             if constexpr (A_RES) {
@@ -162,13 +169,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = sm100::idesc_bf16_f32(BMH, BN);
       uint32_t s = 0, ph = 0, acc = 0, acc_ph = 0, aph = 0;
-      for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int tt0 = (int)(item % nsplit) * tpq, tt1 = tt0 + tpq < t_tiles ? tt0 + tpq : t_tiles;
         if constexpr (A_RES) {
           sm100::mbar_wait(&sm.afull, aph);
           aph ^= 1;
           sm100::tc_fence_after();
         }
-        for (int tt = 0; tt < t_tiles; tt++) {
+        for (int tt = tt0; tt < tt1; tt++) {
           sm100::mbar_wait(&sm.tempty[acc], acc_ph ^ 1);
           sm100::tc_fence_after();
           for (int kc = 0; kc < n_kchunks; kc++) {
@@ -222,7 +230,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int i = 0; i < 64; i++) cid[i >> 5][i & 31] = opaque0 + (uint32_t)i;
     const uint32_t k63 = 63u + opaque0;  // kept in a register
-    for (int64_t mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int64_t mt = item / nsplit;
+      const int q = (int)(item % nsplit);
+      const int tt0 = q * tpq, tt1 = tt0 + tpq < t_tiles ? tt0 + tpq : t_tiles;
       float val[NCAND];
       int idx[NCAND];
       float dropped = -1.0f;
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         val[i] = -1.0f;
         idx[i] = -1;
       }
-      for (int tt = 0; tt < t_tiles; tt++) {
+      for (int tt = tt0; tt < tt1; tt++) {
         sm100::mbar_wait(&sm.tfull[acc], acc_ph);
         sm100::tc_fence_after();
         const uint32_t tbase = tmem + (acc * 2 + half) * BN + ((uint32_t)(quarter * 32) << 16);
@@ -294,13 +305,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       const int64_t grow = mt * BM + row;
-      if (grow < p) {
+      if (grow < p) {  // nsplit > 1: partial lists [p][nsplit][NCAND], merged by merge_cands
+        const int64_t slot = grow * nsplit + q;
 #pragma unroll
         for (int i = 0; i < NCAND; i++) {
-          cand_idx[grow * NCAND + i] = idx[i];
-          cand_val[grow * NCAND + i] = val[i];
+          cand_idx[slot * NCAND + i] = idx[i];
+          cand_val[slot * NCAND + i] = val[i];
         }
-        cand_drop[grow] = dropped;
+        cand_drop[slot] = dropped;
       }
     }
   }
@@ -310,6 +322,57 @@ __global__ void __launch_bounds__(THREADS, 1)
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, TMEM_COLS);
   }
+}
+
+// The nsplit partial top-8 lists of a signal (one per dictionary part) ->
+// its top-8 (by value, lower atom id on equal values) and `dropped` = the
+// largest value left out (the parts' own dropped values included): warp per
+// signal, lane = one partial candidate, its rank found against all 32.
+__global__ void __launch_bounds__(256) merge_cands_kernel(const int *__restrict__ pidx,
+                                                          const float *__restrict__ pval,
+                                                          const float *__restrict__ pdrop,
+                                                          int64_t p, int nsplit,
+                                                          const int *__restrict__ active,
+                                                          int *__restrict__ cand_idx,
+                                                          float *__restrict__ cand_val,
+                                                          float *__restrict__ cand_drop) {
+  griddep_wait();
+  griddep_launch();
+  if (active && *active == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t sig = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (sig >= p) return;
+  const int tot = nsplit * NCAND;  // <= 64: two partial candidates per lane
+  int j[2];
+  float v[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int e = lane + 32 * h;
+    j[h] = e < tot ? pidx[sig * tot + e] : -1;
+    v[h] = e < tot && j[h] >= 0 ? pval[sig * tot + e] : -1.0f;
+  }
+  int rank[2] = {0, 0};
+  for (int q = 0; q < 64; q++) {
+    const float vq = __shfl_sync(CDB_FULL_MASK, v[q >> 5], q & 31);
+    const int jq = __shfl_sync(CDB_FULL_MASK, j[q >> 5], q & 31);
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+      rank[h] += (vq > v[h]) || (vq == v[h] && (unsigned)jq < (unsigned)j[h]) ||
+                 (vq == v[h] && jq == j[h] && q < lane + 32 * h);
+  }
+  float drop = lane < nsplit ? pdrop[sig * nsplit + lane] : -1.0f;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    if (rank[h] < NCAND) {
+      cand_idx[sig * NCAND + rank[h]] = j[h];
+      cand_val[sig * NCAND + rank[h]] = v[h];
+    } else {
+      drop = fmaxf(drop, v[h]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) drop = fmaxf(drop, __shfl_xor_sync(CDB_FULL_MASK, drop, o));
+  if (lane == 0) cand_drop[sig] = drop;
 }
 
 __global__ void to_bf16_rows(const float *__restrict__ rows, int64_t p, int64_t n, int64_t n_pad,
@@ -2144,11 +2207,18 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols_pad, 
 
 }  // namespace
 
+// Full-dictionary scans that stream the signal operand (N_pad > the resident
+// limit: cfg 4 full OMP) split the dictionary into this many parts per signal
+// tile (CDB_CORR_SPLIT overrides; 1 = off): work items (tile, part), the parts'
+// top-8 lists merged by merge_cands_kernel.
+constexpr int kMaxCorrSplit = 8;
+
 int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw) {
   const int64_t n_pad = (n + BK - 1) / BK * BK;
   const int64_t p_pad = (p + BM - 1) / BM * BM;
   return p_pad * n_pad * 2 + p * kw * ((kw + 15) & ~int64_t(15)) * 8 + p * kw * 8 + p * 8 * 6 + p * NCAND * 8 + p * 4 +
-         p * 8 * 3 + p * (3 * 8 * RS_SPLIT + 4) + 4 * 4096 + 21 * 256;
+         p * 8 * 3 + p * (3 * 8 * RS_SPLIT + 4) + 4 * 4096 + 24 * 256 +
+         p * kMaxCorrSplit * (NCAND * 8 + 4);  // partial candidate lists of a split scan
 }
 
 cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
@@ -2180,6 +2250,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   st.cand_idx = cidx;
   st.cand_val = cval;
   st.cand_drop = cdrop;
+  int *pidx = (int *)take(p * kMaxCorrSplit * NCAND * 4);
+  float *pval = (float *)take(p * kMaxCorrSplit * NCAND * 4);
+  float *pdrop = (float *)take(p * kMaxCorrSplit * 4);
   st.active = (int *)take((a.k_max + 1) * 4);
   st.npending = (int *)take((a.k_max + 1) * 4);
   st.pending = (int64_t *)take(p * 8);
@@ -2224,7 +2297,14 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       cudaSuccess)
     return e;
   const int64_t m_tiles = p_pad / BM;
-  unsigned corr_grid = (unsigned)(m_tiles < a.num_sms ? m_tiles : a.num_sms);
+  int nsplit = 1;
+  if (!a_res && (t + BN - 1) / BN >= 32) nsplit = 4;  // 1 / 2 / 4 / 8: 708 / 593 / 482 / 488 ms (cfg 4 full, 65k)
+  if (const char *v = getenv("CDB_CORR_SPLIT")) {
+    const int q = atoi(v);
+    nsplit = q >= 1 && q <= kMaxCorrSplit ? q : nsplit;
+  }
+  const int64_t corr_items = m_tiles * nsplit;
+  unsigned corr_grid = (unsigned)(corr_items < a.num_sms ? corr_items : a.num_sms);
   if (const char *cap = getenv("CDB_CORR_GRID_CAP")) {
     const int c = atoi(cap);
     if (c > 0 && (unsigned)c < corr_grid) corr_grid = (unsigned)c;
@@ -2296,8 +2376,22 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     {
     ProfScope _ps("corr_topk", stream);
     auto kern = a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>;
-    e = launch_k(pdl, kern, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
-                 (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, cidx, cval, cdrop);
+    if (nsplit == 1) {
+      e = launch_k(pdl, kern, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
+                   (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, cidx, cval, cdrop,
+                   1);
+    } else {
+      e = launch_k(pdl, kern, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
+                   (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, pidx, pval, pdrop,
+                   nsplit);
+      if (e == cudaSuccess) {
+        note_launch();
+        e = launch_k(pdl, merge_cands_kernel, (unsigned)((p * 32 + 255) / 256), 256, 0, stream,
+                     (const int *)pidx, (const float *)pval, (const float *)pdrop, p, nsplit,
+                     it ? (const int *)(st.active + it - 1) : (const int *)nullptr, cidx, cval,
+                     cdrop);
+      }
+    }
     if (e != cudaSuccess) return e;
     }
     note_launch();
@@ -2494,7 +2588,7 @@ cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *
   if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
   kern<<<(unsigned)grid, THREADS, corr_smem, stream>>>(tm_a, tm_b, p, t, (int)(n_pad / BK),
                                                        m_tiles, nullptr, cand_idx, cand_val,
-                                                       cand_drop);
+                                                       cand_drop, 1);
   note_launch();
   e = cudaGetLastError();
   cudaFreeAsync(r16, stream);
