@@ -84,13 +84,15 @@ __device__ __forceinline__ void list_insert(float (&val)[NCAND], int (&idx)[NCAN
   }
 }
 
-template <bool A_RES>
+template <bool A_RES, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1)
     corr_topk_kernel(const __grid_constant__ CUtensorMap tm_a,
                      const __grid_constant__ CUtensorMap tm_b, int64_t p, int64_t t,
                      int n_kchunks, int64_t m_tiles, const int *__restrict__ active,
                      int *__restrict__ cand_idx, float *__restrict__ cand_val,
-                     float *__restrict__ cand_drop, int nsplit) {
+                     float *__restrict__ cand_drop, int nsplit_arg) {
+  // SPLIT = false compiles the single-part scan exactly as before the split
+  const int nsplit = SPLIT ? nsplit_arg : 1;
   griddep_wait();  // the previous kernel's residuals and active count (PDL)
   griddep_launch();
   if (active && *active == 0) return;  // every signal already finished
@@ -2292,7 +2294,11 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
 
   const bool a_res = n_pad / BK <= RES_KCHUNKS;
   const size_t corr_smem = (a_res ? sizeof(CorrSmemRes) : sizeof(CorrSmemStr)) + 1024;
-  if ((e = cudaFuncSetAttribute(a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>,
+  if ((e = cudaFuncSetAttribute(a_res ? corr_topk_kernel<true, false> : corr_topk_kernel<false, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)corr_smem)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(a_res ? corr_topk_kernel<true, true> : corr_topk_kernel<false, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)corr_smem)) !=
       cudaSuccess)
     return e;
@@ -2375,13 +2381,14 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   for (int it = 0; it < a.k_max; it++) {
     {
     ProfScope _ps("corr_topk", stream);
-    auto kern = a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>;
+    auto kern = a_res ? corr_topk_kernel<true, false> : corr_topk_kernel<false, false>;
     if (nsplit == 1) {
       e = launch_k(pdl, kern, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
                    (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, cidx, cval, cdrop,
                    1);
     } else {
-      e = launch_k(pdl, kern, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
+      auto kern_s = a_res ? corr_topk_kernel<true, true> : corr_topk_kernel<false, true>;
+      e = launch_k(pdl, kern_s, corr_grid, THREADS, corr_smem, stream, tm_a, tm_b, p, t,
                    (int)(n_pad / BK), m_tiles, it ? st.active + it - 1 : nullptr, pidx, pval, pdrop,
                    nsplit);
       if (e == cudaSuccess) {
@@ -2579,7 +2586,7 @@ cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *
     return cudaErrorInvalidValue;
   const bool a_res = n_pad / BK <= RES_KCHUNKS;
   const size_t corr_smem = (a_res ? sizeof(CorrSmemRes) : sizeof(CorrSmemStr)) + 1024;
-  auto kern = a_res ? corr_topk_kernel<true> : corr_topk_kernel<false>;
+  auto kern = a_res ? corr_topk_kernel<true, false> : corr_topk_kernel<false, false>;
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)corr_smem)) != cudaSuccess)
     return e;
