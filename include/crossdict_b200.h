@@ -221,6 +221,27 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
                                double *high_rnorm, int64_t *high_scans, uint8_t *high_flag,
                                int engine, float *step_ms, void *stream);
 
+/*
+ * Batched zero-tree OMP on the reference's own column batch.  Same as
+ * cdb_zero_tree_batch, but ys_cols is the N x P (M x P with phi_mode) batch
+ * exactly as crossscale.zero_tree_many_arrays receives it (crossscale.py:
+ * 235-283; element (i, p) at ys_cols[i * ld + p], ld >= P, fp64 or fp32 when
+ * ys_is_f32), in HOST memory (pageable is fine): the transpose the reference
+ * makes at pursuit.py:433 happens on the device.  Host threads stage slabs of
+ * columns into page-locked memory -- as fp32 when every value is fp32-exact
+ * (the engines then read fp32 rows) -- while earlier chunks compute.
+ * Outputs as cdb_zero_tree_batch (host or device).
+ */
+cdb_status cdb_zero_tree_batch_cols(const cdb_dictionary *low, const cdb_dictionary *high,
+                                    const int64_t *fine_shape, const int64_t *factors, int rank,
+                                    const void *ys_cols, int ys_is_f32, int64_t ld, int64_t p,
+                                    int64_t k1, int64_t k_high, double rel_tol, int phi_mode,
+                                    int64_t *low_sel, double *low_coef, int64_t *low_count,
+                                    double *low_rnorm, int64_t *low_scans, uint8_t *low_flag,
+                                    int64_t *high_sel, double *high_coef, int64_t *high_count,
+                                    double *high_rnorm, int64_t *high_scans, uint8_t *high_flag,
+                                    int engine, float *step_ms, void *stream);
+
 /* Device-time profiler: when enabled, every kernel launch is bracketed by
  * CUDA events on its own stream.  cdb_profile_enable(1) also clears the
  * records.  cdb_profile_read aggregates per kernel name: up to max_entries

@@ -158,25 +158,33 @@ def _phi_dims(model, phi):
     return phi.output_dim if hasattr(phi, "output_dim") else np.asarray(phi).shape[0]
 
 
-def _solve(model, ys_rows, phi):
-    """Device two-step solve of signal rows; returns (low, high, timings)."""
-    p_all = ys_rows.shape[0]
+def _solve(model, ys_rows, phi, ys_cols=None):
+    """Device two-step solve of signal rows (or, with ``ys_cols``, of the
+    N x P column batch itself, transposed on the device); returns
+    (low, high, timings)."""
     rel = _pursuit._rel_tol()
+    if ys_cols is not None:
+        m = ys_cols.shape[0]
+    else:
+        p_all = ys_rows.shape[0]
+        m = ys_rows.shape[1]
     if phi is None:
         dl = _dev.device_dictionary(model.d_low.atoms_t)
         dh = _dev.device_dictionary(model.d_high.atoms_t)
         k1 = model.k_low
-        lo, hi, ms = _dev.zero_tree_raw(dl, dh, model.scale.fine_shape, model.scale.factors,
-                                        ys_rows, p_all, k1, model.k_high, rel, False,
-                                        _pursuit.ENGINE)
+        fs, fa = model.scale.fine_shape, model.scale.factors
     else:
-        m = ys_rows.shape[1]
         e_low, e_high = _effective(model, phi)
         k1 = min(model.k_low, m, model.t_low)
         dl = _dev.device_dictionary(e_low)
         dh = _dev.device_dictionary(e_high)
-        lo, hi, ms = _dev.zero_tree_raw(dl, dh, None, None, ys_rows, p_all, k1, model.k_high,
-                                        rel, True, _pursuit.ENGINE)
+        fs = fa = None
+    if ys_cols is not None:
+        lo, hi, ms = _dev.zero_tree_cols_raw(dl, dh, fs, fa, ys_cols, k1, model.k_high, rel,
+                                             phi is not None, _pursuit.ENGINE)
+    else:
+        lo, hi, ms = _dev.zero_tree_raw(dl, dh, fs, fa, ys_rows, p_all, k1, model.k_high, rel,
+                                        phi is not None, _pursuit.ENGINE)
     low = _pursuit._make_batch(model.t_low, lo)
     high = _pursuit._make_batch(model.t_high, hi)
     return low, high, {"step1": float(ms[0]) * 1e-3, "step2": float(ms[1]) * 1e-3}
@@ -206,6 +214,8 @@ def zero_tree_many_arrays(model, ys, *, phi=None):
         return (mk(model.t_low, z, z.reshape(0, k1), np.zeros((0, k1)), np.zeros(0), z),
                 mk(model.t_high, z, z.reshape(0, model.k_high), np.zeros((0, model.k_high)),
                    np.zeros(0), z), {"step1": 0.0, "step2": 0.0})
+    if _dev.cols_layout(ys):  # large batch: the device transposes, host staging overlaps
+        return _solve(model, None, phi, ys_cols=ys)
     return _solve(model, _dev.rows_for_device(ys), phi)
 
 

@@ -8,6 +8,7 @@
 #include <string>
 #include <array>
 #include <chrono>
+#include <mutex>
 #include <thread>
 #include <vector>
 #include <algorithm>
@@ -658,6 +659,232 @@ cdb_status run_pipelined(int64_t p, std::vector<RowArr> &arrs, cudaStream_t st, 
     cudaEventDestroy(done[b]);
     cudaEventDestroy(out_done[b]);
   }
+  if (result != CDB_OK) return result;
+  for (cudaError_t e : {ce, e1, e2, e3})
+    if (e != cudaSuccess) return fail(CDB_ERR_CUDA, cudaGetErrorString(e));
+  return CDB_OK;
+}
+
+// ---------------------------------------------------------------- column batches
+// The reference hands its batch over as N x P columns (zero_tree_many_arrays'
+// and omp_many_arrays' `ys`) and transposes it to rows on the host
+// (pursuit.py:433) before the numba kernel.  run_pipelined_cols keeps that
+// layout across the boundary: host threads gather slabs of whole columns
+// (for each of the N coordinates one contiguous run of the slab's signals)
+// into page-locked staging -- as fp32 when every value is fp32-exact, which
+// halves the copy and lets the engines read fp32 rows -- a 2-D copy puts the
+// slab into the chunk's N x len device block, and the device transposes the
+// block into rows (cols_to_rows_kernel) right before the chunk's compute.
+// While chunk c computes, the host stages chunk c+1; chunk sizes grow
+// geometrically from a small first chunk (the only staging nothing hides).
+constexpr int kSlabs = 3;
+constexpr size_t kSlabBytes = size_t(64) << 20;
+
+struct PinnedSlabs {  // process-wide, allocated once
+  void *base = nullptr;
+  cudaError_t get(void **out) {
+    if (!base) {
+      cudaError_t e = cudaHostAlloc(&base, kSlabs * kSlabBytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) {
+        base = nullptr;
+        return e;
+      }
+    }
+    *out = base;
+    return cudaSuccess;
+  }
+};
+PinnedSlabs g_slabs;
+std::mutex g_slabs_mu;  // one column pipeline at a time uses the staging
+
+int stage_threads() {
+  static const int t = [] {
+    if (const char *v = getenv("CDB_STAGE_THREADS")) return std::max(1, atoi(v));
+    return (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+  }();
+  return t;
+}
+
+// Columns [a, a + s) of an n-row column batch (row stride ld elements) into
+// dst as an n x s block.  to_f32 (fp64 source only): converted to fp32;
+// returns false when some value is not fp32-exact (dst is then garbage).
+bool stage_cols(const void *src, bool src_f32, int64_t n, int64_t ld, int64_t a, int64_t s,
+                void *dst, bool to_f32) {
+  int threads = stage_threads();
+  if (threads > n) threads = (int)n;
+  std::atomic<bool> exact{true};
+  auto work = [&](int tid) {
+    const int64_t i0 = n * tid / threads, i1 = n * (tid + 1) / threads;
+    unsigned bad = 0;
+    for (int64_t i = i0; i < i1; i++) {
+      if (src_f32) {
+        memcpy((float *)dst + i * s, (const float *)src + i * ld + a, sizeof(float) * s);
+      } else if (!to_f32) {
+        memcpy((double *)dst + i * s, (const double *)src + i * ld + a, sizeof(double) * s);
+      } else {
+        const double *r = (const double *)src + i * ld + a;
+        float *o = (float *)dst + i * s;
+        for (int64_t j = 0; j < s; j++) {
+          const float f = (float)r[j];
+          o[j] = f;
+          bad |= (unsigned)((double)f != r[j]);  // NaN / out of range: inexact
+        }
+      }
+    }
+    if (bad) exact.store(false, std::memory_order_relaxed);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto &t : pool) t.join();
+  return exact.load();
+}
+
+// Chunk boundaries of a column pipeline: first chunk `first` signals, each
+// next one `grow` times larger up to `cap` (the host stages chunk c+1 while
+// chunk c computes, so a chunk may only be as much larger as the GPU is
+// slower than the staging: configs[4] on the GPU box, 16 threads stage
+// ~1.5 us per signal, the solve takes ~2 us); a short tail joins the
+// previous chunk.
+std::vector<int64_t> cols_bounds(int64_t p) {
+  static const int64_t first = getenv("CDB_COLS_FIRST") ? atoll(getenv("CDB_COLS_FIRST")) : 8192;
+  static const double grow = getenv("CDB_COLS_GROW") ? atof(getenv("CDB_COLS_GROW")) : 2.0;
+  static const int64_t cap = getenv("CDB_COLS_MAX") ? atoll(getenv("CDB_COLS_MAX")) : 131072;
+  std::vector<int64_t> b = {0};
+  double len = (double)std::max<int64_t>(1, first);
+  while (b.back() < p) {
+    int64_t l = std::min<int64_t>((int64_t)len, std::max<int64_t>(1, cap));
+    if (p - b.back() - l < l / 2) l = p - b.back();  // short tail: merge
+    b.push_back(b.back() + l);
+    len *= grow > 1.0 ? grow : 1.0;
+  }
+  return b;
+}
+
+// core(off, len, rows_dev, rows_f32, dv, stream): compute one chunk from the
+// device rows.  `arrs` are the other per-signal arrays (host memory), as in
+// run_pipelined.  *as_f32 in: try fp32 staging (fp64 source); out: the mode
+// used.  Returns CDB_ERR_FORMAT internally only for "retry in fp64" (a later
+// slab was not fp32-exact); the caller then re-runs with *as_f32 = false.
+constexpr cdb_status kRetryF64 = CDB_ERR_FORMAT;
+
+template <typename Core>
+cdb_status run_pipelined_cols(int64_t p, int64_t n, const void *cols, bool src_f32, int64_t ld,
+                              std::vector<RowArr> &arrs, cudaStream_t st, Core core,
+                              bool *as_f32) {
+  std::lock_guard<std::mutex> lock(g_slabs_mu);
+  void *slab_base = nullptr;
+  CDB_CUDA(g_slabs.get(&slab_base));
+  bool f32 = src_f32 || *as_f32;
+  const std::vector<int64_t> bd = cols_bounds(p);
+  const int64_t nch = (int64_t)bd.size() - 1;
+  int64_t chunk = 0;
+  for (int64_t i = 0; i < nch; i++) chunk = std::max(chunk, bd[i + 1] - bd[i]);
+  cudaStream_t cin = copy_stream(0), cout = copy_stream(1);
+  const size_t na = arrs.size();
+  // slab width: whole slabs of at most kSlabBytes at the fp64 staging size
+  const int64_t slab_sig = std::max<int64_t>(1, (int64_t)(kSlabBytes / (8 * (size_t)n)));
+  std::vector<DevBuf> bufs(2 * na);
+  DevBuf colbuf[2], rows;
+  const size_t es_max = 8;
+  for (int b = 0; b < 2; b++) {
+    CDB_CUDA(colbuf[b].alloc(es_max * n * chunk, st));
+    for (size_t a = 0; a < na; a++) CDB_CUDA(bufs[b * na + a].alloc(arrs[a].row_bytes * chunk, st));
+  }
+  CDB_CUDA(rows.alloc(es_max * n * chunk, st));
+  cudaEvent_t ready, slab_ev[kSlabs], in_ready[2], tdone[2], done[2], out_done[2];
+  CDB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  for (int r = 0; r < kSlabs; r++) CDB_CUDA(cudaEventCreateWithFlags(&slab_ev[r], cudaEventDisableTiming));
+  for (int b = 0; b < 2; b++) {
+    CDB_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
+    CDB_CUDA(cudaEventCreateWithFlags(&tdone[b], cudaEventDisableTiming));
+    CDB_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    CDB_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
+  }
+  CDB_CUDA(cudaEventRecord(ready, st));  // buffers allocated (stream-ordered)
+  CDB_CUDA(cudaStreamWaitEvent(cin, ready, 0));
+  CDB_CUDA(cudaStreamWaitEvent(cout, ready, 0));
+  static const bool trace = getenv("CDB_PIPE_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto ms_since = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start)
+        .count();
+  };
+  bool slab_used[kSlabs] = {false, false, false};
+  int64_t slab_no = 0;
+  cdb_status result = CDB_OK;
+  cudaError_t ce = cudaSuccess;
+  for (int64_t c = 0; c < nch && ce == cudaSuccess && result == CDB_OK; c++) {
+    const int b = (int)(c & 1);
+    const int64_t off = bd[c], len = bd[c + 1] - bd[c];
+    const size_t es = f32 ? 4 : 8;
+    if (c >= 2) {
+      // colbuf[b] was consumed by chunk c-2's transpose; the input buffers of
+      // set b by its compute, whose outputs must have left before reuse
+      if ((ce = cudaStreamWaitEvent(cin, tdone[b], 0)) != cudaSuccess) break;
+      if ((ce = cudaStreamWaitEvent(cin, out_done[b], 0)) != cudaSuccess) break;
+    }
+    for (int64_t a0 = 0; a0 < len && ce == cudaSuccess; a0 += slab_sig) {
+      const int64_t s = std::min(slab_sig, len - a0);
+      const int r = (int)(slab_no++ % kSlabs);
+      if (slab_used[r] && (ce = cudaEventSynchronize(slab_ev[r])) != cudaSuccess) break;
+      void *slab = (uint8_t *)slab_base + r * kSlabBytes;
+      bool exact = stage_cols(cols, src_f32, n, ld, off + a0, s, slab, f32 && !src_f32);
+      if (f32 && !src_f32 && !exact) {
+        if (c == 0 && a0 == 0) {  // first slab: decide fp64 for the whole call
+          f32 = false;
+          stage_cols(cols, false, n, ld, off + a0, s, slab, false);
+        } else {
+          result = kRetryF64;
+          break;
+        }
+      }
+      const size_t ess = f32 ? 4 : 8;
+      ce = cudaMemcpy2DAsync((uint8_t *)colbuf[b].ptr + a0 * ess, len * ess, slab, s * ess,
+                             s * ess, n, cudaMemcpyHostToDevice, cin);
+      if (ce == cudaSuccess) ce = cudaEventRecord(slab_ev[r], cin);
+      slab_used[r] = true;
+    }
+    if (ce != cudaSuccess || result != CDB_OK) break;
+    for (size_t a = 0; a < na && ce == cudaSuccess; a++) {
+      if (arrs[a].out || !arrs[a].host) continue;
+      ce = cudaMemcpyAsync(bufs[b * na + a].ptr, (const uint8_t *)arrs[a].host + off * arrs[a].row_bytes,
+                           len * arrs[a].row_bytes, cudaMemcpyHostToDevice, cin);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(in_ready[b], cin);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(st, in_ready[b], 0);
+    if (ce == cudaSuccess) ce = cdb::launch_cols_to_rows(colbuf[b].ptr, f32, n, len, rows.ptr, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(tdone[b], st);
+    if (ce != cudaSuccess) break;
+    (void)es;
+    std::vector<void *> dev(na);
+    for (size_t a = 0; a < na; a++) dev[a] = bufs[b * na + a].ptr;
+    result = core(off, len, rows.ptr, f32, dev, st);
+    if (result != CDB_OK) break;
+    if ((ce = cudaEventRecord(done[b], st)) != cudaSuccess) break;
+    if ((ce = cudaStreamWaitEvent(cout, done[b], 0)) != cudaSuccess) break;
+    for (size_t a = 0; a < na && ce == cudaSuccess; a++) {
+      if (!arrs[a].out || !arrs[a].host) continue;
+      ce = cudaMemcpyAsync((uint8_t *)arrs[a].host + off * arrs[a].row_bytes, dev[a],
+                           len * arrs[a].row_bytes, cudaMemcpyDeviceToHost, cout);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(out_done[b], cout);
+    if (trace)
+      fprintf(stderr, "[cols] chunk %lld len %lld (%s) staged+issued at %.1f ms\n", (long long)c,
+              (long long)len, f32 ? "f32" : "f64", ms_since());
+  }
+  cudaError_t e1 = cudaStreamSynchronize(cin), e2 = cudaStreamSynchronize(cout);
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  if (trace) fprintf(stderr, "[cols] all done at %.1f ms\n", ms_since());
+  cudaEventDestroy(ready);
+  for (int r = 0; r < kSlabs; r++) cudaEventDestroy(slab_ev[r]);
+  for (int b = 0; b < 2; b++) {
+    cudaEventDestroy(in_ready[b]);
+    cudaEventDestroy(tdone[b]);
+    cudaEventDestroy(done[b]);
+    cudaEventDestroy(out_done[b]);
+  }
+  *as_f32 = f32;
   if (result != CDB_OK) return result;
   for (cudaError_t e : {ce, e1, e2, e3})
     if (e != cudaSuccess) return fail(CDB_ERR_CUDA, cudaGetErrorString(e));
@@ -1499,6 +1726,88 @@ cdb_status cdb_zero_tree_batch(const cdb_dictionary *low, const cdb_dictionary *
   CDB_CUDA(cudaStreamSynchronize(st));
   tm.finish(step_ms);
   return CDB_OK;
+}
+
+cdb_status cdb_zero_tree_batch_cols(const cdb_dictionary *low, const cdb_dictionary *high,
+                                    const int64_t *fine_shape, const int64_t *factors, int rank,
+                                    const void *ys_cols, int ys_is_f32, int64_t ld, int64_t p,
+                                    int64_t k1, int64_t k_high, double rel_tol, int phi_mode,
+                                    int64_t *low_sel, double *low_coef, int64_t *low_count,
+                                    double *low_rnorm, int64_t *low_scans, uint8_t *low_flag,
+                                    int64_t *high_sel, double *high_coef, int64_t *high_count,
+                                    double *high_rnorm, int64_t *high_scans, uint8_t *high_flag,
+                                    int engine, float *step_ms, void *stream) {
+  if (!low || !high || p < 0 || k1 < 1 || k_high < 1 || high->t % low->t || ld < p)
+    return fail(CDB_ERR_ARG, "bad zero-tree arguments");
+  if (!phi_mode && (!fine_shape || !factors || rank < 1 || rank > 4))
+    return fail(CDB_ERR_ARG, "bad scale spec");
+  if (phi_mode && low->n != high->n) return fail(CDB_ERR_ARG, "Phi mode needs equal M");
+  if (p == 0) return CDB_OK;
+  if (!ys_cols || is_device_ptr(ys_cols)) return fail(CDB_ERR_ARG, "ys_cols must be host memory");
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  if ((s0 = check_device(low)) != CDB_OK || (s0 = check_device(high)) != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool src_f32 = ys_is_f32 != 0;
+  const int64_t n = high->n;
+  if (step_ms) step_ms[0] = step_ms[1] = 0.0f;
+  std::vector<RowArr> arrs = {
+      {low_sel, sizeof(int64_t) * k1, true}, {low_coef, sizeof(double) * k1, true},
+      {low_count, sizeof(int64_t), true}, {low_rnorm, sizeof(double), true},
+      {low_scans, sizeof(int64_t), true}, {low_flag, sizeof(uint8_t), true},
+      {high_sel, sizeof(int64_t) * k_high, true}, {high_coef, sizeof(double) * k_high, true},
+      {high_count, sizeof(int64_t), true}, {high_rnorm, sizeof(double), true},
+      {high_scans, sizeof(int64_t), true}, {high_flag, sizeof(uint8_t), true}};
+  for (const RowArr &a : arrs)
+    if (!a.host) return fail(CDB_ERR_ARG, "null output");
+  if (!all_host(arrs)) {
+    // device outputs: the whole column batch in one 2-D copy, transposed on
+    // the device, then the device-resident solve
+    const size_t es = src_f32 ? 4 : 8;
+    DevBuf cb, rb;
+    CDB_CUDA(cb.alloc(es * n * p, st));
+    CDB_CUDA(rb.alloc(es * n * p, st));
+    CDB_CUDA(cudaMemcpy2DAsync(cb.ptr, p * es, ys_cols, ld * es, p * es, n, cudaMemcpyHostToDevice,
+                               st));
+    CDB_CUDA(cdb::launch_cols_to_rows(cb.ptr, src_f32, n, p, rb.ptr, st));
+    Outs lo, hi;
+    CDB_CUDA(lo.bind(p, k1, low_sel, low_coef, low_count, low_rnorm, low_scans, low_flag, st));
+    CDB_CUDA(hi.bind(p, k_high, high_sel, high_coef, high_count, high_rnorm, high_scans, high_flag,
+                     st));
+    StepTimer tm;
+    cdb_status s = zero_tree_core(low, high, fine_shape, factors, rank, rb.ptr, src_f32, p, k1,
+                                  k_high, rel_tol, phi_mode, lo, hi, engine,
+                                  step_ms ? &tm : nullptr, di, st);
+    if (s != CDB_OK) return s;
+    CDB_CUDA(lo.finish(st));
+    CDB_CUDA(hi.finish(st));
+    CDB_CUDA(cudaStreamSynchronize(st));
+    tm.finish(step_ms);
+    return CDB_OK;
+  }
+  auto run = [&](bool try_f32) -> cdb_status {
+    bool f32 = try_f32;
+    StepTimer tm;
+    cdb_status s = run_pipelined_cols(
+        p, n, ys_cols, src_f32, ld, arrs, st,
+        [&](int64_t, int64_t len, const void *rows, bool rows_f32, std::vector<void *> &dv,
+            cudaStream_t s2) -> cdb_status {
+          Outs lo, hi;
+          dev_outs(lo, dv[0], dv[1], dv[2], dv[3], dv[4], dv[5]);
+          dev_outs(hi, dv[6], dv[7], dv[8], dv[9], dv[10], dv[11]);
+          return zero_tree_core(low, high, fine_shape, factors, rank, rows, rows_f32, len, k1,
+                                k_high, rel_tol, phi_mode, lo, hi, engine,
+                                step_ms ? &tm : nullptr, di, s2);
+        },
+        &f32);
+    if (step_ms) step_ms[0] = step_ms[1] = 0.0f;
+    tm.finish(step_ms);
+    return s;
+  };
+  cdb_status s = run(!src_f32);
+  if (s == kRetryF64) s = run(false);  // a later slab was not fp32-exact
+  return s;
 }
 
 cdb_status cdb_ksvd_update(int64_t n, int64_t m, int64_t t, const double *y_rows, double *e_rows,

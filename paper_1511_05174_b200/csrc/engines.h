@@ -213,6 +213,9 @@ cudaError_t launch_aggregate(const double *rows, const double *dc, int rank, con
                              const int64_t *pat, const int64_t *str, double *out,
                              unsigned long long *uncovered, cudaStream_t stream);
 cudaError_t launch_to_f32(const double *d64, int64_t count, float *d32, cudaStream_t stream);
+// n x len column block -> len x n rows (fp32 or fp64)
+cudaError_t launch_cols_to_rows(const void *cols, bool f32, int64_t n, int64_t len, void *rows,
+                                cudaStream_t stream);
 cudaError_t launch_collect_delegates(const uint32_t *status, int64_t p, int64_t *ids,
                                      int *count, cudaStream_t stream);
 

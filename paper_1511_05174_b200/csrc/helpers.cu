@@ -1160,4 +1160,43 @@ int64_t route_work_bytes(int64_t t_low, int64_t p, int64_t k1, int64_t n, bool y
          ((m * 8 + 255) / 256) * 256 + p * k1 * 8 + 256;
 }
 
+// ---------------------------------------------------------------- column batches
+// rows[j][i] = cols[i][j]: an n x len column block (the reference's N x P
+// batch layout, pursuit.py:433 transposes it on the host) into len x n rows.
+// 32 x 32 tiles through shared memory (row stride 33: conflict-free column
+// reads), 8 rows per thread; both sides touch whole 128-byte lines for fp32.
+template <typename T>
+__global__ void __launch_bounds__(256) cols_to_rows_kernel(const T *__restrict__ cols, int64_t n,
+                                                           int64_t len, T *__restrict__ rows) {
+  __shared__ T tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < 32; r += 8) {
+    const int64_t i = i0 + ty + r, j = j0 + tx;
+    if (i < n && j < len) tile[ty + r][tx] = cols[i * len + j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 32; r += 8) {
+    const int64_t j = j0 + ty + r, i = i0 + tx;
+    if (j < len && i < n) rows[j * n + i] = tile[tx][ty + r];
+  }
+}
+
+cudaError_t launch_cols_to_rows(const void *cols, bool f32, int64_t n, int64_t len, void *rows,
+                                cudaStream_t stream) {
+  ProfScope _ps("cols_to_rows", stream);
+  if (n <= 0 || len <= 0) return cudaSuccess;
+  if ((n + 31) / 32 > 65535) return cudaErrorInvalidValue;
+  const dim3 grid((unsigned)((len + 31) / 32), (unsigned)((n + 31) / 32));
+  if (f32)
+    cols_to_rows_kernel<float><<<grid, 256, 0, stream>>>((const float *)cols, n, len, (float *)rows);
+  else
+    cols_to_rows_kernel<double><<<grid, 256, 0, stream>>>((const double *)cols, n, len,
+                                                           (double *)rows);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace cdb

@@ -252,6 +252,39 @@ def zero_tree_raw(low: DeviceDictionary, high: DeviceDictionary, fine_shape, fac
     return lo, hi, ms
 
 
+def cols_layout(ys_cols):
+    """True when an N x P batch can cross the ABI as columns as it is: a
+    float32 / float64 numpy array with unit stride along P (the reference's
+    own layout); batches that already are rows in memory (ys.T C-contiguous)
+    take the rows path."""
+    a = ys_cols
+    return (isinstance(a, np.ndarray) and a.ndim == 2 and a.dtype in (np.float32, np.float64)
+            and a.shape[1] >= PIN_MIN and not a.T.flags.c_contiguous
+            and a.strides[1] == a.itemsize and a.strides[0] % a.itemsize == 0
+            and a.strides[0] // a.itemsize >= a.shape[1])
+
+
+def zero_tree_cols_raw(low: DeviceDictionary, high: DeviceDictionary, fine_shape, factors,
+                       ys_cols, k1: int, k_high: int, rel_tol: float, phi_mode: bool,
+                       engine: str = "auto", out_low=None, out_high=None, stream=None):
+    """cdb_zero_tree_batch_cols: the N x P column batch as the reference holds
+    it (host memory); the transpose to rows happens on the device."""
+    p = int(ys_cols.shape[1])
+    lo = out_low if out_low is not None else _out(p, k1)
+    hi = out_high if out_high is not None else _out(p, k_high)
+    fs = np.asarray(fine_shape if fine_shape is not None else [1], dtype=np.int64)
+    fa = np.asarray(factors if factors is not None else [1], dtype=np.int64)
+    ms = np.zeros(2, np.float32)
+    ld = ys_cols.strides[0] // ys_cols.itemsize
+    N.check(N.load().cdb_zero_tree_batch_cols(low.handle, high.handle, N.ptr(fs), N.ptr(fa),
+                                              int(fs.size), N.ptr(ys_cols),
+                                              1 if ys_cols.dtype == np.float32 else 0, ld, p, k1,
+                                              k_high, float(rel_tol), int(phi_mode),
+                                              *_out_ptrs(lo), *_out_ptrs(hi), N.ENGINES[engine],
+                                              N.ptr(ms), stream))
+    return lo, hi, ms
+
+
 # ---------------------------------------------------------------- patch pipeline ends
 def _geom(signal_shape, patch_shape, stride):
     rank = len(signal_shape)

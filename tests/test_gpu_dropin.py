@@ -192,3 +192,57 @@ def test_omp_many_arrays_configs(ci, rel_tol):
     _check_batch(s, ys.shape[0], w.k)
     rep = compare(golden_dict(g), batch_dict(s), hi_t, ys, W.REL_TOL * np.linalg.norm(ys, axis=1))
     assert not rep["bad"], rep["bad"][:3]
+
+
+def _zt_rows(model, ys_rows, f32):
+    """The rows-ABI solve of the same batch (cdb_zero_tree_batch)."""
+    from paper_1511_05174_b200 import device as D
+    dl = D.device_dictionary(model.d_low.atoms_t)
+    dh = D.device_dictionary(model.d_high.atoms_t)
+    rows = np.ascontiguousarray(ys_rows, dtype=np.float32 if f32 else np.float64)
+    lo, hi, _ = D.zero_tree_raw(dl, dh, model.scale.fine_shape, model.scale.factors, rows,
+                                len(rows), model.k_low, model.k_high, W.REL_TOL, False, "auto")
+    return lo, hi
+
+
+@pytest.mark.parametrize("case", ["f64_exact", "f32_input", "strided", "f64_inexact",
+                                  "late_inexact"])
+def test_zero_tree_cols_path(case, rel_tol):
+    """Large N x P batches cross the ABI as columns (cdb_zero_tree_batch_cols):
+    host-staged slabs (fp32 when exact), device transpose, chunk pipeline.
+    Results equal the rows ABI on the same values -- fp32 rows when every value
+    is fp32-exact, fp64 rows otherwise (including a batch whose only inexact
+    value sits in a later chunk: the call is redone in fp64)."""
+    from paper_1511_05174_b200 import device as D
+    rel_tol(W.REL_TOL)
+    ci = 1
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    p = 50_000
+    ys = W.signals(ci, 0, p)
+    f32 = True
+    if case == "f64_inexact":
+        ys = ys * (1.0 + 2.0 ** -40)
+        f32 = False
+    elif case == "late_inexact":
+        ys = ys.copy()
+        ys[41_234, 7] += 2.0 ** -35 * abs(ys[41_234, 7])
+        f32 = False
+    model = _zt_model(d.low_t, d.high_t, w.fine_shape, w.factors, w.k, w.k)
+    if case == "f32_input":
+        cols = np.ascontiguousarray(ys.T, dtype=np.float32)
+    elif case == "strided":
+        wide = np.zeros((ys.shape[1], p + 37))
+        wide[:, 5:5 + p] = ys.T
+        cols = wide[:, 5:5 + p]
+    else:
+        cols = np.ascontiguousarray(ys.T)
+    assert D.cols_layout(cols)
+    low, high, tim = P.zero_tree_many_arrays(model, cols)
+    assert tim["step1"] > 0 and tim["step2"] > 0
+    rl, rh = _zt_rows(model, ys, f32)
+    for a, b in ((low, rl), (high, rh)):
+        assert np.array_equal(a.sel, b["sel"]) and np.array_equal(a.counts, b["counts"])
+        assert np.array_equal(a.scans, b["scans"])
+        np.testing.assert_allclose(a.alpha, b["alpha"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(a.rnorm, b["rnorm"], rtol=1e-12, atol=1e-14)
