@@ -827,6 +827,88 @@ __global__ void __launch_bounds__(128) alpha0_mma_l1_kernel(
   }
 }
 
+// Q = 8, any N (a multiple of 16), pairs blocked PT tiles deep: a warp codes
+// 8 PT pairs of one parent per pass, so each children fragment (2 x 16 B per
+// lane per 16 coordinates, an L2 read: the parent's 8 children are 8 N fp64,
+// 256 KB at N = 4096, more than L1 holds) feeds PT tiles instead of one --
+// the children stream per pair drops PT-fold.  A pair's DMMA sequence (and
+// so its value) is the one of alpha0_mma_l1_kernel: bit-identical.  Warps of
+// the CTA take the part's super-tiles round-robin.
+template <typename YT, int PT>
+__global__ void __launch_bounds__(128) alpha0_mma_pt_kernel(
+    const double *__restrict__ d64, int n, const YT *__restrict__ ys,
+    const int64_t *__restrict__ offs, const int64_t *__restrict__ pairs, int64_t smax, int split,
+    int t_low, double *__restrict__ alpha0) {
+  const int bucket = blockIdx.x / split, part = blockIdx.x % split;
+  const int parent = bucket % t_low;
+  const int64_t lo = offs[bucket], cnt = offs[bucket + 1] - lo;
+  const int64_t a = lo + cnt * part / split, b = lo + cnt * (part + 1) / split;
+  if (a >= b) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int r = lane >> 2, j = lane & 3, nt = n >> 4;
+  const double *dc = d64 + ((int64_t)parent * 8 + r) * n + 4 * j;
+  for (int64_t e0 = a + (int64_t)warp * 8 * PT; e0 < b; e0 += (int64_t)nwarps * 8 * PT) {
+    int64_t pr[PT];
+    const YT *y[PT];
+#pragma unroll
+    for (int pt = 0; pt < PT; pt++) {
+      const int64_t e = e0 + pt * 8 + r;
+      pr[pt] = pairs[e < b ? e : b - 1];
+      y[pt] = ys + (pr[pt] >> 16) * n + 4 * j;
+    }
+    double c[PT][2];
+#pragma unroll
+    for (int pt = 0; pt < PT; pt++) c[pt][0] = c[pt][1] = 0.0;
+#pragma unroll 4
+    for (int t = 0; t < nt; t++) {
+      const double2 u = __ldg(reinterpret_cast<const double2 *>(dc + 16 * t));
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(dc + 16 * t + 2));
+#pragma unroll
+      for (int pt = 0; pt < PT; pt++) {
+        double yv[4];
+        if constexpr (sizeof(YT) == 4) {
+          const float4 f = *reinterpret_cast<const float4 *>(y[pt] + 16 * t);
+          yv[0] = f.x;
+          yv[1] = f.y;
+          yv[2] = f.z;
+          yv[3] = f.w;
+        } else {
+          const double2 p = *reinterpret_cast<const double2 *>(y[pt] + 16 * t);
+          const double2 q = *reinterpret_cast<const double2 *>(y[pt] + 16 * t + 2);
+          yv[0] = p.x;
+          yv[1] = p.y;
+          yv[2] = q.x;
+          yv[3] = q.y;
+        }
+        dmma_8x8x4(c[pt][0], c[pt][1], u.x, yv[0]);
+        dmma_8x8x4(c[pt][0], c[pt][1], u.y, yv[1]);
+        dmma_8x8x4(c[pt][0], c[pt][1], v.x, yv[2]);
+        dmma_8x8x4(c[pt][0], c[pt][1], v.y, yv[3]);
+      }
+    }
+#pragma unroll
+    for (int pt = 0; pt < PT; pt++) {
+      const int64_t base = e0 + pt * 8;
+      const int64_t p0 = __shfl_sync(CDB_FULL_MASK, (long long)pr[pt], 8 * j);
+      const int64_t p1 = __shfl_sync(CDB_FULL_MASK, (long long)pr[pt], 8 * j + 4);
+      if (base + 2 * j < b) alpha0[(p0 >> 16) * smax + (p0 & 0xffff) * 8 + r] = c[pt][0];
+      if (base + 2 * j + 1 < b) alpha0[(p1 >> 16) * smax + (p1 & 0xffff) * 8 + r] = c[pt][1];
+    }
+  }
+}
+
+// configs[4] (131k signals, alpha0 per call): PT 1 / split 8 (the l1 kernel)
+// 30.1 ms; PT 2 / 3 / 4 at split 1: 25.7 / 20.2 / 21.6 ms; PT 3 at split 2:
+// 20.5 ms; larger routing blocks (6144 signals) no better with PT 3.
+int alpha0_pt() {  // CDB_A0_PT: pair tiles per pass for Q = 8, N > 256 (1 = alpha0_mma_l1_kernel)
+  const char *e = getenv("CDB_A0_PT");
+  return e ? atoi(e) : 3;
+}
+int alpha0_split() {  // CDB_A0_SPLIT: CTAs per (signal block, parent) bucket of the PT kernel
+  const char *e = getenv("CDB_A0_SPLIT");
+  return e ? std::max(1, atoi(e)) : 1;
+}
+
 // CDB_A0_MMA=0 keeps the FFMA warp kernel for Q = 8
 bool alpha0_mma_enabled() {
   static const int on = [] {
@@ -870,6 +952,25 @@ bool try_alpha0_warp(const double *d64, int64_t t_low, int64_t buckets, int64_t 
     else
       alpha0_mma_kernel<YT, 16><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
                                                           split, (int)t_low, alpha0, pf);
+    err = cudaGetLastError();
+    return true;
+  }
+  if (q == 8 && n % 16 == 0 && alpha0_mma_enabled() && alpha0_pt() > 1) {
+    const int split = alpha0_split();
+    const unsigned grid = (unsigned)(buckets * split);
+    switch (alpha0_pt()) {
+      case 2:
+        alpha0_mma_pt_kernel<YT, 2><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                              split, (int)t_low, alpha0);
+        break;
+      case 3:
+        alpha0_mma_pt_kernel<YT, 3><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                              split, (int)t_low, alpha0);
+        break;
+      default:
+        alpha0_mma_pt_kernel<YT, 4><<<grid, 128, 0, stream>>>(d64, (int)n, ys, offs, pairs, smax,
+                                                              split, (int)t_low, alpha0);
+    }
     err = cudaGetLastError();
     return true;
   }

@@ -5,7 +5,7 @@ import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1511_05174_b200 import device as D, workloads as W, _native as N
-P = int(sys.argv[1]); ci = 4
+P = int(sys.argv[1]); ci = int(os.environ.get('CI', 4))
 w = W.CONFIGS[ci]; d = W.dictionaries(ci)
 yd = W.signals_device(ci, 0, P); torch.cuda.synchronize()
 lo, hi = D.device_dictionary(d.low_t), D.device_dictionary(d.high_t)
