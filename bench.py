@@ -558,9 +558,10 @@ def bench_ours(args):
     del yh
 
     # ---- e2e through the Python drop-in on the reference's layout (rank 0, N = 1)
-    e2e_api = None
+    e2e_api = e2e_api_full = None
     if rank == 0 and world == 1 and not args.no_api:
         e2e_api = bench_dropin(torch, ci, yd, args.api_signals)
+        e2e_api_full = bench_dropin_full(torch, ci, yd, args.api_full_signals)
 
     # ---- roofline of the dominant kernel and of the whole step
     peaks, peaks_kind = load_peaks()
@@ -654,6 +655,7 @@ def bench_ours(args):
                             "compute / D2H pipeline) + NCCL gather of all outputs to rank 0 "
                             "when N > 1; wall clock, max over ranks; byte counts whole-job"},
             "e2e_api": e2e_api,
+            "e2e_api_full": e2e_api_full,
             "gen_s": t_gen,
             "clocks": clk,
             "gpu_launches": launches,
@@ -708,6 +710,40 @@ def bench_dropin(torch, ci, yd, count):
                     "crosses the C ABI as columns (cdb_zero_tree_batch_cols: host threads stage "
                     "column slabs into pinned memory, fp32 when exact, the device transposes, "
                     "chunks pipelined); includes every copy and the output allocation"}
+
+
+def bench_dropin_full(torch, ci, yd, count):
+    """omp_many_arrays (full OMP) through the Python drop-in on an N x P fp64
+    pageable column batch over the first `count` benchmark signals -- the
+    full-dictionary twin of bench_dropin (cdb_omp_batch_cols underneath)."""
+    from paper_1511_05174_b200 import pursuit as PU
+    w = W.CONFIGS[ci]
+    if w.measurements or count <= 0:
+        return None
+    d = W.dictionaries(ci)
+    m = int(min(count, yd.shape[0]))
+    cols = yd[:m].T.contiguous().double().cpu().numpy()  # N x P fp64, pageable
+    mat = np.ascontiguousarray(d.high_t.T)
+    old = PU.REL_RESIDUAL_TOL
+    PU.REL_RESIDUAL_TOL = W.REL_TOL
+    try:
+        t0 = time.perf_counter()
+        PU.omp_many_arrays(mat, cols, PU.PursuitConfig(w.k))
+        first = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s = PU.omp_many_arrays(mat, cols, PU.PursuitConfig(w.k))
+        dt = time.perf_counter() - t0
+    finally:
+        PU.REL_RESIDUAL_TOL = old
+    h2d_es = 4 if np.array_equal(cols.astype(np.float32), cols) else 8
+    return {"value": m / dt, "unit": "signals/s", "signals": m, "seconds": dt,
+            "first_call_s": first, "h2d_bytes_per_step": m * w.n_high * h2d_es,
+            "d2h_bytes_per_step": int(sum(a.nbytes for a in (s.sel, s.alpha, s.counts, s.rnorm,
+                                                             s.scans))),
+            "what": "paper_1511_05174_b200.pursuit.omp_many_arrays(columns, ys, config) with ys an "
+                    "N x P fp64 pageable numpy array (cdb_omp_batch_cols: column slabs staged, "
+                    "transposed on the device, tolerances on the device)"}
 
 
 def bench_operator_recovery(no_cpu=False):
@@ -897,6 +933,8 @@ def main():
     ap.add_argument("--full-steps", type=int, default=1, help="timed full-OMP passes")
     ap.add_argument("--e2e-steps", type=int, default=3, help="timed e2e passes (<= steps)")
     ap.add_argument("--api-signals", type=int, default=131072, help="signals of the e2e_api leg")
+    ap.add_argument("--api-full-signals", type=int, default=32768,
+                    help="signals of the full-OMP e2e_api_full leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-api", action="store_true", help="skip the e2e_api leg")
     ap.add_argument("--no-extras", action="store_true", help="skip the f-row legs")

@@ -102,6 +102,21 @@ cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f
                          int engine, void *stream);
 
 /*
+ * Batched OMP on the reference's own column batch (omp_many_arrays' `ys`,
+ * pursuit.py:388-441, before its host transpose at pursuit.py:433): element
+ * (i, p) at ys_cols[i * ld + p], ld >= P, fp64 or fp32 (ys_is_f32), HOST
+ * memory; staged, transposed on the device and pipelined as in
+ * cdb_zero_tree_batch_cols.  eps: P host tolerances, or NULL for
+ * rel_tol * ||y_p|| computed on the device (pursuit.py:434-437).  All
+ * candidates (no restriction); host outputs as cdb_omp_batch.
+ */
+cdb_status cdb_omp_batch_cols(const cdb_dictionary *dict, const void *ys_cols, int ys_is_f32,
+                              int64_t ld, int64_t p, int64_t k_max, const double *eps,
+                              double rel_tol, int64_t *out_sel, double *out_coef,
+                              int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                              uint8_t *out_flag, int engine, void *stream);
+
+/*
  * Block-restricted batched OMP: allowed = blocks * q + [0, q)
  * (pursuit.py:417-423, the `allowed_blocks` / `block_q` form).
  * blocks: P x nb int64, each row ascending, 0-based block ids.

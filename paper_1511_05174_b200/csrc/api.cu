@@ -1473,6 +1473,57 @@ cdb_status cdb_omp_batch(const cdb_dictionary *dict, const void *ys, int ys_is_f
                     out_sel, out_coef, out_count, out_rnorm, out_scans, out_flag, engine, stream);
 }
 
+cdb_status cdb_omp_batch_cols(const cdb_dictionary *dict, const void *ys_cols, int ys_is_f32,
+                              int64_t ld, int64_t p, int64_t k_max, const double *eps,
+                              double rel_tol, int64_t *out_sel, double *out_coef,
+                              int64_t *out_count, double *out_rnorm, int64_t *out_scans,
+                              uint8_t *out_flag, int engine, void *stream) {
+  if (!dict || p < 0 || k_max < 0 || ld < p) return fail(CDB_ERR_ARG, "bad omp arguments");
+  if (p == 0) return CDB_OK;
+  if (!ys_cols || is_device_ptr(ys_cols)) return fail(CDB_ERR_ARG, "ys_cols must be host memory");
+  if (eps && is_device_ptr(eps)) return fail(CDB_ERR_ARG, "eps must be host memory");
+  DevInfo di;
+  cdb_status s0 = device_info(di);
+  if (s0 != CDB_OK) return s0;
+  if ((s0 = check_device(dict)) != CDB_OK) return s0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = dict->n;
+  std::vector<RowArr> arrs = {
+      {out_sel, sizeof(int64_t) * k_max, true}, {out_coef, sizeof(double) * k_max, true},
+      {out_count, sizeof(int64_t), true}, {out_rnorm, sizeof(double), true},
+      {out_scans, sizeof(int64_t), true}, {out_flag, sizeof(uint8_t), true},
+      {(void *)eps, sizeof(double), false}};
+  for (size_t a = 0; a < 6; a++)
+    if (!arrs[a].host) return fail(CDB_ERR_ARG, "null output");
+  if (!all_host(arrs)) return fail(CDB_ERR_ARG, "outputs must be host memory");
+  auto run = [&](bool try_f32) -> cdb_status {
+    bool f32 = try_f32;
+    return run_pipelined_cols(
+        p, n, ys_cols, ys_is_f32 != 0, ld, arrs, st,
+        [&](int64_t, int64_t len, const void *rows, bool rows_f32, std::vector<void *> &dv,
+            cudaStream_t s2) -> cdb_status {
+          DevBuf etmp;
+          const double *e_dev = (const double *)dv[6];
+          if (!eps) {  // rel_tol * |y| per signal, on the device
+            CDB_CUDA(etmp.alloc(sizeof(double) * len, s2));
+            CDB_CUDA(cdb::launch_row_tol(rows, rows_f32, len, n, rel_tol, etmp.as<double>(), s2));
+            e_dev = etmp.as<double>();
+          }
+          cdb::Cands c{};
+          c.mode = 0;
+          c.t = dict->t;
+          Outs o;
+          dev_outs(o, dv[0], dv[1], dv[2], dv[3], dv[4], dv[5]);
+          return run_omp(dict, rows, rows_f32, len, k_max, k_max, e_dev, c, dict->t, o, engine, di,
+                         s2);
+        },
+        &f32);
+  };
+  cdb_status s = run(ys_is_f32 == 0);
+  if (s == kRetryF64) s = run(false);
+  return s;
+}
+
 cdb_status cdb_omp_batch_coded(const cdb_dictionary *dict, const double *ys, int64_t m_stride,
                                const int32_t *rows, int64_t fan, int sum_order,
                                const int64_t *m, int64_t p,

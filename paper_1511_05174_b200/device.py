@@ -264,6 +264,22 @@ def cols_layout(ys_cols):
             and a.strides[0] // a.itemsize >= a.shape[1])
 
 
+def omp_cols_raw(dd: DeviceDictionary, ys_cols, k_max: int, eps=None, rel_tol: float = 0.0,
+                 engine: str = "auto", out=None, stream=None):
+    """cdb_omp_batch_cols: the N x P column batch as the reference holds it
+    (host memory); eps None -> rel_tol * |y| per signal on the device."""
+    p = int(ys_cols.shape[1])
+    o = out if out is not None else _out(p, k_max)
+    ek, eptr = _arg(eps, np.float64, "eps")
+    ld = ys_cols.strides[0] // ys_cols.itemsize
+    N.check(N.load().cdb_omp_batch_cols(dd.handle, N.ptr(ys_cols),
+                                        1 if ys_cols.dtype == np.float32 else 0, ld, p, k_max,
+                                        eptr, float(rel_tol), *_out_ptrs(o), N.ENGINES[engine],
+                                        stream))
+    del ek
+    return o
+
+
 def zero_tree_cols_raw(low: DeviceDictionary, high: DeviceDictionary, fine_shape, factors,
                        ys_cols, k1: int, k_high: int, rel_tol: float, phi_mode: bool,
                        engine: str = "auto", out_low=None, out_high=None, stream=None):

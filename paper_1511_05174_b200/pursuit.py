@@ -248,6 +248,15 @@ def omp_many_arrays(columns, ys, config, *, allowed_blocks=None, block_q=None):
         return _types.get("BatchSolve", BatchSolve)(
             t, z, z.reshape(0, k_max), np.zeros((0, k_max)), np.zeros(0), z)
 
+    if blocks is None and _dev.cols_layout(ys):
+        # large column batch: staged and transposed on the device, the
+        # tolerances rel * |y| computed there (pursuit.py:433-437)
+        eps = None
+        if config.residual_tolerance is not None:
+            eps = np.full(p_all, float(config.residual_tolerance))
+        o = _dev.omp_cols_raw(_dev.device_dictionary(cols.mat_t), ys, k_max, eps, _rel_tol(),
+                              ENGINE)
+        return _make_batch(t, o)
     ys_rows = _dev.rows_for_device(ys)
     if config.residual_tolerance is not None:
         eps = np.full(p_all, float(config.residual_tolerance))

@@ -246,3 +246,29 @@ def test_zero_tree_cols_path(case, rel_tol):
         assert np.array_equal(a.scans, b["scans"])
         np.testing.assert_allclose(a.alpha, b["alpha"], rtol=1e-12, atol=1e-14)
         np.testing.assert_allclose(a.rnorm, b["rnorm"], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("case", ["f64_exact", "f32_input", "fixed_tol"])
+def test_omp_many_arrays_cols_path(case, rel_tol):
+    """Large N x P batches of omp_many_arrays cross the ABI as columns
+    (cdb_omp_batch_cols, tolerances rel * |y| on the device): results equal the
+    rows ABI on fp32 rows with the reference's host tolerances."""
+    from paper_1511_05174_b200 import device as D
+    rel_tol(W.REL_TOL)
+    ci = 1
+    w = W.CONFIGS[ci]
+    d = W.dictionaries(ci)
+    p = 40_000
+    ys = W.signals(ci, 0, p)
+    tol = 0.05 if case == "fixed_tol" else None
+    cols = np.ascontiguousarray(ys.T, dtype=np.float32 if case == "f32_input" else np.float64)
+    assert D.cols_layout(cols)
+    s = P.omp_many_arrays(np.ascontiguousarray(d.high_t.T), cols,
+                          PU.PursuitConfig(w.k, residual_tolerance=tol))
+    _check_batch(s, p, w.k)
+    eps = np.full(p, tol) if tol else W.REL_TOL * np.sqrt(np.einsum("pn,pn->p", ys, ys))
+    r = D.omp_batch_raw(D.device_dictionary(d.high_t), ys.astype(np.float32), p, w.k, eps)
+    assert np.array_equal(s.sel, r["sel"]) and np.array_equal(s.counts, r["counts"])
+    assert np.array_equal(s.scans, r["scans"])
+    np.testing.assert_allclose(s.alpha, r["alpha"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(s.rnorm, r["rnorm"], rtol=1e-12, atol=1e-14)
