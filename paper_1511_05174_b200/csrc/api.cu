@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cmath>
 #include <string>
 #include <array>
 #include <chrono>
@@ -20,10 +21,11 @@ struct cdb_dictionary {
   int64_t t = 0, n = 0, n_pad = 0;
   double *d64 = nullptr;   // T x N fp64 atoms (rows)
   double *gram = nullptr;  // T x T fp64 (optional)
-  void *d16 = nullptr;     // T x n_pad bf16 (tensor-core operand)
+  void *d16 = nullptr;     // T x n_pad fp16(dscale * d) (tensor-core operand)
   float *d32 = nullptr;    // T x N fp32 (residual materialisation of the scan operand)
   double dmax = 0.0;       // largest atom norm
-  double emax = 0.0;       // largest |bf16(d_j) - d_j| (tensor-engine certification)
+  double emax = 0.0;       // largest |fp16(dscale d_j) / dscale - d_j| (tensor-engine certification)
+  double dscale = 1.0;     // power of two: the largest atom norm lands in [2^8, 2^9)
   int64_t bytes = 0;
   int device = -1;         // CUDA device holding the arrays
 };
@@ -313,6 +315,7 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
     a.rescans = diag_dev() + 1;  // zeroed by run_omp's diag_clear
     a.dmax = d->dmax;
     a.emax = d->emax;
+    a.dscale = d->dscale;
     a.out_sel = (int64_t *)o.sel.dev + off * kw;
     a.out_coef = (double *)o.coef.dev + off * kw;
     a.out_count = (int64_t *)o.count.dev + off;
@@ -1336,8 +1339,6 @@ cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
   const size_t b16 = 2 * t * d->n_pad;
   if (cudaMalloc(&d->d16, b16) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "d16 alloc");
   d->bytes += b16;
-  if (cdb::launch_to_bf16(d->d64, t, n, d->n_pad, d->d16, st) != cudaSuccess)
-    return cleanup(CDB_ERR_CUDA, "bf16 conversion");
   if (cudaMalloc(&d->d32, 4 * t * n) != cudaSuccess) return cleanup(CDB_ERR_NOMEM, "d32 alloc");
   d->bytes += 4 * t * n;
   if (cdb::launch_to_f32(d->d64, t * n, d->d32, st) != cudaSuccess)
@@ -1349,8 +1350,14 @@ cdb_status cdb_dictionary_create(const double *atoms_t, int64_t t, int64_t n,
     if (cdb::launch_row_norm_max(d->d64, t, n, dm, st) != cudaSuccess ||
         cudaMemcpyAsync(&d->dmax, dm, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
       return cleanup(CDB_ERR_CUDA, "dmax kernel");
-    if (cudaStreamSynchronize(st) != cudaSuccess ||
-        cdb::launch_quant_err_max(d->d64, d->d16, t, n, d->n_pad, dm, st) != cudaSuccess ||
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cleanup(CDB_ERR_CUDA, "dmax sync");
+    // the fp16 operand carries dscale * d: largest atom norm in [2^8, 2^9)
+    d->dscale = 1.0;
+    if (d->dmax > 0x1p-900 && d->dmax < 0x1p900) d->dscale = std::ldexp(1.0, 8 - std::ilogb(d->dmax));
+    if (cdb::launch_to_f16(d->d64, t, n, d->n_pad, d->dscale, d->d16, st) != cudaSuccess)
+      return cleanup(CDB_ERR_CUDA, "fp16 conversion");
+    if (cdb::launch_quant_err_max(d->d64, d->d16, t, n, d->n_pad, d->dscale, dm, st) !=
+            cudaSuccess ||
         cudaMemcpyAsync(&d->emax, dm, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
       return cleanup(CDB_ERR_CUDA, "quantisation-error kernel");
     cudaFreeAsync(dm, st);
@@ -1384,8 +1391,8 @@ cdb_status cdb_debug_corr_topk(const cdb_dictionary *d, const float *rows, int64
                                void *stream) {
   if (!d || !rows || p < 1) return fail(CDB_ERR_ARG, "bad debug_corr_topk arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  CDB_CUDA(cdb::debug_corr_topk(d->d16, d->t, d->n, rows, p, cand_idx, cand_val, cand_drop,
-                                grid_cap, st));
+  CDB_CUDA(cdb::debug_corr_topk(d->d16, d->dscale, d->t, d->n, rows, p, cand_idx, cand_val,
+                                cand_drop, grid_cap, st));
   CDB_CUDA(cudaStreamSynchronize(st));
   return CDB_OK;
 }

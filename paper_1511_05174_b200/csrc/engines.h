@@ -155,7 +155,8 @@ struct TensorArgs {
   const float *d32;      // T x N fp32 atoms (residual materialisation)
   const double *gram;
   double dmax;           // max atom norm (error bound)
-  double emax;           // max |bf16(d_j) - d_j| (error bound)
+  double emax;           // max |fp16(dscale d_j) / dscale - d_j| (error bound)
+  double dscale;         // power-of-two scale of the fp16 dictionary operand
   int *rescans;          // device counter of inline exact rescans
   int64_t *out_sel;
   double *out_coef;
@@ -170,13 +171,13 @@ struct TensorArgs {
 };
 int64_t tensor_state_bytes(int64_t p, int64_t n, int64_t kw);
 cudaError_t run_tensor_chunk(const TensorArgs &args, cudaStream_t stream);
-cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *rows, int64_t p,
-                            int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
-                            cudaStream_t stream);
+cudaError_t debug_corr_topk(const void *d16, double dscale, int64_t t, int64_t n,
+                            const float *rows, int64_t p, int *cand_idx, float *cand_val,
+                            float *cand_drop, int grid_cap, cudaStream_t stream);
 
 // ---------------------------------------------------------------- helpers
 cudaError_t launch_quant_err_max(const double *d64, const void *d16, int64_t t, int64_t n,
-                                 int64_t n_pad, double *out, cudaStream_t stream);
+                                 int64_t n_pad, double scale, double *out, cudaStream_t stream);
 cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double *out,
                                 cudaStream_t stream);
 cudaError_t launch_downsample(const void *ys, bool ys_f32, int64_t p, int64_t n,
@@ -190,8 +191,8 @@ cudaError_t launch_sort_blocks(const int64_t *low_sel, const int64_t *low_count,
                                int64_t k1, int64_t *blocks, cudaStream_t stream);
 cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *gram,
                                cudaStream_t stream);
-cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad,
-                           void *d16, cudaStream_t stream);
+cudaError_t launch_to_f16(const double *d64, int64_t t, int64_t n, int64_t n_pad, double scale,
+                          void *d16, cudaStream_t stream);
 bool route_alpha0_dmma(int64_t q, int64_t n);
 cudaError_t launch_route_alpha0(const double *d64, int64_t t_low, int64_t n, int64_t q,
                                const void *ys, bool ys_f32, const int64_t *blocks,

@@ -1,5 +1,5 @@
 // Small memory-bound kernels around the OMP engines.
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdint>
 #include "common.cuh"
@@ -308,12 +308,16 @@ __global__ void __launch_bounds__(256) gram_matrix_kernel(const double *__restri
     }
 }
 
-__global__ void to_bf16_kernel(const double *__restrict__ d, int64_t t, int64_t n, int64_t n_pad,
-                               __nv_bfloat16 *__restrict__ out) {
+// Tensor-core operand of the dictionary: fp16(scale * d), scale a power of
+// two that puts the largest atom norm near 2^8 (fp16 carries 11 significand
+// bits against bf16's 8, so the certified scan's window is ~8x narrower; the
+// scale keeps every element far from both ends of the fp16 range).
+__global__ void to_f16_kernel(const double *__restrict__ d, int64_t t, int64_t n, int64_t n_pad,
+                              double scale, __half *__restrict__ out) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= t * n_pad) return;
   const int64_t row = gid / n_pad, col = gid % n_pad;
-  out[gid] = __float2bfloat16_rn(col < n ? (float)d[row * n + col] : 0.0f);
+  out[gid] = __float2half_rn(col < n ? (float)(d[row * n + col] * scale) : 0.0f);
 }
 
 __global__ void to_f32_kernel(const double *__restrict__ d, int64_t count, float *__restrict__ out) {
@@ -339,17 +343,18 @@ __global__ void row_norm_max_kernel(const double *__restrict__ d, int64_t t, int
   if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(sqrt(acc)));
 }
 
-// max over atoms of |bf16(d_j) - d_j| (the tensor engine's operand rounding,
-// measured exactly; the certification bound charges it instead of u |d|)
-__global__ void quant_err_max_kernel(const double *__restrict__ d, const __nv_bfloat16 *__restrict__ d16,
-                                     int64_t t, int64_t n, int64_t n_pad,
+// max over atoms of |fp16(scale d_j) / scale - d_j| (the tensor engine's
+// operand rounding, measured exactly; the certification bound charges it
+// instead of u |d|)
+__global__ void quant_err_max_kernel(const double *__restrict__ d, const __half *__restrict__ d16,
+                                     int64_t t, int64_t n, int64_t n_pad, double inv_scale,
                                      unsigned long long *__restrict__ out) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= t) return;
   double acc = 0.0;
   for (int64_t i = lane; i < n; i += 32) {
-    const double e = (double)__bfloat162float(d16[w * n_pad + i]) - d[w * n + i];
+    const double e = (double)__half2float(d16[w * n_pad + i]) * inv_scale - d[w * n + i];
     acc = fma(e, e, acc);
   }
   acc = warp_sum(acc);
@@ -1141,11 +1146,11 @@ cudaError_t launch_gram_matrix(const double *d64, int64_t t, int64_t n, double *
   return cudaGetLastError();
 }
 
-cudaError_t launch_to_bf16(const double *d64, int64_t t, int64_t n, int64_t n_pad, void *d16,
-                           cudaStream_t stream) {
-  ProfScope _ps("to_bf16", stream);
-  to_bf16_kernel<<<blocks_for(t * n_pad, 256), 256, 0, stream>>>(d64, t, n, n_pad,
-                                                                  (__nv_bfloat16 *)d16);
+cudaError_t launch_to_f16(const double *d64, int64_t t, int64_t n, int64_t n_pad, double scale,
+                          void *d16, cudaStream_t stream) {
+  ProfScope _ps("to_f16", stream);
+  to_f16_kernel<<<blocks_for(t * n_pad, 256), 256, 0, stream>>>(d64, t, n, n_pad, scale,
+                                                                 (__half *)d16);
   note_launch();
   return cudaGetLastError();
 }
@@ -1178,11 +1183,11 @@ cudaError_t launch_row_norm_max(const double *d64, int64_t t, int64_t n, double 
 }
 
 cudaError_t launch_quant_err_max(const double *d64, const void *d16, int64_t t, int64_t n,
-                                 int64_t n_pad, double *out, cudaStream_t stream) {
+                                 int64_t n_pad, double scale, double *out, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), stream);
   if (e != cudaSuccess) return e;
   quant_err_max_kernel<<<blocks_for(t * 32, 256), 256, 0, stream>>>(
-      d64, (const __nv_bfloat16 *)d16, t, n, n_pad, (unsigned long long *)out);
+      d64, (const __half *)d16, t, n, n_pad, 1.0 / scale, (unsigned long long *)out);
   note_launch();
   return cudaGetLastError();
 }

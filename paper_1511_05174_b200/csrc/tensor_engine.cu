@@ -3,7 +3,7 @@
 //
 // Per OMP iteration (all signals of the batch in lock-step):
 //
-//  1. corr_topk_kernel  C = R16 . D16^T on tcgen05 (bf16 x bf16 -> fp32 in
+//  1. corr_topk_kernel  C = R16 . D16^T on tcgen05 (fp16 x fp16 -> fp32 in
 //     TMEM), operands staged by TMA with 128-byte swizzle, two 256-column
 //     accumulator buffers so the epilogue of atom tile t overlaps the MMAs
 //     of tile t+1.  The epilogue never writes C: each thread keeps, for its
@@ -11,7 +11,7 @@
 //     Replaces the reference's scan, _kernels.py:94-103.
 //  2. ls_step_kernel (one warp per signal, fp64)  re-scores the approximate
 //     winners exactly (c_j = <d_j, r> in fp64) and CERTIFIES the pick: with
-//     E the rigorous bf16/fp32 error bound of step 1, every atom outside
+//     E the rigorous fp16/fp32 error bound of step 1, every atom outside
 //     the re-scored set has |c| <= (its approximate value) + E < best exact.
 //     Certified picks are therefore the exact fp64 argmax (ties -> lowest
 //     index, as the reference's strict '>' scan).  An uncertifiable pick, or
@@ -20,9 +20,9 @@
 //     (G row gather, explicit L^{-1}), z_k = c_new / d (the reference's
 //     q_k^T y), coefficients x = L^{-T} z, and the residual r = y - D_S x
 //     rematerialised in fp64 from y (no drift), its exact norm for the stop
-//     test (_kernels.py:156) and its bf16 copy as the next GEMM operand.
+//     test (_kernels.py:156) and its scaled fp16 copy as the next GEMM operand.
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -40,7 +40,7 @@ namespace {
 constexpr int BMH = 128;         // rows per M half (one MMA, M = 128)
 constexpr int BM = 2 * BMH;      // signals per CTA tile (two halves share each B stage)
 constexpr int BN = 128;          // atoms per tile (MMA N)
-constexpr int BK = 64;           // bf16 elements per 128-byte swizzled row chunk
+constexpr int BK = 64;           // fp16 elements per 128-byte swizzled row chunk
 constexpr int NCAND = 8;         // approximate candidates kept per signal
 constexpr int EPI_WARPS = 8;     // 4 TMEM lane quarters x 2 M halves: one row per thread
 constexpr int THREADS = 64 + EPI_WARPS * 32;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
-      constexpr uint32_t idesc = sm100::idesc_bf16_f32(BMH, BN);
+      constexpr uint32_t idesc = sm100::idesc_f16_f32(BMH, BN);
       uint32_t s = 0, ph = 0, acc = 0, acc_ph = 0, aph = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int tt0 = (int)(item % nsplit) * tpq, tt1 = tt0 + tpq < t_tiles ? tt0 + tpq : t_tiles;
@@ -198,9 +198,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int k = 0; k < BK / 16; k++) {
               const uint64_t bd = sm100::desc_kmajor_sw128(b + k * 32);
               const uint32_t accum = (kc | k) != 0 ? 1u : 0u;
-              sm100::mma_bf16(tmem + (acc * 2 + 0) * BN, sm100::desc_kmajor_sw128(a0 + k * 32), bd,
+              sm100::mma_f16(tmem + (acc * 2 + 0) * BN, sm100::desc_kmajor_sw128(a0 + k * 32), bd,
                               idesc, accum);
-              sm100::mma_bf16(tmem + (acc * 2 + 1) * BN, sm100::desc_kmajor_sw128(a1 + k * 32), bd,
+              sm100::mma_f16(tmem + (acc * 2 + 1) * BN, sm100::desc_kmajor_sw128(a1 + k * 32), bd,
                               idesc, accum);
             }
             sm100::mma_commit(&sm.empty[s]);
@@ -377,20 +377,46 @@ __global__ void __launch_bounds__(256) merge_cands_kernel(const int *__restrict_
   if (lane == 0) cand_drop[sig] = drop;
 }
 
-__global__ void to_bf16_rows(const float *__restrict__ rows, int64_t p, int64_t n, int64_t n_pad,
-                             __nv_bfloat16 *__restrict__ out) {
+__global__ void to_f16_rows(const float *__restrict__ rows, int64_t p, int64_t n, int64_t n_pad,
+                            __half *__restrict__ out) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= p * n_pad) return;
   const int64_t r = gid / n_pad, c = gid % n_pad;
-  out[gid] = __float2bfloat16_rn(c < n ? rows[r * n + c] : 0.0f);
+  out[gid] = __float2half_rn(c < n ? rows[r * n + c] : 0.0f);
+}
+
+// debug pass: candidate values back in the dictionary's own units
+__global__ void unscale_vals(float *__restrict__ val, float *__restrict__ drop, int64_t p,
+                             float inv) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid < p * NCAND) val[gid] *= inv;
+  if (gid < p) drop[gid] *= inv;
 }
 
 // ---------------------------------------------------------------- LS side
-// Store the bf16 scan operand element of r~ and return its squared rounding error.
-__device__ __forceinline__ double put_r16(__nv_bfloat16 *dst, double v) {
-  const __nv_bfloat16 b = __float2bfloat16_rn((float)v);
+// Power-of-two scale of a signal's fp16 scan operand: with b >= |r~|^2 (the
+// running |y|^2 - |z|^2, floored at 2^-40 |y|^2 against cancellation) every
+// scaled element stays below 2^14, a factor 4 under the fp16 maximum, and the
+// typical element |r~| / sqrt(N) keeps all 11 significand bits.  Writer and
+// reader derive it from the same stored (rn2, yy) pair.  An operand that
+// overflows anyway measures an infinite rounding error, so its picks are
+// never certified (exact rescan).
+// (Exponents are taken and powers of two built from the bit patterns: no
+// libdevice slow-path calls inside the register-tuned operand kernels.)
+__device__ __forceinline__ int scan_scale_exp(double rn2, double yy) {
+  const double b = fmax(rn2, yy * 0x1p-40);
+  if (!(b > 0x1p-200) || !(b < 0x1p200)) return 0;
+  return 13 - ((((__double2hiint(b) >> 20) & 0x7ff) - 1023) >> 1);  // in [-87, 113]
+}
+__device__ __forceinline__ double pow2d(int e) { return __hiloint2double((1023 + e) << 20, 0); }
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
+// Store the fp16 scan operand element of s * r~ and return the squared rounding
+// error of the value the scan sees, fp16(s v) / s - v.
+__device__ __forceinline__ double put_r16(__half *dst, double v, double s, double inv_s) {
+  const __half b = __float2half_rn((float)(v * s));
   *dst = b;
-  const double e = (double)__bfloat162float(b) - v;
+  const double e = (double)__half2float(b) * inv_s - v;
   return e * e;
 }
 
@@ -403,15 +429,16 @@ __device__ __forceinline__ int64_t lsw(int64_t l, int64_t i, int64_t kwp) {
 }
 
 struct TensorState {
-  __nv_bfloat16 *r16;   // Ppad x n_pad   GEMM operand  bf16(r~), r~ = y - D32_S x
+  __half *r16;          // Ppad x n_pad   GEMM operand  fp16(s r~), r~ = y - D32_S x, s = scan_scale
   double *linv;         // P x kw x kwp   L^{-1}, swizzled rows (lsw)
   double *z;            // P x kw         q_i^T y
   double *rn2;          // P   |y|^2 - |z|^2   (= |r|^2 up to rounding)
   double *yy;           // P   |y|^2
-  double *rt;           // P   |r~|  (operand of the bf16 scan)
+  double *rt;           // P   |r~|  (operand of the fp16 scan)
   double *dr;           // P   bound on |r~ - r|
-  double *rq;           // P   |bf16(r~) - r~| (the scan operand's rounding, exact)
-  double emax;          // max_j |bf16(d_j) - d_j| (the dictionary operand's rounding)
+  double *rq;           // P   |fp16(s r~) / s - r~| (the scan operand's rounding, exact)
+  double emax;          // max_j |fp16(dscale d_j) / dscale - d_j| (the dictionary operand's rounding)
+  double dinv;          // 1 / (power-of-two scale of the dictionary operand)
   double *tol;          // P
   uint32_t *status;     // P   ST_DONE | ST_DELEGATE
   const int *cand_idx;
@@ -445,10 +472,13 @@ __global__ void __launch_bounds__(256) ls_init_kernel(const YT *__restrict__ ys,
   double yy = 0.0, q2 = 0.0;
   for (int64_t i = lane; i < n; i += 32) {
     const double v = (double)y[i];
-    q2 += put_r16(st.r16 + sig * n_pad + i, v);
     yy = fma(v, v, yy);
   }
   yy = warp_sum(yy);
+  const int e16 = scan_scale_exp(yy, yy);
+  const double s16 = pow2d(e16), inv16 = pow2d(-e16);
+  for (int64_t i = lane; i < n; i += 32)
+    q2 += put_r16(st.r16 + sig * n_pad + i, (double)y[i], s16, inv16);
   q2 = warp_sum(q2);
   // |y| in the reference's _dot4 order (_kernels.py:27-47,71): lanes 0-3
   // run the four accumulator chains, the tail is added last
@@ -518,7 +548,7 @@ constexpr uint32_t ST_RESID = 8u;   // split mode: the next scan operand is stil
 
 // Append atom `bestj` (exact correlation cbest) to the signal's support:
 // Cholesky update through the Gram row, coefficients, stop test, and the
-// bf16 operand of the next scan.  Whole warp; smem per warp as in ls_step.
+// fp16 operand of the next scan.  Whole warp; smem per warp as in ls_step.
 __device__ void ls_update(const double *__restrict__ d64, const float *__restrict__ d32,
                           const double *__restrict__ gram, int64_t sig, int64_t t, int64_t n,
                           int64_t n_pad, int64_t k_max, int64_t kw, int iter, double dmax,
@@ -602,9 +632,11 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
     if (lane == 0) st.status[sig] |= ST_DONE;
     return;
   }
-  // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16.
+  // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> fp16(s r~).
   // 8 elements per lane per pass: each support atom row is read coalesced.
   double rr = 0.0, sx = 0.0, q2 = 0.0;
+  const int e16 = scan_scale_exp(rn2, yy);
+  const double s16 = pow2d(e16), inv16 = pow2d(-e16);
   for (int64_t i0 = 0; i0 < n; i0 += 256) {
     double acc[8];
 #pragma unroll
@@ -640,7 +672,7 @@ __device__ void ls_update(const double *__restrict__ d64, const float *__restric
     for (int u = 0; u < 8; u++) {
       const int64_t i = i0 + u * 32 + lane;
       if (i < n) {
-        q2 += put_r16(st.r16 + sig * n_pad + i, acc[u]);
+        q2 += put_r16(st.r16 + sig * n_pad + i, acc[u], s16, inv16);
         rr = fma(acc[u], acc[u], rr);
       }
     }
@@ -717,25 +749,26 @@ __global__ void __launch_bounds__(256, 3) ls_step_kernel(
         bg1 = lane + 32 < k ? __ldg(grow + ssel[lane + 32]) : 0.0;
       }
     } else {
-      // ---- candidates: drop taken atoms; rigorous bound E of the bf16 scan
+      // ---- candidates: drop taken atoms; rigorous bound E of the fp16 scan
       if (lane < NCAND) {
         for (int64_t i = 0; i < k && cidx >= 0; i++)
           if (ssel[i] == cidx) cidx = -1;
         if (cidx < 0) cval = -1.0f;
       }
       const double rq = st.rq[sig];  // E: rigorous bound of |c~ - <d, r>| (see c_err)
+      const double vinv = pow2d(-scan_scale_exp(rn2_prev, yy_s)) * st.dinv;  // scan values carry both scales
       const double E = (c_err * (rt + rq) * 1.0079 + rq + drs) * dmax + st.emax * (rt + rq);
-      double best_apx = (double)cval;
+      double best_apx = (double)cval * vinv;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
         best_apx = fmax(best_apx, __shfl_xor_sync(CDB_FULL_MASK, best_apx, o));
-      const bool rescore = cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
+      const bool rescore = cidx >= 0 && (double)cval * vinv >= best_apx - 2.0 * E;
       const unsigned rmask = __ballot_sync(CDB_FULL_MASK, rescore);
-      double unscored = rescore || cidx < 0 ? -1.0 : (double)cval;
+      double unscored = rescore || cidx < 0 ? -1.0 : (double)cval * vinv;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
         unscored = fmax(unscored, __shfl_xor_sync(CDB_FULL_MASK, unscored, o));
-      unscored = fmax(unscored, (double)cdrop);
+      unscored = fmax(unscored, (double)cdrop * vinv);
       for (unsigned m = rmask; m; m &= m - 1) {
         const int c = __ffs(m) - 1;
         const int64_t j = __shfl_sync(CDB_FULL_MASK, cidx, c);
@@ -873,19 +906,20 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
         if (gl == 0) st.status[sig] &= ~ST_RESCAN;
       }
     } else {
-      // ---- candidates: drop taken atoms; rigorous bound E of the bf16 scan
+      // ---- candidates: drop taken atoms; rigorous bound E of the fp16 scan
       if (cidx >= 0) {
         for (int i = 0; i < k; i++)
           if (ssel[i] == cidx) cidx = -1;
         if (cidx < 0) cval = -1.0f;
       }
       const double rq = st.rq[sig];  // E: rigorous bound of |c~ - <d, r>| (see c_err)
+      const double vinv = pow2d(-scan_scale_exp(rn2_prev, yy)) * st.dinv;  // scan values carry both scales
       const double E = (c_err * (rt + rq) * 1.0079 + rq + drs) * dmax + st.emax * (rt + rq);
-      const double best_apx = gmax<G>((double)cval);
-      const bool rescore = act && cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
+      const double best_apx = gmax<G>((double)cval * vinv);
+      const bool rescore = act && cidx >= 0 && (double)cval * vinv >= best_apx - 2.0 * E;
       const unsigned rm = (__ballot_sync(CDB_FULL_MASK, rescore) & gbits) >> (gi * G);
-      double unsc = gmax<G>(rescore || cidx < 0 ? -1.0 : (double)cval);
-      unsc = fmax(unsc, (double)cdrop);
+      double unsc = gmax<G>(rescore || cidx < 0 ? -1.0 : (double)cval * vinv);
+      unsc = fmax(unsc, (double)cdrop * vinv);
       const int nre = __popc(rm);
       const int maxre = (int)__reduce_max_sync(CDB_FULL_MASK, (unsigned)nre);
       unsigned mm = rm;
@@ -1033,10 +1067,12 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
       if (gl == 0) st.status[sig] |= ST_DONE;
       act = false;
     }
-    // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> bf16
+    // ---- next scan operand: r~ = y - D32_S x (fp64 accumulate) -> fp16
     //      (split mode: left to resid_split_kernel, flagged ST_RESID)
     double rr = 0.0, sx = 0.0, q2 = 0.0;
     if (act && !split) {
+      const int e16 = scan_scale_exp(rn2, yy);
+  const double s16 = pow2d(e16), inv16 = pow2d(-e16);
 #pragma unroll
       for (int i0 = 0; i0 < (YM > 0 ? YM * G : n); i0 += 8 * G) {
         if (YM > 0 && i0 >= n) break;
@@ -1081,7 +1117,7 @@ __global__ void __launch_bounds__(128, 6) ls_group_kernel(
         for (int u = 0; u < 8; u++) {
           const int i = i0 + u * G + gl;
           if (i < n) {
-            q2 += put_r16(st.r16 + sig * n_pad + i, acc[u]);
+            q2 += put_r16(st.r16 + sig * n_pad + i, acc[u], s16, inv16);
             rr = fma(acc[u], acc[u], rr);
           }
         }
@@ -1221,18 +1257,19 @@ __global__ void __launch_bounds__(128, MB) ls_wide_kernel(
       }
       const float cdrop = st.cand_drop[sig];
       const double rt = st.rt[sig], drs = st.dr[sig], rq = st.rq[sig];
+      const double vinv = pow2d(-scan_scale_exp(rn2_prev, yy)) * st.dinv;  // scan values carry both scales
       const double E = (c_err * (rt + rq) * 1.0079 + rq + drs) * dmax + st.emax * (rt + rq);
-      double best_apx = (double)cval;
+      double best_apx = (double)cval * vinv;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
         best_apx = fmax(best_apx, __shfl_xor_sync(CDB_FULL_MASK, best_apx, o));
-      const bool rescore = cidx >= 0 && (double)cval >= best_apx - 2.0 * E;
+      const bool rescore = cidx >= 0 && (double)cval * vinv >= best_apx - 2.0 * E;
       const unsigned rmask = __ballot_sync(CDB_FULL_MASK, rescore);
-      double unscored = rescore || cidx < 0 ? -1.0 : (double)cval;
+      double unscored = rescore || cidx < 0 ? -1.0 : (double)cval * vinv;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
         unscored = fmax(unscored, __shfl_xor_sync(CDB_FULL_MASK, unscored, o));
-      unscored = fmax(unscored, (double)cdrop);
+      unscored = fmax(unscored, (double)cdrop * vinv);
       for (unsigned m = rmask; m; m &= m - 1) {
         const int64_t j = __shfl_sync(CDB_FULL_MASK, cidx, __ffs(m) - 1);
         // exact c_j = <d_j, y> - G[j, S] x  (fp64)
@@ -1412,7 +1449,7 @@ __global__ void __launch_bounds__(128, MB) ls_wide_kernel(
   }
 }
 
-// Split-mode scan operand (large N): r~ = y - D32_S x -> bf16 for every signal
+// Split-mode scan operand (large N): r~ = y - D32_S x -> fp16 for every signal
 // flagged ST_RESID, one CTA per signal -- 8 elements x 4 atom rows = 32 loads
 // in flight per thread, so the kd x N fp32 row stream runs near HBM speed
 // instead of at the LS kernel's occupancy (its per-signal L^{-1} state allows
@@ -1429,6 +1466,7 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
   double *xv = xsm;                         // kw
   int64_t *ssel = (int64_t *)(xv + kw);     // kw
   __shared__ double red[3][BT / 32];
+  __shared__ int e16s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the next signal's status, count and code entries (thread l < kw) are
   // loaded one signal ahead (resid_f32_kernel: 12% on cfg 4 step 1)
@@ -1454,6 +1492,9 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
       xv[l] = l == tid ? cx : out_coef[sig * kw + l];
       ssel[l] = l == tid ? csel : out_sel[sig * kw + l];
     }
+    // the operand's scale exponent waits in shared memory: nothing of it is
+    // live across the register-tight row loop
+    if (tid == 0) e16s = scan_scale_exp(st.rn2[sig], st.yy[sig]);
     __syncthreads();
     const YT *y = ys + sig * n;
     double rr = 0.0, q2 = 0.0;
@@ -1492,11 +1533,13 @@ __global__ void __launch_bounds__(BT) resid_split_kernel(const YT *__restrict__ 
           if (i < n) acc[u] = fma(-xl, (double)__ldg(row + i), acc[u]);
         }
       }
+      const int e16 = e16s;
+      const double s16 = pow2d(e16), inv16 = pow2d(-e16);
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         const int64_t i = i0 + u * BT + tid;
         if (i < n) {
-          q2 += put_r16(st.r16 + sig * n_pad + i, acc[u]);
+          q2 += put_r16(st.r16 + sig * n_pad + i, acc[u], s16, inv16);
           rr = fma(acc[u], acc[u], rr);
         }
       }
@@ -1538,7 +1581,7 @@ __device__ __forceinline__ float4 ldg_nc_f4(const float4 *p) {
 
 // fp32 split-mode scan operand: the same r~ = y - D32_S x, accumulated in
 // fp32 with 16-byte loads (V float4 per thread per atom row, 8 rows in
-// flight), packed bf16 stores.  The scan's error budget charges the fp32
+// flight), packed fp16 stores.  The scan's error budget charges the fp32
 // arithmetic exactly (dr below): with u = 2^-24 and g = (k+1) u / (1 - (k+1) u)
 // the FMA chain y32 - sum_l x32_l d32_l has |r~ - r| <= |y32 - y| +
 // sum_l |x32_l d32_l - x_l d_l| + g (|y32| + sum_l |x32_l| |d32_l|), so
@@ -1556,7 +1599,7 @@ __global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys
   float *xf = (float *)xsm;                         // kw fp32 coefficients
   const float **rows = (const float **)(xsm + kw);  // kw row pointers
   __shared__ double red[3][BT / 32];
-  __shared__ double sxs;
+  __shared__ int e16s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the next signal's status, count and (thread l < kw) code entry are loaded
   // one signal ahead, so a signal starts without three dependent round trips
@@ -1586,6 +1629,7 @@ __global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys
     }
     sx = warp_sum(sx);
     if (lane == 0) red[1][warp] = sx;
+    if (tid == 0) e16s = scan_scale_exp(st.rn2[sig], st.yy[sig]);  // read after the row loop
     __syncthreads();
     float4 acc[V];
     const YT *y = ys + sig * n;
@@ -1644,18 +1688,20 @@ __global__ void __launch_bounds__(BT) resid_f32_kernel(const YT *__restrict__ ys
       }
     }
     float rr = 0.0f, q2 = 0.0f;
+    const int e16 = e16s;
+    const float s16 = pow2f(e16), inv16 = pow2f(-e16);
 #pragma unroll
     for (int v = 0; v < V; v++) {
       const float e[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
-      __nv_bfloat16 b[4];
+      __half b[4];
 #pragma unroll
       for (int c = 0; c < 4; c++) {
-        b[c] = __float2bfloat16_rn(e[c]);
-        const float d = __bfloat162float(b[c]) - e[c];  // exact in fp32
+        b[c] = __float2half_rn(e[c] * s16);
+        const float d = __half2float(b[c]) * inv16 - e[c];  // exact in fp32
         q2 = fmaf(d, d, q2);
         rr = fmaf(e[c], e[c], rr);
       }
-      __nv_bfloat162 lo, hi;
+      __half2 lo, hi;
       lo.x = b[0];
       lo.y = b[1];
       hi.x = b[2];
@@ -2201,7 +2247,7 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols_pad, 
   cuuint64_t strides[1] = {(cuuint64_t)cols_pad * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -2235,7 +2281,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
     return r;
   };
   TensorState st{};
-  st.r16 = (__nv_bfloat16 *)take(p_pad * n_pad * 2);
+  st.r16 = (__half *)take(p_pad * n_pad * 2);
   st.linv = (double *)take(p * kw * ((kw + 15) & ~int64_t(15)) * 8);
   st.z = (double *)take(p * kw * 8);
   st.rn2 = (double *)take(p * 8);
@@ -2244,6 +2290,7 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   st.dr = (double *)take(p * 8);
   st.rq = (double *)take(p * 8);
   st.emax = a.emax;
+  st.dinv = 1.0 / a.dscale;
   st.tol = (double *)take(p * 8);
   st.status = a.status;
   int *cidx = (int *)take(p * NCAND * 4);
@@ -2328,8 +2375,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
                              (int)ls_smem);
   if (e != cudaSuccess) return e;
   // E = c_err (|r~| + rq)(1 + 2^-7) dmax + emax (|r~| + rq) + dmax (rq + dr):
-  // the bf16 operands' rounding is charged exactly as measured -- emax =
-  // max_j |bf16(d_j) - d_j| (dictionary), rq = |bf16(r~) - r~| (per signal,
+  // the fp16 operands' rounding is charged exactly as measured (in unscaled
+  // units; the power-of-two operand scales cancel exactly) -- emax =
+  // max_j |d^_j - d_j| (dictionary), rq = |r^ - r~| (per signal,
   // per iteration), via <d^, r^> - <d, r~> = <d^ - d, r^> + <d, r^ - r~> --
   // and c_err covers the fp32 accumulation over n_pad terms and the
   // truncation of the packed epilogue keys (2^-18; 2^-15 kept as margin),
@@ -2570,17 +2618,18 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
 }
 
 // One correlation pass on caller-provided residual rows (debug / unit tests):
-// r16 = bf16(rows) (P x n fp32 device), candidate lists out.
-cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *rows, int64_t p,
-                            int *cand_idx, float *cand_val, float *cand_drop, int grid_cap,
-                            cudaStream_t stream) {
+// r16 = fp16(rows) (P x n fp32 device), candidate lists out (values divided
+// by the dictionary operand's scale).
+cudaError_t debug_corr_topk(const void *d16, double dscale, int64_t t, int64_t n,
+                            const float *rows, int64_t p, int *cand_idx, float *cand_val,
+                            float *cand_drop, int grid_cap, cudaStream_t stream) {
   const int64_t n_pad = (n + BK - 1) / BK * BK;
   const int64_t p_pad = (p + BM - 1) / BM * BM;
-  __nv_bfloat16 *r16 = nullptr;
+  __half *r16 = nullptr;
   cudaError_t e = cudaMallocAsync((void **)&r16, p_pad * n_pad * 2, stream);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(r16, 0, p_pad * n_pad * 2, stream);
-  to_bf16_rows<<<(unsigned)((p * n_pad + 255) / 256), 256, 0, stream>>>(rows, p, n, n_pad, r16);
+  to_f16_rows<<<(unsigned)((p * n_pad + 255) / 256), 256, 0, stream>>>(rows, p, n, n_pad, r16);
   CUtensorMap tm_a, tm_b;
   if (!make_map(&tm_a, r16, p_pad, n_pad, BMH) || !make_map(&tm_b, d16, t, n_pad, BN))
     return cudaErrorInvalidValue;
@@ -2597,6 +2646,8 @@ cudaError_t debug_corr_topk(const void *d16, int64_t t, int64_t n, const float *
                                                        m_tiles, nullptr, cand_idx, cand_val,
                                                        cand_drop, 1);
   note_launch();
+  unscale_vals<<<(unsigned)((p * NCAND + 255) / 256), 256, 0, stream>>>(cand_val, cand_drop, p,
+                                                                        (float)(1.0 / dscale));
   e = cudaGetLastError();
   cudaFreeAsync(r16, stream);
   return e;

@@ -92,15 +92,56 @@ def test_random_blocked(shape, engine):
     _check(ref, got, d, ys, eps, engine, allowed)
 
 
+def _clustered(n, t, k, p, seed, nc=12, spread=3e-4):
+    """Five clusters of `nc` atoms within `spread` of one direction: whenever a
+    cluster leads the scan more than 8 candidates sit inside the certification
+    window of the fp16 scan, so the pick cannot be certified from the top-8 list."""
+    rng = np.random.default_rng(seed)
+    d = rng.standard_normal((t, n))
+    heads = np.arange(0, 5 * nc, nc)
+    for c in heads:
+        d[c + 1:c + nc] = d[c] + spread * np.linalg.norm(d[c]) / np.sqrt(n) * \
+            rng.standard_normal((nc - 1, n))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    x = np.zeros((p, t))
+    for i in range(p):
+        sup = rng.choice(np.arange(5 * nc, t), size=min(k, t) - 1, replace=False)
+        x[i, sup] = rng.standard_normal(sup.size)
+        x[i, rng.choice(heads) + rng.integers(nc)] = 3.0 * (1 if rng.random() < 0.5 else -1)
+    ys = x @ d + 0.01 * rng.standard_normal((p, n))
+    return d, ys
+
+
 def test_tiled_rescan_matches_oracle(monkeypatch):
     """The tensor engine's tiled fp64 rescan (the large-dictionary path),
-    forced on shapes whose bf16 scans leave picks uncertified."""
+    forced on shapes whose fp16 scans leave picks uncertified (clusters of
+    more than 8 nearly parallel atoms) and on noisy near-tie problems."""
     from paper_1511_05174_b200 import _native as N
     monkeypatch.setenv("CDB_RESCAN", "tile")
     rescans = 0
     for n, t, k, p in ((129, 513, 16, 160), (256, 1000, 20, 200), (70, 300, 10, 130)):
+        d, ys = _clustered(n, t, k, p, n + t + 5)
+        eps = 1e-4 * np.linalg.norm(ys, axis=1)
+        ref = _oracle(d, ys, k, eps)
+        got = D.omp_batch_raw(D.DeviceDictionary(d), ys, p, k, eps, None, "tensor")
+        rescans += N.last_run_info()[2]
+        _check(ref, got, d, ys, eps, "tensor")
         d, ys = _problem(n, t, k, p, n + t + 5, True)
         ys += 0.2 * np.random.default_rng(n).standard_normal(ys.shape)  # noisy: near ties
+        eps = 1e-4 * np.linalg.norm(ys, axis=1)
+        ref = _oracle(d, ys, k, eps)
+        got = D.omp_batch_raw(D.DeviceDictionary(d), ys, p, k, eps, None, "tensor")
+        _check(ref, got, d, ys, eps, "tensor")
+    assert rescans > 0
+
+
+def test_grouped_rescan_matches_oracle(monkeypatch):
+    """The grouped exact rescan (small dictionaries) on the clustered problems."""
+    from paper_1511_05174_b200 import _native as N
+    monkeypatch.setenv("CDB_RESCAN", "group")
+    rescans = 0
+    for n, t, k, p in ((64, 256, 8, 150), (129, 513, 16, 100)):
+        d, ys = _clustered(n, t, k, p, n + t + 9)
         eps = 1e-4 * np.linalg.norm(ys, axis=1)
         ref = _oracle(d, ys, k, eps)
         got = D.omp_batch_raw(D.DeviceDictionary(d), ys, p, k, eps, None, "tensor")

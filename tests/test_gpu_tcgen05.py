@@ -1,6 +1,7 @@
-"""Unit test of the tcgen05 correlation kernel (TMA + UMMA bf16 + TMEM top-k
+"""Unit test of the tcgen05 correlation kernel (TMA + UMMA fp16 + TMEM top-k
 epilogue) against a plain PyTorch fp32 reference of the same op:
-c = bf16(R) . bf16(D)^T with exact bf16 products and fp32 sums."""
+c = fp16(R) . fp16(s D)^T / s with exact fp16 products and fp32 sums (s = 2^8
+over the largest atom norm's power of two: the dictionary operand's scale)."""
 
 import numpy as np
 import pytest
@@ -13,8 +14,9 @@ pytestmark = pytest.mark.gpu
 
 
 def reference_topk(rows, atoms):
-    r = torch.from_numpy(rows).cuda().to(torch.bfloat16).float()
-    d = torch.from_numpy(atoms).cuda().to(torch.bfloat16).float()
+    scale = 2.0 ** (8 - int(np.floor(np.log2(np.linalg.norm(atoms, axis=1).max()))))
+    r = torch.from_numpy(rows).cuda().to(torch.float16).float()
+    d = (torch.from_numpy(atoms).cuda() * scale).to(torch.float16).float() / scale
     c = (r @ d.T).abs()
     vals, idx = torch.sort(c, dim=1, descending=True)
     return c.cpu().numpy(), vals.cpu().numpy(), idx.cpu().numpy()
