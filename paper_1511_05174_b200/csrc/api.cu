@@ -291,11 +291,44 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
   CDB_CUDA(status.alloc(sizeof(uint32_t) * p, st));
   CDB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(uint32_t) * p, st));
   const int64_t per = cdb::tensor_state_bytes(1 << 16, d->n, kw) / (1 << 16) + 1;
-  int64_t chunk = kScratchBudget / per;
-  if (chunk < 128) chunk = 128;
-  if (chunk > p) chunk = p;
+  // State per chunk.  When the fp16 dictionary operand stays L2-resident
+  // (<= 32 MiB: every zero-tree step 1) a quarter of the device memory
+  // (45 GB on a B200, capped at 48 GiB): configs[4] step 1 on 1M signals is one
+  // 34 GB chunk instead of nine 4 GiB chunks -- 64 instead of 576 launches of
+  // every per-iteration kernel and no partial waves between chunks (1.747 ->
+  // 1.650 s per 1M signals).  A scan that streams its dictionary from HBM
+  // (configs[4] full OMP, 128 MB) keeps 4 GiB chunks: the CTAs sharing a
+  // dictionary part drift apart over a long launch and lose the L2 reuse
+  // (corr_topk 7.9 -> 9.3 s per 1M signals in one chunk).
+  // CDB_TENSOR_SCRATCH_GB overrides; an allocation that fails is retried at
+  // half the size.
+  int64_t budget = kScratchBudget;
+  if (2 * d->t * d->n_pad <= (int64_t(32) << 20)) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+      budget = std::min<int64_t>(std::max<int64_t>((int64_t)(total_b / 4), kScratchBudget),
+                                 int64_t(48) << 30);
+    else
+      cudaGetLastError();
+  }
+  if (const char *v = getenv("CDB_TENSOR_SCRATCH_GB")) {  // A/B switch: state per chunk
+    const int64_t gb = atoll(v);
+    if (gb >= 1 && gb <= 64) budget = gb << 30;
+  }
+  int64_t chunk = 0;
   DevBuf work;
-  CDB_CUDA(work.alloc((size_t)cdb::tensor_state_bytes(chunk, d->n, kw) + 65536, st));
+  for (;; budget /= 2) {
+    chunk = budget / per;
+    if (chunk < 128) chunk = 128;
+    if (chunk > p) chunk = p;
+    const cudaError_t ae =
+        work.alloc((size_t)cdb::tensor_state_bytes(chunk, d->n, kw) + 65536, st);
+    if (ae == cudaSuccess) break;
+    work.ptr = nullptr;
+    cudaGetLastError();  // clear the allocation failure before the smaller retry
+    if (ae != cudaErrorMemoryAllocation || chunk <= 128 || budget <= (int64_t(1) << 28))
+      return fail(CDB_ERR_NOMEM, "tensor engine state allocation");
+  }
   const size_t ysz = f32 ? 4 : 8;
   for (int64_t off = 0; off < p; off += chunk) {
     cdb::TensorArgs a{};

@@ -2115,7 +2115,10 @@ bool rescan_tiled(int64_t t, int64_t n, int64_t k_max) {
 
 cudaError_t tile_rescan_alloc(TileRescan &tr, int64_t p, int64_t t, int64_t n,
                               cudaStream_t stream) {
-  int64_t cap = (int64_t(256) << 20) / (8 * n);
+  // residual rows of the queued signals: up to 1 GiB, so a whole chunk of a
+  // small-N problem is one (residual, tile) launch pair per iteration (the
+  // pairs beyond the queue's length exit at once but still cost a launch)
+  int64_t cap = (int64_t(1024) << 20) / (8 * n);
   cap = cap / RT_S * RT_S;
   if (cap < RT_S) cap = RT_S;
   if (cap > p) cap = (p + RT_S - 1) / RT_S * RT_S;
