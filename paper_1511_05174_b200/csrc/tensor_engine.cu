@@ -1579,6 +1579,151 @@ __device__ __forceinline__ float4 ldg_nc_f4(const float4 *p) {
   return r;
 }
 
+// Split-mode scan operand for long rows (N = 1024 J <= 4096: cfg 4 full OMP),
+// the row stream on the bulk-copy engine: one producer lane walks the same
+// signal list as the consumers and keeps a ring of RB_S whole fp32 atom rows
+// (4 N bytes each) in flight with 1-D cp.async.bulk copies that complete on
+// mbarriers, so the bytes in flight per SM (2 CTAs x RB_S x 16 KB) no longer
+// depend on registers; 256 consumer threads read each landed row from shared
+// memory (16-byte, conflict-free) and run the same fp64 FMA chain in the same
+// order as resid_split_kernel -- bit-identical operands and bounds.  The
+// producer runs ahead across signal boundaries: the next signal's rows land
+// while the consumers convert and store the current operand.
+constexpr int RB_T = 256;  // consumer threads
+constexpr int RB_S = 6;    // ring stages
+template <typename YT, int J>
+__global__ void __launch_bounds__(RB_T + 32) resid_bulk_kernel(
+    const YT *__restrict__ ys, const float *__restrict__ d32, int64_t p, int64_t n, int64_t n_pad,
+    int64_t kw, double dmax, TensorState st, const int64_t *out_sel, const double *out_coef,
+    const int64_t *out_count) {
+  extern __shared__ __align__(128) unsigned char rbsm[];
+  float *ring = (float *)rbsm;                                  // RB_S x n
+  double *xv = (double *)(rbsm + (size_t)RB_S * n * 4);         // kw
+  uint64_t *full = (uint64_t *)(xv + kw), *empty = full + RB_S;  // RB_S each
+  __shared__ double red[3][RB_T / 32];
+  __shared__ int e16s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < RB_S; s++) {
+      sm100::mbar_init(full + s, 1);
+      sm100::mbar_init(empty + s, RB_T / 32);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t row_bytes = (uint32_t)(n * 4);
+  uint32_t cnt = 0;  // rows issued (producer) / consumed (consumers): same sequence
+  if (warp == RB_T / 32) {
+    // ---- producer warp (lane 0 issues; all lanes hold the support ids)
+    for (int64_t sig = blockIdx.x; sig < p; sig += gridDim.x) {
+      if (!(st.status[sig] & ST_RESID)) continue;
+      const int kd = (int)out_count[sig];
+      const int64_t id0 = lane < kd ? out_sel[sig * kw + lane] : 0;
+      const int64_t id1 = lane + 32 < kd ? out_sel[sig * kw + lane + 32] : 0;
+      for (int l = 0; l < kd; l++, cnt++) {
+        const int64_t id = __shfl_sync(CDB_FULL_MASK, l < 32 ? id0 : id1, l & 31);
+        if (lane == 0) {
+          const uint32_t stage = cnt % RB_S;
+          sm100::mbar_wait(empty + stage, ((cnt / RB_S) & 1) ^ 1);
+          sm100::mbar_expect_tx(full + stage, row_bytes);
+          sm100::bulk_load(ring + (size_t)stage * n, d32 + id * n, row_bytes, full + stage);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  for (int64_t sig = blockIdx.x; sig < p; sig += gridDim.x) {
+    if (!(st.status[sig] & ST_RESID)) continue;  // uniform across the CTA
+    const int kd = (int)out_count[sig];
+    asm volatile("bar.sync 1, %0;" ::"n"(RB_T) : "memory");  // the previous signal's xv is consumed
+    double sx = 0.0;
+    if (tid < kd) {
+      const double c = out_coef[sig * kw + tid];
+      xv[tid] = c;
+      sx = fabs(c);
+    }
+    if (tid == 0) e16s = scan_scale_exp(st.rn2[sig], st.yy[sig]);
+    asm volatile("bar.sync 1, %0;" ::"n"(RB_T) : "memory");
+    const YT *y = ys + sig * n;
+    double acc[J][4];
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+      const int64_t i = 4 * (tid + (int64_t)RB_T * j);
+      if constexpr (sizeof(YT) == 4) {
+        const float4 v = *(const float4 *)(y + i);
+        acc[j][0] = (double)v.x, acc[j][1] = (double)v.y, acc[j][2] = (double)v.z,
+        acc[j][3] = (double)v.w;
+      } else {
+        const double2 a = *(const double2 *)(y + i), b = *(const double2 *)(y + i + 2);
+        acc[j][0] = (double)a.x, acc[j][1] = (double)a.y, acc[j][2] = (double)b.x,
+        acc[j][3] = (double)b.y;
+      }
+    }
+    for (int l = 0; l < kd; l++, cnt++) {
+      const uint32_t stage = cnt % RB_S;
+      sm100::mbar_wait(full + stage, (cnt / RB_S) & 1);
+      const double xl = -xv[l];
+      const float4 *row = (const float4 *)(ring + (size_t)stage * n) + tid;
+      float4 v[J];
+#pragma unroll
+      for (int j = 0; j < J; j++) v[j] = row[RB_T * j];
+#pragma unroll
+      for (int j = 0; j < J; j++) {
+        acc[j][0] = fma(xl, (double)v[j].x, acc[j][0]);
+        acc[j][1] = fma(xl, (double)v[j].y, acc[j][1]);
+        acc[j][2] = fma(xl, (double)v[j].z, acc[j][2]);
+        acc[j][3] = fma(xl, (double)v[j].w, acc[j][3]);
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(empty + stage);
+    }
+    // ---- fp16(s r~) with its exact rounding error, |r~|^2
+    const int e16 = e16s;
+    const double s16 = pow2d(e16), inv16 = pow2d(-e16);
+    double rr = 0.0, q2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+      __half b[4];
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const double a = acc[j][c];
+        b[c] = __float2half_rn((float)(a * s16));
+        const double e = (double)__half2float(b[c]) * inv16 - a;
+        q2 = fma(e, e, q2);
+        rr = fma(a, a, rr);
+      }
+      __half2 lo, hi;
+      lo.x = b[0], lo.y = b[1], hi.x = b[2], hi.y = b[3];
+      uint2 pk;
+      pk.x = *(uint32_t *)&lo;
+      pk.y = *(uint32_t *)&hi;
+      *(uint2 *)(st.r16 + sig * n_pad + 4 * (tid + (int64_t)RB_T * j)) = pk;
+    }
+    rr = warp_sum(rr);
+    sx = warp_sum(sx);
+    q2 = warp_sum(q2);
+    if (lane == 0) {
+      red[0][warp] = rr;
+      red[1][warp] = sx;
+      red[2][warp] = q2;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(RB_T) : "memory");
+    if (tid == 0) {
+      double a = 0.0, b = 0.0, c = 0.0;
+      for (int w = 0; w < RB_T / 32; w++) {
+        a += red[0][w];
+        b += red[1][w];
+        c += red[2][w];
+      }
+      st.rq[sig] = sqrt(c) * (1.0 + 1e-12);
+      st.rt[sig] = sqrt(a);
+      st.dr[sig] = 0x1p-24 * b * dmax * 1.0000001;  // |(D64 - D32) x| bound
+      st.status[sig] &= ~ST_RESID;
+    }
+  }
+}
+
 // fp32 split-mode scan operand: the same r~ = y - D32_S x, accumulated in
 // fp32 with 16-byte loads (V float4 per thread per atom row, 8 rows in
 // flight), packed fp16 stores.  The scan's error budget charges the fp32
@@ -2584,6 +2729,35 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       }
 #undef CDB_RESID32
 #undef CDB_RESID32G
+      // long rows: the bulk-copy ring (CDB_RESID_BULK=0: the register-pipelined kernel)
+      static const bool bulk_ok = !(getenv("CDB_RESID_BULK") && atoi(getenv("CDB_RESID_BULK")) == 0);
+      if (!done32 && bulk_ok && n % 1024 == 0 && n <= 4096 && kw <= 64) {
+        done32 = true;
+        const size_t bsm = (size_t)RB_S * n * 4 + 8 * (size_t)kw + 16 * RB_S;
+        const unsigned bg = (unsigned)(a.num_sms * 2);
+#define CDB_RESIDB(J_)                                                                          \
+  {                                                                                             \
+    auto kf = resid_bulk_kernel<float, J_>;                                                     \
+    auto kd_ = resid_bulk_kernel<double, J_>;                                                   \
+    if (a.ys_f32) {                                                                             \
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);      \
+      if (e == cudaSuccess)                                                                     \
+        kf<<<bg, RB_T + 32, bsm, stream>>>((const float *)a.ys, a.d32, p, n, n_pad, kw, a.dmax, \
+                                           st, a.out_sel, a.out_coef, a.out_count);             \
+    } else {                                                                                    \
+      e = cudaFuncSetAttribute(kd_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);     \
+      if (e == cudaSuccess)                                                                     \
+        kd_<<<bg, RB_T + 32, bsm, stream>>>((const double *)a.ys, a.d32, p, n, n_pad, kw,       \
+                                            a.dmax, st, a.out_sel, a.out_coef, a.out_count);    \
+    }                                                                                           \
+  }
+        if (n == 1024) CDB_RESIDB(1)
+        else if (n == 2048) CDB_RESIDB(2)
+        else if (n == 3072) CDB_RESIDB(3)
+        else CDB_RESIDB(4)
+#undef CDB_RESIDB
+        if (e != cudaSuccess) return e;
+      }
       if (!done32) {
 #define CDB_RESID(BT_)                                                                          \
   if (a.ys_f32)                                                                                 \
