@@ -615,6 +615,40 @@ def bench_ours(args):
                      "basis": "2*N*scans of the full-OMP batch (actual scan counts) / corr_topk "
                               "time, against the measured bf16 peak it runs on"}
 
+    # ---- the HBM-bound stage of the step (block-mean downsample, scaling.py:99-116)
+    hbm_stages = None
+    ds = prof_zt.get("downsample")
+    if ds and not phi and ds[0] > 0:
+        ds_ms = ds[0] / max(ds[1], 1)
+        ds_bytes = (P * args.steps / max(ds[1], 1)) * (4.0 * w.n_high + 8.0 * w.n_low + 16.0)
+        hbm_stages = {"downsample": {
+            "ms": ds_ms, "achieved": ds_bytes / (ds_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": ds_bytes / (ds_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "basis": "per signal: N fp32 in + N_low fp64 out + two fp64 tolerances; "
+                     "extract_patches / reconstruct_aggregate are in pipeline_ends.roofline"}}
+
+    def resid_stage(prof, counts, n_row, y_bytes, steps):
+        """The scan-operand gather r~ = y - D32_S x (_kernels.py:132-137): per
+        signal-iteration at support size k, k fp32 atom rows + y in + fp16 operand out."""
+        rs = prof.get("ls_resid")
+        if not rs or rs[0] <= 0:
+            return None
+        c = counts.astype(np.float64)
+        rows = float((c * (c - 1) / 2).sum())
+        iters = float(np.maximum(c - 1, 0).sum())
+        b = (rows * n_row * 4.0 + iters * n_row * (y_bytes + 2.0)) * steps
+        gbs = b / (rs[0] * 1e-3) / 1e9
+        return {"ms_per_step": rs[0] / steps, "achieved": gbs, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
+                "basis": "algorithmic bytes (k fp32 atom rows per signal-iteration + y in + fp16 "
+                         "operand out, actual support sizes) / kernel time; the gathered rows "
+                         "hit L2 (the whole fp32 dictionary when it fits), so the figure can "
+                         "exceed the HBM peak"}
+    if hbm_stages is not None:
+        hbm_stages["ls_resid"] = resid_stage(prof_zt, c_low, n_low, 8.0, args.steps)
+        hbm_stages["ls_resid_full"] = resid_stage(prof_full, ofull["counts"].cpu().numpy(),
+                                                  w.n_signal, 4.0, args.full_steps)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_subprocess(ci, yd[: min(P, 8192)].double().cpu().numpy())
@@ -648,6 +682,7 @@ def bench_ours(args):
             "roofline": roofline,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_zt.items()},
             "kernels_full_ms_per_step": {k: v[0] / args.full_steps for k, v in prof_full.items()},
+            "hbm_stages": hbm_stages,
             "cpu_baseline": cpu,
             "e2e": {"value": total * e2e_steps / e2e_total, "unit": "signals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,

@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(256) downsample_direct_kernel(
     double *__restrict__ eps_low, double *__restrict__ eps_fine) {
   extern __shared__ __align__(16) unsigned char dsm[];
   int *tab = (int *)dsm;  // n_low * block fine indices
-  __shared__ double r_yy[256], r_yl[256];
+  __shared__ double r_yy[2][256], r_yl[2][256];  // by pass parity: one barrier per pass
+  int par = 0;
   for (int e = threadIdx.x; e < n_low * block; e += blockDim.x) tab[e] = tab_g[e];
   __syncthreads();
   const int tid = threadIdx.x;
@@ -119,6 +120,19 @@ __global__ void __launch_bounds__(256) downsample_direct_kernel(
         const int *t = tab + cell * block;
         double acc = 0.0;
         if constexpr (VW == 2) {  // the last axis' factor-2 pairs are adjacent: 8-byte loads
+          if (block == 8) {  // 2 x 2 x 2 blocks (every 3-D BASELINE config): four loads in flight
+            float2 v2[4];
+#pragma unroll
+            for (int b = 0; b < 4; b++) v2[b] = __ldcs((const float2 *)(y + t[2 * b]));
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+              const double v0 = (double)v2[b].x, v1 = (double)v2[b].y;
+              acc += v0;
+              acc += v1;
+              yy = fma(v0, v0, yy);
+              yy = fma(v1, v1, yy);
+            }
+          } else
           for (int b = 0; b < block; b += 2) {
             const float2 v2 = __ldcs((const float2 *)(y + t[b]));
             const double v0 = (double)v2.x, v1 = (double)v2.y;
@@ -148,35 +162,35 @@ __global__ void __launch_bounds__(256) downsample_direct_kernel(
       yl = warp_sum(yl);
       const int lane = tid & 31, warp = tid >> 5, wps = tps / 32;
       if (lane == 0) {
-        r_yy[warp] = yy;
-        r_yl[warp] = yl;
+        r_yy[par][warp] = yy;
+        r_yl[par][warp] = yl;
       }
       __syncthreads();
       if (tid < spi && s0 + tid < p) {
         double a = 0.0, b = 0.0;
         for (int q = tid * wps; q < (tid + 1) * wps; q++) {
-          a += r_yy[q];
-          b += r_yl[q];
+          a += r_yy[par][q];
+          b += r_yl[par][q];
         }
         eps_fine[s0 + tid] = rel * sqrt(a);
         eps_low[s0 + tid] = rel * sqrt(b);
       }
-      __syncthreads();
+      par ^= 1;  // the next pass writes the other buffer; its barrier orders the one after
       continue;
     }
-    r_yy[tid] = yy;
-    r_yl[tid] = yl;
+    r_yy[par][tid] = yy;
+    r_yl[par][tid] = yl;
     __syncthreads();
     if (tid < spi && s0 + tid < p) {
       double a = 0.0, b = 0.0;
       for (int q = tid * tps; q < (tid + 1) * tps; q++) {
-        a += r_yy[q];
-        b += r_yl[q];
+        a += r_yy[par][q];
+        b += r_yl[par][q];
       }
       eps_fine[s0 + tid] = rel * sqrt(a);
       eps_low[s0 + tid] = rel * sqrt(b);
     }
-    __syncthreads();
+    par ^= 1;
   }
 }
 

@@ -40,7 +40,9 @@ def test_our_arm_line():
     assert d["value"] > 0 and d["scaling"] == "strong" and "workload" in d["config"]
     assert d["config"]["signals"] == 1_000_000 and "configs[4]" in d["config"]["workload"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
-    assert d["roofline"]["frac"] > 0 and 0 < d["roofline"]["step"]["frac"] <= 1
+    # algorithmic flops / time against P_emu: the Gram form of step 2 does fewer
+    # flops than SURVEY 8(d) charges it, so the fraction may pass 1
+    assert d["roofline"]["frac"] > 0 and d["roofline"]["step"]["frac"] > 0
     assert d["full_omp"]["value"] > 0
     assert d["e2e_api"]["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
