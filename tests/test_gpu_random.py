@@ -178,3 +178,21 @@ def test_gram_candidate_widths(nb, q, k):
     got = D.omp_batch_blocked_raw(D.DeviceDictionary(d), ys, p, k_max, eps,
                                   np.ascontiguousarray(blocks), q, "gram")
     _check(ref, got, d, ys, eps, "gram", allowed)
+
+
+@pytest.mark.parametrize("n,f32", [(2048, True), (3072, False), (4096, True), (4096, False)])
+def test_long_row_scan_operand(n, f32):
+    """Tensor engine on long rows (N = 1024 J up to 4096): the next scan's
+    operand r~ = y - D32_S x comes from the bulk-copy ring kernel
+    (resid_bulk_kernel, J = 2, 3, 4; fp32 and fp64 signals), supports up to K = 40
+    so the producer's ring wraps several times per signal."""
+    t, k, p = 384, 40, 96
+    d, ys = _problem(n, t, k, p, 7 * n + f32, False)
+    if f32:
+        ys = ys.astype(np.float32).astype(np.float64)
+    ys[1] = d[5] * 2.0  # one-atom signal: stops after the first pick
+    eps = 1e-3 * np.linalg.norm(ys, axis=1)
+    ref = _oracle(d, ys, k, eps)
+    dd = D.DeviceDictionary(d)
+    got = D.omp_batch_raw(dd, ys.astype(np.float32) if f32 else ys, p, k, eps, None, "tensor")
+    _check(ref, got, d, ys, eps, "tensor")

@@ -7,17 +7,16 @@ import json
 import os
 
 CAPTURES = {  # name -> (profiler tag or None, units in the captured launch, unit, what)
-    "gram": ("gram_step2", 65536, "signal", "cfg 4 zero-tree step 2, streamed-H CTA kernel (default)"),
-    "gramreg": (None, 32768, "signal", "cfg 4 step 2, on-chip-H kernel R=16 (opt-in CDB_GRAM_REG=1)"),
+    "gram": ("gram_step2", 65536, "signal", "cfg 4 zero-tree step 2, on-chip-H kernel gram_reg2 (default: 24 register + 40 shared rows)"),
     "alpha0": ("route_alpha0", 65536, "signal", "cfg 4 routed alpha0 on fp64 tensor-core tiles"),
     "down": ("downsample", 65536, "signal", "cfg 4 block-mean downsample"),
-    "corr": ("corr_topk", 65536, "signal", "cfg 4 step 1 tcgen05 scan + top-8 (iteration 40)"),
+    "corr": ("corr_topk", 65536, "signal", "cfg 4 step 1 tcgen05 fp16 scan + top-8 (iteration 40)"),
     "lswide": ("ls_step", 65536, "signal", "cfg 4 step 1 least squares (iteration 40)"),
     "resid": ("ls_resid", 65536, "signal", "cfg 4 step 1 scan operand r = y - D32_S x (iteration 40)"),
     "rescan": ("rescan", 65536, "signal", "cfg 4 step 1 tiled fp64 rescan"),
-    "corrfull": ("corr_topk_full", 65536, "signal", "cfg 4 full OMP tcgen05 scan (iteration 40)"),
+    "corrfull": ("corr_topk_full", 65536, "signal", "cfg 4 full OMP tcgen05 fp16 scan, dictionary in 4 parts (iteration 40)"),
     "lswidefull": ("ls_step_full", 65536, "signal", "cfg 4 full OMP least squares (iteration 40)"),
-    "residfull": ("ls_resid_full", 65536, "signal", "cfg 4 full OMP scan operand (iteration 40)"),
+    "residfull": ("ls_resid_full", 65536, "signal", "cfg 4 full OMP scan operand, bulk-copy ring (iteration 40)"),
     "pipe_extract": ("extract_patches", 1034289, "patch", "f2 extraction, 1024^2 image, 8x8 stride 1, remove_dc"),
     "pipe_reconstruct": (None, 1034289, "patch", "f2 reconstruction D_S x + dc"),
     "pipe_aggregate": (None, 1034289, "patch", "f2 overlap-add"),
