@@ -13,7 +13,7 @@ CAPTURES = {  # name -> (profiler tag or None, units in the captured launch, uni
     "corr": ("corr_topk", 65536, "signal", "cfg 4 step 1 tcgen05 fp16 scan + top-8 (iteration 40)"),
     "lswide": ("ls_step", 65536, "signal", "cfg 4 step 1 least squares (iteration 40)"),
     "resid": ("ls_resid", 65536, "signal", "cfg 4 step 1 scan operand r = y - D32_S x (iteration 40)"),
-    "rescan": ("rescan", 65536, "signal", "cfg 4 step 1 tiled fp64 rescan"),
+    "rescan": ("rescan", 65536, "signal", "cfg 4 step 1 tiled fp64 rescan (launch 20: queue nearly empty under the fp16 scan)"),
     "corrfull": ("corr_topk_full", 65536, "signal", "cfg 4 full OMP tcgen05 fp16 scan, dictionary in 4 parts (iteration 40)"),
     "lswidefull": ("ls_step_full", 65536, "signal", "cfg 4 full OMP least squares (iteration 40)"),
     "residfull": ("ls_resid_full", 65536, "signal", "cfg 4 full OMP scan operand, bulk-copy ring (iteration 40)"),
