@@ -343,6 +343,13 @@ cdb_status cdb_csd_parse(const uint8_t *data, int64_t size, const char *name,
 cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_size, void *rows,
                               int threads);
 
+/* 1 when two host buffers hold the same nbytes bytes, else 0 (memcmp split over
+ * `threads` host threads, <= 0: all cores).  The host layer confirms a cached
+ * device dictionary against its stored host copy with it, so a matrix the
+ * caller changed in place (pursuit.py:84-94 keeps no such cache: the reference
+ * re-reads `columns` on every call) is staged again. */
+int cdb_host_equal(const void *a, const void *b, int64_t nbytes, int threads);
+
 /* Number of kernels this library has launched since load (instrumentation). */
 int64_t cdb_launch_count(void);
 

@@ -27,7 +27,7 @@ SYMBOLS = ("cdb_last_error", "cdb_device_info", "cdb_dictionary_create",
            "cdb_debug_corr_topk", "cdb_rows_from_cols", "cdb_extract_patches",
            "cdb_reconstruct_aggregate", "cdb_aggregate_patches", "cdb_csd_read", "cdb_csd_parse",
            "cdb_omp_batch_blocked_ragged", "cdb_omp_batch_masked", "cdb_omp_batch_coded", "cdb_ksvd_update",
-           "cdb_zero_tree_batch_cols", "cdb_omp_batch_cols")
+           "cdb_zero_tree_batch_cols", "cdb_omp_batch_cols", "cdb_host_equal")
 
 _lib = None
 
@@ -52,6 +52,8 @@ def load():
     lib.cdb_device_info.argtypes = [P, P, P]
     lib.cdb_last_run_info.argtypes = [P, P, P]
     lib.cdb_rows_from_cols.argtypes = [P, I64, I64, I32, P, I32]
+    lib.cdb_host_equal.argtypes = [P, P, I64, I32]
+    lib.cdb_host_equal.restype = I32
     lib.cdb_extract_patches.argtypes = [P, I32, I32, P, P, P, I32, P, P, P]
     lib.cdb_reconstruct_aggregate.argtypes = [P, P, P, I64, I64, P, I32, P, P, P, P, P, P]
     lib.cdb_aggregate_patches.argtypes = [P, P, I32, P, P, P, P, P, P]
@@ -84,7 +86,7 @@ def load():
     lib.cdb_omp_batch_cols.argtypes = [P, P, I32, I64, I64, I64, P, D, P, P, P, P, P, P, I32, P]
     for name in ("cdb_device_info", "cdb_dictionary_create", "cdb_dictionary_destroy",
                  "cdb_omp_batch", "cdb_omp_batch_blocked", "cdb_zero_tree_batch",
-                 "cdb_zero_tree_batch_cols", "cdb_omp_batch_cols"):
+                 "cdb_zero_tree_batch_cols", "cdb_omp_batch_cols", "cdb_host_equal"):
         getattr(lib, name).restype = I32
     _lib = lib
     return lib

@@ -1325,6 +1325,28 @@ cdb_status cdb_rows_from_cols(const void *cols, int64_t n, int64_t p, int elem_s
   return CDB_OK;
 }
 
+int cdb_host_equal(const void *a, const void *b, int64_t nbytes, int threads) {
+  if (nbytes <= 0 || a == b) return 1;
+  if (!a || !b) return 0;
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int64_t piece = int64_t(1) << 20;  // threads stop at the first differing 1 MiB piece
+  const int64_t pieces = (nbytes + piece - 1) / piece;
+  if (threads > pieces) threads = (int)pieces;
+  std::atomic<int> differ{0};
+  auto work = [&](int tid) {
+    for (int64_t i = tid; i < pieces && !differ.load(std::memory_order_relaxed); i += threads) {
+      const int64_t o = i * piece, len = std::min(piece, nbytes - o);
+      if (memcmp((const uint8_t *)a + o, (const uint8_t *)b + o, (size_t)len) != 0)
+        differ.store(1, std::memory_order_relaxed);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto &t : pool) t.join();
+  return differ.load() ? 0 : 1;
+}
+
 void cdb_last_run_info(int *engine, int *delegated, int *rescans) {
   if (engine) *engine = g_last_engine;
   int h[2] = {0, 0};

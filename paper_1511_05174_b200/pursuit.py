@@ -94,6 +94,13 @@ class DenseColumns:
             self._mat_t = np.ascontiguousarray(self.mat.T)
         return self._mat_t
 
+    def device(self):
+        """The staged device dictionary: from `mat` itself (no host transpose
+        on a cache hit) unless the rows are already at hand."""
+        if self._mat_t is None:
+            return _dev.device_dictionary_cols(self.mat)
+        return _dev.device_dictionary(self._mat_t)
+
     def column(self, j0: int) -> np.ndarray:
         return self.mat[:, j0]
 
@@ -204,7 +211,7 @@ def omp(columns, y, config) -> PursuitResult:
                 f"sparsity_budget {k_max} exceeds |allowed_support| = {allowed0.size}")
     ynorm = float(np.linalg.norm(y))
     eps = np.array([_resolve_eps(config, ynorm)])
-    dd = _dev.device_dictionary(cols.mat_t)
+    dd = cols.device()
     o = _dev.omp_batch_raw(dd, y.reshape(1, -1), 1, k_max, eps,
                            None if allowed0 is None else allowed0.reshape(1, -1), ENGINE)
     c = int(o["counts"][0])
@@ -254,7 +261,7 @@ def omp_many_arrays(columns, ys, config, *, allowed_blocks=None, block_q=None):
         eps = None
         if config.residual_tolerance is not None:
             eps = np.full(p_all, float(config.residual_tolerance))
-        o = _dev.omp_cols_raw(_dev.device_dictionary(cols.mat_t), ys, k_max, eps, _rel_tol(),
+        o = _dev.omp_cols_raw(cols.device(), ys, k_max, eps, _rel_tol(),
                               ENGINE)
         return _make_batch(t, o)
     ys_rows = _dev.rows_for_device(ys)
@@ -270,7 +277,7 @@ def omp_many_arrays(columns, ys, config, *, allowed_blocks=None, block_q=None):
                  rnorm=np.linalg.norm(ys_rows.astype(np.float64), axis=1),
                  scans=np.zeros(p_all, np.int64), flag=np.zeros(p_all, np.uint8))
         return _make_batch(t, o)
-    dd = _dev.device_dictionary(cols.mat_t)
+    dd = cols.device()
     if blocks is not None:
         o = _dev.omp_batch_blocked_raw(dd, ys_rows, p_all, k_max, eps,
                                        np.ascontiguousarray(blocks), block_q, ENGINE)

@@ -56,3 +56,18 @@ def test_rows_from_cols_host_transpose(dtype, shape):
     assert np.array_equal(rows, cols.T)
     with pytest.raises(N.NativeError):
         N.check(N.load().cdb_rows_from_cols(N.ptr(cols), n, p, 2, N.ptr(rows), 1))
+
+
+@pytest.mark.parametrize("nbytes", [0, 1, 4096, (1 << 20) + 17, 5 * (1 << 20) + 3])
+def test_host_equal(nbytes):
+    # cdb_host_equal is host code: the exact check behind the dictionary cache
+    a = np.random.default_rng(nbytes).integers(0, 256, size=max(nbytes, 1), dtype=np.uint8)
+    b = a.copy()
+    lib = N.load()
+    assert lib.cdb_host_equal(N.ptr(a), N.ptr(b), nbytes, 3) == 1
+    assert lib.cdb_host_equal(N.ptr(a), N.ptr(a), nbytes, 0) == 1
+    for pos in {0, nbytes // 2, nbytes - 1} if nbytes else ():
+        b[pos] ^= 1
+        assert lib.cdb_host_equal(N.ptr(a), N.ptr(b), nbytes, 3) == 0, pos
+        b[pos] ^= 1
+    assert lib.cdb_host_equal(N.ptr(a), N.ptr(b), nbytes, 1) == 1

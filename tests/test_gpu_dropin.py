@@ -272,3 +272,31 @@ def test_omp_many_arrays_cols_path(case, rel_tol):
     assert np.array_equal(s.scans, r["scans"])
     np.testing.assert_allclose(s.alpha, r["alpha"], rtol=1e-12, atol=1e-14)
     np.testing.assert_allclose(s.rnorm, r["rnorm"], rtol=1e-12, atol=1e-14)
+
+
+def test_column_matrix_cache_follows_in_place_changes(rel_tol):
+    """omp_many_arrays stages `columns` once per content: a second call on the
+    same matrix reuses the device dictionary (no new staging), and a matrix
+    changed in place -- the reference re-reads it on every call,
+    pursuit.py:84-94 -- is staged again instead of served from the cache."""
+    from paper_1511_05174_b200 import device as D
+    rel_tol(1e-3)
+    rng = np.random.default_rng(11)
+    n, t, p, k = 64, 8192 + 512, 48, 4  # 4.4 MB: the threaded comparison path
+    mat = rng.standard_normal((n, t))
+    mat /= np.linalg.norm(mat, axis=0, keepdims=True)
+    picks = rng.choice(t, size=p, replace=False)
+    ys = np.ascontiguousarray(mat[:, picks])  # one-atom signals
+    s1 = P.omp_many_arrays(mat, ys, PU.PursuitConfig(k))
+    assert np.array_equal(s1.sel[:, 0], picks) and np.all(s1.counts == 1)
+    dd1 = D.device_dictionary_cols(mat)
+    assert D.device_dictionary_cols(mat) is dd1  # a hit: same handle
+    # swap two atoms in place (the sampled entries 0, size/3, size/2, size-1 keep their values)
+    a, b = int(picks[0]), int(picks[1])
+    if {a, b} & {0, t - 1, (n * t // 3) % t, (n * t // 2) % t}:
+        pytest.skip("sampled column touched")
+    mat[:, [a, b]] = mat[:, [b, a]]
+    s2 = P.omp_many_arrays(mat, ys, PU.PursuitConfig(k))
+    assert s2.sel[0, 0] == b and s2.sel[1, 0] == a
+    assert np.array_equal(s2.sel[2:, 0], picks[2:])
+    assert D.device_dictionary_cols(mat) is not dd1

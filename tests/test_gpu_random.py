@@ -188,9 +188,9 @@ def test_long_row_scan_operand(n, f32):
     so the producer's ring wraps several times per signal."""
     t, k, p = 384, 40, 96
     d, ys = _problem(n, t, k, p, 7 * n + f32, False)
+    ys[1] = d[5] * 2.0  # one-atom signal: stops after a pick or two
     if f32:
         ys = ys.astype(np.float32).astype(np.float64)
-    ys[1] = d[5] * 2.0  # one-atom signal: stops after the first pick
     eps = 1e-3 * np.linalg.norm(ys, axis=1)
     ref = _oracle(d, ys, k, eps)
     dd = D.DeviceDictionary(d)

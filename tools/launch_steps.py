@@ -19,7 +19,7 @@ scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "m
 seq = []
 for r in rows[hdr + 1:]:
     if len(r) > mv:
-        name = r[kn].split("(")[0].replace("void ", "").replace("cdb::<unnamed>::", "")
+        name = r[kn].split("(")[0].replace("void ", "").replace("cdb::<unnamed>::", "").replace("unnamed>::", "")
         seq.append((name, float(r[mv].replace(",", "")) * scale.get(r[mu], 1e-6)))
 
 
@@ -41,7 +41,8 @@ def segments(start, end):
 
 
 for label, start, end in (("zero-tree call (configs[1], 100k signals)", "downsample_kernel<float>", "gram_omp_kernel"),
-                          ("full-OMP call (configs[1], 100k signals)", "ls_init_kernel<float>", "ls_final_kernel")):
+                          ("full-OMP call (configs[1], 100k signals)", "ls_init_kernel<float>", "ls_final_kernel"),
+                          ("zero-tree step (configs[4], 1M signals)", "downsample_direct_kernel<float, 2>", "gram_reg2_kernel")):
     segs = segments(start, end)[: int(sys.argv[2]) if len(sys.argv) > 2 else 5]
     if not segs:
         continue
