@@ -355,6 +355,21 @@ def cpu_baseline_subprocess(ci, ys_host):
 
 
 # ------------------------------------------------------------------ reference arm
+def workload_config(ci, total, world):
+    """The `config` object of both arms' lines: the same workload, named once."""
+    w = W.CONFIGS[ci]
+    per = -(-total // world)
+    return {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP: "
+                        f"N={w.n_high}, N_low={w.n_low}, T_high={w.t_high}, "
+                        f"T_low={w.t_low}, Q={w.q}, K={w.k}, {total:,} signals "
+                        f"split over {world} GPU(s), stop K or |r|<=1e-3|y|",
+            "signals": total, "signals_per_gpu": per,
+            "parallelism": f"signal shards x{world}, dictionary replicated",
+            "l2": f"flushed between steps (256 MiB write); inputs {total * w.n_high * 4 / 1e9:.1f} GB"
+                  " > L2" if total * w.n_high * 4 > (126 << 20) else
+                  "flushed between steps (256 MiB write)"}
+
+
 def bench_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -406,8 +421,10 @@ def bench_reference(args):
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator, fp32-exact inputs)",
-        "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP",
-                   "signals_per_step": sample},
+        # the workload of our arm's line; each reference step codes a bounded
+        # sample of it (cpu_baseline.sample)
+        "config": workload_config(ci, args.num_signals or w.signals, world),
+        "signals_per_step": sample,
         "cpu_baseline": {"value": value, "unit": "signals/s", "cores": threads, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "signals/s", "h2d_bytes_per_step": 0,
@@ -667,13 +684,7 @@ def bench_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE generator drawn on the device, fp32 inputs, "
                     "fp64 dictionaries)",
-            "config": {"workload": f"{w.name} (BASELINE configs[{ci}]) zero-tree OMP: "
-                                   f"N={w.n_high}, N_low={w.n_low}, T_high={w.t_high}, "
-                                   f"T_low={w.t_low}, Q={w.q}, K={w.k}, {total:,} signals "
-                                   f"split over {world} GPU(s), stop K or |r|<=1e-3|y|",
-                       "signals": total, "signals_per_gpu": P,
-                       "parallelism": f"signal shards x{world}, dictionary replicated",
-                       "l2": "flushed between steps (256 MiB write); inputs 16.4 GB > L2"},
+            "config": workload_config(ci, total, world),
             "full_omp": {"value": full_value, "unit": "signals/s", "steps": args.full_steps,
                          "ms_per_step": full_ms / args.full_steps, "engine": engine_full[0],
                          "exact_rescans": engine_full[2], "roofline": full_roof,

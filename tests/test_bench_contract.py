@@ -30,7 +30,9 @@ def test_reference_arm_line():
     has_ref = os.path.isdir(os.path.join(REPO, "baseline", "_ref", "crossdict"))
     assert d["cpu_baseline"]["kind"] == ("reference" if has_ref else "port")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert "workload" in d["config"]
+    # the same config object as our arm's line; the bounded sample is named beside it
+    assert d["config"]["signals"] == 1_000_000 and "configs[4]" in d["config"]["workload"]
+    assert d["signals_per_step"] > 0
 
 
 @pytest.mark.gpu
