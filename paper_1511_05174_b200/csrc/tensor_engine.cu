@@ -2569,7 +2569,12 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   // long supports: the wide LS kernel (L^{-1} in global memory, warp per signal);
   // CDB_LS_WIDE=0|1 overrides
   int wide_kr = kw <= 32 ? 1 : (kw <= 64 ? 2 : (kw <= 128 ? 4 : 0));
-  bool wide = kw > 32 && wide_kr > 0;
+  // ... and short supports whose operand is built by its own kernel anyway
+  // (N > 256): cfg 2 full OMP (N = 1024, K = 32), 200 k signals: ls_step 41.9 ->
+  // 24.2 ms, 1.24 M -> 1.39 M signals/s; with the operand fused into the grouped
+  // kernel (N <= 256: cfg 1 full OMP) the wide kernel + its operand pass lose
+  // (7.5 -> 10.4 ms per 100 k)
+  bool wide = (kw > 32 || split) && wide_kr > 0;
   if (const char *v = getenv("CDB_LS_WIDE")) wide = atoi(v) != 0 && wide_kr > 0;
   if (wide) split = 1;
   TileRescan tr;

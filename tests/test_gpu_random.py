@@ -180,6 +180,20 @@ def test_gram_candidate_widths(nb, q, k):
     _check(ref, got, d, ys, eps, "gram", allowed)
 
 
+@pytest.mark.parametrize("n,k", [(320, 7), (1024, 12), (2048, 24), (1000, 32)])
+def test_short_supports_on_long_rows(n, k):
+    """N > 256 with K <= 32: the warp-per-signal least-squares kernel with one
+    support entry per lane (ls_wide_kernel, KR = 1) and the separate scan-operand
+    kernels (fp32 N = 1024, bulk-copy ring N = 2048, generic otherwise)."""
+    t, p = 300, 80
+    d, ys = _problem(n, t, k, p, 11 * n + k, n == 320)
+    eps = 1e-3 * np.linalg.norm(ys, axis=1)
+    ref = _oracle(d, ys, k, eps)
+    dd = D.DeviceDictionary(d)
+    got = D.omp_batch_raw(dd, ys, p, k, eps, None, "tensor")
+    _check(ref, got, d, ys, eps, "tensor")
+
+
 @pytest.mark.parametrize("n,f32", [(2048, True), (3072, False), (4096, True), (4096, False)])
 def test_long_row_scan_operand(n, f32):
     """Tensor engine on long rows (N = 1024 J up to 4096): the next scan's
