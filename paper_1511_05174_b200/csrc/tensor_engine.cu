@@ -2736,7 +2736,11 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
 #undef CDB_RESID32G
       // long rows: the bulk-copy ring (CDB_RESID_BULK=0: the register-pipelined kernel)
       static const bool bulk_ok = !(getenv("CDB_RESID_BULK") && atoi(getenv("CDB_RESID_BULK")) == 0);
-      if (!done32 && bulk_ok && n % 1024 == 0 && n <= 4096 && kw <= 64) {
+      // (measured per 65,536 signals, K = 32, bulk vs register-pipelined: N = 3072
+      // 50.2 vs 61.3 ms; N = 2048 46.3 vs 56.8 ms with a 134 MB fp32 dictionary but
+      // 38.5 vs 33.4 ms with an L2-resident one; N = 1024 93.2 vs 55.0 ms)
+      const bool bulk_n = n >= 3072 || (n == 2048 && t * n * 4 > (int64_t(96) << 20));
+      if (!done32 && bulk_ok && bulk_n && n % 1024 == 0 && n <= 4096 && kw <= 64) {
         done32 = true;
         const size_t bsm = (size_t)RB_S * n * 4 + 8 * (size_t)kw + 16 * RB_S;
         const unsigned bg = (unsigned)(a.num_sms * 2);

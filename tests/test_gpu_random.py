@@ -210,3 +210,17 @@ def test_long_row_scan_operand(n, f32):
     dd = D.DeviceDictionary(d)
     got = D.omp_batch_raw(dd, ys.astype(np.float32) if f32 else ys, p, k, eps, None, "tensor")
     _check(ref, got, d, ys, eps, "tensor")
+
+
+def test_bulk_ring_two_kilobyte_rows_hbm_dictionary():
+    """N = 2048 takes the bulk-copy ring (J = 2) only when the fp32 dictionary
+    is larger than L2 (12,288 atoms: 101 MB)."""
+    n, t, k, p = 2048, 12288, 12, 32
+    d, ys = _problem(n, t, k, p, 2048, False)
+    ys = ys.astype(np.float32).astype(np.float64)
+    eps = 1e-3 * np.linalg.norm(ys, axis=1)
+    ref = _oracle(d, ys, k, eps)
+    dd = D.DeviceDictionary(d)
+    got = D.omp_batch_raw(dd, ys.astype(np.float32), p, k, eps, None, "tensor")
+    _check(ref, got, d, ys, eps, "tensor")
+    dd.close()
