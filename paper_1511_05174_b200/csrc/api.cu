@@ -367,6 +367,13 @@ cdb_status run_tensor(const cdb_dictionary *d, const void *ys, bool f32, int64_t
 // The Gram engine beats the resident one when its per-signal state is small
 // (>= ~13 signals per SM: cfg 0 full 32.7 vs 28.3 M/s, both steps of cfg 0's
 // zero-tree); with a larger H (cfg 1 step 1: 32 KB per signal) resident wins.
+// Full-dictionary scans whose Gram-engine state leaves at most four signals per
+// SM go to the tensor engine when the batch is large enough to amortise its
+// per-iteration launches (cfg 3 zero-tree step 1: T_low = 256, K = 24, 50 KB of H
+// per signal: 19.2 -> 14.1 ms per 100 k signals, zero-tree 3.13 M -> 3.73 M/s).
+constexpr int64_t kTensorPreferBytes = 40 * 1024;
+constexpr int64_t kTensorPreferSignals = 16384;
+
 bool gram_preferred(const cdb_dictionary *d, int64_t max_cands, int64_t kw) {
   return d->gram && max_cands > 0 && max_cands <= 512 && kw <= 64 &&
          cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramPreferBytes;
@@ -394,7 +401,8 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
       engine = CDB_ENGINE_RESIDENT;
     else if (!d->gram || max_cands <= 0)
       engine = CDB_ENGINE_EXACT;
-    else if (h_smem)
+    else if (h_smem && !(cands.mode == 0 && p >= kTensorPreferSignals &&
+                         cdb::gram_total_smem(max_cands, kw, d->n, true) > kTensorPreferBytes))
       engine = CDB_ENGINE_GRAM;
     else if (cands.mode == 0)
       engine = CDB_ENGINE_TENSOR;
