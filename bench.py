@@ -630,7 +630,13 @@ def bench_ours(args):
                                                     P * args.full_steps * w.k / max(corr[1], 1))
                                  if "corr_topk_full" in traffic_tab else None), "launch_ms": c_ms,
                      "basis": "2*N*scans of the full-OMP batch (actual scan counts) / corr_topk "
-                              "time, against the measured bf16 peak it runs on"}
+                              "time, against the measured bf16 peak it runs on (burst figure; "
+                              "frac_sustained: against the sustained one, the kernel being timed "
+                              "inside a long power-capped pass)"}
+        sus = peaks.get("bf16_tflops_sustained")
+        if sus:
+            full_roof["peak_sustained"] = sus
+            full_roof["frac_sustained"] = full_roof["achieved"] / sus
 
     # ---- the HBM-bound stage of the step (block-mean downsample, scaling.py:99-116)
     hbm_stages = None
