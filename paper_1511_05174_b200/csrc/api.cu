@@ -392,7 +392,8 @@ cdb_status run_omp(const cdb_dictionary *d, const void *ys, bool f32, int64_t p,
   if (p <= 0) return CDB_OK;
   static const bool force_onchip = getenv("CDB_GRAM_ONCHIP") && atoi(getenv("CDB_GRAM_ONCHIP")) != 0;
   const bool h_smem = cdb::gram_total_smem(max_cands, kw, d->n, true) <= kGramSmemLimit &&
-                      !(force_onchip && alpha0 && max_cands > 128);
+                      !(force_onchip && alpha0 && max_cands > 128) &&
+                      !cdb::gram_cta_preferred(max_cands, kw, d->n, alpha0 != nullptr);
   const bool resident = cdb::resident_fits(d->n, d->t, kw, max_cands, di.smem_optin);
   if (engine == CDB_ENGINE_RESIDENT && !resident) engine = CDB_ENGINE_AUTO;  // a preference
   const bool gram_small = gram_preferred(d, max_cands, kw);

@@ -116,6 +116,10 @@ struct GramStreamPlan {
   int wpb, nr;
   int64_t per_warp_smem, warps, slot_doubles;
 };
+// Shared-memory-sized H that still goes to the CTA-per-signal kernel: 128 < S <= 256
+// candidates with a precomputed alpha0, every H row in the CTA's third of shared
+// memory (cfg 2 step 2: S = 256, K = 32).
+bool gram_cta_preferred(int64_t max_cands, int64_t k_width, int64_t n, bool has_alpha0);
 GramStreamPlan gram_stream_plan(int64_t max_cands, int64_t k_width, int64_t n, bool stage_y,
                                 int max_smem_per_block, int num_sms);
 

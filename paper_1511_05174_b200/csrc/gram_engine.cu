@@ -1825,9 +1825,25 @@ cudaError_t launch_gram_y(const GramArgs &args, const YT *ys, int u, int h_in_sm
 
 int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_cands); }
 
+// The warp-per-signal kernel keeps 3 signals (3 warps) per SM once H passes
+// ~64 KB; three 128-thread CTAs per SM with every row in shared memory hold as
+// many signals with four times the threads on each chain.  cfg 2 step 2
+// (S = 256, K = 32, 200 k signals): 26.7 -> 20.3 ms (2 / 4 CTAs per SM: 28.6 /
+// 30.1 ms; the on-chip register kernel 55.4 ms); S = 384 (cfg 3, rows padded to
+// 512 candidates, 2 CTAs per SM) loses 12.5 -> 15.1 ms and keeps the warp kernel.
+constexpr int kSmallCtasPerSm = 3;
+bool gram_cta_preferred(int64_t s, int64_t kw, int64_t n, bool has_alpha0) {
+  static const bool off = getenv("CDB_GRAM_CTA3") && atoi(getenv("CDB_GRAM_CTA3")) == 0;
+  if (off || !has_alpha0 || s <= 128 || s > 256 || kw > 64) return false;
+  const int64_t fixed = 8 * (5 * kw + 9 * 4 + 2 + 2);
+  const int64_t per_cta = (int64_t)(228 * 1024) / kSmallCtasPerSm - 1024;
+  return fixed + 8 * kw * 256 <= per_cta && gram_total_smem(s, kw, n, true) > 40 * 1024;
+}
+
 GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
                                 int max_smem_per_block, int num_sms) {
   GramStreamPlan pl{};
+  const bool small_cta = gram_cta_preferred(s, kw, n, !stage_y);
   // on-chip H, one CTA per SM holding one signal's whole H: registers (R rows)
   // + shared memory.  Default: gram_reg2_kernel (256 threads, two candidates
   // per thread, R = 24): cfg 4 step 2, 131,072 signals: 87.8 ms against 93.8 ms
@@ -1838,7 +1854,7 @@ GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
   // traffic of the streamed kernel.
   const char *rv = getenv("CDB_GRAM_REG");
   const int regmode = rv ? atoi(rv) : 2;
-  if (!stage_y && s <= 512 && kw <= 64 && regmode != 0) {
+  if (!stage_y && s <= 512 && kw <= 64 && regmode != 0 && !small_cta) {
     int r = regmode == 2 ? 24 : 16;
     if (const char *v = getenv("CDB_GRAM_R")) r = atoi(v);
     if (r != 16 && r != 24 && r != 32) r = regmode == 2 ? 24 : 16;
@@ -1860,9 +1876,9 @@ GramStreamPlan gram_stream_plan(int64_t s, int64_t kw, int64_t n, bool stage_y,
     pl = GramStreamPlan{};
   }
   const char *cv = getenv("CDB_GRAM_CTA");
-  if (!stage_y && s <= 512 && kw <= 64 && !(cv && atoi(cv) == 0)) {
+  if (!stage_y && s <= 512 && kw <= 64 && (small_cta || !(cv && atoi(cv) == 0))) {
     // CTA per signal (gram_cta_kernel): cps CTAs per SM share its shared memory
-    int cps = kStreamCtasPerSm;
+    int cps = small_cta ? kSmallCtasPerSm : kStreamCtasPerSm;
     if (const char *v = getenv("CDB_GRAM_CPS")) cps = atoi(v) > 0 ? atoi(v) : cps;
     const int cpt = s <= 256 ? 2 : 4;
     const int64_t sp = 128 * cpt;
