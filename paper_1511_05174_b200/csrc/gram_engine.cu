@@ -1829,8 +1829,9 @@ int64_t gram_h_doubles(int64_t max_cands, int64_t kw) { return kw * gram_hs(max_
 // ~64 KB; three 128-thread CTAs per SM with every row in shared memory hold as
 // many signals with four times the threads on each chain.  cfg 2 step 2
 // (S = 256, K = 32, 200 k signals): 26.7 -> 20.3 ms (2 / 4 CTAs per SM: 28.6 /
-// 30.1 ms; the on-chip register kernel 55.4 ms); S = 384 (cfg 3, rows padded to
-// 512 candidates, 2 CTAs per SM) loses 12.5 -> 15.1 ms and keeps the warp kernel.
+// 30.1 ms; the on-chip register kernel 55.4 ms); S = 384 (cfg 3) keeps the warp
+// kernel: 12.5 ms per 100 k against 15.1 ms with rows padded to 512 candidates
+// (2 CTAs per SM) and 16.3 ms with three 192-thread CTAs of exact 384-wide rows.
 constexpr int kSmallCtasPerSm = 3;
 bool gram_cta_preferred(int64_t s, int64_t kw, int64_t n, bool has_alpha0) {
   static const bool off = getenv("CDB_GRAM_CTA3") && atoi(getenv("CDB_GRAM_CTA3")) == 0;
