@@ -2565,6 +2565,11 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
   const bool pdl = pdl_enabled() && !prof_active();
   // large N: build the scan operand in its own kernel (CDB_LS_SPLIT=0|1 overrides)
   int split = n > 256 ? 1 : 0;
+  // N = 128 with K <= 32 (cfg 2 zero-tree step 1): the warp-per-signal LS kernel
+  // plus the one-warp fp32 operand kernel beat the grouped kernel with its fused
+  // operand, 18.6 + 9.3 vs 39.2 ms per 200 k signals (zero-tree 2.95 M -> 3.55 M/s)
+  if (n == 128 && kw <= 32 && !(getenv("CDB_RESID_F32") && atoi(getenv("CDB_RESID_F32")) == 0))
+    split = 1;
   if (const char *v = getenv("CDB_LS_SPLIT")) split = atoi(v) ? 1 : 0;
   // long supports: the wide LS kernel (L^{-1} in global memory, warp per signal);
   // CDB_LS_WIDE=0|1 overrides
@@ -2730,6 +2735,10 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         if (n == 4 * 64 * 2) { CDB_RESID32(64, 2) }
         else if (n == 4 * 128 * 2) { CDB_RESID32(128, 2) }
         else if (n == 4 * 64 * 1) { CDB_RESID32(64, 1) }
+        else if (n == 4 * 32 * 1 && kw <= 32) {  // one warp per signal (cfg 2 step 1)
+          const unsigned g = (unsigned)(a.num_sms * 32);
+          CDB_RESID32(32, 1)
+        }
         else done32 = false;
       }
 #undef CDB_RESID32
