@@ -2712,7 +2712,12 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
       // fp32 vectorised operand build when n = 4 * BT * V (CDB_RESID_F32=0: fp64 kernel)
       static const bool f32_ok = !(getenv("CDB_RESID_F32") && atoi(getenv("CDB_RESID_F32")) == 0);
       const size_t xs32 = 16 * (size_t)kw;
-      static const int rg = getenv("CDB_RESID_G") ? atoi(getenv("CDB_RESID_G")) : 8;
+      // rows per pipeline group (CDB_RESID_G overrides).  Measured per 200 k cfg 2
+      // signals: N = 1024 (full OMP) 8 / 6 / 4 -> 53.1 / 41.4 / 44.2 ms; N = 128 (step 1,
+      // one warp per signal) 9.3 / 9.8 / 6.5 ms; N = 512 (cfg 4 step 1, per 131 k
+      // signals) 51.3 / 41.7 / 45.0 ms
+      static const int rg_env = getenv("CDB_RESID_G") ? atoi(getenv("CDB_RESID_G")) : 0;
+      const int rg = rg_env ? rg_env : (n == 1024 || n == 512 ? 6 : (n == 128 ? 4 : 8));
 #define CDB_RESID32G(BT_, V_, G_)                                                               \
   if (a.ys_f32)                                                                                 \
     resid_f32_kernel<float, BT_, V_, G_><<<g, BT_, xs32, stream>>>(                             \
@@ -2732,7 +2737,12 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         // N = 4096 (cfg 4 full OMP) stays on the fp64 kernel: measured 1988 vs
         // 6287 ms per 250 k signals (register-bound) and 37% more exact rescans
         // from the looser fp32 bound
-        if (n == 4 * 64 * 2) { CDB_RESID32(64, 2) }
+        static const int rbt = getenv("CDB_RESID_BT") ? atoi(getenv("CDB_RESID_BT")) : 0;
+        if (n == 4 * 128 * 1 && rbt == 128) {  // A/B: 128 threads x one float4 per row
+          const unsigned g = (unsigned)(a.num_sms * 16);
+          CDB_RESID32(128, 1)
+        }
+        else if (n == 4 * 64 * 2) { CDB_RESID32(64, 2) }
         else if (n == 4 * 128 * 2) { CDB_RESID32(128, 2) }
         else if (n == 4 * 64 * 1) { CDB_RESID32(64, 1) }
         else if (n == 4 * 32 * 1 && kw <= 32) {  // one warp per signal (cfg 2 step 1)
