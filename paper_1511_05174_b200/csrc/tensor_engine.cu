@@ -2737,12 +2737,9 @@ cudaError_t run_tensor_chunk(const TensorArgs &a, cudaStream_t stream) {
         // N = 4096 (cfg 4 full OMP) stays on the fp64 kernel: measured 1988 vs
         // 6287 ms per 250 k signals (register-bound) and 37% more exact rescans
         // from the looser fp32 bound
-        static const int rbt = getenv("CDB_RESID_BT") ? atoi(getenv("CDB_RESID_BT")) : 0;
-        if (n == 4 * 128 * 1 && rbt == 128) {  // A/B: 128 threads x one float4 per row
-          const unsigned g = (unsigned)(a.num_sms * 16);
-          CDB_RESID32(128, 1)
-        }
-        else if (n == 4 * 64 * 2) { CDB_RESID32(64, 2) }
+        // (N = 512 as 128 threads x one float4 per row: 44.6 ms at best per 131 k cfg-4
+        // signals against 41.7 ms for 64 threads x two)
+        if (n == 4 * 64 * 2) { CDB_RESID32(64, 2) }
         else if (n == 4 * 128 * 2) { CDB_RESID32(128, 2) }
         else if (n == 4 * 64 * 1) { CDB_RESID32(64, 1) }
         else if (n == 4 * 32 * 1 && kw <= 32) {  // one warp per signal (cfg 2 step 1)
